@@ -1,0 +1,182 @@
+/*
+ * panelgwas_b200 — C ABI of the B200 (sm_100a) linear-association scan.
+ *
+ * This is the drop-in boundary for the hot path of the `panelgwas` reference
+ * (/root/reference/pkg/src/panelgwas). The reference has no FFI of its own: its
+ * boundary is Python. Each entry point below names the
+ * reference interface it replaces; the Python host package
+ * `paper_2604_21095_b200` (same names as panelgwas) binds them with ctypes,
+ * and INTEGRATION.md shows the binding a panelgwas maintainer would add.
+ *
+ * Conventions
+ *   - Every function returns a status code (PG_OK == 0). On failure the
+ *     message is available from pg_last_error() (thread-local). Status codes
+ *     map onto the reference exception classes (errors.py:4-17):
+ *     PG_ERR_INVALID -> ValueError, PG_ERR_FORMAT -> FormatError,
+ *     PG_ERR_CONFIG -> ConfigError, anything else -> PanelGwasError.
+ *   - Host pointers are borrowed for the duration of the call. Device
+ *     buffers, pinned staging and streams belong to the pg_ctx.
+ *   - A pg_ctx is bound to one CUDA device; calls on one ctx are serialised
+ *     by the caller (one ctx per GPU / per worker thread).
+ *   - There is no CPU fallback: without a usable sm_100 device every compute
+ *     entry point fails with PG_ERR_CUDA.
+ */
+#ifndef PANELGWAS_B200_H
+#define PANELGWAS_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define PG_API __attribute__((visibility("default")))
+#else
+#define PG_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PG_OK 0
+#define PG_ERR_CUDA 1
+#define PG_ERR_INVALID 2
+#define PG_ERR_FORMAT 3
+#define PG_ERR_NOMEM 4
+#define PG_ERR_STATE 5
+#define PG_ERR_CONFIG 6
+
+/* Output modes (engine.py:41-44). */
+#define PG_MODE_THRESHOLD 0
+#define PG_MODE_TOPK 1
+#define PG_MODE_FULL 2
+
+/* Genotype encodings accepted by pg_scan_*. */
+#define PG_GENO_BED 0       /* PLINK 2-bit codes, SNP-major rows (plink.py:29-61) */
+#define PG_GENO_BGEN8 1     /* BGEN layout-2 probability pairs, 8-bit (bgen.py:238-249) */
+#define PG_GENO_BGEN16 2    /* same, 16-bit */
+#define PG_GENO_DENSE_F64 3 /* real dosages in [0,2], NaN = missing (dense.py:79-97) */
+
+PG_API const char* pg_last_error(void);
+PG_API int pg_abi_version(void);
+/* Number of usable sm_100 devices (0 when none). */
+PG_API int pg_device_count(int* n);
+
+typedef struct pg_ctx pg_ctx;
+
+/* Context lifetime. Replaces the panel-side state the reference shares
+ * between workers, engine._Prepared (engine.py:154-167). */
+PG_API int pg_ctx_create(int device, pg_ctx** out);
+PG_API int pg_ctx_destroy(pg_ctx* ctx);
+/* Synchronise the ctx stream (used before timing / teardown). */
+PG_API int pg_ctx_sync(pg_ctx* ctx);
+
+/* Upload the standardized phenotype panel once; it stays resident in HBM as
+ * fp16 hi/lo planes [P_pad, K_pad] plus fp64 column sums.
+ * Replaces: engine._run_scan_open panel hand-off (engine.py:269-279) — the
+ * `ytil` produced by kernel.standardize_columns (kernel.py:330-347).
+ *   ytil            host f64, row i = kept sample i, `ld` elements per row
+ *   geno_row_index  host i64 [n_kept]: genotype-file row of kept sample i
+ *                   (phenotypes.align_samples, phenotypes.py:165-220)
+ *   n_samples_src   samples in the genotype source (.fam rows) */
+PG_API int pg_ctx_set_panel(pg_ctx* ctx, const double* ytil, int64_t n_kept, int64_t n_pheno, int64_t ld,
+                     const int64_t* geno_row_index, int64_t n_samples_src);
+/* Same, but `d_ytil` is a device pointer on the ctx device. */
+PG_API int pg_ctx_set_panel_device(pg_ctx* ctx, const double* d_ytil, int64_t n_kept, int64_t n_pheno, int64_t ld,
+                            const int64_t* geno_row_index, int64_t n_samples_src);
+/* Export / import the resident split panel (device pointers, same layout and
+ * size reported by *bytes) so it can be broadcast over NCCL between ranks. */
+PG_API int pg_ctx_panel_bytes(pg_ctx* ctx, int64_t* bytes);
+PG_API int pg_ctx_export_panel(pg_ctx* ctx, void* d_dst);
+PG_API int pg_ctx_import_panel(pg_ctx* ctx, const void* d_src, int64_t n_kept, int64_t n_pheno,
+                        const int64_t* geno_row_index, int64_t n_samples_src);
+
+/* Scan parameters. `r_bar` (host f64 [n_pheno]) is the per-phenotype premask
+ * bar on |r| — engine._abs_t_to_abs_r / premask_abs_r (engine.py:170-175,
+ * 321-333) for THRESHOLD, the TopKWriter bar for TOPK (engine.py:205-211).
+ * Candidates are pairs of non-skipped markers with |r| >= r_bar. */
+PG_API int pg_ctx_set_scan(pg_ctx* ctx, double df, int mode, const double* r_bar);
+
+/* Result summary of the last scan call. */
+typedef struct pg_batch_info {
+  int64_t n_markers;
+  int64_t n_candidates; /* THRESHOLD/TOPK: candidate pairs held by the ctx */
+  int64_t clamp_count;  /* |r| > 1 before clipping (kernel.py:455) */
+  int64_t n_skipped_monomorphic;
+  int64_t n_skipped_all_missing;
+  double gemm_ms;       /* device time of the association kernel(s) */
+  double decode_ms;     /* device time of the decode kernel */
+} pg_batch_info;
+
+/* Scan one block of markers from HOST memory.
+ * Replaces, fused: <Source>.read_marker_batch (plink.py:167-185, bgen.py:251-262,
+ * dense.py:79-97) -> prepare_genotype_batch (kernel.py:376-421) ->
+ * correlate (kernel.py:428-457) -> premask + t_from_r (engine.py:197-217) ->
+ * p_from_t for candidates (output.py:129).
+ *   geno_kind  PG_GENO_*
+ *   data       BED: uint8 rows of `row_bytes` = ceil(n_samples_src/4)
+ *              BGEN8/16: per marker, the inflated probability pairs
+ *                        [n_samples_src x 2] (u8 or u16) then n_samples_src
+ *                        ploidy bytes (bit 7 = missing)
+ *              DENSE_F64: f64 rows of n_samples_src dosages
+ *   row_bytes  bytes per marker row in `data` */
+PG_API int pg_scan(pg_ctx* ctx, int geno_kind, const void* data, int64_t n_markers, int64_t row_bytes,
+            pg_batch_info* info);
+/* Same, with `d_data` already resident on the device (rows `row_pitch` bytes apart,
+ * row_pitch a multiple of 16). */
+PG_API int pg_scan_device(pg_ctx* ctx, int geno_kind, const void* d_data, int64_t n_markers, int64_t row_bytes,
+                   int64_t row_pitch, pg_batch_info* info);
+
+/* Per-marker QC of the last scan: StandardizedBatch.allele_frequency,
+ * missing_count, variance_before_scaling, skip_reason (kernel.py:360-373). Any pointer may be NULL. */
+PG_API int pg_fetch_marker_stats(pg_ctx* ctx, double* af, int64_t* missing_count, double* variance, int8_t* skip);
+/* Candidates of the last scan in (marker, phenotype) order: BatchStats.cand_rows,
+ * cand_cols, cand_r, cand_t (output.py:74-87) plus their two-sided p (fp64,
+ * floored at P_FLOOR; kernel.py:192-209). Any pointer may be NULL. */
+PG_API int pg_fetch_candidates(pg_ctx* ctx, int64_t* rows, int64_t* cols, double* r, double* t, double* p);
+/* FULL mode: t of non-skipped markers, row-major [n_ok, n_pheno], f32 (elem=4)
+ * or f64 (elem=8) — BatchStats.t_rows (engine.py:197-198). */
+PG_API int pg_fetch_full(pg_ctx* ctx, void* out, int elem_bytes, int64_t* n_rows);
+/* Per-phenotype max |r| over all non-skipped markers scanned since the last
+ * pg_ctx_set_scan (the minimum-p statistic). */
+PG_API int pg_fetch_max_abs_r(pg_ctx* ctx, double* out);
+
+/* ---- element-wise statistics on the device (host arrays in/out) ---- */
+/* kernel.t_from_r (kernel.py:460-478) */
+PG_API int pg_t_from_r(pg_ctx* ctx, const double* r, int64_t n, double df, double* t);
+/* kernel.p_from_t (kernel.py:192-209); counts p <= P_FLOOR into *underflow (may be NULL) */
+PG_API int pg_p_from_t(pg_ctx* ctx, const double* t, int64_t n, double df, double* p, int64_t* underflow);
+/* kernel.reg_inc_beta (kernel.py:147-189), broadcast already applied by caller */
+PG_API int pg_reg_inc_beta(pg_ctx* ctx, const double* a, const double* b, const double* x, int64_t n, double* out);
+/* kernel.t_threshold_for_p (kernel.py:212-235) */
+PG_API int pg_t_threshold_for_p(pg_ctx* ctx, double p_threshold, double df, double* t_crit);
+
+/* ---- genotype decode on the device (host arrays in/out) ---- */
+/* PlinkSource.read_marker_batch / decode_bed_codes (plink.py:48-61, 167-185):
+ * rows of `row_bytes` packed codes -> dosages (elem 4: f32, 8: f64) [n_markers, n_samples]
+ * with NaN for missing, plus per-row NaN counts. */
+PG_API int pg_decode_bed(pg_ctx* ctx, const uint8_t* packed, int64_t n_markers, int64_t row_bytes, int64_t n_samples,
+                  int elem_bytes, void* dosages, int64_t* missing_count);
+/* BgenSource._decode_variant probability -> dosage map (bgen.py:238-249). */
+PG_API int pg_decode_bgen(pg_ctx* ctx, const void* probs, const uint8_t* ploidy, int64_t n_markers, int64_t n_samples,
+                   int bits, double* dosages, int64_t* missing_count);
+
+/* ---- library kernels (kernel.py public API) ---- */
+/* prepare_genotype_batch (kernel.py:376-421) without genotype residualization
+ * (or with it when q != NULL): f64 in, standardized rows out (elem 4 or 8). */
+PG_API int pg_prepare_batch(pg_ctx* ctx, const double* dosages, int64_t n_markers, int64_t n_samples, const double* q,
+                     int64_t rank, int elem_bytes, void* out, double* af, int64_t* missing_count, double* variance,
+                     int8_t* skip);
+/* correlate (kernel.py:428-457): fp64 R = G Y / N with clamp count. */
+PG_API int pg_correlate_f64(pg_ctx* ctx, const double* gt, int64_t m, int64_t n, const double* yt, int64_t p, double* r,
+                     int64_t* clamp_count);
+
+/* ---- test hooks (exercise single kernels with device pointers) ---- */
+/* Raw association GEMM: X[c, p] = kWH * sum_k qh[p,k] v[c,k] + sum_k q1[p,k] v127[c,k] + q0[p,k] v[c,k]
+ * (int8 operands, exact int32 accumulation, returned as f64 [c_pad, p_pad]).
+ * p_pad % 128 == 0, c_pad % 256 == 0, k_pad % 64 == 0. */
+PG_API int pg_debug_assoc_gemm(const void* d_qh, const void* d_q1, const void* d_q0, int64_t p_pad, const void* d_v,
+                               const void* d_v127, int64_t c_pad, int64_t k_pad, double* d_x, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PANELGWAS_B200_H */

@@ -1,0 +1,150 @@
+"""ctypes binding of the C-ABI library (include/panelgwas_b200.h).
+
+The library is built in-tree (paper_2604_21095_b200/_lib/libpanelgwas_b200.so) by
+`build.py`. There is no CPU fallback: if the library or a sm_100 device is
+missing, compute calls raise immediately.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from ctypes import POINTER, c_char_p, c_double, c_int, c_int8, c_int64, c_void_p
+from pathlib import Path
+
+import numpy as np
+
+from .errors import ConfigError, FormatError, PanelGwasError
+
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libpanelgwas_b200.so"
+
+PG_OK = 0
+PG_ERR_CUDA = 1
+PG_ERR_INVALID = 2
+PG_ERR_FORMAT = 3
+PG_ERR_NOMEM = 4
+PG_ERR_STATE = 5
+PG_ERR_CONFIG = 6
+
+PG_MODE_THRESHOLD = 0
+PG_MODE_TOPK = 1
+PG_MODE_FULL = 2
+
+PG_GENO_BED = 0
+PG_GENO_BGEN8 = 1
+PG_GENO_BGEN16 = 2
+PG_GENO_DENSE_F64 = 3
+
+
+class BatchInfo(ctypes.Structure):
+    _fields_ = [
+        ("n_markers", c_int64),
+        ("n_candidates", c_int64),
+        ("clamp_count", c_int64),
+        ("n_skipped_monomorphic", c_int64),
+        ("n_skipped_all_missing", c_int64),
+        ("gemm_ms", c_double),
+        ("decode_ms", c_double),
+    ]
+
+
+_P = c_void_p  # all array arguments are passed as raw addresses
+# (name, argtypes) for every symbol declared in include/panelgwas_b200.h
+SIGNATURES: dict[str, list] = {
+    "pg_last_error": [],
+    "pg_abi_version": [],
+    "pg_device_count": [_P],
+    "pg_ctx_create": [c_int, _P],
+    "pg_ctx_destroy": [_P],
+    "pg_ctx_sync": [_P],
+    "pg_ctx_set_panel": [_P, _P, c_int64, c_int64, c_int64, _P, c_int64],
+    "pg_ctx_set_panel_device": [_P, _P, c_int64, c_int64, c_int64, _P, c_int64],
+    "pg_ctx_panel_bytes": [_P, _P],
+    "pg_ctx_export_panel": [_P, _P],
+    "pg_ctx_import_panel": [_P, _P, c_int64, c_int64, _P, c_int64],
+    "pg_ctx_set_scan": [_P, c_double, c_int, _P],
+    "pg_scan": [_P, c_int, _P, c_int64, c_int64, _P],
+    "pg_scan_device": [_P, c_int, _P, c_int64, c_int64, c_int64, _P],
+    "pg_fetch_marker_stats": [_P, _P, _P, _P, _P],
+    "pg_fetch_candidates": [_P, _P, _P, _P, _P, _P],
+    "pg_fetch_full": [_P, _P, c_int, _P],
+    "pg_fetch_max_abs_r": [_P, _P],
+    "pg_t_from_r": [_P, _P, c_int64, c_double, _P],
+    "pg_p_from_t": [_P, _P, c_int64, c_double, _P, _P],
+    "pg_reg_inc_beta": [_P, _P, _P, _P, c_int64, _P],
+    "pg_t_threshold_for_p": [_P, c_double, c_double, _P],
+    "pg_decode_bed": [_P, _P, c_int64, c_int64, c_int64, c_int, _P, _P],
+    "pg_decode_bgen": [_P, _P, _P, c_int64, c_int64, c_int, _P, _P],
+    "pg_prepare_batch": [_P, _P, c_int64, c_int64, _P, c_int64, c_int, _P, _P, _P, _P, _P],
+    "pg_correlate_f64": [_P, _P, c_int64, c_int64, _P, c_int64, _P, _P],
+    "pg_debug_assoc_gemm": [_P, _P, _P, c_int64, _P, _P, c_int64, c_int64, _P, _P],
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load_library(path: Path | None = None):
+    """Load (once) and type the shared library; raises if it is absent."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        p = Path(path) if path else LIB_PATH
+        if not p.exists():
+            raise PanelGwasError(
+                f"panelgwas_b200 native library not built: {p} (run paper_2604_21095_b200/build.py)"
+            )
+        lib = ctypes.CDLL(str(p))
+        for name, argtypes in SIGNATURES.items():
+            fn = getattr(lib, name, None)
+            if fn is None:
+                continue
+            fn.argtypes = argtypes
+            fn.restype = c_char_p if name == "pg_last_error" else c_int
+        _lib = lib
+        return lib
+
+
+def exported_symbols(path: Path | None = None) -> set[str]:
+    lib = load_library(path)
+    return {name for name in SIGNATURES if getattr(lib, name, None) is not None}
+
+
+def check(status: int) -> None:
+    """Map a PG_* status onto the reference exception hierarchy (errors.py)."""
+    if status == PG_OK:
+        return
+    msg = (_lib.pg_last_error() or b"").decode(errors="replace") if _lib is not None else ""
+    if status == PG_ERR_INVALID:
+        raise ValueError(msg)
+    if status == PG_ERR_FORMAT:
+        raise FormatError(msg)
+    if status == PG_ERR_CONFIG:
+        raise ConfigError(msg)
+    raise PanelGwasError(f"panelgwas_b200 native error {status}: {msg}")
+
+
+def call(name: str, *args) -> None:
+    lib = load_library()
+    check(getattr(lib, name)(*args))
+
+
+def ptr(a: np.ndarray | None) -> int | None:
+    """Address of a C-contiguous numpy array (None passes NULL)."""
+    if a is None:
+        return None
+    if not a.flags["C_CONTIGUOUS"]:
+        raise ValueError("native call needs a C-contiguous array")
+    return a.ctypes.data
+
+
+def device_count() -> int:
+    n = c_int(0)
+    call("pg_device_count", ctypes.addressof(n))
+    return n.value
+
+
+def require_device() -> None:
+    if device_count() < 1:
+        raise PanelGwasError("panelgwas_b200 requires an NVIDIA B200 (sm_100) device; none is visible")

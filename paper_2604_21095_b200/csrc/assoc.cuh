@@ -1,0 +1,53 @@
+// Internal interface of the association GEMM (K2) + fused epilogue (K3).
+//
+// Exact-integer formulation. The standardized panel is
+// quantized once per phenotype p to q = round(y~ / s_p), |q| <= kQMax, and
+// split into three int8 limbs  q = kWH * qH + 127 * q1 + q0.
+// Genotype rows are ternary codes v in {-1, 0, 1}; the decoder also writes the
+// plane 127*v so that two limbs share one int32 accumulator:
+//   accH[p, c] = sum_k qH[p,k] * v[c,k]
+//   accL[p, c] = sum_k q1[p,k] * (127 v[c,k]) + q0[p,k] * v[c,k]
+//   X[p, c]    = kWH * accH + accL   == sum_k q[p,k] v[c,k]   (exact, int64)
+// All products and sums are integers, so the tensor-core result is exact and
+// independent of tiling, batching and GPU count.
+#pragma once
+#include <cstdint>
+
+#include "pg_common.cuh"
+
+namespace pg {
+
+constexpr int kTileP = 128;   // phenotypes per tile (UMMA M, A operand = panel limbs)
+constexpr int kTileC = 256;   // genotype rows per tile (UMMA N, B operand)
+constexpr int kTileK = 64;    // int8 samples per pipeline stage (one 64-byte swizzle row)
+constexpr int64_t kWH = 32385;          // weight of the high limb: 2*(127*127+63)+1
+constexpr int64_t kQMax = kWH * 127 + 16192;  // largest |q| representable by the limbs
+
+struct AssocEpilogue {
+  int rows_per_marker;          // 1: row = u ; 2: rows = (u, missing mask)
+  int64_t m_valid;              // markers in this launch
+  int64_t p_valid;              // phenotypes
+  const float* mu_f;            // [markers] mean of u over observed kept samples
+  const double* mu_d;
+  const float* invd_f;          // [markers] 1/sqrt(N * V_u); NaN = skipped / padding
+  const double* invd_d;
+  const float* scale_f;         // [p_pad] quantization step s_p
+  const double* scale_d;
+  const float* cq_f;            // [p_pad] sum_k q[p,k]
+  const long long* cq;
+  const float* rbar;            // [p_pad] premask bar on |r| (already widened); null = no candidates
+  unsigned long long* cand_key; // (marker << 32) | phenotype
+  double* cand_r;               // exact fp64 r of the candidate
+  int* cand_count;
+  int64_t cand_cap;
+  unsigned int* max_abs_r;      // [p_pad] running max |r| (float bits), or null
+  double* full_r;               // FULL mode: r[marker * full_ld + p] (fp64), or null
+  int64_t full_ld;
+};
+
+// Launch K2/K3 on `stream`. Panel limbs q*[p_pad, k_pad], genotype planes
+// v / v127 [c_pad, k_pad] (int8, K-major, rows 16-byte aligned).
+int launch_assoc(const int8_t* qh, const int8_t* q1, const int8_t* q0, int64_t p_pad, const int8_t* v,
+                 const int8_t* v127, int64_t c_pad, int64_t k_pad, const AssocEpilogue& ep, cudaStream_t stream);
+
+}  // namespace pg

@@ -1,0 +1,266 @@
+// K2 + K3: the association contraction on the 5th-gen tensor cores with the
+// r -> premask -> candidate-compaction epilogue fused behind it.
+//
+// Reference semantics (what this replaces): kernel.correlate
+// (/root/reference/pkg/src/panelgwas/kernel.py:428-457) computes
+// R = G~ . Y~ / N in float64 over 256-row tiles, then the engine premasks
+// |r| >= r_bar and keeps candidates in (marker, phenotype) order
+// (engine.py:197-217). Here the contraction runs on raw ternary genotype codes
+// against the resident, quantized panel (assoc.cuh), exactly, and the
+// centring / scaling of the reference's G~ is applied in the epilogue:
+//
+//   r[m,p] = s_p * (X[m,p] - mu_m * (Cq_p - Mq[m,p])) / sqrt(N * V_m)
+//
+// with X = sum_k u q, Mq = sum over missing calls of q (only when the batch
+// has missing calls; rows_per_marker == 2), mu_m / V_m the mean / centred
+// sum of squares of u over observed kept samples.
+//
+// Structure: persistent, warp-specialised, 1 CTA per SM, 256 threads.
+//   warp 0 lane 0 : TMA producer (4-stage smem ring, 56 KB per stage)
+//   warp 1 lane 0 : tcgen05.mma (kind::i8) issuer; 3 MMAs per 32 samples
+//   warp 2        : TMEM allocator (512 columns: accH | accL, 128 lanes x 256)
+//   warps 4..7    : epilogue (tcgen05.ld -> X -> r -> premask / compaction / FULL)
+#include <cuda.h>
+
+#include <cmath>
+
+#include "assoc.cuh"
+#include "pg_ptx.cuh"
+
+namespace pg {
+namespace {
+
+constexpr int kStages = 4;
+constexpr int kQBytes = kTileP * kTileK;  // 8 KB per panel limb tile
+constexpr int kVBytes = kTileC * kTileK;  // 16 KB per genotype plane tile
+constexpr int kStageBytes = 3 * kQBytes + 2 * kVBytes;
+constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int kThreads = 256;
+constexpr int kTmemCols = 512;
+constexpr int kGroupC = 8;  // genotype tiles per raster group (panel tiles reused through L2)
+
+__device__ __forceinline__ void tile_coords(int t, int n_ctile, int n_ptile, int& ct, int& pt) {
+  const int group = t / (kGroupC * n_ptile);
+  const int first = group * kGroupC;
+  const int gsz = min(kGroupC, n_ctile - first);
+  const int r = t - group * kGroupC * n_ptile;
+  ct = first + r % gsz;
+  pt = r / gsz;
+}
+
+template <int R>
+__device__ __forceinline__ void epilogue_tile(const AssocEpilogue& ep, uint32_t tH, uint32_t tL, int ct, int pheno,
+                                              int lane) {
+  constexpr int kMarkersPerTile = kTileC / R;
+  const uint32_t lanemask_lt = (1u << lane) - 1u;
+  const float sc_f = ep.scale_f[pheno];
+  const double sc_d = ep.scale_d[pheno];
+  const float cq_f = ep.cq_f[pheno];
+  const long long cq = ep.cq[pheno];
+  const float rb = ep.rbar ? ep.rbar[pheno] : INFINITY;
+  float mx = 0.f;
+#pragma unroll 1
+  for (int c = 0; c < kTileC; c += 16) {
+    uint32_t h[16], l[16];
+    tmem_ld_32x32b_x16(tH + c, h);
+    tmem_ld_32x32b_x16(tL + c, l);
+    tmem_ld_wait();
+#pragma unroll
+    for (int j = 0; j < 16; j += R) {
+      const long long xu = kWH * static_cast<long long>(static_cast<int>(h[j])) + static_cast<int>(l[j]);
+      long long xm = 0;
+      if constexpr (R == 2) xm = kWH * static_cast<long long>(static_cast<int>(h[j + 1])) + static_cast<int>(l[j + 1]);
+      const int m = ct * kMarkersPerTile + (c + j) / R;
+      const float mu = __ldg(ep.mu_f + m);
+      const float iv = __ldg(ep.invd_f + m);  // NaN for skipped / padding markers
+      const float xf = static_cast<float>(xu) - mu * (cq_f - static_cast<float>(xm));
+      const float r = xf * sc_f * iv;
+      const float ar = fabsf(r);
+      mx = fmaxf(mx, ar);
+      const bool hit = ar >= rb;
+      double r64 = 0.0;
+      if (hit || ep.full_r) {
+        r64 = sc_d * (static_cast<double>(xu) - __ldg(ep.mu_d + m) * static_cast<double>(cq - xm)) *
+              __ldg(ep.invd_d + m);
+      }
+      if (ep.full_r) ep.full_r[static_cast<int64_t>(m) * ep.full_ld + pheno] = r64;
+      const uint32_t mask = __ballot_sync(0xffffffffu, hit);
+      if (mask) {
+        int base = 0;
+        if (lane == 0) base = atomicAdd(ep.cand_count, __popc(mask));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (hit) {
+          const int64_t idx = static_cast<int64_t>(base) + __popc(mask & lanemask_lt);
+          if (idx < ep.cand_cap) {
+            ep.cand_key[idx] = (static_cast<unsigned long long>(m) << 32) | static_cast<unsigned>(pheno);
+            ep.cand_r[idx] = r64;
+          }
+        }
+      }
+    }
+  }
+  if (ep.max_abs_r && pheno < ep.p_valid) atomicMax(ep.max_abs_r + pheno, __float_as_uint(mx));
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    assoc_i8_kernel(const __grid_constant__ CUtensorMap tm_qh, const __grid_constant__ CUtensorMap tm_q1,
+                    const __grid_constant__ CUtensorMap tm_q0, const __grid_constant__ CUtensorMap tm_v,
+                    const __grid_constant__ CUtensorMap tm_v127, int n_ctile, int n_ptile, int n_kb,
+                    AssocEpilogue ep) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int n_tiles = n_ctile * n_ptile;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_qh);
+    tma_prefetch_desc(&tm_q1);
+    tma_prefetch_desc(&tm_q0);
+    tma_prefetch_desc(&tm_v);
+    tma_prefetch_desc(&tm_v127);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 4);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ TMA producer
+      const uint64_t pol_keep = l2_policy_evict_last();
+      uint32_t s = 0, ph = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        int ct, pt;
+        tile_coords(t, n_ctile, n_ptile, ct, pt);
+        for (int kb = 0; kb < n_kb; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* st = smem + s * kStageBytes;
+          const int kx = kb * kTileK;
+          mbar_arrive_expect_tx(&full[s], kStageBytes);
+          tma_load_2d_hint(st, &tm_qh, &full[s], kx, pt * kTileP, pol_keep);
+          tma_load_2d_hint(st + kQBytes, &tm_q1, &full[s], kx, pt * kTileP, pol_keep);
+          tma_load_2d_hint(st + 2 * kQBytes, &tm_q0, &full[s], kx, pt * kTileP, pol_keep);
+          tma_load_2d(st + 3 * kQBytes, &tm_v, &full[s], kx, ct * kTileC);
+          tma_load_2d(st + 3 * kQBytes + kVBytes, &tm_v127, &full[s], kx, ct * kTileC);
+          if (++s == kStages) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ MMA issuer
+      constexpr uint32_t idesc = idesc_s8_s32(kTileP, kTileC);
+      const uint32_t dH = tmem_base;
+      const uint32_t dL = tmem_base + kTileC;
+      uint32_t s = 0, ph = 0, aph = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        mbar_wait(tempty, aph ^ 1);
+        tc_fence_after();
+        uint32_t acc = 0;
+        for (int kb = 0; kb < n_kb; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t st = smem_u32(smem + s * kStageBytes);
+          const uint64_t d_qh = umma_desc_sw64(st);
+          const uint64_t d_q1 = umma_desc_sw64(st + kQBytes);
+          const uint64_t d_q0 = umma_desc_sw64(st + 2 * kQBytes);
+          const uint64_t d_v = umma_desc_sw64(st + 3 * kQBytes);
+          const uint64_t d_v127 = umma_desc_sw64(st + 3 * kQBytes + kVBytes);
+#pragma unroll
+          for (int k = 0; k < kTileK / 32; ++k) {
+            // +32 bytes along K inside the 64-byte swizzle row == +2 in the >>4 address field
+            mma_i8_ss(dH, d_qh + 2 * k, d_v + 2 * k, idesc, acc);
+            mma_i8_ss(dL, d_q1 + 2 * k, d_v127 + 2 * k, idesc, acc);
+            mma_i8_ss(dL, d_q0 + 2 * k, d_v + 2 * k, idesc, 1);
+            acc = 1;
+          }
+          mma_commit(&empty[s]);
+          if (++s == kStages) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        mma_commit(tfull);
+        aph ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // -------------------------------------------------------------- epilogue
+    const int ew = warp - 4;  // == warp % 4 -> TMEM lanes [32*ew, 32*ew+32)
+    uint32_t aph = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      int ct, pt;
+      tile_coords(t, n_ctile, n_ptile, ct, pt);
+      const int pheno = pt * kTileP + ew * 32 + lane;
+      mbar_wait(tfull, aph);
+      tc_fence_after();
+      const uint32_t tH = tmem_base + (static_cast<uint32_t>(ew * 32) << 16);
+      const uint32_t tL = tH + kTileC;
+      if (ep.rows_per_marker == 2)
+        epilogue_tile<2>(ep, tH, tL, ct, pheno, lane);
+      else
+        epilogue_tile<1>(ep, tH, tL, ct, pheno, lane);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty);
+      aph ^= 1;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_free(tmem_base, kTmemCols);
+}
+
+}  // namespace
+
+int launch_assoc(const int8_t* qh, const int8_t* q1, const int8_t* q0, int64_t p_pad, const int8_t* v,
+                 const int8_t* v127, int64_t c_pad, int64_t k_pad, const AssocEpilogue& ep, cudaStream_t stream) {
+  PG_REQUIRE(p_pad % kTileP == 0 && c_pad % kTileC == 0 && k_pad % kTileK == 0 && p_pad > 0 && c_pad > 0 &&
+                 k_pad > 0,
+             PG_ERR_INVALID, "assoc: bad padded shape p=%lld c=%lld k=%lld", (long long)p_pad, (long long)c_pad,
+             (long long)k_pad);
+  PG_REQUIRE(ep.rows_per_marker == 1 || ep.rows_per_marker == 2, PG_ERR_INVALID, "assoc: rows_per_marker");
+  CUtensorMap tm_qh, tm_q1, tm_q0, tm_v, tm_v127;
+  const uint64_t pitch = static_cast<uint64_t>(k_pad);
+  PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_qh, qh, k_pad, p_pad, pitch, kTileK, kTileP));
+  PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_q1, q1, k_pad, p_pad, pitch, kTileK, kTileP));
+  PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_q0, q0, k_pad, p_pad, pitch, kTileK, kTileP));
+  PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_v, v, k_pad, c_pad, pitch, kTileK, kTileC));
+  PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_v127, v127, k_pad, c_pad, pitch, kTileK, kTileC));
+  PG_CUDA_CHECK(cudaFuncSetAttribute(assoc_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+  int dev = 0, n_sm = 0;
+  PG_CUDA_CHECK(cudaGetDevice(&dev));
+  PG_CUDA_CHECK(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+  const int n_ctile = static_cast<int>(c_pad / kTileC);
+  const int n_ptile = static_cast<int>(p_pad / kTileP);
+  const int n_tiles = n_ctile * n_ptile;
+  const int grid = n_tiles < n_sm ? n_tiles : n_sm;
+  assoc_i8_kernel<<<grid, kThreads, kSmemBytes, stream>>>(tm_qh, tm_q1, tm_q0, tm_v, tm_v127, n_ctile, n_ptile,
+                                                          static_cast<int>(k_pad / kTileK), ep);
+  PG_CUDA_CHECK(cudaGetLastError());
+  return PG_OK;
+}
+
+}  // namespace pg
