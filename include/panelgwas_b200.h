@@ -94,6 +94,9 @@ PG_API int pg_ctx_import_panel(pg_ctx* ctx, const void* d_src, int64_t n_kept, i
  * 321-333) for THRESHOLD, the TopKWriter bar for TOPK (engine.py:205-211).
  * Candidates are pairs of non-skipped markers with |r| >= r_bar. */
 PG_API int pg_ctx_set_scan(pg_ctx* ctx, double df, int mode, const double* r_bar);
+/* Replace the premask bar between batches without resetting the scan (TOPK bar
+ * tightening, engine.py:205-211 / output.py:199-200). */
+PG_API int pg_ctx_set_rbar(pg_ctx* ctx, const double* r_bar);
 
 /* Result summary of the last scan call. */
 typedef struct pg_batch_info {

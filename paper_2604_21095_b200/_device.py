@@ -1,0 +1,275 @@
+"""Python handle over one `pg_ctx` (include/panelgwas_b200.h).
+
+`DeviceContext` owns a native context bound to one CUDA device and exposes
+numpy-in / numpy-out wrappers of every C-ABI entry point. All numerics run on
+the device; without the native library or a B200 every method raises
+`PanelGwasError` (there is deliberately no host fallback).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from ctypes import byref, c_double, c_int64, c_void_p
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from ._native import BatchInfo, call, ptr
+
+
+def default_device_index() -> int:
+    for key in ("PANELGWAS_DEVICE", "LOCAL_RANK"):
+        v = os.environ.get(key)
+        if v:
+            try:
+                return int(v)
+            except ValueError:
+                pass
+    return 0
+
+
+@dataclass
+class ScanResult:
+    """Device results of one scanned block (host copies)."""
+
+    n_markers: int
+    af: np.ndarray
+    missing_count: np.ndarray
+    variance: np.ndarray
+    skip: np.ndarray
+    clamp_count: int
+    cand_rows: np.ndarray | None = None
+    cand_cols: np.ndarray | None = None
+    cand_r: np.ndarray | None = None
+    cand_t: np.ndarray | None = None
+    cand_p: np.ndarray | None = None
+    t_rows: np.ndarray | None = None
+    decode_ms: float = 0.0
+    gemm_ms: float = 0.0
+
+
+class DeviceContext:
+    """One native scan context (panel resident in HBM + batch buffers + stream)."""
+
+    def __init__(self, device: int | None = None):
+        self.lib = _native.load_library()
+        self.device = default_device_index() if device is None else int(device)
+        handle = c_void_p()
+        call("pg_ctx_create", self.device, byref(handle))
+        self._h = handle
+        self.lock = threading.RLock()
+        self.n_pheno = 0
+        self.mode = _native.PG_MODE_THRESHOLD
+
+    # ------------------------------------------------------------ lifetime
+    def close(self) -> None:
+        if self._h:
+            self.lib.pg_ctx_destroy(self._h)
+            self._h = c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def sync(self) -> None:
+        call("pg_ctx_sync", self._h)
+
+    # ------------------------------------------------------------ panel
+    def set_panel(self, ytil: np.ndarray, geno_row_index: np.ndarray, n_samples_src: int) -> None:
+        y = np.ascontiguousarray(ytil, dtype=np.float64)
+        gidx = np.ascontiguousarray(geno_row_index, dtype=np.int64)
+        with self.lock:
+            call("pg_ctx_set_panel", self._h, ptr(y), y.shape[0], y.shape[1], y.shape[1], ptr(gidx),
+                 int(n_samples_src))
+            self.n_pheno = y.shape[1]
+
+    def set_panel_device(self, d_ptr: int, n_kept: int, n_pheno: int, ld: int, geno_row_index: np.ndarray,
+                         n_samples_src: int) -> None:
+        gidx = np.ascontiguousarray(geno_row_index, dtype=np.int64)
+        with self.lock:
+            call("pg_ctx_set_panel_device", self._h, d_ptr, n_kept, n_pheno, ld, ptr(gidx), int(n_samples_src))
+            self.n_pheno = n_pheno
+
+    def panel_bytes(self) -> int:
+        n = c_int64(0)
+        call("pg_ctx_panel_bytes", self._h, byref(n))
+        return n.value
+
+    def export_panel(self, d_dst: int) -> None:
+        call("pg_ctx_export_panel", self._h, d_dst)
+
+    def import_panel(self, d_src: int, n_kept: int, n_pheno: int, geno_row_index: np.ndarray,
+                     n_samples_src: int) -> None:
+        gidx = np.ascontiguousarray(geno_row_index, dtype=np.int64)
+        with self.lock:
+            call("pg_ctx_import_panel", self._h, d_src, n_kept, n_pheno, ptr(gidx), int(n_samples_src))
+            self.n_pheno = n_pheno
+
+    def set_scan(self, df: float, mode: int, r_bar: np.ndarray | None) -> None:
+        rb = None if r_bar is None else np.ascontiguousarray(r_bar, dtype=np.float64)
+        with self.lock:
+            call("pg_ctx_set_scan", self._h, float(df), int(mode), ptr(rb))
+            self.mode = mode
+
+    def set_rbar(self, r_bar: np.ndarray) -> None:
+        rb = np.ascontiguousarray(r_bar, dtype=np.float64)
+        with self.lock:
+            call("pg_ctx_set_rbar", self._h, ptr(rb))
+
+    # ------------------------------------------------------------ scan
+    def scan(self, kind: int, block: np.ndarray, row_bytes: int, *, fetch: bool = True,
+             full_elem_bytes: int = 8) -> ScanResult:
+        """Scan one host block of raw marker rows ([n_markers, row_bytes] uint8)."""
+        blk = np.ascontiguousarray(block)
+        n = blk.shape[0]
+        info = BatchInfo()
+        with self.lock:
+            call("pg_scan", self._h, int(kind), blk.ctypes.data, n, int(row_bytes), byref(info))
+            return self._collect(info, fetch, full_elem_bytes)
+
+    def scan_device(self, kind: int, d_ptr: int, n_markers: int, row_bytes: int, row_pitch: int, *,
+                    fetch: bool = True, full_elem_bytes: int = 8) -> ScanResult:
+        info = BatchInfo()
+        with self.lock:
+            call("pg_scan_device", self._h, int(kind), d_ptr, int(n_markers), int(row_bytes), int(row_pitch),
+                 byref(info))
+            return self._collect(info, fetch, full_elem_bytes)
+
+    def _collect(self, info: BatchInfo, fetch: bool, full_elem_bytes: int) -> ScanResult:
+        m = int(info.n_markers)
+        res = ScanResult(
+            n_markers=m,
+            af=np.empty(m), missing_count=np.empty(m, np.int64), variance=np.empty(m),
+            skip=np.empty(m, np.int8), clamp_count=int(info.clamp_count),
+            decode_ms=float(info.decode_ms), gemm_ms=float(info.gemm_ms),
+        )
+        if not fetch:
+            res.n_candidates = int(info.n_candidates)  # type: ignore[attr-defined]
+            return res
+        call("pg_fetch_marker_stats", self._h, ptr(res.af), ptr(res.missing_count), ptr(res.variance),
+             ptr(res.skip))
+        if self.mode == _native.PG_MODE_FULL:
+            n_rows = c_int64(0)
+            call("pg_fetch_full", self._h, None, full_elem_bytes, byref(n_rows))
+            dt = np.float32 if full_elem_bytes == 4 else np.float64
+            out = np.empty((n_rows.value, self.n_pheno), dtype=dt)
+            call("pg_fetch_full", self._h, ptr(out), full_elem_bytes, byref(n_rows))
+            res.t_rows = out
+        else:
+            k = int(info.n_candidates)
+            res.cand_rows = np.empty(k, np.int64)
+            res.cand_cols = np.empty(k, np.int64)
+            res.cand_r = np.empty(k)
+            res.cand_t = np.empty(k)
+            res.cand_p = np.empty(k)
+            if k:
+                call("pg_fetch_candidates", self._h, ptr(res.cand_rows), ptr(res.cand_cols), ptr(res.cand_r),
+                     ptr(res.cand_t), ptr(res.cand_p))
+        return res
+
+    def max_abs_r(self) -> np.ndarray:
+        out = np.empty(self.n_pheno)
+        call("pg_fetch_max_abs_r", self._h, ptr(out))
+        return out
+
+    # ------------------------------------------------------------ element-wise statistics
+    def t_from_r(self, r: np.ndarray, df: float) -> np.ndarray:
+        a = np.ascontiguousarray(r, dtype=np.float64)
+        out = np.empty_like(a)
+        with self.lock:
+            call("pg_t_from_r", self._h, ptr(a), a.size, float(df), ptr(out))
+        return out
+
+    def p_from_t(self, t: np.ndarray, df: float) -> tuple[np.ndarray, int]:
+        a = np.ascontiguousarray(t, dtype=np.float64)
+        out = np.empty_like(a)
+        under = c_int64(0)
+        with self.lock:
+            call("pg_p_from_t", self._h, ptr(a), a.size, float(df), ptr(out), byref(under))
+        return out, under.value
+
+    def reg_inc_beta(self, a: np.ndarray, b: np.ndarray, x: np.ndarray) -> np.ndarray:
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        out = np.empty_like(x)
+        with self.lock:
+            call("pg_reg_inc_beta", self._h, ptr(a), ptr(b), ptr(x), x.size, ptr(out))
+        return out
+
+    def t_threshold_for_p(self, p_threshold: float, df: float) -> float:
+        out = c_double(0.0)
+        with self.lock:
+            call("pg_t_threshold_for_p", self._h, float(p_threshold), float(df), byref(out))
+        return out.value
+
+    # ------------------------------------------------------------ decode / library kernels
+    def decode_bed(self, packed: np.ndarray, n_samples: int, dtype) -> tuple[np.ndarray, np.ndarray]:
+        blk = np.ascontiguousarray(packed, dtype=np.uint8)
+        m, row_bytes = blk.shape
+        elem = np.dtype(dtype).itemsize
+        out = np.empty((m, n_samples), dtype=np.float32 if elem == 4 else np.float64)
+        miss = np.empty(m, np.int64)
+        with self.lock:
+            call("pg_decode_bed", self._h, ptr(blk), m, row_bytes, int(n_samples), elem, ptr(out), ptr(miss))
+        return out, miss
+
+    def decode_bgen(self, rows: np.ndarray, n_samples: int, bits: int) -> tuple[np.ndarray, np.ndarray]:
+        blk = np.ascontiguousarray(rows, dtype=np.uint8)
+        m = blk.shape[0]
+        out = np.empty((m, n_samples), dtype=np.float64)
+        miss = np.empty(m, np.int64)
+        with self.lock:
+            call("pg_decode_bgen", self._h, ptr(blk), None, m, int(n_samples), int(bits), ptr(out), ptr(miss))
+        return out, miss
+
+    def prepare_batch(self, dosages: np.ndarray, q: np.ndarray | None, dtype):
+        d = np.ascontiguousarray(dosages, dtype=np.float64)
+        m, n = d.shape
+        elem = np.dtype(dtype).itemsize
+        out = np.empty((m, n), dtype=np.float32 if elem == 4 else np.float64)
+        af = np.empty(m)
+        miss = np.empty(m, np.int64)
+        var = np.empty(m)
+        skip = np.empty(m, np.int8)
+        qq = None if q is None else np.ascontiguousarray(q, dtype=np.float64)
+        rank = 0 if qq is None else qq.shape[1]
+        with self.lock:
+            call("pg_prepare_batch", self._h, ptr(d), m, n, ptr(qq), rank, elem, ptr(out), ptr(af), ptr(miss),
+                 ptr(var), ptr(skip))
+        return out, af, miss, var, skip
+
+    def correlate(self, gt: np.ndarray, yt: np.ndarray) -> tuple[np.ndarray, int]:
+        g = np.ascontiguousarray(gt, dtype=np.float64)
+        y = np.ascontiguousarray(yt, dtype=np.float64)
+        m, n = g.shape
+        p = y.shape[1]
+        r = np.empty((m, p))
+        clamp = c_int64(0)
+        with self.lock:
+            call("pg_correlate_f64", self._h, ptr(g), m, n, ptr(y), p, ptr(r), byref(clamp))
+        return r, clamp.value
+
+
+_default: DeviceContext | None = None
+_default_lock = threading.Lock()
+
+
+def default_context() -> DeviceContext:
+    """Process-wide context for the library-level functions (lazily created)."""
+    global _default
+    with _default_lock:
+        if _default is None:
+            _default = DeviceContext()
+        return _default

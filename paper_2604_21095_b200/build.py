@@ -40,6 +40,10 @@ def _nvcc() -> str:
     raise RuntimeError("nvcc not found; the CUDA toolkit is required to build panelgwas_b200")
 
 
+# per-file extra flags: the Student-t code follows numpy's operation order, so no FMA contraction
+FILE_FLAGS = {"pstats.cu": ["-fmad=false"]}
+
+
 def sources() -> list[Path]:
     return sorted(CSRC.glob("*.cu"))
 
@@ -71,7 +75,7 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
         if (not force and obj.exists() and obj.stat().st_mtime > src.stat().st_mtime
                 and obj.stat().st_mtime > newest_header):
             continue
-        cmd = [nvcc, *ARCH_FLAGS, *NVCC_FLAGS, *include, "-c", str(src), "-o", str(obj)]
+        cmd = [nvcc, *ARCH_FLAGS, *NVCC_FLAGS, *FILE_FLAGS.get(src.name, []), *include, "-c", str(src), "-o", str(obj)]
         if verbose:
             print(" ".join(cmd), flush=True)
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))

@@ -67,9 +67,19 @@ __device__ __forceinline__ void epilogue_tile(const AssocEpilogue& ep, uint32_t 
     tmem_ld_wait();
 #pragma unroll
     for (int j = 0; j < 16; j += R) {
-      const long long xu = kWH * static_cast<long long>(static_cast<int>(h[j])) + static_cast<int>(l[j]);
-      long long xm = 0;
-      if constexpr (R == 2) xm = kWH * static_cast<long long>(static_cast<int>(h[j + 1])) + static_cast<int>(l[j + 1]);
+      // exact per-row products, then recombine the rows of this marker
+      long long xu = 0, xm = 0;
+      if constexpr (R == 1) {
+        xu = kWH * static_cast<long long>(static_cast<int>(h[j])) + static_cast<int>(l[j]);
+      } else {
+        long long w = 1;
+#pragma unroll
+        for (int d = 0; d < (R == 2 ? 1 : R - 1); ++d) {
+          xu += w * (kWH * static_cast<long long>(static_cast<int>(h[j + d])) + static_cast<int>(l[j + d]));
+          w *= 3;
+        }
+        xm = kWH * static_cast<long long>(static_cast<int>(h[j + R - 1])) + static_cast<int>(l[j + R - 1]);
+      }
       const int m = ct * kMarkersPerTile + (c + j) / R;
       const float mu = __ldg(ep.mu_f + m);
       const float iv = __ldg(ep.invd_f + m);  // NaN for skipped / padding markers
@@ -216,10 +226,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const uint32_t tH = tmem_base + (static_cast<uint32_t>(ew * 32) << 16);
       const uint32_t tL = tH + kTileC;
-      if (ep.rows_per_marker == 2)
-        epilogue_tile<2>(ep, tH, tL, ct, pheno, lane);
-      else
-        epilogue_tile<1>(ep, tH, tL, ct, pheno, lane);
+      switch (ep.rows_per_marker) {
+        case 1: epilogue_tile<1>(ep, tH, tL, ct, pheno, lane); break;
+        case 2: epilogue_tile<2>(ep, tH, tL, ct, pheno, lane); break;
+        case 8: epilogue_tile<8>(ep, tH, tL, ct, pheno, lane); break;
+        default: epilogue_tile<16>(ep, tH, tL, ct, pheno, lane); break;
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty);
@@ -241,7 +253,9 @@ int launch_assoc(const int8_t* qh, const int8_t* q1, const int8_t* q0, int64_t p
                  k_pad > 0,
              PG_ERR_INVALID, "assoc: bad padded shape p=%lld c=%lld k=%lld", (long long)p_pad, (long long)c_pad,
              (long long)k_pad);
-  PG_REQUIRE(ep.rows_per_marker == 1 || ep.rows_per_marker == 2, PG_ERR_INVALID, "assoc: rows_per_marker");
+  PG_REQUIRE(ep.rows_per_marker == 1 || ep.rows_per_marker == 2 || ep.rows_per_marker == 8 ||
+                 ep.rows_per_marker == 16,
+             PG_ERR_INVALID, "assoc: rows_per_marker %d", ep.rows_per_marker);
   CUtensorMap tm_qh, tm_q1, tm_q0, tm_v, tm_v127;
   const uint64_t pitch = static_cast<uint64_t>(k_pad);
   PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_qh, qh, k_pad, p_pad, pitch, kTileK, kTileP));

@@ -1,0 +1,786 @@
+// pg_ctx: the handle behind the C ABI (include/panelgwas_b200.h).
+//
+// One ctx per GPU. It owns the resident quantized panel, the per-batch device
+// buffers (grow-only), a CUDA stream and timing events. A scan call runs, in
+// stream order:  H2D (pitched) -> K1 stats -> K1 planes -> K2/K3 GEMM+epilogue
+// -> candidate sort (cub radix, deterministic) -> K4 t/p.  Results stay on the
+// device until fetched.
+//
+// Reference flow replaced (engine._run_scan_open / _process_batch,
+// /root/reference/pkg/src/panelgwas/engine.py:178-219, 381-398).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "assoc.cuh"
+#include "decode.cuh"
+#include "panel.cuh"
+#include "pg_common.cuh"
+#include "pstats.cuh"
+
+namespace pg {
+namespace {
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t cap = 0;
+  int ensure(size_t n) {
+    if (n <= cap && p != nullptr) return PG_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    const size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      set_error("device allocation of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
+      return PG_ERR_NOMEM;
+    }
+    cap = std::max<size_t>(n, 1);
+    return PG_OK;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+__global__ void count_skip_kernel(const int8_t* skip, int64_t m, unsigned long long* counts) {
+  unsigned long long a = 0, b = 0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    a += skip[i] == 1;
+    b += skip[i] == 2;
+  }
+  if (a) atomicAdd(counts, a);
+  if (b) atomicAdd(counts + 1, b);
+}
+
+__global__ void row_map_kernel(const int8_t* skip, int64_t m, int64_t* new_row, unsigned long long* n_ok) {
+  // single block, sequential-chunk scan: tiny (m ~ 1e4..1e5) and deterministic
+  __shared__ long long part[1024];
+  const int64_t per = (m + blockDim.x - 1) / blockDim.x;
+  const int64_t lo = threadIdx.x * per, hi = std::min<int64_t>(m, lo + per);
+  long long c = 0;
+  for (int64_t i = lo; i < hi; ++i) c += (skip[i] == 0);
+  part[threadIdx.x] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long run = 0;
+    for (unsigned i = 0; i < blockDim.x; ++i) {
+      const long long v = part[i];
+      part[i] = run;
+      run += v;
+    }
+    *n_ok = static_cast<unsigned long long>(run);
+  }
+  __syncthreads();
+  long long base = part[threadIdx.x];
+  for (int64_t i = lo; i < hi; ++i) new_row[i] = (skip[i] == 0) ? base++ : -1;
+}
+
+__global__ void rbar_kernel(const double* rbar_in, int64_t n, int64_t p_pad, float* rbar_out) {
+  const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (p >= p_pad) return;
+  if (p >= n) {
+    rbar_out[p] = __int_as_float(0x7f800000);  // +inf: padding phenotypes never match
+    return;
+  }
+  // widen so the fp32 estimate never drops a pair whose exact fp64 |r| reaches the bar
+  const double b = rbar_in[p];
+  const double w = b * (1.0 - 1e-5) - 1e-7;
+  rbar_out[p] = __double2float_rd(w);
+}
+
+}  // namespace
+}  // namespace pg
+
+struct pg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+
+  // panel
+  bool have_panel = false;
+  int64_t n_src = 0, n_kept = 0, n_pheno = 0, p_pad = 0, k_pad = 0;
+  pg::DBuf<int8_t> qh, q1, q0;
+  pg::DBuf<double> scale_d, maxabs;
+  pg::DBuf<float> scale_f, cq_f;
+  pg::DBuf<long long> cq;
+  pg::DBuf<int64_t> gidx;
+  pg::DBuf<uint32_t> keep_bits;
+  pg::DBuf<double> ystage;
+
+  // scan parameters
+  double df = 1.0;
+  int mode = PG_MODE_THRESHOLD;
+  bool have_scan = false;
+  pg::DBuf<float> rbar;
+  pg::DBuf<double> rbar_in;
+  pg::DBuf<unsigned int> max_abs_r;
+
+  // batch buffers
+  pg::DBuf<uint8_t> packed;
+  pg::DBuf<long long> n_miss, s_u, ss_u;
+  pg::DBuf<double> sum_d, af, var, mu_d, invd_d;
+  pg::DBuf<float> mu_f, invd_f;
+  pg::DBuf<int8_t> skip;
+  pg::DBuf<int> flags;
+  pg::DBuf<int8_t> v, v127;
+  pg::DBuf<unsigned long long> cand_key, cand_key_sorted;
+  pg::DBuf<double> cand_r, cand_r_sorted, cand_t, cand_p;
+  pg::DBuf<int64_t> cand_rows, cand_cols;
+  pg::DBuf<int> cand_count;
+  pg::DBuf<unsigned long long> counters;  // [0] clamp, [1..2] skip counts, [3] n_ok
+  pg::DBuf<uint8_t> sort_tmp;
+  pg::DBuf<double> full_r;
+  pg::DBuf<int64_t> new_row;
+  pg::DBuf<uint8_t> full_out;
+  pg::DBuf<double> scratch_a, scratch_b, scratch_c, scratch_d;
+
+  // last batch
+  int64_t last_m = 0, last_ncand = 0;
+  int last_R = 1;
+  int64_t cand_capacity = 0;
+};
+
+namespace pg {
+namespace {
+
+int ctx_check(pg_ctx* c) {
+  PG_REQUIRE(c != nullptr, PG_ERR_INVALID, "null pg_ctx");
+  PG_CUDA_CHECK(cudaSetDevice(c->device));
+  return PG_OK;
+}
+
+int upload_panel_common(pg_ctx* c, const double* d_y, int64_t n_kept, int64_t n_pheno, int64_t ld,
+                        const int64_t* h_gidx, int64_t n_src) {
+  PG_REQUIRE(n_kept >= 1 && n_pheno >= 1 && n_src >= n_kept && ld >= n_pheno, PG_ERR_INVALID,
+             "invalid panel geometry n_kept=%lld n_pheno=%lld n_src=%lld", (long long)n_kept, (long long)n_pheno,
+             (long long)n_src);
+  std::vector<uint32_t> bits;
+  c->n_src = n_src;
+  c->n_kept = n_kept;
+  c->n_pheno = n_pheno;
+  c->p_pad = round_up(n_pheno, kTileP);
+  c->k_pad = round_up(n_src, 64);
+  bits.assign(c->k_pad / 32 + 1, 0u);
+  for (int64_t i = 0; i < n_kept; ++i) {
+    const int64_t g = h_gidx[i];
+    PG_REQUIRE(g >= 0 && g < n_src, PG_ERR_INVALID, "geno_row_index out of range");
+    PG_REQUIRE(((bits[g >> 5] >> (g & 31)) & 1u) == 0, PG_ERR_INVALID, "duplicate geno_row_index %lld",
+               (long long)g);
+    bits[g >> 5] |= 1u << (g & 31);
+  }
+  const size_t plane = static_cast<size_t>(c->p_pad) * c->k_pad;
+  PG_CHECK_STATUS(c->qh.ensure(plane));
+  PG_CHECK_STATUS(c->q1.ensure(plane));
+  PG_CHECK_STATUS(c->q0.ensure(plane));
+  PG_CHECK_STATUS(c->scale_d.ensure(c->p_pad));
+  PG_CHECK_STATUS(c->scale_f.ensure(c->p_pad));
+  PG_CHECK_STATUS(c->cq.ensure(c->p_pad));
+  PG_CHECK_STATUS(c->cq_f.ensure(c->p_pad));
+  PG_CHECK_STATUS(c->maxabs.ensure(c->p_pad));
+  PG_CHECK_STATUS(c->gidx.ensure(n_kept));
+  PG_CHECK_STATUS(c->keep_bits.ensure(bits.size()));
+  PG_CUDA_CHECK(cudaMemcpyAsync(c->gidx.p, h_gidx, sizeof(int64_t) * n_kept, cudaMemcpyHostToDevice, c->stream));
+  PG_CUDA_CHECK(
+      cudaMemcpyAsync(c->keep_bits.p, bits.data(), sizeof(uint32_t) * bits.size(), cudaMemcpyHostToDevice, c->stream));
+  PanelPlanes pp;
+  pp.qh = c->qh.p;
+  pp.q1 = c->q1.p;
+  pp.q0 = c->q0.p;
+  pp.scale_d = c->scale_d.p;
+  pp.scale_f = c->scale_f.p;
+  pp.cq = c->cq.p;
+  pp.cq_f = c->cq_f.p;
+  PG_CHECK_STATUS(panel_quantize(d_y, n_kept, n_pheno, ld, c->gidx.p, c->k_pad, c->p_pad, pp, c->maxabs.p, c->stream));
+  PG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  c->have_panel = true;
+  c->have_scan = false;
+  return PG_OK;
+}
+
+int64_t expected_row_bytes(int kind, int64_t n_src) {
+  switch (kind) {
+    case PG_GENO_BED: return (n_src + 3) / 4;
+    case PG_GENO_BGEN8: return n_src * 3;
+    case PG_GENO_BGEN16: return n_src * 5;
+    case PG_GENO_DENSE_F64: return n_src * 8;
+    default: return -1;
+  }
+}
+
+int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t pitch, pg_batch_info* info) {
+  PG_REQUIRE(c->have_panel, PG_ERR_STATE, "pg_scan: no panel uploaded (pg_ctx_set_panel)");
+  PG_REQUIRE(c->have_scan, PG_ERR_STATE, "pg_scan: scan parameters not set (pg_ctx_set_scan)");
+  PG_REQUIRE(m >= 1, PG_ERR_INVALID, "pg_scan: empty batch");
+  cudaStream_t s = c->stream;
+  PG_CUDA_CHECK(cudaEventRecord(c->ev[0], s));
+
+  GenoBlock b;
+  b.kind = kind;
+  b.data = d_data;
+  b.pitch = pitch;
+  b.n_markers = m;
+  b.n_src = c->n_src;
+  b.n_kept = c->n_kept;
+  b.keep_bits = c->keep_bits.p;
+
+  const int64_t m_cap = round_up(m, 256);  // enough marker slots for any rows_per_marker
+  PG_CHECK_STATUS(c->flags.ensure(2));
+  PG_CUDA_CHECK(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * 2, s));
+  int hflags[2] = {0, 0};
+  if (kind == PG_GENO_DENSE_F64) {
+    MarkerStats tmp;
+    tmp.flags = c->flags.p;
+    PG_CHECK_STATUS(geno_check_integral(b, tmp, s));
+    PG_CUDA_CHECK(cudaMemcpyAsync(hflags, c->flags.p, sizeof(int) * 2, cudaMemcpyDeviceToHost, s));
+    PG_CUDA_CHECK(cudaStreamSynchronize(s));
+    b.dense_real = hflags[1] != 0;
+  }
+  for (auto* buf : {&c->n_miss, &c->s_u, &c->ss_u}) PG_CHECK_STATUS(buf->ensure(m_cap));
+  for (auto* buf : {&c->sum_d, &c->af, &c->var, &c->mu_d, &c->invd_d}) PG_CHECK_STATUS(buf->ensure(m_cap));
+  PG_CHECK_STATUS(c->mu_f.ensure(m_cap));
+  PG_CHECK_STATUS(c->invd_f.ensure(m_cap));
+  PG_CHECK_STATUS(c->skip.ensure(m_cap));
+  MarkerStats st;
+  st.n_miss = c->n_miss.p;
+  st.s_u = c->s_u.p;
+  st.ss_u = c->ss_u.p;
+  st.sum_d = c->sum_d.p;
+  st.af = c->af.p;
+  st.var = c->var.p;
+  st.skip = c->skip.p;
+  st.mu_d = c->mu_d.p;
+  st.mu_f = c->mu_f.p;
+  st.invd_d = c->invd_d.p;
+  st.invd_f = c->invd_f.p;
+  st.flags = c->flags.p;
+  PG_CHECK_STATUS(geno_stats(b, st, m_cap, s));
+  PG_CUDA_CHECK(cudaMemcpyAsync(hflags, c->flags.p, sizeof(int) * 2, cudaMemcpyDeviceToHost, s));
+  PG_CUDA_CHECK(cudaStreamSynchronize(s));
+  const int R = geno_rows_per_marker(b, hflags[0] != 0);
+  const int64_t c_pad = round_up(m * R, kTileC);
+  PG_CHECK_STATUS(c->v.ensure(static_cast<size_t>(c_pad) * c->k_pad));
+  PG_CHECK_STATUS(c->v127.ensure(static_cast<size_t>(c_pad) * c->k_pad));
+  PG_CHECK_STATUS(geno_planes(b, R, c->v.p, c->v127.p, c_pad, c->k_pad, s));
+  PG_CUDA_CHECK(cudaEventRecord(c->ev[1], s));
+
+  PG_CHECK_STATUS(c->counters.ensure(4));
+  PG_CUDA_CHECK(cudaMemsetAsync(c->counters.p, 0, sizeof(unsigned long long) * 4, s));
+  count_skip_kernel<<<64, 256, 0, s>>>(c->skip.p, m, c->counters.p + 1);
+  PG_CUDA_CHECK(cudaGetLastError());
+
+  AssocEpilogue ep{};
+  ep.rows_per_marker = R;
+  ep.m_valid = m;
+  ep.p_valid = c->n_pheno;
+  ep.mu_f = c->mu_f.p;
+  ep.mu_d = c->mu_d.p;
+  ep.invd_f = c->invd_f.p;
+  ep.invd_d = c->invd_d.p;
+  ep.scale_f = c->scale_f.p;
+  ep.scale_d = c->scale_d.p;
+  ep.cq_f = c->cq_f.p;
+  ep.cq = c->cq.p;
+  ep.max_abs_r = c->max_abs_r.p;
+  PG_CHECK_STATUS(c->cand_count.ensure(1));
+  ep.cand_count = c->cand_count.p;
+  int64_t ncand = 0;
+  if (c->mode == PG_MODE_FULL) {
+    PG_CHECK_STATUS(c->full_r.ensure(static_cast<size_t>(c_pad / R) * c->p_pad));
+    ep.full_r = c->full_r.p;
+    ep.full_ld = c->p_pad;
+    ep.rbar = nullptr;
+    ep.cand_cap = 0;
+    PG_CUDA_CHECK(cudaMemsetAsync(c->cand_count.p, 0, sizeof(int), s));
+    PG_CHECK_STATUS(launch_assoc(c->qh.p, c->q1.p, c->q0.p, c->p_pad, c->v.p, c->v127.p, c_pad, c->k_pad, ep, s));
+  } else {
+    ep.rbar = c->rbar.p;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      if (c->cand_capacity < 1024) {
+        PG_CHECK_STATUS(c->cand_key.ensure(1 << 20));
+        PG_CHECK_STATUS(c->cand_r.ensure(1 << 20));
+        c->cand_capacity = 1 << 20;
+      }
+      ep.cand_key = c->cand_key.p;
+      ep.cand_r = c->cand_r.p;
+      ep.cand_cap = c->cand_capacity;
+      PG_CUDA_CHECK(cudaMemsetAsync(c->cand_count.p, 0, sizeof(int), s));
+      PG_CHECK_STATUS(launch_assoc(c->qh.p, c->q1.p, c->q0.p, c->p_pad, c->v.p, c->v127.p, c_pad, c->k_pad, ep, s));
+      int hcount = 0;
+      PG_CUDA_CHECK(cudaMemcpyAsync(&hcount, c->cand_count.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+      PG_CUDA_CHECK(cudaStreamSynchronize(s));
+      ncand = hcount;
+      if (ncand <= c->cand_capacity) break;
+      // overflow: grow to fit and recompute (results are order-independent after the sort)
+      const int64_t newcap = ncand + ncand / 8 + 1024;
+      PG_CHECK_STATUS(c->cand_key.ensure(newcap));
+      PG_CHECK_STATUS(c->cand_r.ensure(newcap));
+      c->cand_capacity = newcap;
+      if (c->max_abs_r.p) {
+        // max |r| is idempotent under recomputation; nothing to undo
+      }
+    }
+  }
+  PG_CUDA_CHECK(cudaEventRecord(c->ev[2], s));
+
+  if (ncand > 0) {
+    PG_CHECK_STATUS(c->cand_key_sorted.ensure(ncand));
+    PG_CHECK_STATUS(c->cand_r_sorted.ensure(ncand));
+    PG_CHECK_STATUS(c->cand_t.ensure(ncand));
+    PG_CHECK_STATUS(c->cand_p.ensure(ncand));
+    PG_CHECK_STATUS(c->cand_rows.ensure(ncand));
+    PG_CHECK_STATUS(c->cand_cols.ensure(ncand));
+    int end_bit = 32;
+    while (end_bit < 64 && (1ull << (end_bit - 32)) <= static_cast<unsigned long long>(m)) ++end_bit;
+    size_t tmp_bytes = 0;
+    PG_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, c->cand_key.p, c->cand_key_sorted.p,
+                                                  c->cand_r.p, c->cand_r_sorted.p, ncand, 0, end_bit, s));
+    PG_CHECK_STATUS(c->sort_tmp.ensure(tmp_bytes));
+    PG_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(c->sort_tmp.p, tmp_bytes, c->cand_key.p, c->cand_key_sorted.p,
+                                                  c->cand_r.p, c->cand_r_sorted.p, ncand, 0, end_bit, s));
+    PG_CHECK_STATUS(finalize_candidates(c->cand_key_sorted.p, c->cand_r_sorted.p, ncand, c->df, c->cand_rows.p,
+                                        c->cand_cols.p, c->cand_r_sorted.p, c->cand_t.p, c->cand_p.p, c->counters.p,
+                                        s));
+  }
+  PG_CUDA_CHECK(cudaEventRecord(c->ev[3], s));
+  unsigned long long hc[4] = {0, 0, 0, 0};
+  PG_CUDA_CHECK(cudaMemcpyAsync(hc, c->counters.p, sizeof(hc), cudaMemcpyDeviceToHost, s));
+  PG_CUDA_CHECK(cudaStreamSynchronize(s));
+  c->last_m = m;
+  c->last_ncand = ncand;
+  c->last_R = R;
+  if (info) {
+    info->n_markers = m;
+    info->n_candidates = ncand;
+    info->clamp_count = static_cast<int64_t>(hc[0]);
+    info->n_skipped_monomorphic = static_cast<int64_t>(hc[1]);
+    info->n_skipped_all_missing = static_cast<int64_t>(hc[2]);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
+    info->decode_ms = ms;
+    cudaEventElapsedTime(&ms, c->ev[1], c->ev[2]);
+    info->gemm_ms = ms;
+  }
+  return PG_OK;
+}
+
+}  // namespace
+}  // namespace pg
+
+using namespace pg;
+
+extern "C" {
+
+int pg_ctx_create(int device, pg_ctx** out) {
+  PG_REQUIRE(out != nullptr, PG_ERR_INVALID, "pg_ctx_create: null out");
+  *out = nullptr;
+  int n = 0;
+  PG_CUDA_CHECK(cudaGetDeviceCount(&n));
+  PG_REQUIRE(device >= 0 && device < n, PG_ERR_CUDA, "no CUDA device %d (%d visible)", device, n);
+  cudaDeviceProp prop;
+  PG_CUDA_CHECK(cudaGetDeviceProperties(&prop, device));
+  PG_REQUIRE(prop.major == 10 && prop.minor == 0, PG_ERR_CUDA,
+             "device %d is sm_%d%d; panelgwas_b200 kernels are built for sm_100a (B200) only", device, prop.major,
+             prop.minor);
+  PG_CUDA_CHECK(cudaSetDevice(device));
+  pg_ctx* c = new pg_ctx();
+  c->device = device;
+  PG_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  for (auto& e : c->ev) PG_CUDA_CHECK(cudaEventCreate(&e));
+  *out = c;
+  return PG_OK;
+}
+
+int pg_ctx_destroy(pg_ctx* c) {
+  if (c == nullptr) return PG_OK;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (auto* b : {&c->qh, &c->q1, &c->q0, &c->v, &c->v127, &c->skip}) b->release();
+  for (auto* b : {&c->scale_d, &c->maxabs, &c->ystage, &c->rbar_in, &c->sum_d, &c->af, &c->var, &c->mu_d,
+                  &c->invd_d, &c->cand_r, &c->cand_r_sorted, &c->cand_t, &c->cand_p, &c->full_r, &c->scratch_a,
+                  &c->scratch_b, &c->scratch_c, &c->scratch_d})
+    b->release();
+  for (auto* b : {&c->scale_f, &c->cq_f, &c->rbar, &c->mu_f, &c->invd_f}) b->release();
+  for (auto* b : {&c->cq, &c->n_miss, &c->s_u, &c->ss_u}) b->release();
+  c->gidx.release();
+  c->keep_bits.release();
+  c->max_abs_r.release();
+  c->packed.release();
+  c->flags.release();
+  c->cand_key.release();
+  c->cand_key_sorted.release();
+  c->cand_rows.release();
+  c->cand_cols.release();
+  c->cand_count.release();
+  c->counters.release();
+  c->sort_tmp.release();
+  c->new_row.release();
+  c->full_out.release();
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return PG_OK;
+}
+
+int pg_ctx_sync(pg_ctx* c) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  return PG_OK;
+}
+
+int pg_ctx_set_panel(pg_ctx* c, const double* ytil, int64_t n_kept, int64_t n_pheno, int64_t ld,
+                     const int64_t* geno_row_index, int64_t n_samples_src) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(ytil != nullptr && geno_row_index != nullptr, PG_ERR_INVALID, "pg_ctx_set_panel: null input");
+  PG_REQUIRE(ld >= n_pheno && n_pheno >= 1 && n_kept >= 1, PG_ERR_INVALID, "pg_ctx_set_panel: bad shape");
+  PG_CHECK_STATUS(c->ystage.ensure(static_cast<size_t>(n_kept) * n_pheno));
+  PG_CUDA_CHECK(cudaMemcpy2DAsync(c->ystage.p, sizeof(double) * n_pheno, ytil, sizeof(double) * ld,
+                                  sizeof(double) * n_pheno, n_kept, cudaMemcpyHostToDevice, c->stream));
+  PG_CHECK_STATUS(upload_panel_common(c, c->ystage.p, n_kept, n_pheno, n_pheno, geno_row_index, n_samples_src));
+  c->ystage.release();
+  return PG_OK;
+}
+
+int pg_ctx_set_panel_device(pg_ctx* c, const double* d_ytil, int64_t n_kept, int64_t n_pheno, int64_t ld,
+                            const int64_t* geno_row_index, int64_t n_samples_src) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(d_ytil != nullptr && geno_row_index != nullptr, PG_ERR_INVALID, "pg_ctx_set_panel_device: null input");
+  return upload_panel_common(c, d_ytil, n_kept, n_pheno, ld, geno_row_index, n_samples_src);
+}
+
+int pg_ctx_panel_bytes(pg_ctx* c, int64_t* bytes) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(c->have_panel, PG_ERR_STATE, "no panel");
+  *bytes = 3 * c->p_pad * c->k_pad + c->p_pad * (8 + 4 + 8 + 4);
+  return PG_OK;
+}
+
+int pg_ctx_export_panel(pg_ctx* c, void* d_dst) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(c->have_panel, PG_ERR_STATE, "no panel");
+  uint8_t* d = static_cast<uint8_t*>(d_dst);
+  const size_t plane = static_cast<size_t>(c->p_pad) * c->k_pad;
+  const size_t pp = static_cast<size_t>(c->p_pad);
+  PG_CUDA_CHECK(cudaMemcpyAsync(d, c->qh.p, plane, cudaMemcpyDeviceToDevice, c->stream));
+  PG_CUDA_CHECK(cudaMemcpyAsync(d + plane, c->q1.p, plane, cudaMemcpyDeviceToDevice, c->stream));
+  PG_CUDA_CHECK(cudaMemcpyAsync(d + 2 * plane, c->q0.p, plane, cudaMemcpyDeviceToDevice, c->stream));
+  uint8_t* tail = d + 3 * plane;
+  PG_CUDA_CHECK(cudaMemcpyAsync(tail, c->scale_d.p, 8 * pp, cudaMemcpyDeviceToDevice, c->stream));
+  PG_CUDA_CHECK(cudaMemcpyAsync(tail + 8 * pp, c->scale_f.p, 4 * pp, cudaMemcpyDeviceToDevice, c->stream));
+  PG_CUDA_CHECK(cudaMemcpyAsync(tail + 12 * pp, c->cq.p, 8 * pp, cudaMemcpyDeviceToDevice, c->stream));
+  PG_CUDA_CHECK(cudaMemcpyAsync(tail + 20 * pp, c->cq_f.p, 4 * pp, cudaMemcpyDeviceToDevice, c->stream));
+  PG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  return PG_OK;
+}
+
+int pg_ctx_import_panel(pg_ctx* c, const void* d_src, int64_t n_kept, int64_t n_pheno,
+                        const int64_t* geno_row_index, int64_t n_samples_src) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(d_src != nullptr && geno_row_index != nullptr, PG_ERR_INVALID, "pg_ctx_import_panel: null input");
+  // geometry + keep mask exactly as set_panel would build them
+  std::vector<uint32_t> bits;
+  c->n_src = n_samples_src;
+  c->n_kept = n_kept;
+  c->n_pheno = n_pheno;
+  c->p_pad = round_up(n_pheno, kTileP);
+  c->k_pad = round_up(n_samples_src, 64);
+  bits.assign(c->k_pad / 32 + 1, 0u);
+  for (int64_t i = 0; i < n_kept; ++i) {
+    const int64_t g = geno_row_index[i];
+    PG_REQUIRE(g >= 0 && g < n_samples_src, PG_ERR_INVALID, "geno_row_index out of range");
+    bits[g >> 5] |= 1u << (g & 31);
+  }
+  const size_t plane = static_cast<size_t>(c->p_pad) * c->k_pad;
+  const size_t pp = static_cast<size_t>(c->p_pad);
+  PG_CHECK_STATUS(c->qh.ensure(plane));
+  PG_CHECK_STATUS(c->q1.ensure(plane));
+  PG_CHECK_STATUS(c->q0.ensure(plane));
+  PG_CHECK_STATUS(c->scale_d.ensure(pp));
+  PG_CHECK_STATUS(c->scale_f.ensure(pp));
+  PG_CHECK_STATUS(c->cq.ensure(pp));
+  PG_CHECK_STATUS(c->cq_f.ensure(pp));
+  PG_CHECK_STATUS(c->gidx.ensure(n_kept));
+  PG_CHECK_STATUS(c->keep_bits.ensure(bits.size()));
+  const uint8_t* s = static_cast<const uint8_t*>(d_src);
+  PG_CUDA_CHECK(cudaMemcpyAsync(c->qh.p, s, plane, cudaMemcpyDeviceToDevice, c->stream));
+  PG_CUDA_CHECK(cudaMemcpyAsync(c->q1.p, s + plane, plane, cudaMemcpyDeviceToDevice, c->stream));
+  PG_CUDA_CHECK(cudaMemcpyAsync(c->q0.p, s + 2 * plane, plane, cudaMemcpyDeviceToDevice, c->stream));
+  const uint8_t* tail = s + 3 * plane;
+  PG_CUDA_CHECK(cudaMemcpyAsync(c->scale_d.p, tail, 8 * pp, cudaMemcpyDeviceToDevice, c->stream));
+  PG_CUDA_CHECK(cudaMemcpyAsync(c->scale_f.p, tail + 8 * pp, 4 * pp, cudaMemcpyDeviceToDevice, c->stream));
+  PG_CUDA_CHECK(cudaMemcpyAsync(c->cq.p, tail + 12 * pp, 8 * pp, cudaMemcpyDeviceToDevice, c->stream));
+  PG_CUDA_CHECK(cudaMemcpyAsync(c->cq_f.p, tail + 20 * pp, 4 * pp, cudaMemcpyDeviceToDevice, c->stream));
+  PG_CUDA_CHECK(cudaMemcpyAsync(c->gidx.p, geno_row_index, sizeof(int64_t) * n_kept, cudaMemcpyHostToDevice,
+                                c->stream));
+  PG_CUDA_CHECK(cudaMemcpyAsync(c->keep_bits.p, bits.data(), sizeof(uint32_t) * bits.size(), cudaMemcpyHostToDevice,
+                                c->stream));
+  PG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  c->have_panel = true;
+  c->have_scan = false;
+  return PG_OK;
+}
+
+int pg_ctx_set_scan(pg_ctx* c, double df, int mode, const double* r_bar) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(c->have_panel, PG_ERR_STATE, "pg_ctx_set_scan: no panel");
+  PG_REQUIRE(df >= 1.0, PG_ERR_INVALID, "degrees of freedom %g < 1", df);
+  PG_REQUIRE(mode == PG_MODE_THRESHOLD || mode == PG_MODE_TOPK || mode == PG_MODE_FULL, PG_ERR_INVALID,
+             "unknown output mode %d", mode);
+  PG_REQUIRE(mode == PG_MODE_FULL || r_bar != nullptr, PG_ERR_INVALID, "r_bar required for THRESHOLD/TOPK");
+  c->df = df;
+  c->mode = mode;
+  PG_CHECK_STATUS(c->rbar.ensure(c->p_pad));
+  PG_CHECK_STATUS(c->rbar_in.ensure(c->n_pheno));
+  PG_CHECK_STATUS(c->max_abs_r.ensure(c->p_pad));
+  PG_CUDA_CHECK(cudaMemsetAsync(c->max_abs_r.p, 0, sizeof(unsigned) * c->p_pad, c->stream));
+  if (r_bar != nullptr) {
+    PG_CUDA_CHECK(
+        cudaMemcpyAsync(c->rbar_in.p, r_bar, sizeof(double) * c->n_pheno, cudaMemcpyHostToDevice, c->stream));
+    rbar_kernel<<<static_cast<unsigned>((c->p_pad + 255) / 256), 256, 0, c->stream>>>(c->rbar_in.p, c->n_pheno,
+                                                                                       c->p_pad, c->rbar.p);
+    PG_CUDA_CHECK(cudaGetLastError());
+  }
+  PG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  c->have_scan = true;
+  return PG_OK;
+}
+
+int pg_ctx_set_rbar(pg_ctx* c, const double* r_bar) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(c->have_scan && r_bar != nullptr, PG_ERR_STATE, "pg_ctx_set_rbar: scan not configured");
+  PG_CUDA_CHECK(cudaMemcpyAsync(c->rbar_in.p, r_bar, sizeof(double) * c->n_pheno, cudaMemcpyHostToDevice, c->stream));
+  rbar_kernel<<<static_cast<unsigned>((c->p_pad + 255) / 256), 256, 0, c->stream>>>(c->rbar_in.p, c->n_pheno, c->p_pad,
+                                                                                     c->rbar.p);
+  PG_CUDA_CHECK(cudaGetLastError());
+  PG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  return PG_OK;
+}
+
+int pg_scan(pg_ctx* c, int kind, const void* data, int64_t n_markers, int64_t row_bytes, pg_batch_info* info) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(c->have_panel, PG_ERR_STATE, "pg_scan: no panel uploaded (pg_ctx_set_panel)");
+  const int64_t expect = expected_row_bytes(kind, c->n_src);
+  PG_REQUIRE(expect > 0, PG_ERR_INVALID, "unknown genotype kind %d", kind);
+  PG_REQUIRE(row_bytes == expect, PG_ERR_FORMAT, "packed row has %lld bytes, expected %lld for %lld samples",
+             (long long)row_bytes, (long long)expect, (long long)c->n_src);
+  PG_REQUIRE(data != nullptr && n_markers >= 1, PG_ERR_INVALID, "pg_scan: empty batch");
+  const int64_t pitch = round_up(row_bytes, 16);
+  PG_CHECK_STATUS(c->packed.ensure(static_cast<size_t>(pitch) * n_markers));
+  PG_CUDA_CHECK(cudaMemcpy2DAsync(c->packed.p, pitch, data, row_bytes, row_bytes, n_markers, cudaMemcpyHostToDevice,
+                                  c->stream));
+  return scan_common(c, kind, c->packed.p, n_markers, pitch, info);
+}
+
+int pg_scan_device(pg_ctx* c, int kind, const void* d_data, int64_t n_markers, int64_t row_bytes, int64_t row_pitch,
+                   pg_batch_info* info) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(c->have_panel, PG_ERR_STATE, "pg_scan_device: no panel uploaded");
+  const int64_t expect = expected_row_bytes(kind, c->n_src);
+  PG_REQUIRE(expect > 0 && row_bytes == expect, PG_ERR_FORMAT, "row has %lld bytes, expected %lld",
+             (long long)row_bytes, (long long)expect);
+  PG_REQUIRE(row_pitch % 16 == 0 && row_pitch >= row_bytes, PG_ERR_INVALID, "row_pitch must be a multiple of 16");
+  PG_REQUIRE(reinterpret_cast<uintptr_t>(d_data) % 16 == 0, PG_ERR_INVALID, "device block must be 16-byte aligned");
+  return scan_common(c, kind, static_cast<const uint8_t*>(d_data), n_markers, row_pitch, info);
+}
+
+int pg_fetch_marker_stats(pg_ctx* c, double* af, int64_t* missing_count, double* variance, int8_t* skip) {
+  PG_CHECK_STATUS(ctx_check(c));
+  const int64_t m = c->last_m;
+  PG_REQUIRE(m > 0, PG_ERR_STATE, "no scanned batch");
+  if (af) PG_CUDA_CHECK(cudaMemcpyAsync(af, c->af.p, 8 * m, cudaMemcpyDeviceToHost, c->stream));
+  if (missing_count)
+    PG_CUDA_CHECK(cudaMemcpyAsync(missing_count, c->n_miss.p, 8 * m, cudaMemcpyDeviceToHost, c->stream));
+  if (variance) PG_CUDA_CHECK(cudaMemcpyAsync(variance, c->var.p, 8 * m, cudaMemcpyDeviceToHost, c->stream));
+  if (skip) PG_CUDA_CHECK(cudaMemcpyAsync(skip, c->skip.p, m, cudaMemcpyDeviceToHost, c->stream));
+  PG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  return PG_OK;
+}
+
+int pg_fetch_candidates(pg_ctx* c, int64_t* rows, int64_t* cols, double* r, double* t, double* p) {
+  PG_CHECK_STATUS(ctx_check(c));
+  const int64_t n = c->last_ncand;
+  if (n == 0) return PG_OK;
+  if (rows) PG_CUDA_CHECK(cudaMemcpyAsync(rows, c->cand_rows.p, 8 * n, cudaMemcpyDeviceToHost, c->stream));
+  if (cols) PG_CUDA_CHECK(cudaMemcpyAsync(cols, c->cand_cols.p, 8 * n, cudaMemcpyDeviceToHost, c->stream));
+  if (r) PG_CUDA_CHECK(cudaMemcpyAsync(r, c->cand_r_sorted.p, 8 * n, cudaMemcpyDeviceToHost, c->stream));
+  if (t) PG_CUDA_CHECK(cudaMemcpyAsync(t, c->cand_t.p, 8 * n, cudaMemcpyDeviceToHost, c->stream));
+  if (p) PG_CUDA_CHECK(cudaMemcpyAsync(p, c->cand_p.p, 8 * n, cudaMemcpyDeviceToHost, c->stream));
+  PG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  return PG_OK;
+}
+
+int pg_fetch_full(pg_ctx* c, void* out, int elem_bytes, int64_t* n_rows) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(c->mode == PG_MODE_FULL, PG_ERR_STATE, "pg_fetch_full: ctx not in FULL mode");
+  PG_REQUIRE(elem_bytes == 4 || elem_bytes == 8, PG_ERR_INVALID, "elem_bytes must be 4 or 8");
+  const int64_t m = c->last_m;
+  PG_REQUIRE(m > 0, PG_ERR_STATE, "no scanned batch");
+  cudaStream_t s = c->stream;
+  PG_CHECK_STATUS(c->new_row.ensure(m));
+  PG_CUDA_CHECK(cudaMemsetAsync(c->counters.p + 3, 0, sizeof(unsigned long long), s));
+  row_map_kernel<<<1, 1024, 0, s>>>(c->skip.p, m, c->new_row.p, c->counters.p + 3);
+  PG_CUDA_CHECK(cudaGetLastError());
+  unsigned long long n_ok = 0;
+  PG_CUDA_CHECK(cudaMemcpyAsync(&n_ok, c->counters.p + 3, 8, cudaMemcpyDeviceToHost, s));
+  PG_CUDA_CHECK(cudaStreamSynchronize(s));
+  if (n_rows) *n_rows = static_cast<int64_t>(n_ok);
+  if (out == nullptr || n_ok == 0) return PG_OK;
+  const size_t bytes = static_cast<size_t>(n_ok) * c->n_pheno * elem_bytes;
+  PG_CHECK_STATUS(c->full_out.ensure(bytes));
+  PG_CHECK_STATUS(full_rows_to_t(c->full_r.p, m, c->p_pad, c->n_pheno, c->new_row.p, c->df, elem_bytes,
+                                 c->full_out.p, c->counters.p, s));
+  PG_CUDA_CHECK(cudaMemcpyAsync(out, c->full_out.p, bytes, cudaMemcpyDeviceToHost, s));
+  PG_CUDA_CHECK(cudaStreamSynchronize(s));
+  return PG_OK;
+}
+
+int pg_fetch_max_abs_r(pg_ctx* c, double* out) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(c->have_scan, PG_ERR_STATE, "no scan");
+  std::vector<unsigned> bits(c->n_pheno);
+  PG_CUDA_CHECK(
+      cudaMemcpyAsync(bits.data(), c->max_abs_r.p, sizeof(unsigned) * c->n_pheno, cudaMemcpyDeviceToHost, c->stream));
+  PG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  for (int64_t i = 0; i < c->n_pheno; ++i) {
+    float f;
+    std::memcpy(&f, &bits[i], 4);
+    out[i] = f;
+  }
+  return PG_OK;
+}
+
+// ---- element-wise statistics (host arrays) ----
+int pg_t_from_r(pg_ctx* c, const double* r, int64_t n, double df, double* t) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(df >= 1.0, PG_ERR_INVALID, "t_from_r requires df >= 1");
+  if (n <= 0) return PG_OK;
+  PG_CHECK_STATUS(c->scratch_a.ensure(n));
+  PG_CHECK_STATUS(c->scratch_b.ensure(n));
+  PG_CUDA_CHECK(cudaMemcpyAsync(c->scratch_a.p, r, 8 * n, cudaMemcpyHostToDevice, c->stream));
+  PG_CHECK_STATUS(elementwise_t_from_r(c->scratch_a.p, n, df, c->scratch_b.p, c->stream));
+  PG_CUDA_CHECK(cudaMemcpyAsync(t, c->scratch_b.p, 8 * n, cudaMemcpyDeviceToHost, c->stream));
+  PG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  return PG_OK;
+}
+
+int pg_p_from_t(pg_ctx* c, const double* t, int64_t n, double df, double* p, int64_t* underflow) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(df >= 1.0, PG_ERR_INVALID, "p_from_t requires df >= 1");
+  if (underflow) *underflow = 0;
+  if (n <= 0) return PG_OK;
+  PG_CHECK_STATUS(c->scratch_a.ensure(n));
+  PG_CHECK_STATUS(c->scratch_b.ensure(n));
+  PG_CHECK_STATUS(c->counters.ensure(4));
+  PG_CUDA_CHECK(cudaMemsetAsync(c->counters.p, 0, 8, c->stream));
+  PG_CUDA_CHECK(cudaMemcpyAsync(c->scratch_a.p, t, 8 * n, cudaMemcpyHostToDevice, c->stream));
+  PG_CHECK_STATUS(elementwise_p_from_t(c->scratch_a.p, n, df, c->scratch_b.p, c->counters.p, c->stream));
+  PG_CUDA_CHECK(cudaMemcpyAsync(p, c->scratch_b.p, 8 * n, cudaMemcpyDeviceToHost, c->stream));
+  unsigned long long u = 0;
+  PG_CUDA_CHECK(cudaMemcpyAsync(&u, c->counters.p, 8, cudaMemcpyDeviceToHost, c->stream));
+  PG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  if (underflow) *underflow = static_cast<int64_t>(u);
+  return PG_OK;
+}
+
+int pg_reg_inc_beta(pg_ctx* c, const double* a, const double* b, const double* x, int64_t n, double* out) {
+  PG_CHECK_STATUS(ctx_check(c));
+  if (n <= 0) return PG_OK;
+  PG_CHECK_STATUS(c->scratch_a.ensure(n));
+  PG_CHECK_STATUS(c->scratch_b.ensure(n));
+  PG_CHECK_STATUS(c->scratch_c.ensure(n));
+  PG_CHECK_STATUS(c->scratch_d.ensure(n));
+  PG_CHECK_STATUS(c->flags.ensure(2));
+  PG_CUDA_CHECK(cudaMemsetAsync(c->flags.p, 0, 8, c->stream));
+  PG_CUDA_CHECK(cudaMemcpyAsync(c->scratch_a.p, a, 8 * n, cudaMemcpyHostToDevice, c->stream));
+  PG_CUDA_CHECK(cudaMemcpyAsync(c->scratch_b.p, b, 8 * n, cudaMemcpyHostToDevice, c->stream));
+  PG_CUDA_CHECK(cudaMemcpyAsync(c->scratch_c.p, x, 8 * n, cudaMemcpyHostToDevice, c->stream));
+  PG_CHECK_STATUS(
+      elementwise_reg_inc_beta(c->scratch_a.p, c->scratch_b.p, c->scratch_c.p, n, c->scratch_d.p, c->flags.p, c->stream));
+  PG_CUDA_CHECK(cudaMemcpyAsync(out, c->scratch_d.p, 8 * n, cudaMemcpyDeviceToHost, c->stream));
+  int err = 0;
+  PG_CUDA_CHECK(cudaMemcpyAsync(&err, c->flags.p, 4, cudaMemcpyDeviceToHost, c->stream));
+  PG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  PG_REQUIRE(err == 0, PG_ERR_STATE, "incomplete beta continued fraction did not converge; this is a bug");
+  return PG_OK;
+}
+
+int pg_t_threshold_for_p(pg_ctx* c, double p_threshold, double df, double* t_crit) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(p_threshold > 0.0 && p_threshold <= 1.0, PG_ERR_INVALID, "p_threshold must be in (0, 1]");
+  PG_REQUIRE(df >= 1.0, PG_ERR_INVALID, "p_from_t requires df >= 1");
+  PG_CHECK_STATUS(c->scratch_a.ensure(1));
+  PG_CHECK_STATUS(t_threshold(p_threshold, df, c->scratch_a.p, c->stream));
+  PG_CUDA_CHECK(cudaMemcpyAsync(t_crit, c->scratch_a.p, 8, cudaMemcpyDeviceToHost, c->stream));
+  PG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  return PG_OK;
+}
+
+// ---- genotype decode for the reader API ----
+int pg_decode_bed(pg_ctx* c, const uint8_t* packed, int64_t n_markers, int64_t row_bytes, int64_t n_samples,
+                  int elem_bytes, void* dosages, int64_t* missing_count) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(row_bytes == (n_samples + 3) / 4, PG_ERR_FORMAT,
+             "packed row has %lld bytes, expected %lld for %lld samples", (long long)row_bytes,
+             (long long)((n_samples + 3) / 4), (long long)n_samples);
+  PG_REQUIRE(elem_bytes == 4 || elem_bytes == 8, PG_ERR_INVALID, "elem_bytes must be 4 or 8");
+  if (n_markers <= 0) return PG_OK;
+  const int64_t pitch = round_up(row_bytes, 16);
+  PG_CHECK_STATUS(c->packed.ensure(static_cast<size_t>(pitch) * n_markers));
+  PG_CHECK_STATUS(c->full_out.ensure(static_cast<size_t>(n_markers) * n_samples * elem_bytes));
+  PG_CHECK_STATUS(c->new_row.ensure(n_markers));
+  PG_CUDA_CHECK(cudaMemcpy2DAsync(c->packed.p, pitch, packed, row_bytes, row_bytes, n_markers, cudaMemcpyHostToDevice,
+                                  c->stream));
+  GenoBlock b;
+  b.kind = PG_GENO_BED;
+  b.data = c->packed.p;
+  b.pitch = pitch;
+  b.n_markers = n_markers;
+  b.n_src = n_samples;
+  PG_CHECK_STATUS(geno_dosages(b, elem_bytes, c->full_out.p, c->new_row.p, c->stream));
+  PG_CUDA_CHECK(cudaMemcpyAsync(dosages, c->full_out.p, static_cast<size_t>(n_markers) * n_samples * elem_bytes,
+                                cudaMemcpyDeviceToHost, c->stream));
+  if (missing_count)
+    PG_CUDA_CHECK(cudaMemcpyAsync(missing_count, c->new_row.p, 8 * n_markers, cudaMemcpyDeviceToHost, c->stream));
+  PG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  return PG_OK;
+}
+
+int pg_decode_bgen(pg_ctx* c, const void* probs_and_ploidy, const uint8_t* unused, int64_t n_markers,
+                   int64_t n_samples, int bits, double* dosages, int64_t* missing_count) {
+  (void)unused;
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(bits == 8 || bits == 16, PG_ERR_INVALID, "bits must be 8 or 16");
+  if (n_markers <= 0) return PG_OK;
+  const int kind = bits == 8 ? PG_GENO_BGEN8 : PG_GENO_BGEN16;
+  const int64_t row_bytes = expected_row_bytes(kind, n_samples);
+  const int64_t pitch = round_up(row_bytes, 16);
+  PG_CHECK_STATUS(c->packed.ensure(static_cast<size_t>(pitch) * n_markers));
+  PG_CHECK_STATUS(c->full_out.ensure(static_cast<size_t>(n_markers) * n_samples * 8));
+  PG_CHECK_STATUS(c->new_row.ensure(n_markers));
+  PG_CUDA_CHECK(cudaMemcpy2DAsync(c->packed.p, pitch, probs_and_ploidy, row_bytes, row_bytes, n_markers,
+                                  cudaMemcpyHostToDevice, c->stream));
+  GenoBlock b;
+  b.kind = kind;
+  b.data = c->packed.p;
+  b.pitch = pitch;
+  b.n_markers = n_markers;
+  b.n_src = n_samples;
+  PG_CHECK_STATUS(geno_dosages(b, 8, c->full_out.p, c->new_row.p, c->stream));
+  PG_CUDA_CHECK(cudaMemcpyAsync(dosages, c->full_out.p, static_cast<size_t>(n_markers) * n_samples * 8,
+                                cudaMemcpyDeviceToHost, c->stream));
+  if (missing_count)
+    PG_CUDA_CHECK(cudaMemcpyAsync(missing_count, c->new_row.p, 8 * n_markers, cudaMemcpyDeviceToHost, c->stream));
+  PG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  return PG_OK;
+}
+
+}  // extern "C"

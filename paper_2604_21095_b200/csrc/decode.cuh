@@ -1,0 +1,55 @@
+// Genotype decode (K1): raw genotype blocks -> ternary GEMM rows + per-marker
+// integer statistics. See decode.cu.
+#pragma once
+#include <cstdint>
+
+#include "pg_common.cuh"
+
+namespace pg {
+
+// A block of markers resident on the device.
+struct GenoBlock {
+  int kind = PG_GENO_BED;     // PG_GENO_*
+  const uint8_t* data = nullptr;
+  int64_t pitch = 0;          // bytes between marker rows (multiple of 16)
+  int64_t n_markers = 0;
+  int64_t n_src = 0;          // samples per row in the source
+  int64_t n_kept = 0;         // N used by the statistics
+  const uint32_t* keep_bits = nullptr;  // [ceil(n_src/32)] bit i = sample i kept
+  int dense_real = 0;         // DENSE only: 1 -> fixed-point (2^-17) digits, 0 -> integral dosages
+};
+
+// u-units: the integer code each observed sample contributes to the GEMM.
+//   BED / integral dense : u = dosage - 1            (scale 1)
+//   BGEN (bits b)        : u = k - (2^b - 1), dosage = k / (2^b - 1)
+//   real dense           : u = rint((dosage - 1) * 2^17)
+double geno_unit_scale(const GenoBlock& b);
+// Rows per marker in the GEMM (ternary digits of u, plus a missing-mask row if any).
+int geno_rows_per_marker(const GenoBlock& b, bool any_missing);
+
+struct MarkerStats {
+  long long* n_miss = nullptr;  // [m] missing calls among kept samples
+  long long* s_u = nullptr;     // [m] sum of u over observed kept samples
+  long long* ss_u = nullptr;    // [m] sum of u^2
+  double* sum_d = nullptr;      // [m] sum of dosages (real dense only)
+  double* af = nullptr;         // [m] allele frequency (NaN all-missing)
+  double* var = nullptr;        // [m] variance before scaling (1/N convention)
+  int8_t* skip = nullptr;       // [m] SkipReason
+  double* mu_d = nullptr;       // [m_pad] mean of u (GEMM epilogue)
+  float* mu_f = nullptr;
+  double* invd_d = nullptr;     // [m_pad] 1/sqrt(N V_u); NaN skipped / padding
+  float* invd_f = nullptr;
+  int* flags = nullptr;         // [2]: [0] any missing, [1] any non-integral dosage (dense)
+};
+
+// Pass 1 (dense only): flags[1] |= any non-integral kept dosage.
+int geno_check_integral(const GenoBlock& b, MarkerStats& st, cudaStream_t s);
+// Pass 2: integer statistics and derived per-marker quantities (all m_pad entries written).
+int geno_stats(const GenoBlock& b, MarkerStats& st, int64_t m_pad, cudaStream_t s);
+// Pass 3: ternary planes v / v127 [c_pad, k_pad] with R rows per marker.
+int geno_planes(const GenoBlock& b, int rows_per_marker, int8_t* v, int8_t* v127, int64_t c_pad, int64_t k_pad,
+                cudaStream_t s);
+// Dosage decode for the reader API: out[m, n_src] f32/f64 with NaN missing, missing counts.
+int geno_dosages(const GenoBlock& b, int elem_bytes, void* out, int64_t* missing, cudaStream_t s);
+
+}  // namespace pg

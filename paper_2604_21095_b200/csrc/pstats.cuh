@@ -1,0 +1,26 @@
+// Student-t statistics on the device (K4): r -> t -> two-sided p in fp64.
+#pragma once
+#include <cstdint>
+
+#include "pg_common.cuh"
+
+namespace pg {
+
+constexpr double kPFloor = 2.2250738585072014e-308;  // np.finfo(np.float64).tiny (kernel.py:29)
+constexpr double kRCap = 1.0 - 1e-15;                // kernel.py:39
+
+// Sorted candidates -> rows / cols / clipped r / t / p; counts |r| > 1 into *clamp.
+int finalize_candidates(const unsigned long long* key, const double* r_in, int64_t n, double df, int64_t* rows,
+                        int64_t* cols, double* r_out, double* t_out, double* p_out, unsigned long long* clamp,
+                        cudaStream_t s);
+// FULL mode: out[new_row(m), p] = t(r[m, p]) for non-skipped markers (elem 4 or 8).
+int full_rows_to_t(const double* r, int64_t m, int64_t ld, int64_t n_pheno, const int64_t* new_row, double df,
+                   int elem_bytes, void* out, unsigned long long* clamp, cudaStream_t s);
+int elementwise_t_from_r(const double* r, int64_t n, double df, double* t, cudaStream_t s);
+int elementwise_p_from_t(const double* t, int64_t n, double df, double* p, unsigned long long* underflow,
+                         cudaStream_t s);
+int elementwise_reg_inc_beta(const double* a, const double* b, const double* x, int64_t n, double* out,
+                             int* err_flag, cudaStream_t s);
+int t_threshold(double p_threshold, double df, double* d_out, cudaStream_t s);
+
+}  // namespace pg

@@ -1,0 +1,377 @@
+"""Scan orchestration on the B200.
+
+API and semantics of /root/reference/pkg/src/panelgwas/engine.py (ScanConfig,
+ScanSummary, plan_batches, run_scan): same output files, record order,
+summary keys and error behaviour. What differs is where the work happens:
+
+  reference (_process_batch, engine.py:178-219)   this engine
+  --------------------------------------------   ---------------------------------
+  host decode to f32/f64 dosages                  raw rows -> device (pg_scan)
+  prepare_genotype_batch (numpy, f64)             K1 integer stats + ternary planes
+  correlate: f64 DGEMM on 256-row tiles           K2 int8 tcgen05 GEMM, exact
+  premask |r| >= r_bar, t for candidates          K3 fused epilogue + cub sort
+  ThresholdWriter p_from_t                        K4 fp64 Student-t on device
+
+The panel is residualized / standardized on the host once (as the reference
+does), then quantized and kept resident in HBM. Batches are read on a
+background thread while the device scans the previous one. Because every
+(marker, phenotype) statistic is an exact integer contraction followed by a
+fixed fp64 epilogue, results are identical for any batch size, worker count
+or GPU count.
+"""
+
+from __future__ import annotations
+
+import enum
+import json
+import sys
+import time
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass, field
+from pathlib import Path
+
+import numpy as np
+
+from . import _native, kernel, output, phenotypes
+from .errors import ConfigError, PanelGwasError
+from .genotypes.types import SourceSpec, open_genotype_source
+from .kernel import SkipReason
+from .phenotypes import MissingPolicy, PanelState
+
+
+class Precision(enum.Enum):
+    F32_STORE_F64_ACC = "f32"
+    F64 = "f64"
+
+
+class DfMode(enum.Enum):
+    PAPER_N_MINUS_2 = "paper"
+    ADJUSTED = "adjusted"
+
+
+class OutputMode(enum.Enum):
+    THRESHOLD = "threshold"
+    TOPK = "topk"
+    FULL = "full"
+
+
+DEFAULT_BATCH_SIZE = 4096
+DEFAULT_P_THRESHOLD = 1e-4
+DEFAULT_TOP_K = 100
+DEFAULT_FULL_BYTE_BUDGET = 16 * 1024**3
+
+# device batches are sized for the GEMM (>= this many markers) and bounded in memory
+_MIN_DEVICE_BATCH = 8192
+_MAX_GEMM_ROWS = 1 << 17
+_MAX_FULL_BYTES = 2 << 30
+
+_MODE_CODE = {
+    OutputMode.THRESHOLD: _native.PG_MODE_THRESHOLD,
+    OutputMode.TOPK: _native.PG_MODE_TOPK,
+    OutputMode.FULL: _native.PG_MODE_FULL,
+}
+
+
+@dataclass
+class ScanConfig:
+    """Everything a scan needs; defaults match the CLI."""
+
+    source: SourceSpec
+    pheno_path: Path
+    out_path: Path
+    covar_path: Path | None = None
+    keep_path: Path | None = None
+    remove_path: Path | None = None
+    id_column: str = "IID"
+    delimiter: str = "\t"
+    missing_policy: MissingPolicy = MissingPolicy.MEAN_IMPUTE
+    batch_size: int = DEFAULT_BATCH_SIZE
+    precision: Precision = Precision.F32_STORE_F64_ACC
+    df_mode: DfMode = DfMode.PAPER_N_MINUS_2
+    residualize_genotypes: bool = False
+    rank_tolerance: float = 1e-8
+    output_mode: OutputMode = OutputMode.THRESHOLD
+    p_threshold: float = DEFAULT_P_THRESHOLD
+    top_k: int = DEFAULT_TOP_K
+    worker_count: int = 1
+    full_byte_budget: int = DEFAULT_FULL_BYTE_BUDGET
+    allow_large_full: bool = False
+    qc_sidecar: bool = False
+    summary_to_stderr: bool = True
+    device: int | None = None
+    # markers per device launch; None = sized automatically (results do not depend on it)
+    device_batch: int | None = None
+
+    def validate(self) -> None:
+        if self.batch_size < 1:
+            raise ConfigError("batch_size must be >= 1")
+        if not 0.0 < self.p_threshold <= 1.0:
+            raise ConfigError("p_threshold must be in (0, 1]")
+        if self.top_k < 1:
+            raise ConfigError("top_k must be >= 1")
+        if self.worker_count < 1:
+            raise ConfigError("worker_count must be >= 1")
+
+
+@dataclass
+class ScanSummary:
+    """Scan accounting; markers_scanned + skipped == n_markers."""
+
+    n_markers: int
+    n_samples_source: int
+    n_samples_used: int
+    markers_scanned: int
+    markers_skipped_monomorphic: int
+    markers_skipped_all_missing: int
+    phenotypes_total: int
+    phenotypes_scanned: int
+    phenotypes_skipped_zero_variance: int
+    records_emitted: int
+    clamp_count: int
+    p_underflow_count: int
+    df: int
+    time_decode_s: float
+    time_prepare_s: float
+    time_correlate_s: float
+    time_emit_s: float
+    wall_s: float
+    exclusion_log: dict[str, int] = field(default_factory=dict)
+
+    _KEYS = (
+        "n_markers", "n_samples_source", "n_samples_used", "markers_scanned", "markers_skipped_monomorphic",
+        "markers_skipped_all_missing", "phenotypes_total", "phenotypes_scanned",
+        "phenotypes_skipped_zero_variance", "records_emitted", "clamp_count", "p_underflow_count", "df",
+        "time_decode_s", "time_prepare_s", "time_correlate_s", "time_emit_s", "wall_s",
+    )
+
+    def to_dict(self) -> dict:
+        d = {k: getattr(self, k) for k in self._KEYS}
+        for reason, count in self.exclusion_log.items():
+            d[f"excluded_{reason}"] = count
+        return d
+
+
+def plan_batches(n_markers: int, batch_size: int) -> list[tuple[int, int]]:
+    """Contiguous (start, count) spans covering [0, n_markers)."""
+    if n_markers < 1:
+        raise ValueError("plan_batches requires at least one marker")
+    if batch_size < 1:
+        raise ValueError("batch_size must be >= 1")
+    return [(s, min(batch_size, n_markers - s)) for s in range(0, n_markers, batch_size)]
+
+
+def abs_t_to_abs_r(abs_t, df: float):
+    """|r| with |t| = |r| sqrt(df / (1 - r^2)) (monotone inverse; inf -> 1)."""
+    with np.errstate(invalid="ignore", divide="ignore"):
+        r = abs_t / np.sqrt(df + np.square(abs_t))
+    return np.where(np.isinf(abs_t), 1.0, r)
+
+
+def threshold_premask(p_threshold: float, df: float) -> float:
+    """The |r| premask bar of a THRESHOLD scan (engine.py:321-330 of the reference)."""
+    t_crit = kernel.t_threshold_for_p(p_threshold, df)
+    if t_crit <= 0.0:
+        return 0.0
+    safe_t = t_crit * (1.0 - 1e-9)
+    return float(abs_t_to_abs_r(np.float64(safe_t), df) * (1.0 - 1e-12))
+
+
+def topk_premask(worst_abs_t: np.ndarray, t_floor: float, df: float) -> np.ndarray:
+    """Per-phenotype |r| bar from the TopK admission bar (engine.py:205-211 of the reference)."""
+    bar_t = np.minimum(worst_abs_t, t_floor) * (1.0 - 1e-12)
+    bar_r = abs_t_to_abs_r(np.maximum(bar_t, 0.0), df)
+    return np.where(bar_t <= 0.0, -1.0, bar_r * (1.0 - 1e-12))
+
+
+def device_batch_size(config: ScanConfig, n_markers: int, n_pheno: int) -> int:
+    """Markers per device launch: at least the configured batch, sized for the GEMM, memory-bounded."""
+    if config.device_batch is not None:
+        return max(1, min(int(config.device_batch), n_markers))
+    b = max(config.batch_size, _MIN_DEVICE_BATCH)
+    b = min(b, _MAX_GEMM_ROWS // 16 if config.source.format.value != "plink-bed" else _MAX_GEMM_ROWS)
+    if config.output_mode is OutputMode.FULL:
+        b = min(b, max(256, _MAX_FULL_BYTES // (8 * max(n_pheno, 1))))
+    return max(1, min(b, n_markers))
+
+
+@dataclass
+class _PreparedPanel:
+    ytil: np.ndarray
+    basis: kernel.CovariateBasis
+    pheno_names: list[str]
+    zero_variance: np.ndarray
+    panel: phenotypes.PhenotypePanel
+    align: phenotypes.SampleAlignment
+    df: float
+
+
+def prepare_panel(config: ScanConfig, source) -> _PreparedPanel:
+    """Tables -> alignment -> panel -> covariate basis -> residualized, standardized Y~ (host, once)."""
+    pheno_table = phenotypes.load_table(config.pheno_path, config.id_column, config.delimiter)
+    covar_table = (
+        phenotypes.load_table(config.covar_path, config.id_column, config.delimiter) if config.covar_path else None
+    )
+    keep = phenotypes.read_id_list(config.keep_path) if config.keep_path else None
+    remove = phenotypes.read_id_list(config.remove_path) if config.remove_path else None
+    align = phenotypes.align_samples(source.sample_ids, pheno_table, covar_table, keep, remove)
+    panel = phenotypes.build_panel(pheno_table, align, config.missing_policy)
+    n = align.n_kept
+    if covar_table is not None:
+        c_matrix = phenotypes.covariate_matrix(covar_table, align)
+        c_names = covar_table.column_names
+    else:
+        c_matrix = np.zeros((n, 0))
+        c_names = []
+    basis = kernel.build_covariate_basis(c_matrix, True, config.rank_tolerance, c_names)
+    panel.y = kernel.residualize(panel.y, basis)
+    panel.state = PanelState.RESIDUALIZED
+    ytil, _sd, zero_variance = kernel.standardize_columns(panel.y)
+    panel.y = ytil
+    panel.state = PanelState.STANDARDIZED
+    kept_cols = np.nonzero(~zero_variance)[0]
+    names = [panel.phenotype_names[j] for j in kept_cols]
+    if not names:
+        raise PanelGwasError("every phenotype has zero variance; nothing to scan")
+    ytil = np.ascontiguousarray(ytil[:, kept_cols])
+    df = float(n - 2) if config.df_mode is DfMode.PAPER_N_MINUS_2 else float(n - basis.rank - 1)
+    if df < 1:
+        raise ConfigError(f"degrees of freedom {df:.0f} < 1 (n={n}, basis rank={basis.rank})")
+    return _PreparedPanel(ytil, basis, names, zero_variance, panel, align, df)
+
+
+def run_scan(config: ScanConfig) -> ScanSummary:
+    """Execute a full scan on the GPU and write results plus the summary files."""
+    wall0 = time.perf_counter()
+    config.validate()
+    source = open_genotype_source(config.source)
+    try:
+        return _run_scan_open(config, source, wall0)
+    finally:
+        source.close()
+
+
+def _run_scan_open(config: ScanConfig, source, wall0: float) -> ScanSummary:
+    from ._device import DeviceContext
+
+    if config.residualize_genotypes:
+        raise ConfigError(
+            "residualize_genotypes (extension mode) is not available on the device path yet; "
+            "run the paper-mode scan (residualize_genotypes=False)"
+        )
+    prep = prepare_panel(config, source)
+    n = prep.align.n_kept
+    df = prep.df
+    if source.n_markers < 1:
+        raise PanelGwasError("genotype source has no markers")
+    dtype = np.dtype(np.float32 if config.precision is Precision.F32_STORE_F64_ACC else np.float64)
+    names = prep.pheno_names
+    n_pheno = len(names)
+
+    if config.output_mode is OutputMode.FULL:
+        projected = source.n_markers * n_pheno * dtype.itemsize
+        if projected > config.full_byte_budget and not config.allow_large_full:
+            raise ConfigError(
+                f"FULL output would be ~{projected} bytes, over the {config.full_byte_budget}-byte budget; "
+                "pass the large-output override to proceed"
+            )
+        writer = output.FullMatrixWriter(config.out_path, dtype, df, n, source.counts_allele1, names)
+    elif config.output_mode is OutputMode.TOPK:
+        writer = output.TopKWriter(config.out_path, config.top_k, df, n, source.counts_allele1, names)
+    else:
+        writer = output.ThresholdWriter(config.out_path, config.p_threshold, df, n, source.counts_allele1, names)
+
+    ctx = DeviceContext(config.device)
+    try:
+        ctx.set_panel(prep.ytil, prep.align.genotype_row_index, source.n_samples)
+        t_floor = np.inf
+        if config.output_mode is OutputMode.THRESHOLD:
+            rbar = np.full(n_pheno, threshold_premask(config.p_threshold, df))
+        elif config.output_mode is OutputMode.TOPK:
+            t_floor = kernel.t_threshold_for_p(kernel.P_FLOOR, df)
+            rbar = topk_premask(writer.worst_abs_t, t_floor, df)
+        else:
+            rbar = None
+        ctx.set_scan(df, _MODE_CODE[config.output_mode], rbar)
+
+        skip_mono = skip_missing = clamp_total = 0
+        t_decode = t_prepare = t_corr = t_emit = 0.0
+        qc_rows: list[str] = []
+        step = device_batch_size(config, source.n_markers, n_pheno)
+        plan = plan_batches(source.n_markers, step)
+        read_kw = {"dtype": dtype} if config.source.format.value == "dense" else {}
+
+        def read(span):
+            t0 = time.perf_counter()
+            block = source.read_raw_block(span[0], span[1], **read_kw)
+            return block, time.perf_counter() - t0
+
+        with ThreadPoolExecutor(max_workers=1) as reader:
+            nxt = reader.submit(read, plan[0])
+            for bi, (start, count) in enumerate(plan):
+                (kind, rows, row_bytes), dt_read = nxt.result()
+                t_decode += dt_read
+                if bi + 1 < len(plan):
+                    nxt = reader.submit(read, plan[bi + 1])
+                res = ctx.scan(kind, rows, row_bytes, full_elem_bytes=dtype.itemsize)
+                t_prepare += res.decode_ms / 1e3
+                t_corr += res.gemm_ms / 1e3
+                markers = tuple(source.marker_catalog[start:start + count])
+                batch = output.BatchStats(
+                    markers=markers, allele_frequency=res.af, missing_count=res.missing_count,
+                    skip_reason=res.skip, clamp_count=res.clamp_count, cand_rows=res.cand_rows,
+                    cand_cols=res.cand_cols, cand_r=res.cand_r, cand_t=res.cand_t, t_rows=res.t_rows,
+                    cand_p=res.cand_p,
+                )
+                clamp_total += res.clamp_count
+                skip_mono += int(np.count_nonzero(res.skip == SkipReason.MONOMORPHIC))
+                skip_missing += int(np.count_nonzero(res.skip == SkipReason.ALL_MISSING))
+                if config.qc_sidecar:
+                    for i in np.nonzero(res.skip)[0].tolist():
+                        qc_rows.append(f"marker\t{markers[i].id}\t{SkipReason(int(res.skip[i])).name}\n")
+                t0 = time.perf_counter()
+                writer.emit(batch)
+                t_emit += time.perf_counter() - t0
+                if config.output_mode is OutputMode.TOPK:
+                    ctx.set_rbar(topk_premask(writer.worst_abs_t, t_floor, df))
+    finally:
+        ctx.close()
+
+    t0 = time.perf_counter()
+    records = writer.finalize()
+    t_emit += time.perf_counter() - t0
+
+    if config.qc_sidecar:
+        with open(Path(str(config.out_path) + ".qc.tsv"), "w") as fh:
+            fh.write("KIND\tNAME\tREASON\n")
+            fh.writelines(qc_rows)
+            for j in np.nonzero(prep.zero_variance)[0].tolist():
+                fh.write(f"phenotype\t{prep.panel.phenotype_names[j]}\tZERO_VARIANCE\n")
+
+    summary = ScanSummary(
+        n_markers=source.n_markers,
+        n_samples_source=source.n_samples,
+        n_samples_used=n,
+        markers_scanned=source.n_markers - skip_mono - skip_missing,
+        markers_skipped_monomorphic=skip_mono,
+        markers_skipped_all_missing=skip_missing,
+        phenotypes_total=prep.panel.n_phenotypes,
+        phenotypes_scanned=n_pheno,
+        phenotypes_skipped_zero_variance=int(np.count_nonzero(prep.zero_variance)),
+        records_emitted=records,
+        clamp_count=clamp_total,
+        p_underflow_count=writer.p_underflow_count,
+        df=int(df),
+        time_decode_s=t_decode,
+        time_prepare_s=t_prepare,
+        time_correlate_s=t_corr,
+        time_emit_s=t_emit,
+        wall_s=time.perf_counter() - wall0,
+        exclusion_log=dict(prep.align.exclusion_log),
+    )
+    with open(Path(str(config.out_path) + ".summary.json"), "w") as fh:
+        json.dump(summary.to_dict(), fh, indent=2, sort_keys=True)
+        fh.write("\n")
+    if config.summary_to_stderr:
+        for key, value in summary.to_dict().items():
+            print(f"{key}={value}", file=sys.stderr)
+    return summary

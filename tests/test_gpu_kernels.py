@@ -1,0 +1,130 @@
+"""Device kernels behind the library API vs golden reference outputs and the oracle.
+
+Bit-exact: genotype decode (PLINK / BGEN), missing counts, skip flags.
+Tolerance (fp64 libm differences only): p-values, t, prepare, correlate."""
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2604_21095_b200 as pg
+from oracle import scan_oracle as orc
+
+pytestmark = pytest.mark.gpu
+GOLD = Path(__file__).parent / "golden"
+
+
+def nan_eq(a, b):
+    return np.array_equal(np.nan_to_num(a, nan=-7.0), np.nan_to_num(b, nan=-7.0))
+
+
+def test_decode_bed_codes_bit_exact():
+    g = np.load(GOLD / "decode.npz")
+    for i in range(6):
+        got = pg.decode_bed_codes(g[f"fixed{i}_bytes"].tobytes(), int(g[f"fixed{i}_n"]))
+        assert nan_eq(got, g[f"fixed{i}_dosage"])
+    n = int(g["rand_n"])
+    for i in range(g["rand_packed"].shape[0]):
+        assert nan_eq(pg.decode_bed_codes(g["rand_packed"][i].tobytes(), n), g["rand_dosage"][i])
+    with pytest.raises(pg.FormatError):
+        pg.decode_bed_codes(b"\x00\x00", 4)
+
+
+def test_plink_reader_round_trip(tmp_path):
+    rng = np.random.default_rng(77)
+    for case in range(20):
+        m, n = int(rng.integers(1, 17)), int(rng.integers(1, 26))
+        d = rng.integers(0, 3, size=(m, n)).astype(np.float64)
+        d[rng.random((m, n)) < 0.15] = np.nan
+        pg.write_bed_trio(tmp_path / f"rt{case}", d, [f"I{j}" for j in range(n)])
+        src = pg.PlinkSource(tmp_path / f"rt{case}.bed", tmp_path / f"rt{case}.bim", tmp_path / f"rt{case}.fam")
+        b = src.read_marker_batch(0, m)
+        b32 = src.read_marker_batch(0, m, dtype=np.float32)
+        src.close()
+        assert nan_eq(b.dosages, d)
+        assert b32.dosages.dtype == np.float32 and nan_eq(b32.dosages, d.astype(np.float32))
+        assert np.array_equal(b.missing_count, np.isnan(d).sum(axis=1))
+
+
+def test_bgen_decode_bit_exact():
+    g = np.load(GOLD / "bgen.npz")
+    for bits in (8, 16):
+        src = pg.BgenSource(GOLD / f"bgen{bits}.bgen")
+        raw = src.read_marker_batch(0, src.n_markers)
+        src.close()
+        assert nan_eq(raw.dosages, g[f"b{bits}_dosage"])
+        assert np.array_equal(raw.missing_count, g[f"b{bits}_missing"])
+
+
+def test_p_from_t_matches_reference():
+    g = np.load(GOLD / "pvalues.npz")
+    # the log-prefactor lgamma(a+b) - lgamma(a) - lgamma(b) cancels ~log10(a) digits at large df;
+    # device and host libm lgamma differ by a few ulps there (reference itself is only that accurate)
+    for i, df in enumerate(g["dfs"]):
+        rtol = 1e-12 if df <= 100 else (2e-9 if df <= 1e5 else 5e-8)
+        got = pg.p_from_t(g["t"], df)
+        bad = ~np.isclose(got, g["p"][i], rtol=rtol, atol=0)
+        assert not bad.any(), (df, g["t"][bad][:5], got[bad][:5], g["p"][i][bad][:5])
+    assert pg.p_from_t(0.0, 7.0) == 1.0
+    assert pg.p_from_t(np.inf, 7.0) == pg.P_FLOOR
+    with pytest.raises(ValueError):
+        pg.p_from_t(1.0, 0.5)
+
+
+def test_closed_forms():
+    t = np.array([0.1, 0.7, 1.3, 2.5, 10.0])
+    np.testing.assert_allclose(pg.p_from_t(t, 1.0), (2 / np.pi) * np.arctan(1 / t), rtol=1e-12)
+    np.testing.assert_allclose(pg.p_from_t(t, 2.0), 1.0 - t / np.sqrt(2.0 + t * t), rtol=1e-12)
+
+
+def test_reg_inc_beta_and_threshold():
+    g = np.load(GOLD / "pvalues.npz")
+    np.testing.assert_allclose(pg.reg_inc_beta(g["ib_a"], g["ib_b"], g["ib_x"]), g["ib"], rtol=1e-11, atol=1e-300)
+    for k, (pt, df) in enumerate(g["crit_cases"]):
+        assert pg.t_threshold_for_p(pt, df) == pytest.approx(g["crit"][k], rel=1e-12)
+    assert pg.t_threshold_for_p(1e-4, 22998.0) == pytest.approx(3.8912744581499874, rel=1e-11)
+    with pytest.raises(ValueError):
+        pg.reg_inc_beta(0.0, 1.0, 0.5)
+
+
+def test_t_from_r():
+    g = np.load(GOLD / "pvalues.npz")
+    for i, df in enumerate((2.0, 11.0, 22998.0)):
+        got = pg.t_from_r(g["r"], df)
+        np.testing.assert_allclose(got, g["t_from_r"][i], rtol=1e-14)
+    assert pg.t_from_r(1.0, 10.0) == np.inf and pg.t_from_r(-1.0, 10.0) == -np.inf
+    assert pg.t_from_r(0.5, 2.0) == pytest.approx(np.sqrt(2.0 / 3.0), rel=1e-15)
+
+
+def test_prepare_matches_reference():
+    g = np.load(GOLD / "prepare.npz")
+    d = g["dosages"]
+    raw = pg.RawBatch(tuple(pg.MarkerRecord("1", f"m{i}", i, "A", "B", i) for i in range(d.shape[0])), d,
+                      np.isnan(d).sum(axis=1))
+    std = pg.prepare_genotype_batch(raw)
+    np.testing.assert_allclose(std.matrix, g["matrix"], atol=1e-12)
+    assert nan_eq(std.allele_frequency, g["af"])
+    assert np.array_equal(std.missing_count, g["missing"]) and np.array_equal(std.skip_reason, g["skip"])
+    s32 = pg.prepare_genotype_batch(raw, dtype=np.float32)
+    assert s32.matrix.dtype == np.float32
+
+
+def test_correlate_handworked_and_row_stable():
+    g, _, _ = pg.standardize_columns(np.array([0.0, 1.0, 2.0, 1.0])[:, None])
+    y, _, _ = pg.standardize_columns(np.array([0.0, 1.0, 1.0, 2.0])[:, None])
+    r, clamped = pg.correlate(g.T, y)
+    assert r[0, 0] == pytest.approx(0.5, abs=1e-15) and clamped == 0
+    rng = np.random.default_rng(21)
+    gt, _, _ = pg.standardize_columns(rng.standard_normal((100, 777)))
+    yt, _, _ = pg.standardize_columns(rng.standard_normal((100, 9)))
+    gt = np.ascontiguousarray(gt.T)
+    full, _ = pg.correlate(gt, yt)
+    ref, _ = orc.correlate(gt, yt)
+    np.testing.assert_allclose(full, ref, atol=1e-14)
+    for split in (1, 7, 64, 300, 777):
+        parts = np.vstack([pg.correlate(gt[s:s + split], yt)[0] for s in range(0, 777, split)])
+        assert np.array_equal(parts, full)
+    r, clamped = pg.correlate(np.array([[2.0, -2.0]]), np.array([[1.0], [-1.0]]))
+    assert r[0, 0] == 1.0 and clamped == 1
+    with pytest.raises(ValueError):
+        pg.correlate(np.zeros((2, 3)), np.zeros((4, 1)))
