@@ -1,0 +1,422 @@
+#!/usr/bin/env python
+"""Benchmark of the BASELINE.json metric: association tests/sec at N=23,000
+samples, P=20,480 phenotypes (config 3: synthetic PLINK .bed, M=1,000,000
+markers per GPU, THRESHOLD hit compaction at p <= 1e-4).
+
+  python bench.py [--gpus N --steps K --warmup W]             # this repo (B200 kernels)
+  python bench.py --impl reference [--steps K --warmup W]     # reference CPU path (oracle port)
+  torchrun --nproc-per-node N bench.py --gpus N ...            # one rank per GPU (weak scaling)
+
+A step scans the rank's whole marker shard (M markers) against the resident
+panel and returns the hits: value = (markers x phenotypes over all ranks) /
+(max over ranks of the device time of K steps). `e2e` times the same through
+the host-buffer C-ABI path (panel upload + NCCL broadcast + pinned .bed rows
+H2D inside the step). Data are synthetic of the paper's shape (random-init
+genotypes Binomial(2, AF), AF ~ U(0.05, 0.95); Gaussian phenotypes
+standardized like the reference panel). Inputs (5.75 GB packed genotypes,
+1.4 GB quantized panel) are far larger than the 126 MB L2.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "association tests/sec (N=23k, P=20,480) at 1/2/4/8 B200; % bf16 tensor peak"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--samples", type=int, default=23_000)
+    ap.add_argument("--markers", type=int, default=1_000_000, help="markers per GPU")
+    ap.add_argument("--phenotypes", type=int, default=20_480)
+    ap.add_argument("--p-threshold", type=float, default=1e-4)
+    ap.add_argument("--device-batch", type=int, default=65_536)
+    ap.add_argument("--cpu-sample", type=int, default=4096, help="markers in the timed CPU-baseline sample")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--seed", type=int, default=3)
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------- helpers
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def workload_config(a, world: int) -> dict:
+    return {
+        "workload": (f"C3: synthetic PLINK .bed N={a.samples:,} x M={a.markers:,} markers per GPU x "
+                     f"P={a.phenotypes:,} phenotypes, THRESHOLD p<={a.p_threshold:g} hit compaction"),
+        "n_samples": a.samples,
+        "n_markers_per_gpu": a.markers,
+        "n_phenotypes": a.phenotypes,
+        "p_threshold": a.p_threshold,
+        "device_batch_markers": a.device_batch,
+        "parallelism": f"marker shards x{world} (panel broadcast once over NCCL)",
+        "l2_policy": "inputs larger than L2 (5.75 GB packed genotypes + 1.4 GB panel limbs per GPU per step)",
+    }
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows: list[list[str]] = []
+        self._stop = threading.Event()
+        self._thr = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                for line in out.stdout.strip().splitlines():
+                    self.rows.append([x.strip() for x in line.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._thr.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._thr.join(timeout=10)
+
+    def summary(self) -> dict:
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_peaks() -> dict:
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {}
+
+
+# --------------------------------------------------------------------------- synthetic data (device, torch plumbing)
+def synth_packed(torch, n_markers: int, n_samples: int, pitch: int, seed: int, device):
+    """Packed .bed rows [M, pitch] uint8 on the device: G ~ Binomial(2, AF), AF ~ U(0.05, 0.95)."""
+    out = torch.zeros((n_markers, pitch), dtype=torch.uint8, device=device)
+    gen = torch.Generator(device=device).manual_seed(seed)
+    bpm = (n_samples + 3) // 4
+    lut = torch.tensor([3, 2, 0], dtype=torch.uint8, device=device)  # dosage 0,1,2 -> code 11,10,00
+    chunk = 8192
+    for s in range(0, n_markers, chunk):
+        e = min(n_markers, s + chunk)
+        af = torch.rand(e - s, 1, generator=gen, device=device) * 0.9 + 0.05
+        g = (torch.rand(e - s, n_samples, generator=gen, device=device) < af).to(torch.uint8)
+        g += (torch.rand(e - s, n_samples, generator=gen, device=device) < af).to(torch.uint8)
+        codes = lut[g.long()]
+        pad = bpm * 4 - n_samples
+        if pad:
+            codes = torch.nn.functional.pad(codes, (0, pad))
+        q = codes.view(e - s, bpm, 4)
+        out[s:e, :bpm] = q[:, :, 0] | (q[:, :, 1] << 2) | (q[:, :, 2] << 4) | (q[:, :, 3] << 6)
+    return out
+
+
+def synth_panel(torch, n_samples: int, n_pheno: int, seed: int, device):
+    """Standardized panel Y~ [N, P] f64: centred (intercept-only residualization), unit 1/N variance."""
+    gen = torch.Generator(device=device).manual_seed(seed + 1000)
+    y = torch.randn(n_samples, n_pheno, generator=gen, device=device, dtype=torch.float64)
+    y -= y.mean(dim=0, keepdim=True)
+    y /= torch.sqrt((y * y).mean(dim=0, keepdim=True))
+    return y
+
+
+def decode_host(packed: np.ndarray, n: int) -> np.ndarray:
+    from oracle.scan_oracle import decode_bed
+
+    return decode_bed(packed, n)
+
+
+# --------------------------------------------------------------------------- reference arm
+def cpu_threads() -> int:
+    try:
+        from threadpoolctl import threadpool_info
+
+        return max(int(i.get("num_threads", 1)) for i in threadpool_info()) or 1
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_cpu_sample(packed_rows: np.ndarray, ytil: np.ndarray, n: int, p_thr: float) -> tuple[float, int]:
+    """Oracle (numpy restatement of the reference path) on a bounded marker sample -> (seconds, hits)."""
+    from oracle import scan_oracle as orc
+
+    t0 = time.perf_counter()
+    dos = orc.decode_bed(packed_rows, n)
+    res = orc.threshold_scan(dos, ytil, float(n - 2), p_thr)
+    return time.perf_counter() - t0, int(res["rows"].size)
+
+
+def reference_arm(a) -> None:
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    rng = np.random.default_rng(a.seed)
+    n, p = a.samples, a.phenotypes
+    sample = max(16, min(a.cpu_sample, a.markers))
+    per_step = max(16, sample // 4)
+    y = rng.standard_normal((n, p))
+    y -= y.mean(axis=0)
+    y /= np.sqrt((y * y).mean(axis=0))
+    bpm = (n + 3) // 4
+    af = rng.uniform(0.05, 0.95, per_step)
+    g = rng.binomial(2, af[:, None], size=(per_step, n))
+    codes = np.array([3, 2, 0], dtype=np.uint8)[g]
+    codes = np.pad(codes, ((0, 0), (0, bpm * 4 - n))).reshape(per_step, bpm, 4)
+    packed = (codes[:, :, 0] | (codes[:, :, 1] << 2) | (codes[:, :, 2] << 4) | (codes[:, :, 3] << 6)).astype(np.uint8)
+    for _ in range(a.warmup):
+        run_cpu_sample(packed, y, n, a.p_threshold)
+    times = [run_cpu_sample(packed, y, n, a.p_threshold)[0] for _ in range(a.steps)]
+    total = sum(times)
+    value = a.steps * per_step * p / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tests/s", "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * total / a.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(a, world),
+        "cpu_baseline": {"value": value, "unit": "tests/s", "cores": cpu_threads(), "kind": "port",
+                         "sample": f"{per_step} markers x {n} samples x {p} phenotypes per step "
+                                   "(oracle/scan_oracle.py: decode + prepare + f64 tiled GEMM + premask + Lentz p)"},
+        "e2e": {"value": value, "unit": "tests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- our arm
+def our_arm(a) -> None:
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_21095_b200 import _native, build as _build
+    from paper_2604_21095_b200._device import DeviceContext
+    from paper_2604_21095_b200.engine import threshold_premask
+
+    world, rank, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    _build.build()  # no-op when the in-tree .so is current
+    n, p, m = a.samples, a.phenotypes, a.markers
+    bpm = (n + 3) // 4
+    pitch = (bpm + 15) // 16 * 16
+    df = float(n - 2)
+
+    ctx = DeviceContext(local)
+    gidx = np.arange(n, dtype=np.int64)
+    ytil = synth_panel(torch, n, p, a.seed, dev) if rank == 0 else None
+
+    def distribute_panel(from_host: np.ndarray | None):
+        """rank 0 uploads + quantizes; panel limbs broadcast once over NCCL; others import."""
+        if rank == 0:
+            if from_host is not None:
+                ctx.set_panel(from_host, gidx, n)
+            else:
+                ctx.set_panel_device(ytil.data_ptr(), n, p, p, gidx, n)
+        if world > 1:
+            nbytes = ctx.panel_bytes() if rank == 0 else 0
+            nb = torch.tensor([nbytes], device=dev, dtype=torch.int64)
+            dist.broadcast(nb, 0)
+            buf = torch.empty(int(nb.item()), dtype=torch.uint8, device=dev)
+            if rank == 0:
+                ctx.export_panel(buf.data_ptr())
+            dist.broadcast(buf, 0)
+            if rank != 0:
+                ctx.import_panel(buf.data_ptr(), n, p, gidx, n)
+            return int(nb.item())
+        return 0
+
+    distribute_panel(None)
+    rbar = np.full(p, threshold_premask(a.p_threshold, df))
+    ctx.set_scan(df, _native.PG_MODE_THRESHOLD, rbar)
+    packed = synth_packed(torch, m, n, pitch, a.seed * 7919 + rank, dev)
+    torch.cuda.synchronize()
+    stream = torch.cuda.ExternalStream(ctx.stream_handle(), device=dev)
+    batches = [(s, min(a.device_batch, m - s)) for s in range(0, m, a.device_batch)]
+
+    def scan_step_device():
+        stats = {"gemm_ms": 0.0, "hits": 0, "launches": 0, "d2h": 0}
+        for s, c in batches:
+            r = ctx.scan_device(_native.PG_GENO_BED, packed.data_ptr() + s * pitch, c, bpm, pitch)
+            stats["gemm_ms"] += r.gemm_ms
+            stats["hits"] += int(np.count_nonzero(r.cand_p <= a.p_threshold))
+            stats["launches"] += r.launches
+            stats["d2h"] += r.cand_rows.size * 40 + c * 25
+        return stats
+
+    def timed(fn, steps):
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        out = [fn() for _ in range(steps)]
+        ev1.record(stream)
+        ev1.synchronize()
+        torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1)
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+            dist.barrier()
+        return ms, out
+
+    for _ in range(a.warmup):
+        scan_step_device()
+    with ClockSampler(local) as clk:
+        ms, outs = timed(scan_step_device, a.steps)
+    tests_per_step = m * p
+    value = world * tests_per_step * a.steps / (ms / 1e3)
+    gemm_ms = sum(o["gemm_ms"] for o in outs)
+    launches = sum(o["launches"] for o in outs)
+    hits = outs[-1]["hits"]
+
+    # roofline of the dominant kernel (assoc_i8_kernel): BASELINE accounting 2*N*M*P x2 (hi/lo) = 4*N*M*P
+    flops = 4.0 * n * m * p * a.steps
+    achieved = flops / (gemm_ms / 1e3) / 1e12
+    peaks = measured_peaks()
+    peak = float(peaks.get("bf16_tflops", 1590.0))
+    peak_sus = float(peaks.get("bf16_tflops_sustained", 1400.0))
+    traffic = None
+    tf = ROOT / "profiles" / "assoc_traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    # hardware view: the kernel issues 3 int8 MMAs (limbs) per padded sample, exact int32 accumulation
+    k_pad = (n + 63) // 64 * 64
+    int8_ops = 2.0 * 3 * k_pad * m * ((p + 127) // 128 * 128) * a.steps
+    int8_achieved = int8_ops / (gemm_ms / 1e3) / 1e12
+    int8_peak = None
+    try:
+        A = torch.randint(-128, 127, (8192, 8192), device=dev, dtype=torch.int8)
+        B = torch.randint(-128, 127, (8192, 8192), device=dev, dtype=torch.int8)
+        best = 1e9
+        for _ in range(4):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch._int_mm(A, B.t())
+            e1.record()
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        int8_peak = 2 * 8192**3 / (best / 1e3) / 1e12
+        del A, B
+    except Exception:
+        pass
+
+    # ------------------------------------------------ end to end through the host-buffer C ABI
+    e2e = None
+    if not a.no_e2e:
+        host_rows = torch.empty((m, bpm), dtype=torch.uint8, pin_memory=True)
+        host_rows.copy_(packed[:, :bpm])
+        host_np = host_rows.numpy()
+        y_host = None
+        if rank == 0:
+            yh = torch.empty((n, p), dtype=torch.float64, pin_memory=True)
+            yh.copy_(ytil)
+            y_host = yh.numpy()
+        del packed
+        torch.cuda.empty_cache()
+
+        def e2e_step():
+            h2d = distribute_panel(y_host) + (n * p * 8 if rank == 0 else 0)
+            ctx.set_scan(df, _native.PG_MODE_THRESHOLD, rbar)
+            d2h = 0
+            for s, c in batches:
+                r = ctx.scan(_native.PG_GENO_BED, host_np[s:s + c], bpm)
+                d2h += r.cand_rows.size * 40 + c * 25
+                h2d += c * bpm
+            return h2d, d2h
+
+        e2e_step()
+        ms_e2e, outs_e2e = timed(e2e_step, a.steps)
+        e2e = {"value": world * tests_per_step * a.steps / (ms_e2e / 1e3), "unit": "tests/s",
+               "h2d_bytes_per_step": int(outs_e2e[-1][0]), "d2h_bytes_per_step": int(outs_e2e[-1][1]),
+               "ms_per_step": ms_e2e / a.steps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        sample = max(16, min(a.cpu_sample, m))
+        rows_np = synth_packed(torch, sample, n, pitch, a.seed * 7919 + 17, dev)[:, :bpm].cpu().numpy()
+        y_np = ytil.cpu().numpy()
+        sec, _ = run_cpu_sample(rows_np, y_np, n, a.p_threshold)
+        cpu = {"value": sample * p / sec, "unit": "tests/s", "cores": cpu_threads(), "kind": "port",
+               "sample": f"{sample} markers x {n} samples x {p} phenotypes, one pass of oracle/scan_oracle.py "
+                         f"(numpy restatement of the reference path) in {sec:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "tests/s", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int8 (exact int32 accumulate; fp64 epilogue)", "data": "synthetic",
+            "config": workload_config(a, world),
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "frac_of_sustained": achieved / peak_sus, "traffic": traffic,
+                         "kernel": "assoc_i8_kernel",
+                         "flops_def": "BASELINE: 2*N*M*P x2 (hi/lo) = 4*N*M*P per launch, N = kept samples",
+                         "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)"},
+            "hw_int8": {"achieved_tops": int8_achieved, "cublas_int8_tops_measured": int8_peak,
+                        "frac": (int8_achieved / int8_peak) if int8_peak else None,
+                        "ops_def": "2 * 3 limbs * K_pad * M * P_pad per launch"},
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "gpu_launches": launches,
+            "hits_per_step": hits,
+            "gemm_ms_per_step": gemm_ms / a.steps,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    a = parse_args()
+    if a.impl == "reference":
+        reference_arm(a)
+    else:
+        our_arm(a)
+
+
+if __name__ == "__main__":
+    main()

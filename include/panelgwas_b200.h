@@ -68,6 +68,8 @@ PG_API int pg_ctx_create(int device, pg_ctx** out);
 PG_API int pg_ctx_destroy(pg_ctx* ctx);
 /* Synchronise the ctx stream (used before timing / teardown). */
 PG_API int pg_ctx_sync(pg_ctx* ctx);
+/* The ctx's cudaStream_t (as void*), for callers that time or order work on it. */
+PG_API int pg_ctx_stream(pg_ctx* ctx, void** stream);
 
 /* Upload the standardized phenotype panel once; it stays resident in HBM as
  * fp16 hi/lo planes [P_pad, K_pad] plus fp64 column sums.
@@ -106,7 +108,9 @@ typedef struct pg_batch_info {
   int64_t n_skipped_monomorphic;
   int64_t n_skipped_all_missing;
   double gemm_ms;       /* device time of the association kernel(s) */
-  double decode_ms;     /* device time of the decode kernel */
+  double decode_ms;     /* device time of the decode kernels */
+  int64_t launches;     /* kernels of this library launched for the batch */
+  int64_t rows_per_marker; /* GEMM rows per marker (1: PLINK, 2: + missing calls, 8/16: BGEN / real dosages) */
 } pg_batch_info;
 
 /* Scan one block of markers from HOST memory.

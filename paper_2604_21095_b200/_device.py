@@ -49,6 +49,9 @@ class ScanResult:
     t_rows: np.ndarray | None = None
     decode_ms: float = 0.0
     gemm_ms: float = 0.0
+    launches: int = 0
+    rows_per_marker: int = 1
+    n_candidates: int = 0
 
 
 class DeviceContext:
@@ -84,6 +87,12 @@ class DeviceContext:
 
     def sync(self) -> None:
         call("pg_ctx_sync", self._h)
+
+    def stream_handle(self) -> int:
+        """cudaStream_t of this ctx (for CUDA-event timing on the launching stream)."""
+        out = c_void_p()
+        call("pg_ctx_stream", self._h, byref(out))
+        return int(out.value or 0)
 
     # ------------------------------------------------------------ panel
     def set_panel(self, ytil: np.ndarray, geno_row_index: np.ndarray, n_samples_src: int) -> None:
@@ -152,10 +161,10 @@ class DeviceContext:
             n_markers=m,
             af=np.empty(m), missing_count=np.empty(m, np.int64), variance=np.empty(m),
             skip=np.empty(m, np.int8), clamp_count=int(info.clamp_count),
-            decode_ms=float(info.decode_ms), gemm_ms=float(info.gemm_ms),
+            decode_ms=float(info.decode_ms), gemm_ms=float(info.gemm_ms), launches=int(info.launches),
+            rows_per_marker=int(info.rows_per_marker), n_candidates=int(info.n_candidates),
         )
         if not fetch:
-            res.n_candidates = int(info.n_candidates)  # type: ignore[attr-defined]
             return res
         call("pg_fetch_marker_stats", self._h, ptr(res.af), ptr(res.missing_count), ptr(res.variance),
              ptr(res.skip))

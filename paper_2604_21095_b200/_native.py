@@ -45,6 +45,8 @@ class BatchInfo(ctypes.Structure):
         ("n_skipped_all_missing", c_int64),
         ("gemm_ms", c_double),
         ("decode_ms", c_double),
+        ("launches", c_int64),
+        ("rows_per_marker", c_int64),
     ]
 
 
@@ -57,6 +59,7 @@ SIGNATURES: dict[str, list] = {
     "pg_ctx_create": [c_int, _P],
     "pg_ctx_destroy": [_P],
     "pg_ctx_sync": [_P],
+    "pg_ctx_stream": [_P, _P],
     "pg_ctx_set_panel": [_P, _P, c_int64, c_int64, c_int64, _P, c_int64],
     "pg_ctx_set_panel_device": [_P, _P, c_int64, c_int64, c_int64, _P, c_int64],
     "pg_ctx_panel_bytes": [_P, _P],

@@ -270,12 +270,15 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
   PG_CHECK_STATUS(c->v.ensure(static_cast<size_t>(c_pad) * c->k_pad));
   PG_CHECK_STATUS(c->v127.ensure(static_cast<size_t>(c_pad) * c->k_pad));
   PG_CHECK_STATUS(geno_planes(b, R, c->v.p, c->v127.p, c_pad, c->k_pad, s));
-  PG_CUDA_CHECK(cudaEventRecord(c->ev[1], s));
+  int64_t launches = (kind == PG_GENO_DENSE_F64 ? 3 : 2);
+  float decode_ms = 0.f;
 
   PG_CHECK_STATUS(c->counters.ensure(4));
   PG_CUDA_CHECK(cudaMemsetAsync(c->counters.p, 0, sizeof(unsigned long long) * 4, s));
   count_skip_kernel<<<64, 256, 0, s>>>(c->skip.p, m, c->counters.p + 1);
   PG_CUDA_CHECK(cudaGetLastError());
+  ++launches;
+  PG_CUDA_CHECK(cudaEventRecord(c->ev[1], s));
 
   AssocEpilogue ep{};
   ep.rows_per_marker = R;
@@ -300,7 +303,10 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
     ep.rbar = nullptr;
     ep.cand_cap = 0;
     PG_CUDA_CHECK(cudaMemsetAsync(c->cand_count.p, 0, sizeof(int), s));
+    PG_CUDA_CHECK(cudaEventRecord(c->ev[1], s));
     PG_CHECK_STATUS(launch_assoc(c->qh.p, c->q1.p, c->q0.p, c->p_pad, c->v.p, c->v127.p, c_pad, c->k_pad, ep, s));
+    PG_CUDA_CHECK(cudaEventRecord(c->ev[2], s));
+    ++launches;
   } else {
     ep.rbar = c->rbar.p;
     for (int attempt = 0; attempt < 2; ++attempt) {
@@ -313,7 +319,10 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
       ep.cand_r = c->cand_r.p;
       ep.cand_cap = c->cand_capacity;
       PG_CUDA_CHECK(cudaMemsetAsync(c->cand_count.p, 0, sizeof(int), s));
+      PG_CUDA_CHECK(cudaEventRecord(c->ev[1], s));
       PG_CHECK_STATUS(launch_assoc(c->qh.p, c->q1.p, c->q0.p, c->p_pad, c->v.p, c->v127.p, c_pad, c->k_pad, ep, s));
+      PG_CUDA_CHECK(cudaEventRecord(c->ev[2], s));
+      ++launches;
       int hcount = 0;
       PG_CUDA_CHECK(cudaMemcpyAsync(&hcount, c->cand_count.p, sizeof(int), cudaMemcpyDeviceToHost, s));
       PG_CUDA_CHECK(cudaStreamSynchronize(s));
@@ -329,7 +338,6 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
       }
     }
   }
-  PG_CUDA_CHECK(cudaEventRecord(c->ev[2], s));
 
   if (ncand > 0) {
     PG_CHECK_STATUS(c->cand_key_sorted.ensure(ncand));
@@ -349,6 +357,7 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
     PG_CHECK_STATUS(finalize_candidates(c->cand_key_sorted.p, c->cand_r_sorted.p, ncand, c->df, c->cand_rows.p,
                                         c->cand_cols.p, c->cand_r_sorted.p, c->cand_t.p, c->cand_p.p, c->counters.p,
                                         s));
+    ++launches;
   }
   PG_CUDA_CHECK(cudaEventRecord(c->ev[3], s));
   unsigned long long hc[4] = {0, 0, 0, 0};
@@ -365,9 +374,11 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
     info->n_skipped_all_missing = static_cast<int64_t>(hc[2]);
     float ms = 0.f;
     cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
-    info->decode_ms = ms;
+    info->decode_ms = ms + decode_ms;
     cudaEventElapsedTime(&ms, c->ev[1], c->ev[2]);
     info->gemm_ms = ms;
+    info->launches = launches;
+    info->rows_per_marker = R;
   }
   return PG_OK;
 }
@@ -428,6 +439,13 @@ int pg_ctx_destroy(pg_ctx* c) {
     if (e) cudaEventDestroy(e);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
+  return PG_OK;
+}
+
+int pg_ctx_stream(pg_ctx* c, void** stream) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(stream != nullptr, PG_ERR_INVALID, "null out");
+  *stream = reinterpret_cast<void*>(c->stream);
   return PG_OK;
 }
 
