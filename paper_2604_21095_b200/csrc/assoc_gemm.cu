@@ -35,7 +35,8 @@ constexpr int kQBytes = kTileP * kTileK;  // 8 KB per panel limb tile
 constexpr int kVBytes = kTileC * kTileK;  // 16 KB per genotype plane tile
 constexpr int kStageBytes = 3 * kQBytes + 2 * kVBytes;
 constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
-constexpr int kThreads = 256;
+constexpr int kEpiWarps = 16;  // 4 lane quarters x 4 column groups of 64
+constexpr int kThreads = 128 + 32 * kEpiWarps;
 constexpr int kTmemCols = 512;
 constexpr int kGroupC = 8;  // genotype tiles per raster group (panel tiles reused through L2)
 
@@ -50,7 +51,7 @@ __device__ __forceinline__ void tile_coords(int t, int n_ctile, int n_ptile, int
 
 template <int R>
 __device__ __forceinline__ void epilogue_tile(const AssocEpilogue& ep, uint32_t tH, uint32_t tL, int ct, int pheno,
-                                              int lane) {
+                                              int lane, int c_begin, int c_end) {
   constexpr int kMarkersPerTile = kTileC / R;
   const uint32_t lanemask_lt = (1u << lane) - 1u;
   const float sc_f = ep.scale_f[pheno];
@@ -60,7 +61,7 @@ __device__ __forceinline__ void epilogue_tile(const AssocEpilogue& ep, uint32_t 
   const float rb = ep.rbar ? ep.rbar[pheno] : INFINITY;
   float mx = 0.f;
 #pragma unroll 1
-  for (int c = 0; c < kTileC; c += 16) {
+  for (int c = c_begin; c < c_end; c += 16) {
     uint32_t h[16], l[16];
     tmem_ld_32x32b_x16(tH + c, h);
     tmem_ld_32x32b_x16(tL + c, l);
@@ -142,7 +143,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(tfull, 1);
-    mbar_init(tempty, 4);
+    mbar_init(tempty, kEpiWarps);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, kTmemCols);
@@ -154,6 +155,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------------------ TMA producer
+      // panel tiles are shared by the kGroupC concurrent CTAs of a raster group -> keep them in L2
       const uint64_t pol_keep = l2_policy_evict_last();
       uint32_t s = 0, ph = 0;
       for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
@@ -216,21 +218,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue
-    const int ew = warp - 4;  // == warp % 4 -> TMEM lanes [32*ew, 32*ew+32)
+    // warp w reads TMEM lanes [32*(w%4), +32) (hardware lane-quarter rule) and
+    // columns [64*cg, +64) of the tile, cg = (w-4)/4: 16 warps drain TMEM 4x faster
+    const int quarter = warp & 3;
+    const int cg = (warp - 4) >> 2;
     uint32_t aph = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
       int ct, pt;
       tile_coords(t, n_ctile, n_ptile, ct, pt);
-      const int pheno = pt * kTileP + ew * 32 + lane;
+      const int pheno = pt * kTileP + quarter * 32 + lane;
       mbar_wait(tfull, aph);
       tc_fence_after();
-      const uint32_t tH = tmem_base + (static_cast<uint32_t>(ew * 32) << 16);
+      const uint32_t tH = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16);
       const uint32_t tL = tH + kTileC;
+      const int c0 = cg * (kTileC / 4), c1 = c0 + kTileC / 4;
       switch (ep.rows_per_marker) {
-        case 1: epilogue_tile<1>(ep, tH, tL, ct, pheno, lane); break;
-        case 2: epilogue_tile<2>(ep, tH, tL, ct, pheno, lane); break;
-        case 8: epilogue_tile<8>(ep, tH, tL, ct, pheno, lane); break;
-        default: epilogue_tile<16>(ep, tH, tL, ct, pheno, lane); break;
+        case 1: epilogue_tile<1>(ep, tH, tL, ct, pheno, lane, c0, c1); break;
+        case 2: epilogue_tile<2>(ep, tH, tL, ct, pheno, lane, c0, c1); break;
+        case 8: epilogue_tile<8>(ep, tH, tL, ct, pheno, lane, c0, c1); break;
+        default: epilogue_tile<16>(ep, tH, tL, ct, pheno, lane, c0, c1); break;
       }
       tc_fence_before();
       __syncwarp();

@@ -134,6 +134,41 @@ __global__ void integral_kernel(GenoBlock b, int* flags) {
   if (__syncthreads_or(nonint) && threadIdx.x == 0) atomicOr(flags + 1, 1);
 }
 
+// spread 16 keep bits onto the even bit positions of a 32-bit word (one per 2-bit code)
+__device__ __forceinline__ uint32_t spread16(uint32_t x) {
+  x = (x | (x << 8)) & 0x00FF00FFu;
+  x = (x | (x << 4)) & 0x0F0F0F0Fu;
+  x = (x | (x << 2)) & 0x33333333u;
+  x = (x | (x << 1)) & 0x55555555u;
+  return x;
+}
+
+// PLINK rows: counts straight from bit planes, 64 samples per lane-step (uint4 loads).
+__device__ __forceinline__ void bed_counts(const GenoBlock& b, int64_t m, int lane, long long& nmiss, long long& su,
+                                           long long& ssu) {
+  const uint8_t* row = b.data + m * b.pitch;
+  const int64_t n_vec = b.pitch / 16;  // pitch is a multiple of 16 bytes
+  long long n2 = 0, n0 = 0, nm = 0;
+  for (int64_t vi = lane; vi < n_vec; vi += 32) {
+    const uint4 w4 = *reinterpret_cast<const uint4*>(row + vi * 16);
+    const uint32_t ws[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t ci = vi * 4 + q;  // 16-sample chunk index
+      if (ci * 16 >= b.n_src) break;
+      const uint32_t km = spread16(keep16(b.keep_bits, ci));
+      const uint32_t w = ws[q];
+      const uint32_t lo = w & 0x55555555u, hi = (w >> 1) & 0x55555555u;
+      nm += __popc(lo & ~hi & km);
+      n2 += __popc(~lo & ~hi & km);
+      n0 += __popc(lo & hi & km);
+    }
+  }
+  nmiss = nm;
+  su = n2 - n0;
+  ssu = n2 + n0;
+}
+
 template <int KIND>
 __global__ void stats_kernel(GenoBlock b, MarkerStats st, int64_t m_pad, double unit_scale) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -152,15 +187,19 @@ __global__ void stats_kernel(GenoBlock b, MarkerStats st, int64_t m_pad, double 
   long long nmiss = 0, su = 0, ssu = 0;
   double dsum = 0.0;
   bool nonint = false;
-  for (int64_t ci = lane; ci < n_chunks; ci += 32) {
-    int u[kChunk];
-    uint32_t miss, obs;
-    load16<KIND>(b, m, ci, u, miss, obs, dsum, nonint);
-    nmiss += __popc(miss);
+  if constexpr (KIND == PG_GENO_BED) {
+    bed_counts(b, m, lane, nmiss, su, ssu);
+  } else {
+    for (int64_t ci = lane; ci < n_chunks; ci += 32) {
+      int u[kChunk];
+      uint32_t miss, obs;
+      load16<KIND>(b, m, ci, u, miss, obs, dsum, nonint);
+      nmiss += __popc(miss);
 #pragma unroll
-    for (int i = 0; i < kChunk; ++i) {
-      su += u[i];
-      ssu += static_cast<long long>(u[i]) * u[i];
+      for (int i = 0; i < kChunk; ++i) {
+        su += u[i];
+        ssu += static_cast<long long>(u[i]) * u[i];
+      }
     }
   }
 #pragma unroll
