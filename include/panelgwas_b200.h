@@ -100,6 +100,10 @@ PG_API int pg_ctx_set_scan(pg_ctx* ctx, double df, int mode, const double* r_bar
  * tightening, engine.py:205-211 / output.py:199-200). */
 PG_API int pg_ctx_set_rbar(pg_ctx* ctx, const double* r_bar);
 
+/* Tuning switch: decode PLINK rows inside the GEMM producer (default 1) or through
+ * materialized int8 planes (0). Results are identical; exposed for A/B measurement. */
+PG_API int pg_ctx_set_fused_decode(pg_ctx* ctx, int enable);
+
 /* Result summary of the last scan call. */
 typedef struct pg_batch_info {
   int64_t n_markers;

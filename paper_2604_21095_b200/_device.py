@@ -131,6 +131,9 @@ class DeviceContext:
             call("pg_ctx_set_scan", self._h, float(df), int(mode), ptr(rb))
             self.mode = mode
 
+    def set_fused_decode(self, enable: bool) -> None:
+        call("pg_ctx_set_fused_decode", self._h, 1 if enable else 0)
+
     def set_rbar(self, r_bar: np.ndarray) -> None:
         rb = np.ascontiguousarray(r_bar, dtype=np.float64)
         with self.lock:

@@ -50,4 +50,10 @@ struct AssocEpilogue {
 int launch_assoc(const int8_t* qh, const int8_t* q1, const int8_t* q0, int64_t p_pad, const int8_t* v,
                  const int8_t* v127, int64_t c_pad, int64_t k_pad, const AssocEpilogue& ep, cudaStream_t stream);
 
+// Fused-decode variant: genotype operand decoded in shared memory from packed
+// 2-bit .bed rows (`pitch` bytes apart, >= k_pad/4 bytes of codes); rows_per_marker 1.
+int launch_assoc_packed(const int8_t* qh, const int8_t* q1, const int8_t* q0, int64_t p_pad, const uint8_t* packed,
+                        int64_t pitch, int64_t n_markers, int64_t k_pad, const AssocEpilogue& ep,
+                        cudaStream_t stream);
+
 }  // namespace pg

@@ -11,15 +11,22 @@
 //
 //   r[m,p] = s_p * (X[m,p] - mu_m * (Cq_p - Mq[m,p])) / sqrt(N * V_m)
 //
-// with X = sum_k u q, Mq = sum over missing calls of q (only when the batch
-// has missing calls; rows_per_marker == 2), mu_m / V_m the mean / centred
-// sum of squares of u over observed kept samples.
+// with X = sum_k u q, Mq = sum over missing calls of q (rows_per_marker >= 2),
+// mu_m / V_m the mean / centred sum of squares of u over observed kept samples
+// (SURVEY.md appendix 3).
 //
-// Structure: persistent, warp-specialised, 1 CTA per SM, 256 threads.
-//   warp 0 lane 0 : TMA producer (4-stage smem ring, 56 KB per stage)
+// Two operand paths for the genotype side (template FUSED):
+//   planes : TMA loads pre-decoded int8 planes v / 127v (any rows_per_marker)
+//   fused  : TMA loads the packed 2-bit .bed tile (256 rows x 16 B per stage) and
+//            4 decoder warps expand it in shared memory into the swizzled v / 127v
+//            operand tiles (PLINK rows without missing calls: rows_per_marker 1).
+//
+// Structure: persistent, warp-specialised, 1 CTA per SM, 768 threads.
+//   warp 0 lane 0 : TMA producer
 //   warp 1 lane 0 : tcgen05.mma (kind::i8) issuer; 3 MMAs per 32 samples
 //   warp 2        : TMEM allocator (512 columns: accH | accL, 128 lanes x 256)
-//   warps 4..7    : epilogue (tcgen05.ld -> X -> r -> premask / compaction / FULL)
+//   warps 4..7    : decoders (fused path)
+//   warps 8..23   : epilogue, 4 lane quarters x 4 column groups
 #include <cuda.h>
 
 #include <cmath>
@@ -30,15 +37,25 @@
 namespace pg {
 namespace {
 
-constexpr int kStages = 4;
 constexpr int kQBytes = kTileP * kTileK;  // 8 KB per panel limb tile
 constexpr int kVBytes = kTileC * kTileK;  // 16 KB per genotype plane tile
-constexpr int kStageBytes = 3 * kQBytes + 2 * kVBytes;
-constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
-constexpr int kEpiWarps = 16;  // 4 lane quarters x 4 column groups of 64
-constexpr int kThreads = 128 + 32 * kEpiWarps;
+constexpr int kPackedBytes = kTileC * (kTileK / 4);  // 4 KB packed .bed tile
+constexpr int kOffV = 3 * kQBytes;
+constexpr int kOffV127 = kOffV + kVBytes;
+constexpr int kOffPacked = kOffV127 + kVBytes;
+constexpr int kEpiWarps = 16;
+constexpr int kFirstEpiWarp = 8;
+constexpr int kThreads = 32 * (kFirstEpiWarp + kEpiWarps);
 constexpr int kTmemCols = 512;
-constexpr int kGroupC = 8;  // genotype tiles per raster group (panel tiles reused through L2)
+constexpr int kGroupC = 8;  // genotype tiles per raster group
+
+template <bool FUSED>
+struct Cfg {
+  static constexpr int kStages = FUSED ? 3 : 4;
+  static constexpr int kStageBytes = FUSED ? kOffPacked + kPackedBytes : kOffPacked;
+  static constexpr int kTmaBytes = FUSED ? 3 * kQBytes + kPackedBytes : kOffPacked;
+  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+};
 
 __device__ __forceinline__ void tile_coords(int t, int n_ctile, int n_ptile, int& ct, int& pt) {
   const int group = t / (kGroupC * n_ptile);
@@ -47,6 +64,35 @@ __device__ __forceinline__ void tile_coords(int t, int n_ctile, int n_ptile, int
   const int r = t - group * kGroupC * n_ptile;
   ct = first + r % gsz;
   pt = r / gsz;
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// 16 packed 2-bit codes (one 32-bit .bed word, low pair first) -> 16 int8 u values
+// (u[0..3]) and their x127 copies (u127[0..3]).  Code 00 -> +1 (two copies of
+// allele1), 10 -> 0, 11 -> -1, 01 (missing) -> 0.  Each code is moved to its own
+// nibble (3 shift/mask steps) and used as a PRMT byte selector into a 4-entry
+// table held in one register: ~1.4 instructions per sample.
+__device__ __forceinline__ uint32_t codes_to_nibbles(uint32_t x16) {
+  uint32_t x = x16 & 0xFFFFu;
+  x = (x | (x << 8)) & 0x00FF00FFu;
+  x = (x | (x << 4)) & 0x0F0F0F0Fu;
+  x = (x | (x << 2)) & 0x33333333u;
+  return x;
+}
+__device__ __forceinline__ void decode_word(uint32_t w, uint32_t (&u)[4], uint32_t (&u127)[4]) {
+  constexpr uint32_t kLutU = 0xFF000001u;     // bytes for codes 0,1,2,3: +1, 0, 0, -1
+  constexpr uint32_t kLutU127 = 0x8100007Fu;  // +127, 0, 0, -127
+  const uint32_t n_lo = codes_to_nibbles(w);
+  const uint32_t n_hi = codes_to_nibbles(w >> 16);
+  const uint32_t sel[4] = {n_lo & 0xFFFFu, n_lo >> 16, n_hi & 0xFFFFu, n_hi >> 16};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    u[i] = __byte_perm(kLutU, 0u, sel[i]);
+    u127[i] = __byte_perm(kLutU127, 0u, sel[i]);
+  }
 }
 
 template <int R>
@@ -113,16 +159,19 @@ __device__ __forceinline__ void epilogue_tile(const AssocEpilogue& ep, uint32_t 
   if (ep.max_abs_r && pheno < ep.p_valid) atomicMax(ep.max_abs_r + pheno, __float_as_uint(mx));
 }
 
+template <bool FUSED>
 __global__ void __launch_bounds__(kThreads, 1)
     assoc_i8_kernel(const __grid_constant__ CUtensorMap tm_qh, const __grid_constant__ CUtensorMap tm_q1,
                     const __grid_constant__ CUtensorMap tm_q0, const __grid_constant__ CUtensorMap tm_v,
                     const __grid_constant__ CUtensorMap tm_v127, int n_ctile, int n_ptile, int n_kb,
                     AssocEpilogue ep) {
+  using C = Cfg<FUSED>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
-  uint64_t* empty = full + kStages;
-  uint64_t* tfull = empty + kStages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* dec = empty + C::kStages;
+  uint64_t* tfull = dec + C::kStages;
   uint64_t* tempty = tfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
 
@@ -135,12 +184,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tm_q1);
     tma_prefetch_desc(&tm_q0);
     tma_prefetch_desc(&tm_v);
-    tma_prefetch_desc(&tm_v127);
+    if (!FUSED) tma_prefetch_desc(&tm_v127);
   }
   if (warp == 1 && lane == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
+      mbar_init(&dec[s], 4);
     }
     mbar_init(tfull, 1);
     mbar_init(tempty, kEpiWarps);
@@ -163,15 +213,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         tile_coords(t, n_ctile, n_ptile, ct, pt);
         for (int kb = 0; kb < n_kb; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
-          uint8_t* st = smem + s * kStageBytes;
+          uint8_t* st = smem + s * C::kStageBytes;
           const int kx = kb * kTileK;
-          mbar_arrive_expect_tx(&full[s], kStageBytes);
+          mbar_arrive_expect_tx(&full[s], C::kTmaBytes);
           tma_load_2d_hint(st, &tm_qh, &full[s], kx, pt * kTileP, pol_keep);
           tma_load_2d_hint(st + kQBytes, &tm_q1, &full[s], kx, pt * kTileP, pol_keep);
           tma_load_2d_hint(st + 2 * kQBytes, &tm_q0, &full[s], kx, pt * kTileP, pol_keep);
-          tma_load_2d(st + 3 * kQBytes, &tm_v, &full[s], kx, ct * kTileC);
-          tma_load_2d(st + 3 * kQBytes + kVBytes, &tm_v127, &full[s], kx, ct * kTileC);
-          if (++s == kStages) {
+          if constexpr (FUSED) {
+            tma_load_2d(st + kOffPacked, &tm_v, &full[s], kb * (kTileK / 4), ct * kTileC);
+          } else {
+            tma_load_2d(st + kOffV, &tm_v, &full[s], kx, ct * kTileC);
+            tma_load_2d(st + kOffV127, &tm_v127, &full[s], kx, ct * kTileC);
+          }
+          if (++s == C::kStages) {
             s = 0;
             ph ^= 1;
           }
@@ -191,13 +245,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t acc = 0;
         for (int kb = 0; kb < n_kb; ++kb) {
           mbar_wait(&full[s], ph);
+          if constexpr (FUSED) mbar_wait(&dec[s], ph);
           tc_fence_after();
-          const uint32_t st = smem_u32(smem + s * kStageBytes);
+          const uint32_t st = smem_u32(smem + s * C::kStageBytes);
           const uint64_t d_qh = umma_desc_sw64(st);
           const uint64_t d_q1 = umma_desc_sw64(st + kQBytes);
           const uint64_t d_q0 = umma_desc_sw64(st + 2 * kQBytes);
-          const uint64_t d_v = umma_desc_sw64(st + 3 * kQBytes);
-          const uint64_t d_v127 = umma_desc_sw64(st + 3 * kQBytes + kVBytes);
+          const uint64_t d_v = umma_desc_sw64(st + kOffV);
+          const uint64_t d_v127 = umma_desc_sw64(st + kOffV127);
 #pragma unroll
           for (int k = 0; k < kTileK / 32; ++k) {
             // +32 bytes along K inside the 64-byte swizzle row == +2 in the >>4 address field
@@ -207,7 +262,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             acc = 1;
           }
           mma_commit(&empty[s]);
-          if (++s == kStages) {
+          if (++s == C::kStages) {
             s = 0;
             ph ^= 1;
           }
@@ -216,12 +271,50 @@ __global__ void __launch_bounds__(kThreads, 1)
         aph ^= 1;
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp >= 4 && warp < kFirstEpiWarp) {
+    if constexpr (FUSED) {
+      // ------------------------------------------------------------ decoders
+      // thread dt expands rows dt and dt+128 of the packed tile: 16 bytes = 64 samples
+      // -> 64 B of v and 64 B of 127v, written as 4 swizzled 16-byte chunks each
+      // (SW64: chunk c of row r lives at r*64 + ((c ^ ((r >> 1) & 3)) << 4)).
+      const int dt = threadIdx.x - 128;
+      uint32_t s = 0, ph = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        for (int kb = 0; kb < n_kb; ++kb) {
+          mbar_wait(&full[s], ph);
+          uint8_t* st = smem + s * C::kStageBytes;
+          const uint4* pk = reinterpret_cast<const uint4*>(st + kOffPacked);
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            const int r = dt + 128 * half;
+            const uint4 w = pk[r];
+            const uint32_t words[4] = {w.x, w.y, w.z, w.w};
+            const uint32_t sw = (static_cast<uint32_t>(r) >> 1) & 3u;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              uint32_t u[4], u7[4];
+              decode_word(words[c], u, u7);
+              const uint32_t off = r * 64 + ((c ^ sw) << 4);
+              *reinterpret_cast<uint4*>(st + kOffV + off) = make_uint4(u[0], u[1], u[2], u[3]);
+              *reinterpret_cast<uint4*>(st + kOffV127 + off) = make_uint4(u7[0], u7[1], u7[2], u7[3]);
+            }
+          }
+          fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the tensor core
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&dec[s]);
+          if (++s == C::kStages) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp >= kFirstEpiWarp) {
     // -------------------------------------------------------------- epilogue
     // warp w reads TMEM lanes [32*(w%4), +32) (hardware lane-quarter rule) and
-    // columns [64*cg, +64) of the tile, cg = (w-4)/4: 16 warps drain TMEM 4x faster
+    // columns [64*cg, +64) of the tile: 16 warps drain the 2 x 256 columns 4x faster
     const int quarter = warp & 3;
-    const int cg = (warp - 4) >> 2;
+    const int cg = (warp - kFirstEpiWarp) >> 2;
     uint32_t aph = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
       int ct, pt;
@@ -251,6 +344,34 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) tmem_free(tmem_base, kTmemCols);
 }
 
+template <bool FUSED>
+int launch_common(const CUtensorMap& tm_qh, const CUtensorMap& tm_q1, const CUtensorMap& tm_q0,
+                  const CUtensorMap& tm_v, const CUtensorMap& tm_v127, int64_t p_pad, int64_t c_pad, int64_t k_pad,
+                  const AssocEpilogue& ep, cudaStream_t stream) {
+  PG_CUDA_CHECK(cudaFuncSetAttribute(assoc_i8_kernel<FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     Cfg<FUSED>::kSmemBytes));
+  int dev = 0, n_sm = 0;
+  PG_CUDA_CHECK(cudaGetDevice(&dev));
+  PG_CUDA_CHECK(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+  const int n_ctile = static_cast<int>(c_pad / kTileC);
+  const int n_ptile = static_cast<int>(p_pad / kTileP);
+  const int n_tiles = n_ctile * n_ptile;
+  const int grid = n_tiles < n_sm ? n_tiles : n_sm;
+  assoc_i8_kernel<FUSED><<<grid, kThreads, Cfg<FUSED>::kSmemBytes, stream>>>(
+      tm_qh, tm_q1, tm_q0, tm_v, tm_v127, n_ctile, n_ptile, static_cast<int>(k_pad / kTileK), ep);
+  PG_CUDA_CHECK(cudaGetLastError());
+  return PG_OK;
+}
+
+int encode_panel(const int8_t* qh, const int8_t* q1, const int8_t* q0, int64_t p_pad, int64_t k_pad,
+                 CUtensorMap& a, CUtensorMap& b, CUtensorMap& c) {
+  const uint64_t pitch = static_cast<uint64_t>(k_pad);
+  PG_CHECK_STATUS(encode_tmap_2d_i8(&a, qh, k_pad, p_pad, pitch, kTileK, kTileP));
+  PG_CHECK_STATUS(encode_tmap_2d_i8(&b, q1, k_pad, p_pad, pitch, kTileK, kTileP));
+  PG_CHECK_STATUS(encode_tmap_2d_i8(&c, q0, k_pad, p_pad, pitch, kTileK, kTileP));
+  return PG_OK;
+}
+
 }  // namespace
 
 int launch_assoc(const int8_t* qh, const int8_t* q1, const int8_t* q0, int64_t p_pad, const int8_t* v,
@@ -263,24 +384,25 @@ int launch_assoc(const int8_t* qh, const int8_t* q1, const int8_t* q0, int64_t p
                  ep.rows_per_marker == 16,
              PG_ERR_INVALID, "assoc: rows_per_marker %d", ep.rows_per_marker);
   CUtensorMap tm_qh, tm_q1, tm_q0, tm_v, tm_v127;
-  const uint64_t pitch = static_cast<uint64_t>(k_pad);
-  PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_qh, qh, k_pad, p_pad, pitch, kTileK, kTileP));
-  PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_q1, q1, k_pad, p_pad, pitch, kTileK, kTileP));
-  PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_q0, q0, k_pad, p_pad, pitch, kTileK, kTileP));
-  PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_v, v, k_pad, c_pad, pitch, kTileK, kTileC));
-  PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_v127, v127, k_pad, c_pad, pitch, kTileK, kTileC));
-  PG_CUDA_CHECK(cudaFuncSetAttribute(assoc_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
-  int dev = 0, n_sm = 0;
-  PG_CUDA_CHECK(cudaGetDevice(&dev));
-  PG_CUDA_CHECK(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
-  const int n_ctile = static_cast<int>(c_pad / kTileC);
-  const int n_ptile = static_cast<int>(p_pad / kTileP);
-  const int n_tiles = n_ctile * n_ptile;
-  const int grid = n_tiles < n_sm ? n_tiles : n_sm;
-  assoc_i8_kernel<<<grid, kThreads, kSmemBytes, stream>>>(tm_qh, tm_q1, tm_q0, tm_v, tm_v127, n_ctile, n_ptile,
-                                                          static_cast<int>(k_pad / kTileK), ep);
-  PG_CUDA_CHECK(cudaGetLastError());
-  return PG_OK;
+  PG_CHECK_STATUS(encode_panel(qh, q1, q0, p_pad, k_pad, tm_qh, tm_q1, tm_q0));
+  PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_v, v, k_pad, c_pad, k_pad, kTileK, kTileC));
+  PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_v127, v127, k_pad, c_pad, k_pad, kTileK, kTileC));
+  return launch_common<false>(tm_qh, tm_q1, tm_q0, tm_v, tm_v127, p_pad, c_pad, k_pad, ep, stream);
+}
+
+int launch_assoc_packed(const int8_t* qh, const int8_t* q1, const int8_t* q0, int64_t p_pad, const uint8_t* packed,
+                        int64_t pitch, int64_t n_markers, int64_t k_pad, const AssocEpilogue& ep,
+                        cudaStream_t stream) {
+  PG_REQUIRE(p_pad % kTileP == 0 && k_pad % kTileK == 0 && n_markers > 0 && pitch * 4 >= k_pad && pitch % 16 == 0,
+             PG_ERR_INVALID, "assoc(packed): bad shape p=%lld m=%lld k=%lld pitch=%lld", (long long)p_pad,
+             (long long)n_markers, (long long)k_pad, (long long)pitch);
+  PG_REQUIRE(ep.rows_per_marker == 1, PG_ERR_INVALID, "assoc(packed): fused decode needs rows_per_marker 1");
+  CUtensorMap tm_qh, tm_q1, tm_q0, tm_pk;
+  PG_CHECK_STATUS(encode_panel(qh, q1, q0, p_pad, k_pad, tm_qh, tm_q1, tm_q0));
+  // packed rows: k_pad/4 bytes of codes per marker (rows past n_markers read as zeros by TMA)
+  PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_pk, packed, k_pad / 4, n_markers, pitch, kTileK / 4, kTileC, false));
+  const int64_t c_pad = round_up(n_markers, kTileC);
+  return launch_common<true>(tm_qh, tm_q1, tm_q0, tm_pk, tm_pk, p_pad, c_pad, k_pad, ep, stream);
 }
 
 }  // namespace pg

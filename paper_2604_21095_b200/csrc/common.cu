@@ -26,7 +26,7 @@ void set_error(const char* fmt, ...) {
 const char* get_error() { return g_err; }
 
 int encode_tmap_2d_i8(CUtensorMap* out, const void* base, uint64_t inner_elems, uint64_t rows,
-                       uint64_t row_pitch_bytes, uint32_t box_inner, uint32_t box_rows) {
+                      uint64_t row_pitch_bytes, uint32_t box_inner, uint32_t box_rows, bool swizzle64) {
   if (g_encode == nullptr) {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -42,7 +42,8 @@ int encode_tmap_2d_i8(CUtensorMap* out, const void* base, uint64_t inner_elems, 
   cuuint32_t box[2] = {box_inner, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = g_encode(out, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        swizzle64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   PG_REQUIRE(r == CUDA_SUCCESS, PG_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return PG_OK;

@@ -147,6 +147,7 @@ struct pg_ctx {
   int64_t last_m = 0, last_ncand = 0;
   int last_R = 1;
   int64_t cand_capacity = 0;
+  bool fused_decode = true;
 };
 
 namespace pg {
@@ -267,10 +268,19 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
   PG_CUDA_CHECK(cudaStreamSynchronize(s));
   const int R = geno_rows_per_marker(b, hflags[0] != 0);
   const int64_t c_pad = round_up(m * R, kTileC);
-  PG_CHECK_STATUS(c->v.ensure(static_cast<size_t>(c_pad) * c->k_pad));
-  PG_CHECK_STATUS(c->v127.ensure(static_cast<size_t>(c_pad) * c->k_pad));
-  PG_CHECK_STATUS(geno_planes(b, R, c->v.p, c->v127.p, c_pad, c->k_pad, s));
-  int64_t launches = (kind == PG_GENO_DENSE_F64 ? 3 : 2);
+  // PLINK rows without missing calls: the GEMM decodes the packed codes itself
+  const bool fused = c->fused_decode && kind == PG_GENO_BED && R == 1;
+  int64_t launches = (kind == PG_GENO_DENSE_F64 ? 2 : 1);
+  if (!fused) {
+    PG_CHECK_STATUS(c->v.ensure(static_cast<size_t>(c_pad) * c->k_pad));
+    PG_CHECK_STATUS(c->v127.ensure(static_cast<size_t>(c_pad) * c->k_pad));
+    PG_CHECK_STATUS(geno_planes(b, R, c->v.p, c->v127.p, c_pad, c->k_pad, s));
+    ++launches;
+  }
+  auto run_gemm = [&](const AssocEpilogue& e) -> int {
+    if (fused) return launch_assoc_packed(c->qh.p, c->q1.p, c->q0.p, c->p_pad, d_data, pitch, m, c->k_pad, e, s);
+    return launch_assoc(c->qh.p, c->q1.p, c->q0.p, c->p_pad, c->v.p, c->v127.p, c_pad, c->k_pad, e, s);
+  };
   float decode_ms = 0.f;
 
   PG_CHECK_STATUS(c->counters.ensure(4));
@@ -304,7 +314,7 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
     ep.cand_cap = 0;
     PG_CUDA_CHECK(cudaMemsetAsync(c->cand_count.p, 0, sizeof(int), s));
     PG_CUDA_CHECK(cudaEventRecord(c->ev[1], s));
-    PG_CHECK_STATUS(launch_assoc(c->qh.p, c->q1.p, c->q0.p, c->p_pad, c->v.p, c->v127.p, c_pad, c->k_pad, ep, s));
+    PG_CHECK_STATUS(run_gemm(ep));
     PG_CUDA_CHECK(cudaEventRecord(c->ev[2], s));
     ++launches;
   } else {
@@ -320,7 +330,7 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
       ep.cand_cap = c->cand_capacity;
       PG_CUDA_CHECK(cudaMemsetAsync(c->cand_count.p, 0, sizeof(int), s));
       PG_CUDA_CHECK(cudaEventRecord(c->ev[1], s));
-      PG_CHECK_STATUS(launch_assoc(c->qh.p, c->q1.p, c->q0.p, c->p_pad, c->v.p, c->v127.p, c_pad, c->k_pad, ep, s));
+      PG_CHECK_STATUS(run_gemm(ep));
       PG_CUDA_CHECK(cudaEventRecord(c->ev[2], s));
       ++launches;
       int hcount = 0;
@@ -569,6 +579,12 @@ int pg_ctx_set_scan(pg_ctx* c, double df, int mode, const double* r_bar) {
   }
   PG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
   c->have_scan = true;
+  return PG_OK;
+}
+
+int pg_ctx_set_fused_decode(pg_ctx* c, int enable) {
+  PG_CHECK_STATUS(ctx_check(c));
+  c->fused_decode = enable != 0;
   return PG_OK;
 }
 

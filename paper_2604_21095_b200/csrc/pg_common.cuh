@@ -41,9 +41,9 @@ const char* get_error();
   } while (0)
 
 // cuTensorMapEncodeTiled resolved through the runtime's driver entry point.
-// 2-D int8 tensor map, 64-byte swizzle (box_inner must be 64).
+// 2-D byte tensor map; 64-byte swizzle by default (box_inner must then be 64).
 int encode_tmap_2d_i8(CUtensorMap* out, const void* base, uint64_t inner_elems, uint64_t rows,
-                      uint64_t row_pitch_bytes, uint32_t box_inner, uint32_t box_rows);
+                      uint64_t row_pitch_bytes, uint32_t box_inner, uint32_t box_rows, bool swizzle64 = true);
 
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 

@@ -24,6 +24,7 @@ from __future__ import annotations
 
 import enum
 import json
+import os
 import sys
 import time
 from concurrent.futures import ThreadPoolExecutor
@@ -281,6 +282,8 @@ def _run_scan_open(config: ScanConfig, source, wall0: float) -> ScanSummary:
         writer = output.ThresholdWriter(config.out_path, config.p_threshold, df, n, source.counts_allele1, names)
 
     ctx = DeviceContext(config.device)
+    if os.environ.get("PANELGWAS_FUSED_DECODE", "1") == "0":
+        ctx.set_fused_decode(False)  # A/B switch; results are identical either way
     try:
         ctx.set_panel(prep.ytil, prep.align.genotype_row_index, source.n_samples)
         t_floor = np.inf

@@ -167,3 +167,11 @@ def test_c1_full_subset(c1, tmp_path):
     assert np.array_equal(rows[pos], g["full_f64_rows"])
     rel = np.abs(t[pos] - g["full_f64_t"]) / np.maximum(1, np.abs(g["full_f64_t"]))
     assert rel.max() <= TOL
+
+
+def test_c1_fused_decode_matches_planes_bitwise(c1, tmp_path, monkeypatch):
+    """The in-GEMM 2-bit decode and the materialized-plane path are the same integers."""
+    _scan(c1, tmp_path / "fused.bin", output_mode=pg.OutputMode.FULL, precision=pg.Precision.F64, device_batch=3000)
+    monkeypatch.setenv("PANELGWAS_FUSED_DECODE", "0")
+    _scan(c1, tmp_path / "planes.bin", output_mode=pg.OutputMode.FULL, precision=pg.Precision.F64, device_batch=3000)
+    assert (tmp_path / "fused.bin").read_bytes() == (tmp_path / "planes.bin").read_bytes()
