@@ -361,10 +361,15 @@ def our_arm(a) -> None:
             h2d = distribute_panel(y_host) + (n * p * 8 if rank == 0 else 0)
             ctx.set_scan(df, _native.PG_MODE_THRESHOLD, rbar)
             d2h = 0
-            for s, c in batches:
-                r = ctx.scan(_native.PG_GENO_BED, host_np[s:s + c], bpm)
-                d2h += r.cand_rows.size * 40 + c * 25
+            # public host-buffer C-ABI path, pipelined: H2D of batch i+1 overlaps the scan of batch i
+            for i, (s, c) in enumerate(batches):
+                ctx.stage(i % 2, _native.PG_GENO_BED, host_np[s:s + c], bpm)
                 h2d += c * bpm
+                if i:
+                    r = ctx.scan_staged((i - 1) % 2)
+                    d2h += r.cand_rows.size * 40 + r.n_markers * 25
+            r = ctx.scan_staged((len(batches) - 1) % 2)
+            d2h += r.cand_rows.size * 40 + r.n_markers * 25
             return h2d, d2h
 
         e2e_step()

@@ -62,6 +62,10 @@ PG_API int pg_device_count(int* n);
 
 typedef struct pg_ctx pg_ctx;
 
+/* Page-locked host memory for staging genotype blocks (cudaHostAlloc). */
+PG_API int pg_host_alloc(int64_t bytes, void** out);
+PG_API int pg_host_free(void* ptr);
+
 /* Context lifetime. Replaces the panel-side state the reference shares
  * between workers, engine._Prepared (engine.py:154-167). */
 PG_API int pg_ctx_create(int device, pg_ctx** out);
@@ -135,6 +139,14 @@ PG_API int pg_scan(pg_ctx* ctx, int geno_kind, const void* data, int64_t n_marke
  * row_pitch a multiple of 16). */
 PG_API int pg_scan_device(pg_ctx* ctx, int geno_kind, const void* d_data, int64_t n_markers, int64_t row_bytes,
                    int64_t row_pitch, pg_batch_info* info);
+
+/* Asynchronous staging for pipelined scans (transfer of batch i+1 overlaps the
+ * GEMM of batch i). pg_stage copies HOST rows into staging slot `slot` (0 or 1) on
+ * the ctx's copy stream and returns immediately; `data` must stay valid (pinned
+ * memory recommended) until pg_scan_staged(slot) returns. pg_scan_staged waits
+ * for the slot's copy on the device, then scans it exactly like pg_scan. */
+PG_API int pg_stage(pg_ctx* ctx, int slot, int geno_kind, const void* data, int64_t n_markers, int64_t row_bytes);
+PG_API int pg_scan_staged(pg_ctx* ctx, int slot, pg_batch_info* info);
 
 /* Per-marker QC of the last scan: StandardizedBatch.allele_frequency,
  * missing_count, variance_before_scaling, skip_reason (kernel.py:360-373). Any pointer may be NULL. */

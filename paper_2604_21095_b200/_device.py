@@ -150,6 +150,19 @@ class DeviceContext:
             call("pg_scan", self._h, int(kind), blk.ctypes.data, n, int(row_bytes), byref(info))
             return self._collect(info, fetch, full_elem_bytes)
 
+    def stage(self, slot: int, kind: int, block: np.ndarray, row_bytes: int) -> None:
+        """Start the async H2D of a host block into staging slot 0/1 (keep `block` alive until scanned)."""
+        blk = block if block.flags["C_CONTIGUOUS"] else np.ascontiguousarray(block)
+        with self.lock:
+            call("pg_stage", self._h, int(slot), int(kind), blk.ctypes.data, blk.shape[0], int(row_bytes))
+        return blk
+
+    def scan_staged(self, slot: int, *, fetch: bool = True, full_elem_bytes: int = 8) -> ScanResult:
+        info = BatchInfo()
+        with self.lock:
+            call("pg_scan_staged", self._h, int(slot), byref(info))
+            return self._collect(info, fetch, full_elem_bytes)
+
     def scan_device(self, kind: int, d_ptr: int, n_markers: int, row_bytes: int, row_pitch: int, *,
                     fetch: bool = True, full_elem_bytes: int = 8) -> ScanResult:
         info = BatchInfo()

@@ -56,6 +56,8 @@ SIGNATURES: dict[str, list] = {
     "pg_last_error": [],
     "pg_abi_version": [],
     "pg_device_count": [_P],
+    "pg_host_alloc": [c_int64, _P],
+    "pg_host_free": [_P],
     "pg_ctx_create": [c_int, _P],
     "pg_ctx_destroy": [_P],
     "pg_ctx_sync": [_P],
@@ -70,6 +72,8 @@ SIGNATURES: dict[str, list] = {
     "pg_ctx_set_fused_decode": [_P, c_int],
     "pg_scan": [_P, c_int, _P, c_int64, c_int64, _P],
     "pg_scan_device": [_P, c_int, _P, c_int64, c_int64, c_int64, _P],
+    "pg_stage": [_P, c_int, c_int, _P, c_int64, c_int64],
+    "pg_scan_staged": [_P, c_int, _P],
     "pg_fetch_marker_stats": [_P, _P, _P, _P, _P],
     "pg_fetch_candidates": [_P, _P, _P, _P, _P, _P],
     "pg_fetch_full": [_P, _P, c_int, _P],
@@ -153,3 +157,26 @@ def device_count() -> int:
 def require_device() -> None:
     if device_count() < 1:
         raise PanelGwasError("panelgwas_b200 requires an NVIDIA B200 (sm_100) device; none is visible")
+
+
+class PinnedBuffer:
+    """Page-locked host bytes (pg_host_alloc) viewed as a numpy uint8 array."""
+
+    def __init__(self, nbytes: int):
+        self.nbytes = int(nbytes)
+        p = c_void_p()
+        call("pg_host_alloc", self.nbytes, ctypes.byref(p))
+        self._ptr = p
+        self.array = np.ctypeslib.as_array((ctypes.c_uint8 * self.nbytes).from_address(p.value))
+
+    def close(self) -> None:
+        if self._ptr:
+            self.array = None
+            load_library().pg_host_free(self._ptr)
+            self._ptr = c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

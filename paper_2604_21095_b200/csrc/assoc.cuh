@@ -17,8 +17,8 @@
 
 namespace pg {
 
-constexpr int kTileP = 128;   // phenotypes per tile (UMMA M, A operand = panel limbs)
-constexpr int kTileC = 256;   // genotype rows per tile (UMMA N, B operand)
+constexpr int kTileP = 256;   // phenotypes per CTA-pair tile (UMMA M = 256, cta_group::2; A = panel limbs)
+constexpr int kTileC = 256;   // genotype rows per pair tile (UMMA N, B operand; 128 per CTA)
 constexpr int kTileK = 64;    // int8 samples per pipeline stage (one 64-byte swizzle row)
 constexpr int64_t kWH = 32385;          // weight of the high limb: 2*(127*127+63)+1
 constexpr int64_t kQMax = kWH * 127 + 16192;  // largest |q| representable by the limbs

@@ -37,9 +37,13 @@
 namespace pg {
 namespace {
 
-constexpr int kQBytes = kTileP * kTileK;  // 8 KB per panel limb tile
-constexpr int kVBytes = kTileC * kTileK;  // 16 KB per genotype plane tile
-constexpr int kPackedBytes = kTileC * (kTileK / 4);  // 4 KB packed .bed tile
+// Pair tile (cta_group::2): 256 phenotypes x 256 genotype rows; each CTA of the
+// pair stages its own 128 phenotypes (A half) and 128 genotype rows (B half).
+constexpr int kHalfP = kTileP / 2;
+constexpr int kHalfC = kTileC / 2;
+constexpr int kQBytes = kHalfP * kTileK;             // 8 KB per panel limb half-tile
+constexpr int kVBytes = kHalfC * kTileK;             // 8 KB per genotype plane half-tile
+constexpr int kPackedBytes = kHalfC * (kTileK / 4);  // 2 KB packed .bed half-tile
 constexpr int kOffV = 3 * kQBytes;
 constexpr int kOffV127 = kOffV + kVBytes;
 constexpr int kOffPacked = kOffV127 + kVBytes;
@@ -51,10 +55,11 @@ constexpr int kGroupC = 8;  // genotype tiles per raster group
 
 template <bool FUSED>
 struct Cfg {
-  static constexpr int kStages = FUSED ? 3 : 4;
-  static constexpr int kStageBytes = FUSED ? kOffPacked + kPackedBytes : kOffPacked;
-  static constexpr int kTmaBytes = FUSED ? 3 * kQBytes + kPackedBytes : kOffPacked;
-  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kStages = 5;
+  static constexpr int kStageBytes = FUSED ? kOffPacked + 2048 : kOffPacked;  // 1 KB-aligned stages
+  static constexpr int kPanelBytes = 3 * kQBytes;
+  static constexpr int kTmaBytes = FUSED ? kPanelBytes : kOffPacked;  // per CTA, signalled on the leader
+  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 512 /*barriers*/;
 };
 
 __device__ __forceinline__ void tile_coords(int t, int n_ctile, int n_ptile, int& ct, int& pt) {
@@ -160,23 +165,29 @@ __device__ __forceinline__ void epilogue_tile(const AssocEpilogue& ep, uint32_t 
 }
 
 template <bool FUSED>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     assoc_i8_kernel(const __grid_constant__ CUtensorMap tm_qh, const __grid_constant__ CUtensorMap tm_q1,
                     const __grid_constant__ CUtensorMap tm_q0, const __grid_constant__ CUtensorMap tm_v,
                     const __grid_constant__ CUtensorMap tm_v127, int n_ctile, int n_ptile, int n_kb,
                     AssocEpilogue ep) {
   using C = Cfg<FUSED>;
+  constexpr int S = C::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
-  uint64_t* empty = full + C::kStages;
-  uint64_t* dec = empty + C::kStages;
-  uint64_t* tfull = dec + C::kStages;
-  uint64_t* tempty = tfull + 1;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * C::kStageBytes);  // leader: TMA of both CTAs
+  uint64_t* empty = full + S;                                                // each CTA: MMA done with stage
+  uint64_t* dec = empty + S;                                                 // leader: decoders of both CTAs
+  uint64_t* pk = dec + S;                                                    // each CTA: its packed tile landed
+  uint64_t* tfull = pk + S;                                                  // each CTA: accumulators ready
+  uint64_t* tempty = tfull + 1;                                              // leader: both CTAs drained TMEM
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t cr = cluster_ctarank();
+  const bool leader = cr == 0;
+  const int cid = blockIdx.x >> 1;
+  const int n_clusters = gridDim.x >> 1;
   const int n_tiles = n_ctile * n_ptile;
 
   if (warp == 0 && lane == 0) {
@@ -187,45 +198,50 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (!FUSED) tma_prefetch_desc(&tm_v127);
   }
   if (warp == 1 && lane == 0) {
-    for (int s = 0; s < C::kStages; ++s) {
-      mbar_init(&full[s], 1);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 2);
       mbar_init(&empty[s], 1);
-      mbar_init(&dec[s], 4);
+      mbar_init(&dec[s], 8);
+      mbar_init(&pk[s], 1);
     }
     mbar_init(tfull, 1);
-    mbar_init(tempty, kEpiWarps);
+    mbar_init(tempty, 2 * kEpiWarps);
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, kTmemCols);
+  if (warp == 2) tmem_alloc_pair(tmem_slot, kTmemCols);
   tc_fence_before();
   __syncthreads();
+  cluster_sync_all();  // peer barriers initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
     if (lane == 0) {
-      // ------------------------------------------------------------ TMA producer
-      // panel tiles are shared by the kGroupC concurrent CTAs of a raster group -> keep them in L2
+      // ------------------------------------------------------------ TMA producer (both CTAs)
       const uint64_t pol_keep = l2_policy_evict_last();
       uint32_t s = 0, ph = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      for (int t = cid; t < n_tiles; t += n_clusters) {
         int ct, pt;
         tile_coords(t, n_ctile, n_ptile, ct, pt);
+        const int prow = pt * kTileP + cr * kHalfP;
+        const int grow = ct * kTileC + cr * kHalfC;
         for (int kb = 0; kb < n_kb; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = smem + s * C::kStageBytes;
           const int kx = kb * kTileK;
-          mbar_arrive_expect_tx(&full[s], C::kTmaBytes);
-          tma_load_2d_hint(st, &tm_qh, &full[s], kx, pt * kTileP, pol_keep);
-          tma_load_2d_hint(st + kQBytes, &tm_q1, &full[s], kx, pt * kTileP, pol_keep);
-          tma_load_2d_hint(st + 2 * kQBytes, &tm_q0, &full[s], kx, pt * kTileP, pol_keep);
+          const uint32_t full0 = map_to_cta(&full[s], 0);
+          mbar_arrive_expect_tx_cluster(full0, C::kTmaBytes);
+          tma_load_2d_pair(st, &tm_qh, full0, kx, prow, pol_keep);
+          tma_load_2d_pair(st + kQBytes, &tm_q1, full0, kx, prow, pol_keep);
+          tma_load_2d_pair(st + 2 * kQBytes, &tm_q0, full0, kx, prow, pol_keep);
           if constexpr (FUSED) {
-            tma_load_2d(st + kOffPacked, &tm_v, &full[s], kb * (kTileK / 4), ct * kTileC);
+            mbar_arrive_expect_tx(&pk[s], kPackedBytes);
+            tma_load_2d(st + kOffPacked, &tm_v, &pk[s], kb * (kTileK / 4), grow);
           } else {
-            tma_load_2d(st + kOffV, &tm_v, &full[s], kx, ct * kTileC);
-            tma_load_2d(st + kOffV127, &tm_v127, &full[s], kx, ct * kTileC);
+            tma_load_2d_pair(st + kOffV, &tm_v, full0, kx, grow, pol_keep);
+            tma_load_2d_pair(st + kOffV127, &tm_v127, full0, kx, grow, pol_keep);
           }
-          if (++s == C::kStages) {
+          if (++s == S) {
             s = 0;
             ph ^= 1;
           }
@@ -233,19 +249,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ------------------------------------------------------------ MMA issuer
-      constexpr uint32_t idesc = idesc_s8_s32(kTileP, kTileC);
+    if (leader && lane == 0) {
+      // ------------------------------------------------------------ MMA issuer (leader CTA)
+      constexpr uint32_t idesc = idesc_s8_s32(kTileP, kTileC);  // M = 256 across the pair
       const uint32_t dH = tmem_base;
       const uint32_t dL = tmem_base + kTileC;
       uint32_t s = 0, ph = 0, aph = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        mbar_wait(tempty, aph ^ 1);
+      for (int t = cid; t < n_tiles; t += n_clusters) {
+        mbar_wait_cluster(tempty, aph ^ 1);
         tc_fence_after();
         uint32_t acc = 0;
         for (int kb = 0; kb < n_kb; ++kb) {
-          mbar_wait(&full[s], ph);
-          if constexpr (FUSED) mbar_wait(&dec[s], ph);
+          mbar_wait_cluster(&full[s], ph);
+          if constexpr (FUSED) mbar_wait_cluster(&dec[s], ph);
           tc_fence_after();
           const uint32_t st = smem_u32(smem + s * C::kStageBytes);
           const uint64_t d_qh = umma_desc_sw64(st);
@@ -256,53 +272,48 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int k = 0; k < kTileK / 32; ++k) {
             // +32 bytes along K inside the 64-byte swizzle row == +2 in the >>4 address field
-            mma_i8_ss(dH, d_qh + 2 * k, d_v + 2 * k, idesc, acc);
-            mma_i8_ss(dL, d_q1 + 2 * k, d_v127 + 2 * k, idesc, acc);
-            mma_i8_ss(dL, d_q0 + 2 * k, d_v + 2 * k, idesc, 1);
+            mma_i8_ss_pair(dH, d_qh + 2 * k, d_v + 2 * k, idesc, acc);
+            mma_i8_ss_pair(dL, d_q1 + 2 * k, d_v127 + 2 * k, idesc, acc);
+            mma_i8_ss_pair(dL, d_q0 + 2 * k, d_v + 2 * k, idesc, 1);
             acc = 1;
           }
-          mma_commit(&empty[s]);
-          if (++s == C::kStages) {
+          mma_commit_pair_multicast(&empty[s], 0x3);
+          if (++s == S) {
             s = 0;
             ph ^= 1;
           }
         }
-        mma_commit(tfull);
+        mma_commit_pair_multicast(tfull, 0x3);
         aph ^= 1;
       }
     }
   } else if (warp >= 4 && warp < kFirstEpiWarp) {
     if constexpr (FUSED) {
-      // ------------------------------------------------------------ decoders
-      // thread dt expands rows dt and dt+128 of the packed tile: 16 bytes = 64 samples
-      // -> 64 B of v and 64 B of 127v, written as 4 swizzled 16-byte chunks each
+      // ------------------------------------------------------------ decoders (both CTAs)
+      // thread r expands row r of this CTA's packed half-tile: 16 bytes = 64 samples
+      // -> 64 B of v and 64 B of 127v, as 4 swizzled 16-byte chunks each
       // (SW64: chunk c of row r lives at r*64 + ((c ^ ((r >> 1) & 3)) << 4)).
-      const int dt = threadIdx.x - 128;
+      const int r = threadIdx.x - 128;
+      const uint32_t sw = (static_cast<uint32_t>(r) >> 1) & 3u;
       uint32_t s = 0, ph = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      for (int t = cid; t < n_tiles; t += n_clusters) {
         for (int kb = 0; kb < n_kb; ++kb) {
-          mbar_wait(&full[s], ph);
+          mbar_wait(&pk[s], ph);
           uint8_t* st = smem + s * C::kStageBytes;
-          const uint4* pk = reinterpret_cast<const uint4*>(st + kOffPacked);
+          const uint4 w = reinterpret_cast<const uint4*>(st + kOffPacked)[r];
+          const uint32_t words[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-          for (int half = 0; half < 2; ++half) {
-            const int r = dt + 128 * half;
-            const uint4 w = pk[r];
-            const uint32_t words[4] = {w.x, w.y, w.z, w.w};
-            const uint32_t sw = (static_cast<uint32_t>(r) >> 1) & 3u;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              uint32_t u[4], u7[4];
-              decode_word(words[c], u, u7);
-              const uint32_t off = r * 64 + ((c ^ sw) << 4);
-              *reinterpret_cast<uint4*>(st + kOffV + off) = make_uint4(u[0], u[1], u[2], u[3]);
-              *reinterpret_cast<uint4*>(st + kOffV127 + off) = make_uint4(u7[0], u7[1], u7[2], u7[3]);
-            }
+          for (int c = 0; c < 4; ++c) {
+            uint32_t u[4], u7[4];
+            decode_word(words[c], u, u7);
+            const uint32_t off = r * 64 + ((c ^ sw) << 4);
+            *reinterpret_cast<uint4*>(st + kOffV + off) = make_uint4(u[0], u[1], u[2], u[3]);
+            *reinterpret_cast<uint4*>(st + kOffV127 + off) = make_uint4(u7[0], u7[1], u7[2], u7[3]);
           }
           fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the tensor core
           __syncwarp();
-          if (lane == 0) mbar_arrive(&dec[s]);
-          if (++s == C::kStages) {
+          if (lane == 0) mbar_arrive_cluster(map_to_cta(&dec[s], 0));
+          if (++s == S) {
             s = 0;
             ph ^= 1;
           }
@@ -310,17 +321,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp >= kFirstEpiWarp) {
-    // -------------------------------------------------------------- epilogue
-    // warp w reads TMEM lanes [32*(w%4), +32) (hardware lane-quarter rule) and
-    // columns [64*cg, +64) of the tile: 16 warps drain the 2 x 256 columns 4x faster
+    // -------------------------------------------------------------- epilogue (both CTAs)
+    // this CTA's TMEM holds its 128 phenotypes (lanes) x all 256 genotype rows of the
+    // pair tile (columns). Warp w reads lanes [32*(w%4), +32) (lane-quarter rule) and
+    // columns [64*cg, +64): 16 warps drain the 2 x 256 columns 4x faster.
     const int quarter = warp & 3;
     const int cg = (warp - kFirstEpiWarp) >> 2;
+    const uint32_t tempty0 = map_to_cta(tempty, 0);
     uint32_t aph = 0;
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    for (int t = cid; t < n_tiles; t += n_clusters) {
       int ct, pt;
       tile_coords(t, n_ctile, n_ptile, ct, pt);
-      const int pheno = pt * kTileP + quarter * 32 + lane;
-      mbar_wait(tfull, aph);
+      const int pheno = pt * kTileP + cr * kHalfP + quarter * 32 + lane;
+      mbar_wait_cluster(tfull, aph);
       tc_fence_after();
       const uint32_t tH = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16);
       const uint32_t tL = tH + kTileC;
@@ -333,15 +346,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty);
+      if (lane == 0) mbar_arrive_cluster(tempty0);
       aph ^= 1;
     }
   }
 
   tc_fence_before();
   __syncthreads();
+  cluster_sync_all();  // both CTAs done with TMEM and with remote barriers
   tc_fence_after();
-  if (warp == 2) tmem_free(tmem_base, kTmemCols);
+  if (warp == 2) tmem_free_pair(tmem_base, kTmemCols);
 }
 
 template <bool FUSED>
@@ -356,7 +370,8 @@ int launch_common(const CUtensorMap& tm_qh, const CUtensorMap& tm_q1, const CUte
   const int n_ctile = static_cast<int>(c_pad / kTileC);
   const int n_ptile = static_cast<int>(p_pad / kTileP);
   const int n_tiles = n_ctile * n_ptile;
-  const int grid = n_tiles < n_sm ? n_tiles : n_sm;
+  const int max_pairs = n_sm / 2;
+  const int grid = 2 * (n_tiles < max_pairs ? n_tiles : max_pairs);
   assoc_i8_kernel<FUSED><<<grid, kThreads, Cfg<FUSED>::kSmemBytes, stream>>>(
       tm_qh, tm_q1, tm_q0, tm_v, tm_v127, n_ctile, n_ptile, static_cast<int>(k_pad / kTileK), ep);
   PG_CUDA_CHECK(cudaGetLastError());
@@ -366,9 +381,9 @@ int launch_common(const CUtensorMap& tm_qh, const CUtensorMap& tm_q1, const CUte
 int encode_panel(const int8_t* qh, const int8_t* q1, const int8_t* q0, int64_t p_pad, int64_t k_pad,
                  CUtensorMap& a, CUtensorMap& b, CUtensorMap& c) {
   const uint64_t pitch = static_cast<uint64_t>(k_pad);
-  PG_CHECK_STATUS(encode_tmap_2d_i8(&a, qh, k_pad, p_pad, pitch, kTileK, kTileP));
-  PG_CHECK_STATUS(encode_tmap_2d_i8(&b, q1, k_pad, p_pad, pitch, kTileK, kTileP));
-  PG_CHECK_STATUS(encode_tmap_2d_i8(&c, q0, k_pad, p_pad, pitch, kTileK, kTileP));
+  PG_CHECK_STATUS(encode_tmap_2d_i8(&a, qh, k_pad, p_pad, pitch, kTileK, kHalfP));
+  PG_CHECK_STATUS(encode_tmap_2d_i8(&b, q1, k_pad, p_pad, pitch, kTileK, kHalfP));
+  PG_CHECK_STATUS(encode_tmap_2d_i8(&c, q0, k_pad, p_pad, pitch, kTileK, kHalfP));
   return PG_OK;
 }
 
@@ -385,8 +400,8 @@ int launch_assoc(const int8_t* qh, const int8_t* q1, const int8_t* q0, int64_t p
              PG_ERR_INVALID, "assoc: rows_per_marker %d", ep.rows_per_marker);
   CUtensorMap tm_qh, tm_q1, tm_q0, tm_v, tm_v127;
   PG_CHECK_STATUS(encode_panel(qh, q1, q0, p_pad, k_pad, tm_qh, tm_q1, tm_q0));
-  PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_v, v, k_pad, c_pad, k_pad, kTileK, kTileC));
-  PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_v127, v127, k_pad, c_pad, k_pad, kTileK, kTileC));
+  PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_v, v, k_pad, c_pad, k_pad, kTileK, kHalfC));
+  PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_v127, v127, k_pad, c_pad, k_pad, kTileK, kHalfC));
   return launch_common<false>(tm_qh, tm_q1, tm_q0, tm_v, tm_v127, p_pad, c_pad, k_pad, ep, stream);
 }
 
@@ -400,7 +415,7 @@ int launch_assoc_packed(const int8_t* qh, const int8_t* q1, const int8_t* q0, in
   CUtensorMap tm_qh, tm_q1, tm_q0, tm_pk;
   PG_CHECK_STATUS(encode_panel(qh, q1, q0, p_pad, k_pad, tm_qh, tm_q1, tm_q0));
   // packed rows: k_pad/4 bytes of codes per marker (rows past n_markers read as zeros by TMA)
-  PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_pk, packed, k_pad / 4, n_markers, pitch, kTileK / 4, kTileC, false));
+  PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_pk, packed, k_pad / 4, n_markers, pitch, kTileK / 4, kHalfC, false));
   const int64_t c_pad = round_up(n_markers, kTileC);
   return launch_common<true>(tm_qh, tm_q1, tm_q0, tm_pk, tm_pk, p_pad, c_pad, k_pad, ep, stream);
 }

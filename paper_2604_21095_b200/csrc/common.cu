@@ -57,6 +57,18 @@ const char* pg_last_error(void) { return pg::get_error(); }
 
 int pg_abi_version(void) { return 1; }
 
+int pg_host_alloc(int64_t bytes, void** out) {
+  PG_REQUIRE(out != nullptr && bytes > 0, PG_ERR_INVALID, "pg_host_alloc: bad arguments");
+  *out = nullptr;
+  PG_CUDA_CHECK(cudaHostAlloc(out, static_cast<size_t>(bytes), cudaHostAllocPortable));
+  return PG_OK;
+}
+
+int pg_host_free(void* ptr) {
+  if (ptr) PG_CUDA_CHECK(cudaFreeHost(ptr));
+  return PG_OK;
+}
+
 int pg_device_count(int* n) {
   int count = 0;
   *n = 0;

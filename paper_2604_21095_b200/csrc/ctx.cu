@@ -84,6 +84,23 @@ __global__ void row_map_kernel(const int8_t* skip, int64_t m, int64_t* new_row, 
   for (int64_t i = lo; i < hi; ++i) new_row[i] = (skip[i] == 0) ? base++ : -1;
 }
 
+// contiguous rows (row_bytes apart) -> rows `pitch` bytes apart, 16-byte vector stores
+__global__ void repitch_kernel(const uint8_t* __restrict__ src, int64_t row_bytes, uint8_t* __restrict__ dst,
+                               int64_t pitch, int64_t m) {
+  const int64_t row = blockIdx.x;
+  const uint8_t* s = src + row * row_bytes;
+  uint8_t* d = dst + row * pitch;
+  for (int64_t c = threadIdx.x; c * 16 < pitch; c += blockDim.x) {
+    uint8_t tmp[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int64_t b = c * 16 + i;
+      tmp[i] = b < row_bytes ? s[b] : 0;
+    }
+    *reinterpret_cast<uint4*>(d + c * 16) = *reinterpret_cast<const uint4*>(tmp);
+  }
+}
+
 __global__ void rbar_kernel(const double* rbar_in, int64_t n, int64_t p_pad, float* rbar_out) {
   const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (p >= p_pad) return;
@@ -126,6 +143,16 @@ struct pg_ctx {
 
   // batch buffers
   pg::DBuf<uint8_t> packed;
+  // pipelined staging: two device slots filled on a copy stream
+  cudaStream_t copy_stream = nullptr;
+  pg::DBuf<uint8_t> stage_buf[2];
+  pg::DBuf<uint8_t> stage_raw[2];
+  pg::DBuf<uint8_t> raw_rows;
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+  cudaEvent_t slot_free_ev[2] = {nullptr, nullptr};
+  int stage_kind[2] = {-1, -1};
+  int64_t stage_m[2] = {0, 0};
+  int64_t stage_pitch[2] = {0, 0};
   pg::DBuf<long long> n_miss, s_u, ss_u;
   pg::DBuf<double> sum_d, af, var, mu_d, invd_d;
   pg::DBuf<float> mu_f, invd_f;
@@ -152,6 +179,21 @@ struct pg_ctx {
 
 namespace pg {
 namespace {
+
+// Host rows -> pitched device rows: one bulk 1-D H2D (fast even for short, odd-sized
+// rows, unlike a 2-D copy of 65k rows) into `raw`, then an on-device repitch.
+int upload_rows(const void* host, int64_t m, int64_t row_bytes, int64_t pitch, pg::DBuf<uint8_t>& raw, uint8_t* dst,
+                cudaStream_t s) {
+  if (row_bytes == pitch) {
+    PG_CUDA_CHECK(cudaMemcpyAsync(dst, host, static_cast<size_t>(m) * row_bytes, cudaMemcpyHostToDevice, s));
+    return PG_OK;
+  }
+  PG_CHECK_STATUS(raw.ensure(static_cast<size_t>(m) * row_bytes));
+  PG_CUDA_CHECK(cudaMemcpyAsync(raw.p, host, static_cast<size_t>(m) * row_bytes, cudaMemcpyHostToDevice, s));
+  repitch_kernel<<<static_cast<unsigned>(m), 128, 0, s>>>(raw.p, row_bytes, dst, pitch, m);
+  PG_CUDA_CHECK(cudaGetLastError());
+  return PG_OK;
+}
 
 int ctx_check(pg_ctx* c) {
   PG_REQUIRE(c != nullptr, PG_ERR_INVALID, "null pg_ctx");
@@ -415,7 +457,12 @@ int pg_ctx_create(int device, pg_ctx** out) {
   pg_ctx* c = new pg_ctx();
   c->device = device;
   PG_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  PG_CUDA_CHECK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
   for (auto& e : c->ev) PG_CUDA_CHECK(cudaEventCreate(&e));
+  for (int i = 0; i < 2; ++i) {
+    PG_CUDA_CHECK(cudaEventCreateWithFlags(&c->stage_ev[i], cudaEventDisableTiming));
+    PG_CUDA_CHECK(cudaEventCreateWithFlags(&c->slot_free_ev[i], cudaEventDisableTiming));
+  }
   *out = c;
   return PG_OK;
 }
@@ -435,6 +482,7 @@ int pg_ctx_destroy(pg_ctx* c) {
   c->keep_bits.release();
   c->max_abs_r.release();
   c->packed.release();
+  c->raw_rows.release();
   c->flags.release();
   c->cand_key.release();
   c->cand_key_sorted.release();
@@ -447,6 +495,16 @@ int pg_ctx_destroy(pg_ctx* c) {
   c->full_out.release();
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
+  for (int i = 0; i < 2; ++i) {
+    c->stage_buf[i].release();
+    c->stage_raw[i].release();
+    if (c->stage_ev[i]) cudaEventDestroy(c->stage_ev[i]);
+    if (c->slot_free_ev[i]) cudaEventDestroy(c->slot_free_ev[i]);
+  }
+  if (c->copy_stream) {
+    cudaStreamSynchronize(c->copy_stream);
+    cudaStreamDestroy(c->copy_stream);
+  }
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return PG_OK;
@@ -471,8 +529,13 @@ int pg_ctx_set_panel(pg_ctx* c, const double* ytil, int64_t n_kept, int64_t n_ph
   PG_REQUIRE(ytil != nullptr && geno_row_index != nullptr, PG_ERR_INVALID, "pg_ctx_set_panel: null input");
   PG_REQUIRE(ld >= n_pheno && n_pheno >= 1 && n_kept >= 1, PG_ERR_INVALID, "pg_ctx_set_panel: bad shape");
   PG_CHECK_STATUS(c->ystage.ensure(static_cast<size_t>(n_kept) * n_pheno));
-  PG_CUDA_CHECK(cudaMemcpy2DAsync(c->ystage.p, sizeof(double) * n_pheno, ytil, sizeof(double) * ld,
-                                  sizeof(double) * n_pheno, n_kept, cudaMemcpyHostToDevice, c->stream));
+  if (ld == n_pheno) {
+    PG_CUDA_CHECK(cudaMemcpyAsync(c->ystage.p, ytil, sizeof(double) * n_pheno * n_kept, cudaMemcpyHostToDevice,
+                                  c->stream));
+  } else {
+    PG_CUDA_CHECK(cudaMemcpy2DAsync(c->ystage.p, sizeof(double) * n_pheno, ytil, sizeof(double) * ld,
+                                    sizeof(double) * n_pheno, n_kept, cudaMemcpyHostToDevice, c->stream));
+  }
   PG_CHECK_STATUS(upload_panel_common(c, c->ystage.p, n_kept, n_pheno, n_pheno, geno_row_index, n_samples_src));
   c->ystage.release();
   return PG_OK;
@@ -609,9 +672,49 @@ int pg_scan(pg_ctx* c, int kind, const void* data, int64_t n_markers, int64_t ro
   PG_REQUIRE(data != nullptr && n_markers >= 1, PG_ERR_INVALID, "pg_scan: empty batch");
   const int64_t pitch = round_up(row_bytes, 16);
   PG_CHECK_STATUS(c->packed.ensure(static_cast<size_t>(pitch) * n_markers));
-  PG_CUDA_CHECK(cudaMemcpy2DAsync(c->packed.p, pitch, data, row_bytes, row_bytes, n_markers, cudaMemcpyHostToDevice,
-                                  c->stream));
+  PG_CHECK_STATUS(upload_rows(data, n_markers, row_bytes, pitch, c->raw_rows, c->packed.p, c->stream));
   return scan_common(c, kind, c->packed.p, n_markers, pitch, info);
+}
+
+int pg_stage(pg_ctx* c, int slot, int kind, const void* data, int64_t n_markers, int64_t row_bytes) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(slot == 0 || slot == 1, PG_ERR_INVALID, "pg_stage: slot must be 0 or 1");
+  PG_REQUIRE(c->have_panel, PG_ERR_STATE, "pg_stage: no panel uploaded (pg_ctx_set_panel)");
+  const int64_t expect = expected_row_bytes(kind, c->n_src);
+  PG_REQUIRE(expect > 0, PG_ERR_INVALID, "unknown genotype kind %d", kind);
+  PG_REQUIRE(row_bytes == expect, PG_ERR_FORMAT, "packed row has %lld bytes, expected %lld for %lld samples",
+             (long long)row_bytes, (long long)expect, (long long)c->n_src);
+  PG_REQUIRE(data != nullptr && n_markers >= 1, PG_ERR_INVALID, "pg_stage: empty batch");
+  const int64_t pitch = round_up(row_bytes, 16);
+  // the slot may still be read by the scan that last used it
+  PG_CUDA_CHECK(cudaStreamWaitEvent(c->copy_stream, c->slot_free_ev[slot], 0));
+  if (c->stage_buf[slot].cap < static_cast<size_t>(pitch) * n_markers) {
+    PG_CUDA_CHECK(cudaStreamSynchronize(c->copy_stream));
+    PG_CHECK_STATUS(c->stage_buf[slot].ensure(static_cast<size_t>(pitch) * n_markers));
+  }
+  if (c->stage_raw[slot].cap < static_cast<size_t>(row_bytes) * n_markers) {
+    PG_CUDA_CHECK(cudaStreamSynchronize(c->copy_stream));
+    PG_CHECK_STATUS(c->stage_raw[slot].ensure(static_cast<size_t>(row_bytes) * n_markers));
+  }
+  PG_CHECK_STATUS(upload_rows(data, n_markers, row_bytes, pitch, c->stage_raw[slot], c->stage_buf[slot].p,
+                              c->copy_stream));
+  PG_CUDA_CHECK(cudaEventRecord(c->stage_ev[slot], c->copy_stream));
+  c->stage_kind[slot] = kind;
+  c->stage_m[slot] = n_markers;
+  c->stage_pitch[slot] = pitch;
+  return PG_OK;
+}
+
+int pg_scan_staged(pg_ctx* c, int slot, pg_batch_info* info) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(slot == 0 || slot == 1, PG_ERR_INVALID, "pg_scan_staged: slot must be 0 or 1");
+  PG_REQUIRE(c->stage_kind[slot] >= 0, PG_ERR_STATE, "pg_scan_staged: slot %d holds no staged batch", slot);
+  PG_CUDA_CHECK(cudaStreamWaitEvent(c->stream, c->stage_ev[slot], 0));
+  const int kind = c->stage_kind[slot];
+  c->stage_kind[slot] = -1;
+  const int rc = scan_common(c, kind, c->stage_buf[slot].p, c->stage_m[slot], c->stage_pitch[slot], info);
+  PG_CUDA_CHECK(cudaEventRecord(c->slot_free_ev[slot], c->stream));
+  return rc;
 }
 
 int pg_scan_device(pg_ctx* c, int kind, const void* d_data, int64_t n_markers, int64_t row_bytes, int64_t row_pitch,
@@ -771,8 +874,7 @@ int pg_decode_bed(pg_ctx* c, const uint8_t* packed, int64_t n_markers, int64_t r
   PG_CHECK_STATUS(c->packed.ensure(static_cast<size_t>(pitch) * n_markers));
   PG_CHECK_STATUS(c->full_out.ensure(static_cast<size_t>(n_markers) * n_samples * elem_bytes));
   PG_CHECK_STATUS(c->new_row.ensure(n_markers));
-  PG_CUDA_CHECK(cudaMemcpy2DAsync(c->packed.p, pitch, packed, row_bytes, row_bytes, n_markers, cudaMemcpyHostToDevice,
-                                  c->stream));
+  PG_CHECK_STATUS(upload_rows(packed, n_markers, row_bytes, pitch, c->raw_rows, c->packed.p, c->stream));
   GenoBlock b;
   b.kind = PG_GENO_BED;
   b.data = c->packed.p;
@@ -800,8 +902,7 @@ int pg_decode_bgen(pg_ctx* c, const void* probs_and_ploidy, const uint8_t* unuse
   PG_CHECK_STATUS(c->packed.ensure(static_cast<size_t>(pitch) * n_markers));
   PG_CHECK_STATUS(c->full_out.ensure(static_cast<size_t>(n_markers) * n_samples * 8));
   PG_CHECK_STATUS(c->new_row.ensure(n_markers));
-  PG_CUDA_CHECK(cudaMemcpy2DAsync(c->packed.p, pitch, probs_and_ploidy, row_bytes, row_bytes, n_markers,
-                                  cudaMemcpyHostToDevice, c->stream));
+  PG_CHECK_STATUS(upload_rows(probs_and_ploidy, n_markers, row_bytes, pitch, c->raw_rows, c->packed.p, c->stream));
   GenoBlock b;
   b.kind = kind;
   b.data = c->packed.p;

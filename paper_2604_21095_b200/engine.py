@@ -303,39 +303,65 @@ def _run_scan_open(config: ScanConfig, source, wall0: float) -> ScanSummary:
         plan = plan_batches(source.n_markers, step)
         read_kw = {"dtype": dtype} if config.source.format.value == "dense" else {}
 
-        def read(span):
+        # pinned ring of 3 host buffers (PLINK) + 2 device staging slots: the read of batch
+        # i+1 and its H2D overlap the device scan of batch i
+        pinned = None
+        if hasattr(source, "bytes_per_marker"):
+            pinned = [_native.PinnedBuffer(step * source.bytes_per_marker) for _ in range(3)]
+
+        def read(i):
             t0 = time.perf_counter()
-            block = source.read_raw_block(span[0], span[1], **read_kw)
+            s0, c0 = plan[i]
+            if pinned is not None:
+                block = source.read_raw_block(s0, c0, out=pinned[i % 3].array)
+            else:
+                block = source.read_raw_block(s0, c0, **read_kw)
             return block, time.perf_counter() - t0
 
-        with ThreadPoolExecutor(max_workers=1) as reader:
-            nxt = reader.submit(read, plan[0])
-            for bi, (start, count) in enumerate(plan):
-                (kind, rows, row_bytes), dt_read = nxt.result()
-                t_decode += dt_read
-                if bi + 1 < len(plan):
-                    nxt = reader.submit(read, plan[bi + 1])
-                res = ctx.scan(kind, rows, row_bytes, full_elem_bytes=dtype.itemsize)
-                t_prepare += res.decode_ms / 1e3
-                t_corr += res.gemm_ms / 1e3
-                markers = tuple(source.marker_catalog[start:start + count])
-                batch = output.BatchStats(
-                    markers=markers, allele_frequency=res.af, missing_count=res.missing_count,
-                    skip_reason=res.skip, clamp_count=res.clamp_count, cand_rows=res.cand_rows,
-                    cand_cols=res.cand_cols, cand_r=res.cand_r, cand_t=res.cand_t, t_rows=res.t_rows,
-                    cand_p=res.cand_p,
-                )
-                clamp_total += res.clamp_count
-                skip_mono += int(np.count_nonzero(res.skip == SkipReason.MONOMORPHIC))
-                skip_missing += int(np.count_nonzero(res.skip == SkipReason.ALL_MISSING))
-                if config.qc_sidecar:
-                    for i in np.nonzero(res.skip)[0].tolist():
-                        qc_rows.append(f"marker\t{markers[i].id}\t{SkipReason(int(res.skip[i])).name}\n")
-                t0 = time.perf_counter()
-                writer.emit(batch)
-                t_emit += time.perf_counter() - t0
-                if config.output_mode is OutputMode.TOPK:
-                    ctx.set_rbar(topk_premask(writer.worst_abs_t, t_floor, df))
+        def finish(i, res):
+            nonlocal t_prepare, t_corr, t_emit, clamp_total, skip_mono, skip_missing
+            start, count = plan[i]
+            t_prepare += res.decode_ms / 1e3
+            t_corr += res.gemm_ms / 1e3
+            markers = tuple(source.marker_catalog[start:start + count])
+            batch = output.BatchStats(
+                markers=markers, allele_frequency=res.af, missing_count=res.missing_count,
+                skip_reason=res.skip, clamp_count=res.clamp_count, cand_rows=res.cand_rows,
+                cand_cols=res.cand_cols, cand_r=res.cand_r, cand_t=res.cand_t, t_rows=res.t_rows,
+                cand_p=res.cand_p,
+            )
+            clamp_total += res.clamp_count
+            skip_mono += int(np.count_nonzero(res.skip == SkipReason.MONOMORPHIC))
+            skip_missing += int(np.count_nonzero(res.skip == SkipReason.ALL_MISSING))
+            if config.qc_sidecar:
+                for j in np.nonzero(res.skip)[0].tolist():
+                    qc_rows.append(f"marker\t{markers[j].id}\t{SkipReason(int(res.skip[j])).name}\n")
+            t0 = time.perf_counter()
+            writer.emit(batch)
+            t_emit += time.perf_counter() - t0
+            if config.output_mode is OutputMode.TOPK:
+                ctx.set_rbar(topk_premask(writer.worst_abs_t, t_floor, df))
+
+        try:
+            staged: list = [None, None]
+            with ThreadPoolExecutor(max_workers=1) as reader:
+                fut = reader.submit(read, 0)
+                pending = None
+                for i in range(len(plan)):
+                    (kind, rows, row_bytes), dt_read = fut.result()
+                    t_decode += dt_read
+                    staged[i % 2] = ctx.stage(i % 2, kind, rows, row_bytes)
+                    if i + 1 < len(plan):
+                        fut = reader.submit(read, i + 1)
+                    if pending is not None:
+                        finish(pending, ctx.scan_staged(pending % 2, full_elem_bytes=dtype.itemsize))
+                    pending = i
+                finish(pending, ctx.scan_staged(pending % 2, full_elem_bytes=dtype.itemsize))
+        finally:
+            if pinned is not None:
+                ctx.sync()
+                for b in pinned:
+                    b.close()
     finally:
         ctx.close()
 

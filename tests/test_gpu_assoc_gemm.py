@@ -35,7 +35,7 @@ def _run(c_pad, p_pad, k_pad, seed=0):
     return x, ref
 
 
-@pytest.mark.parametrize("c_pad,p_pad,k_pad", [(256, 128, 64), (512, 256, 1024), (768, 384, 23040)])
+@pytest.mark.parametrize("c_pad,p_pad,k_pad", [(256, 256, 64), (512, 256, 1024), (768, 512, 23040)])
 def test_gemm_exact(c_pad, p_pad, k_pad):
     x, ref = _run(c_pad, p_pad, k_pad)
     assert torch.equal(x, ref)
