@@ -95,6 +95,15 @@ PG_API int pg_ctx_export_panel(pg_ctx* ctx, void* d_dst);
 PG_API int pg_ctx_import_panel(pg_ctx* ctx, const void* d_src, int64_t n_kept, int64_t n_pheno,
                         const int64_t* geno_row_index, int64_t n_samples_src);
 
+/* Extension mode (--residualize-genotypes; prepare_genotype_batch with
+ * residualize_genotypes=True, kernel.py:409-410): project every genotype row off the
+ * covariate basis Q (host f64 [n_kept, rank], kept-sample order, column 0 = the
+ * normalised intercept as built by build_covariate_basis). Because the panel is already
+ * orthogonal to Q only the per-marker variance changes: V_res = V - |Q^T g_c|^2, computed
+ * by an exact side GEMM of the genotype codes against the quantized basis. rank <= 1
+ * (or q == NULL) switches the extension off. Call after pg_ctx_set_panel. */
+PG_API int pg_ctx_set_basis(pg_ctx* ctx, const double* q, int64_t n_kept, int64_t rank);
+
 /* Scan parameters. `r_bar` (host f64 [n_pheno]) is the per-phenotype premask
  * bar on |r| — engine._abs_t_to_abs_r / premask_abs_r (engine.py:170-175,
  * 321-333) for THRESHOLD, the TopKWriter bar for TOPK (engine.py:205-211).

@@ -131,6 +131,13 @@ class DeviceContext:
             call("pg_ctx_set_scan", self._h, float(df), int(mode), ptr(rb))
             self.mode = mode
 
+    def set_basis(self, q: np.ndarray | None) -> None:
+        """Extension mode: residualize genotype rows against the covariate basis Q [n_kept, rank]."""
+        qq = None if q is None else np.ascontiguousarray(q, dtype=np.float64)
+        with self.lock:
+            call("pg_ctx_set_basis", self._h, ptr(qq), 0 if qq is None else qq.shape[0],
+                 0 if qq is None else qq.shape[1])
+
     def set_fused_decode(self, enable: bool) -> None:
         call("pg_ctx_set_fused_decode", self._h, 1 if enable else 0)
 

@@ -25,6 +25,7 @@ constexpr int64_t kQMax = kWH * 127 + 16192;  // largest |q| representable by th
 
 struct AssocEpilogue {
   int rows_per_marker;          // 1: row = u ; 2: rows = (u, missing mask)
+  int raw;                      // 1: emit s_p * (X - mu (Cq - Mq)) without the 1/den scale (side GEMM K5)
   int64_t m_valid;              // markers in this launch
   int64_t p_valid;              // phenotypes
   const float* mu_f;            // [markers] mean of u over observed kept samples

@@ -134,7 +134,7 @@ __device__ __forceinline__ void epilogue_tile(const AssocEpilogue& ep, uint32_t 
       }
       const int m = ct * kMarkersPerTile + (c + j) / R;
       const float mu = __ldg(ep.mu_f + m);
-      const float iv = __ldg(ep.invd_f + m);  // NaN for skipped / padding markers
+      const float iv = ep.raw ? 1.f : __ldg(ep.invd_f + m);  // NaN for skipped / padding markers
       const float xf = static_cast<float>(xu) - mu * (cq_f - static_cast<float>(xm));
       const float r = xf * sc_f * iv;
       const float ar = fabsf(r);
@@ -143,7 +143,7 @@ __device__ __forceinline__ void epilogue_tile(const AssocEpilogue& ep, uint32_t 
       double r64 = 0.0;
       if (hit || ep.full_r) {
         r64 = sc_d * (static_cast<double>(xu) - __ldg(ep.mu_d + m) * static_cast<double>(cq - xm)) *
-              __ldg(ep.invd_d + m);
+              (ep.raw ? 1.0 : __ldg(ep.invd_d + m));
       }
       if (ep.full_r) ep.full_r[static_cast<int64_t>(m) * ep.full_ld + pheno] = r64;
       const uint32_t mask = __ballot_sync(0xffffffffu, hit);

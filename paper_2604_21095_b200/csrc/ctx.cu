@@ -101,6 +101,30 @@ __global__ void repitch_kernel(const uint8_t* __restrict__ src, int64_t row_byte
   }
 }
 
+// Extension mode: V_res = V_u - sum_j w_j^2 with w = Q^T u_imp (side GEMM output),
+// then the reference's post-projection variance / skip rule (kernel.py:409-417).
+__global__ void resid_kernel(const double* __restrict__ w, int64_t ldw, int64_t n_cols, int64_t m,
+                             const long long* __restrict__ n_miss, const long long* __restrict__ s_u,
+                             const long long* __restrict__ ss_u, int64_t n_kept, double unit_scale, double* var,
+                             int8_t* skip, double* invd_d, float* invd_f) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= m || skip[i] == 2) return;
+  const long long n_obs = n_kept - n_miss[i];
+  const __int128 nv = static_cast<__int128>(n_obs) * ss_u[i] - static_cast<__int128>(s_u[i]) * s_u[i];
+  double v = static_cast<double>(nv) / static_cast<double>(n_obs);
+  for (int64_t j = 0; j < n_cols; ++j) {
+    const double x = w[i * ldw + j];
+    v -= x * x;
+  }
+  const double vr = v / static_cast<double>(n_kept) * unit_scale * unit_scale;
+  var[i] = vr;
+  const bool mono = !(vr > 1e-12);
+  skip[i] = mono ? 1 : 0;
+  const double inv = mono ? __longlong_as_double(0x7ff8000000000000ll) : 1.0 / sqrt(static_cast<double>(n_kept) * v);
+  invd_d[i] = inv;
+  invd_f[i] = static_cast<float>(inv);
+}
+
 __global__ void rbar_kernel(const double* rbar_in, int64_t n, int64_t p_pad, float* rbar_out) {
   const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (p >= p_pad) return;
@@ -175,6 +199,14 @@ struct pg_ctx {
   int last_R = 1;
   int64_t cand_capacity = 0;
   bool fused_decode = true;
+
+  // extension mode: quantized covariate basis (columns 1..rank-1) + side-GEMM output
+  bool have_basis = false;
+  int64_t basis_cols = 0;
+  pg::DBuf<int8_t> bq_h, bq_1, bq_0;
+  pg::DBuf<double> bscale_d, bmaxabs, bstage, wbuf;
+  pg::DBuf<float> bscale_f, bcq_f;
+  pg::DBuf<long long> bcq;
 };
 
 namespace pg {
@@ -246,6 +278,7 @@ int upload_panel_common(pg_ctx* c, const double* d_y, int64_t n_kept, int64_t n_
   PG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
   c->have_panel = true;
   c->have_scan = false;
+  c->have_basis = false;
   return PG_OK;
 }
 
@@ -319,10 +352,40 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
     PG_CHECK_STATUS(geno_planes(b, R, c->v.p, c->v127.p, c_pad, c->k_pad, s));
     ++launches;
   }
-  auto run_gemm = [&](const AssocEpilogue& e) -> int {
-    if (fused) return launch_assoc_packed(c->qh.p, c->q1.p, c->q0.p, c->p_pad, d_data, pitch, m, c->k_pad, e, s);
-    return launch_assoc(c->qh.p, c->q1.p, c->q0.p, c->p_pad, c->v.p, c->v127.p, c_pad, c->k_pad, e, s);
+  auto run_gemm_on = [&](const AssocEpilogue& e, const int8_t* a, const int8_t* b1, const int8_t* b0,
+                         int64_t pp) -> int {
+    if (fused) return launch_assoc_packed(a, b1, b0, pp, d_data, pitch, m, c->k_pad, e, s);
+    return launch_assoc(a, b1, b0, pp, c->v.p, c->v127.p, c_pad, c->k_pad, e, s);
   };
+  auto run_gemm = [&](const AssocEpilogue& e) -> int { return run_gemm_on(e, c->qh.p, c->q1.p, c->q0.p, c->p_pad); };
+  if (c->have_basis) {
+    // K5: w = Q^T u_imp for every marker (exact side GEMM against the quantized basis)
+    PG_CHECK_STATUS(c->wbuf.ensure(static_cast<size_t>(c_pad / R) * kTileP));
+    PG_CHECK_STATUS(c->cand_count.ensure(1));
+    AssocEpilogue eb{};
+    eb.rows_per_marker = R;
+    eb.raw = 1;
+    eb.m_valid = m;
+    eb.p_valid = c->basis_cols;
+    eb.mu_f = c->mu_f.p;
+    eb.mu_d = c->mu_d.p;
+    eb.invd_f = c->invd_f.p;
+    eb.invd_d = c->invd_d.p;
+    eb.scale_f = c->bscale_f.p;
+    eb.scale_d = c->bscale_d.p;
+    eb.cq_f = c->bcq_f.p;
+    eb.cq = c->bcq.p;
+    eb.rbar = nullptr;
+    eb.cand_count = c->cand_count.p;
+    eb.full_r = c->wbuf.p;
+    eb.full_ld = kTileP;
+    PG_CHECK_STATUS(run_gemm_on(eb, c->bq_h.p, c->bq_1.p, c->bq_0.p, kTileP));
+    resid_kernel<<<static_cast<unsigned>((m + 255) / 256), 256, 0, s>>>(
+        c->wbuf.p, kTileP, c->basis_cols, m, c->n_miss.p, c->s_u.p, c->ss_u.p, c->n_kept, geno_unit_scale(b),
+        c->var.p, c->skip.p, c->invd_d.p, c->invd_f.p);
+    PG_CUDA_CHECK(cudaGetLastError());
+    launches += 2;
+  }
   float decode_ms = 0.f;
 
   PG_CHECK_STATUS(c->counters.ensure(4));
@@ -617,6 +680,7 @@ int pg_ctx_import_panel(pg_ctx* c, const void* d_src, int64_t n_kept, int64_t n_
   PG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
   c->have_panel = true;
   c->have_scan = false;
+  c->have_basis = false;
   return PG_OK;
 }
 
@@ -642,6 +706,48 @@ int pg_ctx_set_scan(pg_ctx* c, double df, int mode, const double* r_bar) {
   }
   PG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
   c->have_scan = true;
+  return PG_OK;
+}
+
+int pg_ctx_set_basis(pg_ctx* c, const double* q, int64_t n_kept, int64_t rank) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(c->have_panel, PG_ERR_STATE, "pg_ctx_set_basis: set the panel first");
+  if (q == nullptr || rank <= 1) {
+    c->have_basis = false;
+    return PG_OK;
+  }
+  PG_REQUIRE(n_kept == c->n_kept, PG_ERR_INVALID, "pg_ctx_set_basis: %lld rows, panel has %lld kept samples",
+             (long long)n_kept, (long long)c->n_kept);
+  PG_REQUIRE(rank - 1 <= kTileP, PG_ERR_INVALID, "pg_ctx_set_basis: rank %lld > %d", (long long)rank, kTileP + 1);
+  const size_t plane = static_cast<size_t>(kTileP) * c->k_pad;
+  PG_CHECK_STATUS(c->bq_h.ensure(plane));
+  PG_CHECK_STATUS(c->bq_1.ensure(plane));
+  PG_CHECK_STATUS(c->bq_0.ensure(plane));
+  PG_CHECK_STATUS(c->bscale_d.ensure(kTileP));
+  PG_CHECK_STATUS(c->bscale_f.ensure(kTileP));
+  PG_CHECK_STATUS(c->bcq.ensure(kTileP));
+  PG_CHECK_STATUS(c->bcq_f.ensure(kTileP));
+  PG_CHECK_STATUS(c->bmaxabs.ensure(kTileP));
+  PG_CHECK_STATUS(c->bstage.ensure(static_cast<size_t>(n_kept) * rank));
+  PG_CUDA_CHECK(cudaMemcpyAsync(c->bstage.p, q, sizeof(double) * n_kept * rank, cudaMemcpyHostToDevice, c->stream));
+  PanelPlanes pp;
+  pp.qh = c->bq_h.p;
+  pp.q1 = c->bq_1.p;
+  pp.q0 = c->bq_0.p;
+  pp.scale_d = c->bscale_d.p;
+  pp.scale_f = c->bscale_f.p;
+  pp.cq = c->bcq.p;
+  pp.cq_f = c->bcq_f.p;
+  // columns 1..rank-1 (the intercept column contributes exactly 0 after centring)
+  PG_CHECK_STATUS(panel_quantize(c->bstage.p + 1, n_kept, rank - 1, rank, c->gidx.p, c->k_pad, kTileP, pp,
+                                 c->bmaxabs.p, c->stream));
+  // w_j = sum over ALL kept samples: no centring term (Cq = 0 in the epilogue formula)
+  PG_CUDA_CHECK(cudaMemsetAsync(c->bcq.p, 0, sizeof(long long) * kTileP, c->stream));
+  PG_CUDA_CHECK(cudaMemsetAsync(c->bcq_f.p, 0, sizeof(float) * kTileP, c->stream));
+  PG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  c->bstage.release();
+  c->basis_cols = rank - 1;
+  c->have_basis = true;
   return PG_OK;
 }
 

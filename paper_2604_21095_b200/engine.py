@@ -254,11 +254,6 @@ def run_scan(config: ScanConfig) -> ScanSummary:
 def _run_scan_open(config: ScanConfig, source, wall0: float) -> ScanSummary:
     from ._device import DeviceContext
 
-    if config.residualize_genotypes:
-        raise ConfigError(
-            "residualize_genotypes (extension mode) is not available on the device path yet; "
-            "run the paper-mode scan (residualize_genotypes=False)"
-        )
     prep = prepare_panel(config, source)
     n = prep.align.n_kept
     df = prep.df
@@ -286,6 +281,8 @@ def _run_scan_open(config: ScanConfig, source, wall0: float) -> ScanSummary:
         ctx.set_fused_decode(False)  # A/B switch; results are identical either way
     try:
         ctx.set_panel(prep.ytil, prep.align.genotype_row_index, source.n_samples)
+        if config.residualize_genotypes and prep.basis.rank:
+            ctx.set_basis(prep.basis.q)  # extension mode: side GEMM K5 for |Q^T g|^2
         t_floor = np.inf
         if config.output_mode is OutputMode.THRESHOLD:
             rbar = np.full(n_pheno, threshold_premask(config.p_threshold, df))

@@ -175,3 +175,39 @@ def test_c1_fused_decode_matches_planes_bitwise(c1, tmp_path, monkeypatch):
     monkeypatch.setenv("PANELGWAS_FUSED_DECODE", "0")
     _scan(c1, tmp_path / "planes.bin", output_mode=pg.OutputMode.FULL, precision=pg.Precision.F64, device_batch=3000)
     assert (tmp_path / "fused.bin").read_bytes() == (tmp_path / "planes.bin").read_bytes()
+
+
+def test_s1_extension_mode_residualized_genotypes(s1, tmp_path):
+    """--residualize-genotypes + adjusted df (the FWL / `validate --exact` mode): side GEMM K5."""
+    g = np.load(GOLD / "s1.npz")
+    _scan(s1, tmp_path / "adj.tsv", p_threshold=1.0, precision=pg.Precision.F64, df_mode=pg.DfMode.ADJUSTED,
+          residualize_genotypes=True)
+    a = _arrays(tmp_path / "adj.tsv")
+    assert np.array_equal(a["rows"], g["adj_f64_rows"]) and np.array_equal(a["cols"], g["adj_f64_cols"])
+    _assert_close_t_p(a["t"], g["adj_f64_t"], a["p"], g["adj_f64_p"])
+    rel = np.max(np.abs(a["t"] - g["adj_f64_t"]) / np.maximum(1, np.abs(g["adj_f64_t"])))
+    assert rel < 1e-5
+
+
+def test_fwl_matches_full_ols(tmp_path):
+    """Extension mode equals full OLS y ~ 1 + C + g (reference tests/test_engine.py:417-432)."""
+    rng = np.random.default_rng(19)
+    n = 30
+    af = rng.uniform(0.2, 0.8, size=10)
+    d = rng.binomial(2, af[:, None], size=(10, n)).astype(np.float64)
+    y = rng.standard_normal((n, 2))
+    covar = rng.standard_normal((n, 2))
+    y[:, 0] += covar @ [0.8, -0.5]
+    ids = [f"S{i + 1}" for i in range(n)]
+    bed, bim, fam = pg.write_bed_trio(tmp_path / "g", d, ids)
+    from conftest_helpers import write_tsv
+
+    pheno = write_tsv(tmp_path / "p.tsv", ids, ["ph1", "ph2"], y)
+    cov = write_tsv(tmp_path / "c.tsv", ids, ["cv1", "cv2"], covar)
+    spec = pg.SourceSpec(pg.GenotypeFormat.PLINK_BED, bed_path=bed, bim_path=bim, fam_path=fam)
+    pg.run_scan(pg.ScanConfig(source=spec, pheno_path=pheno, covar_path=cov, out_path=tmp_path / "o.tsv",
+                              p_threshold=1.0, df_mode=pg.DfMode.ADJUSTED, residualize_genotypes=True,
+                              precision=pg.Precision.F64, summary_to_stderr=False))
+    for rec in pg.load_association_records(tmp_path / "o.tsv"):
+        ref = pg.ols_single(y[:, int(rec.phenotype[2:]) - 1], d[rec.pos - 1], covar)
+        assert rec.t == pytest.approx(ref.t, abs=1e-5)
