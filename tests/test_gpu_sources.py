@@ -1,0 +1,82 @@
+"""Device scans over BGEN (8/16-bit, missing calls: balanced-ternary rows + missing
+row) and dense NPY sources vs reference goldens and vs the PLINK path."""
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2604_21095_b200 as pg
+from conftest_helpers import write_tsv
+
+pytestmark = pytest.mark.gpu
+GOLD = Path(__file__).parent / "golden"
+
+
+def _records(path):
+    recs = pg.load_association_records(path)
+    return recs, np.array([r.t for r in recs]), np.array([r.p for r in recs])
+
+
+@pytest.mark.parametrize("bits", [8, 16])
+def test_bgen_scan_matches_reference(bits, tmp_path):
+    g = np.load(GOLD / "bgen.npz")
+    spec = pg.SourceSpec(pg.GenotypeFormat.BGEN, bgen_path=GOLD / f"bgen{bits}.bgen")
+    pg.run_scan(pg.ScanConfig(source=spec, pheno_path=GOLD / "bgen_pheno.tsv", out_path=tmp_path / "o.tsv",
+                              p_threshold=1.0, precision=pg.Precision.F64, summary_to_stderr=False))
+    recs, t, p = _records(tmp_path / "o.tsv")
+    rows = np.array([int(r.id[2:]) - 1 for r in recs])
+    cols = np.array([int(r.phenotype[2:]) - 1 for r in recs])
+    assert np.array_equal(rows, g[f"b{bits}_rows"]) and np.array_equal(cols, g[f"b{bits}_cols"])
+    assert all((r.counted_allele, r.other_allele) == ("B", "A") for r in recs)  # BGEN counts allele2
+    np.testing.assert_allclose([r.af for r in recs], g[f"b{bits}_af"], rtol=1e-12)
+    dt = np.abs(t - g[f"b{bits}_t"]) / np.maximum(1, np.abs(g[f"b{bits}_t"]))
+    assert dt.max() <= 1e-5
+    lp, lr = -np.log10(p), -np.log10(g[f"b{bits}_p"])
+    assert (np.abs(lp - lr) / np.maximum(1, lr)).max() <= 1e-4
+
+
+def test_dense_integral_equals_plink_exactly(tmp_path):
+    rng = np.random.default_rng(24)
+    d = rng.integers(0, 3, size=(40, 50)).astype(np.float64)
+    d[rng.random(d.shape) < 0.05] = np.nan
+    y = rng.standard_normal((50, 3))
+    ids = [f"S{i + 1}" for i in range(50)]
+    bed, bim, fam = pg.write_bed_trio(tmp_path / "g", d, ids)
+    pheno = write_tsv(tmp_path / "p.tsv", ids, ["ph1", "ph2", "ph3"], y)
+    np.save(tmp_path / "g.npy", d.T)
+    (tmp_path / "s.txt").write_text("\n".join(ids) + "\n")
+    plink = pg.SourceSpec(pg.GenotypeFormat.PLINK_BED, bed_path=bed, bim_path=bim, fam_path=fam)
+    dense = pg.SourceSpec(pg.GenotypeFormat.DENSE, dense_path=tmp_path / "g.npy", sample_id_path=tmp_path / "s.txt",
+                          dense_orientation=pg.DenseOrientation.SAMPLES_BY_MARKERS)
+    for spec, out in ((plink, "a.tsv"), (dense, "b.tsv")):
+        pg.run_scan(pg.ScanConfig(source=spec, pheno_path=pheno, out_path=tmp_path / out, p_threshold=1.0,
+                                  precision=pg.Precision.F64, summary_to_stderr=False))
+    a = pg.load_association_records(tmp_path / "a.tsv")
+    b = pg.load_association_records(tmp_path / "b.tsv")
+    assert len(a) == len(b)
+    for ra, rb in zip(a, b):  # same integers through the same exact contraction -> identical bits
+        assert (ra.t, ra.p, ra.r, ra.af, ra.missing_count) == (rb.t, rb.p, rb.r, rb.af, rb.missing_count)
+
+
+def test_dense_fractional_dosages(tmp_path):
+    """Real-valued dosages take the 2^-17 fixed-point ternary path; compare with the oracle."""
+    from oracle import scan_oracle as orc
+
+    rng = np.random.default_rng(31)
+    m, n, k = 25, 64, 4
+    d = np.clip(rng.binomial(2, 0.4, size=(m, n)) + rng.normal(0, 0.15, size=(m, n)), 0, 2)
+    d[rng.random(d.shape) < 0.04] = np.nan
+    y = rng.standard_normal((n, k))
+    ids = [f"S{i + 1}" for i in range(n)]
+    pheno = write_tsv(tmp_path / "p.tsv", ids, [f"ph{j + 1}" for j in range(k)], y)
+    np.save(tmp_path / "g.npy", d)
+    (tmp_path / "s.txt").write_text("\n".join(ids) + "\n")
+    spec = pg.SourceSpec(pg.GenotypeFormat.DENSE, dense_path=tmp_path / "g.npy", sample_id_path=tmp_path / "s.txt")
+    pg.run_scan(pg.ScanConfig(source=spec, pheno_path=pheno, out_path=tmp_path / "o.tsv", p_threshold=1.0,
+                              precision=pg.Precision.F64, summary_to_stderr=False))
+    recs, t, _ = _records(tmp_path / "o.tsv")
+    ytil, _ = orc.standardized_panel(y, orc.covariate_basis(np.zeros((n, 0))))
+    want = orc.threshold_scan(d, ytil, float(n - 2), 1.0)
+    assert len(recs) == want["t"].size
+    dt = np.abs(t - want["t"]) / np.maximum(1, np.abs(want["t"]))
+    assert dt.max() <= 1e-4
