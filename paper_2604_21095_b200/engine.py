@@ -137,6 +137,7 @@ class ScanSummary:
     time_emit_s: float
     wall_s: float
     exclusion_log: dict[str, int] = field(default_factory=dict)
+    phenotype_names: list[str] = field(default_factory=list)  # not serialized (engine extension)
 
     _KEYS = (
         "n_markers", "n_samples_source", "n_samples_used", "markers_scanned", "markers_skipped_monomorphic",
@@ -240,18 +241,23 @@ def prepare_panel(config: ScanConfig, source) -> _PreparedPanel:
     return _PreparedPanel(ytil, basis, names, zero_variance, panel, align, df)
 
 
-def run_scan(config: ScanConfig) -> ScanSummary:
-    """Execute a full scan on the GPU and write results plus the summary files."""
+def run_scan(config: ScanConfig, marker_range: tuple[int, int] | None = None, panel_hook=None) -> ScanSummary:
+    """Execute a full scan on the GPU and write results plus the summary files.
+
+    marker_range / panel_hook are used by the multi-GPU driver (distributed.py): scan only
+    markers [start, stop) of the source, and obtain the resident panel through
+    `panel_hook(ctx, prep)` (NCCL broadcast from rank 0) instead of uploading it.
+    """
     wall0 = time.perf_counter()
     config.validate()
     source = open_genotype_source(config.source)
     try:
-        return _run_scan_open(config, source, wall0)
+        return _run_scan_open(config, source, wall0, marker_range, panel_hook)
     finally:
         source.close()
 
 
-def _run_scan_open(config: ScanConfig, source, wall0: float) -> ScanSummary:
+def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, panel_hook=None) -> ScanSummary:
     from ._device import DeviceContext
 
     prep = prepare_panel(config, source)
@@ -280,7 +286,10 @@ def _run_scan_open(config: ScanConfig, source, wall0: float) -> ScanSummary:
     if os.environ.get("PANELGWAS_FUSED_DECODE", "1") == "0":
         ctx.set_fused_decode(False)  # A/B switch; results are identical either way
     try:
-        ctx.set_panel(prep.ytil, prep.align.genotype_row_index, source.n_samples)
+        if panel_hook is not None:
+            panel_hook(ctx, prep)
+        else:
+            ctx.set_panel(prep.ytil, prep.align.genotype_row_index, source.n_samples)
         if config.residualize_genotypes and prep.basis.rank:
             ctx.set_basis(prep.basis.q)  # extension mode: side GEMM K5 for |Q^T g|^2
         t_floor = np.inf
@@ -296,8 +305,9 @@ def _run_scan_open(config: ScanConfig, source, wall0: float) -> ScanSummary:
         skip_mono = skip_missing = clamp_total = 0
         t_decode = t_prepare = t_corr = t_emit = 0.0
         qc_rows: list[str] = []
-        step = device_batch_size(config, source.n_markers, n_pheno)
-        plan = plan_batches(source.n_markers, step)
+        lo, hi = marker_range if marker_range is not None else (0, source.n_markers)
+        step = device_batch_size(config, hi - lo, n_pheno)
+        plan = [(lo + s0, c0) for s0, c0 in plan_batches(hi - lo, step)]
         read_kw = {"dtype": dtype} if config.source.format.value == "dense" else {}
 
         # pinned ring of 3 host buffers (PLINK) + 2 device staging slots: the read of batch
@@ -373,11 +383,12 @@ def _run_scan_open(config: ScanConfig, source, wall0: float) -> ScanSummary:
             for j in np.nonzero(prep.zero_variance)[0].tolist():
                 fh.write(f"phenotype\t{prep.panel.phenotype_names[j]}\tZERO_VARIANCE\n")
 
+    n_scanned_range = (marker_range[1] - marker_range[0]) if marker_range is not None else source.n_markers
     summary = ScanSummary(
-        n_markers=source.n_markers,
+        n_markers=n_scanned_range,
         n_samples_source=source.n_samples,
         n_samples_used=n,
-        markers_scanned=source.n_markers - skip_mono - skip_missing,
+        markers_scanned=n_scanned_range - skip_mono - skip_missing,
         markers_skipped_monomorphic=skip_mono,
         markers_skipped_all_missing=skip_missing,
         phenotypes_total=prep.panel.n_phenotypes,
@@ -393,6 +404,7 @@ def _run_scan_open(config: ScanConfig, source, wall0: float) -> ScanSummary:
         time_emit_s=t_emit,
         wall_s=time.perf_counter() - wall0,
         exclusion_log=dict(prep.align.exclusion_log),
+        phenotype_names=list(names),
     )
     with open(Path(str(config.out_path) + ".summary.json"), "w") as fh:
         json.dump(summary.to_dict(), fh, indent=2, sort_keys=True)

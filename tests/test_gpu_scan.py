@@ -211,3 +211,38 @@ def test_fwl_matches_full_ols(tmp_path):
     for rec in pg.load_association_records(tmp_path / "o.tsv"):
         ref = pg.ols_single(y[:, int(rec.phenotype[2:]) - 1], d[rec.pos - 1], covar)
         assert rec.t == pytest.approx(ref.t, abs=1e-5)
+
+
+def test_two_shard_flow_equals_single_gpu(s1, tmp_path):
+    """The multi-GPU flow (panel export -> broadcast bytes -> import; contiguous marker
+    shards; rank-order merge) run as two sequential 'ranks' on one GPU: byte-identical
+    to the single scan."""
+    import torch
+
+    from paper_2604_21095_b200 import distributed
+
+    spec = pg.SourceSpec(pg.GenotypeFormat.PLINK_BED, bed_path=s1["bed_path"], bim_path=s1["bim_path"],
+                         fam_path=s1["fam_path"])
+    base = dict(source=spec, pheno_path=s1["pheno_path"], covar_path=s1["covar_path"], p_threshold=1e-2,
+                precision=pg.Precision.F64, summary_to_stderr=False)
+    pg.run_scan(pg.ScanConfig(out_path=tmp_path / "single.tsv", **base))
+    exported = {}
+
+    def hook0(ctx, prep):
+        ctx.set_panel(prep.ytil, prep.align.genotype_row_index, 300)
+        buf = torch.empty(ctx.panel_bytes(), dtype=torch.uint8, device="cuda")
+        ctx.export_panel(buf.data_ptr())
+        exported["buf"] = buf
+
+    def hook1(ctx, prep):
+        ctx.import_panel(exported["buf"].data_ptr(), prep.ytil.shape[0], prep.ytil.shape[1],
+                         prep.align.genotype_row_index, 300)
+
+    shards = []
+    for rank, hook in ((0, hook0), (1, hook1)):
+        lo, hi = distributed.shard_span(600, 2, rank)
+        out = distributed.shard_path(tmp_path / "multi.tsv", rank)
+        pg.run_scan(pg.ScanConfig(out_path=out, **base), marker_range=(lo, hi), panel_hook=hook)
+        shards.append(out)
+    distributed.merge_tsv(shards, tmp_path / "multi.tsv")
+    assert (tmp_path / "multi.tsv").read_bytes() == (tmp_path / "single.tsv").read_bytes()
