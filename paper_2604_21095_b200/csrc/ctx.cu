@@ -599,8 +599,9 @@ int pg_ctx_set_panel(pg_ctx* c, const double* ytil, int64_t n_kept, int64_t n_ph
     PG_CUDA_CHECK(cudaMemcpy2DAsync(c->ystage.p, sizeof(double) * n_pheno, ytil, sizeof(double) * ld,
                                     sizeof(double) * n_pheno, n_kept, cudaMemcpyHostToDevice, c->stream));
   }
+  // the f64 staging buffer stays allocated: re-uploading a panel (e.g. per scan in a
+  // service) must not pay a multi-GB cudaMalloc/cudaFree each time
   PG_CHECK_STATUS(upload_panel_common(c, c->ystage.p, n_kept, n_pheno, n_pheno, geno_row_index, n_samples_src));
-  c->ystage.release();
   return PG_OK;
 }
 
