@@ -1,0 +1,219 @@
+"""Engine behaviour on the device, following the reference engine / CLI test
+strategy (tests/test_engine.py, tests/test_cli.py): record order and
+contract, premask == brute-force filter, TOPK selection and ties, FULL payload and
+budget guard, invariances, accounting, keep/remove, df modes, missing policies,
+OLS equivalence, CLI subcommands and exit codes."""
+import json
+
+import numpy as np
+import pytest
+
+import paper_2604_21095_b200 as pg
+from conftest_helpers import write_tsv
+from paper_2604_21095_b200 import cli
+
+pytestmark = pytest.mark.gpu
+
+
+def dataset(tmp_path, d, y, covar=None, subdir="data"):
+    root = tmp_path / subdir
+    root.mkdir(parents=True, exist_ok=True)
+    n = d.shape[1]
+    ids = [f"S{i + 1}" for i in range(n)]
+    bed, bim, fam = pg.write_bed_trio(root / "geno", d, ids)
+    pheno = write_tsv(root / "pheno.tsv", ids, [f"ph{j + 1}" for j in range(y.shape[1])], y)
+    cov = write_tsv(root / "covar.tsv", ids, [f"cv{j + 1}" for j in range(covar.shape[1])], covar) \
+        if covar is not None else None
+    spec = pg.SourceSpec(pg.GenotypeFormat.PLINK_BED, bed_path=bed, bim_path=bim, fam_path=fam)
+    return spec, pheno, cov, root
+
+
+def scan(spec, pheno, out, covar=None, **kw):
+    kw.setdefault("summary_to_stderr", False)
+    return pg.run_scan(pg.ScanConfig(source=spec, pheno_path=pheno, out_path=out, covar_path=covar, **kw))
+
+
+def random_dataset(rng, m, n, p, maf=(0.2, 0.8)):
+    af = rng.uniform(*maf, size=m)
+    return rng.binomial(2, af[:, None], size=(m, n)).astype(np.float64), rng.standard_normal((n, p))
+
+
+def test_open_threshold_emits_all_pairs_in_order(tmp_path):
+    d, y = random_dataset(np.random.default_rng(0), 20, 30, 4)
+    spec, pheno, _, root = dataset(tmp_path, d, y)
+    s = scan(spec, pheno, root / "out.tsv", p_threshold=1.0)
+    recs = pg.load_association_records(root / "out.tsv")
+    assert len(recs) == s.markers_scanned * s.phenotypes_scanned == s.records_emitted
+    keys = [(r.pos, r.phenotype) for r in recs]
+    assert keys == sorted(keys)
+    rec = recs[0]
+    assert (rec.n, rec.df, rec.counted_allele, rec.other_allele) == (30, 28, "A", "B")
+
+
+@pytest.mark.parametrize("thr,planted", [(0.2, False), (1e-6, True)])
+def test_premask_equals_bruteforce(tmp_path, thr, planted):
+    rng = np.random.default_rng(2 if not planted else 27)
+    d, y = random_dataset(rng, 40 if not planted else 30, 50 if not planted else 200, 6 if not planted else 3)
+    if planted:
+        y[:, 0] += 0.8 * d[4]
+        y[:, 2] -= 0.9 * d[17]
+    spec, pheno, _, root = dataset(tmp_path, d, y)
+    scan(spec, pheno, root / "all.tsv", p_threshold=1.0, precision=pg.Precision.F64)
+    scan(spec, pheno, root / "cut.tsv", p_threshold=thr, precision=pg.Precision.F64)
+    full = pg.load_association_records(root / "all.tsv")
+    expected = {(r.id, r.phenotype) for r in full if r.p <= thr}
+    assert expected or not planted
+    assert {(r.id, r.phenotype) for r in pg.load_association_records(root / "cut.tsv")} == expected
+
+
+def test_topk_matches_bruteforce_and_ties(tmp_path):
+    d, y = random_dataset(np.random.default_rng(5), 25, 30, 3)
+    spec, pheno, _, root = dataset(tmp_path, d, y)
+    scan(spec, pheno, root / "all.tsv", p_threshold=1.0, precision=pg.Precision.F64, device_batch=7)
+    scan(spec, pheno, root / "top.tsv", output_mode=pg.OutputMode.TOPK, top_k=4, precision=pg.Precision.F64,
+         device_batch=7)
+    full = pg.load_association_records(root / "all.tsv")
+    by = {}
+    for r in full:
+        by.setdefault(r.phenotype, []).append(r)
+    expected = set()
+    for name, recs in by.items():
+        recs.sort(key=lambda r: (r.p, r.pos))
+        expected |= {(r.id, name) for r in recs[:4]}
+    assert {(r.id, r.phenotype) for r in pg.load_association_records(root / "top.tsv")} == expected
+    # duplicated marker rows: identical p, the earlier source index wins
+    rng = np.random.default_rng(6)
+    row = rng.binomial(2, 0.5, size=20).astype(np.float64)
+    d2 = np.vstack([row, rng.binomial(2, 0.5, size=(6, 20)).astype(np.float64), row])
+    spec, pheno, _, root = dataset(tmp_path, d2, rng.standard_normal((20, 1)), subdir="dup")
+    scan(spec, pheno, root / "top.tsv", output_mode=pg.OutputMode.TOPK, top_k=d2.shape[0] - 1)
+    ids = [r.id for r in pg.load_association_records(root / "top.tsv")]
+    assert len(ids) == d2.shape[0] - 1
+    assert "snp1" in ids and ("snp8" not in ids or ids.index("snp1") < ids.index("snp8"))
+
+
+def test_full_payload_budget_and_f32(tmp_path):
+    d, y = random_dataset(np.random.default_rng(7), 12, 30, 3)
+    d[4] = 2.0
+    spec, pheno, _, root = dataset(tmp_path, d, y)
+    s = scan(spec, pheno, root / "full.bin", output_mode=pg.OutputMode.FULL, precision=pg.Precision.F64)
+    t, lines, names = pg.read_full_matrix(root / "full.bin")
+    assert t.shape == (11, 3) and names == ["ph1", "ph2", "ph3"] and s.records_emitted == 33
+    assert not any(x.split("\t")[2] == "snp5" for x in lines)
+    scan(spec, pheno, root / "f32.bin", output_mode=pg.OutputMode.FULL)
+    assert pg.read_full_matrix(root / "f32.bin")[0].dtype == np.dtype("<f4")
+    with pytest.raises(pg.ConfigError, match="budget"):
+        scan(spec, pheno, root / "b.bin", output_mode=pg.OutputMode.FULL, full_byte_budget=10)
+    scan(spec, pheno, root / "b.bin", output_mode=pg.OutputMode.FULL, full_byte_budget=10, allow_large_full=True)
+    # FULL t == THRESHOLD t for every pair
+    scan(spec, pheno, root / "thr.tsv", p_threshold=1.0, precision=pg.Precision.F64)
+    lookup = {(r.id, r.phenotype): r.t for r in pg.load_association_records(root / "thr.tsv")}
+    for line, row in zip(lines, t):
+        for j, name in enumerate(names):
+            assert row[j] == lookup[(line.split("\t")[2], name)]
+
+
+def test_invariances(tmp_path):
+    rng = np.random.default_rng(13)
+    d, y = random_dataset(rng, 33, 40, 4)
+    y[rng.random(y.shape) < 0.05] = np.nan
+    spec, pheno, cov, root = dataset(tmp_path, d, y, covar=rng.standard_normal((40, 2)))
+    outs = []
+    for workers, db in ((1, 5), (2, 33), (8, 1)):
+        out = root / f"w{workers}.tsv"
+        scan(spec, pheno, out, covar=cov, p_threshold=1.0, precision=pg.Precision.F64, worker_count=workers,
+             device_batch=db)
+        outs.append(out.read_bytes())
+    assert outs[0] == outs[1] == outs[2]
+    scan(spec, pheno, root / "f32.tsv", covar=cov, p_threshold=1.0)
+    a = pg.load_association_records(root / "w1.tsv")
+    b = pg.load_association_records(root / "f32.tsv")
+    assert all(abs(ra.t - rb.t) <= 1e-4 * max(1.0, abs(ra.t)) for ra, rb in zip(a, b))
+
+
+def test_accounting_qc_keep_remove_and_df(tmp_path):
+    rng = np.random.default_rng(16)
+    d, y = random_dataset(rng, 15, 30, 3)
+    d[2] = 0.0
+    d[9] = np.nan
+    y[:, 1] = 42.0
+    spec, pheno, _, root = dataset(tmp_path, d, y)
+    s = scan(spec, pheno, root / "out.tsv", p_threshold=1.0, qc_sidecar=True)
+    assert (s.markers_skipped_monomorphic, s.markers_skipped_all_missing, s.markers_scanned) == (1, 1, 13)
+    assert (s.phenotypes_skipped_zero_variance, s.phenotypes_scanned, s.records_emitted) == (1, 2, 26)
+    blob = json.loads((root / "out.tsv.summary.json").read_text())
+    assert blob["markers_scanned"] == 13 and blob["records_emitted"] == 26
+    qc = (root / "out.tsv.qc.tsv").read_text()
+    assert "snp3\tMONOMORPHIC" in qc and "snp10\tALL_MISSING" in qc and "ph2\tZERO_VARIANCE" in qc
+    d, y = random_dataset(np.random.default_rng(17), 6, 12, 2)
+    spec, pheno, _, root = dataset(tmp_path, d, y, subdir="kr")
+    (root / "keep.txt").write_text("".join(f"S{i}\n" for i in range(1, 11)))
+    (root / "remove.txt").write_text("S1\nS2\n")
+    s = scan(spec, pheno, root / "o.tsv", p_threshold=1.0, keep_path=root / "keep.txt",
+             remove_path=root / "remove.txt", precision=pg.Precision.F64)
+    assert s.n_samples_used == 8 and s.exclusion_log["remove-listed"] == 2
+    rec = pg.load_association_records(root / "o.tsv")[0]
+    assert rec.n == 8
+    # kept-sample subset: same t as OLS on the kept rows only
+    keep = np.array([i for i in range(12) if f"S{i + 1}" not in {"S1", "S2", "S11", "S12"}])
+    for r in pg.load_association_records(root / "o.tsv"):
+        ref = pg.ols_single(y[keep, int(r.phenotype[2:]) - 1], d[r.pos - 1, keep])
+        assert r.t == pytest.approx(ref.t, abs=1e-5)
+    d, y = random_dataset(np.random.default_rng(18), 8, 30, 2)
+    spec, pheno, cov, root = dataset(tmp_path, d, y, covar=np.random.default_rng(1).standard_normal((30, 3)),
+                                     subdir="df")
+    scan(spec, pheno, root / "o.tsv", covar=cov, p_threshold=1.0, df_mode=pg.DfMode.ADJUSTED)
+    assert pg.load_association_records(root / "o.tsv")[0].df == 30 - 4 - 1
+
+
+def test_paper_df_matches_ols_and_missing_policy(tmp_path):
+    rng = np.random.default_rng(20)
+    d, y = random_dataset(rng, 12, 25, 3)
+    spec, pheno, _, root = dataset(tmp_path, d, y)
+    scan(spec, pheno, root / "out.tsv", p_threshold=1.0, precision=pg.Precision.F64)
+    for rec in pg.load_association_records(root / "out.tsv"):
+        ref = pg.ols_single(y[:, int(rec.phenotype[2:]) - 1], d[rec.pos - 1])
+        assert rec.t == pytest.approx(ref.t, abs=1e-5)
+        assert rec.p == pytest.approx(ref.p, rel=1e-4)
+    d, y = random_dataset(np.random.default_rng(21), 5, 20, 2)
+    y[3, 0] = np.nan
+    spec, pheno, _, root = dataset(tmp_path, d, y, subdir="mp")
+    assert scan(spec, pheno, root / "o.tsv", p_threshold=1.0).records_emitted > 0
+    with pytest.raises(pg.PanelGwasError, match="missing"):
+        scan(spec, pheno, root / "o2.tsv", p_threshold=1.0, missing_policy=pg.MissingPolicy.FAIL)
+
+
+class TestCli:
+    def test_run_bench_validate_convert(self, tmp_path, capsys):
+        d, y = random_dataset(np.random.default_rng(3), 20, 40, 2)
+        spec, pheno, _, root = dataset(tmp_path, d, y)
+        prefix = root / "geno"
+        assert cli.main(["run", "--bfile", str(prefix), "--pheno", str(pheno), "--out", str(root / "o.tsv"),
+                         "--p-threshold", "1"]) == 0
+        assert len(pg.load_association_records(root / "o.tsv")) == 40
+        capsys.readouterr()
+        assert cli.main(["bench", "--simulate", "--n-samples", "200", "--n-markers", "500", "--n-phenotypes", "8",
+                         "--out-dir", str(tmp_path / "b")]) == 0
+        keys = dict(line.split("=", 1) for line in capsys.readouterr().out.split())
+        assert int(keys["tests"]) == 500 * 8 - 8 * (int(keys["markers_skipped_monomorphic"]))
+        assert float(keys["tests_per_second"]) > 0
+        assert cli.main(["validate", "--simulate", "--out-dir", str(tmp_path / "v")]) == 0
+        assert "PASS" in capsys.readouterr().out
+        assert cli.main(["validate", "--simulate", "--exact", "--out-dir", str(tmp_path / "vx")]) == 0
+        assert "PASS" in capsys.readouterr().out
+        assert cli.main(["convert", "--bfile", str(prefix), "--to", "dense", "--out", str(root / "conv")]) == 0
+        arr = np.load(root / "conv.npy")
+        assert np.array_equal(np.nan_to_num(arr, nan=-1), np.nan_to_num(d, nan=-1))
+
+    def test_usage_errors_exit_2(self, tmp_path):
+        with pytest.raises(SystemExit) as e:
+            cli.main(["run", "--pheno", "p", "--out", "o"])
+        assert e.value.code == 2
+        with pytest.raises(SystemExit) as e:
+            cli.main(["run", "--bfile", "x", "--pheno", "p", "--out", "o", "--full", "--top-k", "3"])
+        assert e.value.code == 2
+
+    def test_error_exit_1(self, tmp_path, capsys):
+        assert cli.main(["run", "--bfile", str(tmp_path / "nope"), "--pheno", str(tmp_path / "p.tsv"),
+                         "--out", str(tmp_path / "o.tsv")]) == 1
+        assert "missing file" in capsys.readouterr().err
