@@ -181,6 +181,17 @@ PG_API int pg_reg_inc_beta(pg_ctx* ctx, const double* a, const double* b, const 
 /* kernel.t_threshold_for_p (kernel.py:212-235) */
 PG_API int pg_t_threshold_for_p(pg_ctx* ctx, double p_threshold, double df, double* t_crit);
 
+/* ---- native TSV emitter (host code; output.py:50-52, 106-113) ---- */
+/* Python repr(float) of each value, one per line ('\n'-terminated). */
+PG_API int pg_format_float_repr(const double* x, int64_t n, char* out, int64_t out_cap, int64_t* out_len);
+/* THRESHOLD / TOPK record lines, byte-identical to the reference writer: per record
+ * <prefix[row]>AF\tN_MISS<mid>R\tT\tP\t<pheno[col]>\n with repr() floats. prefix / pheno
+ * strings are given as blobs + offset arrays (n_rows+1 / n_pheno+1 entries). */
+PG_API int pg_format_tsv(int64_t n, const int64_t* rows, const int64_t* cols, const double* r, const double* t,
+                         const double* p, const double* af, const int64_t* n_miss, const char* prefix_blob,
+                         const int64_t* prefix_off, const char* pheno_blob, const int64_t* pheno_off,
+                         const char* mid, int64_t mid_len, char* out, int64_t out_cap, int64_t* out_len);
+
 /* ---- genotype decode on the device (host arrays in/out) ---- */
 /* PlinkSource.read_marker_batch / decode_bed_codes (plink.py:48-61, 167-185):
  * rows of `row_bytes` packed codes -> dosages (elem 4: f32, 8: f64) [n_markers, n_samples]

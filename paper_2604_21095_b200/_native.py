@@ -87,6 +87,8 @@ SIGNATURES: dict[str, list] = {
     "pg_decode_bgen": [_P, _P, _P, c_int64, c_int64, c_int, _P, _P],
     "pg_prepare_batch": [_P, _P, c_int64, c_int64, _P, c_int64, c_int, _P, _P, _P, _P, _P],
     "pg_correlate_f64": [_P, _P, c_int64, c_int64, _P, c_int64, _P, _P],
+    "pg_format_float_repr": [_P, c_int64, _P, c_int64, _P],
+    "pg_format_tsv": [c_int64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, c_int64, _P, c_int64, _P],
     "pg_debug_assoc_gemm": [_P, _P, _P, c_int64, _P, _P, c_int64, c_int64, _P, _P],
 }
 

@@ -63,3 +63,47 @@ def test_sm100a_only_binary():
     assert "UTCIMMA" in sass  # tcgen05.mma kind::i8
     assert "UTMALDG" in sass  # TMA tile loads
     assert "LDTM" in sass     # tcgen05.ld
+
+
+def test_native_float_repr_matches_python():
+    import ctypes
+
+    import numpy as np
+
+    from paper_2604_21095_b200 import _native
+
+    rng = np.random.default_rng(11)
+    vals = np.concatenate([
+        rng.standard_normal(2000) * 10.0 ** rng.integers(-30, 30, 2000),
+        np.array([0.0, -0.0, 1.0, -1.0, 1e16, 1e17, 9999999999999998.0, 1e-4, 1e-5, 0.0001234, 123456789.0,
+                  5e-324, 1.7976931348623157e308, 2.2250738585072014e-308, np.inf, -np.inf, np.nan, 0.1, 1 / 3]),
+        rng.random(2000),
+    ])
+    cap = vals.size * 40
+    out = ctypes.create_string_buffer(cap)
+    n = ctypes.c_int64(0)
+    _native.call("pg_format_float_repr", vals.ctypes.data, vals.size, out, cap, ctypes.byref(n))
+    got = out.raw[:n.value].decode().split("\n")[:-1]
+    assert got == [repr(float(v)) for v in vals]
+
+
+def test_native_tsv_lines_match_python_formatting():
+    import numpy as np
+
+    import paper_2604_21095_b200 as pg
+    from paper_2604_21095_b200 import output
+
+    rng = np.random.default_rng(5)
+    markers = [pg.MarkerRecord(str(1 + i % 3), f"rs{i}", 100 * i + 1, "A", "GT", i) for i in range(7)]
+    names = ["height", "bmi_z", "phéno"]
+    w = output.ThresholdWriter.__new__(output.ThresholdWriter)
+    output._Writer.__init__(w, 812.0, 815, False, names)
+    rows = rng.integers(0, 7, 50)
+    cols = rng.integers(0, 3, 50)
+    r, t, p = rng.standard_normal(50) / 10, rng.standard_normal(50) * 5, rng.random(50) ** 8
+    af = rng.random(7)
+    miss = rng.integers(0, 9, 7)
+    text = output.format_records(markers, af, miss, rows, cols, r, t, p, w._pheno_blob, w._pheno_off, w._tail, False)
+    want = "".join(w._line(markers[i], af[i], int(miss[i]), names[j], r[k], t[k], p[k])
+                   for k, (i, j) in enumerate(zip(rows.tolist(), cols.tolist())))
+    assert text == want
