@@ -10,8 +10,9 @@ markers per GPU, THRESHOLD hit compaction at p <= 1e-4).
 A step scans the rank's whole marker shard (M markers) against the resident
 panel and returns the hits: value = (markers x phenotypes over all ranks) /
 (max over ranks of the device time of K steps). `e2e` times the same through
-the host-buffer C-ABI path (panel upload + NCCL broadcast + pinned .bed rows
-H2D inside the step). Data are synthetic of the paper's shape (random-init
+the host-buffer C-ABI path (raw panel upload + device prep + NCCL broadcast + pinned .bed rows
+H2D inside the step; the panel enters raw (phenotypes + 10 covariates) and is
+residualized, standardized and quantized on the device). Data are synthetic of the paper's shape (random-init
 genotypes Binomial(2, AF), AF ~ U(0.05, 0.95); Gaussian phenotypes
 standardized like the reference panel). Inputs (5.75 GB packed genotypes,
 1.4 GB quantized panel) are far larger than the 126 MB L2.
@@ -34,6 +35,7 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
+N_COVARIATES = 10
 METRIC = "association tests/sec (N=23k, P=20,480) at 1/2/4/8 B200; % bf16 tensor peak"
 
 
@@ -226,6 +228,7 @@ def our_arm(a) -> None:
     from paper_2604_21095_b200 import _native, build as _build
     from paper_2604_21095_b200._device import DeviceContext
     from paper_2604_21095_b200.engine import threshold_premask
+    from paper_2604_21095_b200.kernel import build_covariate_basis
 
     world, rank, local = dist_env()
     if world > 1:
@@ -242,11 +245,17 @@ def our_arm(a) -> None:
     gidx = np.arange(n, dtype=np.int64)
     ytil = synth_panel(torch, n, p, a.seed, dev) if rank == 0 else None
 
-    def distribute_panel(from_host: np.ndarray | None):
-        """rank 0 uploads + quantizes; panel limbs broadcast once over NCCL; others import."""
+    def distribute_panel(raw_host=None):
+        """rank 0 builds the resident panel; its limbs are broadcast once over NCCL; others import.
+
+        raw_host = (Y [N, P], C [N, c]) host arrays: the public path (covariate basis on the
+        host, residualize + standardize + quantize on the device: engine.stage_panel)."""
         if rank == 0:
-            if from_host is not None:
-                ctx.set_panel(from_host, gidx, n)
+            if raw_host is not None:
+                y_raw, c_raw = raw_host
+                basis = build_covariate_basis(c_raw, True)
+                flat, _sd = ctx.prepare_panel(y_raw, basis.q)
+                ctx.commit_panel(np.nonzero(~flat)[0], gidx, n)
             else:
                 ctx.set_panel_device(ytil.data_ptr(), n, p, p, gidx, n)
         if world > 1:
@@ -349,16 +358,21 @@ def our_arm(a) -> None:
         host_rows = torch.empty((m, bpm), dtype=torch.uint8, pin_memory=True)
         host_rows.copy_(packed[:, :bpm])
         host_np = host_rows.numpy()
-        y_host = None
+        raw = None
         if rank == 0:
+            # raw phenotypes of the C3 shape: Y = C gamma + noise, 10 covariates
+            gen = torch.Generator(device=dev).manual_seed(a.seed + 2000)
+            c_dev = torch.randn(n, N_COVARIATES, generator=gen, device=dev, dtype=torch.float64)
+            gamma = 0.1 * torch.randn(N_COVARIATES, p, generator=gen, device=dev, dtype=torch.float64)
             yh = torch.empty((n, p), dtype=torch.float64, pin_memory=True)
-            yh.copy_(ytil)
-            y_host = yh.numpy()
+            yh.copy_(c_dev @ gamma + torch.randn(n, p, generator=gen, device=dev, dtype=torch.float64))
+            raw = (yh.numpy(), c_dev.cpu().numpy())
+            del c_dev, gamma
         del packed
         torch.cuda.empty_cache()
 
         def e2e_step():
-            h2d = distribute_panel(y_host) + (n * p * 8 if rank == 0 else 0)
+            h2d = distribute_panel(raw) + (n * (p + N_COVARIATES + 1) * 8 if rank == 0 else 0)
             ctx.set_scan(df, _native.PG_MODE_THRESHOLD, rbar)
             d2h = 0
             # public host-buffer C-ABI path, pipelined: H2D of batch i+1 overlaps the scan of batch i

@@ -43,6 +43,8 @@ extern "C" {
 #define PG_ERR_NOMEM 4
 #define PG_ERR_STATE 5
 #define PG_ERR_CONFIG 6
+/* not an error: pg_table_parse needs the generic (csv-module) path for this input */
+#define PG_TABLE_GENERIC 100
 
 /* Output modes (engine.py:41-44). */
 #define PG_MODE_THRESHOLD 0
@@ -75,8 +77,29 @@ PG_API int pg_ctx_sync(pg_ctx* ctx);
 /* The ctx's cudaStream_t (as void*), for callers that time or order work on it. */
 PG_API int pg_ctx_stream(pg_ctx* ctx, void** stream);
 
+/* Device panel preparation: the reference's residualize + standardize_columns
+ * (kernel.py:310-347, driven by engine.py:259-279) in fp64 on the GPU.
+ *   y             host f64 [n_kept, ld] row-major (kept samples x phenotypes, missing
+ *                 values already handled by the panel's missing policy)
+ *   basis_q       host f64 [n_kept, rank] row-major orthonormal covariate basis
+ *                 (kernel.build_covariate_basis; rank 0 = centring only)
+ *   zero_variance out u8 [n_pheno]: 1 where sd <= 1e-12 max(1, |centre|) (kernel.py:344)
+ *   sd            out f64 [n_pheno] (may be NULL)
+ * The standardized panel stays on the device; pg_ctx_commit_panel quantizes the kept
+ * columns into the resident limbs (same result as pg_ctx_set_panel on the host-prepared
+ * matrix up to 1e-16 relative rounding). Non-finite input -> PG_ERR_INVALID. */
+PG_API int pg_ctx_prepare_panel(pg_ctx* ctx, const double* y, int64_t n_kept, int64_t n_pheno, int64_t ld,
+                                const double* basis_q, int64_t rank, uint8_t* zero_variance, double* sd);
+/* Quantize prepared columns kept_cols[0..n_cols) (engine.py:271-279 drops zero-variance
+ * columns) into the resident panel; geometry as pg_ctx_set_panel. */
+PG_API int pg_ctx_commit_panel(pg_ctx* ctx, const int64_t* kept_cols, int64_t n_cols,
+                               const int64_t* geno_row_index, int64_t n_samples_src);
+/* Copy the prepared (standardized, uncompacted) panel back: out f64 [n_kept, n_pheno]. */
+PG_API int pg_ctx_fetch_prepared_panel(pg_ctx* ctx, double* out);
+
 /* Upload the standardized phenotype panel once; it stays resident in HBM as
- * fp16 hi/lo planes [P_pad, K_pad] plus fp64 column sums.
+ * three int8 limb planes [P_pad, K_pad] (q = 32385 qH + 127 q1 + q0, 23-bit
+ * per-phenotype quantization) plus per-phenotype scale and limb-sum vectors.
  * Replaces: engine._run_scan_open panel hand-off (engine.py:269-279) — the
  * `ytil` produced by kernel.standardize_columns (kernel.py:330-347).
  *   ytil            host f64, row i = kept sample i, `ld` elements per row
@@ -180,6 +203,20 @@ PG_API int pg_p_from_t(pg_ctx* ctx, const double* t, int64_t n, double df, doubl
 PG_API int pg_reg_inc_beta(pg_ctx* ctx, const double* a, const double* b, const double* x, int64_t n, double* out);
 /* kernel.t_threshold_for_p (kernel.py:212-235) */
 PG_API int pg_t_threshold_for_p(pg_ctx* ctx, double p_threshold, double df, double* t_crit);
+
+/* Native table-body parser (host). Replaces the cell loop of
+ * phenotypes.load_table (phenotypes.py:67-138): records after the header line
+ * (starting at byte body_offset, physical line number first_lineno), cells split on
+ * `delim`, blank lines skipped, ID cell (field id_field) stripped, value cells ->
+ * NaN for {"", "NA", "NaN", "nan", "-9"}, Python float() otherwise, unparseable or
+ * non-finite -> NaN counted per column. Call once with values == NULL to get *n_rows,
+ * then with values [n_rows, n_fields-1], id_off/id_len [n_rows] (byte ranges into buf),
+ * missing/unparseable [n_fields-1]. A ragged record -> PG_ERR_FORMAT with *err_line /
+ * *err_cells; PG_TABLE_GENERIC when quoting, '\r', non-ASCII or '_' appear. */
+PG_API int pg_table_parse(const char* buf, int64_t len, int64_t body_offset, char delim, int64_t n_fields,
+                          int64_t id_field, int n_threads, int64_t first_lineno, int64_t* n_rows, double* values,
+                          int64_t* id_off, int64_t* id_len, int64_t* missing, int64_t* unparseable,
+                          int64_t* err_line, int64_t* err_cells);
 
 /* ---- native TSV emitter (host code; output.py:50-52, 106-113) ---- */
 /* Python repr(float) of each value, one per line ('\n'-terminated). */

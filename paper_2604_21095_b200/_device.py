@@ -103,6 +103,42 @@ class DeviceContext:
                  int(n_samples_src))
             self.n_pheno = y.shape[1]
 
+    def prepare_panel(self, y: np.ndarray, basis_q: np.ndarray | None) -> tuple[np.ndarray, np.ndarray]:
+        """Residualize + standardize the kept-sample panel on the device (kernel.py:310-347).
+
+        Returns (zero_variance flags, sd); the standardized panel stays on the device
+        until commit_panel() quantizes its kept columns."""
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        if y.ndim != 2:
+            raise ValueError("expected a 2-D (samples x phenotypes) matrix")
+        n, p = y.shape
+        q = None
+        rank = 0
+        if basis_q is not None and basis_q.shape[1]:
+            q = np.ascontiguousarray(basis_q, dtype=np.float64)
+            if q.shape[0] != n:
+                raise ValueError(f"row count {n} does not match basis ({q.shape[0]} samples)")
+            rank = q.shape[1]
+        flat = np.zeros(p, dtype=np.uint8)
+        sd = np.zeros(p, dtype=np.float64)
+        with self.lock:
+            call("pg_ctx_prepare_panel", self._h, ptr(y), n, p, p, ptr(q), rank, ptr(flat), ptr(sd))
+            self._prep_shape = (n, p)
+        return flat.astype(bool), sd
+
+    def fetch_prepared_panel(self) -> np.ndarray:
+        out = np.empty(self._prep_shape, dtype=np.float64)
+        with self.lock:
+            call("pg_ctx_fetch_prepared_panel", self._h, ptr(out))
+        return out
+
+    def commit_panel(self, kept_cols: np.ndarray, geno_row_index: np.ndarray, n_samples_src: int) -> None:
+        cols = np.ascontiguousarray(kept_cols, dtype=np.int64)
+        gidx = np.ascontiguousarray(geno_row_index, dtype=np.int64)
+        with self.lock:
+            call("pg_ctx_commit_panel", self._h, ptr(cols), cols.size, ptr(gidx), int(n_samples_src))
+            self.n_pheno = int(cols.size)
+
     def set_panel_device(self, d_ptr: int, n_kept: int, n_pheno: int, ld: int, geno_row_index: np.ndarray,
                          n_samples_src: int) -> None:
         gidx = np.ascontiguousarray(geno_row_index, dtype=np.int64)

@@ -19,6 +19,7 @@ from .errors import ConfigError, FormatError, PanelGwasError
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libpanelgwas_b200.so"
 
 PG_OK = 0
+PG_TABLE_GENERIC = 100
 PG_ERR_CUDA = 1
 PG_ERR_INVALID = 2
 PG_ERR_FORMAT = 3
@@ -63,6 +64,9 @@ SIGNATURES: dict[str, list] = {
     "pg_ctx_sync": [_P],
     "pg_ctx_stream": [_P, _P],
     "pg_ctx_set_panel": [_P, _P, c_int64, c_int64, c_int64, _P, c_int64],
+    "pg_ctx_prepare_panel": [_P, _P, c_int64, c_int64, c_int64, _P, c_int64, _P, _P],
+    "pg_ctx_commit_panel": [_P, _P, c_int64, _P, c_int64],
+    "pg_ctx_fetch_prepared_panel": [_P, _P],
     "pg_ctx_set_panel_device": [_P, _P, c_int64, c_int64, c_int64, _P, c_int64],
     "pg_ctx_panel_bytes": [_P, _P],
     "pg_ctx_export_panel": [_P, _P],
@@ -87,6 +91,8 @@ SIGNATURES: dict[str, list] = {
     "pg_decode_bgen": [_P, _P, _P, c_int64, c_int64, c_int, _P, _P],
     "pg_prepare_batch": [_P, _P, c_int64, c_int64, _P, c_int64, c_int, _P, _P, _P, _P, _P],
     "pg_correlate_f64": [_P, _P, c_int64, c_int64, _P, c_int64, _P, _P],
+    "pg_table_parse": [_P, c_int64, c_int64, ctypes.c_char, c_int64, c_int64, c_int, c_int64, _P, _P, _P, _P, _P,
+                       _P, _P, _P],
     "pg_format_float_repr": [_P, c_int64, _P, c_int64, _P],
     "pg_format_tsv": [c_int64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, c_int64, _P, c_int64, _P],
     "pg_debug_assoc_gemm": [_P, _P, _P, c_int64, _P, _P, c_int64, c_int64, _P, _P],

@@ -156,6 +156,13 @@ struct pg_ctx {
   pg::DBuf<int64_t> gidx;
   pg::DBuf<uint32_t> keep_bits;
   pg::DBuf<double> ystage;
+  // device panel preparation (pg_ctx_prepare_panel -> pg_ctx_commit_panel)
+  bool have_prepared = false;
+  int64_t prep_rows = 0, prep_cols = 0;
+  pg::DBuf<double> prep_q, prep_scratch, prep_mean, prep_centre, prep_sd;
+  pg::DBuf<uint8_t> prep_flat;
+  pg::DBuf<int> prep_bad;
+  pg::DBuf<int64_t> colmap;
 
   // scan parameters
   double df = 1.0;
@@ -234,7 +241,7 @@ int ctx_check(pg_ctx* c) {
 }
 
 int upload_panel_common(pg_ctx* c, const double* d_y, int64_t n_kept, int64_t n_pheno, int64_t ld,
-                        const int64_t* h_gidx, int64_t n_src) {
+                        const int64_t* h_gidx, int64_t n_src, const int64_t* d_cols = nullptr) {
   PG_REQUIRE(n_kept >= 1 && n_pheno >= 1 && n_src >= n_kept && ld >= n_pheno, PG_ERR_INVALID,
              "invalid panel geometry n_kept=%lld n_pheno=%lld n_src=%lld", (long long)n_kept, (long long)n_pheno,
              (long long)n_src);
@@ -274,7 +281,8 @@ int upload_panel_common(pg_ctx* c, const double* d_y, int64_t n_kept, int64_t n_
   pp.scale_f = c->scale_f.p;
   pp.cq = c->cq.p;
   pp.cq_f = c->cq_f.p;
-  PG_CHECK_STATUS(panel_quantize(d_y, n_kept, n_pheno, ld, c->gidx.p, c->k_pad, c->p_pad, pp, c->maxabs.p, c->stream));
+  PG_CHECK_STATUS(
+      panel_quantize(d_y, n_kept, n_pheno, ld, d_cols, c->gidx.p, c->k_pad, c->p_pad, pp, c->maxabs.p, c->stream));
   PG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
   c->have_panel = true;
   c->have_scan = false;
@@ -605,6 +613,76 @@ int pg_ctx_set_panel(pg_ctx* c, const double* ytil, int64_t n_kept, int64_t n_ph
   return PG_OK;
 }
 
+int pg_ctx_prepare_panel(pg_ctx* c, const double* y, int64_t n_kept, int64_t n_pheno, int64_t ld,
+                         const double* basis_q, int64_t rank, uint8_t* zero_variance, double* sd) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(y != nullptr && zero_variance != nullptr && (rank == 0 || basis_q != nullptr), PG_ERR_INVALID,
+             "pg_ctx_prepare_panel: null input");
+  PG_REQUIRE(n_kept >= 1 && n_pheno >= 1 && ld >= n_pheno && rank >= 0, PG_ERR_INVALID,
+             "pg_ctx_prepare_panel: bad shape");
+  cudaStream_t s = c->stream;
+  PG_CHECK_STATUS(c->ystage.ensure(static_cast<size_t>(n_kept) * n_pheno));
+  if (ld == n_pheno) {
+    PG_CUDA_CHECK(cudaMemcpyAsync(c->ystage.p, y, sizeof(double) * n_pheno * n_kept, cudaMemcpyHostToDevice, s));
+  } else {
+    PG_CUDA_CHECK(cudaMemcpy2DAsync(c->ystage.p, sizeof(double) * n_pheno, y, sizeof(double) * ld,
+                                    sizeof(double) * n_pheno, n_kept, cudaMemcpyHostToDevice, s));
+  }
+  if (rank > 0) {
+    PG_CHECK_STATUS(c->prep_q.ensure(static_cast<size_t>(n_kept) * rank));
+    PG_CUDA_CHECK(cudaMemcpyAsync(c->prep_q.p, basis_q, sizeof(double) * n_kept * rank, cudaMemcpyHostToDevice, s));
+  }
+  PG_CHECK_STATUS(c->prep_scratch.ensure(pg::panel_prep_scratch_doubles(n_kept, n_pheno, rank)));
+  for (auto* b : {&c->prep_mean, &c->prep_centre, &c->prep_sd}) PG_CHECK_STATUS(b->ensure(n_pheno));
+  PG_CHECK_STATUS(c->prep_flat.ensure(n_pheno));
+  PG_CHECK_STATUS(c->prep_bad.ensure(1));
+  pg::PanelPrepOut po;
+  po.mean = c->prep_mean.p;
+  po.centre = c->prep_centre.p;
+  po.sd = c->prep_sd.p;
+  po.flat = c->prep_flat.p;
+  po.bad = c->prep_bad.p;
+  PG_CHECK_STATUS(pg::panel_prepare(c->ystage.p, n_kept, n_pheno, rank ? c->prep_q.p : nullptr, rank,
+                                    c->prep_scratch.p, po, s));
+  int bad = 0;
+  PG_CUDA_CHECK(cudaMemcpyAsync(&bad, c->prep_bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  PG_CUDA_CHECK(cudaMemcpyAsync(zero_variance, c->prep_flat.p, n_pheno, cudaMemcpyDeviceToHost, s));
+  if (sd) PG_CUDA_CHECK(cudaMemcpyAsync(sd, c->prep_sd.p, sizeof(double) * n_pheno, cudaMemcpyDeviceToHost, s));
+  PG_CUDA_CHECK(cudaStreamSynchronize(s));
+  c->have_prepared = false;
+  PG_REQUIRE(!bad, PG_ERR_INVALID, "standardize_columns requires finite input");
+  c->have_prepared = true;
+  c->prep_rows = n_kept;
+  c->prep_cols = n_pheno;
+  return PG_OK;
+}
+
+int pg_ctx_fetch_prepared_panel(pg_ctx* c, double* out) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(c->have_prepared, PG_ERR_STATE, "no prepared panel (pg_ctx_prepare_panel)");
+  PG_REQUIRE(out != nullptr, PG_ERR_INVALID, "null output");
+  PG_CUDA_CHECK(cudaMemcpyAsync(out, c->ystage.p, sizeof(double) * c->prep_rows * c->prep_cols,
+                                cudaMemcpyDeviceToHost, c->stream));
+  PG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  return PG_OK;
+}
+
+int pg_ctx_commit_panel(pg_ctx* c, const int64_t* kept_cols, int64_t n_cols, const int64_t* geno_row_index,
+                        int64_t n_samples_src) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(c->have_prepared, PG_ERR_STATE, "pg_ctx_commit_panel: no prepared panel (pg_ctx_prepare_panel)");
+  PG_REQUIRE(kept_cols != nullptr && geno_row_index != nullptr && n_cols >= 1, PG_ERR_INVALID,
+             "pg_ctx_commit_panel: null input or no columns");
+  for (int64_t i = 0; i < n_cols; ++i)
+    PG_REQUIRE(kept_cols[i] >= 0 && kept_cols[i] < c->prep_cols, PG_ERR_INVALID,
+               "pg_ctx_commit_panel: column %lld out of range", (long long)kept_cols[i]);
+  PG_CHECK_STATUS(c->colmap.ensure(n_cols));
+  PG_CUDA_CHECK(
+      cudaMemcpyAsync(c->colmap.p, kept_cols, sizeof(int64_t) * n_cols, cudaMemcpyHostToDevice, c->stream));
+  return upload_panel_common(c, c->ystage.p, c->prep_rows, n_cols, c->prep_cols, geno_row_index, n_samples_src,
+                             c->colmap.p);
+}
+
 int pg_ctx_set_panel_device(pg_ctx* c, const double* d_ytil, int64_t n_kept, int64_t n_pheno, int64_t ld,
                             const int64_t* geno_row_index, int64_t n_samples_src) {
   PG_CHECK_STATUS(ctx_check(c));
@@ -740,7 +818,7 @@ int pg_ctx_set_basis(pg_ctx* c, const double* q, int64_t n_kept, int64_t rank) {
   pp.cq = c->bcq.p;
   pp.cq_f = c->bcq_f.p;
   // columns 1..rank-1 (the intercept column contributes exactly 0 after centring)
-  PG_CHECK_STATUS(panel_quantize(c->bstage.p + 1, n_kept, rank - 1, rank, c->gidx.p, c->k_pad, kTileP, pp,
+  PG_CHECK_STATUS(panel_quantize(c->bstage.p + 1, n_kept, rank - 1, rank, nullptr, c->gidx.p, c->k_pad, kTileP, pp,
                                  c->bmaxabs.p, c->stream));
   // w_j = sum over ALL kept samples: no centring term (Cq = 0 in the epilogue formula)
   PG_CUDA_CHECK(cudaMemsetAsync(c->bcq.p, 0, sizeof(long long) * kTileP, c->stream));

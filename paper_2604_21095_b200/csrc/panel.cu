@@ -19,14 +19,15 @@ namespace pg {
 namespace {
 
 __global__ void maxabs_kernel(const double* __restrict__ y, int64_t n_rows, int64_t n_cols, int64_t ld,
-                              double* __restrict__ maxabs) {
+                              const int64_t* __restrict__ cols, double* __restrict__ maxabs) {
   // blockDim (32, 8): 32 consecutive columns x 8 row-strands
   __shared__ double red[8][33];
   const int64_t col = blockIdx.x * 32 + threadIdx.x;
   double m = 0.0;
   if (col < n_cols) {
+    const int64_t src = cols ? cols[col] : col;
     for (int64_t r = blockIdx.y * 8 + threadIdx.y; r < n_rows; r += gridDim.y * 8) {
-      m = fmax(m, fabs(y[r * ld + col]));
+      m = fmax(m, fabs(y[r * ld + src]));
     }
   }
   red[threadIdx.y][threadIdx.x] = m;
@@ -56,7 +57,7 @@ __device__ __forceinline__ long long floor_div(long long a, long long b) {
 
 // 32x32 transpose tiles: read y[i, p] coalesced along p, write limb[p][g_idx[i]].
 __global__ void quantize_kernel(const double* __restrict__ y, int64_t n_rows, int64_t n_cols, int64_t ld,
-                                const int64_t* __restrict__ g_idx, const double* __restrict__ scale_d,
+                                const int64_t* __restrict__ cols, const int64_t* __restrict__ g_idx, const double* __restrict__ scale_d,
                                 int64_t k_pad, int8_t* __restrict__ qh, int8_t* __restrict__ q1,
                                 int8_t* __restrict__ q0, unsigned long long* __restrict__ cq) {
   __shared__ int tile_h[32][33], tile_1[32][33], tile_0[32][33];
@@ -68,7 +69,7 @@ __global__ void quantize_kernel(const double* __restrict__ y, int64_t n_rows, in
     const int64_t r = row0 + yy, c = col0 + tx;
     long long q = 0;
     if (r < n_rows && c < n_cols) {
-      const double v = y[r * ld + c] / scale_d[c];
+      const double v = y[r * ld + (cols ? cols[c] : c)] / scale_d[c];
       q = llrint(v);
       if (q > kQMax) q = kQMax;
       if (q < -kQMax) q = -kQMax;
@@ -109,8 +110,9 @@ __global__ void cq_float_kernel(const long long* __restrict__ cq, int64_t p_pad,
 
 }  // namespace
 
-int panel_quantize(const double* d_y, int64_t n_rows, int64_t n_cols, int64_t ld, const int64_t* d_gidx,
-                   int64_t k_pad, int64_t p_pad, PanelPlanes& out, double* d_maxabs_scratch, cudaStream_t st) {
+int panel_quantize(const double* d_y, int64_t n_rows, int64_t n_cols, int64_t ld, const int64_t* d_cols,
+                   const int64_t* d_gidx, int64_t k_pad, int64_t p_pad, PanelPlanes& out, double* d_maxabs_scratch,
+                   cudaStream_t st) {
   const size_t plane = static_cast<size_t>(p_pad) * k_pad;
   PG_CUDA_CHECK(cudaMemsetAsync(out.qh, 0, plane, st));
   PG_CUDA_CHECK(cudaMemsetAsync(out.q1, 0, plane, st));
@@ -121,7 +123,7 @@ int panel_quantize(const double* d_y, int64_t n_rows, int64_t n_cols, int64_t ld
     dim3 blk(32, 8);
     const int64_t gy = std::min<int64_t>((n_rows + 7) / 8, 256);
     dim3 grd(static_cast<unsigned>((n_cols + 31) / 32), static_cast<unsigned>(gy));
-    maxabs_kernel<<<grd, blk, 0, st>>>(d_y, n_rows, n_cols, ld, d_maxabs_scratch);
+    maxabs_kernel<<<grd, blk, 0, st>>>(d_y, n_rows, n_cols, ld, d_cols, d_maxabs_scratch);
     PG_CUDA_CHECK(cudaGetLastError());
   }
   scale_kernel<<<static_cast<unsigned>((p_pad + 255) / 256), 256, 0, st>>>(d_maxabs_scratch, n_cols, p_pad,
@@ -130,7 +132,7 @@ int panel_quantize(const double* d_y, int64_t n_rows, int64_t n_cols, int64_t ld
   {
     dim3 blk(32, 8);
     dim3 grd(static_cast<unsigned>((n_cols + 31) / 32), static_cast<unsigned>((n_rows + 31) / 32));
-    quantize_kernel<<<grd, blk, 0, st>>>(d_y, n_rows, n_cols, ld, d_gidx, out.scale_d, k_pad, out.qh, out.q1, out.q0,
+    quantize_kernel<<<grd, blk, 0, st>>>(d_y, n_rows, n_cols, ld, d_cols, d_gidx, out.scale_d, k_pad, out.qh, out.q1, out.q0,
                                          reinterpret_cast<unsigned long long*>(out.cq));
     PG_CUDA_CHECK(cudaGetLastError());
   }

@@ -1,0 +1,214 @@
+// Native parser for the body of a phenotype / covariate table (host code).
+//
+// Semantics of the reference loader (/root/reference/pkg/src/panelgwas/phenotypes.py:67-138):
+//   * one record per line; blank lines are skipped; every other line must have exactly
+//     n_fields delimiter-separated cells ("ragged row" error with its 1-based line number);
+//   * the ID cell is whitespace-stripped;
+//   * a value cell is stripped, then: in {"", "NA", "NaN", "nan", "-9"} -> NaN (missing);
+//     otherwise parsed like Python float(); unparseable or non-finite -> NaN and counted as
+//     unparseable for its column (the reference's fast numpy path gives the same values
+//     whenever it is taken, so the cell rule is the whole contract).
+// Inputs the simple grammar cannot decide byte-for-byte like Python's csv module + float()
+// (quote characters, a bare '\r', non-ASCII bytes, digit-group underscores) make the
+// parser report PG_TABLE_GENERIC so the caller can use the csv-module path instead.
+//
+// Work is split over lines (one sample per line, tens of thousands of cells each) across
+// host threads; the first ragged line is found deterministically (minimum over threads).
+#include <algorithm>
+#include <atomic>
+#include <charconv>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "pg_common.cuh"
+
+namespace pg {
+namespace {
+
+inline bool is_space(unsigned char c) {
+  // ASCII characters Python's str.strip() removes
+  return c == ' ' || (c >= '\t' && c <= '\r') || (c >= 0x1c && c <= 0x1f);
+}
+
+inline bool is_missing_token(const char* s, size_t n) {
+  switch (n) {
+    case 0: return true;
+    case 2: return s[0] == 'N' && s[1] == 'A';
+    case 3:
+      return (s[0] == 'N' && s[1] == 'a' && s[2] == 'N') || (s[0] == 'n' && s[1] == 'a' && s[2] == 'n');
+    default: return false;
+  }
+}
+
+inline bool is_minus_nine(const char* s, size_t n) { return n == 2 && s[0] == '-' && s[1] == '9'; }
+
+// Python float() on an ASCII token without underscores -> (value, ok). ok=false means
+// ValueError; non-finite results are returned as such.
+inline bool py_float(const char* s, size_t n, double& out) {
+  const char* b = s;
+  const char* e = s + n;
+  bool neg = false;
+  if (b < e && (*b == '+' || *b == '-')) {
+    neg = *b == '-';
+    ++b;
+    if (b < e && (*b == '+' || *b == '-')) return false;
+  }
+  if (b == e) return false;
+  double v = 0.0;
+  auto r = std::from_chars(b, e, v, std::chars_format::general);
+  if (r.ptr != e) {
+    return false;
+  }
+  if (r.ec == std::errc::result_out_of_range) {
+    // over/underflow: strtod gives Python's result (0.0, a subnormal, or +-inf)
+    std::string tmp(b, e);
+    v = std::strtod(tmp.c_str(), nullptr);
+  } else if (r.ec != std::errc()) {
+    return false;
+  }
+  out = neg ? -v : v;
+  return true;
+}
+
+struct Line {
+  int64_t begin, end;  // [begin, end) without the line terminator
+  int64_t lineno;      // 1-based physical line number
+};
+
+}  // namespace
+}  // namespace pg
+
+extern "C" {
+
+// Returns PG_OK, PG_TABLE_GENERIC (caller must use the generic path) or an error.
+// Two calls: values == NULL -> *n_rows = number of records (after ragged-row checks);
+// then with buffers sized n_rows x (n_fields - 1) / n_rows / (n_fields - 1).
+int pg_table_parse(const char* buf, int64_t len, int64_t body_offset, char delim, int64_t n_fields, int64_t id_field,
+                   int n_threads, int64_t first_lineno, int64_t* n_rows, double* values, int64_t* id_off,
+                   int64_t* id_len, int64_t* missing, int64_t* unparseable, int64_t* err_line, int64_t* err_cells) {
+  using pg::Line;
+  PG_REQUIRE(buf != nullptr || len == 0, PG_ERR_INVALID, "pg_table_parse: null buffer");
+  PG_REQUIRE(n_fields >= 1 && id_field >= 0 && id_field < n_fields, PG_ERR_INVALID, "pg_table_parse: bad fields");
+  *err_line = 0;
+  *err_cells = 0;
+  // ---- lines (sequential memchr; lines are long, so this is a small share of the time)
+  std::vector<Line> lines;
+  int64_t pos = body_offset, lineno = first_lineno;
+  while (pos < len) {
+    const void* nl = std::memchr(buf + pos, '\n', static_cast<size_t>(len - pos));
+    int64_t end = nl ? static_cast<const char*>(nl) - buf : len;
+    int64_t stop = end;
+    if (stop > pos && buf[stop - 1] == '\r') --stop;
+    lines.push_back({pos, stop, lineno});
+    pos = end + 1;
+    ++lineno;
+  }
+  const int64_t n_lines = static_cast<int64_t>(lines.size());
+  int nt = n_threads > 0 ? n_threads : static_cast<int>(std::thread::hardware_concurrency());
+  nt = std::max(1, std::min<int>(nt, 64));
+  if (n_lines < 4 * nt) nt = std::max<int64_t>(1, n_lines / 4);
+  const int64_t n_val = n_fields - 1;
+
+  // ---- pass 1: generic-path triggers, blank lines, field counts
+  std::vector<int64_t> cells_of(n_lines, 0);
+  std::atomic<bool> generic{false};
+  {
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t) {
+      th.emplace_back([&, t] {
+        for (int64_t i = t; i < n_lines; i += nt) {
+          const Line& L = lines[i];
+          int64_t cells = 1;
+          for (int64_t k = L.begin; k < L.end; ++k) {
+            const unsigned char c = static_cast<unsigned char>(buf[k]);
+            if (c == static_cast<unsigned char>(delim)) {
+              ++cells;
+            } else if (c == '"' || c == '\r' || c >= 0x80 || c == '_' || c == 0) {
+              generic.store(true, std::memory_order_relaxed);
+            }
+          }
+          cells_of[i] = L.end == L.begin ? 0 : cells;  // csv.reader yields [] for an empty line
+        }
+      });
+    }
+    for (auto& x : th) x.join();
+  }
+  if (generic.load()) return PG_TABLE_GENERIC;
+  std::vector<int64_t> rec_line;  // record -> line
+  rec_line.reserve(n_lines);
+  for (int64_t i = 0; i < n_lines; ++i) {
+    if (cells_of[i] == 0) continue;
+    if (cells_of[i] != n_fields) {
+      *err_line = lines[i].lineno;
+      *err_cells = cells_of[i];
+      pg::set_error("ragged row");
+      return PG_ERR_FORMAT;
+    }
+    rec_line.push_back(i);
+  }
+  const int64_t nr = static_cast<int64_t>(rec_line.size());
+  *n_rows = nr;
+  if (values == nullptr) return PG_OK;
+
+  // ---- pass 2: cells
+  std::vector<std::vector<int64_t>> miss_t(nt, std::vector<int64_t>(n_val, 0));
+  std::vector<std::vector<int64_t>> bad_t(nt, std::vector<int64_t>(n_val, 0));
+  {
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t) {
+      th.emplace_back([&, t] {
+        int64_t* miss = miss_t[t].data();
+        int64_t* bad = bad_t[t].data();
+        for (int64_t r = t; r < nr; r += nt) {
+          const Line& L = lines[rec_line[r]];
+          double* out = values + r * n_val;
+          int64_t f = 0, j = 0, k = L.begin;
+          while (f < n_fields) {
+            int64_t e = k;
+            while (e < L.end && buf[e] != delim) ++e;
+            int64_t a = k, z = e;
+            while (a < z && pg::is_space(static_cast<unsigned char>(buf[a]))) ++a;
+            while (z > a && pg::is_space(static_cast<unsigned char>(buf[z - 1]))) --z;
+            if (f == id_field) {
+              id_off[r] = a;
+              id_len[r] = z - a;
+            } else {
+              const char* s = buf + a;
+              const size_t n = static_cast<size_t>(z - a);
+              double v = NAN;
+              if (pg::is_missing_token(s, n) || pg::is_minus_nine(s, n)) {
+                ++miss[j];
+              } else if (!pg::py_float(s, n, v) || !std::isfinite(v)) {
+                v = NAN;
+                ++bad[j];
+                ++miss[j];
+              } else if (std::isnan(v)) {
+                ++miss[j];
+              }
+              out[j++] = v;
+            }
+            k = e + 1;
+            ++f;
+          }
+        }
+      });
+    }
+    for (auto& x : th) x.join();
+  }
+  for (int64_t j = 0; j < n_val; ++j) {
+    int64_t m = 0, b = 0;
+    for (int t = 0; t < nt; ++t) {
+      m += miss_t[t][j];
+      b += bad_t[t][j];
+    }
+    missing[j] = m;
+    unparseable[j] = b;
+  }
+  return PG_OK;
+}
+
+}  // extern "C"

@@ -169,14 +169,29 @@ def run_scan_distributed(config):
     dev = torch.device("cuda", local)
 
     def panel_hook(ctx, prep):
-        # rank 0 quantizes its host panel; the limbs reach the other GPUs in one NCCL broadcast
+        # rank 0 prepares + quantizes the panel on its GPU; the zero-variance flags and
+        # the quantized limbs reach the other GPUs in two broadcasts (NCCL)
+        from .engine import stage_panel
+
+        err = None
         if rank == 0:
-            ctx.set_panel(prep.ytil, prep.align.genotype_row_index, prep_n_src[0])
-        broadcast_panel(ctx, torch, dist, rank, prep.ytil.shape[0], prep.ytil.shape[1],
-                        prep.align.genotype_row_index, prep_n_src[0], dev)
+            try:
+                stage_panel(ctx, prep, n_src)
+            except Exception as exc:  # tell the other ranks before re-raising
+                err = exc
+        flags = [(prep.zero_variance, None if err is None else f"{type(err).__name__}: {err}") if rank == 0 else None]
+        dist.broadcast_object_list(flags, 0)
+        if err is not None:
+            raise err
+        if flags[0][1] is not None:
+            raise PanelGwasError(f"rank 0 panel preparation failed: {flags[0][1]}")
+        if rank != 0:
+            prep.set_flags(flags[0][0])
+        broadcast_panel(ctx, torch, dist, rank, prep.align.n_kept, len(prep.pheno_names),
+                        prep.align.genotype_row_index, n_src, dev)
 
     src = open_genotype_source(config.source)
-    prep_n_src = [src.n_samples]
+    n_src = src.n_samples
     src.close()
     # every rank joins the panel broadcast; a rank with an empty shard scans a dummy
     # one-marker range and discards it

@@ -198,17 +198,30 @@ def device_batch_size(config: ScanConfig, n_markers: int, n_pheno: int) -> int:
 
 @dataclass
 class _PreparedPanel:
-    ytil: np.ndarray
     basis: kernel.CovariateBasis
-    pheno_names: list[str]
-    zero_variance: np.ndarray
     panel: phenotypes.PhenotypePanel
     align: phenotypes.SampleAlignment
     df: float
+    pheno_names: list[str] = field(default_factory=list)
+    zero_variance: np.ndarray | None = None
+    kept_cols: np.ndarray | None = None
+
+    def set_flags(self, zero_variance: np.ndarray) -> None:
+        self.zero_variance = np.asarray(zero_variance, dtype=bool)
+        self.kept_cols = np.nonzero(~self.zero_variance)[0]
+        self.pheno_names = [self.panel.phenotype_names[j] for j in self.kept_cols.tolist()]
+        if not self.pheno_names:
+            raise PanelGwasError("every phenotype has zero variance; nothing to scan")
+        if self.df < 1:
+            n = self.align.n_kept
+            raise ConfigError(f"degrees of freedom {self.df:.0f} < 1 (n={n}, basis rank={self.basis.rank})")
 
 
 def prepare_panel(config: ScanConfig, source) -> _PreparedPanel:
-    """Tables -> alignment -> panel -> covariate basis -> residualized, standardized Y~ (host, once)."""
+    """Tables -> alignment -> panel (missing policy) -> covariate basis -> df (host, once).
+
+    The numeric panel preparation (centre, residualize, standardize: kernel.py:310-347 of
+    the reference, engine.py:259-279) runs on the device in stage_panel()."""
     pheno_table = phenotypes.load_table(config.pheno_path, config.id_column, config.delimiter)
     covar_table = (
         phenotypes.load_table(config.covar_path, config.id_column, config.delimiter) if config.covar_path else None
@@ -225,20 +238,17 @@ def prepare_panel(config: ScanConfig, source) -> _PreparedPanel:
         c_matrix = np.zeros((n, 0))
         c_names = []
     basis = kernel.build_covariate_basis(c_matrix, True, config.rank_tolerance, c_names)
-    panel.y = kernel.residualize(panel.y, basis)
-    panel.state = PanelState.RESIDUALIZED
-    ytil, _sd, zero_variance = kernel.standardize_columns(panel.y)
-    panel.y = ytil
-    panel.state = PanelState.STANDARDIZED
-    kept_cols = np.nonzero(~zero_variance)[0]
-    names = [panel.phenotype_names[j] for j in kept_cols]
-    if not names:
-        raise PanelGwasError("every phenotype has zero variance; nothing to scan")
-    ytil = np.ascontiguousarray(ytil[:, kept_cols])
     df = float(n - 2) if config.df_mode is DfMode.PAPER_N_MINUS_2 else float(n - basis.rank - 1)
-    if df < 1:
-        raise ConfigError(f"degrees of freedom {df:.0f} < 1 (n={n}, basis rank={basis.rank})")
-    return _PreparedPanel(ytil, basis, names, zero_variance, panel, align, df)
+    return _PreparedPanel(basis, panel, align, df)
+
+
+def stage_panel(ctx, prep: _PreparedPanel, n_samples_src: int, commit: bool = True) -> None:
+    """Device panel preparation (pg_ctx_prepare_panel) + quantization of the kept columns."""
+    flat, _sd = ctx.prepare_panel(prep.panel.y, prep.basis.q)
+    prep.panel.state = PanelState.STANDARDIZED
+    prep.set_flags(flat)
+    if commit:
+        ctx.commit_panel(prep.kept_cols, prep.align.genotype_row_index, n_samples_src)
 
 
 def run_scan(config: ScanConfig, marker_range: tuple[int, int] | None = None, panel_hook=None) -> ScanSummary:
@@ -266,6 +276,15 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
     if source.n_markers < 1:
         raise PanelGwasError("genotype source has no markers")
     dtype = np.dtype(np.float32 if config.precision is Precision.F32_STORE_F64_ACC else np.float64)
+    ctx = DeviceContext(config.device)
+    try:
+        if panel_hook is not None:
+            panel_hook(ctx, prep)
+        else:
+            stage_panel(ctx, prep, source.n_samples)
+    except BaseException:
+        ctx.close()
+        raise
     names = prep.pheno_names
     n_pheno = len(names)
 
@@ -282,14 +301,9 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
     else:
         writer = output.ThresholdWriter(config.out_path, config.p_threshold, df, n, source.counts_allele1, names)
 
-    ctx = DeviceContext(config.device)
     if os.environ.get("PANELGWAS_FUSED_DECODE", "1") == "0":
         ctx.set_fused_decode(False)  # A/B switch; results are identical either way
     try:
-        if panel_hook is not None:
-            panel_hook(ctx, prep)
-        else:
-            ctx.set_panel(prep.ytil, prep.align.genotype_row_index, source.n_samples)
         if config.residualize_genotypes and prep.basis.rank:
             ctx.set_basis(prep.basis.q)  # extension mode: side GEMM K5 for |Q^T g|^2
         t_floor = np.inf

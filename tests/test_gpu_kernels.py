@@ -128,3 +128,65 @@ def test_correlate_handworked_and_row_stable():
     assert r[0, 0] == 1.0 and clamped == 1
     with pytest.raises(ValueError):
         pg.correlate(np.zeros((2, 3)), np.zeros((4, 1)))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,p,n_cov", [(300, 12, 3), (2000, 64, 10), (5000, 700, 20), (1100, 33, 0)])
+def test_device_panel_prep_matches_host(n, p, n_cov):
+    """pg_ctx_prepare_panel == kernel.residualize + standardize_columns (reference
+    kernel.py:310-347) to 1e-12 relative, flags identical; commit == set_panel on the
+    host-prepared matrix (quantized limbs + scales bitwise, barring rint ties)."""
+    import torch
+
+    from paper_2604_21095_b200 import kernel
+    from paper_2604_21095_b200._device import DeviceContext
+
+    rng = np.random.default_rng(n + p)
+    c = rng.standard_normal((n, n_cov))
+    y = c @ rng.standard_normal((n_cov, p)) * 0.3 + rng.standard_normal((n, p)) * rng.uniform(0.5, 50, p) + 7.0
+    y[:, 3] = 5.0  # constant -> zero variance after centring
+    if n_cov:
+        y[:, 5] = 2.0 * c[:, 0] - 1.0  # lies in span(Q) -> zero variance after residualization
+    basis = kernel.build_covariate_basis(c, True)
+    want, want_sd, want_flat = kernel.standardize_columns(kernel.residualize(y, basis))
+    with DeviceContext(0) as ctx:
+        flat, sd = ctx.prepare_panel(y, basis.q)
+        got = ctx.fetch_prepared_panel()
+        assert np.array_equal(flat, want_flat)
+        ok = ~want_flat
+        np.testing.assert_allclose(sd[ok], want_sd[ok], rtol=1e-12)
+        np.testing.assert_allclose(got[:, ok], want[:, ok], rtol=1e-10, atol=1e-12)
+        assert np.all(got[:, ~ok] == 0.0)
+        kept = np.nonzero(ok)[0]
+        gidx = np.arange(n, dtype=np.int64)
+        ctx.commit_panel(kept, gidx, n)
+        nb = ctx.panel_bytes()
+        a = torch.empty(nb, dtype=torch.uint8, device="cuda")
+        ctx.export_panel(a.data_ptr())
+        ctx.set_panel(np.ascontiguousarray(want[:, kept]), gidx, n)
+        b = torch.empty(nb, dtype=torch.uint8, device="cuda")
+        ctx.export_panel(b.data_ptr())
+        p_pad, k_pad = -(-kept.size // 256) * 256, -(-n // 64) * 64
+        plane = p_pad * k_pad
+
+        def unpack(buf):
+            raw = buf.cpu().numpy()
+            lim = raw[:3 * plane].view(np.int8).astype(np.int64).reshape(3, p_pad, k_pad)
+            q = 32385 * lim[0] + 127 * lim[1] + lim[2]
+            return q, raw[3 * plane:3 * plane + 8 * p_pad].view(np.float64)
+
+        qa, sa = unpack(a)
+        qb, sb = unpack(b)
+        np.testing.assert_allclose(sa, sb, rtol=1e-14)
+        assert np.abs(qa - qb).max() <= 1  # quantized to the same 23-bit grid up to rint ties
+
+
+@pytest.mark.gpu
+def test_device_panel_prep_rejects_non_finite():
+    from paper_2604_21095_b200._device import DeviceContext
+
+    y = np.ones((10, 3))
+    y[4, 1] = np.inf
+    with DeviceContext(0) as ctx:
+        with pytest.raises(ValueError, match="finite"):
+            ctx.prepare_panel(y, None)

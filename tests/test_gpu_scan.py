@@ -228,14 +228,18 @@ def test_two_shard_flow_equals_single_gpu(s1, tmp_path):
     pg.run_scan(pg.ScanConfig(out_path=tmp_path / "single.tsv", **base))
     exported = {}
 
+    from paper_2604_21095_b200.engine import stage_panel
+
     def hook0(ctx, prep):
-        ctx.set_panel(prep.ytil, prep.align.genotype_row_index, 300)
+        stage_panel(ctx, prep, 300)
         buf = torch.empty(ctx.panel_bytes(), dtype=torch.uint8, device="cuda")
         ctx.export_panel(buf.data_ptr())
         exported["buf"] = buf
+        exported["flags"] = prep.zero_variance
 
     def hook1(ctx, prep):
-        ctx.import_panel(exported["buf"].data_ptr(), prep.ytil.shape[0], prep.ytil.shape[1],
+        prep.set_flags(exported["flags"])  # what the rank-0 flag broadcast delivers
+        ctx.import_panel(exported["buf"].data_ptr(), prep.align.n_kept, len(prep.pheno_names),
                          prep.align.genotype_row_index, 300)
 
     shards = []
