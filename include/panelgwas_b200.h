@@ -204,6 +204,29 @@ PG_API int pg_reg_inc_beta(pg_ctx* ctx, const double* a, const double* b, const 
 /* kernel.t_threshold_for_p (kernel.py:212-235) */
 PG_API int pg_t_threshold_for_p(pg_ctx* ctx, double p_threshold, double df, double* t_crit);
 
+/* Native BGEN v1.2 variant index (host). Replaces BgenSource._index_variants
+ * (genotypes/bgen.py:130-168): walks n_variants headers from byte first_variant of the
+ * memory-mapped file. Per variant: block_offset/block_size of the compressed genotype
+ * block, position, and 5 strings (variant id, rsid, chrom, allele1, allele2) as byte
+ * ranges text[text_off[5v+s] .. text_off[5v+s+1]) (text_off has 5n+1 entries).
+ * On PG_ERR_FORMAT diag = {variant, kind, detail, 0}: kind 1 truncated header field
+ * (detail = field code), 2 n_alleles != 2 (detail = n), 3 payload past EOF (detail = size);
+ * PG_ERR_INVALID with kind 4: text buffer too small. On success diag[0] = end offset. */
+PG_API int pg_bgen_index(const char* path, int64_t first_variant, int64_t n_variants, int64_t* block_offset,
+                         int64_t* block_size, uint32_t* position, char* text, int64_t text_cap, int64_t* text_off,
+                         int64_t* diag);
+/* Parallel zlib inflate + validation of `count` genotype blocks (host threads; replaces the
+ * inflate half of BgenSource._decode_variant, genotypes/bgen.py:183-232) into device-staging
+ * rows [2n probabilities (u8 | u16) | n ploidy bytes]. `rows` must hold count x row_cap
+ * bytes with row_cap >= 5n; on success rows are packed at *out_row_bytes (3n or 5n) and
+ * *out_bits is 8 or 16 (mixed batches are widened exactly, x257). On PG_ERR_FORMAT
+ * diag = {variant, reason, a, b} (reasons: 1 block < 4 B, 2 zlib (message in pg_last_error),
+ * 3 inflated size (a got, b want), 4 sample count (a), 5 alleles (a), 6 ploidy range (a, b),
+ * 7 non-diploid, 8 phased, 9 bits (a), 10 block size (a got, b want), 11 past EOF). */
+PG_API int pg_bgen_inflate(const char* path, const int64_t* block_offset, const int64_t* block_size, int64_t count,
+                           int64_t n_samples, int n_threads, uint8_t* rows, int64_t row_cap, int* out_bits,
+                           int64_t* out_row_bytes, int64_t* diag);
+
 /* Native table-body parser (host). Replaces the cell loop of
  * phenotypes.load_table (phenotypes.py:67-138): records after the header line
  * (starting at byte body_offset, physical line number first_lineno), cells split on

@@ -91,6 +91,8 @@ SIGNATURES: dict[str, list] = {
     "pg_decode_bgen": [_P, _P, _P, c_int64, c_int64, c_int, _P, _P],
     "pg_prepare_batch": [_P, _P, c_int64, c_int64, _P, c_int64, c_int, _P, _P, _P, _P, _P],
     "pg_correlate_f64": [_P, _P, c_int64, c_int64, _P, c_int64, _P, _P],
+    "pg_bgen_index": [c_char_p, c_int64, c_int64, _P, _P, _P, _P, c_int64, _P, _P],
+    "pg_bgen_inflate": [c_char_p, _P, _P, c_int64, c_int64, c_int, _P, c_int64, _P, _P, _P],
     "pg_table_parse": [_P, c_int64, c_int64, ctypes.c_char, c_int64, c_int64, c_int, c_int64, _P, _P, _P, _P, _P,
                        _P, _P, _P],
     "pg_format_float_repr": [_P, c_int64, _P, c_int64, _P],

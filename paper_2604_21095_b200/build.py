@@ -91,8 +91,8 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
         msg = "\n".join(f"--- {s.name}\n{t}" for s, t in failed)
         raise RuntimeError(f"nvcc failed:\n{msg}")
     tmp = LIB_PATH.with_suffix(".so.tmp")
-    link = [nvcc, *ARCH_FLAGS, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs), "-lrt", "-ldl",
-            "-lpthread"]
+    link = [nvcc, *ARCH_FLAGS, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs), "-lz", "-lrt",
+            "-ldl", "-lpthread"]
     if verbose:
         print(" ".join(link), flush=True)
     res = subprocess.run(link, capture_output=True, text=True)
