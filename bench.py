@@ -352,6 +352,16 @@ def our_arm(a) -> None:
     except Exception:
         pass
 
+    # HBM roofline of the decode stage: K1 statistics kernel alone over the whole shard
+    # (reads ceil(N/4) bytes per marker, writes 56 B of per-marker stats)
+    k1_ms = ctx.time_marker_stats(_native.PG_GENO_BED, packed.data_ptr(), m, pitch, reps=3)
+    k1_bytes = m * (bpm + 56)
+    hbm_peak = float(peaks.get("hbm_gbs", 6548.8))
+    decode_hbm = {"kernel": "stats_kernel", "achieved": k1_bytes / (k1_ms / 1e3) / 1e9, "peak": hbm_peak,
+                  "unit": "GB/s", "frac": k1_bytes / (k1_ms / 1e3) / 1e9 / hbm_peak, "ms": k1_ms,
+                  "bytes_def": "ceil(N/4) packed bytes read + 56 B stats written per marker",
+                  "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+
     # ------------------------------------------------ end to end through the host-buffer C ABI
     e2e = None
     if not a.no_e2e:
@@ -416,6 +426,7 @@ def our_arm(a) -> None:
             "hw_int8": {"achieved_tops": int8_achieved, "cublas_int8_tops_measured": int8_peak,
                         "frac": (int8_achieved / int8_peak) if int8_peak else None,
                         "ops_def": "2 * 3 limbs * K_pad * M * P_pad per launch"},
+            "decode_hbm": decode_hbm,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),

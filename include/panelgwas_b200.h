@@ -272,6 +272,12 @@ PG_API int pg_prepare_batch(pg_ctx* ctx, const double* dosages, int64_t n_marker
 PG_API int pg_correlate_f64(pg_ctx* ctx, const double* gt, int64_t m, int64_t n, const double* yt, int64_t p, double* r,
                      int64_t* clamp_count);
 
+/* Measurement hook: average device time (CUDA events on the ctx stream) of the per-marker
+ * statistics kernel K1 alone over `reps` launches on a device block, for the HBM roofline
+ * of the decode stage (bench.py). Same inputs as pg_scan_device; results are discarded. */
+PG_API int pg_time_marker_stats(pg_ctx* ctx, int kind, const void* d_data, int64_t n_markers, int64_t row_pitch,
+                                int reps, float* ms);
+
 /* ---- test hooks (exercise single kernels with device pointers) ---- */
 /* Raw association GEMM: X[c, p] = kWH * sum_k qh[p,k] v[c,k] + sum_k q1[p,k] v127[c,k] + q0[p,k] v[c,k]
  * (int8 operands, exact int32 accumulation, returned as f64 [c_pad, p_pad]).

@@ -246,6 +246,13 @@ class DeviceContext:
                      ptr(res.cand_t), ptr(res.cand_p))
         return res
 
+    def time_marker_stats(self, kind: int, d_ptr: int, n_markers: int, pitch: int, reps: int = 5) -> float:
+        """Average ms of the statistics kernel alone on a device block (measurement hook)."""
+        ms = ctypes.c_float(0.0)
+        with self.lock:
+            call("pg_time_marker_stats", self._h, int(kind), d_ptr, n_markers, pitch, reps, byref(ms))
+        return float(ms.value)
+
     def max_abs_r(self) -> np.ndarray:
         out = np.empty(self.n_pheno)
         call("pg_fetch_max_abs_r", self._h, ptr(out))

@@ -315,6 +315,7 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
   b.n_src = c->n_src;
   b.n_kept = c->n_kept;
   b.keep_bits = c->keep_bits.p;
+  b.all_kept = c->n_kept == c->n_src ? 1 : 0;
 
   const int64_t m_cap = round_up(m, 256);  // enough marker slots for any rows_per_marker
   PG_CHECK_STATUS(c->flags.ensure(2));
@@ -455,10 +456,7 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
       const int64_t newcap = ncand + ncand / 8 + 1024;
       PG_CHECK_STATUS(c->cand_key.ensure(newcap));
       PG_CHECK_STATUS(c->cand_r.ensure(newcap));
-      c->cand_capacity = newcap;
-      if (c->max_abs_r.p) {
-        // max |r| is idempotent under recomputation; nothing to undo
-      }
+      c->cand_capacity = newcap;  // max |r| is idempotent under recomputation
     }
   }
 
@@ -912,6 +910,52 @@ int pg_scan_device(pg_ctx* c, int kind, const void* d_data, int64_t n_markers, i
   PG_REQUIRE(row_pitch % 16 == 0 && row_pitch >= row_bytes, PG_ERR_INVALID, "row_pitch must be a multiple of 16");
   PG_REQUIRE(reinterpret_cast<uintptr_t>(d_data) % 16 == 0, PG_ERR_INVALID, "device block must be 16-byte aligned");
   return scan_common(c, kind, static_cast<const uint8_t*>(d_data), n_markers, row_pitch, info);
+}
+
+int pg_time_marker_stats(pg_ctx* c, int kind, const void* d_data, int64_t n_markers, int64_t row_pitch, int reps,
+                         float* ms) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(c->have_panel, PG_ERR_STATE, "pg_time_marker_stats: no panel uploaded");
+  PG_REQUIRE(ms != nullptr && reps >= 1 && n_markers >= 1, PG_ERR_INVALID, "pg_time_marker_stats: bad arguments");
+  PG_REQUIRE(row_pitch % 16 == 0 && reinterpret_cast<uintptr_t>(d_data) % 16 == 0, PG_ERR_INVALID,
+             "pg_time_marker_stats: rows must be 16-byte aligned");
+  GenoBlock b;
+  b.kind = kind;
+  b.data = static_cast<const uint8_t*>(d_data);
+  b.pitch = row_pitch;
+  b.n_markers = n_markers;
+  b.n_src = c->n_src;
+  b.n_kept = c->n_kept;
+  b.keep_bits = c->keep_bits.p;
+  b.all_kept = c->n_kept == c->n_src ? 1 : 0;
+  const int64_t m_cap = round_up(n_markers, 256);
+  for (auto* buf : {&c->n_miss, &c->s_u, &c->ss_u}) PG_CHECK_STATUS(buf->ensure(m_cap));
+  for (auto* buf : {&c->sum_d, &c->af, &c->var, &c->mu_d, &c->invd_d}) PG_CHECK_STATUS(buf->ensure(m_cap));
+  PG_CHECK_STATUS(c->mu_f.ensure(m_cap));
+  PG_CHECK_STATUS(c->invd_f.ensure(m_cap));
+  PG_CHECK_STATUS(c->skip.ensure(m_cap));
+  PG_CHECK_STATUS(c->flags.ensure(2));
+  MarkerStats st;
+  st.n_miss = c->n_miss.p;
+  st.s_u = c->s_u.p;
+  st.ss_u = c->ss_u.p;
+  st.sum_d = c->sum_d.p;
+  st.af = c->af.p;
+  st.var = c->var.p;
+  st.skip = c->skip.p;
+  st.mu_d = c->mu_d.p;
+  st.mu_f = c->mu_f.p;
+  st.invd_d = c->invd_d.p;
+  st.invd_f = c->invd_f.p;
+  st.flags = c->flags.p;
+  PG_CHECK_STATUS(geno_stats(b, st, m_cap, c->stream));  // warm-up
+  PG_CUDA_CHECK(cudaEventRecord(c->ev[0], c->stream));
+  for (int i = 0; i < reps; ++i) PG_CHECK_STATUS(geno_stats(b, st, m_cap, c->stream));
+  PG_CUDA_CHECK(cudaEventRecord(c->ev[1], c->stream));
+  PG_CUDA_CHECK(cudaEventSynchronize(c->ev[1]));
+  PG_CUDA_CHECK(cudaEventElapsedTime(ms, c->ev[0], c->ev[1]));
+  *ms /= static_cast<float>(reps);
+  return PG_OK;
 }
 
 int pg_fetch_marker_stats(pg_ctx* c, double* af, int64_t* missing_count, double* variance, int8_t* skip) {

@@ -143,25 +143,39 @@ __device__ __forceinline__ uint32_t spread16(uint32_t x) {
   return x;
 }
 
-// PLINK rows: counts straight from bit planes, 64 samples per lane-step (uint4 loads).
+// PLINK rows: counts straight from bit planes. Each lane keeps 4 independent 16-byte
+// streaming loads in flight (64 samples each) before counting, so a warp has 2 KB of
+// the row outstanding: enough memory-level parallelism for HBM rate at ~40 warps/SM.
+// With every sample kept only the tail chunk needs a mask (padding codes past n_src).
 __device__ __forceinline__ void bed_counts(const GenoBlock& b, int64_t m, int lane, long long& nmiss, long long& su,
                                            long long& ssu) {
-  const uint8_t* row = b.data + m * b.pitch;
-  const int64_t n_vec = b.pitch / 16;  // pitch is a multiple of 16 bytes
-  long long n2 = 0, n0 = 0, nm = 0;
-  for (int64_t vi = lane; vi < n_vec; vi += 32) {
-    const uint4 w4 = *reinterpret_cast<const uint4*>(row + vi * 16);
-    const uint32_t ws[4] = {w4.x, w4.y, w4.z, w4.w};
+  const uint4* row = reinterpret_cast<const uint4*>(b.data + m * b.pitch);
+  const int64_t n_vec = (b.n_src + 63) / 64;  // 16-byte vectors holding real samples
+  int n2 = 0, n0 = 0, nm = 0;
+  for (int64_t base = lane; base < n_vec; base += 4 * 32) {
+    uint4 w4[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int64_t ci = vi * 4 + q;  // 16-sample chunk index
-      if (ci * 16 >= b.n_src) break;
-      const uint32_t km = spread16(keep16(b.keep_bits, ci));
-      const uint32_t w = ws[q];
-      const uint32_t lo = w & 0x55555555u, hi = (w >> 1) & 0x55555555u;
-      nm += __popc(lo & ~hi & km);
-      n2 += __popc(~lo & ~hi & km);
-      n0 += __popc(lo & hi & km);
+    for (int j = 0; j < 4; ++j) {
+      const int64_t vi = base + 32 * j;
+      w4[j] = vi < n_vec ? __ldcs(row + vi) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t vi = base + 32 * j;
+      if (vi >= n_vec) break;
+      const uint32_t ws[4] = {w4[j].x, w4[j].y, w4[j].z, w4[j].w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t ci = vi * 4 + q;  // 16-sample chunk index
+        uint32_t km = 0xFFFFFFFFu;
+        if (!b.all_kept || (ci + 1) * 16 > b.n_src) km = spread16(keep16(b.keep_bits, ci)) * 3u;
+        const uint32_t w = ws[q] & km;  // excluded / padding codes -> 00 then masked below
+        const uint32_t lo = w & 0x55555555u, hi = (w >> 1) & 0x55555555u;
+        const uint32_t kk = km & 0x55555555u;
+        nm += __popc(lo & ~hi);
+        n2 += __popc(~lo & ~hi & kk);
+        n0 += __popc(lo & hi);
+      }
     }
   }
   nmiss = nm;

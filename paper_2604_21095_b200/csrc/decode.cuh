@@ -17,6 +17,7 @@ struct GenoBlock {
   int64_t n_kept = 0;         // N used by the statistics
   const uint32_t* keep_bits = nullptr;  // [ceil(n_src/32)] bit i = sample i kept
   int dense_real = 0;         // DENSE only: 1 -> fixed-point (2^-17) digits, 0 -> integral dosages
+  int all_kept = 0;           // every source sample is kept (keep_bits needed only past n_src)
 };
 
 // u-units: the integer code each observed sample contributes to the GEMM.

@@ -141,6 +141,29 @@ def merge_full(shards: list[Path], out_path: Path) -> int:
     return rows
 
 
+def merge_min_p(shards: list[Path], out_path: Path) -> int:
+    """Per phenotype keep the shard row with the largest max |r| (= the smallest p)."""
+    best: dict[str, list[str]] = {}
+    order: list[str] = []
+    for p in shards:
+        with open(p) as fh:
+            fh.readline()
+            for line in fh:
+                f = line.rstrip("\n").split("\t")
+                if f[0] not in best:
+                    order.append(f[0])
+                    best[f[0]] = f
+                elif float(f[1]) > float(best[f[0]][1]):
+                    best[f[0]] = f
+    from .engine import MIN_P_COLUMNS
+
+    with open(out_path, "w") as out:
+        out.write("\t".join(MIN_P_COLUMNS) + "\n")
+        for name in order:
+            out.write("\t".join(best[name]) + "\n")
+    return len(order)
+
+
 # ----------------------------------------------------------------------------- the distributed scan
 def run_scan_distributed(config):
     """torchrun entry: every rank scans its marker shard; rank 0 merges and writes the summary."""
@@ -226,6 +249,8 @@ def run_scan_distributed(config):
             total[key] = sum(g[key] for g in gathered if g is not None)
         total["n_markers"] = n_markers
         total["records_emitted"] = records
+        if config.min_p_sidecar:
+            merge_min_p([Path(str(p) + ".minp.tsv") for p in shards], Path(str(config.out_path) + ".minp.tsv"))
         for key in ("time_decode_s", "time_prepare_s", "time_correlate_s", "time_emit_s", "wall_s"):
             total[key] = max(g[key] for g in gathered if g is not None)
         import json
@@ -234,7 +259,7 @@ def run_scan_distributed(config):
             json.dump(total, fh, indent=2, sort_keys=True)
             fh.write("\n")
         for p in [shard_path(Path(config.out_path), r) for r in range(world)]:
-            for suffix in ("", ".summary.json", ".markers.tsv", ".phenotypes.txt", ".qc.tsv"):
+            for suffix in ("", ".summary.json", ".markers.tsv", ".phenotypes.txt", ".qc.tsv", ".minp.tsv"):
                 q = Path(str(p) + suffix)
                 if q.exists():
                     q.unlink()

@@ -98,6 +98,7 @@ class ScanConfig:
     full_byte_budget: int = DEFAULT_FULL_BYTE_BUDGET
     allow_large_full: bool = False
     qc_sidecar: bool = False
+    min_p_sidecar: bool = False  # engine extension: <out>.minp.tsv, per-phenotype max |t| / min p
     summary_to_stderr: bool = True
     device: int | None = None
     # markers per device launch; None = sized automatically (results do not depend on it)
@@ -251,6 +252,17 @@ def stage_panel(ctx, prep: _PreparedPanel, n_samples_src: int, commit: bool = Tr
         ctx.commit_panel(prep.kept_cols, prep.align.genotype_row_index, n_samples_src)
 
 
+MIN_P_COLUMNS = ("PHENO", "MAX_ABS_R", "MAX_ABS_T", "MIN_P")
+
+
+def write_min_p(path: Path, names, max_abs_r, max_abs_t, min_p) -> None:
+    """Per-phenotype minimum p over the scan (north star (3)); floats as repr()."""
+    with open(path, "w") as fh:
+        fh.write("\t".join(MIN_P_COLUMNS) + "\n")
+        for j, name in enumerate(names):
+            fh.write(f"{name}\t{float(max_abs_r[j])!r}\t{float(max_abs_t[j])!r}\t{float(min_p[j])!r}\n")
+
+
 def run_scan(config: ScanConfig, marker_range: tuple[int, int] | None = None, panel_hook=None) -> ScanSummary:
     """Execute a full scan on the GPU and write results plus the summary files.
 
@@ -378,6 +390,11 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
                         finish(pending, ctx.scan_staged(pending % 2, full_elem_bytes=dtype.itemsize))
                     pending = i
                 finish(pending, ctx.scan_staged(pending % 2, full_elem_bytes=dtype.itemsize))
+            if config.min_p_sidecar:
+                # per-phenotype max |r| over every scanned marker (fused into the GEMM epilogue)
+                max_abs_r = ctx.max_abs_r()
+                max_abs_t = ctx.t_from_r(max_abs_r, df)
+                min_p, _ = ctx.p_from_t(max_abs_t, df)
         finally:
             if pinned is not None:
                 ctx.sync()
@@ -389,6 +406,9 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
     t0 = time.perf_counter()
     records = writer.finalize()
     t_emit += time.perf_counter() - t0
+
+    if config.min_p_sidecar:
+        write_min_p(Path(str(config.out_path) + ".minp.tsv"), names, max_abs_r, max_abs_t, min_p)
 
     if config.qc_sidecar:
         with open(Path(str(config.out_path) + ".qc.tsv"), "w") as fh:

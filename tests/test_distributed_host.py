@@ -122,3 +122,15 @@ def test_merge_full(tmp_path):
     distributed.merge_full(shards, tmp_path / "f.bin")
     assert (tmp_path / "f.bin").read_bytes() == (tmp_path / "s.bin").read_bytes()
     assert (tmp_path / "f.bin.markers.tsv").read_text() == (tmp_path / "s.bin.markers.tsv").read_text()
+
+
+def test_merge_min_p_takes_best_shard(tmp_path):
+    from paper_2604_21095_b200.engine import write_min_p
+
+    names = ["a", "b", "c"]
+    write_min_p(tmp_path / "s0", names, [0.1, 0.5, 0.2], [1.0, 5.0, 2.0], [0.3, 1e-6, 0.04])
+    write_min_p(tmp_path / "s1", names, [0.3, 0.4, 0.2], [3.0, 4.0, 2.0], [0.003, 1e-5, 0.04])
+    assert distributed.merge_min_p([tmp_path / "s0", tmp_path / "s1"], tmp_path / "m") == 3
+    rows = [ln.split("\t") for ln in (tmp_path / "m").read_text().splitlines()[1:]]
+    assert [r[0] for r in rows] == names
+    assert [float(r[3]) for r in rows] == [0.003, 1e-6, 0.04]

@@ -217,3 +217,25 @@ class TestCli:
         assert cli.main(["run", "--bfile", str(tmp_path / "nope"), "--pheno", str(tmp_path / "p.tsv"),
                          "--out", str(tmp_path / "o.tsv")]) == 1
         assert "missing file" in capsys.readouterr().err
+
+
+def test_min_p_sidecar_equals_full_scan_minimum(tmp_path):
+    """<out>.minp.tsv (per-phenotype max |t| / min p, fused into the GEMM epilogue) ==
+    the minimum over the FULL t matrix of the same scan (tolerance of the fp32 max)."""
+    rng = np.random.default_rng(41)
+    d, y = random_dataset(rng, 300, 120, 9)
+    y[:, 3] += 0.7 * d[11]
+    spec, pheno, _, root = dataset(tmp_path, d, y)
+    scan(spec, pheno, root / "thr.tsv", p_threshold=1e-3, min_p_sidecar=True, device_batch=64)
+    scan(spec, pheno, root / "full.bin", output_mode=pg.OutputMode.FULL, precision=pg.Precision.F64)
+    t, _, names = pg.read_full_matrix(root / "full.bin")
+    rows = [ln.split("\t") for ln in (root / "thr.tsv.minp.tsv").read_text().splitlines()]
+    assert rows[0] == ["PHENO", "MAX_ABS_R", "MAX_ABS_T", "MIN_P"]
+    assert [r[0] for r in rows[1:]] == names
+    got_t = np.array([float(r[2]) for r in rows[1:]])
+    got_p = np.array([float(r[3]) for r in rows[1:]])
+    want_t = np.abs(t).max(axis=0)
+    np.testing.assert_allclose(got_t, want_t, rtol=1e-6)
+    want_p = pg.p_from_t(want_t, 118.0)
+    np.testing.assert_allclose(-np.log10(got_p), -np.log10(want_p), rtol=1e-4)
+    assert np.argmin(got_p) == 3
