@@ -172,6 +172,17 @@ PG_API int pg_scan(pg_ctx* ctx, int geno_kind, const void* data, int64_t n_marke
 PG_API int pg_scan_device(pg_ctx* ctx, int geno_kind, const void* d_data, int64_t n_markers, int64_t row_bytes,
                    int64_t row_pitch, pg_batch_info* info);
 
+/* Stage a BGEN batch COMPRESSED: `blob` is the host byte range of the file holding the
+ * batch's genotype blocks; block i = blob[block_off[i], +block_size[i]) (the u32
+ * uncompressed length + zlib stream, bgen.py:183-196). The blocks are inflated on the GPU
+ * (one warp per stream), validated with the reference reader's checks and repacked into
+ * slot `slot` for pg_scan_staged (8- or 16-bit rows; mixed batches widened exactly).
+ * On PG_ERR_FORMAT diag = {variant, reason, a, b} as pg_bgen_inflate; reason 2 (zlib
+ * stream error or oversize output) carries no message: re-inflate that block with
+ * pg_bgen_inflate on the host to obtain zlib's own text. */
+PG_API int pg_stage_bgen(pg_ctx* ctx, int slot, const void* blob, int64_t blob_bytes, const int64_t* block_off,
+                         const int64_t* block_size, int64_t count, int64_t* diag);
+
 /* Asynchronous staging for pipelined scans (transfer of batch i+1 overlaps the
  * GEMM of batch i). pg_stage copies HOST rows into staging slot `slot` (0 or 1) on
  * the ctx's copy stream and returns immediately; `data` must stay valid (pinned
@@ -277,6 +288,12 @@ PG_API int pg_correlate_f64(pg_ctx* ctx, const double* gt, int64_t m, int64_t n,
  * of the decode stage (bench.py). Same inputs as pg_scan_device; results are discarded. */
 PG_API int pg_time_marker_stats(pg_ctx* ctx, int kind, const void* d_data, int64_t n_markers, int64_t row_pitch,
                                 int reps, float* ms);
+
+/* Test hook: inflate `count` zlib streams (stream i = blob[off[i] + skip, off[i] + size[i]))
+ * with the GPU decoder used by pg_stage_bgen; out [count, out_stride], out_len and status
+ * (0 ok, 1 malformed / bad checksum, 2 output larger than out_stride) per stream. */
+PG_API int pg_debug_inflate(const void* blob, int64_t blob_bytes, const int64_t* off, const int64_t* size,
+                            int64_t count, int64_t skip, void* out, int64_t out_stride, int64_t* out_len, int* status);
 
 /* ---- test hooks (exercise single kernels with device pointers) ---- */
 /* Raw association GEMM: X[c, p] = kWH * sum_k qh[p,k] v[c,k] + sum_k q1[p,k] v127[c,k] + q0[p,k] v[c,k]

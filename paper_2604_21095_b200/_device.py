@@ -200,6 +200,22 @@ class DeviceContext:
             call("pg_stage", self._h, int(slot), int(kind), blk.ctypes.data, blk.shape[0], int(row_bytes))
         return blk
 
+    def stage_bgen(self, slot: int, blob: np.ndarray, block_off: np.ndarray, block_size: np.ndarray):
+        """Stage a compressed BGEN batch (GPU inflate + validation) into slot 0/1.
+
+        Returns None on success, else (variant, reason, a, b) of the first failing block."""
+        b = np.ascontiguousarray(blob, dtype=np.uint8)
+        off = np.ascontiguousarray(block_off, dtype=np.int64)
+        size = np.ascontiguousarray(block_size, dtype=np.int64)
+        diag = np.zeros(4, dtype=np.int64)
+        with self.lock:
+            status = self.lib.pg_stage_bgen(self._h, int(slot), b.ctypes.data, b.size, off.ctypes.data,
+                                            size.ctypes.data, off.size, diag.ctypes.data)
+        if status == _native.PG_ERR_FORMAT and diag[1]:
+            return tuple(int(x) for x in diag)
+        _native.check(status)
+        return None
+
     def scan_staged(self, slot: int, *, fetch: bool = True, full_elem_bytes: int = 8) -> ScanResult:
         info = BatchInfo()
         with self.lock:

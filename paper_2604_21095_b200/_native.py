@@ -78,6 +78,7 @@ SIGNATURES: dict[str, list] = {
     "pg_scan": [_P, c_int, _P, c_int64, c_int64, _P],
     "pg_scan_device": [_P, c_int, _P, c_int64, c_int64, c_int64, _P],
     "pg_stage": [_P, c_int, c_int, _P, c_int64, c_int64],
+    "pg_stage_bgen": [_P, c_int, _P, c_int64, _P, _P, c_int64, _P],
     "pg_scan_staged": [_P, c_int, _P],
     "pg_fetch_marker_stats": [_P, _P, _P, _P, _P],
     "pg_fetch_candidates": [_P, _P, _P, _P, _P, _P],
@@ -98,6 +99,7 @@ SIGNATURES: dict[str, list] = {
     "pg_format_float_repr": [_P, c_int64, _P, c_int64, _P],
     "pg_format_tsv": [c_int64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, c_int64, _P, c_int64, _P],
     "pg_time_marker_stats": [_P, c_int, _P, c_int64, c_int64, c_int, _P],
+    "pg_debug_inflate": [_P, c_int64, _P, _P, c_int64, c_int64, _P, c_int64, _P, _P],
     "pg_debug_assoc_gemm": [_P, _P, _P, c_int64, _P, _P, c_int64, c_int64, _P, _P],
 }
 

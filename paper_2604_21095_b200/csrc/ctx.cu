@@ -18,6 +18,8 @@
 #include "assoc.cuh"
 #include "decode.cuh"
 #include "panel.cuh"
+#include "inflate.cuh"
+#include "bgen_stage.cuh"
 #include "pg_common.cuh"
 #include "pstats.cuh"
 
@@ -28,6 +30,10 @@ template <class T>
 struct DBuf {
   T* p = nullptr;
   size_t cap = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
   int ensure(size_t n) {
     if (n <= cap && p != nullptr) return PG_OK;
     if (p) cudaFree(p);
@@ -182,6 +188,12 @@ struct pg_ctx {
   cudaEvent_t stage_ev[2] = {nullptr, nullptr};
   cudaEvent_t slot_free_ev[2] = {nullptr, nullptr};
   int stage_kind[2] = {-1, -1};
+  // compressed BGEN staging (pg_stage_bgen): blob, block table, inflate scratch, checks
+  pg::DBuf<uint8_t> bgen_blob[2], bgen_raw[2];
+  pg::DBuf<int64_t> bgen_off[2], bgen_size[2], bgen_len[2];
+  pg::DBuf<int> bgen_zstatus[2], bgen_bits[2];
+  pg::DBuf<long long> bgen_diag[2];
+  pg::DBuf<unsigned long long> bgen_summary[2];
   int64_t stage_m[2] = {0, 0};
   int64_t stage_pitch[2] = {0, 0};
   pg::DBuf<long long> n_miss, s_u, ss_u;
@@ -884,6 +896,69 @@ int pg_stage(pg_ctx* c, int slot, int kind, const void* data, int64_t n_markers,
   PG_CUDA_CHECK(cudaEventRecord(c->stage_ev[slot], c->copy_stream));
   c->stage_kind[slot] = kind;
   c->stage_m[slot] = n_markers;
+  c->stage_pitch[slot] = pitch;
+  return PG_OK;
+}
+
+int pg_stage_bgen(pg_ctx* c, int slot, const void* blob, int64_t blob_bytes, const int64_t* block_off,
+                  const int64_t* block_size, int64_t count, int64_t* diag) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(slot == 0 || slot == 1, PG_ERR_INVALID, "pg_stage_bgen: slot must be 0 or 1");
+  PG_REQUIRE(c->have_panel, PG_ERR_STATE, "pg_stage_bgen: no panel uploaded (pg_ctx_set_panel)");
+  PG_REQUIRE(blob != nullptr && block_off != nullptr && block_size != nullptr && diag != nullptr && count >= 1,
+             PG_ERR_INVALID, "pg_stage_bgen: empty batch or null argument");
+  for (int64_t i = 0; i < count; ++i)
+    PG_REQUIRE(block_off[i] >= 0 && block_size[i] >= 0 && block_off[i] + block_size[i] <= blob_bytes,
+               PG_ERR_INVALID, "pg_stage_bgen: block %lld outside the blob", (long long)i);
+  diag[0] = diag[1] = diag[2] = diag[3] = 0;
+  const int64_t n = c->n_src;
+  const int64_t raw_stride = round_up(10 + 5 * n, 16);
+  cudaStream_t cs = c->copy_stream;
+  PG_CUDA_CHECK(cudaStreamWaitEvent(cs, c->slot_free_ev[slot], 0));
+  PG_CUDA_CHECK(cudaStreamSynchronize(cs));
+  PG_CHECK_STATUS(c->bgen_blob[slot].ensure(blob_bytes));
+  PG_CHECK_STATUS(c->bgen_raw[slot].ensure(static_cast<size_t>(raw_stride) * count));
+  for (auto* b : {&c->bgen_off[slot], &c->bgen_size[slot], &c->bgen_len[slot]}) PG_CHECK_STATUS(b->ensure(count));
+  PG_CHECK_STATUS(c->bgen_zstatus[slot].ensure(count));
+  PG_CHECK_STATUS(c->bgen_bits[slot].ensure(count));
+  PG_CHECK_STATUS(c->bgen_diag[slot].ensure(3 * count));
+  PG_CHECK_STATUS(c->bgen_summary[slot].ensure(2));
+  PG_CUDA_CHECK(cudaMemcpyAsync(c->bgen_blob[slot].p, blob, blob_bytes, cudaMemcpyHostToDevice, cs));
+  PG_CUDA_CHECK(cudaMemcpyAsync(c->bgen_off[slot].p, block_off, sizeof(int64_t) * count, cudaMemcpyHostToDevice, cs));
+  PG_CUDA_CHECK(
+      cudaMemcpyAsync(c->bgen_size[slot].p, block_size, sizeof(int64_t) * count, cudaMemcpyHostToDevice, cs));
+  // genotype block = u32 uncompressed length + zlib stream
+  PG_CHECK_STATUS(pg::inflate_streams(c->bgen_blob[slot].p, c->bgen_off[slot].p, c->bgen_size[slot].p, count, 4,
+                                      c->bgen_raw[slot].p, raw_stride, c->bgen_len[slot].p, c->bgen_zstatus[slot].p,
+                                      cs));
+  unsigned long long init[2] = {~0ull, 0ull};
+  PG_CUDA_CHECK(cudaMemcpyAsync(c->bgen_summary[slot].p, init, sizeof(init), cudaMemcpyHostToDevice, cs));
+  PG_CHECK_STATUS(pg::bgen_validate(c->bgen_blob[slot].p, c->bgen_off[slot].p, c->bgen_size[slot].p,
+                                    c->bgen_raw[slot].p, raw_stride, c->bgen_len[slot].p, c->bgen_zstatus[slot].p,
+                                    count, n, c->bgen_diag[slot].p, c->bgen_bits[slot].p, c->bgen_summary[slot].p,
+                                    cs));
+  unsigned long long summary[2] = {0, 0};
+  PG_CUDA_CHECK(cudaMemcpyAsync(summary, c->bgen_summary[slot].p, sizeof(summary), cudaMemcpyDeviceToHost, cs));
+  PG_CUDA_CHECK(cudaStreamSynchronize(cs));
+  if (summary[0] != ~0ull) {
+    long long d3[3] = {0, 0, 0};
+    PG_CUDA_CHECK(cudaMemcpy(d3, c->bgen_diag[slot].p + 3 * summary[0], sizeof(d3), cudaMemcpyDeviceToHost));
+    diag[0] = static_cast<int64_t>(summary[0]);
+    diag[1] = d3[0];
+    diag[2] = d3[1];
+    diag[3] = d3[2];
+    pg::set_error("BGEN block %lld failed validation (reason %lld)", (long long)summary[0], d3[0]);
+    return PG_ERR_FORMAT;
+  }
+  const bool wide16 = (summary[1] & 2ull) != 0;
+  const int64_t row_bytes = wide16 ? 5 * n : 3 * n;
+  const int64_t pitch = round_up(row_bytes, 16);
+  PG_CHECK_STATUS(c->stage_buf[slot].ensure(static_cast<size_t>(pitch) * count));
+  PG_CHECK_STATUS(pg::bgen_repack(c->bgen_raw[slot].p, raw_stride, c->bgen_bits[slot].p, count, n, wide16,
+                                  c->stage_buf[slot].p, pitch, cs));
+  PG_CUDA_CHECK(cudaEventRecord(c->stage_ev[slot], cs));
+  c->stage_kind[slot] = wide16 ? PG_GENO_BGEN16 : PG_GENO_BGEN8;
+  c->stage_m[slot] = count;
   c->stage_pitch[slot] = pitch;
   return PG_OK;
 }

@@ -145,38 +145,55 @@ __device__ __forceinline__ uint32_t spread16(uint32_t x) {
 
 // PLINK rows: counts straight from bit planes. Each lane keeps 4 independent 16-byte
 // streaming loads in flight (64 samples each) before counting, so a warp has 2 KB of
-// the row outstanding: enough memory-level parallelism for HBM rate at ~40 warps/SM.
-// With every sample kept only the tail chunk needs a mask (padding codes past n_src).
+// the row outstanding. Per 16-sample word: n0 = popc(lo & hi), missing = popc(lo) - n0,
+// n2 = 16 - popc(lo | hi) (~10 integer ops). Masks (excluded samples, the padding codes
+// of the last vector) are applied only where needed, in a separate path, so the common
+// all-kept loop stays branch-free and under the HBM rate.
+__device__ __forceinline__ void bed_word(uint32_t w, int& nm, int& n2, int& n0) {
+  const uint32_t lo = w & 0x55555555u, hi = (w >> 1) & 0x55555555u;
+  const int c0 = __popc(lo & hi);
+  n0 += c0;
+  nm += __popc(lo) - c0;
+  n2 += 16 - __popc(lo | hi);
+}
+
+__device__ __forceinline__ void bed_word_masked(uint32_t w, uint32_t kk, int& nm, int& n2, int& n0) {
+  // kk: one bit per kept code (even positions)
+  const uint32_t lo = w & kk, hi = (w >> 1) & kk;
+  const int c0 = __popc(lo & hi);
+  n0 += c0;
+  nm += __popc(lo) - c0;
+  n2 += __popc(kk) - __popc(lo | hi);
+}
+
 __device__ __forceinline__ void bed_counts(const GenoBlock& b, int64_t m, int lane, long long& nmiss, long long& su,
                                            long long& ssu) {
   const uint4* row = reinterpret_cast<const uint4*>(b.data + m * b.pitch);
-  const int64_t n_vec = (b.n_src + 63) / 64;  // 16-byte vectors holding real samples
+  const int64_t n_vec = (b.n_src + 63) / 64;                 // 16-byte vectors holding real samples
+  const int64_t n_plain = b.all_kept ? b.n_src / 64 : 0;     // vectors needing no mask
   int n2 = 0, n0 = 0, nm = 0;
-  for (int64_t base = lane; base < n_vec; base += 4 * 32) {
+  for (int64_t base = lane; base < n_plain; base += 4 * 32) {
     uint4 w4[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int64_t vi = base + 32 * j;
-      w4[j] = vi < n_vec ? __ldcs(row + vi) : make_uint4(0, 0, 0, 0);
+      w4[j] = vi < n_plain ? __ldcs(row + vi) : make_uint4(0x55555555u, 0x55555555u, 0x55555555u, 0x55555555u);
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const int64_t vi = base + 32 * j;
-      if (vi >= n_vec) break;
-      const uint32_t ws[4] = {w4[j].x, w4[j].y, w4[j].z, w4[j].w};
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int64_t ci = vi * 4 + q;  // 16-sample chunk index
-        uint32_t km = 0xFFFFFFFFu;
-        if (!b.all_kept || (ci + 1) * 16 > b.n_src) km = spread16(keep16(b.keep_bits, ci)) * 3u;
-        const uint32_t w = ws[q] & km;  // excluded / padding codes -> 00 then masked below
-        const uint32_t lo = w & 0x55555555u, hi = (w >> 1) & 0x55555555u;
-        const uint32_t kk = km & 0x55555555u;
-        nm += __popc(lo & ~hi);
-        n2 += __popc(~lo & ~hi & kk);
-        n0 += __popc(lo & hi);
-      }
+      // out-of-range vectors were filled with all-missing codes (01): undo their count
+      if (base + 32 * j >= n_plain) nm -= 64;
+      bed_word(w4[j].x, nm, n2, n0);
+      bed_word(w4[j].y, nm, n2, n0);
+      bed_word(w4[j].z, nm, n2, n0);
+      bed_word(w4[j].w, nm, n2, n0);
     }
+  }
+  for (int64_t vi = n_plain + lane; vi < n_vec; vi += 32) {
+    const uint4 w4 = __ldcs(row + vi);
+    const uint32_t ws[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) bed_word_masked(ws[q], spread16(keep16(b.keep_bits, vi * 4 + q)), nm, n2, n0);
   }
   nmiss = nm;
   su = n2 - n0;

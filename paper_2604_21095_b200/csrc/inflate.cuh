@@ -1,0 +1,15 @@
+// GPU zlib inflate (inflate.cu) and BGEN block staging (bgen_stage.cu).
+#pragma once
+#include <cstdint>
+
+#include "pg_common.cuh"
+
+namespace pg {
+
+// Inflate `count` zlib streams: stream i is d_blob[d_off[i] + skip, d_off[i] + d_len[i]);
+// output to d_out + i * out_stride (at most out_stride bytes). Per stream: d_out_len =
+// bytes produced, d_status = 0 ok, 1 malformed stream / checksum, 2 output overflow.
+int inflate_streams(const uint8_t* d_blob, const int64_t* d_off, const int64_t* d_len, int64_t count, int64_t skip,
+                    uint8_t* d_out, int64_t out_stride, int64_t* d_out_len, int* d_status, cudaStream_t s);
+
+}  // namespace pg

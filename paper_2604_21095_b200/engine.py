@@ -336,20 +336,36 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
         plan = [(lo + s0, c0) for s0, c0 in plan_batches(hi - lo, step)]
         read_kw = {"dtype": dtype} if config.source.format.value == "dense" else {}
 
-        # pinned ring of 3 host buffers (PLINK) + 2 device staging slots: the read of batch
-        # i+1 and its H2D overlap the device scan of batch i
+        # pinned ring of 3 host buffers + 2 device staging slots: the read of batch i+1 and
+        # its H2D overlap the device scan of batch i. BGEN batches travel compressed and are
+        # inflated on the GPU (pg_stage_bgen); other formats as raw rows (pg_stage).
+        compressed = hasattr(source, "read_compressed_block") and os.environ.get("PANELGWAS_HOST_INFLATE") != "1"
         pinned = None
-        if hasattr(source, "bytes_per_marker"):
+        if compressed:
+            pinned = [_native.PinnedBuffer(step * source.compressed_bytes_per_marker) for _ in range(3)]
+        elif hasattr(source, "bytes_per_marker"):
             pinned = [_native.PinnedBuffer(step * source.bytes_per_marker) for _ in range(3)]
 
         def read(i):
             t0 = time.perf_counter()
             s0, c0 = plan[i]
-            if pinned is not None:
+            if compressed:
+                block = source.read_compressed_block(s0, c0, out=pinned[i % 3].array)
+            elif pinned is not None:
                 block = source.read_raw_block(s0, c0, out=pinned[i % 3].array)
             else:
                 block = source.read_raw_block(s0, c0, **read_kw)
             return block, time.perf_counter() - t0
+
+        def stage(i, block):
+            if compressed:
+                blob, offs, sizes = block
+                bad = ctx.stage_bgen(i % 2, blob, offs, sizes)
+                if bad is not None:
+                    source.raise_block_error(plan[i][0] + bad[0], bad[1], bad[2], bad[3])
+                return blob
+            kind, rows, row_bytes = block
+            return ctx.stage(i % 2, kind, rows, row_bytes)
 
         def finish(i, res):
             nonlocal t_prepare, t_corr, t_emit, clamp_total, skip_mono, skip_missing
@@ -381,9 +397,9 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
                 fut = reader.submit(read, 0)
                 pending = None
                 for i in range(len(plan)):
-                    (kind, rows, row_bytes), dt_read = fut.result()
+                    block, dt_read = fut.result()
                     t_decode += dt_read
-                    staged[i % 2] = ctx.stage(i % 2, kind, rows, row_bytes)
+                    staged[i % 2] = stage(i, block)
                     if i + 1 < len(plan):
                         fut = reader.submit(read, i + 1)
                     if pending is not None:
