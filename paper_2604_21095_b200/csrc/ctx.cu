@@ -916,7 +916,7 @@ int pg_stage_bgen(pg_ctx* c, int slot, const void* blob, int64_t blob_bytes, con
   cudaStream_t cs = c->copy_stream;
   PG_CUDA_CHECK(cudaStreamWaitEvent(cs, c->slot_free_ev[slot], 0));
   PG_CUDA_CHECK(cudaStreamSynchronize(cs));
-  PG_CHECK_STATUS(c->bgen_blob[slot].ensure(blob_bytes));
+  PG_CHECK_STATUS(c->bgen_blob[slot].ensure(blob_bytes + 16));  // the decoder peeks up to 8 B past a stream
   PG_CHECK_STATUS(c->bgen_raw[slot].ensure(static_cast<size_t>(raw_stride) * count));
   for (auto* b : {&c->bgen_off[slot], &c->bgen_size[slot], &c->bgen_len[slot]}) PG_CHECK_STATUS(b->ensure(count));
   PG_CHECK_STATUS(c->bgen_zstatus[slot].ensure(count));

@@ -51,37 +51,26 @@ struct WarpSmem {
   uint16_t codes[288];
 };
 
+// Bit input over an absolute bit position: every peek is two aligned 32-bit loads and a
+// funnel shift (no refill loop, no branches). The stream's bytes may be followed by other
+// data (the next stream, or >= 8 bytes of padding): peeks past the end read those, and
+// truncation is detected by comparing the position with the end after each step.
 struct Bits {
-  const uint8_t* in;
-  int64_t len, pos;  // next byte to load
-  uint64_t buf;
-  int cnt;
-  bool ok;
+  const uint32_t* w;  // 4-byte aligned base
+  const uint8_t* b8;  // same base, bytes
+  uint32_t bp;        // absolute bit position from w
+  uint32_t end;       // bit position just past the stream
 
-  __device__ __forceinline__ void refill() {
-    while (cnt <= 56 && pos < len) {
-      buf |= static_cast<uint64_t>(__ldg(in + pos)) << cnt;
-      ++pos;
-      cnt += 8;
-    }
+  __device__ __forceinline__ uint32_t peek32() const {
+    const uint32_t i = bp >> 5;
+    return __funnelshift_r(__ldg(w + i), __ldg(w + i + 1), bp & 31);
   }
-  __device__ __forceinline__ bool need(int n) {
-    if (cnt < n) refill();
-    if (cnt < n) ok = false;
-    return ok;
-  }
-  __device__ __forceinline__ uint32_t peek(int n) const { return static_cast<uint32_t>(buf & ((1ull << n) - 1)); }
-  __device__ __forceinline__ void drop(int n) {
-    buf >>= n;
-    cnt -= n;
-  }
-  __device__ __forceinline__ uint32_t get(int n) {
-    if (n == 0) return 0;
-    if (!need(n)) return 0;
-    const uint32_t v = peek(n);
-    drop(n);
+  __device__ __forceinline__ uint32_t get(int n) {  // n <= 16
+    const uint32_t v = peek32() & ((1u << n) - 1u);
+    bp += n;
     return v;
   }
+  __device__ __forceinline__ bool ok() const { return bp <= end; }
 };
 
 // Build the decode structures for lens[0..n) (lane 0 computes codes, the warp fills the
@@ -137,28 +126,21 @@ __device__ bool build(const uint8_t* lens, int n, Huff& h, uint16_t* codes, int 
 
 // Decode one symbol; -1 on error.
 __device__ __forceinline__ int decode(Bits& br, const Huff& h) {
-  if (br.cnt < 15) br.refill();  // fewer than 15 bits may legitimately remain at the end
-  if (br.cnt == 0) {
-    br.ok = false;
-    return -1;
-  }
-  // bits past cnt read as zero; an entry only counts if its length is available
-  const uint16_t e = h.lut[br.peek(h.lut_bits)];
-  if (e && (e >> 9) <= br.cnt) {
-    br.drop(e >> 9);
+  const uint32_t bits = br.peek32();
+  const uint16_t e = h.lut[bits & ((1u << h.lut_bits) - 1u)];
+  if (e) {
+    br.bp += e >> 9;
     return e & 511;
   }
-  // slow path: canonical decode bit by bit (codes longer than the table)
+  // slow path: canonical decode bit by bit (codes longer than the table, or invalid)
   int code = 0, first = 0, index = 0;
   for (int l = 1; l < 16; ++l) {
-    if (br.cnt < 1) {
-      br.ok = false;
-      return -1;
-    }
-    code |= static_cast<int>(br.peek(1));
-    br.drop(1);
+    code |= static_cast<int>((bits >> (l - 1)) & 1u);
     const int c = h.count[l];
-    if (code - c < first) return h.sym[index + (code - first)];
+    if (code - c < first) {
+      br.bp += l;
+      return h.sym[index + (code - first)];
+    }
     index += c;
     first += c;
     first <<= 1;
@@ -181,56 +163,57 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
   if (stream >= count) return;
 
   Bits br;
-  br.in = blob + off[stream] + skip;
-  br.len = len[stream] - skip;
-  br.pos = 0;
-  br.buf = 0;
-  br.cnt = 0;
-  br.ok = br.len >= 0;
+  {
+    const uint8_t* start = blob + off[stream] + skip;
+    const uintptr_t base = reinterpret_cast<uintptr_t>(start) & ~uintptr_t(3);
+    br.w = reinterpret_cast<const uint32_t*>(base);
+    br.b8 = reinterpret_cast<const uint8_t*>(base);
+    br.bp = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(start) - base) * 8u;
+    const int64_t n_in = len[stream] - skip;
+    br.end = n_in < 0 ? 0 : br.bp + static_cast<uint32_t>(n_in) * 8u;
+  }
   uint8_t* dst = out + stream * out_stride;
-  int64_t pos = 0;
-  int err = 0;
+  const int32_t cap = static_cast<int32_t>(out_stride);
+  int32_t pos = 0;
+  int err = len[stream] - skip < 2 ? 1 : 0;
 
   Huff lit{sm.lit_lut, kLitBits, {}, sm.lit_sym};
   Huff dist{sm.dist_lut, kDistBits, {}, sm.dist_sym};
   Huff clen{sm.clen_lut, kClenBits, {}, sm.clen_sym};
 
   // zlib header
-  {
+  if (!err) {
     const uint32_t cmf = br.get(8), flg = br.get(8);
-    if (!br.ok || (cmf & 15) != 8 || (cmf >> 4) > 7 || ((cmf << 8) | flg) % 31 != 0 || (flg & 0x20)) err = 1;
+    if ((cmf & 15) != 8 || (cmf >> 4) > 7 || ((cmf << 8) | flg) % 31 != 0 || (flg & 0x20)) err = 1;
   }
   bool last = false;
   while (!err && !last) {
     last = br.get(1);
     const uint32_t type = br.get(2);
-    if (!br.ok) {
+    if (!br.ok()) {
       err = 1;
       break;
     }
     if (type == 0) {
-      // stored block: drop to the byte boundary, then LEN, NLEN and raw bytes
-      br.drop(br.cnt & 7);
-      const int64_t byte_pos = br.pos - br.cnt / 8;
-      br.buf = 0;
-      br.cnt = 0;
-      if (byte_pos + 4 > br.len) {
+      // stored block: skip to the byte boundary, then LEN, NLEN and raw bytes
+      const uint32_t byte_pos = (br.bp + 7) >> 3;
+      if (byte_pos * 8 + 32 > br.end) {
         err = 1;
         break;
       }
-      const uint32_t n = br.in[byte_pos] | (br.in[byte_pos + 1] << 8);
-      const uint32_t nn = br.in[byte_pos + 2] | (br.in[byte_pos + 3] << 8);
-      if ((n ^ 0xFFFFu) != nn || byte_pos + 4 + n > br.len) {
+      const uint32_t n = br.b8[byte_pos] | (br.b8[byte_pos + 1] << 8);
+      const uint32_t nn = br.b8[byte_pos + 2] | (br.b8[byte_pos + 3] << 8);
+      if ((n ^ 0xFFFFu) != nn || (byte_pos + 4 + n) * 8 > br.end) {
         err = 1;
         break;
       }
-      if (pos + n > out_stride) {
+      if (pos + static_cast<int32_t>(n) > cap) {
         err = 2;
         break;
       }
-      for (uint32_t j = lane; j < n; j += 32) dst[pos + j] = br.in[byte_pos + 4 + j];
+      for (uint32_t j = lane; j < n; j += 32) dst[pos + j] = br.b8[byte_pos + 4 + j];
       pos += n;
-      br.pos = byte_pos + 4 + n;
+      br.bp = (byte_pos + 4 + n) * 8;
       __syncwarp();
       continue;
     }
@@ -246,14 +229,14 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
       build(sm.lens + 288, 32, dist, sm.codes, 2, lane);
     } else {
       const int hlit = br.get(5) + 257, hdist = br.get(5) + 1, hclen = br.get(4) + 4;
-      if (!br.ok || hlit > 286 || hdist > 30) {
+      if (!br.ok() || hlit > 286 || hdist > 30) {
         err = 1;
         break;
       }
       uint8_t cl[19];
       for (int i = 0; i < 19; ++i) cl[i] = 0;
       for (int i = 0; i < hclen; ++i) cl[c_clen_order[i]] = static_cast<uint8_t>(br.get(3));
-      if (!br.ok) {
+      if (!br.ok()) {
         err = 1;
         break;
       }
@@ -294,7 +277,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
         } else {
           rep = 11 + br.get(7);
         }
-        if (!br.ok || idx + rep > total) {
+        if (!br.ok() || idx + rep > total) {
           err = 1;
           break;
         }
@@ -302,7 +285,10 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
         idx += rep;
         lens_buf_last = val;
       }
-      if (err) break;
+      if (err || !br.ok()) {
+        err = 1;
+        break;
+      }
       __syncwarp();
       if (sm.lens[256] == 0) {  // no end-of-block code
         err = 1;
@@ -326,12 +312,12 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
     // ---- compressed data
     for (;;) {
       const int sym = decode(br, lit);
-      if (sym < 0) {
-        err = 1;
-        break;
-      }
       if (sym < 256) {
-        if (pos >= out_stride) {
+        if (sym < 0 || br.bp > br.end) {
+          err = 1;
+          break;
+        }
+        if (pos >= cap) {
           err = 2;
           break;
         }
@@ -339,7 +325,10 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
         ++pos;
         continue;
       }
-      if (sym == 256) break;
+      if (sym == 256) {
+        if (!br.ok()) err = 1;
+        break;
+      }
       const int li = sym - 257;
       if (li >= 29) {
         err = 1;
@@ -352,11 +341,11 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
         break;
       }
       const int distance = c_dist_base[ds] + static_cast<int>(br.get(c_dist_extra[ds]));
-      if (!br.ok || distance > pos) {
+      if (!br.ok() || distance > pos) {
         err = 1;
         break;
       }
-      if (pos + length > out_stride) {
+      if (pos + length > cap) {
         err = 2;
         break;
       }
@@ -372,17 +361,16 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
   }
   // Adler-32 trailer (big-endian, byte aligned after the last block)
   if (!err) {
-    br.drop(br.cnt & 7);
-    const int64_t byte_pos = br.pos - br.cnt / 8;
-    if (byte_pos + 4 > br.len) {
+    const uint32_t byte_pos = (br.bp + 7) >> 3;
+    if (byte_pos * 8 + 32 > br.end) {
       err = 1;
     } else {
-      const uint32_t want = (static_cast<uint32_t>(br.in[byte_pos]) << 24) | (br.in[byte_pos + 1] << 16) |
-                            (br.in[byte_pos + 2] << 8) | br.in[byte_pos + 3];
+      const uint32_t want = (static_cast<uint32_t>(br.b8[byte_pos]) << 24) | (br.b8[byte_pos + 1] << 16) |
+                            (br.b8[byte_pos + 2] << 8) | br.b8[byte_pos + 3];
       __syncwarp();
       unsigned long long s1 = 0, s2 = 0;
-      const int64_t chunk = (pos + 31) / 32;
-      const int64_t a = lane * chunk, e = min(pos, a + chunk);
+      const int64_t chunk = (static_cast<int64_t>(pos) + 31) / 32;
+      const int64_t a = lane * chunk, e = min(static_cast<int64_t>(pos), a + chunk);
       for (int64_t i = a; i < e; ++i) {
         const unsigned long long d = dst[i];
         s1 += d;
@@ -433,7 +421,7 @@ extern "C" int pg_debug_inflate(const void* blob, int64_t blob_bytes, const int6
     rc = PG_ERR_CUDA;
   };
   cudaError_t e;
-  if ((e = cudaMalloc(&d_blob, blob_bytes)) != cudaSuccess ||
+  if ((e = cudaMalloc(&d_blob, blob_bytes + 16)) != cudaSuccess ||  // decoder peeks up to 8 B past a stream
       (e = cudaMalloc(&d_out, static_cast<size_t>(out_stride) * count)) != cudaSuccess ||
       (e = cudaMalloc(&d_off, sizeof(int64_t) * count)) != cudaSuccess ||
       (e = cudaMalloc(&d_size, sizeof(int64_t) * count)) != cudaSuccess ||
