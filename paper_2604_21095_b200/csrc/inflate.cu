@@ -1,16 +1,23 @@
 // zlib / DEFLATE (RFC 1950 / 1951) decoder on the GPU, one warp per stream.
 //
 // The reference inflates every BGEN genotype block on the host with zlib.decompress
-// (/root/reference/pkg/src/panelgwas/genotypes/bgen.py:188-196). A batch holds tens of
-// thousands of independent streams, so the B200 decodes them in parallel: each warp owns
-// one stream, all 32 lanes run the (inherently serial) Huffman decode in lock-step on the
-// same bit buffer (table reads are shared-memory broadcasts), lane 0 writes literals and
-// the warp copies LZ77 matches 32 bytes per step. Per-warp tables live in shared memory:
-// a 2^10-entry first-level table for literal/length codes, 2^8 for distances, 2^7 for
-// code-length codes, plus canonical (count, symbol) arrays for the rare longer codes.
-// The zlib header and the Adler-32 trailer are checked like zlib does (warp-parallel
-// checksum). Any malformed stream is reported per stream (status != 0); the caller
-// re-inflates that one block with host zlib to raise zlib's own message.
+// (/root/reference/pkg/src/panelgwas/genotypes/bgen.py:188-196). A batch holds thousands
+// of independent streams, so the B200 decodes them in parallel: each warp owns one stream
+// and all 32 lanes run the (inherently serial) Huffman decode in lock-step on the same
+// register bit buffer; table reads are shared-memory broadcasts, lane 0 writes literals
+// and the warp copies LZ77 matches up to 32 bytes per step.
+//
+// Latency is what bounds a warp here (one symbol depends on the previous one), so the hot
+// loop avoids global-memory round trips: the bit buffer is refilled 32 bits at a time
+// from the next aligned input word (prefetched one refill ahead), and the last 4 KB of
+// output are mirrored in a per-warp shared-memory ring that serves match sources (typical
+// BGEN distances are short); only farther matches read back from global memory.
+//
+// Per-warp shared memory: first-level tables (2^10 literal/length, 2^8 distance,
+// 2^7 code-length entries), canonical (count, symbol) arrays for longer codes, and the
+// ring. The zlib header and the Adler-32 trailer are checked like zlib does. Malformed
+// streams are reported per stream (status != 0); the caller re-inflates that one block
+// with host zlib to raise zlib's own message.
 #include <cstdint>
 
 #include "inflate.cuh"
@@ -22,6 +29,8 @@ constexpr int kLitBits = 10;
 constexpr int kDistBits = 8;
 constexpr int kClenBits = 7;
 constexpr int kWarpsPerBlock = 4;
+constexpr int kRing = 4096;             // bytes of recent output mirrored in smem
+constexpr int kRingSafe = kRing - 258;  // a copy never overwrites its own sources
 
 __constant__ uint16_t c_len_base[29] = {3,  4,  5,  6,  7,  8,  9,  10, 11,  13,  15,  17,  19,  23, 27,
                                         31, 35, 43, 51, 59, 67, 83, 99, 115, 131, 163, 195, 227, 258};
@@ -31,119 +40,118 @@ __constant__ uint16_t c_dist_base[30] = {1,   2,   3,   4,   5,   7,    9,    13
 __constant__ uint8_t c_dist_extra[30] = {0, 0, 0, 0, 1, 1, 2, 2, 3, 3, 4, 4, 5, 5, 6, 6, 7, 7, 8, 8, 9, 9, 10, 10, 11, 11, 12, 12, 13, 13};
 __constant__ uint8_t c_clen_order[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
 
-// Canonical Huffman code (RFC 1951 §3.2.2) with a first-level lookup table.
-// lut entry: (length << 9) | symbol, 0 = longer than the table (slow path) or invalid.
-struct Huff {
-  uint16_t* lut;
-  int lut_bits;
+// One canonical Huffman code (RFC 1951 §3.2.2): first-level table entries
+// (length << 9) | symbol (0 = longer than the table, or no such code) + canonical arrays.
+template <int BITS, int NSYM>
+struct Table {
+  uint16_t lut[1 << BITS];
   uint16_t count[16];
-  uint16_t* sym;  // symbols ordered by (length, value)
+  uint16_t sym[NSYM];
 };
 
 struct WarpSmem {
-  uint16_t lit_lut[1 << kLitBits];
-  uint16_t dist_lut[1 << kDistBits];
-  uint16_t clen_lut[1 << kClenBits];
-  uint16_t lit_sym[288];
-  uint16_t dist_sym[32];
-  uint16_t clen_sym[19];
-  uint8_t lens[288 + 32];
+  Table<kLitBits, 288> lit;
+  Table<kDistBits, 32> dist;
+  Table<kClenBits, 19> clen;
   uint16_t codes[288];
+  uint8_t lens[288 + 32];
+  uint8_t ring[kRing];
 };
 
-// Bit input over an absolute bit position: every peek is two aligned 32-bit loads and a
-// funnel shift (no refill loop, no branches). The stream's bytes may be followed by other
-// data (the next stream, or >= 8 bytes of padding): peeks past the end read those, and
-// truncation is detected by comparing the position with the end after each step.
+// Register bit buffer over 4-byte aligned input words. After refill(): cnt >= 33.
 struct Bits {
-  const uint32_t* w;  // 4-byte aligned base
-  const uint8_t* b8;  // same base, bytes
-  uint32_t bp;        // absolute bit position from w
-  uint32_t end;       // bit position just past the stream
-
-  __device__ __forceinline__ uint32_t peek32() const {
-    const uint32_t i = bp >> 5;
-    return __funnelshift_r(__ldg(w + i), __ldg(w + i + 1), bp & 31);
+  const uint32_t* w;
+  uint32_t wi;     // next word to load
+  uint32_t nextw;  // w[wi], loaded one refill ahead
+  uint64_t buf;
+  int cnt;
+  uint32_t end;  // stream end, in bits from w
+  __device__ __forceinline__ void refill() {
+    if (cnt <= 32) {
+      buf |= static_cast<uint64_t>(nextw) << cnt;
+      cnt += 32;
+      nextw = __ldg(w + (++wi));
+    }
   }
-  __device__ __forceinline__ uint32_t get(int n) {  // n <= 16
-    const uint32_t v = peek32() & ((1u << n) - 1u);
-    bp += n;
+  __device__ __forceinline__ uint32_t get(int n) {  // n <= 32 buffered bits
+    const uint32_t v = static_cast<uint32_t>(buf) & static_cast<uint32_t>((1ull << n) - 1ull);
+    buf >>= n;
+    cnt -= n;
     return v;
   }
-  __device__ __forceinline__ bool ok() const { return bp <= end; }
+  __device__ __forceinline__ uint32_t consumed() const { return wi * 32u - static_cast<uint32_t>(cnt); }
+  __device__ __forceinline__ bool ok() const { return consumed() <= end; }
 };
 
-// Build the decode structures for lens[0..n) (lane 0 computes codes, the warp fills the
-// table). zlib's completeness rules (inflate_table): over-subscribed -> error; incomplete
-// only for a single code of length 1 (kind 1/2), never for code-length codes (kind 0).
-__device__ bool build(const uint8_t* lens, int n, Huff& h, uint16_t* codes, int kind, int lane) {
-  for (int i = 0; i < 16; ++i) h.count[i] = 0;
-  for (int s = 0; s < n; ++s) ++h.count[lens[s]];
+// zlib's completeness rules (inflate_table): over-subscribed -> error; an incomplete code
+// only for a single code of length 1 (lit/len, dist); never for code-length codes.
+template <int BITS, int NSYM>
+__device__ bool build(Table<BITS, NSYM>& t, const uint8_t* lens, int n, uint16_t* codes, bool code_lengths,
+                      int lane) {
+  uint16_t count[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) count[i] = 0;
+  for (int s = 0; s < n; ++s) ++count[lens[s]];
   int left = 1, max_len = 0;
+#pragma unroll
   for (int l = 1; l < 16; ++l) {
-    left <<= 1;
-    left -= h.count[l];
-    if (left < 0) return false;  // over-subscribed
-    if (h.count[l]) max_len = l;
+    left = (left << 1) - count[l];
+    if (left < 0) return false;
+    if (count[l]) max_len = l;
   }
-  if (left > 0 && (kind == 0 || max_len != 1)) {
-    if (!(kind != 0 && max_len == 0)) return false;  // incomplete (an all-zero distance set is allowed)
-  }
-  // canonical codes + symbol order (lane 0; <= 288 symbols)
+  if (left > 0 && (code_lengths || max_len != 1) && !(!code_lengths && max_len == 0)) return false;
   if (lane == 0) {
     uint16_t next[16], offs[16];
     int code = 0, off = 0;
-    h.count[0] = 0;
+    count[0] = 0;
     for (int l = 1; l < 16; ++l) {
-      code = (code + h.count[l - 1]) << 1;
+      code = (code + count[l - 1]) << 1;
       next[l] = static_cast<uint16_t>(code);
       offs[l] = static_cast<uint16_t>(off);
-      off += h.count[l];
+      off += count[l];
+      t.count[l] = count[l];
     }
     for (int s = 0; s < n; ++s) {
       const int l = lens[s];
       if (l) {
         codes[s] = next[l]++;
-        h.sym[offs[l]++] = static_cast<uint16_t>(s);
+        t.sym[offs[l]++] = static_cast<uint16_t>(s);
       }
     }
   }
-  __syncwarp();
-  const int size = 1 << h.lut_bits;
-  for (int i = lane; i < size; i += 32) h.lut[i] = 0;
+  for (int i = lane; i < (1 << BITS); i += 32) t.lut[i] = 0;
   __syncwarp();
   for (int s = lane; s < n; s += 32) {
     const int l = lens[s];
-    if (l == 0 || l > h.lut_bits) continue;
-    // DEFLATE codes are read LSB first: index the table by the bit-reversed code
+    if (l == 0 || l > BITS) continue;
+    // codes are read LSB first: index the table by the bit-reversed code
     const uint32_t rev = __brev(static_cast<uint32_t>(codes[s])) >> (32 - l);
     const uint16_t e = static_cast<uint16_t>((l << 9) | s);
-    for (uint32_t i = rev; i < static_cast<uint32_t>(size); i += 1u << l) h.lut[i] = e;
+    for (uint32_t i = rev; i < (1u << BITS); i += 1u << l) t.lut[i] = e;
   }
   __syncwarp();
   return true;
 }
 
-// Decode one symbol; -1 on error.
-__device__ __forceinline__ int decode(Bits& br, const Huff& h) {
-  const uint32_t bits = br.peek32();
-  const uint16_t e = h.lut[bits & ((1u << h.lut_bits) - 1u)];
+// One symbol (the caller refilled: >= 33 buffered bits); -1 = no valid code.
+template <int BITS, int NSYM>
+__device__ __forceinline__ int decode(Bits& br, const Table<BITS, NSYM>& t) {
+  const uint32_t bits = static_cast<uint32_t>(br.buf);
+  const uint16_t e = t.lut[bits & ((1u << BITS) - 1u)];
   if (e) {
-    br.bp += e >> 9;
+    br.get(e >> 9);
     return e & 511;
   }
-  // slow path: canonical decode bit by bit (codes longer than the table, or invalid)
   int code = 0, first = 0, index = 0;
   for (int l = 1; l < 16; ++l) {
     code |= static_cast<int>((bits >> (l - 1)) & 1u);
-    const int c = h.count[l];
+    const int c = t.count[l];
     if (code - c < first) {
-      br.bp += l;
-      return h.sym[index + (code - first)];
+      br.get(l);
+      return t.sym[index + (code - first)];
     }
     index += c;
-    first += c;
-    first <<= 1;
+    first = (first + c) << 1;
     code <<= 1;
   }
   return -1;
@@ -157,52 +165,52 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
                                                                      int* __restrict__ status) {
   __shared__ WarpSmem sm_all[kWarpsPerBlock];
   const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
-  WarpSmem& sm = sm_all[wib];
-  const int64_t stream = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + wib;
+  WarpSmem& sm = sm_all[threadIdx.x >> 5];
+  const int64_t stream = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
   if (stream >= count) return;
 
+  const uint8_t* start = blob + off[stream] + skip;
+  const int64_t n_in = len[stream] - skip;
+  const uintptr_t base = reinterpret_cast<uintptr_t>(start) & ~uintptr_t(3);
+  const uint8_t* b8 = reinterpret_cast<const uint8_t*>(base);
+  const uint32_t lead = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(start) - base) * 8u;
   Bits br;
-  {
-    const uint8_t* start = blob + off[stream] + skip;
-    const uintptr_t base = reinterpret_cast<uintptr_t>(start) & ~uintptr_t(3);
-    br.w = reinterpret_cast<const uint32_t*>(base);
-    br.b8 = reinterpret_cast<const uint8_t*>(base);
-    br.bp = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(start) - base) * 8u;
-    const int64_t n_in = len[stream] - skip;
-    br.end = n_in < 0 ? 0 : br.bp + static_cast<uint32_t>(n_in) * 8u;
-  }
-  uint8_t* dst = out + stream * out_stride;
+  br.w = reinterpret_cast<const uint32_t*>(base);
+  br.wi = 0;
+  br.nextw = __ldg(br.w);
+  br.buf = 0;
+  br.cnt = 0;
+  br.end = n_in < 0 ? 0 : lead + static_cast<uint32_t>(n_in) * 8u;
+  br.refill();
+  br.refill();
+  br.get(lead);
+  uint8_t* const dst = out + stream * out_stride;
   const int32_t cap = static_cast<int32_t>(out_stride);
   int32_t pos = 0;
-  int err = len[stream] - skip < 2 ? 1 : 0;
+  int err = n_in < 2 ? 1 : 0;
 
-  Huff lit{sm.lit_lut, kLitBits, {}, sm.lit_sym};
-  Huff dist{sm.dist_lut, kDistBits, {}, sm.dist_sym};
-  Huff clen{sm.clen_lut, kClenBits, {}, sm.clen_sym};
-
-  // zlib header
-  if (!err) {
+  if (!err) {  // zlib header: CM 8, CINFO <= 7, FCHECK, no preset dictionary
     const uint32_t cmf = br.get(8), flg = br.get(8);
     if ((cmf & 15) != 8 || (cmf >> 4) > 7 || ((cmf << 8) | flg) % 31 != 0 || (flg & 0x20)) err = 1;
   }
   bool last = false;
   while (!err && !last) {
+    br.refill();
     last = br.get(1);
     const uint32_t type = br.get(2);
-    if (!br.ok()) {
+    if (!br.ok() || type == 3) {
       err = 1;
       break;
     }
     if (type == 0) {
-      // stored block: skip to the byte boundary, then LEN, NLEN and raw bytes
-      const uint32_t byte_pos = (br.bp + 7) >> 3;
+      // stored block: byte boundary, LEN, NLEN, raw bytes; the bit buffer restarts after it
+      const uint32_t byte_pos = (br.consumed() + 7) >> 3;
       if (byte_pos * 8 + 32 > br.end) {
         err = 1;
         break;
       }
-      const uint32_t n = br.b8[byte_pos] | (br.b8[byte_pos + 1] << 8);
-      const uint32_t nn = br.b8[byte_pos + 2] | (br.b8[byte_pos + 3] << 8);
+      const uint32_t n = b8[byte_pos] | (b8[byte_pos + 1] << 8);
+      const uint32_t nn = b8[byte_pos + 2] | (b8[byte_pos + 3] << 8);
       if ((n ^ 0xFFFFu) != nn || (byte_pos + 4 + n) * 8 > br.end) {
         err = 1;
         break;
@@ -211,109 +219,111 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
         err = 2;
         break;
       }
-      for (uint32_t j = lane; j < n; j += 32) dst[pos + j] = br.b8[byte_pos + 4 + j];
+      for (uint32_t j = lane; j < n; j += 32) {
+        const uint8_t v = b8[byte_pos + 4 + j];
+        dst[pos + j] = v;
+        sm.ring[(pos + j) & (kRing - 1)] = v;
+      }
       pos += n;
-      br.bp = (byte_pos + 4 + n) * 8;
+      const uint32_t next_bit = (byte_pos + 4 + n) * 8;
+      br.wi = next_bit >> 5;
+      br.nextw = __ldg(br.w + br.wi);
+      br.buf = 0;
+      br.cnt = 0;
+      br.refill();
+      br.refill();
+      br.get(next_bit & 31);
       __syncwarp();
       continue;
     }
-    if (type == 3) {
-      err = 1;
-      break;
-    }
     if (type == 1) {
-      for (int s = lane; s < 288; s += 32) sm.lens[s] = s < 144 ? 8 : s < 256 ? 9 : s < 280 ? 7 : 8;
-      for (int s = lane; s < 32; s += 32) sm.lens[288 + s] = 5;  // 30, 31 complete the code, never valid
+      for (int s = lane; s < 320; s += 32) sm.lens[s] = s < 144 ? 8 : s < 256 ? 9 : s < 280 ? 7 : s < 288 ? 8 : 5;
       __syncwarp();
-      build(sm.lens, 288, lit, sm.codes, 1, lane);
-      build(sm.lens + 288, 32, dist, sm.codes, 2, lane);
+      build(sm.lit, sm.lens, 288, sm.codes, false, lane);
+      build(sm.dist, sm.lens + 288, 32, sm.codes, false, lane);  // 30, 31 complete the code, never valid
     } else {
       const int hlit = br.get(5) + 257, hdist = br.get(5) + 1, hclen = br.get(4) + 4;
-      if (!br.ok() || hlit > 286 || hdist > 30) {
+      if (hlit > 286 || hdist > 30) {
         err = 1;
         break;
       }
+      br.refill();
       uint8_t cl[19];
+#pragma unroll
       for (int i = 0; i < 19; ++i) cl[i] = 0;
-      for (int i = 0; i < hclen; ++i) cl[c_clen_order[i]] = static_cast<uint8_t>(br.get(3));
-      if (!br.ok()) {
-        err = 1;
-        break;
+      for (int i = 0; i < hclen; ++i) {
+        if (i == 10) br.refill();
+        cl[c_clen_order[i]] = static_cast<uint8_t>(br.get(3));
       }
-      for (int s = lane; s < 19; s += 32) sm.lens[s] = cl[s];
+      if (lane < 19) sm.lens[lane] = cl[lane];
       __syncwarp();
-      if (!build(sm.lens, 19, clen, sm.codes, 0, lane)) {
+      if (!build(sm.clen, sm.lens, 19, sm.codes, true, lane)) {
         err = 1;
         break;
       }
-      // literal/length + distance code lengths (run-length coded); every lane decodes,
-      // lane 0 stores, so the loop stays uniform
+      // literal/length + distance code lengths (run-length coded); every lane decodes
       int idx = 0;
       const int total = hlit + hdist;
-      uint8_t lens_buf_last = 0;
+      uint8_t prev = 0;
       while (idx < total) {
-        const int sym = decode(br, clen);
+        br.refill();
+        const int sym = decode(br, sm.clen);
         if (sym < 0) {
           err = 1;
           break;
         }
         if (sym < 16) {
           if (lane == 0) sm.lens[idx] = static_cast<uint8_t>(sym);
-          lens_buf_last = static_cast<uint8_t>(sym);
+          prev = static_cast<uint8_t>(sym);
           ++idx;
           continue;
         }
-        int rep = 0;
+        int rep;
         uint8_t val = 0;
         if (sym == 16) {
           if (idx == 0) {
             err = 1;
             break;
           }
-          val = lens_buf_last;
+          val = prev;
           rep = 3 + br.get(2);
         } else if (sym == 17) {
           rep = 3 + br.get(3);
         } else {
           rep = 11 + br.get(7);
         }
-        if (!br.ok() || idx + rep > total) {
+        if (idx + rep > total) {
           err = 1;
           break;
         }
         for (int j = lane; j < rep; j += 32) sm.lens[idx + j] = val;
         idx += rep;
-        lens_buf_last = val;
+        prev = val;
       }
       if (err || !br.ok()) {
         err = 1;
         break;
       }
       __syncwarp();
-      if (sm.lens[256] == 0) {  // no end-of-block code
+      if (sm.lens[256] == 0 || !build(sm.lit, sm.lens, hlit, sm.codes, false, lane)) {
         err = 1;
         break;
       }
-      // distance lengths live right after the hlit literal/length lengths
-      if (!build(sm.lens, hlit, lit, sm.codes, 1, lane)) {
-        err = 1;
-        break;
-      }
-      // distance lengths -> their own slot (ranges may overlap: read all, then write)
-      const uint8_t dl = lane < hdist ? sm.lens[hlit + lane] : 0;
+      const uint8_t dl = lane < hdist ? sm.lens[hlit + lane] : 0;  // ranges may overlap
       __syncwarp();
       if (lane < hdist) sm.lens[288 + lane] = dl;
       __syncwarp();
-      if (!build(sm.lens + 288, hdist, dist, sm.codes, 2, lane)) {
+      if (!build(sm.dist, sm.lens + 288, hdist, sm.codes, false, lane)) {
         err = 1;
         break;
       }
     }
     // ---- compressed data
     for (;;) {
-      const int sym = decode(br, lit);
+      br.refill();
+      const int sym = decode(br, sm.lit);
       if (sym < 256) {
-        if (sym < 0 || br.bp > br.end) {
+        if (sym < 0) {
           err = 1;
           break;
         }
@@ -321,7 +331,10 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
           err = 2;
           break;
         }
-        if (lane == 0) dst[pos] = static_cast<uint8_t>(sym);
+        if (lane == 0) {
+          dst[pos] = static_cast<uint8_t>(sym);
+          sm.ring[pos & (kRing - 1)] = static_cast<uint8_t>(sym);
+        }
         ++pos;
         continue;
       }
@@ -335,13 +348,14 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
         break;
       }
       const int length = c_len_base[li] + static_cast<int>(br.get(c_len_extra[li]));
-      const int ds = decode(br, dist);
+      br.refill();
+      const int ds = decode(br, sm.dist);
       if (ds < 0 || ds >= 30) {
         err = 1;
         break;
       }
       const int distance = c_dist_base[ds] + static_cast<int>(br.get(c_dist_extra[ds]));
-      if (!br.ok() || distance > pos) {
+      if (distance > pos || !br.ok()) {
         err = 1;
         break;
       }
@@ -350,29 +364,32 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
         break;
       }
       __syncwarp();  // earlier literals / copies by other lanes are visible
-      // overlapping matches repeat the last `distance` bytes: source index j mod distance
-      if (distance >= length) {
-        for (int j = lane; j < length; j += 32) dst[pos + j] = dst[pos - distance + j];
-      } else {
-        for (int j = lane; j < length; j += 32) dst[pos + j] = dst[pos - distance + (j % distance)];
+      // an overlapping match repeats the last `distance` bytes: source offset j mod distance
+      for (int j = lane; j < length; j += 32) {
+        const int jj = distance >= length ? j : j % distance;
+        const int src = pos - distance + jj;
+        const uint8_t v = distance <= kRingSafe ? sm.ring[src & (kRing - 1)] : dst[src];
+        dst[pos + j] = v;
+        sm.ring[(pos + j) & (kRing - 1)] = v;
       }
       pos += length;
+      __syncwarp();
     }
   }
   // Adler-32 trailer (big-endian, byte aligned after the last block)
   if (!err) {
-    const uint32_t byte_pos = (br.bp + 7) >> 3;
+    const uint32_t byte_pos = (br.consumed() + 7) >> 3;
     if (byte_pos * 8 + 32 > br.end) {
       err = 1;
     } else {
-      const uint32_t want = (static_cast<uint32_t>(br.b8[byte_pos]) << 24) | (br.b8[byte_pos + 1] << 16) |
-                            (br.b8[byte_pos + 2] << 8) | br.b8[byte_pos + 3];
+      const uint32_t want = (static_cast<uint32_t>(b8[byte_pos]) << 24) | (b8[byte_pos + 1] << 16) |
+                            (b8[byte_pos + 2] << 8) | b8[byte_pos + 3];
       __syncwarp();
       unsigned long long s1 = 0, s2 = 0;
-      const int64_t chunk = (static_cast<int64_t>(pos) + 31) / 32;
-      const int64_t a = lane * chunk, e = min(static_cast<int64_t>(pos), a + chunk);
-      for (int64_t i = a; i < e; ++i) {
-        const unsigned long long d = dst[i];
+      const int32_t chunk = (pos + 31) / 32;
+      const int32_t a = lane * chunk, e = min(pos, a + chunk);
+      for (int32_t i = a; i < e; ++i) {
+        const uint32_t d = dst[i];
         s1 += d;
         s2 += static_cast<unsigned long long>(pos - i) * d;
       }
@@ -416,25 +433,25 @@ extern "C" int pg_debug_inflate(const void* blob, int64_t blob_bytes, const int6
   int64_t *d_off = nullptr, *d_size = nullptr, *d_len = nullptr;
   int* d_status = nullptr;
   int rc = PG_OK;
-  auto fail = [&](cudaError_t e) {
-    set_error("pg_debug_inflate: %s", cudaGetErrorString(e));
-    rc = PG_ERR_CUDA;
-  };
   cudaError_t e;
-  if ((e = cudaMalloc(&d_blob, blob_bytes + 16)) != cudaSuccess ||  // decoder peeks up to 8 B past a stream
+  if ((e = cudaMalloc(&d_blob, blob_bytes + 16)) != cudaSuccess ||  // the decoder reads ahead <= 8 bytes
       (e = cudaMalloc(&d_out, static_cast<size_t>(out_stride) * count)) != cudaSuccess ||
       (e = cudaMalloc(&d_off, sizeof(int64_t) * count)) != cudaSuccess ||
       (e = cudaMalloc(&d_size, sizeof(int64_t) * count)) != cudaSuccess ||
       (e = cudaMalloc(&d_len, sizeof(int64_t) * count)) != cudaSuccess ||
       (e = cudaMalloc(&d_status, sizeof(int) * count)) != cudaSuccess) {
-    fail(e);
+    set_error("pg_debug_inflate: %s", cudaGetErrorString(e));
+    rc = PG_ERR_CUDA;
   } else {
     cudaMemcpy(d_blob, blob, blob_bytes, cudaMemcpyHostToDevice);
     cudaMemcpy(d_off, off, sizeof(int64_t) * count, cudaMemcpyHostToDevice);
     cudaMemcpy(d_size, size, sizeof(int64_t) * count, cudaMemcpyHostToDevice);
     rc = inflate_streams(d_blob, d_off, d_size, count, skip, d_out, out_stride, d_len, d_status, nullptr);
     if (rc == PG_OK) {
-      if ((e = cudaDeviceSynchronize()) != cudaSuccess) fail(e);
+      if ((e = cudaDeviceSynchronize()) != cudaSuccess) {
+        set_error("pg_debug_inflate: %s", cudaGetErrorString(e));
+        rc = PG_ERR_CUDA;
+      }
       cudaMemcpy(out, d_out, static_cast<size_t>(out_stride) * count, cudaMemcpyDeviceToHost);
       cudaMemcpy(out_len, d_len, sizeof(int64_t) * count, cudaMemcpyDeviceToHost);
       cudaMemcpy(status, d_status, sizeof(int) * count, cudaMemcpyDeviceToHost);
