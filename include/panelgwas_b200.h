@@ -136,6 +136,10 @@ PG_API int pg_ctx_set_scan(pg_ctx* ctx, double df, int mode, const double* r_bar
  * tightening, engine.py:205-211 / output.py:199-200). */
 PG_API int pg_ctx_set_rbar(pg_ctx* ctx, const double* r_bar);
 
+/* Dosage sources (BGEN, real-valued dense) use the wide-digit GEMM (base-255 digits, 4 rows
+ * per marker, 3 accumulators) by default; 0 selects the balanced-ternary planes (8 / 16 rows).
+ * Both are exact integer contractions: results are bitwise identical (A/B switch). */
+PG_API int pg_ctx_set_wide_digits(pg_ctx* ctx, int enable);
 /* Tuning switch: decode PLINK rows inside the GEMM producer (default 1) or through
  * materialized int8 planes (0). Results are identical; exposed for A/B measurement. */
 PG_API int pg_ctx_set_fused_decode(pg_ctx* ctx, int enable);

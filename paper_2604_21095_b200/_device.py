@@ -174,6 +174,9 @@ class DeviceContext:
             call("pg_ctx_set_basis", self._h, ptr(qq), 0 if qq is None else qq.shape[0],
                  0 if qq is None else qq.shape[1])
 
+    def set_wide_digits(self, enable: bool) -> None:
+        call("pg_ctx_set_wide_digits", self._h, 1 if enable else 0)
+
     def set_fused_decode(self, enable: bool) -> None:
         call("pg_ctx_set_fused_decode", self._h, 1 if enable else 0)
 

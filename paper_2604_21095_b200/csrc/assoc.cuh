@@ -24,7 +24,7 @@ constexpr int64_t kWH = 32385;          // weight of the high limb: 2*(127*127+6
 constexpr int64_t kQMax = kWH * 127 + 16192;  // largest |q| representable by the limbs
 
 struct AssocEpilogue {
-  int rows_per_marker;          // 1: row = u ; 2: rows = (u, missing mask)
+  int rows_per_marker;          // ternary: 1 (u), 2 (u, missing), 8 / 16 (digits + missing); wide: 4
   int raw;                      // 1: emit s_p * (X - mu (Cq - Mq)) without the 1/den scale (side GEMM K5)
   int64_t m_valid;              // markers in this launch
   int64_t p_valid;              // phenotypes
@@ -56,5 +56,13 @@ int launch_assoc(const int8_t* qh, const int8_t* q1, const int8_t* q0, int64_t p
 int launch_assoc_packed(const int8_t* qh, const int8_t* q1, const int8_t* q0, int64_t p_pad, const uint8_t* packed,
                         int64_t pitch, int64_t n_markers, int64_t k_pad, const AssocEpilogue& ep,
                         cudaStream_t stream);
+
+// Wide-digit variant for dosage sources: one int8 plane v [c_pad, k_pad] of balanced
+// base-255 digits (rows per marker: digit0, digit1, digit2, missing mask; rows_per_marker
+// kWideRows), c_pad a multiple of kTileCWide. Three accumulators per tile.
+constexpr int kTileCWide = 128;
+constexpr int kWideRows = 4;
+int launch_assoc_wide(const int8_t* qh, const int8_t* q1, const int8_t* q0, int64_t p_pad, const int8_t* v,
+                      int64_t c_pad, int64_t k_pad, const AssocEpilogue& ep, cudaStream_t stream);
 
 }  // namespace pg

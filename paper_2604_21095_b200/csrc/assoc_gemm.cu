@@ -15,11 +15,16 @@
 // mu_m / V_m the mean / centred sum of squares of u over observed kept samples
 // (SURVEY.md appendix 3).
 //
-// Two operand paths for the genotype side (template FUSED):
-//   planes : TMA loads pre-decoded int8 planes v / 127v (any rows_per_marker)
-//   fused  : TMA loads the packed 2-bit .bed tile (256 rows x 16 B per stage) and
-//            4 decoder warps expand it in shared memory into the swizzled v / 127v
-//            operand tiles (PLINK rows without missing calls: rows_per_marker 1).
+// Three operand paths for the genotype side (template MODE):
+//   kPlanes : TMA loads pre-decoded ternary int8 planes v / 127v (rows_per_marker 1/2/8/16)
+//   kFused  : TMA loads the packed 2-bit .bed tile (256 rows x 16 B per stage) and
+//             4 decoder warps expand it in shared memory into the swizzled v / 127v
+//             operand tiles (PLINK rows without missing calls: rows_per_marker 1).
+//   kWide   : dosage sources (BGEN, real-valued dense): one int8 plane of balanced
+//             base-255 digits of u (3 digit rows + missing row per marker) against the
+//             three limbs into three accumulators (A = qH v, B = q1 v, C = q0 v,
+//             X_row = 32385 A + 127 B + C), tile N = 128 rows (3 x 128 TMEM columns):
+//             4 rows per marker instead of 8 / 16 ternary rows, 2-4x fewer MMAs.
 //
 // Structure: persistent, warp-specialised, 1 CTA per SM, 768 threads.
 //   warp 0 lane 0 : TMA producer
@@ -48,6 +53,12 @@ constexpr int kPackedBytes = kHalfC * (kTileK / 4);  // 2 KB packed .bed half-ti
 constexpr int kOffV = 3 * kQBytes;
 constexpr int kOffV127 = kOffV + kVBytes;
 constexpr int kOffPacked = kOffV127 + kVBytes;
+// wide-digit mode: 128 genotype rows per pair tile (64 per CTA), three accumulators
+constexpr int kTileCW = 128;
+constexpr int kHalfCW = kTileCW / 2;
+constexpr int kVBytesW = kHalfCW * kTileK;  // 4 KB
+constexpr int kRowsW = 4;                   // digits 255^0, 255^1, 255^2 + missing row
+constexpr int kPlanes = 0, kFused = 1, kWide = 2;
 constexpr int kEpiWarps = 16;
 constexpr int kFirstEpiWarp = 8;
 constexpr int kThreads = 32 * (kFirstEpiWarp + kEpiWarps);
@@ -60,13 +71,18 @@ constexpr int kTmemCols = 512;
 // Measured on the C3 slice (tools/sweep_l2.sh): 2.06e10 tests/s vs 1.91e10 for the
 // previous 32-tile groups; both operands evict_last (evict_first panel: -15%).
 
-template <bool FUSED>
+template <int MODE>
 struct Cfg {
-  static constexpr int kStages = 5;
-  static constexpr int kStageBytes = FUSED ? kOffPacked + 2048 : kOffPacked;  // 1 KB-aligned stages
+  static constexpr bool FUSED = MODE == kFused;
+  static constexpr bool WIDE = MODE == kWide;
+  static constexpr int kStages = WIDE ? 7 : 5;
+  // 1 KB-aligned stages
+  static constexpr int kStageBytes = WIDE ? kOffV + kVBytesW : (FUSED ? kOffPacked + 2048 : kOffPacked);
   static constexpr int kPanelBytes = 3 * kQBytes;
-  static constexpr int kTmaBytes = FUSED ? kPanelBytes : kOffPacked;  // per CTA, signalled on the leader
+  static constexpr int kTmaBytes = FUSED ? kPanelBytes : (WIDE ? kOffV + kVBytesW : kOffPacked);  // per CTA
   static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 512 /*barriers*/;
+  static constexpr int kTileRows = WIDE ? kTileCW : kTileC;  // genotype rows per pair tile
+  static constexpr int kHalfRows = kTileRows / 2;
 };
 
 __device__ __forceinline__ void tile_coords(int t, int n_ctile, int n_ptile, int group_c, int& ct, int& pt) {
@@ -107,6 +123,71 @@ __device__ __forceinline__ void decode_word(uint32_t w, uint32_t (&u)[4], uint32
   }
 }
 
+// shared tail of the epilogues: fp32 premask, fp64 r for candidates / FULL, compaction
+__device__ __forceinline__ void epilogue_value(const AssocEpilogue& ep, long long xu, long long xm, int m, int pheno,
+                                               float sc_f, double sc_d, float cq_f, long long cq, float rb, int lane,
+                                               uint32_t lanemask_lt, float& mx) {
+  const float mu = __ldg(ep.mu_f + m);
+  const float iv = ep.raw ? 1.f : __ldg(ep.invd_f + m);  // NaN for skipped / padding markers
+  const float xf = static_cast<float>(xu) - mu * (cq_f - static_cast<float>(xm));
+  const float r = xf * sc_f * iv;
+  const float ar = fabsf(r);
+  mx = fmaxf(mx, ar);
+  const bool hit = ar >= rb;
+  double r64 = 0.0;
+  if (hit || ep.full_r) {
+    r64 = sc_d * (static_cast<double>(xu) - __ldg(ep.mu_d + m) * static_cast<double>(cq - xm)) *
+          (ep.raw ? 1.0 : __ldg(ep.invd_d + m));
+  }
+  if (ep.full_r) ep.full_r[static_cast<int64_t>(m) * ep.full_ld + pheno] = r64;
+  const uint32_t mask = __ballot_sync(0xffffffffu, hit);
+  if (mask) {
+    int base = 0;
+    if (lane == 0) base = atomicAdd(ep.cand_count, __popc(mask));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (hit) {
+      const int64_t idx = static_cast<int64_t>(base) + __popc(mask & lanemask_lt);
+      if (idx < ep.cand_cap) {
+        ep.cand_key[idx] = (static_cast<unsigned long long>(m) << 32) | static_cast<unsigned>(pheno);
+        ep.cand_r[idx] = r64;
+      }
+    }
+  }
+}
+
+// wide-digit tile: per marker rows (digit0, digit1, digit2, missing); X_row = kWH A + 127 B + C
+__device__ __forceinline__ void epilogue_tile_wide(const AssocEpilogue& ep, uint32_t tA, int ct, int pheno, int lane,
+                                                   int c_begin, int c_end) {
+  constexpr int kMarkersPerTile = kTileCW / kRowsW;
+  const uint32_t lanemask_lt = (1u << lane) - 1u;
+  const float sc_f = ep.scale_f[pheno];
+  const double sc_d = ep.scale_d[pheno];
+  const float cq_f = ep.cq_f[pheno];
+  const long long cq = ep.cq[pheno];
+  const float rb = ep.rbar ? ep.rbar[pheno] : INFINITY;
+  float mx = 0.f;
+#pragma unroll 1
+  for (int c = c_begin; c < c_end; c += 16) {
+    uint32_t a[16], b[16], d[16];
+    tmem_ld_32x32b_x16(tA + c, a);
+    tmem_ld_32x32b_x16(tA + kTileCW + c, b);
+    tmem_ld_32x32b_x16(tA + 2 * kTileCW + c, d);
+    tmem_ld_wait();
+#pragma unroll
+    for (int j = 0; j < 16; j += kRowsW) {
+      long long x[kRowsW];
+#pragma unroll
+      for (int t = 0; t < kRowsW; ++t)
+        x[t] = kWH * static_cast<long long>(static_cast<int>(a[j + t])) + 127ll * static_cast<int>(b[j + t]) +
+               static_cast<int>(d[j + t]);
+      const long long xu = x[0] + 255ll * x[1] + 65025ll * x[2];
+      const int m = ct * kMarkersPerTile + (c + j) / kRowsW;
+      epilogue_value(ep, xu, x[3], m, pheno, sc_f, sc_d, cq_f, cq, rb, lane, lanemask_lt, mx);
+    }
+  }
+  if (ep.max_abs_r && pheno < ep.p_valid) atomicMax(ep.max_abs_r + pheno, __float_as_uint(mx));
+}
+
 template <int R>
 __device__ __forceinline__ void epilogue_tile(const AssocEpilogue& ep, uint32_t tH, uint32_t tL, int ct, int pheno,
                                               int lane, int c_begin, int c_end) {
@@ -140,44 +221,21 @@ __device__ __forceinline__ void epilogue_tile(const AssocEpilogue& ep, uint32_t 
         xm = kWH * static_cast<long long>(static_cast<int>(h[j + R - 1])) + static_cast<int>(l[j + R - 1]);
       }
       const int m = ct * kMarkersPerTile + (c + j) / R;
-      const float mu = __ldg(ep.mu_f + m);
-      const float iv = ep.raw ? 1.f : __ldg(ep.invd_f + m);  // NaN for skipped / padding markers
-      const float xf = static_cast<float>(xu) - mu * (cq_f - static_cast<float>(xm));
-      const float r = xf * sc_f * iv;
-      const float ar = fabsf(r);
-      mx = fmaxf(mx, ar);
-      const bool hit = ar >= rb;
-      double r64 = 0.0;
-      if (hit || ep.full_r) {
-        r64 = sc_d * (static_cast<double>(xu) - __ldg(ep.mu_d + m) * static_cast<double>(cq - xm)) *
-              (ep.raw ? 1.0 : __ldg(ep.invd_d + m));
-      }
-      if (ep.full_r) ep.full_r[static_cast<int64_t>(m) * ep.full_ld + pheno] = r64;
-      const uint32_t mask = __ballot_sync(0xffffffffu, hit);
-      if (mask) {
-        int base = 0;
-        if (lane == 0) base = atomicAdd(ep.cand_count, __popc(mask));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (hit) {
-          const int64_t idx = static_cast<int64_t>(base) + __popc(mask & lanemask_lt);
-          if (idx < ep.cand_cap) {
-            ep.cand_key[idx] = (static_cast<unsigned long long>(m) << 32) | static_cast<unsigned>(pheno);
-            ep.cand_r[idx] = r64;
-          }
-        }
-      }
+      epilogue_value(ep, xu, xm, m, pheno, sc_f, sc_d, cq_f, cq, rb, lane, lanemask_lt, mx);
     }
   }
   if (ep.max_abs_r && pheno < ep.p_valid) atomicMax(ep.max_abs_r + pheno, __float_as_uint(mx));
 }
 
-template <bool FUSED>
+template <int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     assoc_i8_kernel(const __grid_constant__ CUtensorMap tm_qh, const __grid_constant__ CUtensorMap tm_q1,
                     const __grid_constant__ CUtensorMap tm_q0, const __grid_constant__ CUtensorMap tm_v,
                     const __grid_constant__ CUtensorMap tm_v127, int n_ctile, int n_ptile, int n_kb,
                     int group_c, uint32_t l2_codes, AssocEpilogue ep) {
-  using C = Cfg<FUSED>;
+  using C = Cfg<MODE>;
+  constexpr bool FUSED = C::FUSED;
+  constexpr bool WIDE = C::WIDE;
   constexpr int S = C::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -202,7 +260,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tm_q1);
     tma_prefetch_desc(&tm_q0);
     tma_prefetch_desc(&tm_v);
-    if (!FUSED) tma_prefetch_desc(&tm_v127);
+    if (MODE == kPlanes) tma_prefetch_desc(&tm_v127);
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < S; ++s) {
@@ -232,7 +290,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         int ct, pt;
         tile_coords(t, n_ctile, n_ptile, group_c, ct, pt);
         const int prow = pt * kTileP + cr * kHalfP;
-        const int grow = ct * kTileC + cr * kHalfC;
+        const int grow = ct * C::kTileRows + cr * C::kHalfRows;
         for (int kb = 0; kb < n_kb; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = smem + s * C::kStageBytes;
@@ -245,6 +303,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if constexpr (FUSED) {
             mbar_arrive_expect_tx(&pk[s], kPackedBytes);
             tma_load_2d_hint(st + kOffPacked, &tm_v, &pk[s], kb * (kTileK / 4), grow, pol_geno);
+          } else if constexpr (WIDE) {
+            tma_load_2d_pair(st + kOffV, &tm_v, full0, kx, grow, pol_geno);
           } else {
             tma_load_2d_pair(st + kOffV, &tm_v, full0, kx, grow, pol_geno);
             tma_load_2d_pair(st + kOffV127, &tm_v127, full0, kx, grow, pol_geno);
@@ -259,9 +319,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     if (leader && lane == 0) {
       // ------------------------------------------------------------ MMA issuer (leader CTA)
-      constexpr uint32_t idesc = idesc_s8_s32(kTileP, kTileC);  // M = 256 across the pair
+      constexpr uint32_t idesc = idesc_s8_s32(kTileP, C::kTileRows);  // M = 256 across the pair
       const uint32_t dH = tmem_base;
-      const uint32_t dL = tmem_base + kTileC;
+      const uint32_t dL = tmem_base + C::kTileRows;
+      const uint32_t dC = tmem_base + 2 * C::kTileRows;  // wide mode only
       uint32_t s = 0, ph = 0, aph = 0;
       for (int t = cid; t < n_tiles; t += n_clusters) {
         mbar_wait_cluster(tempty, aph ^ 1);
@@ -280,9 +341,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int k = 0; k < kTileK / 32; ++k) {
             // +32 bytes along K inside the 64-byte swizzle row == +2 in the >>4 address field
-            mma_i8_ss_pair(dH, d_qh + 2 * k, d_v + 2 * k, idesc, acc);
-            mma_i8_ss_pair(dL, d_q1 + 2 * k, d_v127 + 2 * k, idesc, acc);
-            mma_i8_ss_pair(dL, d_q0 + 2 * k, d_v + 2 * k, idesc, 1);
+            if constexpr (WIDE) {
+              mma_i8_ss_pair(dH, d_qh + 2 * k, d_v + 2 * k, idesc, acc);
+              mma_i8_ss_pair(dL, d_q1 + 2 * k, d_v + 2 * k, idesc, acc);
+              mma_i8_ss_pair(dC, d_q0 + 2 * k, d_v + 2 * k, idesc, acc);
+            } else {
+              mma_i8_ss_pair(dH, d_qh + 2 * k, d_v + 2 * k, idesc, acc);
+              mma_i8_ss_pair(dL, d_q1 + 2 * k, d_v127 + 2 * k, idesc, acc);
+              mma_i8_ss_pair(dL, d_q0 + 2 * k, d_v + 2 * k, idesc, 1);
+            }
             acc = 1;
           }
           mma_commit_pair_multicast(&empty[s], 0x3);
@@ -344,13 +411,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_wait_cluster(tfull, aph);
       tc_fence_after();
       const uint32_t tH = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16);
-      const uint32_t tL = tH + kTileC;
-      const int c0 = cg * (kTileC / 4), c1 = c0 + kTileC / 4;
-      switch (ep.rows_per_marker) {
-        case 1: epilogue_tile<1>(ep, tH, tL, ct, pheno, lane, c0, c1); break;
-        case 2: epilogue_tile<2>(ep, tH, tL, ct, pheno, lane, c0, c1); break;
-        case 8: epilogue_tile<8>(ep, tH, tL, ct, pheno, lane, c0, c1); break;
-        default: epilogue_tile<16>(ep, tH, tL, ct, pheno, lane, c0, c1); break;
+      const uint32_t tL = tH + C::kTileRows;
+      const int c0 = cg * (C::kTileRows / 4), c1 = c0 + C::kTileRows / 4;
+      if constexpr (WIDE) {
+        epilogue_tile_wide(ep, tH, ct, pheno, lane, c0, c1);
+      } else {
+        switch (ep.rows_per_marker) {
+          case 1: epilogue_tile<1>(ep, tH, tL, ct, pheno, lane, c0, c1); break;
+          case 2: epilogue_tile<2>(ep, tH, tL, ct, pheno, lane, c0, c1); break;
+          case 8: epilogue_tile<8>(ep, tH, tL, ct, pheno, lane, c0, c1); break;
+          default: epilogue_tile<16>(ep, tH, tL, ct, pheno, lane, c0, c1); break;
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -368,16 +439,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
 constexpr uint32_t kDefaultL2Codes = 1u | (1u << 2);  // panel and genotypes evict_last
 
-template <bool FUSED>
+template <int MODE>
 int launch_common(const CUtensorMap& tm_qh, const CUtensorMap& tm_q1, const CUtensorMap& tm_q0,
                   const CUtensorMap& tm_v, const CUtensorMap& tm_v127, int64_t p_pad, int64_t c_pad, int64_t k_pad,
                   const AssocEpilogue& ep, cudaStream_t stream) {
-  PG_CUDA_CHECK(cudaFuncSetAttribute(assoc_i8_kernel<FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     Cfg<FUSED>::kSmemBytes));
+  PG_CUDA_CHECK(cudaFuncSetAttribute(assoc_i8_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     Cfg<MODE>::kSmemBytes));
   int dev = 0, n_sm = 0;
   PG_CUDA_CHECK(cudaGetDevice(&dev));
   PG_CUDA_CHECK(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
-  const int n_ctile = static_cast<int>(c_pad / kTileC);
+  const int n_ctile = static_cast<int>(c_pad / Cfg<MODE>::kTileRows);
   const int n_ptile = static_cast<int>(p_pad / kTileP);
   const int n_tiles = n_ctile * n_ptile;
   const int max_pairs = n_sm / 2;
@@ -395,7 +466,7 @@ int launch_common(const CUtensorMap& tm_qh, const CUtensorMap& tm_q1, const CUte
   }();
   const int group_c = env_group > 0 ? env_group : pairs;
   const uint32_t l2_codes = env_l2 >= 0 ? static_cast<uint32_t>(env_l2) : kDefaultL2Codes;
-  assoc_i8_kernel<FUSED><<<grid, kThreads, Cfg<FUSED>::kSmemBytes, stream>>>(
+  assoc_i8_kernel<MODE><<<grid, kThreads, Cfg<MODE>::kSmemBytes, stream>>>(
       tm_qh, tm_q1, tm_q0, tm_v, tm_v127, n_ctile, n_ptile, static_cast<int>(k_pad / kTileK), group_c, l2_codes,
       ep);
   PG_CUDA_CHECK(cudaGetLastError());
@@ -426,7 +497,7 @@ int launch_assoc(const int8_t* qh, const int8_t* q1, const int8_t* q0, int64_t p
   PG_CHECK_STATUS(encode_panel(qh, q1, q0, p_pad, k_pad, tm_qh, tm_q1, tm_q0));
   PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_v, v, k_pad, c_pad, k_pad, kTileK, kHalfC));
   PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_v127, v127, k_pad, c_pad, k_pad, kTileK, kHalfC));
-  return launch_common<false>(tm_qh, tm_q1, tm_q0, tm_v, tm_v127, p_pad, c_pad, k_pad, ep, stream);
+  return launch_common<kPlanes>(tm_qh, tm_q1, tm_q0, tm_v, tm_v127, p_pad, c_pad, k_pad, ep, stream);
 }
 
 int launch_assoc_packed(const int8_t* qh, const int8_t* q1, const int8_t* q0, int64_t p_pad, const uint8_t* packed,
@@ -441,7 +512,20 @@ int launch_assoc_packed(const int8_t* qh, const int8_t* q1, const int8_t* q0, in
   // packed rows: k_pad/4 bytes of codes per marker (rows past n_markers read as zeros by TMA)
   PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_pk, packed, k_pad / 4, n_markers, pitch, kTileK / 4, kHalfC, false));
   const int64_t c_pad = round_up(n_markers, kTileC);
-  return launch_common<true>(tm_qh, tm_q1, tm_q0, tm_pk, tm_pk, p_pad, c_pad, k_pad, ep, stream);
+  return launch_common<kFused>(tm_qh, tm_q1, tm_q0, tm_pk, tm_pk, p_pad, c_pad, k_pad, ep, stream);
+}
+
+int launch_assoc_wide(const int8_t* qh, const int8_t* q1, const int8_t* q0, int64_t p_pad, const int8_t* v,
+                      int64_t c_pad, int64_t k_pad, const AssocEpilogue& ep, cudaStream_t stream) {
+  PG_REQUIRE(p_pad % kTileP == 0 && c_pad % kTileCW == 0 && k_pad % kTileK == 0 && p_pad > 0 && c_pad > 0 &&
+                 k_pad > 0,
+             PG_ERR_INVALID, "assoc(wide): bad padded shape p=%lld c=%lld k=%lld", (long long)p_pad,
+             (long long)c_pad, (long long)k_pad);
+  PG_REQUIRE(ep.rows_per_marker == kRowsW, PG_ERR_INVALID, "assoc(wide): rows_per_marker must be %d", kRowsW);
+  CUtensorMap tm_qh, tm_q1, tm_q0, tm_v;
+  PG_CHECK_STATUS(encode_panel(qh, q1, q0, p_pad, k_pad, tm_qh, tm_q1, tm_q0));
+  PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_v, v, k_pad, c_pad, k_pad, kTileK, kHalfCW));
+  return launch_common<kWide>(tm_qh, tm_q1, tm_q0, tm_v, tm_v, p_pad, c_pad, k_pad, ep, stream);
 }
 
 }  // namespace pg

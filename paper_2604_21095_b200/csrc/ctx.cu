@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -218,6 +219,7 @@ struct pg_ctx {
   int last_R = 1;
   int64_t cand_capacity = 0;
   bool fused_decode = true;
+  bool wide_digits = true;
 
   // extension mode: quantized covariate basis (columns 1..rank-1) + side-GEMM output
   bool have_basis = false;
@@ -362,20 +364,23 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
   PG_CHECK_STATUS(geno_stats(b, st, m_cap, s));
   PG_CUDA_CHECK(cudaMemcpyAsync(hflags, c->flags.p, sizeof(int) * 2, cudaMemcpyDeviceToHost, s));
   PG_CUDA_CHECK(cudaStreamSynchronize(s));
-  const int R = geno_rows_per_marker(b, hflags[0] != 0);
-  const int64_t c_pad = round_up(m * R, kTileC);
+  // dosage sources use the wide-digit GEMM (4 rows per marker) unless disabled for A/B tests
+  const int R = geno_rows_per_marker(b, hflags[0] != 0, c->wide_digits);
+  const bool wide = R == kWideRows;
+  const int64_t c_pad = round_up(m * R, wide ? kTileCWide : kTileC);
   // PLINK rows without missing calls: the GEMM decodes the packed codes itself
   const bool fused = c->fused_decode && kind == PG_GENO_BED && R == 1;
   int64_t launches = (kind == PG_GENO_DENSE_F64 ? 2 : 1);
   if (!fused) {
     PG_CHECK_STATUS(c->v.ensure(static_cast<size_t>(c_pad) * c->k_pad));
-    PG_CHECK_STATUS(c->v127.ensure(static_cast<size_t>(c_pad) * c->k_pad));
-    PG_CHECK_STATUS(geno_planes(b, R, c->v.p, c->v127.p, c_pad, c->k_pad, s));
+    if (!wide) PG_CHECK_STATUS(c->v127.ensure(static_cast<size_t>(c_pad) * c->k_pad));
+    PG_CHECK_STATUS(geno_planes(b, R, c->v.p, wide ? nullptr : c->v127.p, c_pad, c->k_pad, s));
     ++launches;
   }
   auto run_gemm_on = [&](const AssocEpilogue& e, const int8_t* a, const int8_t* b1, const int8_t* b0,
                          int64_t pp) -> int {
     if (fused) return launch_assoc_packed(a, b1, b0, pp, d_data, pitch, m, c->k_pad, e, s);
+    if (wide) return launch_assoc_wide(a, b1, b0, pp, c->v.p, c_pad, c->k_pad, e, s);
     return launch_assoc(a, b1, b0, pp, c->v.p, c->v127.p, c_pad, c->k_pad, e, s);
   };
   auto run_gemm = [&](const AssocEpilogue& e) -> int { return run_gemm_on(e, c->qh.p, c->q1.p, c->q0.p, c->p_pad); };
@@ -837,6 +842,12 @@ int pg_ctx_set_basis(pg_ctx* c, const double* q, int64_t n_kept, int64_t rank) {
   c->bstage.release();
   c->basis_cols = rank - 1;
   c->have_basis = true;
+  return PG_OK;
+}
+
+int pg_ctx_set_wide_digits(pg_ctx* c, int enable) {
+  PG_CHECK_STATUS(ctx_check(c));
+  c->wide_digits = enable != 0;
   return PG_OK;
 }
 

@@ -30,7 +30,12 @@ double geno_unit_scale(const GenoBlock& b) {
   }
 }
 
-int geno_rows_per_marker(const GenoBlock& b, bool any_missing) {
+bool geno_wide(const GenoBlock& b) {
+  return b.kind == PG_GENO_BGEN8 || b.kind == PG_GENO_BGEN16 || (b.kind == PG_GENO_DENSE_F64 && b.dense_real);
+}
+
+int geno_rows_per_marker(const GenoBlock& b, bool any_missing, bool allow_wide) {
+  if (allow_wide && geno_wide(b)) return 4;  // base-255 digits (|u| <= 131072 < 127 * (1 + 255 + 255^2)) + missing row
   switch (b.kind) {
     case PG_GENO_BGEN8: return 8;    // 6 ternary digits (|u| <= 255 < 364) + missing row
     case PG_GENO_BGEN16: return 16;  // 11 digits (|u| <= 65535 < 88573) + missing row
@@ -314,11 +319,33 @@ __global__ void planes_kernel(GenoBlock b, int8_t* __restrict__ v, int8_t* __res
   const int64_t base = m * R;
   auto put = [&](int64_t row, const int (&x)[kChunk]) {
     uint4* pv = reinterpret_cast<uint4*>(v + row * k_pad + ci * kChunk);
-    uint4* pw = reinterpret_cast<uint4*>(v127 + row * k_pad + ci * kChunk);
     *pv = pack16(x, 1);
-    *pw = pack16(x, 127);
+    if constexpr (R != 4) {
+      uint4* pw = reinterpret_cast<uint4*>(v127 + row * k_pad + ci * kChunk);
+      *pw = pack16(x, 127);
+    }
   };
-  if constexpr (R == 1) {
+  if constexpr (R == 4) {
+    // wide-digit operand: balanced base-255 digits of u (rows 0..2), missing mask (row 3)
+    int cur[kChunk], t[kChunk];
+#pragma unroll
+    for (int i = 0; i < kChunk; ++i) cur[i] = u[i];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+#pragma unroll
+      for (int i = 0; i < kChunk; ++i) {
+        int r = cur[i] % 255;  // in (-255, 255)
+        if (r > 127) r -= 255;
+        if (r < -127) r += 255;
+        t[i] = r;
+        cur[i] = (cur[i] - r) / 255;
+      }
+      put(base + j, t);
+    }
+#pragma unroll
+    for (int i = 0; i < kChunk; ++i) t[i] = (miss >> i) & 1u;
+    put(base + 3, t);
+  } else if constexpr (R == 1) {
     put(base, u);
   } else if constexpr (R == 2) {
     put(base, u);
@@ -425,6 +452,7 @@ int planes_dispatch(const GenoBlock& b, int R, int8_t* v, int8_t* v127, int64_t 
   switch (R) {
     case 1: return planes_launch<KIND, 1>(b, v, v127, c_pad, k_pad, s);
     case 2: return planes_launch<KIND, 2>(b, v, v127, c_pad, k_pad, s);
+    case 4: return planes_launch<KIND, 4>(b, v, v127, c_pad, k_pad, s);
     case 8: return planes_launch<KIND, 8>(b, v, v127, c_pad, k_pad, s);
     case 16: return planes_launch<KIND, 16>(b, v, v127, c_pad, k_pad, s);
     default: set_error("unsupported rows_per_marker %d", R); return PG_ERR_INVALID;

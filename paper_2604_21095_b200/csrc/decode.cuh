@@ -26,7 +26,9 @@ struct GenoBlock {
 //   real dense           : u = rint((dosage - 1) * 2^17)
 double geno_unit_scale(const GenoBlock& b);
 // Rows per marker in the GEMM (ternary digits of u, plus a missing-mask row if any).
-int geno_rows_per_marker(const GenoBlock& b, bool any_missing);
+int geno_rows_per_marker(const GenoBlock& b, bool any_missing, bool allow_wide = true);
+// Dosage sources with wide digits (BGEN, real-valued dense): rows_per_marker 4, launch_assoc_wide.
+bool geno_wide(const GenoBlock& b);
 
 struct MarkerStats {
   long long* n_miss = nullptr;  // [m] missing calls among kept samples
@@ -47,7 +49,8 @@ struct MarkerStats {
 int geno_check_integral(const GenoBlock& b, MarkerStats& st, cudaStream_t s);
 // Pass 2: integer statistics and derived per-marker quantities (all m_pad entries written).
 int geno_stats(const GenoBlock& b, MarkerStats& st, int64_t m_pad, cudaStream_t s);
-// Pass 3: ternary planes v / v127 [c_pad, k_pad] with R rows per marker.
+// Pass 3: GEMM operand planes [c_pad, k_pad] with R rows per marker: ternary digits v / 127v
+// (R = 1, 2, 8, 16), or for R = 4 (wide mode, geno_wide) base-255 digits in v only.
 int geno_planes(const GenoBlock& b, int rows_per_marker, int8_t* v, int8_t* v127, int64_t c_pad, int64_t k_pad,
                 cudaStream_t s);
 // Dosage decode for the reader API: out[m, n_src] f32/f64 with NaN missing, missing counts.

@@ -315,6 +315,8 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
 
     if os.environ.get("PANELGWAS_FUSED_DECODE", "1") == "0":
         ctx.set_fused_decode(False)  # A/B switch; results are identical either way
+    if os.environ.get("PANELGWAS_WIDE_DIGITS", "1") == "0":
+        ctx.set_wide_digits(False)  # A/B switch; results are identical either way
     try:
         if config.residualize_genotypes and prep.basis.rank:
             ctx.set_basis(prep.basis.q)  # extension mode: side GEMM K5 for |Q^T g|^2

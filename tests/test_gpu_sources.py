@@ -80,3 +80,35 @@ def test_dense_fractional_dosages(tmp_path):
     assert len(recs) == want["t"].size
     dt = np.abs(t - want["t"]) / np.maximum(1, np.abs(want["t"]))
     assert dt.max() <= 1e-4
+
+
+@pytest.mark.parametrize("source", ["bgen8", "bgen16", "dense_real"])
+@pytest.mark.parametrize("extension", [False, True])
+def test_wide_digits_equal_ternary_bitwise(source, extension, tmp_path, monkeypatch):
+    """Wide-digit GEMM (base-255 digits, 3 accumulators, N=128) and the balanced-ternary
+    planes are two exact integer contractions of the same codes: FULL output identical."""
+    rng = np.random.default_rng(77)
+    n, m = 130, 70
+    ids = [f"S{i + 1}" for i in range(n)]
+    d = rng.uniform(0, 2, (m, n))
+    d[rng.random(d.shape) < 0.06] = np.nan
+    y = rng.standard_normal((n, 5))
+    cov = rng.standard_normal((n, 2))
+    pheno = write_tsv(tmp_path / "p.tsv", ids, [f"ph{j}" for j in range(5)], y)
+    covar = write_tsv(tmp_path / "c.tsv", ids, ["c1", "c2"], cov)
+    if source.startswith("bgen"):
+        from bgen_fixture import write_bgen
+
+        spec = pg.SourceSpec(pg.GenotypeFormat.BGEN,
+                             bgen_path=write_bgen(tmp_path / "g.bgen", d, ids, bits=int(source[4:])))
+    else:
+        np.save(tmp_path / "g.npy", d)
+        (tmp_path / "s.txt").write_text("\n".join(ids) + "\n")
+        spec = pg.SourceSpec(pg.GenotypeFormat.DENSE, dense_path=tmp_path / "g.npy", sample_id_path=tmp_path / "s.txt")
+    kw = dict(source=spec, pheno_path=pheno, covar_path=covar, output_mode=pg.OutputMode.FULL,
+              precision=pg.Precision.F64, summary_to_stderr=False, device_batch=40,
+              residualize_genotypes=extension, df_mode=pg.DfMode.ADJUSTED if extension else pg.DfMode.PAPER_N_MINUS_2)
+    pg.run_scan(pg.ScanConfig(out_path=tmp_path / "wide.bin", **kw))
+    monkeypatch.setenv("PANELGWAS_WIDE_DIGITS", "0")
+    pg.run_scan(pg.ScanConfig(out_path=tmp_path / "tern.bin", **kw))
+    assert (tmp_path / "wide.bin").read_bytes() == (tmp_path / "tern.bin").read_bytes()
