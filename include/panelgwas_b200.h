@@ -186,6 +186,13 @@ PG_API int pg_scan_device(pg_ctx* ctx, int geno_kind, const void* d_data, int64_
  * pg_bgen_inflate on the host to obtain zlib's own text. */
 PG_API int pg_stage_bgen(pg_ctx* ctx, int slot, const void* blob, int64_t blob_bytes, const int64_t* block_off,
                          const int64_t* block_size, int64_t count, int64_t* diag);
+/* The same in two phases, so the H2D and inflate of batch i+1 overlap the scan of batch i:
+ * _begin enqueues everything on the copy stream and returns (`blob` must stay valid and
+ * unmodified until _end; pinned memory makes the copy asynchronous); _end waits for the
+ * validation summary, reports errors like pg_stage_bgen, and enqueues the repack. */
+PG_API int pg_stage_bgen_begin(pg_ctx* ctx, int slot, const void* blob, int64_t blob_bytes,
+                               const int64_t* block_off, const int64_t* block_size, int64_t count);
+PG_API int pg_stage_bgen_end(pg_ctx* ctx, int slot, int64_t* diag);
 
 /* Asynchronous staging for pipelined scans (transfer of batch i+1 overlaps the
  * GEMM of batch i). pg_stage copies HOST rows into staging slot `slot` (0 or 1) on

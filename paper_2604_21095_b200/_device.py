@@ -219,6 +219,27 @@ class DeviceContext:
         _native.check(status)
         return None
 
+    def stage_bgen_begin(self, slot: int, blob: np.ndarray, block_off: np.ndarray, block_size: np.ndarray):
+        """Enqueue H2D + GPU inflate + validation of a compressed BGEN batch; returns the
+        arrays that must stay alive until stage_bgen_end(slot)."""
+        b = np.ascontiguousarray(blob, dtype=np.uint8)
+        off = np.ascontiguousarray(block_off, dtype=np.int64)
+        size = np.ascontiguousarray(block_size, dtype=np.int64)
+        with self.lock:
+            call("pg_stage_bgen_begin", self._h, int(slot), b.ctypes.data, b.size, off.ctypes.data, size.ctypes.data,
+                 off.size)
+        return b, off, size
+
+    def stage_bgen_end(self, slot: int):
+        """None when the batch is staged, else (variant, reason, a, b) of the first bad block."""
+        diag = np.zeros(4, dtype=np.int64)
+        with self.lock:
+            status = self.lib.pg_stage_bgen_end(self._h, int(slot), diag.ctypes.data)
+        if status == _native.PG_ERR_FORMAT and diag[1]:
+            return tuple(int(x) for x in diag)
+        _native.check(status)
+        return None
+
     def scan_staged(self, slot: int, *, fetch: bool = True, full_elem_bytes: int = 8) -> ScanResult:
         info = BatchInfo()
         with self.lock:

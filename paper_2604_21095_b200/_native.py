@@ -80,6 +80,8 @@ SIGNATURES: dict[str, list] = {
     "pg_scan_device": [_P, c_int, _P, c_int64, c_int64, c_int64, _P],
     "pg_stage": [_P, c_int, c_int, _P, c_int64, c_int64],
     "pg_stage_bgen": [_P, c_int, _P, c_int64, _P, _P, c_int64, _P],
+    "pg_stage_bgen_begin": [_P, c_int, _P, c_int64, _P, _P, c_int64],
+    "pg_stage_bgen_end": [_P, c_int, _P],
     "pg_scan_staged": [_P, c_int, _P],
     "pg_fetch_marker_stats": [_P, _P, _P, _P, _P],
     "pg_fetch_candidates": [_P, _P, _P, _P, _P, _P],

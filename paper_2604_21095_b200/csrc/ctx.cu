@@ -195,6 +195,8 @@ struct pg_ctx {
   pg::DBuf<int> bgen_zstatus[2], bgen_bits[2];
   pg::DBuf<long long> bgen_diag[2];
   pg::DBuf<unsigned long long> bgen_summary[2];
+  void* bgen_host[2] = {nullptr, nullptr};  // pinned copies of the validation summaries
+  int64_t bgen_pending[2] = {0, 0};         // batch size begun but not ended, per slot
   int64_t stage_m[2] = {0, 0};
   int64_t stage_pitch[2] = {0, 0};
   pg::DBuf<long long> n_miss, s_u, ss_u;
@@ -581,16 +583,15 @@ int pg_ctx_destroy(pg_ctx* c) {
   c->full_out.release();
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
+  if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
   for (int i = 0; i < 2; ++i) {
     c->stage_buf[i].release();
     c->stage_raw[i].release();
     if (c->stage_ev[i]) cudaEventDestroy(c->stage_ev[i]);
     if (c->slot_free_ev[i]) cudaEventDestroy(c->slot_free_ev[i]);
+    if (c->bgen_host[i]) cudaFreeHost(c->bgen_host[i]);
   }
-  if (c->copy_stream) {
-    cudaStreamSynchronize(c->copy_stream);
-    cudaStreamDestroy(c->copy_stream);
-  }
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return PG_OK;
@@ -911,29 +912,33 @@ int pg_stage(pg_ctx* c, int slot, int kind, const void* data, int64_t n_markers,
   return PG_OK;
 }
 
-int pg_stage_bgen(pg_ctx* c, int slot, const void* blob, int64_t blob_bytes, const int64_t* block_off,
-                  const int64_t* block_size, int64_t count, int64_t* diag) {
+int pg_stage_bgen_begin(pg_ctx* c, int slot, const void* blob, int64_t blob_bytes, const int64_t* block_off,
+                        const int64_t* block_size, int64_t count) {
   PG_CHECK_STATUS(ctx_check(c));
   PG_REQUIRE(slot == 0 || slot == 1, PG_ERR_INVALID, "pg_stage_bgen: slot must be 0 or 1");
   PG_REQUIRE(c->have_panel, PG_ERR_STATE, "pg_stage_bgen: no panel uploaded (pg_ctx_set_panel)");
-  PG_REQUIRE(blob != nullptr && block_off != nullptr && block_size != nullptr && diag != nullptr && count >= 1,
-             PG_ERR_INVALID, "pg_stage_bgen: empty batch or null argument");
+  PG_REQUIRE(blob != nullptr && block_off != nullptr && block_size != nullptr && count >= 1, PG_ERR_INVALID,
+             "pg_stage_bgen: empty batch or null argument");
+  PG_REQUIRE(c->bgen_pending[slot] == 0, PG_ERR_STATE, "pg_stage_bgen: slot %d already has a batch in flight", slot);
   for (int64_t i = 0; i < count; ++i)
     PG_REQUIRE(block_off[i] >= 0 && block_size[i] >= 0 && block_off[i] + block_size[i] <= blob_bytes,
                PG_ERR_INVALID, "pg_stage_bgen: block %lld outside the blob", (long long)i);
-  diag[0] = diag[1] = diag[2] = diag[3] = 0;
   const int64_t n = c->n_src;
   const int64_t raw_stride = round_up(10 + 5 * n, 16);
   cudaStream_t cs = c->copy_stream;
+  // the slot's buffers may still be read by the scan that last used it
   PG_CUDA_CHECK(cudaStreamWaitEvent(cs, c->slot_free_ev[slot], 0));
-  PG_CUDA_CHECK(cudaStreamSynchronize(cs));
-  PG_CHECK_STATUS(c->bgen_blob[slot].ensure(blob_bytes + 16));  // the decoder peeks up to 8 B past a stream
+  if (c->bgen_blob[slot].cap < static_cast<size_t>(blob_bytes + 16) ||
+      c->bgen_raw[slot].cap < static_cast<size_t>(raw_stride) * count || c->bgen_off[slot].cap < static_cast<size_t>(count))
+    PG_CUDA_CHECK(cudaStreamSynchronize(cs));  // reallocation below must not free memory in use
+  PG_CHECK_STATUS(c->bgen_blob[slot].ensure(blob_bytes + 16));  // the decoder reads ahead <= 8 B past a stream
   PG_CHECK_STATUS(c->bgen_raw[slot].ensure(static_cast<size_t>(raw_stride) * count));
   for (auto* b : {&c->bgen_off[slot], &c->bgen_size[slot], &c->bgen_len[slot]}) PG_CHECK_STATUS(b->ensure(count));
   PG_CHECK_STATUS(c->bgen_zstatus[slot].ensure(count));
   PG_CHECK_STATUS(c->bgen_bits[slot].ensure(count));
   PG_CHECK_STATUS(c->bgen_diag[slot].ensure(3 * count));
   PG_CHECK_STATUS(c->bgen_summary[slot].ensure(2));
+  if (c->bgen_host[slot] == nullptr) PG_CUDA_CHECK(cudaHostAlloc(&c->bgen_host[slot], 64, cudaHostAllocDefault));
   PG_CUDA_CHECK(cudaMemcpyAsync(c->bgen_blob[slot].p, blob, blob_bytes, cudaMemcpyHostToDevice, cs));
   PG_CUDA_CHECK(cudaMemcpyAsync(c->bgen_off[slot].p, block_off, sizeof(int64_t) * count, cudaMemcpyHostToDevice, cs));
   PG_CUDA_CHECK(
@@ -942,15 +947,29 @@ int pg_stage_bgen(pg_ctx* c, int slot, const void* blob, int64_t blob_bytes, con
   PG_CHECK_STATUS(pg::inflate_streams(c->bgen_blob[slot].p, c->bgen_off[slot].p, c->bgen_size[slot].p, count, 4,
                                       c->bgen_raw[slot].p, raw_stride, c->bgen_len[slot].p, c->bgen_zstatus[slot].p,
                                       cs));
-  unsigned long long init[2] = {~0ull, 0ull};
-  PG_CUDA_CHECK(cudaMemcpyAsync(c->bgen_summary[slot].p, init, sizeof(init), cudaMemcpyHostToDevice, cs));
+  PG_CUDA_CHECK(cudaMemsetAsync(c->bgen_summary[slot].p, 0xFF, sizeof(unsigned long long), cs));
+  PG_CUDA_CHECK(cudaMemsetAsync(c->bgen_summary[slot].p + 1, 0, sizeof(unsigned long long), cs));
   PG_CHECK_STATUS(pg::bgen_validate(c->bgen_blob[slot].p, c->bgen_off[slot].p, c->bgen_size[slot].p,
                                     c->bgen_raw[slot].p, raw_stride, c->bgen_len[slot].p, c->bgen_zstatus[slot].p,
                                     count, n, c->bgen_diag[slot].p, c->bgen_bits[slot].p, c->bgen_summary[slot].p,
                                     cs));
-  unsigned long long summary[2] = {0, 0};
-  PG_CUDA_CHECK(cudaMemcpyAsync(summary, c->bgen_summary[slot].p, sizeof(summary), cudaMemcpyDeviceToHost, cs));
-  PG_CUDA_CHECK(cudaStreamSynchronize(cs));
+  PG_CUDA_CHECK(cudaMemcpyAsync(c->bgen_host[slot], c->bgen_summary[slot].p, 2 * sizeof(unsigned long long),
+                                cudaMemcpyDeviceToHost, cs));
+  PG_CUDA_CHECK(cudaEventRecord(c->stage_ev[slot], cs));
+  c->bgen_pending[slot] = count;
+  return PG_OK;
+}
+
+int pg_stage_bgen_end(pg_ctx* c, int slot, int64_t* diag) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(slot == 0 || slot == 1, PG_ERR_INVALID, "pg_stage_bgen_end: slot must be 0 or 1");
+  PG_REQUIRE(diag != nullptr, PG_ERR_INVALID, "pg_stage_bgen_end: null diag");
+  const int64_t count = c->bgen_pending[slot];
+  PG_REQUIRE(count > 0, PG_ERR_STATE, "pg_stage_bgen_end: no batch in flight in slot %d", slot);
+  c->bgen_pending[slot] = 0;
+  diag[0] = diag[1] = diag[2] = diag[3] = 0;
+  PG_CUDA_CHECK(cudaEventSynchronize(c->stage_ev[slot]));
+  const unsigned long long* summary = static_cast<const unsigned long long*>(c->bgen_host[slot]);
   if (summary[0] != ~0ull) {
     long long d3[3] = {0, 0, 0};
     PG_CUDA_CHECK(cudaMemcpy(d3, c->bgen_diag[slot].p + 3 * summary[0], sizeof(d3), cudaMemcpyDeviceToHost));
@@ -961,10 +980,16 @@ int pg_stage_bgen(pg_ctx* c, int slot, const void* blob, int64_t blob_bytes, con
     pg::set_error("BGEN block %lld failed validation (reason %lld)", (long long)summary[0], d3[0]);
     return PG_ERR_FORMAT;
   }
+  const int64_t n = c->n_src;
+  const int64_t raw_stride = round_up(10 + 5 * n, 16);
   const bool wide16 = (summary[1] & 2ull) != 0;
   const int64_t row_bytes = wide16 ? 5 * n : 3 * n;
   const int64_t pitch = round_up(row_bytes, 16);
-  PG_CHECK_STATUS(c->stage_buf[slot].ensure(static_cast<size_t>(pitch) * count));
+  cudaStream_t cs = c->copy_stream;
+  if (c->stage_buf[slot].cap < static_cast<size_t>(pitch) * count) {
+    PG_CUDA_CHECK(cudaStreamSynchronize(cs));
+    PG_CHECK_STATUS(c->stage_buf[slot].ensure(static_cast<size_t>(pitch) * count));
+  }
   PG_CHECK_STATUS(pg::bgen_repack(c->bgen_raw[slot].p, raw_stride, c->bgen_bits[slot].p, count, n, wide16,
                                   c->stage_buf[slot].p, pitch, cs));
   PG_CUDA_CHECK(cudaEventRecord(c->stage_ev[slot], cs));
@@ -972,6 +997,13 @@ int pg_stage_bgen(pg_ctx* c, int slot, const void* blob, int64_t blob_bytes, con
   c->stage_m[slot] = count;
   c->stage_pitch[slot] = pitch;
   return PG_OK;
+}
+
+int pg_stage_bgen(pg_ctx* c, int slot, const void* blob, int64_t blob_bytes, const int64_t* block_off,
+                  const int64_t* block_size, int64_t count, int64_t* diag) {
+  PG_REQUIRE(diag != nullptr, PG_ERR_INVALID, "pg_stage_bgen: null diag");
+  PG_CHECK_STATUS(pg_stage_bgen_begin(c, slot, blob, blob_bytes, block_off, block_size, count));
+  return pg_stage_bgen_end(c, slot, diag);
 }
 
 int pg_scan_staged(pg_ctx* c, int slot, pg_batch_info* info) {

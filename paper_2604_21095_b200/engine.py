@@ -360,14 +360,16 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
             return block, time.perf_counter() - t0
 
         def stage(i, block):
-            if compressed:
-                blob, offs, sizes = block
-                bad = ctx.stage_bgen(i % 2, blob, offs, sizes)
-                if bad is not None:
-                    source.raise_block_error(plan[i][0] + bad[0], bad[1], bad[2], bad[3])
-                return blob
+            if compressed:  # H2D + GPU inflate run while the previous batch is scanned
+                return ctx.stage_bgen_begin(i % 2, *block)
             kind, rows, row_bytes = block
             return ctx.stage(i % 2, kind, rows, row_bytes)
+
+        def staged_ready(i):
+            if compressed:
+                bad = ctx.stage_bgen_end(i % 2)
+                if bad is not None:
+                    source.raise_block_error(plan[i][0] + bad[0], bad[1], bad[2], bad[3])
 
         def finish(i, res):
             nonlocal t_prepare, t_corr, t_emit, clamp_total, skip_mono, skip_missing
@@ -406,6 +408,7 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
                         fut = reader.submit(read, i + 1)
                     if pending is not None:
                         finish(pending, ctx.scan_staged(pending % 2, full_elem_bytes=dtype.itemsize))
+                    staged_ready(i)
                     pending = i
                 finish(pending, ctx.scan_staged(pending % 2, full_elem_bytes=dtype.itemsize))
             if config.min_p_sidecar:
