@@ -60,7 +60,7 @@ int launch_assoc_packed(const int8_t* qh, const int8_t* q1, const int8_t* q0, in
 // Wide-digit variant for dosage sources: one int8 plane v [c_pad, k_pad] of balanced
 // base-255 digits (rows per marker: digit0, digit1, digit2, missing mask; rows_per_marker
 // kWideRows), c_pad a multiple of kTileCWide. Three accumulators per tile.
-constexpr int kTileCWide = 128;
+constexpr int kTileCWide = 160;
 constexpr int kWideRows = 4;
 int launch_assoc_wide(const int8_t* qh, const int8_t* q1, const int8_t* q0, int64_t p_pad, const int8_t* v,
                       int64_t c_pad, int64_t k_pad, const AssocEpilogue& ep, cudaStream_t stream);

@@ -53,10 +53,12 @@ constexpr int kPackedBytes = kHalfC * (kTileK / 4);  // 2 KB packed .bed half-ti
 constexpr int kOffV = 3 * kQBytes;
 constexpr int kOffV127 = kOffV + kVBytes;
 constexpr int kOffPacked = kOffV127 + kVBytes;
-// wide-digit mode: 128 genotype rows per pair tile (64 per CTA), three accumulators
-constexpr int kTileCW = 128;
+// wide-digit mode: 160 genotype rows per pair tile (80 per CTA), three accumulators in
+// 3 x 160 = 480 TMEM columns (the widest N that fits 512: operand bytes per MAC are
+// 17 % lower than at N = 128, and this mode is L2-bandwidth bound)
+constexpr int kTileCW = kTileCWide;
 constexpr int kHalfCW = kTileCW / 2;
-constexpr int kVBytesW = kHalfCW * kTileK;  // 4 KB
+constexpr int kVBytesW = kHalfCW * kTileK;  // 5 KB
 constexpr int kRowsW = 4;                   // digits 255^0, 255^1, 255^2 + missing row
 constexpr int kPlanes = 0, kFused = 1, kWide = 2;
 constexpr int kEpiWarps = 16;
@@ -83,6 +85,9 @@ struct Cfg {
   static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 512 /*barriers*/;
   static constexpr int kTileRows = WIDE ? kTileCW : kTileC;  // genotype rows per pair tile
   static constexpr int kHalfRows = kTileRows / 2;
+  static_assert(kStageBytes % 1024 == 0 && kOffV % 512 == 0, "stage / operand alignment (SW64 atoms)");
+  static_assert(kTileRows % 16 == 0 && kHalfRows % 8 == 0, "UMMA N and swizzle-atom granularity");
+  static_assert(kSmemBytes <= 227 * 1024, "shared memory per CTA");
 };
 
 __device__ __forceinline__ void tile_coords(int t, int n_ctile, int n_ptile, int group_c, int& ct, int& pt) {
@@ -412,7 +417,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const uint32_t tH = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16);
       const uint32_t tL = tH + C::kTileRows;
-      const int c0 = cg * (C::kTileRows / 4), c1 = c0 + C::kTileRows / 4;
+      // split the tile's 16-column chunks over the 4 column groups
+      constexpr int kChunks = C::kTileRows / 16;
+      const int c0 = 16 * ((cg * kChunks) / 4), c1 = 16 * (((cg + 1) * kChunks) / 4);
       if constexpr (WIDE) {
         epilogue_tile_wide(ep, tH, ct, pheno, lane, c0, c1);
       } else {

@@ -333,7 +333,8 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
   b.keep_bits = c->keep_bits.p;
   b.all_kept = c->n_kept == c->n_src ? 1 : 0;
 
-  const int64_t m_cap = round_up(m, 256);  // enough marker slots for any rows_per_marker
+  // marker slots for any tiling: ternary tiles hold 256 / R markers, wide tiles 40
+  const int64_t m_cap = round_up(m, 256) + 64;
   PG_CHECK_STATUS(c->flags.ensure(2));
   PG_CUDA_CHECK(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * 2, s));
   int hflags[2] = {0, 0};

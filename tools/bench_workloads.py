@@ -84,8 +84,13 @@ def main():
     if a.workload == "c2":
         bpm = (n + 3) // 4
         pitch = (bpm + 15) // 16 * 16
-        host = rng.integers(0, 256, (batch, pitch), dtype=np.uint8)
-        host[:, :bpm] = np.where(host[:, :bpm] == 0x55, 0, host[:, :bpm])  # avoid all-missing words
+        # Binomial(2, AF) genotypes without missing calls (as C3 / bench.py)
+        af = rng.uniform(0.05, 0.95, (batch, 1))
+        g = (rng.random((batch, n)) < af).astype(np.uint8) + (rng.random((batch, n)) < af).astype(np.uint8)
+        codes = np.array([3, 2, 0], np.uint8)[g]
+        codes = np.pad(codes, ((0, 0), (0, bpm * 4 - n))).reshape(batch, bpm, 4)
+        host = np.zeros((batch, pitch), np.uint8)
+        host[:, :bpm] = codes[:, :, 0] | (codes[:, :, 1] << 2) | (codes[:, :, 2] << 4) | (codes[:, :, 3] << 6)
         kind, row_bytes = _native.PG_GENO_BED, bpm
         rows_dev = torch.from_numpy(host).to(dev)
         blocks = None
