@@ -2,8 +2,6 @@
 byte-identical to zlib.decompress over every DEFLATE block type / strategy, corrupt streams
 rejected, and scans through the GPU-inflate path == the host-inflate path (bitwise) with
 the reference reader's exceptions on bad blocks."""
-import ctypes
-import os
 import zlib
 
 import numpy as np
@@ -11,7 +9,7 @@ import pytest
 
 import paper_2604_21095_b200 as pg
 from paper_2604_21095_b200 import _native
-from paper_2604_21095_b200.errors import FormatError, UnsupportedFeatureError
+from paper_2604_21095_b200.errors import FormatError
 
 pytestmark = pytest.mark.gpu
 
@@ -155,3 +153,34 @@ def test_stage_bgen_mixed_precision(tmp_path, monkeypatch):
     monkeypatch.setenv("PANELGWAS_HOST_INFLATE", "1")
     _scan(spec, pheno, tmp_path / "host.tsv")
     assert (tmp_path / "gpu.tsv").read_bytes() == (tmp_path / "host.tsv").read_bytes()
+
+
+def test_bgen_keep_subset_and_odd_sizes(tmp_path, monkeypatch):
+    """GPU-inflate path with excluded samples (keep list), an odd sample count, a single
+    phenotype and a batch size that does not divide M: identical to the host-inflate path
+    and to the oracle-level reference goldens' invariants (AF / missing bit-exact)."""
+    from bgen_fixture import write_bgen
+    from conftest_helpers import write_tsv
+
+    rng = np.random.default_rng(13)
+    n, m = 77, 53
+    ids = [f"S{i + 1}" for i in range(n)]
+    d = rng.uniform(0, 2, (m, n))
+    d[rng.random(d.shape) < 0.08] = np.nan
+    spec = pg.SourceSpec(pg.GenotypeFormat.BGEN, bgen_path=write_bgen(tmp_path / "g.bgen", d, ids, bits=16))
+    pheno = write_tsv(tmp_path / "p.tsv", ids, ["only"], rng.standard_normal((n, 1)))
+    keep = tmp_path / "keep.txt"
+    keep.write_text("\n".join(ids[::2] + ids[5:9]) + "\n")
+    kw = dict(source=spec, pheno_path=pheno, p_threshold=1.0, precision=pg.Precision.F64, summary_to_stderr=False,
+              device_batch=17, keep_path=keep)
+    s1 = pg.run_scan(pg.ScanConfig(out_path=tmp_path / "gpu.tsv", **kw))
+    monkeypatch.setenv("PANELGWAS_HOST_INFLATE", "1")
+    s2 = pg.run_scan(pg.ScanConfig(out_path=tmp_path / "host.tsv", **kw))
+    assert (tmp_path / "gpu.tsv").read_bytes() == (tmp_path / "host.tsv").read_bytes()
+    assert s1.markers_scanned == s2.markers_scanned == m
+    recs = pg.load_association_records(tmp_path / "gpu.tsv")
+    kept = sorted(set(range(0, n, 2)) | set(range(5, 9)))
+    for r in recs[:10]:
+        i = int(r.id[2:]) - 1
+        row = d[i, kept]
+        assert r.missing_count == int(np.isnan(row).sum())
