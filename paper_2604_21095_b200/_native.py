@@ -9,7 +9,7 @@ from __future__ import annotations
 
 import ctypes
 import threading
-from ctypes import POINTER, c_char_p, c_double, c_int, c_int8, c_int64, c_void_p
+from ctypes import c_char_p, c_double, c_int, c_int64, c_void_p
 from pathlib import Path
 
 import numpy as np

@@ -2,7 +2,6 @@
 integer and the int32 tensor-core accumulation cannot round, so the result is
 compared bit-for-bit with a float64 product of the same integers (all partial
 sums are far below 2**53)."""
-import numpy as np
 import pytest
 
 torch = pytest.importorskip("torch")

@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 import paper_2604_21095_b200 as pg
-from paper_2604_21095_b200 import engine, output, phenotypes
+from paper_2604_21095_b200 import engine, output
 from paper_2604_21095_b200.errors import ConfigError, FormatError, PanelGwasError, UnsupportedFeatureError
 
 
