@@ -65,12 +65,14 @@ struct Bits {
   uint32_t nextw;  // w[wi], loaded one refill ahead
   uint64_t buf;
   int cnt;
-  uint32_t end;  // stream end, in bits from w
+  uint32_t end;        // stream end, in bits from w
+  uint32_t last_word;  // loads stop here (a malformed stream cannot run past the blob padding)
   __device__ __forceinline__ void refill() {
     if (cnt <= 32) {
       buf |= static_cast<uint64_t>(nextw) << cnt;
       cnt += 32;
-      nextw = __ldg(w + (++wi));
+      ++wi;
+      nextw = wi <= last_word ? __ldg(w + wi) : 0u;
     }
   }
   __device__ __forceinline__ uint32_t get(int n) {  // n <= 32 buffered bits
@@ -181,6 +183,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
   br.buf = 0;
   br.cnt = 0;
   br.end = n_in < 0 ? 0 : lead + static_cast<uint32_t>(n_in) * 8u;
+  br.last_word = (br.end + 31) / 32 + 1;  // within the 16 B of padding after the last stream
   br.refill();
   br.refill();
   br.get(lead);
@@ -227,7 +230,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
       pos += n;
       const uint32_t next_bit = (byte_pos + 4 + n) * 8;
       br.wi = next_bit >> 5;
-      br.nextw = __ldg(br.w + br.wi);
+      br.nextw = br.wi <= br.last_word ? __ldg(br.w + br.wi) : 0u;
       br.buf = 0;
       br.cnt = 0;
       br.refill();
@@ -355,7 +358,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
         break;
       }
       const int distance = c_dist_base[ds] + static_cast<int>(br.get(c_dist_extra[ds]));
-      if (distance > pos || !br.ok()) {
+      // (reading past the stream end only consumes padding / the next stream's bytes; the
+      // end-of-block check below reports truncation)
+      if (distance > pos) {
         err = 1;
         break;
       }
@@ -373,7 +378,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
         sm.ring[(pos + j) & (kRing - 1)] = v;
       }
       pos += length;
-      __syncwarp();
+      // no barrier here: the next match's __syncwarp orders these writes before its reads
     }
   }
   // Adler-32 trailer (big-endian, byte aligned after the last block)

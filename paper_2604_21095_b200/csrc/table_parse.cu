@@ -79,14 +79,29 @@ struct Line {
   int64_t lineno;      // 1-based physical line number
 };
 
+inline bool has_special(const char* s, size_t n) {
+  for (size_t i = 0; i < n; ++i) {
+    const unsigned char c = static_cast<unsigned char>(s[i]);
+    if (c == '"' || c == '\r' || c >= 0x80 || c == '_' || c == 0) return true;
+  }
+  return false;
+}
+
 }  // namespace
 }  // namespace pg
 
 extern "C" {
 
 // Returns PG_OK, PG_TABLE_GENERIC (caller must use the generic path) or an error.
-// Two calls: values == NULL -> *n_rows = number of records (after ragged-row checks);
-// then with buffers sized n_rows x (n_fields - 1) / n_rows / (n_fields - 1).
+// Two calls: values == NULL -> *n_rows = number of records (non-blank lines); then with
+// buffers sized n_rows x (n_fields - 1) / n_rows / (n_fields - 1). Ragged records are
+// reported by the second call (PG_ERR_FORMAT, *err_line / *err_cells: the first one).
+//
+// One pass per line: fields are found with memchr, a value cell is stripped only when
+// it starts or ends with whitespace, and the bytes that would make Python's csv module
+// read the line differently (quote, bare CR, non-ASCII, NUL, '_' digit groups) can only
+// occur in a cell that fails to parse as a number or in the ID cell, so only those are
+// scanned for them.
 int pg_table_parse(const char* buf, int64_t len, int64_t body_offset, char delim, int64_t n_fields, int64_t id_field,
                    int n_threads, int64_t first_lineno, int64_t* n_rows, double* values, int64_t* id_off,
                    int64_t* id_len, int64_t* missing, int64_t* unparseable, int64_t* err_line, int64_t* err_cells) {
@@ -95,66 +110,28 @@ int pg_table_parse(const char* buf, int64_t len, int64_t body_offset, char delim
   PG_REQUIRE(n_fields >= 1 && id_field >= 0 && id_field < n_fields, PG_ERR_INVALID, "pg_table_parse: bad fields");
   *err_line = 0;
   *err_cells = 0;
-  // ---- lines (sequential memchr; lines are long, so this is a small share of the time)
+  // ---- records: non-blank lines (csv.reader yields [] for an empty line)
   std::vector<Line> lines;
   int64_t pos = body_offset, lineno = first_lineno;
   while (pos < len) {
     const void* nl = std::memchr(buf + pos, '\n', static_cast<size_t>(len - pos));
-    int64_t end = nl ? static_cast<const char*>(nl) - buf : len;
+    const int64_t end = nl ? static_cast<const char*>(nl) - buf : len;
     int64_t stop = end;
     if (stop > pos && buf[stop - 1] == '\r') --stop;
-    lines.push_back({pos, stop, lineno});
+    if (stop > pos) lines.push_back({pos, stop, lineno});
     pos = end + 1;
     ++lineno;
   }
-  const int64_t n_lines = static_cast<int64_t>(lines.size());
-  int nt = n_threads > 0 ? n_threads : static_cast<int>(std::thread::hardware_concurrency());
-  nt = std::max(1, std::min<int>(nt, 64));
-  if (n_lines < 4 * nt) nt = std::max<int64_t>(1, n_lines / 4);
-  const int64_t n_val = n_fields - 1;
-
-  // ---- pass 1: generic-path triggers, blank lines, field counts
-  std::vector<int64_t> cells_of(n_lines, 0);
-  std::atomic<bool> generic{false};
-  {
-    std::vector<std::thread> th;
-    for (int t = 0; t < nt; ++t) {
-      th.emplace_back([&, t] {
-        for (int64_t i = t; i < n_lines; i += nt) {
-          const Line& L = lines[i];
-          int64_t cells = 1;
-          for (int64_t k = L.begin; k < L.end; ++k) {
-            const unsigned char c = static_cast<unsigned char>(buf[k]);
-            if (c == static_cast<unsigned char>(delim)) {
-              ++cells;
-            } else if (c == '"' || c == '\r' || c >= 0x80 || c == '_' || c == 0) {
-              generic.store(true, std::memory_order_relaxed);
-            }
-          }
-          cells_of[i] = L.end == L.begin ? 0 : cells;  // csv.reader yields [] for an empty line
-        }
-      });
-    }
-    for (auto& x : th) x.join();
-  }
-  if (generic.load()) return PG_TABLE_GENERIC;
-  std::vector<int64_t> rec_line;  // record -> line
-  rec_line.reserve(n_lines);
-  for (int64_t i = 0; i < n_lines; ++i) {
-    if (cells_of[i] == 0) continue;
-    if (cells_of[i] != n_fields) {
-      *err_line = lines[i].lineno;
-      *err_cells = cells_of[i];
-      pg::set_error("ragged row");
-      return PG_ERR_FORMAT;
-    }
-    rec_line.push_back(i);
-  }
-  const int64_t nr = static_cast<int64_t>(rec_line.size());
+  const int64_t nr = static_cast<int64_t>(lines.size());
   *n_rows = nr;
   if (values == nullptr) return PG_OK;
 
-  // ---- pass 2: cells
+  int nt = n_threads > 0 ? n_threads : static_cast<int>(std::thread::hardware_concurrency());
+  nt = std::max(1, std::min<int>(nt, 64));
+  if (nr < 4 * nt) nt = static_cast<int>(std::max<int64_t>(1, nr / 4));
+  const int64_t n_val = n_fields - 1;
+  std::atomic<bool> generic{false};
+  std::atomic<int64_t> bad_rec{INT64_MAX};  // first ragged record
   std::vector<std::vector<int64_t>> miss_t(nt, std::vector<int64_t>(n_val, 0));
   std::vector<std::vector<int64_t>> bad_t(nt, std::vector<int64_t>(n_val, 0));
   {
@@ -164,40 +141,72 @@ int pg_table_parse(const char* buf, int64_t len, int64_t body_offset, char delim
         int64_t* miss = miss_t[t].data();
         int64_t* bad = bad_t[t].data();
         for (int64_t r = t; r < nr; r += nt) {
-          const Line& L = lines[rec_line[r]];
+          if (generic.load(std::memory_order_relaxed)) return;
+          const Line& L = lines[r];
           double* out = values + r * n_val;
-          int64_t f = 0, j = 0, k = L.begin;
-          while (f < n_fields) {
-            int64_t e = k;
-            while (e < L.end && buf[e] != delim) ++e;
+          int64_t k = L.begin, j = 0;
+          bool ragged = false;
+          for (int64_t f = 0; f < n_fields; ++f) {
+            if (k > L.end) {  // fewer cells than the header
+              ragged = true;
+              break;
+            }
+            const void* dp = std::memchr(buf + k, delim, static_cast<size_t>(L.end - k));
+            const int64_t e = dp ? static_cast<const char*>(dp) - buf : L.end;
+            if (f == n_fields - 1 && e != L.end) {  // more cells than the header
+              ragged = true;
+              break;
+            }
             int64_t a = k, z = e;
-            while (a < z && pg::is_space(static_cast<unsigned char>(buf[a]))) ++a;
-            while (z > a && pg::is_space(static_cast<unsigned char>(buf[z - 1]))) --z;
+            if (a < z && (pg::is_space(static_cast<unsigned char>(buf[a])) ||
+                          pg::is_space(static_cast<unsigned char>(buf[z - 1])))) {
+              while (a < z && pg::is_space(static_cast<unsigned char>(buf[a]))) ++a;
+              while (z > a && pg::is_space(static_cast<unsigned char>(buf[z - 1]))) --z;
+            }
+            const char* s = buf + a;
+            const size_t n = static_cast<size_t>(z - a);
             if (f == id_field) {
+              if (pg::has_special(buf + k, static_cast<size_t>(e - k))) generic.store(true);
               id_off[r] = a;
               id_len[r] = z - a;
             } else {
-              const char* s = buf + a;
-              const size_t n = static_cast<size_t>(z - a);
               double v = NAN;
               if (pg::is_missing_token(s, n) || pg::is_minus_nine(s, n)) {
                 ++miss[j];
               } else if (!pg::py_float(s, n, v) || !std::isfinite(v)) {
+                if (pg::has_special(buf + k, static_cast<size_t>(e - k))) generic.store(true);
                 v = NAN;
                 ++bad[j];
-                ++miss[j];
-              } else if (std::isnan(v)) {
                 ++miss[j];
               }
               out[j++] = v;
             }
             k = e + 1;
-            ++f;
+          }
+          if (ragged) {
+            int64_t cur = bad_rec.load();
+            while (r < cur && !bad_rec.compare_exchange_weak(cur, r)) {
+            }
           }
         }
       });
     }
     for (auto& x : th) x.join();
+  }
+  if (generic.load()) return PG_TABLE_GENERIC;
+  if (bad_rec.load() != INT64_MAX) {
+    // any quote / CR / non-ASCII byte on an earlier line would have made csv read differently
+    const int64_t r = bad_rec.load();
+    for (int64_t q = 0; q <= r; ++q)
+      if (pg::has_special(buf + lines[q].begin, static_cast<size_t>(lines[q].end - lines[q].begin)))
+        return PG_TABLE_GENERIC;
+    const Line& L = lines[r];
+    int64_t cells = 1;
+    for (int64_t k = L.begin; k < L.end; ++k) cells += buf[k] == delim;
+    *err_line = L.lineno;
+    *err_cells = cells;
+    pg::set_error("ragged row");
+    return PG_ERR_FORMAT;
   }
   for (int64_t j = 0; j < n_val; ++j) {
     int64_t m = 0, b = 0;

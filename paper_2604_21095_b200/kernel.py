@@ -110,8 +110,9 @@ def build_covariate_basis(covariates: np.ndarray, include_intercept: bool = True
     labels = list(column_names) if column_names else [f"covar{j + 1}" for j in range(c.shape[1])]
     if len(labels) != c.shape[1]:
         raise ValueError("column_names length does not match covariates")
+    ct = np.ascontiguousarray(c.T)  # contiguous columns (the loop below is per column)
     cols = ([("intercept", np.ones(n))] if include_intercept else []) + [
-        (labels[j], c[:, j]) for j in range(c.shape[1])
+        (labels[j], ct[j]) for j in range(c.shape[1])
     ]
     basis: list[np.ndarray] = []
     kept: list[str] = []
