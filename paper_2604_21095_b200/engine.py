@@ -401,20 +401,40 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
 
         try:
             staged: list = [None, None]
-            with ThreadPoolExecutor(max_workers=1) as reader:
-                fut = reader.submit(read, 0)
-                pending = None
-                for i in range(len(plan)):
-                    block, dt_read = fut.result()
-                    t_decode += dt_read
-                    staged[i % 2] = stage(i, block)
-                    if i + 1 < len(plan):
-                        fut = reader.submit(read, i + 1)
-                    if pending is not None:
-                        finish(pending, ctx.scan_staged(pending % 2, full_elem_bytes=dtype.itemsize))
-                    staged_ready(i)
-                    pending = i
-                finish(pending, ctx.scan_staged(pending % 2, full_elem_bytes=dtype.itemsize))
+            # records of batch i-1 are formatted / written on a writer thread while batch i
+            # scans (TOPK stays synchronous: its bar feeds the next batch's premask)
+            emitter = ThreadPoolExecutor(max_workers=1) if config.output_mode is not OutputMode.TOPK else None
+            emit_fut = None
+
+            def dispatch(i, res):
+                nonlocal emit_fut
+                if emitter is None:
+                    finish(i, res)
+                    return
+                if emit_fut is not None:
+                    emit_fut.result()  # one batch in the writer at a time; re-raises its errors
+                emit_fut = emitter.submit(finish, i, res)
+
+            try:
+                with ThreadPoolExecutor(max_workers=1) as reader:
+                    fut = reader.submit(read, 0)
+                    pending = None
+                    for i in range(len(plan)):
+                        block, dt_read = fut.result()
+                        t_decode += dt_read
+                        staged[i % 2] = stage(i, block)
+                        if i + 1 < len(plan):
+                            fut = reader.submit(read, i + 1)
+                        if pending is not None:
+                            dispatch(pending, ctx.scan_staged(pending % 2, full_elem_bytes=dtype.itemsize))
+                        staged_ready(i)
+                        pending = i
+                    dispatch(pending, ctx.scan_staged(pending % 2, full_elem_bytes=dtype.itemsize))
+                if emit_fut is not None:
+                    emit_fut.result()
+            finally:
+                if emitter is not None:
+                    emitter.shutdown(wait=True)
             if config.min_p_sidecar:
                 # per-phenotype max |r| over every scanned marker (fused into the GEMM epilogue)
                 max_abs_r = ctx.max_abs_r()
