@@ -370,10 +370,18 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
       }
       __syncwarp();  // earlier literals / copies by other lanes are visible
       // an overlapping match repeats the last `distance` bytes: source offset j mod distance
+      // (j < 258: a float reciprocal gives the quotient within one, fixed up exactly)
+      const float inv_d = __frcp_rn(static_cast<float>(distance));
+      const bool from_ring = distance <= kRingSafe;
       for (int j = lane; j < length; j += 32) {
-        const int jj = distance >= length ? j : j % distance;
+        int jj = j;
+        if (distance < length) {
+          jj = j - distance * __float2int_rz(static_cast<float>(j) * inv_d);
+          jj += jj < 0 ? distance : 0;
+          jj -= jj >= distance ? distance : 0;
+        }
         const int src = pos - distance + jj;
-        const uint8_t v = distance <= kRingSafe ? sm.ring[src & (kRing - 1)] : dst[src];
+        const uint8_t v = from_ring ? sm.ring[src & (kRing - 1)] : dst[src];
         dst[pos + j] = v;
         sm.ring[(pos + j) & (kRing - 1)] = v;
       }
