@@ -9,7 +9,7 @@
 //
 // Latency is what bounds a warp here (one symbol depends on the previous one), so the hot
 // loop avoids global-memory round trips: the bit buffer is refilled 32 bits at a time
-// from the next aligned input word (prefetched one refill ahead), and the last 4 KB of
+// from the next aligned input word (prefetched one refill ahead), and the last 2 KB of
 // output are mirrored in a per-warp shared-memory ring that serves match sources (typical
 // BGEN distances are short); only farther matches read back from global memory.
 //
@@ -29,7 +29,7 @@ constexpr int kLitBits = 10;
 constexpr int kDistBits = 8;
 constexpr int kClenBits = 7;
 constexpr int kWarpsPerBlock = 4;
-constexpr int kRing = 4096;             // bytes of recent output mirrored in smem
+constexpr int kRing = 2048;             // bytes of recent output mirrored in smem
 constexpr int kRingSafe = kRing - 258;  // a copy never overwrites its own sources
 
 __constant__ uint16_t c_len_base[29] = {3,  4,  5,  6,  7,  8,  9,  10, 11,  13,  15,  17,  19,  23, 27,

@@ -1,0 +1,72 @@
+"""Parity at the BASELINE sizes (N = 23,000 samples, P = 20,480 phenotypes; fewer markers):
+the device FULL statistics for a sample of markers equal the oracle's float64 restatement
+of the reference path (|dt| <= 1e-4 max(1, |t|)), and the THRESHOLD hits equal the
+brute-force p <= 1e-4 filter of the same FULL matrix away from the threshold
+(size-independent properties of the full-size contraction: K = 23,040, 80 phenotype tiles)."""
+import numpy as np
+import pytest
+
+from oracle import scan_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+N, P, M = 23_000, 20_480, 1_024
+
+
+@pytest.fixture(scope="module")
+def full_size():
+    from paper_2604_21095_b200 import _native
+    from paper_2604_21095_b200._device import DeviceContext
+
+    rng = np.random.default_rng(2604)
+    y = rng.standard_normal((N, P), dtype=np.float32).astype(np.float64)
+    y -= y.mean(axis=0)
+    y /= np.sqrt((y * y).mean(axis=0))
+    af = rng.uniform(0.05, 0.95, M)
+    g = rng.binomial(2, af[:, None], size=(M, N)).astype(np.uint8)
+    miss = rng.random((M, N)) < 0.01
+    miss[: M // 2] = False  # half the markers without missing calls
+    codes = np.array([3, 2, 0], np.uint8)[g]
+    codes[miss] = 1
+    bpm = (N + 3) // 4
+    codes = np.pad(codes, ((0, 0), (0, bpm * 4 - N))).reshape(M, bpm, 4)
+    packed = (codes[:, :, 0] | (codes[:, :, 1] << 2) | (codes[:, :, 2] << 4) | (codes[:, :, 3] << 6)).astype(np.uint8)
+    ctx = DeviceContext(0)
+    ctx.set_panel(y, np.arange(N, dtype=np.int64), N)
+    df = float(N - 2)
+    yield ctx, y, packed, df, _native
+    ctx.close()
+
+
+def test_full_statistics_match_oracle(full_size):
+    ctx, y, packed, df, _native = full_size
+    ctx.set_scan(df, _native.PG_MODE_FULL, None)
+    res = ctx.scan(_native.PG_GENO_BED, packed, packed.shape[1])
+    t_dev = res.t_rows
+    assert t_dev.shape == (M, P)
+    pick = np.r_[0:4, M // 2:M // 2 + 4, M - 4:M]  # markers with and without missing calls
+    dos = orc.decode_bed(packed[pick], N)
+    ref = orc.threshold_scan(dos, y, df, 1.0)  # every pair: (rows, cols, r, t, p)
+    t_ref = np.zeros((pick.size, P))
+    t_ref[ref["rows"], ref["cols"]] = ref["t"]
+    rel = np.abs(t_dev[pick] - t_ref) / np.maximum(1.0, np.abs(t_ref))
+    assert rel.max() <= 1e-4
+
+
+def test_threshold_hits_equal_full_filter(full_size):
+    from paper_2604_21095_b200.engine import threshold_premask
+    from paper_2604_21095_b200.kernel import t_threshold_for_p
+
+    ctx, y, packed, df, _native = full_size
+    ctx.set_scan(df, _native.PG_MODE_FULL, None)
+    t_full = ctx.scan(_native.PG_GENO_BED, packed, packed.shape[1]).t_rows
+    ctx.set_scan(df, _native.PG_MODE_THRESHOLD, np.full(P, threshold_premask(1e-4, df)))
+    res = ctx.scan(_native.PG_GENO_BED, packed, packed.shape[1])
+    hits = set(zip(res.cand_rows[res.cand_p <= 1e-4].tolist(), res.cand_cols[res.cand_p <= 1e-4].tolist()))
+    t_crit = t_threshold_for_p(1e-4, df)
+    a = np.abs(t_full)
+    sure_in = set(zip(*np.nonzero(a > t_crit * (1 + 1e-4))))
+    sure_out = set(zip(*np.nonzero(a < t_crit * (1 - 1e-4))))
+    assert sure_in <= hits
+    assert not (hits & sure_out)
+    assert 0.5e-4 * M * P < len(hits) < 2e-4 * M * P  # null: ~1e-4 of the tests
