@@ -187,6 +187,29 @@ def topk_premask(worst_abs_t: np.ndarray, t_floor: float, df: float) -> np.ndarr
     return np.where(bar_t <= 0.0, -1.0, bar_r * (1.0 - 1e-12))
 
 
+_TOPK_NULL_FACTOR = 16.0  # expected null candidates per missing top-k slot in a batch
+
+
+def topk_batch_bars(writer, top_k: int, batch_markers: int, t_floor: float, df: float):
+    """Per-phenotype |r| bars for the next TOPK batch and the candidate counts they must yield.
+
+    Phenotypes already holding k records use the admission bar of their k-th record (the
+    reference's rule, engine.py:205-211). A phenotype still short of k records would admit
+    every marker (the reference's per-4,096-marker batches can afford that; a 65,536-marker
+    device batch x 20,480 phenotypes cannot), so its bar is the null quantile at
+    p = 16 * missing / batch: all markers beating the batch's k-th best are then above the
+    bar whenever at least `missing` candidates pass, which the caller checks (and rescans
+    the batch without a bar for any phenotype that falls short)."""
+    bars = topk_premask(writer.worst_abs_t, t_floor, df)
+    kept = writer.kept_counts()
+    short = kept < top_k
+    need = np.where(short, top_k - kept, 0)
+    for miss in np.unique(need[short]).tolist():
+        p_q = min(1.0, _TOPK_NULL_FACTOR * miss / max(batch_markers, 1))
+        bars[need == miss] = threshold_premask(p_q, df) if p_q < 1.0 else -1.0
+    return bars, need
+
+
 def device_batch_size(config: ScanConfig, n_markers: int, n_pheno: int) -> int:
     """Markers per device launch: at least the configured batch, sized for the GEMM, memory-bounded."""
     if config.device_batch is not None:
@@ -329,7 +352,7 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
             rbar = np.full(n_pheno, threshold_premask(config.p_threshold, df))
         elif config.output_mode is OutputMode.TOPK:
             t_floor = kernel.t_threshold_for_p(kernel.P_FLOOR, df)
-            rbar = topk_premask(writer.worst_abs_t, t_floor, df)
+            rbar = None  # set per batch below (topk_batch_bars)
         else:
             rbar = None
         ctx.set_scan(df, _MODE_CODE[config.output_mode], rbar)
@@ -364,6 +387,8 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
             return block, time.perf_counter() - t0
 
         def stage(i, block):
+            if config.output_mode is OutputMode.TOPK:
+                kept_blocks[i] = block  # kept for a (rare) rescan
             if compressed:  # H2D + GPU inflate run while the previous batch is scanned
                 return ctx.stage_bgen_begin(i % 2, *block)
             kind, rows, row_bytes = block
@@ -375,8 +400,44 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
                 if bad is not None:
                     source.raise_block_error(plan[i][0] + bad[0], bad[1], bad[2], bad[3])
 
+        topk_need = {}
+        kept_blocks = {}
+
+        def set_topk_bars(i):
+            if config.output_mode is OutputMode.TOPK and i < len(plan):
+                bars, need = topk_batch_bars(writer, config.top_k, plan[i][1], t_floor, df)
+                ctx.set_rbar(bars)
+                topk_need[i] = (bars, need)
+
+        def topk_complete(i, res):
+            """Rescan batch i without a bar for phenotypes whose null-quantile bar admitted
+            fewer candidates than they still need (rare; exactness of the top-k selection)."""
+            bars, need = topk_need.pop(i)
+            have = np.bincount(res.cand_cols, minlength=n_pheno) if res.cand_cols is not None else np.zeros(n_pheno)
+            short = (need > 0) & (bars > 0) & (have < need)
+            if not short.any():
+                return res
+            start, count = plan[i]
+            block = kept_blocks[i]
+            if compressed:
+                block = source.read_raw_block(start, count)
+            kind, rows, row_bytes = block
+            ctx.set_rbar(np.where(short, -1.0, 2.0))  # everything for the short phenotypes, nothing else
+            extra = ctx.scan(kind, rows, row_bytes, full_elem_bytes=dtype.itemsize)
+            keep_old = ~short[res.cand_cols]
+            rows_ = np.concatenate([res.cand_rows[keep_old], extra.cand_rows])
+            cols_ = np.concatenate([res.cand_cols[keep_old], extra.cand_cols])
+            order = np.lexsort((cols_, rows_))  # (marker, phenotype) order
+            for name in ("cand_r", "cand_t", "cand_p"):
+                setattr(res, name, np.concatenate([getattr(res, name)[keep_old], getattr(extra, name)])[order])
+            res.cand_rows, res.cand_cols = rows_[order], cols_[order]
+            return res
+
         def finish(i, res):
             nonlocal t_prepare, t_corr, t_emit, clamp_total, skip_mono, skip_missing
+            if config.output_mode is OutputMode.TOPK:
+                res = topk_complete(i, res)
+                kept_blocks.pop(i, None)
             start, count = plan[i]
             t_prepare += res.decode_ms / 1e3
             t_corr += res.gemm_ms / 1e3
@@ -396,8 +457,7 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
             t0 = time.perf_counter()
             writer.emit(batch)
             t_emit += time.perf_counter() - t0
-            if config.output_mode is OutputMode.TOPK:
-                ctx.set_rbar(topk_premask(writer.worst_abs_t, t_floor, df))
+            set_topk_bars(i + 1)
 
         try:
             staged: list = [None, None]
@@ -415,6 +475,7 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
                     emit_fut.result()  # one batch in the writer at a time; re-raises its errors
                 emit_fut = emitter.submit(finish, i, res)
 
+            set_topk_bars(0)
             try:
                 with ThreadPoolExecutor(max_workers=1) as reader:
                     fut = reader.submit(read, 0)

@@ -239,3 +239,31 @@ def test_min_p_sidecar_equals_full_scan_minimum(tmp_path):
     want_p = pg.p_from_t(want_t, 118.0)
     np.testing.assert_allclose(-np.log10(got_p), -np.log10(want_p), rtol=1e-4)
     assert np.argmin(got_p) == 3
+
+
+def test_topk_large_batches_null_bar_and_rescan(tmp_path):
+    """Device batches much larger than 16k markers: phenotypes short of k records get a
+    null-quantile bar instead of admitting every marker; a phenotype whose statistics are
+    far below the null (one informative sample) falls short and its batch is rescanned.
+    The output equals the brute-force top-k by (p, source index) of the full scan."""
+    rng = np.random.default_rng(31)
+    n, m, k = 60, 900, 3
+    d, y = random_dataset(rng, m, n, 4)
+    d[:, 0] = 1.0  # sample 0 heterozygous everywhere ...
+    y[:, 2] = 0.0
+    y[0, 2] = 1.0  # ... and phenotype 3 supported on it: |t| < 1.1 for every marker (sub-null)
+    y[:, 3] += 0.9 * d[123]  # a planted hit
+    spec, pheno, _, root = dataset(tmp_path, d, y)
+    scan(spec, pheno, root / "all.tsv", p_threshold=1.0, precision=pg.Precision.F64)
+    scan(spec, pheno, root / "top.tsv", output_mode=pg.OutputMode.TOPK, top_k=k, precision=pg.Precision.F64,
+         device_batch=400)
+    by = {}
+    for r in pg.load_association_records(root / "all.tsv"):
+        by.setdefault(r.phenotype, []).append(r)
+    expected = []
+    for name in sorted(by):
+        recs = sorted(by[name], key=lambda r: (r.p, r.pos))[:k]
+        expected += [(r.id, name, r.t) for r in recs]
+    got = [(r.id, r.phenotype, r.t) for r in pg.load_association_records(root / "top.tsv")]
+    assert sorted(got, key=lambda x: (x[1], x[0])) == sorted(expected, key=lambda x: (x[1], x[0]))
+    assert ("snp124", "ph4") in {(g[0], g[1]) for g in got}
