@@ -352,7 +352,7 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
             rbar = np.full(n_pheno, threshold_premask(config.p_threshold, df))
         elif config.output_mode is OutputMode.TOPK:
             t_floor = kernel.t_threshold_for_p(kernel.P_FLOOR, df)
-            rbar = None  # set per batch below (topk_batch_bars)
+            rbar = np.full(n_pheno, -1.0)  # replaced per batch below (topk_batch_bars)
         else:
             rbar = None
         ctx.set_scan(df, _MODE_CODE[config.output_mode], rbar)
