@@ -188,6 +188,7 @@ def topk_premask(worst_abs_t: np.ndarray, t_floor: float, df: float) -> np.ndarr
 
 
 _TOPK_NULL_FACTOR = 16.0  # expected null candidates per missing top-k slot in a batch
+topk_rescans = 0  # batches rescanned because a null-quantile bar admitted too few (diagnostics)
 
 
 def topk_batch_bars(writer, top_k: int, batch_markers: int, t_floor: float, df: float):
@@ -417,6 +418,8 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
             short = (need > 0) & (bars > 0) & (have < need)
             if not short.any():
                 return res
+            global topk_rescans
+            topk_rescans += 1
             start, count = plan[i]
             block = kept_blocks[i]
             if compressed:

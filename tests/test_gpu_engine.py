@@ -255,8 +255,12 @@ def test_topk_large_batches_null_bar_and_rescan(tmp_path):
     y[:, 3] += 0.9 * d[123]  # a planted hit
     spec, pheno, _, root = dataset(tmp_path, d, y)
     scan(spec, pheno, root / "all.tsv", p_threshold=1.0, precision=pg.Precision.F64)
+    from paper_2604_21095_b200 import engine
+
+    before = engine.topk_rescans
     scan(spec, pheno, root / "top.tsv", output_mode=pg.OutputMode.TOPK, top_k=k, precision=pg.Precision.F64,
          device_batch=400)
+    assert engine.topk_rescans > before  # the sub-null phenotype forced the exact fallback
     by = {}
     for r in pg.load_association_records(root / "all.tsv"):
         by.setdefault(r.phenotype, []).append(r)
