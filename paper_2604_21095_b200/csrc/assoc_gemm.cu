@@ -90,13 +90,28 @@ struct Cfg {
   static_assert(kSmemBytes <= 227 * 1024, "shared memory per CTA");
 };
 
+// group_c > 0: genotype-stationary groups of group_c genotype tiles x all phenotype tiles
+//              (phenotype-major inside a group);
+// group_c < 0: panel-stationary groups of -group_c phenotype tiles x all genotype tiles
+//              (genotype-major inside a group: a wave streams genotype tiles past a panel
+//              slice that stays in L2).
 __device__ __forceinline__ void tile_coords(int t, int n_ctile, int n_ptile, int group_c, int& ct, int& pt) {
-  const int group = t / (group_c * n_ptile);
-  const int first = group * group_c;
-  const int gsz = min(group_c, n_ctile - first);
-  const int r = t - group * group_c * n_ptile;
-  ct = first + r % gsz;
-  pt = r / gsz;
+  if (group_c > 0) {
+    const int group = t / (group_c * n_ptile);
+    const int first = group * group_c;
+    const int gsz = min(group_c, n_ctile - first);
+    const int r = t - group * group_c * n_ptile;
+    ct = first + r % gsz;
+    pt = r / gsz;
+  } else {
+    const int gp = -group_c;
+    const int group = t / (gp * n_ctile);
+    const int first = group * gp;
+    const int gsz = min(gp, n_ptile - first);
+    const int r = t - group * gp * n_ctile;
+    pt = first + r % gsz;
+    ct = r / gsz;
+  }
 }
 
 __device__ __forceinline__ void fence_proxy_async_smem() {
@@ -463,7 +478,7 @@ int launch_common(const CUtensorMap& tm_qh, const CUtensorMap& tm_q1, const CUte
   const int grid = 2 * pairs;
   // tuning knobs (defaults measured best): raster group width and
   // L2 priorities (panel | geno << 2; 0 normal, 1 evict_last, 2 evict_first)
-  static const int env_group = [] {
+  static const int env_group = [] {  // > 0 genotype-stationary width, < 0 panel-stationary height
     const char* e = std::getenv("PG_GROUP_C");
     return e ? std::atoi(e) : 0;
   }();
@@ -471,7 +486,7 @@ int launch_common(const CUtensorMap& tm_qh, const CUtensorMap& tm_q1, const CUte
     const char* e = std::getenv("PG_L2_CODES");
     return e ? std::atoi(e) : -1;
   }();
-  const int group_c = env_group > 0 ? env_group : pairs;
+  const int group_c = env_group != 0 ? env_group : pairs;
   const uint32_t l2_codes = env_l2 >= 0 ? static_cast<uint32_t>(env_l2) : kDefaultL2Codes;
   assoc_i8_kernel<MODE><<<grid, kThreads, Cfg<MODE>::kSmemBytes, stream>>>(
       tm_qh, tm_q1, tm_q0, tm_v, tm_v127, n_ctile, n_ptile, static_cast<int>(k_pad / kTileK), group_c, l2_codes,
