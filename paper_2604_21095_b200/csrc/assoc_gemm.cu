@@ -65,13 +65,12 @@ constexpr int kEpiWarps = 16;
 constexpr int kFirstEpiWarp = 8;
 constexpr int kThreads = 32 * (kFirstEpiWarp + kEpiWarps);
 constexpr int kTmemCols = 512;
-// Raster: tiles are visited in groups of `group_c` genotype tiles x all phenotype
-// tiles, phenotype-major inside a group. With group_c = number of pairs (74 on a
-// B200) every wave of the persistent grid covers exactly one phenotype tile, read by
-// all pairs at the same time (one DRAM fetch, 73 L2 hits), and every pair keeps the
-// same genotype tile for the whole group (74 x 1.5 MB packed rows stay in L2).
-// Measured on the C3 slice (tools/sweep_l2.sh): 2.06e10 tests/s vs 1.91e10 for the
-// previous 32-tile groups; both operands evict_last (evict_first panel: -15%).
+// Raster (tile_coords): groups of tiles visited by the persistent grid so that one wave
+// (74 pair tiles) shares operands in L2. Measured on the C3 slice (tools/sweep_l2.sh,
+// tools/dram_sweep.sh): genotype-stationary groups of 74 genotype tiles (one phenotype tile
+// per wave) 2.06e10 tests/s and 49 GB DRAM per launch, vs 1.91e10 for 32-tile groups;
+// panel-stationary groups of 2 phenotype tiles (the default) 22 GB per launch at equal or
+// better throughput; evict_first on the panel costs 15 %.
 
 template <int MODE>
 struct Cfg {
@@ -460,6 +459,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 }
 
 constexpr uint32_t kDefaultL2Codes = 1u | (1u << 2);  // panel and genotypes evict_last
+// Panel-stationary raster, 2 phenotype tiles per group (35 MB of limbs stay in L2 while the
+// genotype tiles stream past): DRAM per C3 launch 22 GB vs 49 GB for 74-tile
+// genotype-stationary groups (tools/dram_sweep.sh, ncu), with equal or better throughput.
+constexpr int kDefaultGroup = -2;
 
 template <int MODE>
 int launch_common(const CUtensorMap& tm_qh, const CUtensorMap& tm_q1, const CUtensorMap& tm_q0,
@@ -486,7 +489,7 @@ int launch_common(const CUtensorMap& tm_qh, const CUtensorMap& tm_q1, const CUte
     const char* e = std::getenv("PG_L2_CODES");
     return e ? std::atoi(e) : -1;
   }();
-  const int group_c = env_group != 0 ? env_group : pairs;
+  const int group_c = env_group != 0 ? env_group : kDefaultGroup;
   const uint32_t l2_codes = env_l2 >= 0 ? static_cast<uint32_t>(env_l2) : kDefaultL2Codes;
   assoc_i8_kernel<MODE><<<grid, kThreads, Cfg<MODE>::kSmemBytes, stream>>>(
       tm_qh, tm_q1, tm_q0, tm_v, tm_v127, n_ctile, n_ptile, static_cast<int>(k_pad / kTileK), group_c, l2_codes,
