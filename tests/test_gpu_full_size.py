@@ -70,3 +70,32 @@ def test_threshold_hits_equal_full_filter(full_size):
     assert sure_in <= hits
     assert not (hits & sure_out)
     assert 0.5e-4 * M * P < len(hits) < 2e-4 * M * P  # null: ~1e-4 of the tests
+
+
+@pytest.mark.parametrize("p", [255, 700, 1300])
+def test_odd_tile_counts_match_oracle(p):
+    """Phenotype-tile counts that do not divide the raster group (1, 3, 6 tiles of 256) and a
+    marker count that leaves partial genotype tiles: every (marker, phenotype) visited once."""
+    from paper_2604_21095_b200 import _native
+    from paper_2604_21095_b200._device import DeviceContext
+
+    rng = np.random.default_rng(p)
+    n, m = 333, 1111
+    y = rng.standard_normal((n, p))
+    y -= y.mean(axis=0)
+    y /= np.sqrt((y * y).mean(axis=0))
+    g = rng.binomial(2, rng.uniform(0.1, 0.9, (m, 1)), size=(m, n)).astype(np.uint8)
+    bpm = (n + 3) // 4
+    codes = np.pad(np.array([3, 2, 0], np.uint8)[g], ((0, 0), (0, bpm * 4 - n))).reshape(m, bpm, 4)
+    packed = (codes[:, :, 0] | (codes[:, :, 1] << 2) | (codes[:, :, 2] << 4) | (codes[:, :, 3] << 6)).astype(np.uint8)
+    with DeviceContext(0) as ctx:
+        ctx.set_panel(y, np.arange(n, dtype=np.int64), n)
+        ctx.set_scan(float(n - 2), _native.PG_MODE_FULL, None)
+        t_dev = ctx.scan(_native.PG_GENO_BED, packed, bpm).t_rows
+    ref = orc.threshold_scan(orc.decode_bed(packed, n), y, float(n - 2), 1.0)
+    t_ref = np.zeros((m, p))
+    t_ref[ref["rows"], ref["cols"]] = ref["t"]
+    ok = ref["skip"] == 0
+    t_ok = t_dev[ok] if t_dev.shape[0] == m else t_dev  # FULL rows may list non-skipped markers only
+    rel = np.abs(t_ok - t_ref[ok]) / np.maximum(1.0, np.abs(t_ref[ok]))
+    assert rel.max() <= 1e-4
