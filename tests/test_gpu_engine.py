@@ -271,3 +271,45 @@ def test_topk_large_batches_null_bar_and_rescan(tmp_path):
     got = [(r.id, r.phenotype, r.t) for r in pg.load_association_records(root / "top.tsv")]
     assert sorted(got, key=lambda x: (x[1], x[0])) == sorted(expected, key=lambda x: (x[1], x[0]))
     assert ("snp124", "ph4") in {(g[0], g[1]) for g in got}
+
+
+def test_bgen_matches_plink_with_alleles_swapped_and_rerun_identical(tmp_path):
+    """The same dosage matrix through the PLINK and BGEN-16 readers: identical statistics,
+    opposite counted-allele labels (PLINK counts allele1, BGEN allele2); and a rerun of the
+    same scan is byte-identical (reference tests: engine / determinism)."""
+    from bgen_fixture import write_bgen
+
+    rng = np.random.default_rng(23)
+    d = rng.integers(0, 3, size=(8, 30)).astype(np.float64)
+    y = rng.standard_normal((30, 2))
+    spec, pheno, _, root = dataset(tmp_path, d, y)
+    ids = [f"S{i + 1}" for i in range(30)]
+    bspec = pg.SourceSpec(pg.GenotypeFormat.BGEN, bgen_path=write_bgen(root / "g.bgen", d, ids, bits=16))
+    scan(spec, pheno, root / "plink.tsv", p_threshold=1.0, precision=pg.Precision.F64)
+    scan(bspec, pheno, root / "bgen.tsv", p_threshold=1.0, precision=pg.Precision.F64)
+    a = pg.load_association_records(root / "plink.tsv")
+    b = pg.load_association_records(root / "bgen.tsv")
+    assert len(a) == len(b) == 16
+    for ra, rb in zip(a, b):
+        assert ra.phenotype == rb.phenotype
+        assert (ra.counted_allele, ra.other_allele) == ("A", "B")
+        assert (rb.counted_allele, rb.other_allele) == ("B", "A")
+        assert rb.t == pytest.approx(ra.t, rel=1e-9, abs=1e-12)
+        assert rb.af == pytest.approx(ra.af, abs=1e-12)
+    scan(bspec, pheno, root / "bgen2.tsv", p_threshold=1.0, precision=pg.Precision.F64)
+    assert (root / "bgen2.tsv").read_bytes() == (root / "bgen.tsv").read_bytes()
+
+
+def test_null_calibration(tmp_path):
+    """Under the null the p-values are uniform: P(p <= a) ~ a, KS distance small
+    (reference acceptance criterion 9)."""
+    rng = np.random.default_rng(909)
+    d, y = random_dataset(rng, 2000, 400, 64, maf=(0.05, 0.95))
+    spec, pheno, _, root = dataset(tmp_path, d, y)
+    scan(spec, pheno, root / "all.tsv", p_threshold=1.0, precision=pg.Precision.F64)
+    p = np.sort(np.array([r.p for r in pg.load_association_records(root / "all.tsv")]))
+    m = p.size
+    for a, tol in ((0.05, 0.004), (0.01, 0.0015)):
+        assert abs(np.mean(p <= a) - a) < tol
+    ks = np.max(np.abs(p - (np.arange(1, m + 1) / m)))
+    assert ks < 0.01
