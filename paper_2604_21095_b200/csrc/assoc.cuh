@@ -11,6 +11,7 @@
 // All products and sums are integers, so the tensor-core result is exact and
 // independent of tiling, batching and GPU count.
 #pragma once
+#include <climits>
 #include <cstdint>
 
 #include "pg_common.cuh"
@@ -22,6 +23,9 @@ constexpr int kTileC = 256;   // genotype rows per pair tile (UMMA N, B operand;
 constexpr int kTileK = 64;    // int8 samples per pipeline stage (one 64-byte swizzle row)
 constexpr int64_t kWH = 32385;          // weight of the high limb: 2*(127*127+63)+1
 constexpr int64_t kQMax = kWH * 127 + 16192;  // largest |q| representable by the limbs
+// Largest padded sample count whose int32 accumulators cannot overflow: one sample adds at
+// most 127*127 + 63 = 16192 to accL (ternary) or 127*127 to A / B (wide digits).
+constexpr int64_t kMaxExactK = (INT32_MAX / 16192) / 64 * 64;  // 132,608
 
 struct AssocEpilogue {
   int rows_per_marker;          // ternary: 1 (u), 2 (u, missing), 8 / 16 (digits + missing); wide: 4

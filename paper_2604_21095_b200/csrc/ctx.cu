@@ -266,6 +266,9 @@ int upload_panel_common(pg_ctx* c, const double* d_y, int64_t n_kept, int64_t n_
   c->n_kept = n_kept;
   c->n_pheno = n_pheno;
   c->p_pad = round_up(n_pheno, kTileP);
+  PG_REQUIRE(round_up(n_src, 64) <= kMaxExactK, PG_ERR_CONFIG,
+             "%lld genotype samples exceed the exact int32 tensor-core accumulation range (%lld); "
+             "split the cohort", (long long)n_src, (long long)kMaxExactK);
   c->k_pad = round_up(n_src, 64);
   bits.assign(c->k_pad / 32 + 1, 0u);
   for (int64_t i = 0; i < n_kept; ++i) {
@@ -742,6 +745,9 @@ int pg_ctx_import_panel(pg_ctx* c, const void* d_src, int64_t n_kept, int64_t n_
   c->n_kept = n_kept;
   c->n_pheno = n_pheno;
   c->p_pad = round_up(n_pheno, kTileP);
+  PG_REQUIRE(round_up(n_samples_src, 64) <= kMaxExactK, PG_ERR_CONFIG,
+             "%lld genotype samples exceed the exact int32 tensor-core accumulation range (%lld); "
+             "split the cohort", (long long)n_samples_src, (long long)kMaxExactK);
   c->k_pad = round_up(n_samples_src, 64);
   bits.assign(c->k_pad / 32 + 1, 0u);
   for (int64_t i = 0; i < n_kept; ++i) {

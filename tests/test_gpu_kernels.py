@@ -190,3 +190,16 @@ def test_device_panel_prep_rejects_non_finite():
     with DeviceContext(0) as ctx:
         with pytest.raises(ValueError, match="finite"):
             ctx.prepare_panel(y, None)
+
+
+@pytest.mark.gpu
+def test_sample_count_beyond_exact_range_is_refused():
+    """K_pad > 132,608 would let the int32 accumulators overflow: refused loudly, never a
+    silently wrong statistic."""
+    from paper_2604_21095_b200._device import DeviceContext
+    from paper_2604_21095_b200.errors import ConfigError
+
+    with DeviceContext(0) as ctx:
+        with pytest.raises(ConfigError, match="exact int32"):
+            ctx.set_panel(np.ones((3, 1)) * [[1.0], [-1.0], [0.5]], np.arange(3, dtype=np.int64), 140_000)
+        ctx.set_panel(np.array([[1.0], [-1.0], [0.5]]), np.arange(3, dtype=np.int64), 132_608)
