@@ -26,6 +26,10 @@ constexpr int64_t kQMax = kWH * 127 + 16192;  // largest |q| representable by th
 // Largest padded sample count whose int32 accumulators cannot overflow: one sample adds at
 // most 127*127 + 63 = 16192 to accL (ternary) or 127*127 to A / B (wide digits).
 constexpr int64_t kMaxExactK = (INT32_MAX / 16192) / 64 * 64;  // 132,608
+// Larger cohorts run the contraction in K slices of kSliceK samples whose int32 results
+// are exact and are summed in int64 (AssocEpilogue::x_accum).
+constexpr int64_t kSliceK = 131072;
+static_assert(kSliceK <= kMaxExactK, "slice must stay inside the exact int32 range");
 
 struct AssocEpilogue {
   int rows_per_marker;          // ternary: 1 (u), 2 (u, missing), 8 / 16 (digits + missing); wide: 4
@@ -48,6 +52,8 @@ struct AssocEpilogue {
   unsigned int* max_abs_r;      // [p_pad] running max |r| (float bits), or null
   double* full_r;               // FULL mode: r[marker * full_ld + p] (fp64), or null
   int64_t full_ld;
+  long long* x_accum;           // K-sliced runs (k_pad > kSliceK): int64 (xu, xm) partials
+  int64_t x_ld;                 //   [marker slot][x_ld = p_pad][2]; null otherwise
 };
 
 // Launch K2/K3 on `stream`. Panel limbs q*[p_pad, k_pad], genotype planes

@@ -201,10 +201,16 @@ __device__ __forceinline__ void epilogue_tile_wide(const AssocEpilogue& ep, uint
                static_cast<int>(d[j + t]);
       const long long xu = x[0] + 255ll * x[1] + 65025ll * x[2];
       const int m = ct * kMarkersPerTile + (c + j) / kRowsW;
+      if (ep.x_accum) {
+        long long* xa = ep.x_accum + (static_cast<int64_t>(m) * ep.x_ld + pheno) * 2;
+        xa[0] += xu;
+        xa[1] += x[3];
+        continue;
+      }
       epilogue_value(ep, xu, x[3], m, pheno, sc_f, sc_d, cq_f, cq, rb, lane, lanemask_lt, mx);
     }
   }
-  if (ep.max_abs_r && pheno < ep.p_valid) atomicMax(ep.max_abs_r + pheno, __float_as_uint(mx));
+  if (ep.max_abs_r && !ep.x_accum && pheno < ep.p_valid) atomicMax(ep.max_abs_r + pheno, __float_as_uint(mx));
 }
 
 template <int R>
@@ -240,17 +246,23 @@ __device__ __forceinline__ void epilogue_tile(const AssocEpilogue& ep, uint32_t 
         xm = kWH * static_cast<long long>(static_cast<int>(h[j + R - 1])) + static_cast<int>(l[j + R - 1]);
       }
       const int m = ct * kMarkersPerTile + (c + j) / R;
+      if (ep.x_accum) {  // K-sliced run: exact int64 partials, statistics after the last slice
+        long long* x = ep.x_accum + (static_cast<int64_t>(m) * ep.x_ld + pheno) * 2;
+        x[0] += xu;
+        x[1] += xm;
+        continue;
+      }
       epilogue_value(ep, xu, xm, m, pheno, sc_f, sc_d, cq_f, cq, rb, lane, lanemask_lt, mx);
     }
   }
-  if (ep.max_abs_r && pheno < ep.p_valid) atomicMax(ep.max_abs_r + pheno, __float_as_uint(mx));
+  if (ep.max_abs_r && !ep.x_accum && pheno < ep.p_valid) atomicMax(ep.max_abs_r + pheno, __float_as_uint(mx));
 }
 
 template <int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     assoc_i8_kernel(const __grid_constant__ CUtensorMap tm_qh, const __grid_constant__ CUtensorMap tm_q1,
                     const __grid_constant__ CUtensorMap tm_q0, const __grid_constant__ CUtensorMap tm_v,
-                    const __grid_constant__ CUtensorMap tm_v127, int n_ctile, int n_ptile, int n_kb,
+                    const __grid_constant__ CUtensorMap tm_v127, int n_ctile, int n_ptile, int kb_begin, int n_kb,
                     int group_c, uint32_t l2_codes, AssocEpilogue ep) {
   using C = Cfg<MODE>;
   constexpr bool FUSED = C::FUSED;
@@ -313,7 +325,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < n_kb; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = smem + s * C::kStageBytes;
-          const int kx = kb * kTileK;
+          const int kx = (kb_begin + kb) * kTileK;
           const uint32_t full0 = map_to_cta(&full[s], 0);
           mbar_arrive_expect_tx_cluster(full0, C::kTmaBytes);
           tma_load_2d_pair(st, &tm_qh, full0, kx, prow, pol_panel);
@@ -321,7 +333,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           tma_load_2d_pair(st + 2 * kQBytes, &tm_q0, full0, kx, prow, pol_panel);
           if constexpr (FUSED) {
             mbar_arrive_expect_tx(&pk[s], kPackedBytes);
-            tma_load_2d_hint(st + kOffPacked, &tm_v, &pk[s], kb * (kTileK / 4), grow, pol_geno);
+            tma_load_2d_hint(st + kOffPacked, &tm_v, &pk[s], (kb_begin + kb) * (kTileK / 4), grow, pol_geno);
           } else if constexpr (WIDE) {
             tma_load_2d_pair(st + kOffV, &tm_v, full0, kx, grow, pol_geno);
           } else {
@@ -458,6 +470,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 2) tmem_free_pair(tmem_base, kTmemCols);
 }
 
+// Statistics of a K-sliced run from the accumulated int64 partials (xu, xm) per
+// (marker slot, phenotype): lanes = 32 consecutive phenotypes (so the warp-aggregated
+// compaction and the premask work as in the GEMM epilogue), warps stride over markers.
+__global__ void x_epilogue_kernel(AssocEpilogue ep, int64_t m_slots) {
+  const int lane = threadIdx.x & 31;
+  const int pheno = blockIdx.x * 32 + lane;
+  const uint32_t lanemask_lt = (1u << lane) - 1u;
+  const float sc_f = ep.scale_f[pheno];
+  const double sc_d = ep.scale_d[pheno];
+  const float cq_f = ep.cq_f[pheno];
+  const long long cq = ep.cq[pheno];
+  const float rb = ep.rbar ? ep.rbar[pheno] : INFINITY;
+  float mx = 0.f;
+  for (int64_t m = static_cast<int64_t>(blockIdx.y) * (blockDim.x >> 5) + (threadIdx.x >> 5); m < m_slots;
+       m += static_cast<int64_t>(gridDim.y) * (blockDim.x >> 5)) {
+    const long long* x = ep.x_accum + (m * ep.x_ld + pheno) * 2;
+    AssocEpilogue e = ep;
+    e.x_accum = nullptr;
+    epilogue_value(e, x[0], x[1], static_cast<int>(m), pheno, sc_f, sc_d, cq_f, cq, rb, lane, lanemask_lt, mx);
+  }
+  if (ep.max_abs_r && pheno < ep.p_valid) atomicMax(ep.max_abs_r + pheno, __float_as_uint(mx));
+}
+
 constexpr uint32_t kDefaultL2Codes = 1u | (1u << 2);  // panel and genotypes evict_last
 // Panel-stationary raster, 2 phenotype tiles per group (35 MB of limbs stay in L2 while the
 // genotype tiles stream past): DRAM per C3 launch 22 GB vs 49 GB for 74-tile
@@ -491,9 +526,28 @@ int launch_common(const CUtensorMap& tm_qh, const CUtensorMap& tm_q1, const CUte
   }();
   const int group_c = env_group != 0 ? env_group : kDefaultGroup;
   const uint32_t l2_codes = env_l2 >= 0 ? static_cast<uint32_t>(env_l2) : kDefaultL2Codes;
-  assoc_i8_kernel<MODE><<<grid, kThreads, Cfg<MODE>::kSmemBytes, stream>>>(
-      tm_qh, tm_q1, tm_q0, tm_v, tm_v127, n_ctile, n_ptile, static_cast<int>(k_pad / kTileK), group_c, l2_codes,
-      ep);
+  const int n_kb = static_cast<int>(k_pad / kTileK);
+  constexpr int kSliceKb = static_cast<int>(kSliceK / kTileK);
+  if (n_kb <= kSliceKb) {
+    PG_REQUIRE(ep.x_accum == nullptr, PG_ERR_INVALID, "assoc: x_accum given for an unsliced run");
+    assoc_i8_kernel<MODE><<<grid, kThreads, Cfg<MODE>::kSmemBytes, stream>>>(
+        tm_qh, tm_q1, tm_q0, tm_v, tm_v127, n_ctile, n_ptile, 0, n_kb, group_c, l2_codes, ep);
+  } else {
+    // more samples than one int32-exact slice: accumulate int64 partials slice by slice,
+    // then derive the statistics (same epilogue arithmetic) from the exact sums
+    PG_REQUIRE(ep.x_accum != nullptr && ep.x_ld == p_pad, PG_ERR_INVALID, "assoc: K-sliced run needs x_accum");
+    const int rows = MODE == kWide ? kRowsW : ep.rows_per_marker;
+    const int64_t m_slots = c_pad / rows;
+    PG_CUDA_CHECK(cudaMemsetAsync(ep.x_accum, 0, sizeof(long long) * 2 * m_slots * p_pad, stream));
+    for (int kb0 = 0; kb0 < n_kb; kb0 += kSliceKb) {
+      const int nk = n_kb - kb0 < kSliceKb ? n_kb - kb0 : kSliceKb;
+      assoc_i8_kernel<MODE><<<grid, kThreads, Cfg<MODE>::kSmemBytes, stream>>>(
+          tm_qh, tm_q1, tm_q0, tm_v, tm_v127, n_ctile, n_ptile, kb0, nk, group_c, l2_codes, ep);
+      PG_CUDA_CHECK(cudaGetLastError());
+    }
+    const unsigned gy = static_cast<unsigned>(m_slots < 4096 ? (m_slots + 7) / 8 : 512);
+    x_epilogue_kernel<<<dim3(static_cast<unsigned>(p_pad / 32), gy), 256, 0, stream>>>(ep, m_slots);
+  }
   PG_CUDA_CHECK(cudaGetLastError());
   return PG_OK;
 }

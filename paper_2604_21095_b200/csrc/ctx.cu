@@ -215,6 +215,7 @@ struct pg_ctx {
   pg::DBuf<int64_t> new_row;
   pg::DBuf<uint8_t> full_out;
   pg::DBuf<double> scratch_a, scratch_b, scratch_c, scratch_d;
+  pg::DBuf<long long> xacc, xacc_b;  // K-sliced runs (cohorts above kSliceK samples)
 
   // last batch
   int64_t last_m = 0, last_ncand = 0;
@@ -266,9 +267,8 @@ int upload_panel_common(pg_ctx* c, const double* d_y, int64_t n_kept, int64_t n_
   c->n_kept = n_kept;
   c->n_pheno = n_pheno;
   c->p_pad = round_up(n_pheno, kTileP);
-  PG_REQUIRE(round_up(n_src, 64) <= kMaxExactK, PG_ERR_CONFIG,
-             "%lld genotype samples exceed the exact int32 tensor-core accumulation range (%lld); "
-             "split the cohort", (long long)n_src, (long long)kMaxExactK);
+  PG_REQUIRE(round_up(n_src, 64) <= (int64_t(1) << 30), PG_ERR_CONFIG, "%lld genotype samples: too many",
+             (long long)n_src);
   c->k_pad = round_up(n_src, 64);
   bits.assign(c->k_pad / 32 + 1, 0u);
   for (int64_t i = 0; i < n_kept; ++i) {
@@ -411,6 +411,11 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
     eb.cand_count = c->cand_count.p;
     eb.full_r = c->wbuf.p;
     eb.full_ld = kTileP;
+    if (c->k_pad > kSliceK) {  // more samples than one exact int32 slice
+      PG_CHECK_STATUS(c->xacc_b.ensure(static_cast<size_t>(c_pad / R) * kTileP * 2));
+      eb.x_accum = c->xacc_b.p;
+      eb.x_ld = kTileP;
+    }
     PG_CHECK_STATUS(run_gemm_on(eb, c->bq_h.p, c->bq_1.p, c->bq_0.p, kTileP));
     resid_kernel<<<static_cast<unsigned>((m + 255) / 256), 256, 0, s>>>(
         c->wbuf.p, kTileP, c->basis_cols, m, c->n_miss.p, c->s_u.p, c->ss_u.p, c->n_kept, geno_unit_scale(b),
@@ -442,6 +447,11 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
   ep.max_abs_r = c->max_abs_r.p;
   PG_CHECK_STATUS(c->cand_count.ensure(1));
   ep.cand_count = c->cand_count.p;
+  if (c->k_pad > kSliceK) {  // K-sliced contraction: exact int64 partials per (marker, phenotype)
+    PG_CHECK_STATUS(c->xacc.ensure(static_cast<size_t>(c_pad / R) * c->p_pad * 2));
+    ep.x_accum = c->xacc.p;
+    ep.x_ld = c->p_pad;
+  }
   int64_t ncand = 0;
   if (c->mode == PG_MODE_FULL) {
     PG_CHECK_STATUS(c->full_r.ensure(static_cast<size_t>(c_pad / R) * c->p_pad));
@@ -745,9 +755,8 @@ int pg_ctx_import_panel(pg_ctx* c, const void* d_src, int64_t n_kept, int64_t n_
   c->n_kept = n_kept;
   c->n_pheno = n_pheno;
   c->p_pad = round_up(n_pheno, kTileP);
-  PG_REQUIRE(round_up(n_samples_src, 64) <= kMaxExactK, PG_ERR_CONFIG,
-             "%lld genotype samples exceed the exact int32 tensor-core accumulation range (%lld); "
-             "split the cohort", (long long)n_samples_src, (long long)kMaxExactK);
+  PG_REQUIRE(round_up(n_samples_src, 64) <= (int64_t(1) << 30), PG_ERR_CONFIG, "%lld genotype samples: too many",
+             (long long)n_samples_src);
   c->k_pad = round_up(n_samples_src, 64);
   bits.assign(c->k_pad / 32 + 1, 0u);
   for (int64_t i = 0; i < n_kept; ++i) {

@@ -64,6 +64,7 @@ DEFAULT_FULL_BYTE_BUDGET = 16 * 1024**3
 # device batches are sized for the GEMM (>= this many markers) and bounded in memory
 _MIN_DEVICE_BATCH = 8192
 _PLINK_DEVICE_BATCH = 65536
+_SLICE_SAMPLES = 131072  # csrc/assoc.cuh kSliceK
 _MAX_GEMM_ROWS = 1 << 17
 _MAX_FULL_BYTES = 2 << 30
 
@@ -211,7 +212,7 @@ def topk_batch_bars(writer, top_k: int, batch_markers: int, t_floor: float, df: 
     return bars, need
 
 
-def device_batch_size(config: ScanConfig, n_markers: int, n_pheno: int) -> int:
+def device_batch_size(config: ScanConfig, n_markers: int, n_pheno: int, n_samples: int = 0) -> int:
     """Markers per device launch: at least the configured batch, sized for the GEMM, memory-bounded."""
     if config.device_batch is not None:
         return max(1, min(int(config.device_batch), n_markers))
@@ -222,6 +223,8 @@ def device_batch_size(config: ScanConfig, n_markers: int, n_pheno: int) -> int:
     b = min(b, _MAX_GEMM_ROWS if plink else _MAX_GEMM_ROWS // 16)
     if config.output_mode is OutputMode.FULL:
         b = min(b, max(256, _MAX_FULL_BYTES // (8 * max(n_pheno, 1))))
+    if n_samples > _SLICE_SAMPLES:  # K-sliced device runs hold 16 B of partials per test
+        b = min(b, max(256, _MAX_FULL_BYTES * 2 // (16 * max(n_pheno, 1))))
     return max(1, min(b, n_markers))
 
 
@@ -362,7 +365,7 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
         t_decode = t_prepare = t_corr = t_emit = 0.0
         qc_rows: list[str] = []
         lo, hi = marker_range if marker_range is not None else (0, source.n_markers)
-        step = device_batch_size(config, hi - lo, n_pheno)
+        step = device_batch_size(config, hi - lo, n_pheno, source.n_samples)
         plan = [(lo + s0, c0) for s0, c0 in plan_batches(hi - lo, step)]
         read_kw = {"dtype": dtype} if config.source.format.value == "dense" else {}
 

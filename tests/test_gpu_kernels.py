@@ -193,13 +193,45 @@ def test_device_panel_prep_rejects_non_finite():
 
 
 @pytest.mark.gpu
-def test_sample_count_beyond_exact_range_is_refused():
-    """K_pad > 132,608 would let the int32 accumulators overflow: refused loudly, never a
-    silently wrong statistic."""
+@pytest.mark.parametrize("case", ["plink", "plink_missing", "dense_real"])
+def test_k_sliced_contraction_matches_oracle(case):
+    """Cohorts above 131,072 samples (one int32-exact slice) run the contraction in K slices
+    summed in int64: statistics equal the oracle's float64 path (PLINK fused, PLINK with
+    missing calls, real-valued dosages through the wide-digit GEMM)."""
+    from paper_2604_21095_b200 import _native
     from paper_2604_21095_b200._device import DeviceContext
-    from paper_2604_21095_b200.errors import ConfigError
 
+    rng = np.random.default_rng(140)
+    n, m, p = 140_000, 64, 8
+    y = rng.standard_normal((n, p))
+    y -= y.mean(axis=0)
+    y /= np.sqrt((y * y).mean(axis=0))
+    y[:, 1] += 0.05 * rng.standard_normal(n)
+    af = rng.uniform(0.1, 0.9, (m, 1))
+    g = rng.binomial(2, af, size=(m, n)).astype(np.float64)
+    y[:, 2] += 0.02 * (g[7] - g[7].mean())  # a planted association
+    if case == "plink_missing":
+        g[rng.random(g.shape) < 0.02] = np.nan
     with DeviceContext(0) as ctx:
-        with pytest.raises(ConfigError, match="exact int32"):
-            ctx.set_panel(np.ones((3, 1)) * [[1.0], [-1.0], [0.5]], np.arange(3, dtype=np.int64), 140_000)
-        ctx.set_panel(np.array([[1.0], [-1.0], [0.5]]), np.arange(3, dtype=np.int64), 132_608)
+        ytil = y / np.sqrt((y * y).mean(axis=0))
+        ytil -= ytil.mean(axis=0)
+        ytil /= np.sqrt((ytil * ytil).mean(axis=0))
+        ctx.set_panel(ytil, np.arange(n, dtype=np.int64), n)
+        ctx.set_scan(float(n - 2), _native.PG_MODE_FULL, None)
+        if case == "dense_real":
+            d = np.clip(g + rng.normal(0, 0.2, g.shape), 0, 2)
+            res = ctx.scan(_native.PG_GENO_DENSE_F64, np.ascontiguousarray(d).view(np.uint8), 8 * n)
+        else:
+            d = g
+            bpm = (n + 3) // 4
+            codes = np.where(np.isnan(g), 1, np.array([3, 2, 0], np.uint8)[np.nan_to_num(g).astype(int)])
+            codes = np.pad(codes.astype(np.uint8), ((0, 0), (0, bpm * 4 - n))).reshape(m, bpm, 4)
+            packed = (codes[:, :, 0] | (codes[:, :, 1] << 2) | (codes[:, :, 2] << 4)
+                      | (codes[:, :, 3] << 6)).astype(np.uint8)
+            res = ctx.scan(_native.PG_GENO_BED, packed, bpm)
+    ref = orc.threshold_scan(d, ytil, float(n - 2), 1.0)
+    t_ref = np.zeros((m, p))
+    t_ref[ref["rows"], ref["cols"]] = ref["t"]
+    rel = np.abs(res.t_rows - t_ref) / np.maximum(1.0, np.abs(t_ref))
+    assert rel.max() <= 1e-4
+    assert abs(t_ref[7, 2]) > 4 and np.sign(res.t_rows[7, 2]) == np.sign(t_ref[7, 2])
