@@ -99,3 +99,36 @@ def test_odd_tile_counts_match_oracle(p):
     t_ok = t_dev[ok] if t_dev.shape[0] == m else t_dev  # FULL rows may list non-skipped markers only
     rel = np.abs(t_ok - t_ref[ok]) / np.maximum(1.0, np.abs(t_ref[ok]))
     assert rel.max() <= 1e-4
+
+
+def test_k_sliced_extension_mode_through_engine(tmp_path):
+    """N = 140,000 (> one int32-exact slice) through the engine with covariates and
+    --residualize-genotypes: the side GEMM K5 and the main contraction both run K-sliced;
+    t equals the oracle's FWL restatement (adjusted df)."""
+    import paper_2604_21095_b200 as pg
+    from conftest_helpers import write_tsv
+
+    rng = np.random.default_rng(1400)
+    n, m, p = 140_000, 24, 3
+    ids = [f"S{i + 1}" for i in range(n)]
+    g = rng.binomial(2, rng.uniform(0.1, 0.9, (m, 1)), size=(m, n)).astype(np.float64)
+    c = rng.standard_normal((n, 2))
+    y = c @ rng.standard_normal((2, p)) + rng.standard_normal((n, p))
+    y[:, 0] += 0.03 * g[5]
+    bed, bim, fam = pg.write_bed_trio(tmp_path / "g", g, ids)
+    pheno = write_tsv(tmp_path / "p.tsv", ids, [f"ph{j}" for j in range(p)], y)
+    covar = write_tsv(tmp_path / "c.tsv", ids, ["c1", "c2"], c)
+    spec = pg.SourceSpec(pg.GenotypeFormat.PLINK_BED, bed_path=bed, bim_path=bim, fam_path=fam)
+    pg.run_scan(pg.ScanConfig(source=spec, pheno_path=pheno, covar_path=covar, out_path=tmp_path / "o.tsv",
+                              p_threshold=1.0, precision=pg.Precision.F64, summary_to_stderr=False,
+                              residualize_genotypes=True, df_mode=pg.DfMode.ADJUSTED))
+    recs = pg.load_association_records(tmp_path / "o.tsv")
+    q = orc.covariate_basis(c)
+    ytil, _ = orc.standardized_panel(y, q)
+    mat, *_ = orc.prepare(g, q)
+    r, _ = orc.correlate(mat, ytil)
+    t_ref = orc.t_from_r(r, float(n - q.shape[1] - 1))
+    got = np.array([x.t for x in recs]).reshape(m, p)
+    rel = np.abs(got - t_ref) / np.maximum(1.0, np.abs(t_ref))
+    assert rel.max() <= 1e-4
+    assert abs(t_ref[5, 0]) > 5
