@@ -313,18 +313,33 @@ def run_scan(config: ScanConfig, marker_range: tuple[int, int] | None = None, pa
 def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, panel_hook=None) -> ScanSummary:
     from ._device import DeviceContext
 
-    prep = prepare_panel(config, source)
+    # CUDA context creation (~0.5 s) overlaps the host table parsing; every C-ABI entry
+    # selects the ctx's device itself, so the handle may be created on another thread
+    with ThreadPoolExecutor(max_workers=1) as init:
+        ctx_fut = init.submit(DeviceContext, config.device)
+        try:
+            phases = {"start": time.perf_counter() - wall0}
+            prep = prepare_panel(config, source)
+            phases["tables_panel_host"] = time.perf_counter() - wall0
+            if source.n_markers < 1:
+                raise PanelGwasError("genotype source has no markers")
+        except BaseException:
+            try:
+                ctx_fut.result().close()
+            except Exception:
+                pass
+            raise
+        ctx = ctx_fut.result()
+        phases["device_ready"] = time.perf_counter() - wall0
     n = prep.align.n_kept
     df = prep.df
-    if source.n_markers < 1:
-        raise PanelGwasError("genotype source has no markers")
     dtype = np.dtype(np.float32 if config.precision is Precision.F32_STORE_F64_ACC else np.float64)
-    ctx = DeviceContext(config.device)
     try:
         if panel_hook is not None:
             panel_hook(ctx, prep)
         else:
             stage_panel(ctx, prep, source.n_samples)
+        phases["panel_on_device"] = time.perf_counter() - wall0
     except BaseException:
         ctx.close()
         raise
@@ -515,9 +530,13 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
     finally:
         ctx.close()
 
+    phases["scan_loop_done"] = time.perf_counter() - wall0
     t0 = time.perf_counter()
     records = writer.finalize()
     t_emit += time.perf_counter() - t0
+    phases["finalized"] = time.perf_counter() - wall0
+    if os.environ.get("PANELGWAS_PROFILE") == "1":  # cumulative seconds since run_scan entry
+        print(json.dumps({"panelgwas_phases_s": phases}), file=sys.stderr)
 
     if config.min_p_sidecar:
         write_min_p(Path(str(config.out_path) + ".minp.tsv"), names, max_abs_r, max_abs_t, min_p)

@@ -88,7 +88,8 @@ def main():
            str(d / "pheno.tsv"), "--covar", str(d / "covar.tsv"), "--p-threshold", "1e-4", "--out",
            str(d / "hits.tsv")]
     t0 = time.perf_counter()
-    res = subprocess.run(cmd, capture_output=True, text=True, cwd=str(ROOT))
+    res = subprocess.run(cmd, capture_output=True, text=True, cwd=str(ROOT),
+                         env={**os.environ, "PANELGWAS_PROFILE": "1"})
     wall = time.perf_counter() - t0
     if res.returncode != 0:
         print(res.stdout[-2000:], res.stderr[-4000:])
@@ -98,7 +99,9 @@ def main():
     line = {"workload": f"C3 via CLI: N={n:,} M={a.markers:,} P={p:,} + {a.covariates} covariates, p<=1e-4",
             "wall_s": wall, "tests": tests, "tests_per_s_wall": tests / wall, "records": summary["records_emitted"],
             "file_bytes": sizes, "write_inputs_s": t_write,
-            "summary_times": {k: summary[k] for k in summary if k.startswith("time_") or k == "wall_s"}}
+            "summary_times": {k: summary[k] for k in summary if k.startswith("time_") or k == "wall_s"},
+            "phases": next((json.loads(ln)["panelgwas_phases_s"] for ln in res.stderr.splitlines()
+                            if ln.startswith('{"panelgwas_phases_s"')), None)}
     print(json.dumps(line), flush=True)
 
 
