@@ -487,14 +487,24 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
             emitter = ThreadPoolExecutor(max_workers=1) if config.output_mode is not OutputMode.TOPK else None
             emit_fut = None
 
+            waits = {"read": 0.0, "scan": 0.0, "emit": 0.0, "stage": 0.0}
+
             def dispatch(i, res):
                 nonlocal emit_fut
                 if emitter is None:
                     finish(i, res)
                     return
                 if emit_fut is not None:
+                    t0 = time.perf_counter()
                     emit_fut.result()  # one batch in the writer at a time; re-raises its errors
+                    waits["emit"] += time.perf_counter() - t0
                 emit_fut = emitter.submit(finish, i, res)
+
+            def scan(slot):
+                t0 = time.perf_counter()
+                res = ctx.scan_staged(slot, full_elem_bytes=dtype.itemsize)
+                waits["scan"] += time.perf_counter() - t0
+                return res
 
             set_topk_bars(0)
             try:
@@ -502,16 +512,20 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
                     fut = reader.submit(read, 0)
                     pending = None
                     for i in range(len(plan)):
+                        t0 = time.perf_counter()
                         block, dt_read = fut.result()
+                        waits["read"] += time.perf_counter() - t0
                         t_decode += dt_read
+                        t0 = time.perf_counter()
                         staged[i % 2] = stage(i, block)
+                        waits["stage"] += time.perf_counter() - t0
                         if i + 1 < len(plan):
                             fut = reader.submit(read, i + 1)
                         if pending is not None:
-                            dispatch(pending, ctx.scan_staged(pending % 2, full_elem_bytes=dtype.itemsize))
+                            dispatch(pending, scan(pending % 2))
                         staged_ready(i)
                         pending = i
-                    dispatch(pending, ctx.scan_staged(pending % 2, full_elem_bytes=dtype.itemsize))
+                    dispatch(pending, scan(pending % 2))
                 if emit_fut is not None:
                     emit_fut.result()
             finally:
@@ -531,6 +545,7 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
         ctx.close()
 
     phases["scan_loop_done"] = time.perf_counter() - wall0
+    phases["loop_main_thread_waits"] = waits
     t0 = time.perf_counter()
     records = writer.finalize()
     t_emit += time.perf_counter() - t0

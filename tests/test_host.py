@@ -353,3 +353,25 @@ class TestSimulate:
             pack_bed_codes(np.array([[0.5]]))
         with pytest.raises(ConfigError):
             pg.SimSpec(seed=1, n_samples=0, n_markers=1, n_phenotypes=1)
+
+
+def test_bim_fast_path_equals_line_reader(tmp_path):
+    from paper_2604_21095_b200.genotypes import plink
+
+    lines = [f"{1 + i % 22}\trs{i}\t0.{i}\t{100 * i + 7}\t{'ACGT'[i % 4]}\t{'TGCA'[i % 4]}" for i in range(500)]
+    lines.insert(10, "")  # blank lines are skipped by both
+    lines[20] = "  " + lines[20].replace("\t", "   ") + "  "  # any whitespace between fields
+    p = tmp_path / "a.bim"
+    p.write_text("\n".join(lines) + "\n")
+    fast = plink._parse_bim_fast(p)
+    assert fast is not None and fast == plink._parse_bim_lines(p)
+    assert [r.source_index for r in fast] == list(range(500))
+    bad = tmp_path / "b.bim"
+    bad.write_text("1 rs1 0 5 A G\n1 rs2 0 6 A\n")
+    assert plink._parse_bim_fast(bad) is None
+    with pytest.raises(FormatError, match="expected 6 columns"):
+        plink._parse_bim(bad)
+    neg = tmp_path / "c.bim"
+    neg.write_text("1 rs1 0 -5 A G\n")
+    with pytest.raises(FormatError, match="negative position"):
+        plink._parse_bim(neg)
