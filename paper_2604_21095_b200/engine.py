@@ -507,6 +507,10 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
                 return res
 
             set_topk_bars(0)
+            # the writer thread formats in Python while this thread mostly waits in ctypes
+            # calls: hand the GIL back quickly so each scan is issued as soon as it can be
+            switch_interval = sys.getswitchinterval()
+            sys.setswitchinterval(2e-4)
             try:
                 with ThreadPoolExecutor(max_workers=1) as reader:
                     fut = reader.submit(read, 0)
@@ -529,6 +533,7 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
                 if emit_fut is not None:
                     emit_fut.result()
             finally:
+                sys.setswitchinterval(switch_interval)
                 if emitter is not None:
                     emitter.shutdown(wait=True)
             if config.min_p_sidecar:
