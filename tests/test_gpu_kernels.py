@@ -235,3 +235,31 @@ def test_k_sliced_contraction_matches_oracle(case):
     rel = np.abs(res.t_rows - t_ref) / np.maximum(1.0, np.abs(t_ref))
     assert rel.max() <= 1e-4
     assert abs(t_ref[7, 2]) > 4 and np.sign(res.t_rows[7, 2]) == np.sign(t_ref[7, 2])
+
+
+@pytest.mark.gpu
+def test_c_abi_misuse_fails_loudly():
+    """State and argument errors come back as the mapped exceptions, never a crash or a
+    silently empty result."""
+    from paper_2604_21095_b200 import _native
+    from paper_2604_21095_b200._device import DeviceContext
+    from paper_2604_21095_b200.errors import FormatError, PanelGwasError
+
+    rows = np.zeros((4, 3), np.uint8)
+    with DeviceContext(0) as ctx:
+        with pytest.raises(PanelGwasError, match="no panel"):
+            ctx.scan(_native.PG_GENO_BED, rows, 3)
+        ctx.set_panel(np.random.default_rng(0).standard_normal((10, 2)), np.arange(10, dtype=np.int64), 10)
+        ctx.set_scan(8.0, _native.PG_MODE_THRESHOLD, np.full(2, 0.5))
+        with pytest.raises(FormatError, match="expected 3"):
+            ctx.scan(_native.PG_GENO_BED, np.zeros((4, 5), np.uint8), 5)
+        with pytest.raises(ValueError, match="slot"):
+            ctx.stage(2, _native.PG_GENO_BED, rows, 3)
+        with pytest.raises(PanelGwasError, match="no batch in flight"):
+            ctx.stage_bgen_end(0)
+        with pytest.raises(PanelGwasError, match="holds no staged batch"):
+            ctx.scan_staged(1)
+        with pytest.raises(ValueError, match="r_bar required"):
+            ctx.set_scan(8.0, _native.PG_MODE_THRESHOLD, None)
+        res = ctx.scan(_native.PG_GENO_BED, rows, 3)  # still usable after the errors
+        assert res.n_markers == 4
