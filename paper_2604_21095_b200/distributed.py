@@ -178,8 +178,16 @@ def run_scan_distributed(config):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world == 1:
         return engine.run_scan(config)
+    # test hooks: PANELGWAS_DIST_BACKEND=gloo + PANELGWAS_DIST_DEVICE=0 run several ranks on
+    # one GPU (host collectives only; no kernel of one rank waits on another)
+    backend = os.environ.get("PANELGWAS_DIST_BACKEND", "nccl")
+    if os.environ.get("PANELGWAS_DIST_DEVICE"):
+        local = int(os.environ["PANELGWAS_DIST_DEVICE"])
     if not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     torch.cuda.set_device(local)
     src = open_genotype_source(config.source)
     try:
@@ -216,10 +224,28 @@ def run_scan_distributed(config):
     src = open_genotype_source(config.source)
     n_src = src.n_samples
     src.close()
+    def prep_hook(source):
+        # rank 0 parses the phenotype / covariate tables and sends the small metadata; the
+        # other ranks never read the (multi-GB) tables
+        err = prep = meta = None
+        if rank == 0:
+            try:
+                prep = engine.prepare_panel(config, source)
+                meta = engine.panel_metadata(prep)
+            except Exception as exc:
+                err = exc
+        box = [(meta, None if err is None else f"{type(err).__name__}: {err}") if rank == 0 else None]
+        dist.broadcast_object_list(box, 0)
+        if err is not None:
+            raise err
+        if box[0][1] is not None:
+            raise PanelGwasError(f"rank 0 panel preparation failed: {box[0][1]}")
+        return prep if rank == 0 else engine.panel_from_metadata(box[0][0])
+
     # every rank joins the panel broadcast; a rank with an empty shard scans a dummy
     # one-marker range and discards it
     rng = (start, stop) if stop > start else (0, 1)
-    summary = engine.run_scan(shard_cfg, marker_range=rng, panel_hook=panel_hook)
+    summary = engine.run_scan(shard_cfg, marker_range=rng, panel_hook=panel_hook, prep_hook=prep_hook)
     if stop <= start:
         summary = None
     gathered = [None] * world

@@ -274,6 +274,21 @@ def prepare_panel(config: ScanConfig, source) -> _PreparedPanel:
     return _PreparedPanel(basis, panel, align, df)
 
 
+def panel_metadata(prep: _PreparedPanel) -> dict:
+    """Everything a scan needs about the prepared panel except its values (small, picklable):
+    what rank 0 sends the other ranks instead of having each parse the phenotype tables."""
+    return {"basis": prep.basis, "names": prep.panel.phenotype_names, "missing": prep.panel.missing_count,
+            "shape": prep.panel.y.shape, "align": prep.align, "df": prep.df}
+
+
+def panel_from_metadata(meta: dict) -> _PreparedPanel:
+    """A _PreparedPanel for a rank that receives the quantized panel over NCCL: no values
+    (the placeholder matrix is never touched, so no host memory is committed)."""
+    y = np.empty(meta["shape"], dtype=np.float64)
+    panel = phenotypes.PhenotypePanel(y, list(meta["names"]), meta["missing"], PanelState.STANDARDIZED)
+    return _PreparedPanel(meta["basis"], panel, meta["align"], meta["df"])
+
+
 def stage_panel(ctx, prep: _PreparedPanel, n_samples_src: int, commit: bool = True) -> None:
     """Device panel preparation (pg_ctx_prepare_panel) + quantization of the kept columns."""
     flat, _sd = ctx.prepare_panel(prep.panel.y, prep.basis.q)
@@ -294,23 +309,26 @@ def write_min_p(path: Path, names, max_abs_r, max_abs_t, min_p) -> None:
             fh.write(f"{name}\t{float(max_abs_r[j])!r}\t{float(max_abs_t[j])!r}\t{float(min_p[j])!r}\n")
 
 
-def run_scan(config: ScanConfig, marker_range: tuple[int, int] | None = None, panel_hook=None) -> ScanSummary:
+def run_scan(config: ScanConfig, marker_range: tuple[int, int] | None = None, panel_hook=None,
+             prep_hook=None) -> ScanSummary:
     """Execute a full scan on the GPU and write results plus the summary files.
 
-    marker_range / panel_hook are used by the multi-GPU driver (distributed.py): scan only
-    markers [start, stop) of the source, and obtain the resident panel through
-    `panel_hook(ctx, prep)` (NCCL broadcast from rank 0) instead of uploading it.
+    marker_range / panel_hook / prep_hook are used by the multi-GPU driver (distributed.py):
+    scan only markers [start, stop) of the source, obtain the resident panel through
+    `panel_hook(ctx, prep)` (NCCL broadcast from rank 0) instead of uploading it, and the host
+    panel metadata through `prep_hook(source)` (rank 0 parses the tables for everyone).
     """
     wall0 = time.perf_counter()
     config.validate()
     source = open_genotype_source(config.source)
     try:
-        return _run_scan_open(config, source, wall0, marker_range, panel_hook)
+        return _run_scan_open(config, source, wall0, marker_range, panel_hook, prep_hook)
     finally:
         source.close()
 
 
-def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, panel_hook=None) -> ScanSummary:
+def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, panel_hook=None,
+                   prep_hook=None) -> ScanSummary:
     from ._device import DeviceContext
 
     # CUDA context creation (~0.5 s) overlaps the host table parsing; every C-ABI entry
@@ -319,7 +337,7 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
         ctx_fut = init.submit(DeviceContext, config.device)
         try:
             phases = {"start": time.perf_counter() - wall0}
-            prep = prepare_panel(config, source)
+            prep = prep_hook(source) if prep_hook is not None else prepare_panel(config, source)
             phases["tables_panel_host"] = time.perf_counter() - wall0
             if source.n_markers < 1:
                 raise PanelGwasError("genotype source has no markers")

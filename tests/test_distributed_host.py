@@ -134,3 +134,36 @@ def test_merge_min_p_takes_best_shard(tmp_path):
     rows = [ln.split("\t") for ln in (tmp_path / "m").read_text().splitlines()[1:]]
     assert [r[0] for r in rows] == names
     assert [float(r[3]) for r in rows] == [0.003, 1e-6, 0.04]
+
+
+def test_panel_metadata_round_trip(tmp_path):
+    """What rank 0 broadcasts instead of every rank parsing the tables: a pickled metadata
+    dict that rebuilds a values-free _PreparedPanel with the same names, alignment, basis, df."""
+    import pickle
+
+    from conftest_helpers import write_tsv
+    from paper_2604_21095_b200 import engine
+
+    rng = np.random.default_rng(8)
+    n = 40
+    ids = [f"S{i + 1}" for i in range(n)]
+    d = rng.integers(0, 3, (6, n)).astype(np.float64)
+    bed, bim, fam = pg.write_bed_trio(tmp_path / "g", d, ids)
+    y = rng.standard_normal((n, 3))
+    y[3, 1] = np.nan
+    pheno = write_tsv(tmp_path / "p.tsv", ids, ["a", "b", "c"], y)
+    covar = write_tsv(tmp_path / "c.tsv", ids, ["x"], rng.standard_normal((n, 1)))
+    (tmp_path / "keep.txt").write_text("\n".join(ids[:35]) + "\n")
+    spec = pg.SourceSpec(pg.GenotypeFormat.PLINK_BED, bed_path=bed, bim_path=bim, fam_path=fam)
+    cfg = pg.ScanConfig(source=spec, pheno_path=pheno, covar_path=covar, out_path=tmp_path / "o.tsv",
+                        keep_path=tmp_path / "keep.txt", df_mode=pg.DfMode.ADJUSTED)
+    with pg.open_genotype_source(spec) as src:
+        prep = engine.prepare_panel(cfg, src)
+    got = engine.panel_from_metadata(pickle.loads(pickle.dumps(engine.panel_metadata(prep))))
+    assert got.df == prep.df == 35 - 2 - 1
+    assert got.panel.phenotype_names == prep.panel.phenotype_names
+    assert got.panel.n_phenotypes == 3 and got.panel.n_samples == 35
+    assert np.array_equal(got.panel.missing_count, prep.panel.missing_count)
+    assert np.array_equal(got.align.genotype_row_index, prep.align.genotype_row_index)
+    assert got.align.exclusion_log == prep.align.exclusion_log
+    assert np.array_equal(got.basis.q, prep.basis.q) and got.basis.rank == prep.basis.rank
