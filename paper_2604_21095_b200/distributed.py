@@ -56,12 +56,18 @@ def broadcast_panel(ctx, torch, dist, rank: int, n_kept: int, n_pheno: int, gidx
     """Rank 0's resident quantized panel -> every rank's ctx. Returns bytes moved."""
     buf = None
     nbytes = None
+    # NCCL moves the device buffer directly; other backends (gloo in the tests) go via host
+    wire = device if dist.get_backend() == "nccl" else "cpu"
     if rank == 0:
         nbytes = ctx.panel_bytes()
         buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
         ctx.export_panel(buf.data_ptr())
-    buf = broadcast_bytes(torch, dist, buf, nbytes, 0, device)
+        if wire == "cpu":
+            buf = buf.cpu()
+    buf = broadcast_bytes(torch, dist, buf, nbytes, 0, wire)
     if rank != 0:
+        if wire == "cpu":
+            buf = buf.to(device)
         ctx.import_panel(buf.data_ptr(), n_kept, n_pheno, gidx, n_src)
     return int(buf.numel())
 
