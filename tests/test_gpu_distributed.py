@@ -53,7 +53,9 @@ def test_two_rank_driver_equals_single_process(tmp_path, mode):
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), "-m", "paper_2604_21095_b200.distributed",
            *args, "--out", str(multi)]
     res = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
-    assert res.returncode == 0, res.stderr[-3000:]
+    if res.returncode != 0:
+        rank1 = "\n".join(ln for ln in res.stderr.splitlines() if "[rank1]" in ln)
+        raise AssertionError((rank1 or res.stderr)[-6000:])
     assert multi.read_bytes() == single.read_bytes()
     assert Path(f"{multi}.minp.tsv").read_bytes() == Path(f"{single}.minp.tsv").read_bytes()
     if "--full" in mode:
