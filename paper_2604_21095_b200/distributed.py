@@ -189,6 +189,7 @@ def run_scan_distributed(config):
     backend = os.environ.get("PANELGWAS_DIST_BACKEND", "nccl")
     if os.environ.get("PANELGWAS_DIST_DEVICE"):
         local = int(os.environ["PANELGWAS_DIST_DEVICE"])
+        os.environ["PANELGWAS_DEVICE"] = str(local)  # the module-level helper context too
     if not dist.is_initialized():
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
