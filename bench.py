@@ -231,8 +231,16 @@ def our_arm(a) -> None:
     from paper_2604_21095_b200.kernel import build_covariate_basis
 
     world, rank, local = dist_env()
+    # test hooks (as distributed.py): several ranks on one GPU over gloo for a functional check
+    backend = os.environ.get("PANELGWAS_DIST_BACKEND", "nccl")
+    if os.environ.get("PANELGWAS_DIST_DEVICE"):
+        local = int(os.environ["PANELGWAS_DIST_DEVICE"])
+        os.environ["PANELGWAS_DEVICE"] = str(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     _build.build()  # no-op when the in-tree .so is current
@@ -259,14 +267,18 @@ def our_arm(a) -> None:
             else:
                 ctx.set_panel_device(ytil.data_ptr(), n, p, p, gidx, n)
         if world > 1:
+            wire = dev if backend == "nccl" else torch.device("cpu")  # NCCL: device to device
             nbytes = ctx.panel_bytes() if rank == 0 else 0
-            nb = torch.tensor([nbytes], device=dev, dtype=torch.int64)
+            nb = torch.tensor([nbytes], device=wire, dtype=torch.int64)
             dist.broadcast(nb, 0)
             buf = torch.empty(int(nb.item()), dtype=torch.uint8, device=dev)
             if rank == 0:
                 ctx.export_panel(buf.data_ptr())
-            dist.broadcast(buf, 0)
+            wbuf = buf if wire == dev else buf.cpu()
+            dist.broadcast(wbuf, 0)
             if rank != 0:
+                if wbuf is not buf:
+                    buf.copy_(wbuf)
                 ctx.import_panel(buf.data_ptr(), n, p, gidx, n)
             return int(nb.item())
         return 0
@@ -302,7 +314,7 @@ def our_arm(a) -> None:
         torch.cuda.synchronize()
         ms = ev0.elapsed_time(ev1)
         if world > 1:
-            t = torch.tensor([ms], device=dev)
+            t = torch.tensor([ms], device=dev if backend == "nccl" else "cpu")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
             dist.barrier()

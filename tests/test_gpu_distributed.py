@@ -62,3 +62,21 @@ def test_two_rank_driver_equals_single_process(tmp_path, mode):
         for suffix in (".markers.tsv", ".phenotypes.txt"):
             assert Path(f"{multi}{suffix}").read_bytes() == Path(f"{single}{suffix}").read_bytes()
     assert not list(tmp_path.glob("multi.out.rank*"))  # shard files cleaned up
+
+
+def test_bench_two_ranks_functional():
+    """bench.py under torchrun with 2 ranks (functional check of the multi-GPU bench path on
+    one GPU over gloo: panel broadcast, max-over-ranks timing, one JSON line from rank 0)."""
+    import json
+
+    env = {**os.environ, "PANELGWAS_DIST_BACKEND": "gloo", "PANELGWAS_DIST_DEVICE": "0"}
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "2",
+           "--markers", "8192", "--phenotypes", "512", "--samples", "2000", "--steps", "3", "--warmup", "3",
+           "--device-batch", "4096"]
+    res = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-4000:]
+    lines = [ln for ln in res.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0 and d["cpu_baseline"] is None
