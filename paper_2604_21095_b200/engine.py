@@ -188,7 +188,7 @@ def topk_premask(worst_abs_t: np.ndarray, t_floor: float, df: float) -> np.ndarr
     return np.where(bar_t <= 0.0, -1.0, bar_r * (1.0 - 1e-12))
 
 
-_TOPK_NULL_FACTOR = 16.0  # expected null candidates per missing top-k slot in a batch
+_TOPK_NULL_FACTOR = 16.0  # (/4 = floor of) expected null candidates per missing top-k slot
 topk_rescans = 0  # batches rescanned because a null-quantile bar admitted too few (diagnostics)
 
 
@@ -199,15 +199,19 @@ def topk_batch_bars(writer, top_k: int, batch_markers: int, t_floor: float, df: 
     reference's rule, engine.py:205-211). A phenotype still short of k records would admit
     every marker (the reference's per-4,096-marker batches can afford that; a 65,536-marker
     device batch x 20,480 phenotypes cannot), so its bar is the null quantile at
-    p = 16 * missing / batch: all markers beating the batch's k-th best are then above the
-    bar whenever at least `missing` candidates pass, which the caller checks (and rescans
-    the batch without a bar for any phenotype that falls short)."""
+    p = max(4, 32 / k) * missing / batch: all markers beating the batch's k-th best are then
+    above the bar whenever at least `missing` candidates pass, which the caller checks (and
+    rescans the batch without a bar for any phenotype that falls short)."""
     bars = topk_premask(writer.worst_abs_t, t_floor, df)
     kept = writer.kept_counts()
     short = kept < top_k
     need = np.where(short, top_k - kept, 0)
+    # expected null candidates per phenotype: factor x missing slots (>= 32), so falling short
+    # needs a Poisson(>= 32) draw below `missing` (rescans stay rare) while the first batch
+    # of a C3-sized scan admits ~k x max(4, ...) candidates per phenotype, not 65,536
+    factor = max(_TOPK_NULL_FACTOR / 4.0, 32.0 / max(top_k, 1))
     for miss in np.unique(need[short]).tolist():
-        p_q = min(1.0, _TOPK_NULL_FACTOR * miss / max(batch_markers, 1))
+        p_q = min(1.0, factor * miss / max(batch_markers, 1))
         bars[need == miss] = threshold_premask(p_q, df) if p_q < 1.0 else -1.0
     return bars, need
 
