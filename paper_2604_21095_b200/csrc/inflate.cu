@@ -13,7 +13,7 @@
 // output are mirrored in a per-warp shared-memory ring that serves match sources (typical
 // BGEN distances are short); only farther matches read back from global memory.
 //
-// Per-warp shared memory: first-level tables (2^10 literal/length, 2^8 distance,
+// Per-warp shared memory: first-level tables (2^10 literal/length, 2^7 distance,
 // 2^7 code-length entries), canonical (count, symbol) arrays for longer codes, and the
 // ring. The zlib header and the Adler-32 trailer are checked like zlib does. Malformed
 // streams are reported per stream (status != 0); the caller re-inflates that one block
@@ -26,7 +26,7 @@ namespace pg {
 namespace {
 
 constexpr int kLitBits = 10;
-constexpr int kDistBits = 8;
+constexpr int kDistBits = 7;
 constexpr int kClenBits = 7;
 constexpr int kWarpsPerBlock = 4;
 constexpr int kRing = 2048;             // bytes of recent output mirrored in smem
@@ -40,18 +40,47 @@ __constant__ uint16_t c_dist_base[30] = {1,   2,   3,   4,   5,   7,    9,    13
 __constant__ uint8_t c_dist_extra[30] = {0, 0, 0, 0, 1, 1, 2, 2, 3, 3, 4, 4, 5, 5, 6, 6, 7, 7, 8, 8, 9, 9, 10, 10, 11, 11, 12, 12, 13, 13};
 __constant__ uint8_t c_clen_order[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
 
-// One canonical Huffman code (RFC 1951 §3.2.2): first-level table entries
-// (length << 9) | symbol (0 = longer than the table, or no such code) + canonical arrays.
-template <int BITS, int NSYM>
+// One canonical Huffman code (RFC 1951 §3.2.2): a first-level table of pre-decoded entries
+// (0 = code longer than the table, or no such code) + canonical (count, symbol) arrays.
+// Entry layouts (Enc):
+//   code-length codes  : u16  len | sym << 4
+//   literal / length   : u16  len | extra << 4 | value << 7 | is_length << 15  (literal byte;
+//                        or length base - 3 with `extra` bits; extra 7 = end of block,
+//                        extra 6 = invalid symbol 286 / 287)
+//   distance           : u32  len | extra << 4 | invalid << 8 | base << 16
+// so the hot loop reads a length / distance with no constant-table lookups, and the
+// literal table keeps 16-bit entries (occupancy is what this kernel is bound by).
+template <int BITS, int NSYM, class T = uint16_t>
 struct Table {
-  uint16_t lut[1 << BITS];
+  T lut[1 << BITS];
   uint16_t count[16];
   uint16_t sym[NSYM];
 };
 
+struct EncClen {
+  __device__ static uint32_t enc(int s, int l) { return static_cast<uint32_t>(l) | (static_cast<uint32_t>(s) << 4); }
+};
+struct EncLit {
+  static constexpr uint32_t kLength = 1u << 15;
+  __device__ static uint32_t enc(int s, int l) {
+    if (s < 256) return static_cast<uint32_t>(l) | (static_cast<uint32_t>(s) << 7);
+    if (s == 256) return static_cast<uint32_t>(l) | (7u << 4) | kLength;
+    if (s > 285) return static_cast<uint32_t>(l) | (6u << 4) | kLength;
+    return static_cast<uint32_t>(l) | (static_cast<uint32_t>(c_len_extra[s - 257]) << 4) |
+           (static_cast<uint32_t>(c_len_base[s - 257] - 3) << 7) | kLength;
+  }
+};
+struct EncDist {
+  __device__ static uint32_t enc(int s, int l) {
+    if (s >= 30) return static_cast<uint32_t>(l) | (1u << 8);
+    return static_cast<uint32_t>(l) | (static_cast<uint32_t>(c_dist_extra[s]) << 4) |
+           (static_cast<uint32_t>(c_dist_base[s]) << 16);
+  }
+};
+
 struct WarpSmem {
   Table<kLitBits, 288> lit;
-  Table<kDistBits, 32> dist;
+  Table<kDistBits, 32, uint32_t> dist;
   Table<kClenBits, 19> clen;
   uint16_t codes[288];
   uint8_t lens[288 + 32];
@@ -87,8 +116,8 @@ struct Bits {
 
 // zlib's completeness rules (inflate_table): over-subscribed -> error; an incomplete code
 // only for a single code of length 1 (lit/len, dist); never for code-length codes.
-template <int BITS, int NSYM>
-__device__ bool build(Table<BITS, NSYM>& t, const uint8_t* lens, int n, uint16_t* codes, bool code_lengths,
+template <class Enc, int BITS, int NSYM, class T>
+__device__ bool build(Table<BITS, NSYM, T>& t, const uint8_t* lens, int n, uint16_t* codes, bool code_lengths,
                       int lane) {
   uint16_t count[16];
 #pragma unroll
@@ -128,22 +157,17 @@ __device__ bool build(Table<BITS, NSYM>& t, const uint8_t* lens, int n, uint16_t
     if (l == 0 || l > BITS) continue;
     // codes are read LSB first: index the table by the bit-reversed code
     const uint32_t rev = __brev(static_cast<uint32_t>(codes[s])) >> (32 - l);
-    const uint16_t e = static_cast<uint16_t>((l << 9) | s);
+    const T e = static_cast<T>(Enc::enc(s, l));
     for (uint32_t i = rev; i < (1u << BITS); i += 1u << l) t.lut[i] = e;
   }
   __syncwarp();
   return true;
 }
 
-// One symbol (the caller refilled: >= 33 buffered bits); -1 = no valid code.
-template <int BITS, int NSYM>
-__device__ __forceinline__ int decode(Bits& br, const Table<BITS, NSYM>& t) {
+// Canonical decode bit by bit (codes longer than the table, or invalid); -1 = no such code.
+template <int BITS, int NSYM, class T>
+__device__ __noinline__ int decode_slow(Bits& br, const Table<BITS, NSYM, T>& t) {
   const uint32_t bits = static_cast<uint32_t>(br.buf);
-  const uint16_t e = t.lut[bits & ((1u << BITS) - 1u)];
-  if (e) {
-    br.get(e >> 9);
-    return e & 511;
-  }
   int code = 0, first = 0, index = 0;
   for (int l = 1; l < 16; ++l) {
     code |= static_cast<int>((bits >> (l - 1)) & 1u);
@@ -157,6 +181,18 @@ __device__ __forceinline__ int decode(Bits& br, const Table<BITS, NSYM>& t) {
     code <<= 1;
   }
   return -1;
+}
+
+// One pre-decoded entry (the caller refilled: >= 33 buffered bits); 0 = no valid code.
+template <class Enc, int BITS, int NSYM, class T>
+__device__ __forceinline__ uint32_t decode(Bits& br, const Table<BITS, NSYM, T>& t) {
+  const uint32_t e = t.lut[static_cast<uint32_t>(br.buf) & ((1u << BITS) - 1u)];
+  if (e & 15u) {
+    br.get(e & 15u);
+    return e;
+  }
+  const int s = decode_slow(br, t);
+  return s < 0 ? 0u : Enc::enc(s, 1);  // bits already consumed; only the fields matter
 }
 
 __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint8_t* __restrict__ blob,
@@ -242,8 +278,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
     if (type == 1) {
       for (int s = lane; s < 320; s += 32) sm.lens[s] = s < 144 ? 8 : s < 256 ? 9 : s < 280 ? 7 : s < 288 ? 8 : 5;
       __syncwarp();
-      build(sm.lit, sm.lens, 288, sm.codes, false, lane);
-      build(sm.dist, sm.lens + 288, 32, sm.codes, false, lane);  // 30, 31 complete the code, never valid
+      build<EncLit>(sm.lit, sm.lens, 288, sm.codes, false, lane);
+      build<EncDist>(sm.dist, sm.lens + 288, 32, sm.codes, false, lane);  // 30, 31 complete the code, never valid
     } else {
       const int hlit = br.get(5) + 257, hdist = br.get(5) + 1, hclen = br.get(4) + 4;
       if (hlit > 286 || hdist > 30) {
@@ -260,7 +296,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
       }
       if (lane < 19) sm.lens[lane] = cl[lane];
       __syncwarp();
-      if (!build(sm.clen, sm.lens, 19, sm.codes, true, lane)) {
+      if (!build<EncClen>(sm.clen, sm.lens, 19, sm.codes, true, lane)) {
         err = 1;
         break;
       }
@@ -270,11 +306,12 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
       uint8_t prev = 0;
       while (idx < total) {
         br.refill();
-        const int sym = decode(br, sm.clen);
-        if (sym < 0) {
+        const uint32_t ce = decode<EncClen>(br, sm.clen);
+        if (!ce) {
           err = 1;
           break;
         }
+        const int sym = static_cast<int>(ce >> 4);
         if (sym < 16) {
           if (lane == 0) sm.lens[idx] = static_cast<uint8_t>(sym);
           prev = static_cast<uint8_t>(sym);
@@ -308,7 +345,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
         break;
       }
       __syncwarp();
-      if (sm.lens[256] == 0 || !build(sm.lit, sm.lens, hlit, sm.codes, false, lane)) {
+      if (sm.lens[256] == 0 || !build<EncLit>(sm.lit, sm.lens, hlit, sm.codes, false, lane)) {
         err = 1;
         break;
       }
@@ -316,7 +353,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
       __syncwarp();
       if (lane < hdist) sm.lens[288 + lane] = dl;
       __syncwarp();
-      if (!build(sm.dist, sm.lens + 288, hdist, sm.codes, false, lane)) {
+      if (!build<EncDist>(sm.dist, sm.lens + 288, hdist, sm.codes, false, lane)) {
         err = 1;
         break;
       }
@@ -324,9 +361,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
     // ---- compressed data
     for (;;) {
       br.refill();
-      const int sym = decode(br, sm.lit);
-      if (sym < 256) {
-        if (sym < 0) {
+      const uint32_t e = decode<EncLit>(br, sm.lit);
+      if (!(e & EncLit::kLength)) {
+        if (!e) {
           err = 1;
           break;
         }
@@ -335,29 +372,26 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
           break;
         }
         if (lane == 0) {
-          dst[pos] = static_cast<uint8_t>(sym);
-          sm.ring[pos & (kRing - 1)] = static_cast<uint8_t>(sym);
+          const uint8_t b = static_cast<uint8_t>(e >> 7);
+          dst[pos] = b;
+          sm.ring[pos & (kRing - 1)] = b;
         }
         ++pos;
         continue;
       }
-      if (sym == 256) {
-        if (!br.ok()) err = 1;
+      const uint32_t extra = (e >> 4) & 7u;
+      if (extra >= 6) {  // 7: end of block, 6: invalid length symbol
+        if (extra == 6 || !br.ok()) err = 1;
         break;
       }
-      const int li = sym - 257;
-      if (li >= 29) {
-        err = 1;
-        break;
-      }
-      const int length = c_len_base[li] + static_cast<int>(br.get(c_len_extra[li]));
+      const int length = 3 + static_cast<int>((e >> 7) & 255u) + static_cast<int>(br.get(extra));
       br.refill();
-      const int ds = decode(br, sm.dist);
-      if (ds < 0 || ds >= 30) {
+      const uint32_t de = decode<EncDist>(br, sm.dist);
+      if (!de || (de & 0x100u)) {
         err = 1;
         break;
       }
-      const int distance = c_dist_base[ds] + static_cast<int>(br.get(c_dist_extra[ds]));
+      const int distance = static_cast<int>(de >> 16) + static_cast<int>(br.get((de >> 4) & 15u));
       // (reading past the stream end only consumes padding / the next stream's bytes; the
       // end-of-block check below reports truncation)
       if (distance > pos) {
