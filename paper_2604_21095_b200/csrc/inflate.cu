@@ -13,7 +13,7 @@
 // output are mirrored in a per-warp shared-memory ring that serves match sources (typical
 // BGEN distances are short); only farther matches read back from global memory.
 //
-// Per-warp shared memory: first-level tables (2^10 literal/length, 2^7 distance,
+// Per-warp shared memory: first-level tables (2^10 literal/length, 2^8 distance,
 // 2^7 code-length entries), canonical (count, symbol) arrays for longer codes, and the
 // ring. The zlib header and the Adler-32 trailer are checked like zlib does. Malformed
 // streams are reported per stream (status != 0); the caller re-inflates that one block
@@ -26,7 +26,7 @@ namespace pg {
 namespace {
 
 constexpr int kLitBits = 10;
-constexpr int kDistBits = 7;
+constexpr int kDistBits = 8;
 constexpr int kClenBits = 7;
 constexpr int kWarpsPerBlock = 4;
 constexpr int kRing = 2048;             // bytes of recent output mirrored in smem
@@ -47,7 +47,7 @@ __constant__ uint8_t c_clen_order[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4
 //   literal / length   : u16  len | extra << 4 | value << 7 | is_length << 15  (literal byte;
 //                        or length base - 3 with `extra` bits; extra 7 = end of block,
 //                        extra 6 = invalid symbol 286 / 287)
-//   distance           : u32  len | extra << 4 | invalid << 8 | base << 16
+//   distance           : u16  len | extra << 4 | symbol << 8 (base from c_dist_base; >= 30 invalid)
 // so the hot loop reads a length / distance with no constant-table lookups, and the
 // literal table keeps 16-bit entries (occupancy is what this kernel is bound by).
 template <int BITS, int NSYM, class T = uint16_t>
@@ -72,15 +72,14 @@ struct EncLit {
 };
 struct EncDist {
   __device__ static uint32_t enc(int s, int l) {
-    if (s >= 30) return static_cast<uint32_t>(l) | (1u << 8);
-    return static_cast<uint32_t>(l) | (static_cast<uint32_t>(c_dist_extra[s]) << 4) |
-           (static_cast<uint32_t>(c_dist_base[s]) << 16);
+    const uint32_t extra = s < 30 ? c_dist_extra[s] : 0u;
+    return static_cast<uint32_t>(l) | (extra << 4) | (static_cast<uint32_t>(s) << 8);
   }
 };
 
 struct WarpSmem {
   Table<kLitBits, 288> lit;
-  Table<kDistBits, 32, uint32_t> dist;
+  Table<kDistBits, 32> dist;
   Table<kClenBits, 19> clen;
   uint16_t codes[288];
   uint8_t lens[288 + 32];
@@ -166,7 +165,7 @@ __device__ bool build(Table<BITS, NSYM, T>& t, const uint8_t* lens, int n, uint1
 
 // Canonical decode bit by bit (codes longer than the table, or invalid); -1 = no such code.
 template <int BITS, int NSYM, class T>
-__device__ __noinline__ int decode_slow(Bits& br, const Table<BITS, NSYM, T>& t) {
+__device__ __forceinline__ int decode_slow(Bits& br, const Table<BITS, NSYM, T>& t) {
   const uint32_t bits = static_cast<uint32_t>(br.buf);
   int code = 0, first = 0, index = 0;
   for (int l = 1; l < 16; ++l) {
@@ -387,11 +386,12 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
       const int length = 3 + static_cast<int>((e >> 7) & 255u) + static_cast<int>(br.get(extra));
       br.refill();
       const uint32_t de = decode<EncDist>(br, sm.dist);
-      if (!de || (de & 0x100u)) {
+      const uint32_t dsym = de >> 8;
+      if (!de || dsym >= 30) {
         err = 1;
         break;
       }
-      const int distance = static_cast<int>(de >> 16) + static_cast<int>(br.get((de >> 4) & 15u));
+      const int distance = c_dist_base[dsym] + static_cast<int>(br.get((de >> 4) & 15u));
       // (reading past the stream end only consumes padding / the next stream's bytes; the
       // end-of-block check below reports truncation)
       if (distance > pos) {
