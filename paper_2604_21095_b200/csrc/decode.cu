@@ -148,8 +148,8 @@ __device__ __forceinline__ uint32_t spread16(uint32_t x) {
   return x;
 }
 
-// PLINK rows: counts straight from bit planes. Each lane keeps 4 independent 16-byte
-// streaming loads in flight (64 samples each) before counting, so a warp has 2 KB of
+// PLINK rows: counts straight from bit planes. Each lane keeps 6 independent 16-byte
+// streaming loads in flight (64 samples each) before counting, so a warp has 3 KB of
 // the row outstanding. Per 16-sample word: n0 = popc(lo & hi), missing = popc(lo) - n0,
 // n2 = 16 - popc(lo | hi) (~10 integer ops). Masks (excluded samples, the padding codes
 // of the last vector) are applied only where needed, in a separate path, so the common
@@ -177,15 +177,16 @@ __device__ __forceinline__ void bed_counts(const GenoBlock& b, int64_t m, int la
   const int64_t n_vec = (b.n_src + 63) / 64;                 // 16-byte vectors holding real samples
   const int64_t n_plain = b.all_kept ? b.n_src / 64 : 0;     // vectors needing no mask
   int n2 = 0, n0 = 0, nm = 0;
-  for (int64_t base = lane; base < n_plain; base += 4 * 32) {
-    uint4 w4[4];
+  constexpr int kU = 6;  // loads in flight per lane: a 23k-sample row is two rounds of 6 x 32 x 16 B
+  for (int64_t base = lane; base < n_plain; base += kU * 32) {
+    uint4 w4[kU];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < kU; ++j) {
       const int64_t vi = base + 32 * j;
       w4[j] = vi < n_plain ? __ldcs(row + vi) : make_uint4(0x55555555u, 0x55555555u, 0x55555555u, 0x55555555u);
     }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < kU; ++j) {
       // out-of-range vectors were filled with all-missing codes (01): undo their count
       if (base + 32 * j >= n_plain) nm -= 64;
       bed_word(w4[j].x, nm, n2, n0);
@@ -225,6 +226,17 @@ __global__ void stats_kernel(GenoBlock b, MarkerStats st, int64_t m_pad, double 
   bool nonint = false;
   if constexpr (KIND == PG_GENO_BED) {
     bed_counts(b, m, lane, nmiss, su, ssu);
+    // per-lane counts fit in 32 bits: reduce them as int (one shuffle each, not two)
+    int a = static_cast<int>(nmiss), c = static_cast<int>(su), d = static_cast<int>(ssu);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      c += __shfl_xor_sync(0xffffffffu, c, o);
+      d += __shfl_xor_sync(0xffffffffu, d, o);
+    }
+    nmiss = a;
+    su = c;
+    ssu = d;
   } else {
     for (int64_t ci = lane; ci < n_chunks; ci += 32) {
       int u[kChunk];
@@ -238,12 +250,14 @@ __global__ void stats_kernel(GenoBlock b, MarkerStats st, int64_t m_pad, double 
       }
     }
   }
+  if constexpr (KIND != PG_GENO_BED) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    nmiss += __shfl_xor_sync(0xffffffffu, nmiss, o);
-    su += __shfl_xor_sync(0xffffffffu, su, o);
-    ssu += __shfl_xor_sync(0xffffffffu, ssu, o);
-    dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
+    for (int o = 16; o > 0; o >>= 1) {
+      nmiss += __shfl_xor_sync(0xffffffffu, nmiss, o);
+      su += __shfl_xor_sync(0xffffffffu, su, o);
+      ssu += __shfl_xor_sync(0xffffffffu, ssu, o);
+      dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
+    }
   }
   if (lane != 0) return;
   const double nan = __longlong_as_double(0x7ff8000000000000ll);
