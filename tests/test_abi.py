@@ -96,14 +96,13 @@ def test_native_tsv_lines_match_python_formatting():
     rng = np.random.default_rng(5)
     markers = [pg.MarkerRecord(str(1 + i % 3), f"rs{i}", 100 * i + 1, "A", "GT", i) for i in range(7)]
     names = ["height", "bmi_z", "phéno"]
-    w = output.ThresholdWriter.__new__(output.ThresholdWriter)
-    output._Writer.__init__(w, 812.0, 815, False, names)
+    fmt = output._RecordText(812.0, 815, False, names)
     rows = rng.integers(0, 7, 50)
     cols = rng.integers(0, 3, 50)
     r, t, p = rng.standard_normal(50) / 10, rng.standard_normal(50) * 5, rng.random(50) ** 8
     af = rng.random(7)
     miss = rng.integers(0, 9, 7)
-    text = output.format_records(markers, af, miss, rows, cols, r, t, p, w._pheno_blob, w._pheno_off, w._tail, False)
-    want = "".join(w._line(markers[i], af[i], int(miss[i]), names[j], r[k], t[k], p[k])
+    text = output.format_records(markers, af, miss, rows, cols, r, t, p, fmt.pheno_blob, fmt.pheno_off, fmt.mid, False)
+    want = "".join(fmt.python_line(markers[i], af[i], int(miss[i]), names[j], r[k], t[k], p[k])
                    for k, (i, j) in enumerate(zip(rows.tolist(), cols.tolist())))
     assert text == want
