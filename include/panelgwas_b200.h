@@ -274,6 +274,14 @@ PG_API int pg_format_tsv(int64_t n, const int64_t* rows, const int64_t* cols, co
                          const int64_t* prefix_off, const char* pheno_blob, const int64_t* pheno_off,
                          const char* mid, int64_t mid_len, char* out, int64_t out_cap, int64_t* out_len);
 
+/* FULL-mode marker sidecar lines "SOURCE_INDEX CHR ID POS A1 A2 AF N_MISS" (tab-separated, LF) of
+ * markers rows[0..n): replaces the per-marker f-string of FullMatrixWriter.emit
+ * (/root/reference/pkg/src/panelgwas/output.py:245-252). prefix blob/offsets as in pg_format_tsv;
+ * AF rendered as Python repr. PG_ERR_INVALID when out_cap is too small. */
+PG_API int pg_format_marker_lines(int64_t n, const int64_t* rows, const int64_t* src_index,
+                                  const char* prefix_blob, const int64_t* prefix_off, const double* af,
+                                  const int64_t* n_miss, char* out, int64_t out_cap, int64_t* out_len);
+
 /* ---- genotype decode on the device (host arrays in/out) ---- */
 /* PlinkSource.read_marker_batch / decode_bed_codes (plink.py:48-61, 167-185):
  * rows of `row_bytes` packed codes -> dosages (elem 4: f32, 8: f64) [n_markers, n_samples]

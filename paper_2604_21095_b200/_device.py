@@ -240,11 +240,14 @@ class DeviceContext:
         _native.check(status)
         return None
 
-    def scan_staged(self, slot: int, *, fetch: bool = True, full_elem_bytes: int = 8) -> ScanResult:
+    def scan_staged(self, slot: int, *, fetch: bool = True, full_elem_bytes: int = 8,
+                    full_out: np.ndarray | None = None) -> ScanResult:
+        """Scan staging slot 0/1. In FULL mode `full_out` (e.g. a pinned uint8 buffer large
+        enough for the batch) receives the t rows and `t_rows` is a view of it."""
         info = BatchInfo()
         with self.lock:
             call("pg_scan_staged", self._h, int(slot), byref(info))
-            return self._collect(info, fetch, full_elem_bytes)
+            return self._collect(info, fetch, full_elem_bytes, full_out)
 
     def scan_device(self, kind: int, d_ptr: int, n_markers: int, row_bytes: int, row_pitch: int, *,
                     fetch: bool = True, full_elem_bytes: int = 8) -> ScanResult:
@@ -254,7 +257,8 @@ class DeviceContext:
                  byref(info))
             return self._collect(info, fetch, full_elem_bytes)
 
-    def _collect(self, info: BatchInfo, fetch: bool, full_elem_bytes: int) -> ScanResult:
+    def _collect(self, info: BatchInfo, fetch: bool, full_elem_bytes: int,
+                 full_out: np.ndarray | None = None) -> ScanResult:
         m = int(info.n_markers)
         res = ScanResult(
             n_markers=m,
@@ -271,7 +275,11 @@ class DeviceContext:
             n_rows = c_int64(0)
             call("pg_fetch_full", self._h, None, full_elem_bytes, byref(n_rows))
             dt = np.float32 if full_elem_bytes == 4 else np.float64
-            out = np.empty((n_rows.value, self.n_pheno), dtype=dt)
+            need = n_rows.value * self.n_pheno * full_elem_bytes
+            if full_out is not None and full_out.nbytes >= need:
+                out = full_out.reshape(-1)[:need].view(dt).reshape(n_rows.value, self.n_pheno)
+            else:
+                out = np.empty((n_rows.value, self.n_pheno), dtype=dt)
             call("pg_fetch_full", self._h, ptr(out), full_elem_bytes, byref(n_rows))
             res.t_rows = out
         else:

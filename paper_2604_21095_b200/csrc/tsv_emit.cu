@@ -153,4 +153,32 @@ int pg_format_tsv(int64_t n, const int64_t* rows, const int64_t* cols, const dou
   return PG_OK;
 }
 
+// FULL-mode marker sidecar lines "SOURCE_INDEX\tCHR\tID\tPOS\tA1\tA2\tAF\tN_MISS\n" for markers
+// rows[0..n): the "CHR..A2\t" part comes pre-rendered per marker (prefix blob + offsets), AF as
+// Python repr, integers in decimal. Replaces a Python f-string per scanned marker.
+int pg_format_marker_lines(int64_t n, const int64_t* rows, const int64_t* src_index, const char* prefix_blob,
+                           const int64_t* prefix_off, const double* af, const int64_t* n_miss, char* out,
+                           int64_t out_cap, int64_t* out_len) {
+  int64_t o = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t k = rows[i];
+    const int64_t plen = prefix_off[k + 1] - prefix_off[k];
+    if (o + plen + 3 * 24 + 40 > out_cap) {
+      *out_len = o;
+      pg::set_error("pg_format_marker_lines: output buffer too small at marker %lld", (long long)i);
+      return PG_ERR_INVALID;
+    }
+    o += pg::put_int(src_index[k], out + o);
+    out[o++] = '\t';
+    std::memcpy(out + o, prefix_blob + prefix_off[k], plen);
+    o += plen;
+    o += pg::py_repr(af[k], out + o);
+    out[o++] = '\t';
+    o += pg::put_int(n_miss[k], out + o);
+    out[o++] = '\n';
+  }
+  *out_len = o;
+  return PG_OK;
+}
+
 }  // extern "C"

@@ -502,6 +502,7 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
             t_emit += time.perf_counter() - t0
             set_topk_bars(i + 1)
 
+        pinned_out: list = []
         try:
             staged: list = [None, None]
             # records of batch i-1 are formatted / written on a writer thread while batch i
@@ -522,9 +523,20 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
                     waits["emit"] += time.perf_counter() - t0
                 emit_fut = emitter.submit(finish, i, res)
 
+            # FULL: t rows land in two pinned buffers used alternately. The writer holds at most
+            # one batch (dispatch waits for it before handing over the next), so batch i's
+            # buffer is free again by the time batch i+2 is fetched into it.
+            full_bufs = []
+            if config.output_mode is OutputMode.FULL:
+                full_bufs = [_native.PinnedBuffer(step * n_pheno * dtype.itemsize) for _ in range(2)]
+                pinned_out.extend(full_bufs)
+            n_scanned = [0]
+
             def scan(slot):
                 t0 = time.perf_counter()
-                res = ctx.scan_staged(slot, full_elem_bytes=dtype.itemsize)
+                out = full_bufs[n_scanned[0] % 2].array if full_bufs else None
+                n_scanned[0] += 1
+                res = ctx.scan_staged(slot, full_elem_bytes=dtype.itemsize, full_out=out)
                 waits["scan"] += time.perf_counter() - t0
                 return res
 
@@ -564,9 +576,9 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
                 max_abs_t = ctx.t_from_r(max_abs_r, df)
                 min_p, _ = ctx.p_from_t(max_abs_t, df)
         finally:
-            if pinned is not None:
+            if pinned is not None or pinned_out:
                 ctx.sync()
-                for b in pinned:
+                for b in (pinned or []) + pinned_out:
                     b.close()
     finally:
         ctx.close()

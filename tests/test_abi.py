@@ -106,3 +106,32 @@ def test_native_tsv_lines_match_python_formatting():
     want = "".join(fmt.python_line(markers[i], af[i], int(miss[i]), names[j], r[k], t[k], p[k])
                    for k, (i, j) in enumerate(zip(rows.tolist(), cols.tolist())))
     assert text == want
+
+
+def test_full_writer_marker_sidecar_matches_python_formatting(tmp_path, monkeypatch):
+    """FullMatrixWriter renders <out>.markers.tsv natively (pg_format_marker_lines); the lines
+    equal the reference's per-marker f-string with repr() floats, skipped markers omitted."""
+    import numpy as np
+
+    import paper_2604_21095_b200 as pg
+    from paper_2604_21095_b200 import output
+
+    monkeypatch.setattr(output, "_WRITE_CHUNK", 20)  # exercise the parallel pwrite split
+    rng = np.random.default_rng(11)
+    m, p = 9, 3
+    markers = tuple(pg.MarkerRecord(str(1 + i % 2), f"rs{i}", 10 * i + 7, "AC", "T", 100 + i) for i in range(m))
+    af = np.r_[rng.random(m - 2), 0.5, 1.0 / 3.0]
+    miss = rng.integers(0, 5, m)
+    skip = np.zeros(m, np.int8)
+    skip[[2, 5]] = 1
+    t_rows = rng.standard_normal((m - 2, p)).astype(np.float32)
+    w = output.FullMatrixWriter(tmp_path / "f.bin", np.float32, 10.0, 12, False, ["a", "b", "c"])
+    w.emit(output.BatchStats(markers=markers, allele_frequency=af, missing_count=miss, skip_reason=skip,
+                             clamp_count=0, t_rows=t_rows))
+    w.finalize()
+    t, lines, names = output.read_full_matrix(tmp_path / "f.bin")
+    want = [f"{mk.source_index}\t{mk.chrom}\t{mk.id}\t{mk.pos}\t{mk.allele2}\t{mk.allele1}\t{repr(float(af[i]))}\t"
+            f"{int(miss[i])}" for i, mk in enumerate(markers) if not skip[i]]
+    assert lines == want
+    assert names == ["a", "b", "c"]
+    assert np.array_equal(t, t_rows)

@@ -71,6 +71,7 @@ def main():
     ap.add_argument("--covariates", type=int, default=10)
     ap.add_argument("--seed", type=int, default=3)
     ap.add_argument("--top-k", type=int, default=0, help="TOPK mode with this k instead of THRESHOLD p <= 1e-4")
+    ap.add_argument("--full", action="store_true", help="FULL mode (f32 t matrix) instead of THRESHOLD")
     a = ap.parse_args()
     d = Path(a.dir)
     d.mkdir(parents=True, exist_ok=True)
@@ -87,7 +88,8 @@ def main():
     sizes = {f: os.path.getsize(d / f) for f in ("geno.bed", "pheno.tsv", "covar.tsv")}
     cmd = [sys.executable, "-m", "paper_2604_21095_b200", "run", "--bfile", str(d / "geno"), "--pheno",
            str(d / "pheno.tsv"), "--covar", str(d / "covar.tsv"),
-           *(["--top-k", str(a.top_k)] if a.top_k else ["--p-threshold", "1e-4"]), "--out", str(d / "hits.tsv")]
+           *(["--full", "--allow-large-full"] if a.full else ["--top-k", str(a.top_k)] if a.top_k
+             else ["--p-threshold", "1e-4"]), "--out", str(d / "hits.tsv")]
     t0 = time.perf_counter()
     res = subprocess.run(cmd, capture_output=True, text=True, cwd=str(ROOT),
                          env={**os.environ, "PANELGWAS_PROFILE": "1"})
@@ -97,10 +99,10 @@ def main():
         raise SystemExit(res.returncode)
     summary = json.loads((d / "hits.tsv.summary.json").read_text())
     tests = summary["markers_scanned"] * summary["phenotypes_scanned"]
-    mode = f"TOPK k={a.top_k}" if a.top_k else "p<=1e-4"
+    mode = "FULL f32" if a.full else f"TOPK k={a.top_k}" if a.top_k else "p<=1e-4"
     line = {"workload": f"C3 via CLI: N={n:,} M={a.markers:,} P={p:,} + {a.covariates} covariates, {mode}",
             "wall_s": wall, "tests": tests, "tests_per_s_wall": tests / wall, "records": summary["records_emitted"],
-            "file_bytes": sizes, "write_inputs_s": t_write,
+            "file_bytes": {**sizes, "out": os.path.getsize(d / "hits.tsv")}, "write_inputs_s": t_write,
             "summary_times": {k: summary[k] for k in summary if k.startswith("time_") or k == "wall_s"},
             "phases": next((json.loads(ln)["panelgwas_phases_s"] for ln in res.stderr.splitlines()
                             if ln.startswith('{"panelgwas_phases_s"')), None)}
