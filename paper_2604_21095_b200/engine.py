@@ -216,6 +216,15 @@ def topk_batch_bars(writer, top_k: int, batch_markers: int, t_floor: float, df: 
     return bars, need
 
 
+def _pinned_buffers(sizes: list[int]) -> list:
+    return [_native.PinnedBuffer(n) for n in sizes]
+
+
+def _free_pinned(bufs) -> None:
+    for b in bufs or []:
+        b.close()
+
+
 def device_batch_size(config: ScanConfig, n_markers: int, n_pheno: int, n_samples: int = 0) -> int:
     """Markers per device launch: at least the configured batch, sized for the GEMM, memory-bounded."""
     if config.device_batch is not None:
@@ -335,24 +344,34 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
                    prep_hook=None) -> ScanSummary:
     from ._device import DeviceContext
 
-    # CUDA context creation (~0.5 s) overlaps the host table parsing; every C-ABI entry
-    # selects the ctx's device itself, so the handle may be created on another thread
-    with ThreadPoolExecutor(max_workers=1) as init:
-        ctx_fut = init.submit(DeviceContext, config.device)
-        try:
-            phases = {"start": time.perf_counter() - wall0}
-            prep = prep_hook(source) if prep_hook is not None else prepare_panel(config, source)
-            phases["tables_panel_host"] = time.perf_counter() - wall0
-            if source.n_markers < 1:
-                raise PanelGwasError("genotype source has no markers")
-        except BaseException:
+    # CUDA context creation (~0.5 s) and the pinned read ring (~0.4 s per GB) overlap the host
+    # table parsing; every C-ABI entry selects the ctx's device itself, so the handle may be
+    # created on another thread
+    lo, hi = marker_range if marker_range is not None else (0, source.n_markers)
+    compressed = hasattr(source, "read_compressed_block") and os.environ.get("PANELGWAS_HOST_INFLATE") != "1"
+    row_bytes = (source.compressed_bytes_per_marker if compressed
+                 else getattr(source, "bytes_per_marker", 0))
+    # the batch only shrinks as phenotypes are added, so one phenotype bounds every ring slot
+    ring_bytes = device_batch_size(config, max(hi - lo, 1), 1, source.n_samples) * row_bytes
+    init = ThreadPoolExecutor(max_workers=1)
+    ctx_fut = init.submit(DeviceContext, config.device)
+    ring_fut = init.submit(_pinned_buffers, [ring_bytes] * 3 if ring_bytes else [])
+    init.shutdown(wait=False)
+    try:
+        phases = {"start": time.perf_counter() - wall0}
+        prep = prep_hook(source) if prep_hook is not None else prepare_panel(config, source)
+        phases["tables_panel_host"] = time.perf_counter() - wall0
+        if source.n_markers < 1:
+            raise PanelGwasError("genotype source has no markers")
+        ctx = ctx_fut.result()
+    except BaseException:
+        for fut, release in ((ring_fut, _free_pinned), (ctx_fut, lambda c: c.close())):
             try:
-                ctx_fut.result().close()
+                release(fut.result())
             except Exception:
                 pass
-            raise
-        ctx = ctx_fut.result()
-        phases["device_ready"] = time.perf_counter() - wall0
+        raise
+    phases["device_ready"] = time.perf_counter() - wall0
     n = prep.align.n_kept
     df = prep.df
     dtype = np.dtype(np.float32 if config.precision is Precision.F32_STORE_F64_ACC else np.float64)
@@ -362,24 +381,27 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
         else:
             stage_panel(ctx, prep, source.n_samples)
         phases["panel_on_device"] = time.perf_counter() - wall0
+        names = prep.pheno_names
+        n_pheno = len(names)
+        if config.output_mode is OutputMode.FULL:
+            projected = source.n_markers * n_pheno * dtype.itemsize
+            if projected > config.full_byte_budget and not config.allow_large_full:
+                raise ConfigError(
+                    f"FULL output would be ~{projected} bytes, over the {config.full_byte_budget}-byte budget; "
+                    "pass the large-output override to proceed"
+                )
+            writer = output.FullMatrixWriter(config.out_path, dtype, df, n, source.counts_allele1, names)
+        elif config.output_mode is OutputMode.TOPK:
+            writer = output.TopKWriter(config.out_path, config.top_k, df, n, source.counts_allele1, names)
+        else:
+            writer = output.ThresholdWriter(config.out_path, config.p_threshold, df, n, source.counts_allele1,
+                                            names)
     except BaseException:
-        ctx.close()
+        try:
+            _free_pinned(ring_fut.result())
+        finally:
+            ctx.close()
         raise
-    names = prep.pheno_names
-    n_pheno = len(names)
-
-    if config.output_mode is OutputMode.FULL:
-        projected = source.n_markers * n_pheno * dtype.itemsize
-        if projected > config.full_byte_budget and not config.allow_large_full:
-            raise ConfigError(
-                f"FULL output would be ~{projected} bytes, over the {config.full_byte_budget}-byte budget; "
-                "pass the large-output override to proceed"
-            )
-        writer = output.FullMatrixWriter(config.out_path, dtype, df, n, source.counts_allele1, names)
-    elif config.output_mode is OutputMode.TOPK:
-        writer = output.TopKWriter(config.out_path, config.top_k, df, n, source.counts_allele1, names)
-    else:
-        writer = output.ThresholdWriter(config.out_path, config.p_threshold, df, n, source.counts_allele1, names)
 
     if os.environ.get("PANELGWAS_FUSED_DECODE", "1") == "0":
         ctx.set_fused_decode(False)  # A/B switch; results are identical either way
@@ -401,7 +423,6 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
         skip_mono = skip_missing = clamp_total = 0
         t_decode = t_prepare = t_corr = t_emit = 0.0
         qc_rows: list[str] = []
-        lo, hi = marker_range if marker_range is not None else (0, source.n_markers)
         step = device_batch_size(config, hi - lo, n_pheno, source.n_samples)
         plan = [(lo + s0, c0) for s0, c0 in plan_batches(hi - lo, step)]
         read_kw = {"dtype": dtype} if config.source.format.value == "dense" else {}
@@ -409,12 +430,7 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
         # pinned ring of 3 host buffers + 2 device staging slots: the read of batch i+1 and
         # its H2D overlap the device scan of batch i. BGEN batches travel compressed and are
         # inflated on the GPU (pg_stage_bgen); other formats as raw rows (pg_stage).
-        compressed = hasattr(source, "read_compressed_block") and os.environ.get("PANELGWAS_HOST_INFLATE") != "1"
-        pinned = None
-        if compressed:
-            pinned = [_native.PinnedBuffer(step * source.compressed_bytes_per_marker) for _ in range(3)]
-        elif hasattr(source, "bytes_per_marker"):
-            pinned = [_native.PinnedBuffer(step * source.bytes_per_marker) for _ in range(3)]
+        pinned = ring_fut.result() or None  # allocated during table parsing (>= step * row bytes each)
 
         def read(i):
             t0 = time.perf_counter()
@@ -510,7 +526,7 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
             emitter = ThreadPoolExecutor(max_workers=1) if config.output_mode is not OutputMode.TOPK else None
             emit_fut = None
 
-            waits = {"read": 0.0, "scan": 0.0, "emit": 0.0, "stage": 0.0}
+            waits = {"read": 0.0, "scan": 0.0, "emit": 0.0, "stage": 0.0, "finish_thread": 0.0}
 
             def dispatch(i, res):
                 nonlocal emit_fut
@@ -521,13 +537,18 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
                     t0 = time.perf_counter()
                     emit_fut.result()  # one batch in the writer at a time; re-raises its errors
                     waits["emit"] += time.perf_counter() - t0
-                emit_fut = emitter.submit(finish, i, res)
+                emit_fut = emitter.submit(timed_finish, i, res)
+
+            def timed_finish(i, res):
+                t0 = time.perf_counter()
+                finish(i, res)
+                waits["finish_thread"] += time.perf_counter() - t0
 
             # FULL: t rows land in two pinned buffers used alternately. The writer holds at most
             # one batch (dispatch waits for it before handing over the next), so batch i's
             # buffer is free again by the time batch i+2 is fetched into it.
             full_bufs = []
-            if config.output_mode is OutputMode.FULL:
+            if config.output_mode is OutputMode.FULL and os.environ.get("PANELGWAS_FULL_PINNED") != "0":
                 full_bufs = [_native.PinnedBuffer(step * n_pheno * dtype.itemsize) for _ in range(2)]
                 pinned_out.extend(full_bufs)
             n_scanned = [0]
@@ -589,6 +610,8 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
     records = writer.finalize()
     t_emit += time.perf_counter() - t0
     phases["finalized"] = time.perf_counter() - wall0
+    if hasattr(writer, "timings"):
+        phases["writer"] = writer.timings
     if os.environ.get("PANELGWAS_PROFILE") == "1":  # cumulative seconds since run_scan entry
         print(json.dumps({"panelgwas_phases_s": phases}), file=sys.stderr)
 

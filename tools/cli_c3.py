@@ -90,6 +90,8 @@ def main():
            str(d / "pheno.tsv"), "--covar", str(d / "covar.tsv"),
            *(["--full", "--allow-large-full"] if a.full else ["--top-k", str(a.top_k)] if a.top_k
              else ["--p-threshold", "1e-4"]), "--out", str(d / "hits.tsv")]
+    for old in d.glob("hits.tsv*"):  # a rewrite of an existing file costs extra (truncate + flush on close)
+        old.unlink()
     t0 = time.perf_counter()
     res = subprocess.run(cmd, capture_output=True, text=True, cwd=str(ROOT),
                          env={**os.environ, "PANELGWAS_PROFILE": "1"})
