@@ -282,6 +282,19 @@ PG_API int pg_format_marker_lines(int64_t n, const int64_t* rows, const int64_t*
                                   const char* prefix_blob, const int64_t* prefix_off, const double* af,
                                   const int64_t* n_miss, char* out, int64_t out_cap, int64_t* out_len);
 
+/* PLINK .bim catalog (host). pg_bim_index validates the reference grammar
+ * (/root/reference/pkg/src/panelgwas/genotypes/plink.py:64-90: 6 fields per non-blank line,
+ * position an integer >= 0) and records per marker the byte spans of chrom / id / allele1 /
+ * allele2 (tok_start, tok_len: [cap x 4]) and the position; *same counts markers with equal
+ * alleles. PG_TABLE_GENERIC (100) when the file needs the line-by-line reader (non-ASCII, bare
+ * CR, field-count or position errors: that reader raises the reference's message).
+ * pg_bim_prefixes renders "CHR\tID\tPOS\tA1\tA2\t" for markers [first, first+count)
+ * (alleles swapped when swap != 0) with out_off[count+1] byte offsets. */
+PG_API int pg_bim_index(const char* buf, int64_t len, int64_t cap, int64_t* n, int64_t* tok_start,
+                        int32_t* tok_len, int64_t* pos, int64_t* same);
+PG_API int pg_bim_prefixes(const char* buf, const int64_t* tok_start, const int32_t* tok_len, const int64_t* pos,
+                           int64_t first, int64_t count, int swap, char* out, int64_t out_cap, int64_t* out_off);
+
 /* ---- genotype decode on the device (host arrays in/out) ---- */
 /* PlinkSource.read_marker_batch / decode_bed_codes (plink.py:48-61, 167-185):
  * rows of `row_bytes` packed codes -> dosages (elem 4: f32, 8: f64) [n_markers, n_samples]

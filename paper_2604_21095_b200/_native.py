@@ -102,6 +102,8 @@ SIGNATURES: dict[str, list] = {
     "pg_format_float_repr": [_P, c_int64, _P, c_int64, _P],
     "pg_format_tsv": [c_int64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, c_int64, _P, c_int64, _P],
     "pg_format_marker_lines": [c_int64, _P, _P, _P, _P, _P, _P, _P, c_int64, _P],
+    "pg_bim_index": [_P, c_int64, c_int64, _P, _P, _P, _P, _P],
+    "pg_bim_prefixes": [_P, _P, _P, _P, c_int64, c_int64, c_int, _P, c_int64, _P],
     "pg_time_marker_stats": [_P, c_int, _P, c_int64, c_int64, c_int, _P],
     "pg_debug_inflate": [_P, c_int64, _P, _P, c_int64, c_int64, _P, c_int64, _P, _P],
     "pg_debug_assoc_gemm": [_P, _P, _P, c_int64, _P, _P, c_int64, c_int64, _P, _P],

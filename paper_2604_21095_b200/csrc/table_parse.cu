@@ -87,6 +87,46 @@ inline bool has_special(const char* s, size_t n) {
   return false;
 }
 
+// Non-blank lines of buf[body_offset, len) with their 1-based physical line numbers (a CR
+// before the LF is not part of the line). The newline scan -- a pass over the whole table,
+// gigabytes at C3 -- is split over threads by byte range; the line list is then assembled
+// in order.
+std::vector<Line> find_lines(const char* buf, int64_t len, int64_t body_offset, int64_t first_lineno, int nt) {
+  const int64_t span = len - body_offset;
+  if (span <= (int64_t{8} << 20)) nt = 1;
+  std::vector<std::vector<int64_t>> nl(nt);
+  {
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t) {
+      th.emplace_back([&, t] {
+        int64_t pos = body_offset + span * t / nt;
+        const int64_t stop = body_offset + span * (t + 1) / nt;
+        while (pos < stop) {
+          const void* hit = std::memchr(buf + pos, '\n', static_cast<size_t>(stop - pos));
+          if (!hit) break;
+          const int64_t at = static_cast<const char*>(hit) - buf;
+          nl[t].push_back(at);
+          pos = at + 1;
+        }
+      });
+    }
+    for (auto& x : th) x.join();
+  }
+  std::vector<Line> lines;
+  int64_t begin = body_offset, lineno = first_lineno;
+  auto add = [&](int64_t end) {
+    int64_t stop = end;
+    if (stop > begin && buf[stop - 1] == '\r') --stop;
+    if (stop > begin) lines.push_back({begin, stop, lineno});
+    begin = end + 1;
+    ++lineno;
+  };
+  for (const auto& v : nl)
+    for (int64_t e : v) add(e);
+  if (begin < len) add(len);
+  return lines;
+}
+
 }  // namespace
 }  // namespace pg
 
@@ -111,23 +151,13 @@ int pg_table_parse(const char* buf, int64_t len, int64_t body_offset, char delim
   *err_line = 0;
   *err_cells = 0;
   // ---- records: non-blank lines (csv.reader yields [] for an empty line)
-  std::vector<Line> lines;
-  int64_t pos = body_offset, lineno = first_lineno;
-  while (pos < len) {
-    const void* nl = std::memchr(buf + pos, '\n', static_cast<size_t>(len - pos));
-    const int64_t end = nl ? static_cast<const char*>(nl) - buf : len;
-    int64_t stop = end;
-    if (stop > pos && buf[stop - 1] == '\r') --stop;
-    if (stop > pos) lines.push_back({pos, stop, lineno});
-    pos = end + 1;
-    ++lineno;
-  }
+  int nt = n_threads > 0 ? n_threads : static_cast<int>(std::thread::hardware_concurrency());
+  nt = std::max(1, std::min<int>(nt, 64));
+  const std::vector<Line> lines = pg::find_lines(buf, len, body_offset, first_lineno, nt);
   const int64_t nr = static_cast<int64_t>(lines.size());
   *n_rows = nr;
   if (values == nullptr) return PG_OK;
 
-  int nt = n_threads > 0 ? n_threads : static_cast<int>(std::thread::hardware_concurrency());
-  nt = std::max(1, std::min<int>(nt, 64));
   if (nr < 4 * nt) nt = static_cast<int>(std::max<int64_t>(1, nr / 4));
   const int64_t n_val = n_fields - 1;
   std::atomic<bool> generic{false};

@@ -500,7 +500,7 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
             start, count = plan[i]
             t_prepare += res.decode_ms / 1e3
             t_corr += res.gemm_ms / 1e3
-            markers = tuple(source.marker_catalog[start:start + count])
+            markers = source.marker_catalog[start:start + count]  # a lazy catalog slice for the writers
             batch = output.BatchStats(
                 markers=markers, allele_frequency=res.af, missing_count=res.missing_count,
                 skip_reason=res.skip, clamp_count=res.clamp_count, cand_rows=res.cand_rows,

@@ -355,7 +355,7 @@ class TestSimulate:
             pg.SimSpec(seed=1, n_samples=0, n_markers=1, n_phenotypes=1)
 
 
-def test_bim_fast_path_equals_line_reader(tmp_path):
+def test_bim_native_path_equals_line_reader(tmp_path):
     from paper_2604_21095_b200.genotypes import plink
 
     lines = [f"{1 + i % 22}\trs{i}\t0.{i}\t{100 * i + 7}\t{'ACGT'[i % 4]}\t{'TGCA'[i % 4]}" for i in range(500)]
@@ -363,15 +363,69 @@ def test_bim_fast_path_equals_line_reader(tmp_path):
     lines[20] = "  " + lines[20].replace("\t", "   ") + "  "  # any whitespace between fields
     p = tmp_path / "a.bim"
     p.write_text("\n".join(lines) + "\n")
-    fast = plink._parse_bim_fast(p)
+    fast = plink._parse_bim_native(p)
     assert fast is not None and fast == plink._parse_bim_lines(p)
     assert [r.source_index for r in fast] == list(range(500))
     bad = tmp_path / "b.bim"
     bad.write_text("1 rs1 0 5 A G\n1 rs2 0 6 A\n")
-    assert plink._parse_bim_fast(bad) is None
+    assert plink._parse_bim_native(bad) is None
     with pytest.raises(FormatError, match="expected 6 columns"):
         plink._parse_bim(bad)
     neg = tmp_path / "c.bim"
     neg.write_text("1 rs1 0 -5 A G\n")
     with pytest.raises(FormatError, match="negative position"):
         plink._parse_bim(neg)
+
+
+def test_marker_catalog_behaves_like_the_reference_list():
+    """Sources expose marker_catalog as a lazy column catalog; it must read like the
+    reference's list[MarkerRecord] (indexing, slicing, iteration, equality, len)."""
+    from paper_2604_21095_b200.genotypes.types import MarkerCatalog, MarkerRecord
+
+    cols = (["1", "2", "X"], ["rs1", "rs2", "rs3"], [10, 20, 30], ["A", "C", "G"], ["T", "G", "A"])
+    want = [MarkerRecord(c, i, p, a, b, k) for k, (c, i, p, a, b) in enumerate(zip(*cols))]
+    cat = MarkerCatalog(*cols)
+    assert len(cat) == 3 and list(cat) == want and cat == want
+    assert cat[0] == want[0] and cat[-1] == want[2]
+    assert cat[1:] == want[1:] and cat[1:][0].source_index == 1
+    assert cat[::2] == want[::2]
+    assert [m.id for m in cat[1:3]] == ["rs2", "rs3"]
+    assert cat[1:].prefixes(True) == ["2\trs2\t20\tC\tG\t", "X\trs3\t30\tG\tA\t"]
+    assert cat.prefixes(False)[0] == "1\trs1\t10\tT\tA\t"
+    assert cat[1:].source_indices().tolist() == [1, 2]
+    with pytest.raises(IndexError):
+        cat[3]
+
+
+@pytest.mark.parametrize("text", [
+    "1\trs1\t0\t10\tA\tG\n2 rs2 0.5 +20 C T\r\n\n  X\trs3\t0\t007\tG\tG  \n",  # plain, CRLF, blank, '+', '007'
+    "1\trs1\t0\t10\tA\tG",                        # no final newline
+    "1\trs1\t0\t1_000\tA\tG\n",                   # Python int() digit groups: generic reader
+    "1\trs1\t0\t-5\tA\tG\n",                      # negative position: the reference's error
+    "1\trs1\t0\t10\tA\n",                         # 5 fields
+    "1\trs1\t0\t10\tA\tG\tx\n",                   # 7 fields
+    "1\trs1\t0\t10\tA\tG\r2\trs2\t0\t5\tA\tG\n",   # bare CR: a line break for Python
+    "1\trsé\t0\t10\tA\tG\n",                      # non-ASCII
+    "1\trs1\t0\tten\tA\tG\n",                     # bad position
+])
+def test_native_bim_index_equals_line_reader(tmp_path, text):
+    """pg_bim_index + BimCatalog give the line-by-line reader's catalog, or defer to it."""
+    from paper_2604_21095_b200.errors import FormatError
+    from paper_2604_21095_b200.genotypes import plink
+
+    path = tmp_path / "g.bim"
+    path.write_bytes(text.encode())
+    try:
+        want = plink._parse_bim_lines(path)
+    except FormatError as exc:
+        want = exc
+    native = plink._parse_bim_native(path)
+    if isinstance(want, FormatError):
+        assert native is None
+        with pytest.raises(FormatError, match=str(want).split(": ", 1)[1][:20]):
+            plink._parse_bim(path)
+        return
+    got = plink._parse_bim(path)
+    assert list(got) == want and len(got) == len(want)
+    if native is not None:
+        assert got[1:].prefixes(False) == [f"{m.chrom}\t{m.id}\t{m.pos}\t{m.allele2}\t{m.allele1}\t" for m in want[1:]]

@@ -109,3 +109,32 @@ def test_matches_reference_loader(tmp_path):
     assert np.array_equal(got.values, want.values, equal_nan=True)
     assert got.missing_count.tolist() == want.missing_count.tolist()
     assert got.unparseable_count.tolist() == want.unparseable_count.tolist()
+
+
+def test_multithreaded_line_scan_native_equals_csv(tmp_path):
+    """A body over 8 MB takes the threaded newline scan: chunk edges fall inside lines, CRLF
+    and LF endings are mixed, blank lines keep the physical line numbers of a ragged row."""
+    rng = np.random.default_rng(8)
+    n, p = 2300, 400
+    vals = rng.standard_normal((n, p))
+    lines = ["IID\t" + "\t".join(f"p{j}" for j in range(p))]
+    for i in range(n):
+        end = "\r" if i % 3 == 0 else ""
+        lines.append(f"S{i}\t" + "\t".join(repr(float(v)) for v in vals[i]) + end)
+        if i % 97 == 0:
+            lines.append("")
+    text = "\n".join(lines) + "\n"
+    assert len(text) > 9 << 20
+    path = _write(tmp_path / "big.tsv", text)
+    native, csvp = _tables(path)
+    assert native is not None
+    _same(native, csvp)
+    assert np.array_equal(native[2], vals)
+    # a ragged row deep in the file is reported with its physical line number by both readers
+    lines[2000] = lines[2000] + "\t1.0"
+    path = _write(tmp_path / "ragged.tsv", "\n".join(lines) + "\n")
+    with pytest.raises(PanelGwasError, match=":2001: ragged row") as e1:
+        phenotypes._load_table_native(path, "IID", "\t")
+    with pytest.raises(PanelGwasError, match=":2001: ragged row") as e2:
+        phenotypes._load_table_csv(path, "IID", "\t")
+    assert str(e1.value) == str(e2.value)
