@@ -494,9 +494,6 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
 
         def finish(i, res):
             nonlocal t_prepare, t_corr, t_emit, clamp_total, skip_mono, skip_missing
-            if config.output_mode is OutputMode.TOPK:
-                res = topk_complete(i, res)
-                kept_blocks.pop(i, None)
             start, count = plan[i]
             t_prepare += res.decode_ms / 1e3
             t_corr += res.gemm_ms / 1e3
@@ -516,27 +513,30 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, 
             t0 = time.perf_counter()
             writer.emit(batch)
             t_emit += time.perf_counter() - t0
-            set_topk_bars(i + 1)
 
         pinned_out: list = []
         try:
             staged: list = [None, None]
-            # records of batch i-1 are formatted / written on a writer thread while batch i
-            # scans (TOPK stays synchronous: its bar feeds the next batch's premask)
-            emitter = ThreadPoolExecutor(max_workers=1) if config.output_mode is not OutputMode.TOPK else None
+            # records of batch i-1 are formatted / written (TOPK: merged) on a writer thread while
+            # batch i scans
+            emitter = ThreadPoolExecutor(max_workers=1)
             emit_fut = None
 
             waits = {"read": 0.0, "scan": 0.0, "emit": 0.0, "stage": 0.0, "finish_thread": 0.0}
 
             def dispatch(i, res):
                 nonlocal emit_fut
-                if emitter is None:
-                    finish(i, res)
-                    return
+                if config.output_mode is OutputMode.TOPK:
+                    res = topk_complete(i, res)  # device rescans stay on this thread
+                    kept_blocks.pop(i, None)
                 if emit_fut is not None:
                     t0 = time.perf_counter()
                     emit_fut.result()  # one batch in the writer at a time; re-raises its errors
                     waits["emit"] += time.perf_counter() - t0
+                # TOPK: the bars of batch i+1 come from the writer after batch i-1 while batch i
+                # merges on the writer thread. A lagged bar is lower (and a lagged `need`
+                # larger), so batch i+1 admits a superset of the candidates it must: exact.
+                set_topk_bars(i + 1)
                 emit_fut = emitter.submit(timed_finish, i, res)
 
             def timed_finish(i, res):
