@@ -177,24 +177,36 @@ __device__ __forceinline__ void bed_counts(const GenoBlock& b, int64_t m, int la
   const int64_t n_vec = (b.n_src + 63) / 64;                 // 16-byte vectors holding real samples
   const int64_t n_plain = b.all_kept ? b.n_src / 64 : 0;     // vectors needing no mask
   int n2 = 0, n0 = 0, nm = 0;
+  // all-kept vectors: two words share each popcount. With M the even-bit mask, the low code
+  // bits of word a go to even and those of word b to odd positions of one register,
+  //   L = (a & M) | ((b << 1) & ~M),   H = ((a >> 1) & M) | (b & ~M),
+  // so popc(L) = #codes with lo set (missing 01 + hom2 11), popc(H) = #codes with hi set
+  // (het 10 + 11) and popc(L & H) = #11 codes, for both words: 3 POPC + 2 SHF + 3 LOP per
+  // 32 samples instead of 6 POPC + 8 other ops.
+  constexpr uint32_t kM = 0x55555555u;
+  int sl = 0, sh = 0, slh = 0, valid = 0;
   constexpr int kU = 6;  // loads in flight per lane: a 23k-sample row is two rounds of 6 x 32 x 16 B
   for (int64_t base = lane; base < n_plain; base += kU * 32) {
     uint4 w4[kU];
 #pragma unroll
     for (int j = 0; j < kU; ++j) {
       const int64_t vi = base + 32 * j;
-      w4[j] = vi < n_plain ? __ldcs(row + vi) : make_uint4(0x55555555u, 0x55555555u, 0x55555555u, 0x55555555u);
+      w4[j] = vi < n_plain ? __ldcs(row + vi) : make_uint4(0u, 0u, 0u, 0u);
     }
 #pragma unroll
     for (int j = 0; j < kU; ++j) {
-      // out-of-range vectors were filled with all-missing codes (01): undo their count
-      if (base + 32 * j >= n_plain) nm -= 64;
-      bed_word(w4[j].x, nm, n2, n0);
-      bed_word(w4[j].y, nm, n2, n0);
-      bed_word(w4[j].z, nm, n2, n0);
-      bed_word(w4[j].w, nm, n2, n0);
+      valid += base + 32 * j < n_plain;  // zero-filled vectors count as hom allele-1 codes: drop them below
+      const uint32_t l0 = (w4[j].x & kM) | ((w4[j].y << 1) & ~kM), h0 = ((w4[j].x >> 1) & kM) | (w4[j].y & ~kM);
+      const uint32_t l1 = (w4[j].z & kM) | ((w4[j].w << 1) & ~kM), h1 = ((w4[j].z >> 1) & kM) | (w4[j].w & ~kM);
+      sl += __popc(l0) + __popc(l1);
+      sh += __popc(h0) + __popc(h1);
+      slh += __popc(l0 & h0) + __popc(l1 & h1);
     }
   }
+  // code classes: 11 -> 0 copies (n0), 01 missing, 10 het, 00 -> 2 copies (n2)
+  n0 = slh;
+  nm = sl - slh;
+  n2 = 64 * valid - sl - sh + slh;
   for (int64_t vi = n_plain + lane; vi < n_vec; vi += 32) {
     const uint4 w4 = __ldcs(row + vi);
     const uint32_t ws[4] = {w4.x, w4.y, w4.z, w4.w};
