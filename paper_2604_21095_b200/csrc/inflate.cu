@@ -432,19 +432,39 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
       const uint32_t want = (static_cast<uint32_t>(b8[byte_pos]) << 24) | (b8[byte_pos + 1] << 16) |
                             (b8[byte_pos + 2] << 8) | b8[byte_pos + 3];
       __syncwarp();
-      unsigned long long s1 = 0, s2 = 0;
-      const int32_t chunk = (pos + 31) / 32;
-      const int32_t a = lane * chunk, e = min(pos, a + chunk);
-      for (int32_t i = a; i < e; ++i) {
-        const uint32_t d = dst[i];
+      // A = 1 + sum d_k, B = pos + sum (pos - k) d_k = pos + pos * S1 - sum k d_k. Lanes read
+      // coalesced 4-byte words (byte sums and 0..3-weighted byte sums by DP4A); the unaligned
+      // head and the tail are done bytewise.
+      unsigned long long s1 = 0, t = 0;  // S1, sum k d_k
+      int32_t head = static_cast<int32_t>((4u - (reinterpret_cast<uintptr_t>(dst) & 3u)) & 3u);
+      head = min(head, pos);
+      const int32_t n_words = (pos - head) >> 2;
+      const int32_t tail = head + 4 * n_words;
+      for (int32_t k = lane; k < head; k += 32) {
+        const uint32_t d = dst[k];
         s1 += d;
-        s2 += static_cast<unsigned long long>(pos - i) * d;
+        t += static_cast<unsigned long long>(k) * d;
       }
+      for (int32_t k = tail + lane; k < pos; k += 32) {
+        const uint32_t d = dst[k];
+        s1 += d;
+        t += static_cast<unsigned long long>(k) * d;
+      }
+      const uint32_t* words = reinterpret_cast<const uint32_t*>(dst + head);
+      uint32_t s1w = 0;  // <= 69 KB x 255 per lane: fits
+      for (int32_t w = lane; w < n_words; w += 32) {
+        const uint32_t x = words[w];
+        const uint32_t sb = __dp4a(x, 0x01010101u, 0u);
+        s1w += sb;
+        t += static_cast<unsigned long long>(head + 4 * w) * sb + __dp4a(x, 0x03020100u, 0u);
+      }
+      s1 += s1w;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        t += __shfl_xor_sync(0xffffffffu, t, o);
       }
+      const unsigned long long s2 = static_cast<unsigned long long>(pos) * s1 - t;
       const uint32_t A = static_cast<uint32_t>((1 + s1) % 65521ull);
       const uint32_t B = static_cast<uint32_t>((static_cast<unsigned long long>(pos) + s2) % 65521ull);
       if (((B << 16) | A) != want) err = 1;
