@@ -16,6 +16,7 @@
 // one int8 row per digit (plus a 0/1 row of missing calls when present), and
 // its x127 copy (assoc.cuh).
 #include <cmath>
+#include <cstdlib>
 
 #include "decode.cuh"
 
@@ -171,6 +172,7 @@ __device__ __forceinline__ void bed_word_masked(uint32_t w, uint32_t kk, int& nm
   n2 += __popc(kk) - __popc(lo | hi);
 }
 
+template <int kU>
 __device__ __forceinline__ void bed_counts(const GenoBlock& b, int64_t m, int lane, long long& nmiss, long long& su,
                                            long long& ssu) {
   const uint4* row = reinterpret_cast<const uint4*>(b.data + m * b.pitch);
@@ -185,7 +187,7 @@ __device__ __forceinline__ void bed_counts(const GenoBlock& b, int64_t m, int la
   // 32 samples instead of 6 POPC + 8 other ops.
   constexpr uint32_t kM = 0x55555555u;
   int sl = 0, sh = 0, slh = 0, valid = 0;
-  constexpr int kU = 6;  // loads in flight per lane: a 23k-sample row is two rounds of 6 x 32 x 16 B
+  // kU loads in flight per lane (a 23k-sample row: 359 vectors = 2 rounds of 6 x 32)
   for (int64_t base = lane; base < n_plain; base += kU * 32) {
     uint4 w4[kU];
 #pragma unroll
@@ -218,7 +220,7 @@ __device__ __forceinline__ void bed_counts(const GenoBlock& b, int64_t m, int la
   ssu = n2 + n0;
 }
 
-template <int KIND>
+template <int KIND, int kU = 6>
 __global__ void stats_kernel(GenoBlock b, MarkerStats st, int64_t m_pad, double unit_scale) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t m = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + warp;
@@ -237,7 +239,7 @@ __global__ void stats_kernel(GenoBlock b, MarkerStats st, int64_t m_pad, double 
   double dsum = 0.0;
   bool nonint = false;
   if constexpr (KIND == PG_GENO_BED) {
-    bed_counts(b, m, lane, nmiss, su, ssu);
+    bed_counts<kU>(b, m, lane, nmiss, su, ssu);
     // per-lane counts fit in 32 bits: reduce them as int (one shuffle each, not two)
     int a = static_cast<int>(nmiss), c = static_cast<int>(su), d = static_cast<int>(ssu);
 #pragma unroll
@@ -452,11 +454,26 @@ __global__ void dosage_kernel(GenoBlock b, int elem_bytes, void* __restrict__ ou
   }
 }
 
+// PG_STATS_KU / PG_STATS_WPB (measurement switches): loads in flight per lane and warps per
+// block of the PLINK statistics kernel; read once.
+inline int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+
 template <int KIND>
 int stats_dispatch(const GenoBlock& b, MarkerStats& st, int64_t m_pad, cudaStream_t s) {
-  const int wpb = 8;
+  static const int ku = env_int("PG_STATS_KU", 6), wpb_env = env_int("PG_STATS_WPB", 8);
+  const int wpb = (wpb_env == 4 || wpb_env == 16) ? wpb_env : 8;
   const unsigned grid = static_cast<unsigned>((m_pad + wpb - 1) / wpb);
-  stats_kernel<KIND><<<grid, wpb * 32, 0, s>>>(b, st, m_pad, geno_unit_scale(b));
+  const double scale = geno_unit_scale(b);
+  if (KIND == PG_GENO_BED && ku == 12) {
+    stats_kernel<KIND, 12><<<grid, wpb * 32, 0, s>>>(b, st, m_pad, scale);
+  } else if (KIND == PG_GENO_BED && ku == 4) {
+    stats_kernel<KIND, 4><<<grid, wpb * 32, 0, s>>>(b, st, m_pad, scale);
+  } else {
+    stats_kernel<KIND><<<grid, wpb * 32, 0, s>>>(b, st, m_pad, scale);
+  }
   PG_CUDA_CHECK(cudaGetLastError());
   return PG_OK;
 }
