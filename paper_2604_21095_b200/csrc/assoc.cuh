@@ -72,6 +72,10 @@ int launch_assoc_packed(const int8_t* qh, const int8_t* q1, const int8_t* q0, in
 // kWideRows), c_pad a multiple of kTileCWide. Three accumulators per tile.
 constexpr int kTileCWide = 160;
 constexpr int kWideRows = 4;
+// BGEN-8 dosages (|u| <= 510) need two base-255 digits: 3 rows per marker (2 digits + missing),
+// 144-row pair tiles (48 markers; 3 x 144 = 432 TMEM columns)
+constexpr int kTileCWide3 = 144;
+constexpr int kWideRows3 = 3;
 int launch_assoc_wide(const int8_t* qh, const int8_t* q1, const int8_t* q0, int64_t p_pad, const int8_t* v,
                       int64_t c_pad, int64_t k_pad, const AssocEpilogue& ep, cudaStream_t stream);
 

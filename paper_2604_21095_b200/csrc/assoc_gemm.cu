@@ -60,7 +60,7 @@ constexpr int kTileCW = kTileCWide;
 constexpr int kHalfCW = kTileCW / 2;
 constexpr int kVBytesW = kHalfCW * kTileK;  // 5 KB
 constexpr int kRowsW = 4;                   // digits 255^0, 255^1, 255^2 + missing row
-constexpr int kPlanes = 0, kFused = 1, kWide = 2;
+constexpr int kPlanes = 0, kFused = 1, kWide = 2, kWide3 = 3;
 constexpr int kEpiWarps = 16;
 constexpr int kFirstEpiWarp = 8;
 constexpr int kThreads = 32 * (kFirstEpiWarp + kEpiWarps);
@@ -75,15 +75,19 @@ constexpr int kTmemCols = 512;
 template <int MODE>
 struct Cfg {
   static constexpr bool FUSED = MODE == kFused;
-  static constexpr bool WIDE = MODE == kWide;
+  static constexpr bool WIDE = MODE == kWide || MODE == kWide3;
   static constexpr int kStages = WIDE ? 7 : 5;
-  // 1 KB-aligned stages
-  static constexpr int kStageBytes = WIDE ? kOffV + kVBytesW : (FUSED ? kOffPacked + 2048 : kOffPacked);
-  static constexpr int kPanelBytes = 3 * kQBytes;
-  static constexpr int kTmaBytes = FUSED ? kPanelBytes : (WIDE ? kOffV + kVBytesW : kOffPacked);  // per CTA
-  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 512 /*barriers*/;
-  static constexpr int kTileRows = WIDE ? kTileCW : kTileC;  // genotype rows per pair tile
+  // genotype rows per pair tile; wide modes: rows per marker
+  static constexpr int kTileRows = MODE == kWide3 ? kTileCWide3 : (WIDE ? kTileCW : kTileC);
   static constexpr int kHalfRows = kTileRows / 2;
+  static constexpr int kWideR = MODE == kWide3 ? kWideRows3 : kRowsW;
+  static constexpr int kVBytesWide = kHalfRows * kTileK;
+  // 1 KB-aligned stages
+  static constexpr int kStageBytes =
+      WIDE ? kOffV + (kVBytesWide + 1023) / 1024 * 1024 : (FUSED ? kOffPacked + 2048 : kOffPacked);
+  static constexpr int kPanelBytes = 3 * kQBytes;
+  static constexpr int kTmaBytes = FUSED ? kPanelBytes : (WIDE ? kOffV + kVBytesWide : kOffPacked);  // per CTA
+  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 512 /*barriers*/;
   static_assert(kStageBytes % 1024 == 0 && kOffV % 512 == 0, "stage / operand alignment (SW64 atoms)");
   static_assert(kTileRows % 16 == 0 && kHalfRows % 8 == 0, "UMMA N and swizzle-atom granularity");
   static_assert(kSmemBytes <= 227 * 1024, "shared memory per CTA");
@@ -208,6 +212,49 @@ __device__ __forceinline__ void epilogue_tile_wide(const AssocEpilogue& ep, uint
         continue;
       }
       epilogue_value(ep, xu, x[3], m, pheno, sc_f, sc_d, cq_f, cq, rb, lane, lanemask_lt, mx);
+    }
+  }
+  if (ep.max_abs_r && !ep.x_accum && pheno < ep.p_valid) atomicMax(ep.max_abs_r + pheno, __float_as_uint(mx));
+}
+
+// BGEN-8 wide tile: per marker rows (digit0, digit1, missing), 12 columns (4 markers) per step
+__device__ __forceinline__ void epilogue_tile_wide3(const AssocEpilogue& ep, uint32_t tA, int ct, int pheno, int lane,
+                                                    int c_begin, int c_end) {
+  constexpr int kR = kWideRows3;
+  constexpr int kMarkersPerTile = kTileCWide3 / kR;
+  const uint32_t lanemask_lt = (1u << lane) - 1u;
+  const float sc_f = ep.scale_f[pheno];
+  const double sc_d = ep.scale_d[pheno];
+  const float cq_f = ep.cq_f[pheno];
+  const long long cq = ep.cq[pheno];
+  const float rb = ep.rbar ? ep.rbar[pheno] : INFINITY;
+  float mx = 0.f;
+#pragma unroll 1
+  for (int c = c_begin; c < c_end; c += 12) {
+    uint32_t a[12], b[12], d[12];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      tmem_ld_32x32b_x4(tA + c + 4 * q, a + 4 * q);
+      tmem_ld_32x32b_x4(tA + kTileCWide3 + c + 4 * q, b + 4 * q);
+      tmem_ld_32x32b_x4(tA + 2 * kTileCWide3 + c + 4 * q, d + 4 * q);
+    }
+    tmem_ld_wait();
+#pragma unroll
+    for (int j = 0; j < 12; j += kR) {
+      long long x[kR];
+#pragma unroll
+      for (int t = 0; t < kR; ++t)
+        x[t] = kWH * static_cast<long long>(static_cast<int>(a[j + t])) + 127ll * static_cast<int>(b[j + t]) +
+               static_cast<int>(d[j + t]);
+      const long long xu = x[0] + 255ll * x[1];
+      const int m = ct * kMarkersPerTile + (c + j) / kR;
+      if (ep.x_accum) {
+        long long* xa = ep.x_accum + (static_cast<int64_t>(m) * ep.x_ld + pheno) * 2;
+        xa[0] += xu;
+        xa[1] += x[2];
+        continue;
+      }
+      epilogue_value(ep, xu, x[2], m, pheno, sc_f, sc_d, cq_f, cq, rb, lane, lanemask_lt, mx);
     }
   }
   if (ep.max_abs_r && !ep.x_accum && pheno < ep.p_valid) atomicMax(ep.max_abs_r + pheno, __float_as_uint(mx));
@@ -443,10 +490,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const uint32_t tH = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16);
       const uint32_t tL = tH + C::kTileRows;
-      // split the tile's 16-column chunks over the 4 column groups
-      constexpr int kChunks = C::kTileRows / 16;
-      const int c0 = 16 * ((cg * kChunks) / 4), c1 = 16 * (((cg + 1) * kChunks) / 4);
-      if constexpr (WIDE) {
+      // split the tile's 16-column chunks over the 4 column groups (12-column = 4-marker
+      // units in the 3-row mode)
+      constexpr int kUnit = MODE == kWide3 ? 12 : 16;
+      constexpr int kChunks = C::kTileRows / kUnit;
+      const int c0 = kUnit * ((cg * kChunks) / 4), c1 = kUnit * (((cg + 1) * kChunks) / 4);
+      if constexpr (MODE == kWide3) {
+        epilogue_tile_wide3(ep, tH, ct, pheno, lane, c0, c1);
+      } else if constexpr (WIDE) {
         epilogue_tile_wide(ep, tH, ct, pheno, lane, c0, c1);
       } else {
         switch (ep.rows_per_marker) {
@@ -536,7 +587,7 @@ int launch_common(const CUtensorMap& tm_qh, const CUtensorMap& tm_q1, const CUte
     // more samples than one int32-exact slice: accumulate int64 partials slice by slice,
     // then derive the statistics (same epilogue arithmetic) from the exact sums
     PG_REQUIRE(ep.x_accum != nullptr && ep.x_ld == p_pad, PG_ERR_INVALID, "assoc: K-sliced run needs x_accum");
-    const int rows = MODE == kWide ? kRowsW : ep.rows_per_marker;
+    const int rows = Cfg<MODE>::WIDE ? Cfg<MODE>::kWideR : ep.rows_per_marker;
     const int64_t m_slots = c_pad / rows;
     PG_CUDA_CHECK(cudaMemsetAsync(ep.x_accum, 0, sizeof(long long) * 2 * m_slots * p_pad, stream));
     for (int kb0 = 0; kb0 < n_kb; kb0 += kSliceKb) {
@@ -596,14 +647,18 @@ int launch_assoc_packed(const int8_t* qh, const int8_t* q1, const int8_t* q0, in
 
 int launch_assoc_wide(const int8_t* qh, const int8_t* q1, const int8_t* q0, int64_t p_pad, const int8_t* v,
                       int64_t c_pad, int64_t k_pad, const AssocEpilogue& ep, cudaStream_t stream) {
-  PG_REQUIRE(p_pad % kTileP == 0 && c_pad % kTileCW == 0 && k_pad % kTileK == 0 && p_pad > 0 && c_pad > 0 &&
+  const int R = ep.rows_per_marker;
+  PG_REQUIRE(R == kRowsW || R == kWideRows3, PG_ERR_INVALID, "assoc(wide): rows_per_marker must be 3 or 4, got %d",
+             R);
+  const int tile = R == kWideRows3 ? kTileCWide3 : kTileCW;
+  PG_REQUIRE(p_pad % kTileP == 0 && c_pad % tile == 0 && k_pad % kTileK == 0 && p_pad > 0 && c_pad > 0 &&
                  k_pad > 0,
              PG_ERR_INVALID, "assoc(wide): bad padded shape p=%lld c=%lld k=%lld", (long long)p_pad,
              (long long)c_pad, (long long)k_pad);
-  PG_REQUIRE(ep.rows_per_marker == kRowsW, PG_ERR_INVALID, "assoc(wide): rows_per_marker must be %d", kRowsW);
   CUtensorMap tm_qh, tm_q1, tm_q0, tm_v;
   PG_CHECK_STATUS(encode_panel(qh, q1, q0, p_pad, k_pad, tm_qh, tm_q1, tm_q0));
-  PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_v, v, k_pad, c_pad, k_pad, kTileK, kHalfCW));
+  PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_v, v, k_pad, c_pad, k_pad, kTileK, tile / 2));
+  if (R == kWideRows3) return launch_common<kWide3>(tm_qh, tm_q1, tm_q0, tm_v, tm_v, p_pad, c_pad, k_pad, ep, stream);
   return launch_common<kWide>(tm_qh, tm_q1, tm_q0, tm_v, tm_v, p_pad, c_pad, k_pad, ep, stream);
 }
 

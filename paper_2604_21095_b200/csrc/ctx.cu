@@ -370,10 +370,11 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
   PG_CHECK_STATUS(geno_stats(b, st, m_cap, s));
   PG_CUDA_CHECK(cudaMemcpyAsync(hflags, c->flags.p, sizeof(int) * 2, cudaMemcpyDeviceToHost, s));
   PG_CUDA_CHECK(cudaStreamSynchronize(s));
-  // dosage sources use the wide-digit GEMM (4 rows per marker) unless disabled for A/B tests
+  // dosage sources use the wide-digit GEMM (3 rows per BGEN-8 marker, 4 otherwise) unless
+  // disabled for A/B tests
   const int R = geno_rows_per_marker(b, hflags[0] != 0, c->wide_digits);
-  const bool wide = R == kWideRows;
-  const int64_t c_pad = round_up(m * R, wide ? kTileCWide : kTileC);
+  const bool wide = R == kWideRows || R == kWideRows3;
+  const int64_t c_pad = round_up(m * R, wide ? (R == kWideRows3 ? kTileCWide3 : kTileCWide) : kTileC);
   // PLINK rows without missing calls: the GEMM decodes the packed codes itself
   const bool fused = c->fused_decode && kind == PG_GENO_BED && R == 1;
   int64_t launches = (kind == PG_GENO_DENSE_F64 ? 2 : 1);

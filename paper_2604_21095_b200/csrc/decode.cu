@@ -36,7 +36,9 @@ bool geno_wide(const GenoBlock& b) {
 }
 
 int geno_rows_per_marker(const GenoBlock& b, bool any_missing, bool allow_wide) {
-  if (allow_wide && geno_wide(b)) return 4;  // base-255 digits (|u| <= 131072 < 127 * (1 + 255 + 255^2)) + missing row
+  // base-255 digits + missing row: BGEN-8 |u| <= 510 < 127 * (1 + 255) needs two digits,
+  // BGEN-16 / real dense |u| <= 131072 < 127 * (1 + 255 + 255^2) three
+  if (allow_wide && geno_wide(b)) return b.kind == PG_GENO_BGEN8 ? 3 : 4;
   switch (b.kind) {
     case PG_GENO_BGEN8: return 8;    // 6 ternary digits (|u| <= 255 < 364) + missing row
     case PG_GENO_BGEN16: return 16;  // 11 digits (|u| <= 65535 < 88573) + missing row
@@ -348,18 +350,18 @@ __global__ void planes_kernel(GenoBlock b, int8_t* __restrict__ v, int8_t* __res
   auto put = [&](int64_t row, const int (&x)[kChunk]) {
     uint4* pv = reinterpret_cast<uint4*>(v + row * k_pad + ci * kChunk);
     *pv = pack16(x, 1);
-    if constexpr (R != 4) {
+    if constexpr (R != 4 && R != 3) {
       uint4* pw = reinterpret_cast<uint4*>(v127 + row * k_pad + ci * kChunk);
       *pw = pack16(x, 127);
     }
   };
-  if constexpr (R == 4) {
-    // wide-digit operand: balanced base-255 digits of u (rows 0..2), missing mask (row 3)
+  if constexpr (R == 4 || R == 3) {
+    // wide-digit operand: balanced base-255 digits of u (rows 0..R-2), missing mask (row R-1)
     int cur[kChunk], t[kChunk];
 #pragma unroll
     for (int i = 0; i < kChunk; ++i) cur[i] = u[i];
 #pragma unroll
-    for (int j = 0; j < 3; ++j) {
+    for (int j = 0; j < R - 1; ++j) {
 #pragma unroll
       for (int i = 0; i < kChunk; ++i) {
         int r = cur[i] % 255;  // in (-255, 255)
@@ -372,7 +374,7 @@ __global__ void planes_kernel(GenoBlock b, int8_t* __restrict__ v, int8_t* __res
     }
 #pragma unroll
     for (int i = 0; i < kChunk; ++i) t[i] = (miss >> i) & 1u;
-    put(base + 3, t);
+    put(base + R - 1, t);
   } else if constexpr (R == 1) {
     put(base, u);
   } else if constexpr (R == 2) {
@@ -495,6 +497,7 @@ int planes_dispatch(const GenoBlock& b, int R, int8_t* v, int8_t* v127, int64_t 
   switch (R) {
     case 1: return planes_launch<KIND, 1>(b, v, v127, c_pad, k_pad, s);
     case 2: return planes_launch<KIND, 2>(b, v, v127, c_pad, k_pad, s);
+    case 3: return planes_launch<KIND, 3>(b, v, v127, c_pad, k_pad, s);
     case 4: return planes_launch<KIND, 4>(b, v, v127, c_pad, k_pad, s);
     case 8: return planes_launch<KIND, 8>(b, v, v127, c_pad, k_pad, s);
     case 16: return planes_launch<KIND, 16>(b, v, v127, c_pad, k_pad, s);

@@ -85,7 +85,7 @@ def test_dense_fractional_dosages(tmp_path):
 @pytest.mark.parametrize("source", ["bgen8", "bgen16", "dense_real"])
 @pytest.mark.parametrize("extension", [False, True])
 def test_wide_digits_equal_ternary_bitwise(source, extension, tmp_path, monkeypatch):
-    """Wide-digit GEMM (base-255 digits, 3 accumulators, N=128) and the balanced-ternary
+    """Wide-digit GEMM (base-255 digits, 3 accumulators; 3 rows per BGEN-8 marker, 4 otherwise) and the balanced-ternary
     planes are two exact integer contractions of the same codes: FULL output identical."""
     rng = np.random.default_rng(77)
     n, m = 130, 70
@@ -108,6 +108,27 @@ def test_wide_digits_equal_ternary_bitwise(source, extension, tmp_path, monkeypa
     kw = dict(source=spec, pheno_path=pheno, covar_path=covar, output_mode=pg.OutputMode.FULL,
               precision=pg.Precision.F64, summary_to_stderr=False, device_batch=40,
               residualize_genotypes=extension, df_mode=pg.DfMode.ADJUSTED if extension else pg.DfMode.PAPER_N_MINUS_2)
+    pg.run_scan(pg.ScanConfig(out_path=tmp_path / "wide.bin", **kw))
+    monkeypatch.setenv("PANELGWAS_WIDE_DIGITS", "0")
+    pg.run_scan(pg.ScanConfig(out_path=tmp_path / "tern.bin", **kw))
+    assert (tmp_path / "wide.bin").read_bytes() == (tmp_path / "tern.bin").read_bytes()
+
+
+def test_wide3_k_sliced_equals_ternary_bitwise(tmp_path, monkeypatch):
+    """BGEN-8 at N = 140,000 (> one int32-exact K slice): the 3-row wide GEMM accumulates
+    int64 partials slice by slice; FULL output equals the ternary planes' bit for bit."""
+    from bgen_fixture import write_bgen
+
+    rng = np.random.default_rng(140)
+    n, m = 140_000, 9
+    ids = [f"S{i + 1}" for i in range(n)]
+    d = rng.uniform(0, 2, (m, n))
+    d[rng.random(d.shape) < 0.05] = np.nan
+    y = rng.standard_normal((n, 3))
+    pheno = write_tsv(tmp_path / "p.tsv", ids, ["a", "b", "c"], y)
+    spec = pg.SourceSpec(pg.GenotypeFormat.BGEN, bgen_path=write_bgen(tmp_path / "g.bgen", d, ids, bits=8))
+    kw = dict(source=spec, pheno_path=pheno, output_mode=pg.OutputMode.FULL, precision=pg.Precision.F64,
+              summary_to_stderr=False)
     pg.run_scan(pg.ScanConfig(out_path=tmp_path / "wide.bin", **kw))
     monkeypatch.setenv("PANELGWAS_WIDE_DIGITS", "0")
     pg.run_scan(pg.ScanConfig(out_path=tmp_path / "tern.bin", **kw))
