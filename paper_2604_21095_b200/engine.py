@@ -331,30 +331,44 @@ def run_scan(config: ScanConfig, marker_range: tuple[int, int] | None = None, pa
     `panel_hook(ctx, prep)` (NCCL broadcast from rank 0) instead of uploading it, and the host
     panel metadata through `prep_hook(source)` (rank 0 parses the tables for everyone).
     """
+    from ._device import DeviceContext
+
     wall0 = time.perf_counter()
     config.validate()
-    source = open_genotype_source(config.source)
+    # CUDA context creation (0.5-2 s) overlaps opening the source (the BGEN index) and parsing
+    # the tables; every C-ABI entry selects the ctx's device itself, so the handle may be
+    # created on another thread
+    init = ThreadPoolExecutor(max_workers=1)
+    ctx_fut = init.submit(DeviceContext, config.device)
     try:
-        return _run_scan_open(config, source, wall0, marker_range, panel_hook, prep_hook)
+        source = open_genotype_source(config.source)
+    except BaseException:
+        init.shutdown(wait=False)
+        _close_when_done(ctx_fut)
+        raise
+    try:
+        return _run_scan_open(config, source, wall0, init, ctx_fut, marker_range, panel_hook, prep_hook)
     finally:
         source.close()
 
 
-def _run_scan_open(config: ScanConfig, source, wall0: float, marker_range=None, panel_hook=None,
-                   prep_hook=None) -> ScanSummary:
-    from ._device import DeviceContext
+def _close_when_done(ctx_fut) -> None:
+    try:
+        ctx_fut.result().close()
+    except Exception:
+        pass
 
-    # CUDA context creation (~0.5 s) and the pinned read ring (~0.4 s per GB) overlap the host
-    # table parsing; every C-ABI entry selects the ctx's device itself, so the handle may be
-    # created on another thread
+
+def _run_scan_open(config: ScanConfig, source, wall0: float, init, ctx_fut, marker_range=None, panel_hook=None,
+                   prep_hook=None) -> ScanSummary:
+    # the pinned read ring (~0.4 s per GB) is allocated on the init thread after the context,
+    # also while the tables parse
     lo, hi = marker_range if marker_range is not None else (0, source.n_markers)
     compressed = hasattr(source, "read_compressed_block") and os.environ.get("PANELGWAS_HOST_INFLATE") != "1"
     row_bytes = (source.compressed_bytes_per_marker if compressed
                  else getattr(source, "bytes_per_marker", 0))
     # the batch only shrinks as phenotypes are added, so one phenotype bounds every ring slot
     ring_bytes = device_batch_size(config, max(hi - lo, 1), 1, source.n_samples) * row_bytes
-    init = ThreadPoolExecutor(max_workers=1)
-    ctx_fut = init.submit(DeviceContext, config.device)
     ring_fut = init.submit(_pinned_buffers, [ring_bytes] * 3 if ring_bytes else [])
     init.shutdown(wait=False)
     try:

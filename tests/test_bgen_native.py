@@ -152,3 +152,31 @@ def test_matches_reference_reader(tmp_path):
             got = orc.decode_bgen(rows[i, :w].view("u1" if bits == 8 else "<u2"), rows[i, w:], bits)
             assert np.array_equal(got, want[i], equal_nan=True)
         ref.close()
+
+
+def test_bgen_catalog_ids_and_utf8(tmp_path):
+    """The byte-backed BGEN catalog: id = rsid, else the variant id; UTF-8 identifiers and
+    alleles survive into records and record prefixes."""
+    import struct
+    import zlib
+
+    from paper_2604_21095_b200.genotypes.bgen import BgenSource
+
+    n = 3
+
+    def variant(vid, rsid, chrom, pos, a1, a2):
+        data = struct.pack("<IHBB", n, 2, 2, 2) + bytes([2] * n) + bytes([0, 8]) + bytes([255, 0] * n)
+        comp = zlib.compress(data)
+        return (struct.pack("<H", len(vid)) + vid + struct.pack("<H", len(rsid)) + rsid + struct.pack("<H", len(chrom))
+                + chrom + struct.pack("<IH", pos, 2) + struct.pack("<I", len(a1)) + a1 + struct.pack("<I", len(a2)) + a2
+                + struct.pack("<II", len(comp) + 4, len(data)) + comp)
+
+    body = [variant(b"v1", b"", b"1", 10, b"A", b"G"), variant(b"v2", b"rs2", "Xé".encode(), 20, b"AT", "α".encode()),
+            variant(b"", b"", b"2", 30, b"C", b"T")]
+    path = tmp_path / "u.bgen"
+    path.write_bytes(struct.pack("<I", 20) + struct.pack("<III", 20, 3, n) + b"bgen" + struct.pack("<I", 1 | 2 << 2)
+                     + b"".join(body))
+    src = BgenSource(path, sample_ids=["a", "b", "c"])
+    assert [(m.chrom, m.id, m.pos, m.allele1, m.allele2) for m in src.marker_catalog] == [
+        ("1", "v1", 10, "A", "G"), ("Xé", "rs2", 20, "AT", "α"), ("2", "", 30, "C", "T")]
+    assert src.marker_catalog[1:2].prefixes(False) == ["Xé\trs2\t20\tα\tAT\t"]

@@ -409,7 +409,7 @@ def test_marker_catalog_behaves_like_the_reference_list():
     "1\trs1\t0\tten\tA\tG\n",                     # bad position
 ])
 def test_native_bim_index_equals_line_reader(tmp_path, text):
-    """pg_bim_index + BimCatalog give the line-by-line reader's catalog, or defer to it."""
+    """pg_bim_index + ByteCatalog give the line-by-line reader's catalog, or defer to it."""
     from paper_2604_21095_b200.errors import FormatError
     from paper_2604_21095_b200.genotypes import plink
 
