@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <thread>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -196,6 +197,8 @@ struct pg_ctx {
   pg::DBuf<long long> bgen_diag[2];
   pg::DBuf<unsigned long long> bgen_summary[2];
   void* bgen_host[2] = {nullptr, nullptr};  // pinned copies of the validation summaries
+  void* h2d_stage[2] = {nullptr, nullptr};   // pinned bounce buffers for large pageable uploads
+  cudaEvent_t h2d_ev[2] = {nullptr, nullptr};
   int64_t bgen_pending[2] = {0, 0};         // batch size begun but not ended, per slot
   int64_t stage_m[2] = {0, 0};
   int64_t stage_pitch[2] = {0, 0};
@@ -605,6 +608,9 @@ int pg_ctx_destroy(pg_ctx* c) {
     if (c->stage_ev[i]) cudaEventDestroy(c->stage_ev[i]);
     if (c->slot_free_ev[i]) cudaEventDestroy(c->slot_free_ev[i]);
     if (c->bgen_host[i]) cudaFreeHost(c->bgen_host[i]);
+    if (c->h2d_ev[i]) cudaEventSynchronize(c->h2d_ev[i]);
+    if (c->h2d_stage[i]) cudaFreeHost(c->h2d_stage[i]);
+    if (c->h2d_ev[i]) cudaEventDestroy(c->h2d_ev[i]);
   }
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -644,6 +650,48 @@ int pg_ctx_set_panel(pg_ctx* c, const double* ytil, int64_t n_kept, int64_t n_ph
   return PG_OK;
 }
 
+namespace {
+
+// Host -> device copy of a large pageable buffer: 64 MB chunks are copied into two pinned
+// bounce buffers by several host threads (one memcpy thread cannot feed the link) while
+// the previous chunk's H2D runs on `s`. Already page-locked sources go straight through.
+int upload_pageable(pg_ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  constexpr size_t kChunk = size_t{64} << 20;
+  cudaPointerAttributes attr{};
+  const bool pinned = cudaPointerGetAttributes(&attr, src) == cudaSuccess && attr.type == cudaMemoryTypeHost;
+  cudaGetLastError();  // a pageable pointer may leave an error behind on older drivers
+  if (pinned || bytes < 2 * kChunk) {
+    PG_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+    return PG_OK;
+  }
+  for (int i = 0; i < 2; ++i) {
+    if (c->h2d_stage[i] == nullptr) PG_CUDA_CHECK(cudaHostAlloc(&c->h2d_stage[i], kChunk, cudaHostAllocDefault));
+    if (c->h2d_ev[i] == nullptr) PG_CUDA_CHECK(cudaEventCreateWithFlags(&c->h2d_ev[i], cudaEventDisableTiming));
+  }
+  const int nt = static_cast<int>(std::max(1u, std::min(8u, std::thread::hardware_concurrency() / 2)));
+  const char* from = static_cast<const char*>(src);
+  char* to = static_cast<char*>(dst);
+  int k = 0;
+  for (size_t off = 0; off < bytes; off += kChunk, k ^= 1) {
+    const size_t len = std::min(kChunk, bytes - off);
+    PG_CUDA_CHECK(cudaEventSynchronize(c->h2d_ev[k]));  // this bounce buffer's previous H2D is done
+    char* stage = static_cast<char*>(c->h2d_stage[k]);
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t) {
+      th.emplace_back([=] {
+        const size_t a = len * t / nt, b = len * (t + 1) / nt;
+        std::memcpy(stage + a, from + off + a, b - a);
+      });
+    }
+    for (auto& x : th) x.join();
+    PG_CUDA_CHECK(cudaMemcpyAsync(to + off, stage, len, cudaMemcpyHostToDevice, s));
+    PG_CUDA_CHECK(cudaEventRecord(c->h2d_ev[k], s));
+  }
+  return PG_OK;
+}
+
+}  // namespace
+
 int pg_ctx_prepare_panel(pg_ctx* c, const double* y, int64_t n_kept, int64_t n_pheno, int64_t ld,
                          const double* basis_q, int64_t rank, uint8_t* zero_variance, double* sd) {
   PG_CHECK_STATUS(ctx_check(c));
@@ -654,7 +702,7 @@ int pg_ctx_prepare_panel(pg_ctx* c, const double* y, int64_t n_kept, int64_t n_p
   cudaStream_t s = c->stream;
   PG_CHECK_STATUS(c->ystage.ensure(static_cast<size_t>(n_kept) * n_pheno));
   if (ld == n_pheno) {
-    PG_CUDA_CHECK(cudaMemcpyAsync(c->ystage.p, y, sizeof(double) * n_pheno * n_kept, cudaMemcpyHostToDevice, s));
+    PG_CHECK_STATUS(upload_pageable(c, c->ystage.p, y, sizeof(double) * n_pheno * n_kept, s));
   } else {
     PG_CUDA_CHECK(cudaMemcpy2DAsync(c->ystage.p, sizeof(double) * n_pheno, y, sizeof(double) * ld,
                                     sizeof(double) * n_pheno, n_kept, cudaMemcpyHostToDevice, s));
