@@ -403,21 +403,31 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
         break;
       }
       __syncwarp();  // earlier literals / copies by other lanes are visible
-      // an overlapping match repeats the last `distance` bytes: source offset j mod distance
-      // (j < 258: a float reciprocal gives the quotient within one, fixed up exactly)
-      const float inv_d = __frcp_rn(static_cast<float>(distance));
       const bool from_ring = distance <= kRingSafe;
-      for (int j = lane; j < length; j += 32) {
-        int jj = j;
-        if (distance < length) {
-          jj = j - distance * __float2int_rz(static_cast<float>(j) * inv_d);
-          jj += jj < 0 ? distance : 0;
-          jj -= jj >= distance ? distance : 0;
+      if (length <= 32 && distance >= length) {
+        // the common short match: one step, every source byte already written
+        if (lane < length) {
+          const int src = pos - distance + lane;
+          const uint8_t v = from_ring ? sm.ring[src & (kRing - 1)] : dst[src];
+          dst[pos + lane] = v;
+          sm.ring[(pos + lane) & (kRing - 1)] = v;
         }
-        const int src = pos - distance + jj;
-        const uint8_t v = from_ring ? sm.ring[src & (kRing - 1)] : dst[src];
-        dst[pos + j] = v;
-        sm.ring[(pos + j) & (kRing - 1)] = v;
+      } else {
+        // an overlapping match repeats the last `distance` bytes: source offset j mod distance
+        // (j < 258: a float reciprocal gives the quotient within one, fixed up exactly)
+        const float inv_d = __frcp_rn(static_cast<float>(distance));
+        for (int j = lane; j < length; j += 32) {
+          int jj = j;
+          if (distance < length) {
+            jj = j - distance * __float2int_rz(static_cast<float>(j) * inv_d);
+            jj += jj < 0 ? distance : 0;
+            jj -= jj >= distance ? distance : 0;
+          }
+          const int src = pos - distance + jj;
+          const uint8_t v = from_ring ? sm.ring[src & (kRing - 1)] : dst[src];
+          dst[pos + j] = v;
+          sm.ring[(pos + j) & (kRing - 1)] = v;
+        }
       }
       pos += length;
       // no barrier here: the next match's __syncwarp orders these writes before its reads
