@@ -19,6 +19,7 @@
 // streams are reported per stream (status != 0); the caller re-inflates that one block
 // with host zlib to raise zlib's own message.
 #include <cstdint>
+#include <cstdlib>
 
 #include "inflate.cuh"
 
@@ -28,7 +29,6 @@ namespace {
 constexpr int kLitBits = 10;
 constexpr int kDistBits = 8;
 constexpr int kClenBits = 7;
-constexpr int kWarpsPerBlock = 4;
 constexpr int kRing = 2048;             // bytes of recent output mirrored in smem
 constexpr int kRingSafe = kRing - 258;  // a copy never overwrites its own sources
 
@@ -115,9 +115,9 @@ struct Bits {
 
 // zlib's completeness rules (inflate_table): over-subscribed -> error; an incomplete code
 // only for a single code of length 1 (lit/len, dist); never for code-length codes.
-template <class Enc, int BITS, int NSYM, class T>
+template <int L, class Enc, int BITS, int NSYM, class T>
 __device__ bool build(Table<BITS, NSYM, T>& t, const uint8_t* lens, int n, uint16_t* codes, bool code_lengths,
-                      int lane) {
+                      int lane, unsigned mask) {
   uint16_t count[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) count[i] = 0;
@@ -149,9 +149,9 @@ __device__ bool build(Table<BITS, NSYM, T>& t, const uint8_t* lens, int n, uint1
       }
     }
   }
-  for (int i = lane; i < (1 << BITS); i += 32) t.lut[i] = 0;
-  __syncwarp();
-  for (int s = lane; s < n; s += 32) {
+  for (int i = lane; i < (1 << BITS); i += L) t.lut[i] = 0;
+  __syncwarp(mask);
+  for (int s = lane; s < n; s += L) {
     const int l = lens[s];
     if (l == 0 || l > BITS) continue;
     // codes are read LSB first: index the table by the bit-reversed code
@@ -159,7 +159,7 @@ __device__ bool build(Table<BITS, NSYM, T>& t, const uint8_t* lens, int n, uint1
     const T e = static_cast<T>(Enc::enc(s, l));
     for (uint32_t i = rev; i < (1u << BITS); i += 1u << l) t.lut[i] = e;
   }
-  __syncwarp();
+  __syncwarp(mask);
   return true;
 }
 
@@ -194,16 +194,22 @@ __device__ __forceinline__ uint32_t decode(Bits& br, const Table<BITS, NSYM, T>&
   return s < 0 ? 0u : Enc::enc(s, 1);  // bits already consumed; only the fields matter
 }
 
-__global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint8_t* __restrict__ blob,
+// L lanes decode one stream: L = 32 (a warp per stream, the default) or 16 (two streams per
+// warp; the two half-warps share an instruction only while their streams take the same branch).
+// Blocks hold 4 streams either way (27 KB of static shared memory).
+template <int L>
+__global__ void __launch_bounds__(4 * L) inflate_kernel(const uint8_t* __restrict__ blob,
                                                                      const int64_t* __restrict__ off,
                                                                      const int64_t* __restrict__ len, int64_t count,
                                                                      int64_t skip, uint8_t* __restrict__ out,
                                                                      int64_t out_stride, int64_t* __restrict__ out_len,
                                                                      int* __restrict__ status) {
-  __shared__ WarpSmem sm_all[kWarpsPerBlock];
-  const int lane = threadIdx.x & 31;
-  WarpSmem& sm = sm_all[threadIdx.x >> 5];
-  const int64_t stream = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
+  constexpr int kStreams = 4;
+  __shared__ WarpSmem sm_all[kStreams];
+  const int lane = threadIdx.x & (L - 1);
+  const unsigned mask = L == 32 ? 0xffffffffu : (0xffffu << (threadIdx.x & 16));
+  WarpSmem& sm = sm_all[threadIdx.x / L];
+  const int64_t stream = static_cast<int64_t>(blockIdx.x) * kStreams + threadIdx.x / L;
   if (stream >= count) return;
 
   const uint8_t* start = blob + off[stream] + skip;
@@ -257,7 +263,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
         err = 2;
         break;
       }
-      for (uint32_t j = lane; j < n; j += 32) {
+      for (uint32_t j = lane; j < n; j += L) {
         const uint8_t v = b8[byte_pos + 4 + j];
         dst[pos + j] = v;
         sm.ring[(pos + j) & (kRing - 1)] = v;
@@ -271,14 +277,14 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
       br.refill();
       br.refill();
       br.get(next_bit & 31);
-      __syncwarp();
+      __syncwarp(mask);
       continue;
     }
     if (type == 1) {
-      for (int s = lane; s < 320; s += 32) sm.lens[s] = s < 144 ? 8 : s < 256 ? 9 : s < 280 ? 7 : s < 288 ? 8 : 5;
-      __syncwarp();
-      build<EncLit>(sm.lit, sm.lens, 288, sm.codes, false, lane);
-      build<EncDist>(sm.dist, sm.lens + 288, 32, sm.codes, false, lane);  // 30, 31 complete the code, never valid
+      for (int s = lane; s < 320; s += L) sm.lens[s] = s < 144 ? 8 : s < 256 ? 9 : s < 280 ? 7 : s < 288 ? 8 : 5;
+      __syncwarp(mask);
+      build<L, EncLit>(sm.lit, sm.lens, 288, sm.codes, false, lane, mask);
+      build<L, EncDist>(sm.dist, sm.lens + 288, 32, sm.codes, false, lane, mask);  // 30, 31 complete the code, never valid
     } else {
       const int hlit = br.get(5) + 257, hdist = br.get(5) + 1, hclen = br.get(4) + 4;
       if (hlit > 286 || hdist > 30) {
@@ -293,9 +299,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
         if (i == 10) br.refill();
         cl[c_clen_order[i]] = static_cast<uint8_t>(br.get(3));
       }
-      if (lane < 19) sm.lens[lane] = cl[lane];
-      __syncwarp();
-      if (!build<EncClen>(sm.clen, sm.lens, 19, sm.codes, true, lane)) {
+      for (int i = lane; i < 19; i += L) sm.lens[i] = cl[i];
+      __syncwarp(mask);
+      if (!build<L, EncClen>(sm.clen, sm.lens, 19, sm.codes, true, lane, mask)) {
         err = 1;
         break;
       }
@@ -335,7 +341,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
           err = 1;
           break;
         }
-        for (int j = lane; j < rep; j += 32) sm.lens[idx + j] = val;
+        for (int j = lane; j < rep; j += L) sm.lens[idx + j] = val;
         idx += rep;
         prev = val;
       }
@@ -343,16 +349,20 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
         err = 1;
         break;
       }
-      __syncwarp();
-      if (sm.lens[256] == 0 || !build<EncLit>(sm.lit, sm.lens, hlit, sm.codes, false, lane)) {
+      __syncwarp(mask);
+      if (sm.lens[256] == 0 || !build<L, EncLit>(sm.lit, sm.lens, hlit, sm.codes, false, lane, mask)) {
         err = 1;
         break;
       }
-      const uint8_t dl = lane < hdist ? sm.lens[hlit + lane] : 0;  // ranges may overlap
-      __syncwarp();
-      if (lane < hdist) sm.lens[288 + lane] = dl;
-      __syncwarp();
-      if (!build<EncDist>(sm.dist, sm.lens + 288, hdist, sm.codes, false, lane)) {
+      uint8_t dl[32 / L];  // the ranges may overlap: read everything before writing
+#pragma unroll
+      for (int q = 0; q < 32 / L; ++q) dl[q] = lane + q * L < hdist ? sm.lens[hlit + lane + q * L] : 0;
+      __syncwarp(mask);
+#pragma unroll
+      for (int q = 0; q < 32 / L; ++q)
+        if (lane + q * L < hdist) sm.lens[288 + lane + q * L] = dl[q];
+      __syncwarp(mask);
+      if (!build<L, EncDist>(sm.dist, sm.lens + 288, hdist, sm.codes, false, lane, mask)) {
         err = 1;
         break;
       }
@@ -402,9 +412,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
         err = 2;
         break;
       }
-      __syncwarp();  // earlier literals / copies by other lanes are visible
+      __syncwarp(mask);  // earlier literals / copies by other lanes are visible
       const bool from_ring = distance <= kRingSafe;
-      if (length <= 32 && distance >= length) {
+      if (length <= L && distance >= length) {
         // the common short match: one step, every source byte already written
         if (lane < length) {
           const int src = pos - distance + lane;
@@ -416,7 +426,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
         // an overlapping match repeats the last `distance` bytes: source offset j mod distance
         // (j < 258: a float reciprocal gives the quotient within one, fixed up exactly)
         const float inv_d = __frcp_rn(static_cast<float>(distance));
-        for (int j = lane; j < length; j += 32) {
+        for (int j = lane; j < length; j += L) {
           int jj = j;
           if (distance < length) {
             jj = j - distance * __float2int_rz(static_cast<float>(j) * inv_d);
@@ -441,7 +451,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
     } else {
       const uint32_t want = (static_cast<uint32_t>(b8[byte_pos]) << 24) | (b8[byte_pos + 1] << 16) |
                             (b8[byte_pos + 2] << 8) | b8[byte_pos + 3];
-      __syncwarp();
+      __syncwarp(mask);
       // A = 1 + sum d_k, B = pos + sum (pos - k) d_k = pos + pos * S1 - sum k d_k. Lanes read
       // coalesced 4-byte words (byte sums and 0..3-weighted byte sums by DP4A); the unaligned
       // head and the tail are done bytewise.
@@ -450,19 +460,19 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
       head = min(head, pos);
       const int32_t n_words = (pos - head) >> 2;
       const int32_t tail = head + 4 * n_words;
-      for (int32_t k = lane; k < head; k += 32) {
+      for (int32_t k = lane; k < head; k += L) {
         const uint32_t d = dst[k];
         s1 += d;
         t += static_cast<unsigned long long>(k) * d;
       }
-      for (int32_t k = tail + lane; k < pos; k += 32) {
+      for (int32_t k = tail + lane; k < pos; k += L) {
         const uint32_t d = dst[k];
         s1 += d;
         t += static_cast<unsigned long long>(k) * d;
       }
       const uint32_t* words = reinterpret_cast<const uint32_t*>(dst + head);
       uint32_t s1w = 0;  // <= 69 KB x 255 per lane: fits
-      for (int32_t w = lane; w < n_words; w += 32) {
+      for (int32_t w = lane; w < n_words; w += L) {
         const uint32_t x = words[w];
         const uint32_t sb = __dp4a(x, 0x01010101u, 0u);
         s1w += sb;
@@ -470,9 +480,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
       }
       s1 += s1w;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-        t += __shfl_xor_sync(0xffffffffu, t, o);
+      for (int o = L / 2; o > 0; o >>= 1) {
+        s1 += __shfl_xor_sync(mask, s1, o);
+        t += __shfl_xor_sync(mask, t, o);
       }
       const unsigned long long s2 = static_cast<unsigned long long>(pos) * s1 - t;
       const uint32_t A = static_cast<uint32_t>((1 + s1) % 65521ull);
@@ -491,9 +501,20 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) inflate_kernel(const uint
 int inflate_streams(const uint8_t* d_blob, const int64_t* d_off, const int64_t* d_len, int64_t count, int64_t skip,
                     uint8_t* d_out, int64_t out_stride, int64_t* d_out_len, int* d_status, cudaStream_t s) {
   if (count <= 0) return PG_OK;
-  const unsigned blocks = static_cast<unsigned>((count + kWarpsPerBlock - 1) / kWarpsPerBlock);
-  inflate_kernel<<<blocks, 32 * kWarpsPerBlock, 0, s>>>(d_blob, d_off, d_len, count, skip, d_out, out_stride,
-                                                        d_out_len, d_status);
+  // PG_INFLATE_LANES=16: two streams per warp (A/B switch; measured 10 % slower on C5: the
+  // half-warps diverge on literal / match often enough to lose the shared issue slots)
+  static const int lanes = [] {
+    const char* e = std::getenv("PG_INFLATE_LANES");
+    return e && std::atoi(e) == 16 ? 16 : 32;
+  }();
+  const unsigned blocks = static_cast<unsigned>((count + 3) / 4);  // 4 streams per block
+  if (lanes == 16) {
+    inflate_kernel<16><<<blocks, 64, 0, s>>>(d_blob, d_off, d_len, count, skip, d_out, out_stride, d_out_len,
+                                            d_status);
+  } else {
+    inflate_kernel<32><<<blocks, 128, 0, s>>>(d_blob, d_off, d_len, count, skip, d_out, out_stride, d_out_len,
+                                             d_status);
+  }
   PG_CUDA_CHECK(cudaGetLastError());
   return PG_OK;
 }
