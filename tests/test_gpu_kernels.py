@@ -131,7 +131,8 @@ def test_correlate_handworked_and_row_stable():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("n,p,n_cov", [(300, 12, 3), (2000, 64, 10), (5000, 700, 20), (1100, 33, 0)])
+@pytest.mark.parametrize("n,p,n_cov", [(300, 12, 3), (2000, 64, 10), (5000, 700, 20), (1100, 33, 0),
+                                       (12000, 1601, 5)])  # 154 MB: chunked pinned upload
 def test_device_panel_prep_matches_host(n, p, n_cov):
     """pg_ctx_prepare_panel == kernel.residualize + standardize_columns (reference
     kernel.py:310-347) to 1e-12 relative, flags identical; commit == set_panel on the
