@@ -62,6 +62,16 @@ def write_bed(prefix: Path, n: int, m: int, seed: int) -> None:
         fh.writelines(f"F{i + 1}\tS{i + 1}\t0\t0\t0\t-9\n" for i in range(n))
 
 
+def write_inputs(d: Path, n: int, p: int, a) -> None:
+    ids = [f"S{i + 1}" for i in range(n)]
+    write_bed(d / "geno", n, a.markers, a.seed)
+    rng = np.random.default_rng(a.seed + 1)
+    c = rng.standard_normal((n, a.covariates))
+    y = c @ (0.1 * rng.standard_normal((a.covariates, p))) + rng.standard_normal((n, p))
+    write_repr_tsv(d / "covar.tsv", ids, [f"c{j + 1}" for j in range(a.covariates)], c)
+    write_repr_tsv(d / "pheno.tsv", ids, [f"ph{j + 1}" for j in range(p)], y)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--dir", default="/tmp/c3")
@@ -72,24 +82,21 @@ def main():
     ap.add_argument("--seed", type=int, default=3)
     ap.add_argument("--top-k", type=int, default=0, help="TOPK mode with this k instead of THRESHOLD p <= 1e-4")
     ap.add_argument("--full", action="store_true", help="FULL mode (f32 t matrix) instead of THRESHOLD")
+    ap.add_argument("--reuse", action="store_true", help="keep the input files of a previous run in --dir")
+    ap.add_argument("--extra", default="", help="extra CLI flags for `panelgwas run` (space-separated)")
     a = ap.parse_args()
     d = Path(a.dir)
     d.mkdir(parents=True, exist_ok=True)
     n, p = a.samples, a.phenotypes
-    ids = [f"S{i + 1}" for i in range(n)]
     t0 = time.perf_counter()
-    write_bed(d / "geno", n, a.markers, a.seed)
-    rng = np.random.default_rng(a.seed + 1)
-    c = rng.standard_normal((n, a.covariates))
-    y = c @ (0.1 * rng.standard_normal((a.covariates, p))) + rng.standard_normal((n, p))
-    write_repr_tsv(d / "covar.tsv", ids, [f"c{j + 1}" for j in range(a.covariates)], c)
-    write_repr_tsv(d / "pheno.tsv", ids, [f"ph{j + 1}" for j in range(p)], y)
+    if not (a.reuse and (d / "geno.bed").exists() and (d / "pheno.tsv").exists()):
+        write_inputs(d, n, p, a)
     t_write = time.perf_counter() - t0
     sizes = {f: os.path.getsize(d / f) for f in ("geno.bed", "pheno.tsv", "covar.tsv")}
     cmd = [sys.executable, "-m", "paper_2604_21095_b200", "run", "--bfile", str(d / "geno"), "--pheno",
            str(d / "pheno.tsv"), "--covar", str(d / "covar.tsv"),
            *(["--full", "--allow-large-full"] if a.full else ["--top-k", str(a.top_k)] if a.top_k
-             else ["--p-threshold", "1e-4"]), "--out", str(d / "hits.tsv")]
+             else ["--p-threshold", "1e-4"]), *a.extra.split(), "--out", str(d / "hits.tsv")]
     for old in d.glob("hits.tsv*"):  # a rewrite of an existing file costs extra (truncate + flush on close)
         old.unlink()
     t0 = time.perf_counter()
@@ -101,7 +108,7 @@ def main():
         raise SystemExit(res.returncode)
     summary = json.loads((d / "hits.tsv.summary.json").read_text())
     tests = summary["markers_scanned"] * summary["phenotypes_scanned"]
-    mode = "FULL f32" if a.full else f"TOPK k={a.top_k}" if a.top_k else "p<=1e-4"
+    mode = ("FULL f32" if a.full else f"TOPK k={a.top_k}" if a.top_k else "p<=1e-4") + (f" {a.extra}" if a.extra else "")
     line = {"workload": f"C3 via CLI: N={n:,} M={a.markers:,} P={p:,} + {a.covariates} covariates, {mode}",
             "wall_s": wall, "tests": tests, "tests_per_s_wall": tests / wall, "records": summary["records_emitted"],
             "file_bytes": {**sizes, "out": os.path.getsize(d / "hits.tsv")}, "write_inputs_s": t_write,
