@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import csv
 import mmap
+import os
 from ctypes import byref, c_int64
 from pathlib import Path
 
@@ -77,7 +78,9 @@ def _native_body(path: Path, mm, addr: int, size: int, body_at: int, width: int,
 
     lib = _native.load_library()
     rows, err_line, err_cells = c_int64(0), c_int64(0), c_int64(0)
-    fixed = (addr, size, body_at, delimiter.encode(), width, at, 0, 2)
+    # leave two cores to the CUDA context creation that runs concurrently (engine.run_scan)
+    threads = max(1, (os.cpu_count() or 4) - 2)
+    fixed = (addr, size, body_at, delimiter.encode(), width, at, threads, 2)
 
     def run(*outputs) -> bool:
         status = lib.pg_table_parse(*fixed, byref(rows), *outputs, byref(err_line), byref(err_cells))
