@@ -202,6 +202,9 @@ struct pg_ctx {
   int64_t bgen_pending[2] = {0, 0};         // batch size begun but not ended, per slot
   int64_t stage_m[2] = {0, 0};
   int64_t stage_pitch[2] = {0, 0};
+  const uint8_t* stage_data[2] = {nullptr, nullptr};  // staged rows (stage_buf, or the inflated BGEN-8 blocks)
+  int64_t stage_probs_off[2] = {0, 0};
+  int64_t stage_ploidy_off[2] = {-1, -1};
   pg::DBuf<long long> n_miss, s_u, ss_u;
   pg::DBuf<double> sum_d, af, var, mu_d, invd_d;
   pg::DBuf<float> mu_f, invd_f;
@@ -322,7 +325,8 @@ int64_t expected_row_bytes(int kind, int64_t n_src) {
   }
 }
 
-int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t pitch, pg_batch_info* info) {
+int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t pitch, pg_batch_info* info,
+                int64_t probs_off = 0, int64_t ploidy_off = -1) {
   PG_REQUIRE(c->have_panel, PG_ERR_STATE, "pg_scan: no panel uploaded (pg_ctx_set_panel)");
   PG_REQUIRE(c->have_scan, PG_ERR_STATE, "pg_scan: scan parameters not set (pg_ctx_set_scan)");
   PG_REQUIRE(m >= 1, PG_ERR_INVALID, "pg_scan: empty batch");
@@ -338,6 +342,8 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
   b.n_kept = c->n_kept;
   b.keep_bits = c->keep_bits.p;
   b.all_kept = c->n_kept == c->n_src ? 1 : 0;
+  b.probs_off = probs_off;
+  b.ploidy_off = ploidy_off;
 
   // marker slots for any tiling: ternary tiles hold 256 / R markers, wide tiles 40
   const int64_t m_cap = round_up(m, 256) + 64;
@@ -972,6 +978,9 @@ int pg_stage(pg_ctx* c, int slot, int kind, const void* data, int64_t n_markers,
                               c->copy_stream));
   PG_CUDA_CHECK(cudaEventRecord(c->stage_ev[slot], c->copy_stream));
   c->stage_kind[slot] = kind;
+  c->stage_data[slot] = c->stage_buf[slot].p;
+  c->stage_probs_off[slot] = 0;
+  c->stage_ploidy_off[slot] = -1;
   c->stage_m[slot] = n_markers;
   c->stage_pitch[slot] = pitch;
   return PG_OK;
@@ -1050,6 +1059,16 @@ int pg_stage_bgen_end(pg_ctx* c, int slot, int64_t* diag) {
   const bool wide16 = (summary[1] & 2ull) != 0;
   const int64_t row_bytes = wide16 ? 5 * n : 3 * n;
   const int64_t pitch = round_up(row_bytes, 16);
+  c->stage_kind[slot] = wide16 ? PG_GENO_BGEN16 : PG_GENO_BGEN8;
+  c->stage_m[slot] = count;
+  if (!wide16) {
+    // all-8-bit batch: the decoders read the inflated blocks in place (no repack pass)
+    c->stage_data[slot] = c->bgen_raw[slot].p;
+    c->stage_pitch[slot] = raw_stride;
+    c->stage_probs_off[slot] = 10 + n;
+    c->stage_ploidy_off[slot] = 8;
+    return PG_OK;
+  }
   cudaStream_t cs = c->copy_stream;
   if (c->stage_buf[slot].cap < static_cast<size_t>(pitch) * count) {
     PG_CUDA_CHECK(cudaStreamSynchronize(cs));
@@ -1058,9 +1077,10 @@ int pg_stage_bgen_end(pg_ctx* c, int slot, int64_t* diag) {
   PG_CHECK_STATUS(pg::bgen_repack(c->bgen_raw[slot].p, raw_stride, c->bgen_bits[slot].p, count, n, wide16,
                                   c->stage_buf[slot].p, pitch, cs));
   PG_CUDA_CHECK(cudaEventRecord(c->stage_ev[slot], cs));
-  c->stage_kind[slot] = wide16 ? PG_GENO_BGEN16 : PG_GENO_BGEN8;
-  c->stage_m[slot] = count;
+  c->stage_data[slot] = c->stage_buf[slot].p;
   c->stage_pitch[slot] = pitch;
+  c->stage_probs_off[slot] = 0;
+  c->stage_ploidy_off[slot] = -1;
   return PG_OK;
 }
 
@@ -1078,7 +1098,8 @@ int pg_scan_staged(pg_ctx* c, int slot, pg_batch_info* info) {
   PG_CUDA_CHECK(cudaStreamWaitEvent(c->stream, c->stage_ev[slot], 0));
   const int kind = c->stage_kind[slot];
   c->stage_kind[slot] = -1;
-  const int rc = scan_common(c, kind, c->stage_buf[slot].p, c->stage_m[slot], c->stage_pitch[slot], info);
+  const int rc = scan_common(c, kind, c->stage_data[slot], c->stage_m[slot], c->stage_pitch[slot], info,
+                             c->stage_probs_off[slot], c->stage_ploidy_off[slot]);
   PG_CUDA_CHECK(cudaEventRecord(c->slot_free_ev[slot], c->stream));
   return rc;
 }

@@ -81,7 +81,8 @@ __device__ __forceinline__ void load16(const GenoBlock& b, int64_t m, int64_t ci
   } else if constexpr (KIND == PG_GENO_BGEN8 || KIND == PG_GENO_BGEN16) {
     constexpr int den = (KIND == PG_GENO_BGEN8) ? 255 : 65535;
     constexpr int bw = (KIND == PG_GENO_BGEN8) ? 1 : 2;
-    const uint8_t* ploidy = row + b.n_src * 2 * bw;
+    const uint8_t* ploidy = row + (b.ploidy_off >= 0 ? b.ploidy_off : b.n_src * 2 * bw);
+    const uint8_t* probs = row + b.probs_off;
 #pragma unroll
     for (int i = 0; i < kChunk; ++i) {
       const int64_t s = ci * kChunk + i;
@@ -93,10 +94,10 @@ __device__ __forceinline__ void load16(const GenoBlock& b, int64_t m, int64_t ci
       }
       int v0, v1;
       if constexpr (bw == 1) {
-        v0 = row[2 * s];
-        v1 = row[2 * s + 1];
+        v0 = probs[2 * s];
+        v1 = probs[2 * s + 1];
       } else {
-        const uint16_t* p16 = reinterpret_cast<const uint16_t*>(row);
+        const uint16_t* p16 = reinterpret_cast<const uint16_t*>(probs);
         v0 = p16[2 * s];
         v1 = p16[2 * s + 1];
       }
@@ -421,13 +422,14 @@ __global__ void dosage_kernel(GenoBlock b, int elem_bytes, void* __restrict__ ou
     } else {
       constexpr int bw = (KIND == PG_GENO_BGEN8) ? 1 : 2;
       constexpr double den = (KIND == PG_GENO_BGEN8) ? 255.0 : 65535.0;
-      const uint8_t* ploidy = row + b.n_src * 2 * bw;
+      const uint8_t* ploidy = row + (b.ploidy_off >= 0 ? b.ploidy_off : b.n_src * 2 * bw);
+      const uint8_t* probs = row + b.probs_off;
       double v0, v1;
       if constexpr (bw == 1) {
-        v0 = row[2 * s];
-        v1 = row[2 * s + 1];
+        v0 = probs[2 * s];
+        v1 = probs[2 * s + 1];
       } else {
-        const uint16_t* p16 = reinterpret_cast<const uint16_t*>(row);
+        const uint16_t* p16 = reinterpret_cast<const uint16_t*>(probs);
         v0 = p16[2 * s];
         v1 = p16[2 * s + 1];
       }

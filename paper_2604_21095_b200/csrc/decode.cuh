@@ -18,6 +18,11 @@ struct GenoBlock {
   const uint32_t* keep_bits = nullptr;  // [ceil(n_src/32)] bit i = sample i kept
   int dense_real = 0;         // DENSE only: 1 -> fixed-point (2^-17) digits, 0 -> integral dosages
   int all_kept = 0;           // every source sample is kept (keep_bits needed only past n_src)
+  // BGEN rows: byte offsets of the probability pairs and of the ploidy bytes within a row
+  // (default: probabilities first, ploidy right after; the GPU-inflated layout of a BGEN-8
+  // block is used in place with probs at 10 + n, ploidy at 8)
+  int64_t probs_off = 0;
+  int64_t ploidy_off = -1;
 };
 
 // u-units: the integer code each observed sample contributes to the GEMM.
