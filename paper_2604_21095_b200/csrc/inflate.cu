@@ -35,8 +35,10 @@ constexpr int kRingSafe = kRing - 258;  // a copy never overwrites its own sourc
 __constant__ uint16_t c_len_base[29] = {3,  4,  5,  6,  7,  8,  9,  10, 11,  13,  15,  17,  19,  23, 27,
                                         31, 35, 43, 51, 59, 67, 83, 99, 115, 131, 163, 195, 227, 258};
 __constant__ uint8_t c_len_extra[29] = {0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 2, 2, 2, 2, 3, 3, 3, 3, 4, 4, 4, 4, 5, 5, 5, 5, 0};
-__constant__ uint16_t c_dist_base[30] = {1,   2,   3,   4,   5,   7,    9,    13,   17,   25,   33,   49,   65,    97,    129,
-                                         193, 257, 385, 513, 769, 1025, 1537, 2049, 3073, 4097, 6145, 8193, 12289, 16385, 24577};
+// symbols 30 / 31 (and undecodable codes, decoded as 31) get a distance no stream can reach
+__constant__ int32_t c_dist_base[32] = {1,     2,     3,     4,     5,     7,     9,      13,     17,    25,   33,
+                                        49,    65,    97,    129,   193,   257,   385,    513,    769,   1025, 1537,
+                                        2049,  3073,  4097,  6145,  8193,  12289, 16385,  24577,  1 << 30, 1 << 30};
 __constant__ uint8_t c_dist_extra[30] = {0, 0, 0, 0, 1, 1, 2, 2, 3, 3, 4, 4, 5, 5, 6, 6, 7, 7, 8, 8, 9, 9, 10, 10, 11, 11, 12, 12, 13, 13};
 __constant__ uint8_t c_clen_order[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
 
@@ -58,10 +60,12 @@ struct Table {
 };
 
 struct EncClen {
+  static constexpr uint32_t kInvalid = 0;
   __device__ static uint32_t enc(int s, int l) { return static_cast<uint32_t>(l) | (static_cast<uint32_t>(s) << 4); }
 };
 struct EncLit {
   static constexpr uint32_t kLength = 1u << 15;
+  static constexpr uint32_t kInvalid = 0;
   __device__ static uint32_t enc(int s, int l) {
     if (s < 256) return static_cast<uint32_t>(l) | (static_cast<uint32_t>(s) << 7);
     if (s == 256) return static_cast<uint32_t>(l) | (7u << 4) | kLength;
@@ -71,6 +75,7 @@ struct EncLit {
   }
 };
 struct EncDist {
+  static constexpr uint32_t kInvalid = 31u << 8;  // symbol 31: an unreachable distance
   __device__ static uint32_t enc(int s, int l) {
     const uint32_t extra = s < 30 ? c_dist_extra[s] : 0u;
     return static_cast<uint32_t>(l) | (extra << 4) | (static_cast<uint32_t>(s) << 8);
@@ -191,7 +196,7 @@ __device__ __forceinline__ uint32_t decode(Bits& br, const Table<BITS, NSYM, T>&
     return e;
   }
   const int s = decode_slow(br, t);
-  return s < 0 ? 0u : Enc::enc(s, 1);  // bits already consumed; only the fields matter
+  return s < 0 ? Enc::kInvalid : Enc::enc(s, 1);  // bits already consumed; only the fields matter
 }
 
 // L lanes decode one stream: L = 32 (a warp per stream, the default) or 16 (two streams per
@@ -396,20 +401,12 @@ __global__ void __launch_bounds__(4 * L) inflate_kernel(const uint8_t* __restric
       const int length = 3 + static_cast<int>((e >> 7) & 255u) + static_cast<int>(br.get(extra));
       br.refill();
       const uint32_t de = decode<EncDist>(br, sm.dist);
-      const uint32_t dsym = de >> 8;
-      if (!de || dsym >= 30) {
-        err = 1;
-        break;
-      }
-      const int distance = c_dist_base[dsym] + static_cast<int>(br.get((de >> 4) & 15u));
+      // invalid distance symbols (30, 31, no code) carry an unreachable base: one check below
+      const int distance = c_dist_base[de >> 8] + static_cast<int>(br.get((de >> 4) & 15u));
       // (reading past the stream end only consumes padding / the next stream's bytes; the
       // end-of-block check below reports truncation)
-      if (distance > pos) {
-        err = 1;
-        break;
-      }
-      if (pos + length > cap) {
-        err = 2;
+      if (distance > pos || pos + length > cap) {
+        err = distance > pos ? 1 : 2;
         break;
       }
       __syncwarp(mask);  // earlier literals / copies by other lanes are visible
