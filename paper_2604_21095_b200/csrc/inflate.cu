@@ -109,7 +109,7 @@ struct Bits {
     }
   }
   __device__ __forceinline__ uint32_t get(int n) {  // n <= 32 buffered bits
-    const uint32_t v = static_cast<uint32_t>(buf) & static_cast<uint32_t>((1ull << n) - 1ull);
+    const uint32_t v = static_cast<uint32_t>(buf) & ((1u << n) - 1u);  // n < 32 at every call
     buf >>= n;
     cnt -= n;
     return v;
