@@ -420,20 +420,30 @@ __global__ void __launch_bounds__(4 * L) inflate_kernel(const uint8_t* __restric
           sm.ring[(pos + lane) & (kRing - 1)] = v;
         }
       } else {
-        // an overlapping match repeats the last `distance` bytes: source offset j mod distance
-        // (j < 258: a float reciprocal gives the quotient within one, fixed up exactly)
-        const float inv_d = __frcp_rn(static_cast<float>(distance));
+        // a long or overlapping match: lane j copies source offset j mod distance (an overlapping
+        // match repeats the last `distance` bytes). The first offset comes from a float
+        // reciprocal (exact after one fix-up: j < 258), later ones by adding L mod distance.
+        int jj = lane, step = L;
+        if (distance < length) {
+          const float inv_d = __frcp_rn(static_cast<float>(distance));
+          jj = lane - distance * __float2int_rz(static_cast<float>(lane) * inv_d);
+          jj += jj < 0 ? distance : 0;
+          jj -= jj >= distance ? distance : 0;
+          step = L - distance * __float2int_rz(static_cast<float>(L) * inv_d);
+          step += step < 0 ? distance : 0;
+          step -= step >= distance ? distance : 0;
+        }
         for (int j = lane; j < length; j += L) {
-          int jj = j;
-          if (distance < length) {
-            jj = j - distance * __float2int_rz(static_cast<float>(j) * inv_d);
-            jj += jj < 0 ? distance : 0;
-            jj -= jj >= distance ? distance : 0;
-          }
           const int src = pos - distance + jj;
           const uint8_t v = from_ring ? sm.ring[src & (kRing - 1)] : dst[src];
           dst[pos + j] = v;
           sm.ring[(pos + j) & (kRing - 1)] = v;
+          if (distance < length) {
+            jj += step;
+            jj -= jj >= distance ? distance : 0;
+          } else {
+            jj += L;
+          }
         }
       }
       pos += length;
