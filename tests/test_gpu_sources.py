@@ -133,3 +133,30 @@ def test_wide3_k_sliced_equals_ternary_bitwise(tmp_path, monkeypatch):
     monkeypatch.setenv("PANELGWAS_WIDE_DIGITS", "0")
     pg.run_scan(pg.ScanConfig(out_path=tmp_path / "tern.bin", **kw))
     assert (tmp_path / "wide.bin").read_bytes() == (tmp_path / "tern.bin").read_bytes()
+
+
+def test_bgen8_in_place_blocks_equal_host_inflate_with_sample_subset(tmp_path, monkeypatch):
+    """All-8-bit BGEN batches are decoded straight from the GPU-inflated blocks (probs at
+    10 + n, ploidy at 8); with a --keep / --remove subset and samples missing from the
+    phenotype table the FULL output equals the host-inflate path (repacked rows) bit for bit."""
+    from bgen_fixture import write_bgen
+
+    rng = np.random.default_rng(808)
+    n, m = 157, 90
+    ids = [f"S{i + 1}" for i in range(n)]
+    d = rng.uniform(0, 2, (m, n))
+    d[rng.random(d.shape) < 0.07] = np.nan
+    y = rng.standard_normal((n - 5, 4))  # the last 5 genotype samples have no phenotypes
+    pheno = write_tsv(tmp_path / "p.tsv", ids[:-5], ["a", "b", "c", "d"], y)
+    (tmp_path / "keep.txt").write_text("".join(f"{s}\n" for s in ids[3:140]))
+    (tmp_path / "remove.txt").write_text("S10\nS11\n")
+    spec = pg.SourceSpec(pg.GenotypeFormat.BGEN, bgen_path=write_bgen(tmp_path / "g.bgen", d, ids, bits=8))
+    kw = dict(source=spec, pheno_path=pheno, output_mode=pg.OutputMode.FULL, precision=pg.Precision.F64,
+              summary_to_stderr=False, keep_path=tmp_path / "keep.txt", remove_path=tmp_path / "remove.txt",
+              device_batch=32)
+    pg.run_scan(pg.ScanConfig(out_path=tmp_path / "gpu.bin", **kw))
+    monkeypatch.setenv("PANELGWAS_HOST_INFLATE", "1")
+    pg.run_scan(pg.ScanConfig(out_path=tmp_path / "host.bin", **kw))
+    assert (tmp_path / "gpu.bin").read_bytes() == (tmp_path / "host.bin").read_bytes()
+    t, markers, names = pg.read_full_matrix(tmp_path / "gpu.bin")
+    assert t.shape == (m, 4) and np.isfinite(t).all()
