@@ -223,60 +223,76 @@ __device__ __forceinline__ void bed_counts(const GenoBlock& b, int64_t m, int la
   ssu = n2 + n0;
 }
 
+constexpr int kMarkersPerWarp = 4;
+
 template <int KIND, int kU = 6>
 __global__ void stats_kernel(GenoBlock b, MarkerStats st, int64_t m_pad, double unit_scale) {
+  // a warp counts kMarkersPerWarp rows one after the other (all lanes), then lane k finalizes
+  // marker k: the fp64 / int128 tail of each marker costs one lane-parallel pass, not a warp's
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t m = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + warp;
-  if (m >= m_pad) return;
-  if (m >= b.n_markers) {  // padding marker: neutral, never a candidate
-    if (lane == 0) {
-      st.mu_d[m] = 0.0;
-      st.mu_f[m] = 0.f;
-      st.invd_d[m] = __longlong_as_double(0x7ff8000000000000ll);
-      st.invd_f[m] = __int_as_float(0x7fc00000);
-    }
-    return;
-  }
-  const int64_t n_chunks = (b.n_src + kChunk - 1) / kChunk;
-  long long nmiss = 0, su = 0, ssu = 0;
-  double dsum = 0.0;
-  bool nonint = false;
-  if constexpr (KIND == PG_GENO_BED) {
-    bed_counts<kU>(b, m, lane, nmiss, su, ssu);
-    // per-lane counts fit in 32 bits: reduce them as int (one shuffle each, not two)
-    int a = static_cast<int>(nmiss), c = static_cast<int>(su), d = static_cast<int>(ssu);
+  const int64_t m0 = (static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + warp) * kMarkersPerWarp;
+  long long k_nmiss = 0, k_su = 0, k_ssu = 0;
+  double k_dsum = 0.0;
+  for (int k = 0; k < kMarkersPerWarp; ++k) {
+    const int64_t m = m0 + k;
+    if (m >= b.n_markers) break;  // uniform across the warp
+    const int64_t n_chunks = (b.n_src + kChunk - 1) / kChunk;
+    long long nmiss = 0, su = 0, ssu = 0;
+    double dsum = 0.0;
+    bool nonint = false;
+    if constexpr (KIND == PG_GENO_BED) {
+      bed_counts<kU>(b, m, lane, nmiss, su, ssu);
+      // per-lane counts fit in 32 bits: reduce them as int (one shuffle each, not two)
+      int a = static_cast<int>(nmiss), c = static_cast<int>(su), d = static_cast<int>(ssu);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      a += __shfl_xor_sync(0xffffffffu, a, o);
-      c += __shfl_xor_sync(0xffffffffu, c, o);
-      d += __shfl_xor_sync(0xffffffffu, d, o);
-    }
-    nmiss = a;
-    su = c;
-    ssu = d;
-  } else {
-    for (int64_t ci = lane; ci < n_chunks; ci += 32) {
-      int u[kChunk];
-      uint32_t miss, obs;
-      load16<KIND>(b, m, ci, u, miss, obs, dsum, nonint);
-      nmiss += __popc(miss);
+      for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        c += __shfl_xor_sync(0xffffffffu, c, o);
+        d += __shfl_xor_sync(0xffffffffu, d, o);
+      }
+      nmiss = a;
+      su = c;
+      ssu = d;
+    } else {
+      for (int64_t ci = lane; ci < n_chunks; ci += 32) {
+        int u[kChunk];
+        uint32_t miss, obs;
+        load16<KIND>(b, m, ci, u, miss, obs, dsum, nonint);
+        nmiss += __popc(miss);
 #pragma unroll
-      for (int i = 0; i < kChunk; ++i) {
-        su += u[i];
-        ssu += static_cast<long long>(u[i]) * u[i];
+        for (int i = 0; i < kChunk; ++i) {
+          su += u[i];
+          ssu += static_cast<long long>(u[i]) * u[i];
+        }
       }
     }
-  }
-  if constexpr (KIND != PG_GENO_BED) {
+    if constexpr (KIND != PG_GENO_BED) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      nmiss += __shfl_xor_sync(0xffffffffu, nmiss, o);
-      su += __shfl_xor_sync(0xffffffffu, su, o);
-      ssu += __shfl_xor_sync(0xffffffffu, ssu, o);
-      dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
+      for (int o = 16; o > 0; o >>= 1) {
+        nmiss += __shfl_xor_sync(0xffffffffu, nmiss, o);
+        su += __shfl_xor_sync(0xffffffffu, su, o);
+        ssu += __shfl_xor_sync(0xffffffffu, ssu, o);
+        dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
+      }
+    }
+    if (lane == k) {
+      k_nmiss = nmiss;
+      k_su = su;
+      k_ssu = ssu;
+      k_dsum = dsum;
     }
   }
-  if (lane != 0) return;
+  const int64_t m = m0 + lane;
+  if (lane >= kMarkersPerWarp || m >= m_pad) return;
+  if (m >= b.n_markers) {  // padding marker: neutral, never a candidate
+    st.mu_d[m] = 0.0;
+    st.mu_f[m] = 0.f;
+    st.invd_d[m] = __longlong_as_double(0x7ff8000000000000ll);
+    st.invd_f[m] = __int_as_float(0x7fc00000);
+    return;
+  }
+  const long long nmiss = k_nmiss, su = k_su, ssu = k_ssu;
+  const double dsum = k_dsum;
   const double nan = __longlong_as_double(0x7ff8000000000000ll);
   st.n_miss[m] = nmiss;
   st.s_u[m] = su;
@@ -469,7 +485,8 @@ template <int KIND>
 int stats_dispatch(const GenoBlock& b, MarkerStats& st, int64_t m_pad, cudaStream_t s) {
   static const int ku = env_int("PG_STATS_KU", 6), wpb_env = env_int("PG_STATS_WPB", 8);
   const int wpb = (wpb_env == 4 || wpb_env == 16) ? wpb_env : 8;
-  const unsigned grid = static_cast<unsigned>((m_pad + wpb - 1) / wpb);
+  const int64_t per_block = static_cast<int64_t>(wpb) * kMarkersPerWarp;
+  const unsigned grid = static_cast<unsigned>((m_pad + per_block - 1) / per_block);
   const double scale = geno_unit_scale(b);
   if (KIND == PG_GENO_BED && ku == 12) {
     stats_kernel<KIND, 12><<<grid, wpb * 32, 0, s>>>(b, st, m_pad, scale);
