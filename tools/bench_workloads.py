@@ -58,7 +58,9 @@ def main():
     ap.add_argument("--markers", type=int, default=1_000_000)
     ap.add_argument("--samples", type=int, default=23_000)
     ap.add_argument("--steps", type=int, default=3)
-    ap.add_argument("--distinct", type=int, default=8192, help="distinct markers in the resident batch")
+    ap.add_argument("--distinct", type=int, default=0,
+                    help="distinct markers in the resident batch = markers per launch (default: the engine's device "
+                         "batch, 65,536 for PLINK and 8,192 for BGEN)")
     a = ap.parse_args()
 
     import torch
@@ -80,7 +82,7 @@ def main():
     df = float(n - 2)
     ctx.set_scan(df, _native.PG_MODE_THRESHOLD, np.full(p, threshold_premask(1e-4, df)))
     rng = np.random.default_rng(9)
-    batch = a.distinct
+    batch = a.distinct or (65536 if a.workload == "c2" else 32768)
     if a.workload == "c2":
         bpm = (n + 3) // 4
         pitch = (bpm + 15) // 16 * 16
