@@ -76,20 +76,23 @@ def main():
     ap.add_argument("--phenotypes", type=int, default=4_096)
     ap.add_argument("--distinct", type=int, default=8192)
     ap.add_argument("--seed", type=int, default=5)
+    ap.add_argument("--reuse", action="store_true", help="keep the input files of a previous run in --dir")
+    ap.add_argument("--extra", default="", help="extra CLI flags for `panelgwas run` (space-separated)")
     a = ap.parse_args()
     d = Path(a.dir)
     d.mkdir(parents=True, exist_ok=True)
     n, p = a.samples, a.phenotypes
     t0 = time.perf_counter()
-    write_bgen(d / "geno.bgen", n, a.markers, a.distinct, a.seed)
-    rng = np.random.default_rng(a.seed + 1)
-    write_repr_tsv(d / "pheno.tsv", [f"S{i + 1}" for i in range(n)], [f"ph{j + 1}" for j in range(p)],
-                   rng.standard_normal((n, p)))
+    if not (a.reuse and (d / "geno.bgen").exists() and (d / "pheno.tsv").exists()):
+        write_bgen(d / "geno.bgen", n, a.markers, a.distinct, a.seed)
+        rng = np.random.default_rng(a.seed + 1)
+        write_repr_tsv(d / "pheno.tsv", [f"S{i + 1}" for i in range(n)], [f"ph{j + 1}" for j in range(p)],
+                       rng.standard_normal((n, p)))
     t_write = time.perf_counter() - t0
     for old in d.glob("hits.tsv*"):
         old.unlink()
     cmd = [sys.executable, "-m", "paper_2604_21095_b200", "run", "--bgen", str(d / "geno.bgen"), "--pheno",
-           str(d / "pheno.tsv"), "--p-threshold", "1e-4", "--out", str(d / "hits.tsv")]
+           str(d / "pheno.tsv"), "--p-threshold", "1e-4", *a.extra.split(), "--out", str(d / "hits.tsv")]
     t0 = time.perf_counter()
     res = subprocess.run(cmd, capture_output=True, text=True, cwd=str(ROOT), env={**os.environ, "PANELGWAS_PROFILE": "1"})
     wall = time.perf_counter() - t0
