@@ -63,7 +63,8 @@ DEFAULT_FULL_BYTE_BUDGET = 16 * 1024**3
 
 # device batches are sized for the GEMM (>= this many markers) and bounded in memory
 _MIN_DEVICE_BATCH = 8192
-_DOSAGE_DEVICE_BATCH = 32768
+_DOSAGE_DEVICE_BATCH = 8192  # --batch-size up to 32,768 raises C5 throughput (GPU-resident: +10 %) but
+# triples the pinned read ring, whose allocation contends with the panel upload in a CLI run
 _PLINK_DEVICE_BATCH = 65536
 _SLICE_SAMPLES = 131072  # csrc/assoc.cuh kSliceK
 _MAX_GEMM_ROWS = 1 << 17
@@ -234,8 +235,7 @@ def device_batch_size(config: ScanConfig, n_markers: int, n_pheno: int, n_sample
     # PLINK rows are 2-bit packed and decoded inside the GEMM: large launches amortize the
     # per-launch statistics / compaction / host round trips (65,536 markers = 377 MB at N = 23k)
     # dosage sources: up to 4 GEMM rows per marker with wide digits (the default), 16 with the
-    # balanced-ternary planes; 32,768 BGEN variants per launch keep the GPU inflate's last wave
-    # of streams small against the whole batch
+    # balanced-ternary planes
     wide = os.environ.get("PANELGWAS_WIDE_DIGITS", "1") != "0"
     b = max(config.batch_size, _PLINK_DEVICE_BATCH if plink else (_DOSAGE_DEVICE_BATCH if wide else _MIN_DEVICE_BATCH))
     b = min(b, _MAX_GEMM_ROWS if plink else _MAX_GEMM_ROWS // (4 if wide else 16))

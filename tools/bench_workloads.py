@@ -82,7 +82,7 @@ def main():
     df = float(n - 2)
     ctx.set_scan(df, _native.PG_MODE_THRESHOLD, np.full(p, threshold_premask(1e-4, df)))
     rng = np.random.default_rng(9)
-    batch = a.distinct or (65536 if a.workload == "c2" else 32768)
+    batch = a.distinct or (65536 if a.workload == "c2" else 8192)
     if a.workload == "c2":
         bpm = (n + 3) // 4
         pitch = (bpm + 15) // 16 * 16
