@@ -159,12 +159,6 @@ def synth_panel(torch, n_samples: int, n_pheno: int, seed: int, device):
     return y
 
 
-def decode_host(packed: np.ndarray, n: int) -> np.ndarray:
-    from oracle.scan_oracle import decode_bed
-
-    return decode_bed(packed, n)
-
-
 # --------------------------------------------------------------------------- reference arm
 def cpu_threads() -> int:
     try:
