@@ -429,3 +429,32 @@ def test_native_bim_index_equals_line_reader(tmp_path, text):
     assert list(got) == want and len(got) == len(want)
     if native is not None:
         assert got[1:].prefixes(False) == [f"{m.chrom}\t{m.id}\t{m.pos}\t{m.allele2}\t{m.allele1}\t" for m in want[1:]]
+
+
+def test_device_batch_sizes(monkeypatch):
+    """Markers per device launch: PLINK 65,536; dosage sources 8,192 by default and up to
+    32,768 through --batch-size with wide digits (8,192 with the ternary planes); FULL and
+    K-sliced runs shrink it to their memory bounds; never more markers than the scan has."""
+    from pathlib import Path
+
+    import paper_2604_21095_b200 as pg
+    from paper_2604_21095_b200.engine import device_batch_size
+
+    def cfg(fmt, **kw):
+        spec = pg.SourceSpec(fmt, bed_path=Path("a.bed"), bim_path=Path("a.bim"), fam_path=Path("a.fam"),
+                             bgen_path=Path("a.bgen"))
+        return pg.ScanConfig(source=spec, pheno_path=Path("p.tsv"), out_path=Path("o.tsv"), **kw)
+
+    plink, bgen = pg.GenotypeFormat.PLINK_BED, pg.GenotypeFormat.BGEN
+    assert device_batch_size(cfg(plink), 10**6, 20480, 23000) == 65536
+    assert device_batch_size(cfg(plink), 1000, 20480, 23000) == 1000
+    assert device_batch_size(cfg(bgen), 10**6, 4096, 23000) == 8192
+    assert device_batch_size(cfg(bgen, batch_size=32768), 10**6, 4096, 23000) == 32768
+    assert device_batch_size(cfg(bgen, batch_size=10**6), 10**6, 4096, 23000) == 32768
+    monkeypatch.setenv("PANELGWAS_WIDE_DIGITS", "0")
+    assert device_batch_size(cfg(bgen, batch_size=32768), 10**6, 4096, 23000) == 8192
+    monkeypatch.delenv("PANELGWAS_WIDE_DIGITS")
+    full = device_batch_size(cfg(plink, output_mode=pg.OutputMode.FULL), 10**6, 20480, 23000)
+    assert 256 <= full < 65536
+    sliced = device_batch_size(cfg(plink), 10**6, 20480, 500_000)
+    assert 256 <= sliced < 65536
