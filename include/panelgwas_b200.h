@@ -212,9 +212,31 @@ PG_API int pg_fetch_candidates(pg_ctx* ctx, int64_t* rows, int64_t* cols, double
 /* FULL mode: t of non-skipped markers, row-major [n_ok, n_pheno], f32 (elem=4)
  * or f64 (elem=8) — BatchStats.t_rows (engine.py:197-198). */
 PG_API int pg_fetch_full(pg_ctx* ctx, void* out, int elem_bytes, int64_t* n_rows);
-/* Per-phenotype max |r| over all non-skipped markers scanned since the last
- * pg_ctx_set_scan (the minimum-p statistic). */
+/* Per-phenotype max |r| (exact fp64 r of the maximizing pair) over all non-skipped markers
+ * scanned since tracking was enabled: the minimum-p statistic. Tracking is off by default
+ * (it costs the GEMM epilogue a compare per pair); pg_ctx_track_max_abs_r(ctx, 1) after
+ * pg_ctx_set_scan enables it and clears the maxima. */
+PG_API int pg_ctx_track_max_abs_r(pg_ctx* ctx, int enable);
 PG_API int pg_fetch_max_abs_r(pg_ctx* ctx, double* out);
+
+/* ---- effect sizes (north star: beta / t / -log10 p) ----
+ * The reference engine reports R T P only (output.py:29-43); beta exists in its OLS oracle
+ * (oracle.ols_single, oracle.py:35-90). With pheno_sd[j] = sd (1/N) of kept residualized
+ * phenotype j (standardize_columns, kernel.py:330-347) and var = the marker's
+ * variance_before_scaling (kernel.py:411), each scan also yields
+ *   beta = r * pheno_sd / sqrt(var),  se = pheno_sd / sqrt(var) * sqrt((1 - r^2) / df),
+ * the slope of y_res on g and its standard error (beta / se == t). With
+ * residualize_genotypes + adjusted df these equal ols_single(y, g, C).beta / .se.
+ * pheno_sd == NULL disables; a new panel disables. */
+PG_API int pg_ctx_set_beta_scale(pg_ctx* ctx, const double* pheno_sd, int64_t n_pheno);
+/* beta / se of the last scan's candidates, aligned with pg_fetch_candidates. NULL skips. */
+PG_API int pg_fetch_candidate_beta(pg_ctx* ctx, double* beta, double* se);
+/* FULL mode: beta rows aligned with pg_fetch_full (se = beta / t). */
+PG_API int pg_fetch_full_beta(pg_ctx* ctx, void* out, int elem_bytes, int64_t* n_rows);
+/* Test hook: the next scans start the 64-bit candidate counter at `base` instead of 0
+ * (candidate slots are counter - base), so a test can drive the counter across 2^31
+ * inside one launch without producing 2^31 candidates. */
+PG_API int pg_ctx_debug_candidate_base(pg_ctx* ctx, uint64_t base);
 
 /* ---- element-wise statistics on the device (host arrays in/out) ---- */
 /* kernel.t_from_r (kernel.py:460-478) */
@@ -273,6 +295,11 @@ PG_API int pg_format_tsv(int64_t n, const int64_t* rows, const int64_t* cols, co
                          const double* p, const double* af, const int64_t* n_miss, const char* prefix_blob,
                          const int64_t* prefix_off, const char* pheno_blob, const int64_t* pheno_off,
                          const char* mid, int64_t mid_len, char* out, int64_t out_cap, int64_t* out_len);
+
+/* n lines of ncols tab-separated doubles rendered as Python repr() (effect-size sidecar
+ * BETA\tSE lines, aligned with the record lines). PG_ERR_INVALID when out_cap is too small. */
+PG_API int pg_format_float_columns(int64_t n, int ncols, const double* const* cols, char* out, int64_t out_cap,
+                                   int64_t* out_len);
 
 /* FULL-mode marker sidecar lines "SOURCE_INDEX CHR ID POS A1 A2 AF N_MISS" (tab-separated, LF) of
  * markers rows[0..n): replaces the per-marker f-string of FullMatrixWriter.emit

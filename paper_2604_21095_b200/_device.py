@@ -47,6 +47,9 @@ class ScanResult:
     cand_t: np.ndarray | None = None
     cand_p: np.ndarray | None = None
     t_rows: np.ndarray | None = None
+    cand_beta: np.ndarray | None = None  # effect sizes (set_beta_scale): aligned with cand_* / t_rows
+    cand_se: np.ndarray | None = None
+    beta_rows: np.ndarray | None = None
     decode_ms: float = 0.0
     gemm_ms: float = 0.0
     launches: int = 0
@@ -66,6 +69,7 @@ class DeviceContext:
         self.lock = threading.RLock()
         self.n_pheno = 0
         self.mode = _native.PG_MODE_THRESHOLD
+        self.beta_on = False
 
     # ------------------------------------------------------------ lifetime
     def close(self) -> None:
@@ -102,6 +106,7 @@ class DeviceContext:
             call("pg_ctx_set_panel", self._h, ptr(y), y.shape[0], y.shape[1], y.shape[1], ptr(gidx),
                  int(n_samples_src))
             self.n_pheno = y.shape[1]
+            self.beta_on = False  # the native ctx drops phenotype scales with the panel
 
     def prepare_panel(self, y: np.ndarray, basis_q: np.ndarray | None) -> tuple[np.ndarray, np.ndarray]:
         """Residualize + standardize the kept-sample panel on the device (kernel.py:310-347).
@@ -138,6 +143,7 @@ class DeviceContext:
         with self.lock:
             call("pg_ctx_commit_panel", self._h, ptr(cols), cols.size, ptr(gidx), int(n_samples_src))
             self.n_pheno = int(cols.size)
+            self.beta_on = False  # the native ctx drops phenotype scales with the panel
 
     def set_panel_device(self, d_ptr: int, n_kept: int, n_pheno: int, ld: int, geno_row_index: np.ndarray,
                          n_samples_src: int) -> None:
@@ -145,6 +151,7 @@ class DeviceContext:
         with self.lock:
             call("pg_ctx_set_panel_device", self._h, d_ptr, n_kept, n_pheno, ld, ptr(gidx), int(n_samples_src))
             self.n_pheno = n_pheno
+            self.beta_on = False  # the native ctx drops phenotype scales with the panel
 
     def panel_bytes(self) -> int:
         n = c_int64(0)
@@ -160,6 +167,7 @@ class DeviceContext:
         with self.lock:
             call("pg_ctx_import_panel", self._h, d_src, n_kept, n_pheno, ptr(gidx), int(n_samples_src))
             self.n_pheno = n_pheno
+            self.beta_on = False  # the native ctx drops phenotype scales with the panel
 
     def set_scan(self, df: float, mode: int, r_bar: np.ndarray | None) -> None:
         rb = None if r_bar is None else np.ascontiguousarray(r_bar, dtype=np.float64)
@@ -173,6 +181,18 @@ class DeviceContext:
         with self.lock:
             call("pg_ctx_set_basis", self._h, ptr(qq), 0 if qq is None else qq.shape[0],
                  0 if qq is None else qq.shape[1])
+
+    def set_beta_scale(self, pheno_sd: np.ndarray | None) -> None:
+        """Enable effect sizes: sd (1/N) of each scanned residualized phenotype, in panel
+        column order (None disables). Every later scan also returns beta / se."""
+        sd = None if pheno_sd is None else np.ascontiguousarray(pheno_sd, dtype=np.float64)
+        with self.lock:
+            call("pg_ctx_set_beta_scale", self._h, ptr(sd), 0 if sd is None else sd.size)
+            self.beta_on = sd is not None
+
+    def debug_candidate_base(self, base: int) -> None:
+        """Test hook: start the 64-bit candidate counter of later scans at `base`."""
+        call("pg_ctx_debug_candidate_base", self._h, int(base))
 
     def set_wide_digits(self, enable: bool) -> None:
         call("pg_ctx_set_wide_digits", self._h, 1 if enable else 0)
@@ -282,6 +302,9 @@ class DeviceContext:
                 out = np.empty((n_rows.value, self.n_pheno), dtype=dt)
             call("pg_fetch_full", self._h, ptr(out), full_elem_bytes, byref(n_rows))
             res.t_rows = out
+            if self.beta_on:
+                res.beta_rows = np.empty((n_rows.value, self.n_pheno), dtype=dt)
+                call("pg_fetch_full_beta", self._h, ptr(res.beta_rows), full_elem_bytes, byref(n_rows))
         else:
             k = int(info.n_candidates)
             res.cand_rows = np.empty(k, np.int64)
@@ -292,6 +315,11 @@ class DeviceContext:
             if k:
                 call("pg_fetch_candidates", self._h, ptr(res.cand_rows), ptr(res.cand_cols), ptr(res.cand_r),
                      ptr(res.cand_t), ptr(res.cand_p))
+            if self.beta_on:
+                res.cand_beta = np.empty(k)
+                res.cand_se = np.empty(k)
+                if k:
+                    call("pg_fetch_candidate_beta", self._h, ptr(res.cand_beta), ptr(res.cand_se))
         return res
 
     def time_marker_stats(self, kind: int, d_ptr: int, n_markers: int, pitch: int, reps: int = 5) -> float:
@@ -300,6 +328,10 @@ class DeviceContext:
         with self.lock:
             call("pg_time_marker_stats", self._h, int(kind), d_ptr, n_markers, pitch, reps, byref(ms))
         return float(ms.value)
+
+    def track_max_abs_r(self, enable: bool = True) -> None:
+        """Track the per-phenotype max |r| of later scans (min-p sidecar); clears it."""
+        call("pg_ctx_track_max_abs_r", self._h, 1 if enable else 0)
 
     def max_abs_r(self) -> np.ndarray:
         out = np.empty(self.n_pheno)

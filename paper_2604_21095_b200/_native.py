@@ -87,6 +87,12 @@ SIGNATURES: dict[str, list] = {
     "pg_fetch_candidates": [_P, _P, _P, _P, _P, _P],
     "pg_fetch_full": [_P, _P, c_int, _P],
     "pg_fetch_max_abs_r": [_P, _P],
+    "pg_ctx_track_max_abs_r": [_P, c_int],
+    "pg_format_float_columns": [c_int64, c_int, _P, _P, c_int64, _P],
+    "pg_ctx_set_beta_scale": [_P, _P, c_int64],
+    "pg_fetch_candidate_beta": [_P, _P, _P],
+    "pg_fetch_full_beta": [_P, _P, c_int, _P],
+    "pg_ctx_debug_candidate_base": [_P, ctypes.c_uint64],
     "pg_t_from_r": [_P, _P, c_int64, c_double, _P],
     "pg_p_from_t": [_P, _P, c_int64, c_double, _P, _P],
     "pg_reg_inc_beta": [_P, _P, _P, _P, c_int64, _P],

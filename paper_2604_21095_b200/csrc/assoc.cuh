@@ -47,9 +47,10 @@ struct AssocEpilogue {
   const float* rbar;            // [p_pad] premask bar on |r| (already widened); null = no candidates
   unsigned long long* cand_key; // (marker << 32) | phenotype
   double* cand_r;               // exact fp64 r of the candidate
-  int* cand_count;
+  unsigned long long* cand_count;  // 64-bit: a launch may produce more than 2^31 candidates
+  unsigned long long cand_base;    // initial counter value (test hook); slot = counter - cand_base
   int64_t cand_cap;
-  unsigned int* max_abs_r;      // [p_pad] running max |r| (float bits), or null
+  unsigned long long* max_abs_r;  // [p_pad] running max |r| (bits of a non-negative double), or null = off
   double* full_r;               // FULL mode: r[marker * full_ld + p] (fp64), or null
   int64_t full_ld;
   long long* x_accum;           // K-sliced runs (k_pad > kSliceK): int64 (xu, xm) partials

@@ -146,31 +146,46 @@ __device__ __forceinline__ void decode_word(uint32_t w, uint32_t (&u)[4], uint32
   }
 }
 
+// Running per-phenotype max |r| (min-p sidecar, only when ep.max_abs_r is set): the fp32
+// estimate selects, the exact fp64 r decides. r64 is evaluated for every pair whose fp32 |r|
+// comes within the premask's error window of the thread's fp32 maximum so far, so the fp64
+// maximum over those pairs is the fp64 maximum over all pairs.
+struct MaxAbsR {
+  float f = 0.f;      // fp32 |r| maximum seen
+  double d = 0.0;     // fp64 |r| maximum over the window candidates
+};
+
 // shared tail of the epilogues: fp32 premask, fp64 r for candidates / FULL, compaction
 __device__ __forceinline__ void epilogue_value(const AssocEpilogue& ep, long long xu, long long xm, int m, int pheno,
                                                float sc_f, double sc_d, float cq_f, long long cq, float rb, int lane,
-                                               uint32_t lanemask_lt, float& mx) {
+                                               uint32_t lanemask_lt, MaxAbsR& mx) {
   const float mu = __ldg(ep.mu_f + m);
   const float iv = ep.raw ? 1.f : __ldg(ep.invd_f + m);  // NaN for skipped / padding markers
   const float xf = static_cast<float>(xu) - mu * (cq_f - static_cast<float>(xm));
   const float r = xf * sc_f * iv;
   const float ar = fabsf(r);
-  mx = fmaxf(mx, ar);
   const bool hit = ar >= rb;
+  // same widening as the premask bar (ctx.cu rbar_kernel), doubled
+  const bool near_max = ep.max_abs_r != nullptr && ar >= mx.f * (1.f - 2e-5f) - 2e-7f;
   double r64 = 0.0;
-  if (hit || ep.full_r) {
+  if (hit || ep.full_r || near_max) {
     r64 = sc_d * (static_cast<double>(xu) - __ldg(ep.mu_d + m) * static_cast<double>(cq - xm)) *
           (ep.raw ? 1.0 : __ldg(ep.invd_d + m));
+  }
+  if (near_max) {
+    mx.f = fmaxf(mx.f, ar);
+    mx.d = fmax(mx.d, fabs(r64));  // NaN (skipped / padding markers) is ignored by fmax
   }
   if (ep.full_r) ep.full_r[static_cast<int64_t>(m) * ep.full_ld + pheno] = r64;
   const uint32_t mask = __ballot_sync(0xffffffffu, hit);
   if (mask) {
-    int base = 0;
-    if (lane == 0) base = atomicAdd(ep.cand_count, __popc(mask));
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(ep.cand_count, static_cast<unsigned long long>(__popc(mask)));
     base = __shfl_sync(0xffffffffu, base, 0);
     if (hit) {
-      const int64_t idx = static_cast<int64_t>(base) + __popc(mask & lanemask_lt);
-      if (idx < ep.cand_cap) {
+      // unsigned 64-bit slot: no wrap, and slots past the capacity are counted but not stored
+      const unsigned long long idx = base - ep.cand_base + __popc(mask & lanemask_lt);
+      if (idx < static_cast<unsigned long long>(ep.cand_cap)) {
         ep.cand_key[idx] = (static_cast<unsigned long long>(m) << 32) | static_cast<unsigned>(pheno);
         ep.cand_r[idx] = r64;
       }
@@ -188,7 +203,7 @@ __device__ __forceinline__ void epilogue_tile_wide(const AssocEpilogue& ep, uint
   const float cq_f = ep.cq_f[pheno];
   const long long cq = ep.cq[pheno];
   const float rb = ep.rbar ? ep.rbar[pheno] : INFINITY;
-  float mx = 0.f;
+  MaxAbsR mx;
 #pragma unroll 1
   for (int c = c_begin; c < c_end; c += 16) {
     uint32_t a[16], b[16], d[16];
@@ -214,7 +229,8 @@ __device__ __forceinline__ void epilogue_tile_wide(const AssocEpilogue& ep, uint
       epilogue_value(ep, xu, x[3], m, pheno, sc_f, sc_d, cq_f, cq, rb, lane, lanemask_lt, mx);
     }
   }
-  if (ep.max_abs_r && !ep.x_accum && pheno < ep.p_valid) atomicMax(ep.max_abs_r + pheno, __float_as_uint(mx));
+  if (ep.max_abs_r && !ep.x_accum && pheno < ep.p_valid)
+    atomicMax(ep.max_abs_r + pheno, static_cast<unsigned long long>(__double_as_longlong(mx.d)));
 }
 
 // BGEN-8 wide tile: per marker rows (digit0, digit1, missing), 12 columns (4 markers) per step
@@ -228,7 +244,7 @@ __device__ __forceinline__ void epilogue_tile_wide3(const AssocEpilogue& ep, uin
   const float cq_f = ep.cq_f[pheno];
   const long long cq = ep.cq[pheno];
   const float rb = ep.rbar ? ep.rbar[pheno] : INFINITY;
-  float mx = 0.f;
+  MaxAbsR mx;
 #pragma unroll 1
   for (int c = c_begin; c < c_end; c += 12) {
     uint32_t a[12], b[12], d[12];
@@ -257,7 +273,8 @@ __device__ __forceinline__ void epilogue_tile_wide3(const AssocEpilogue& ep, uin
       epilogue_value(ep, xu, x[2], m, pheno, sc_f, sc_d, cq_f, cq, rb, lane, lanemask_lt, mx);
     }
   }
-  if (ep.max_abs_r && !ep.x_accum && pheno < ep.p_valid) atomicMax(ep.max_abs_r + pheno, __float_as_uint(mx));
+  if (ep.max_abs_r && !ep.x_accum && pheno < ep.p_valid)
+    atomicMax(ep.max_abs_r + pheno, static_cast<unsigned long long>(__double_as_longlong(mx.d)));
 }
 
 template <int R>
@@ -270,7 +287,7 @@ __device__ __forceinline__ void epilogue_tile(const AssocEpilogue& ep, uint32_t 
   const float cq_f = ep.cq_f[pheno];
   const long long cq = ep.cq[pheno];
   const float rb = ep.rbar ? ep.rbar[pheno] : INFINITY;
-  float mx = 0.f;
+  MaxAbsR mx;
 #pragma unroll 1
   for (int c = c_begin; c < c_end; c += 16) {
     uint32_t h[16], l[16];
@@ -302,7 +319,8 @@ __device__ __forceinline__ void epilogue_tile(const AssocEpilogue& ep, uint32_t 
       epilogue_value(ep, xu, xm, m, pheno, sc_f, sc_d, cq_f, cq, rb, lane, lanemask_lt, mx);
     }
   }
-  if (ep.max_abs_r && !ep.x_accum && pheno < ep.p_valid) atomicMax(ep.max_abs_r + pheno, __float_as_uint(mx));
+  if (ep.max_abs_r && !ep.x_accum && pheno < ep.p_valid)
+    atomicMax(ep.max_abs_r + pheno, static_cast<unsigned long long>(__double_as_longlong(mx.d)));
 }
 
 template <int MODE>
@@ -533,7 +551,7 @@ __global__ void x_epilogue_kernel(AssocEpilogue ep, int64_t m_slots) {
   const float cq_f = ep.cq_f[pheno];
   const long long cq = ep.cq[pheno];
   const float rb = ep.rbar ? ep.rbar[pheno] : INFINITY;
-  float mx = 0.f;
+  MaxAbsR mx;
   for (int64_t m = static_cast<int64_t>(blockIdx.y) * (blockDim.x >> 5) + (threadIdx.x >> 5); m < m_slots;
        m += static_cast<int64_t>(gridDim.y) * (blockDim.x >> 5)) {
     const long long* x = ep.x_accum + (m * ep.x_ld + pheno) * 2;
@@ -541,7 +559,8 @@ __global__ void x_epilogue_kernel(AssocEpilogue ep, int64_t m_slots) {
     e.x_accum = nullptr;
     epilogue_value(e, x[0], x[1], static_cast<int>(m), pheno, sc_f, sc_d, cq_f, cq, rb, lane, lanemask_lt, mx);
   }
-  if (ep.max_abs_r && pheno < ep.p_valid) atomicMax(ep.max_abs_r + pheno, __float_as_uint(mx));
+  if (ep.max_abs_r && pheno < ep.p_valid)
+    atomicMax(ep.max_abs_r + pheno, static_cast<unsigned long long>(__double_as_longlong(mx.d)));
 }
 
 constexpr uint32_t kDefaultL2Codes = 1u | (1u << 2);  // panel and genotypes evict_last

@@ -95,7 +95,7 @@ int pg_debug_assoc_gemm(const void* d_qh, const void* d_q1, const void* d_q0, in
   float *mu_f, *iv_f, *sc_f, *cq_f;
   double *mu_d, *iv_d, *sc_d;
   long long* cq;
-  int* cnt;
+  unsigned long long* cnt;
   PG_CUDA_CHECK(cudaMallocAsync(&mu_f, 4 * c_pad, st));
   PG_CUDA_CHECK(cudaMallocAsync(&iv_f, 4 * c_pad, st));
   PG_CUDA_CHECK(cudaMallocAsync(&mu_d, 8 * c_pad, st));
@@ -104,12 +104,12 @@ int pg_debug_assoc_gemm(const void* d_qh, const void* d_q1, const void* d_q0, in
   PG_CUDA_CHECK(cudaMallocAsync(&cq_f, 4 * p_pad, st));
   PG_CUDA_CHECK(cudaMallocAsync(&sc_d, 8 * p_pad, st));
   PG_CUDA_CHECK(cudaMallocAsync(&cq, 8 * p_pad, st));
-  PG_CUDA_CHECK(cudaMallocAsync(&cnt, 4, st));
+  PG_CUDA_CHECK(cudaMallocAsync(&cnt, 8, st));
   PG_CUDA_CHECK(cudaMemsetAsync(mu_f, 0, 4 * c_pad, st));
   PG_CUDA_CHECK(cudaMemsetAsync(mu_d, 0, 8 * c_pad, st));
   PG_CUDA_CHECK(cudaMemsetAsync(cq_f, 0, 4 * p_pad, st));
   PG_CUDA_CHECK(cudaMemsetAsync(cq, 0, 8 * p_pad, st));
-  PG_CUDA_CHECK(cudaMemsetAsync(cnt, 0, 4, st));
+  PG_CUDA_CHECK(cudaMemsetAsync(cnt, 0, 8, st));
   PG_CUDA_CHECK(cudaMemcpyAsync(iv_f, ones_c.data(), 4 * c_pad, cudaMemcpyHostToDevice, st));
   PG_CUDA_CHECK(cudaMemcpyAsync(iv_d, ones_cd.data(), 8 * c_pad, cudaMemcpyHostToDevice, st));
   PG_CUDA_CHECK(cudaMemcpyAsync(sc_f, ones_p.data(), 4 * p_pad, cudaMemcpyHostToDevice, st));

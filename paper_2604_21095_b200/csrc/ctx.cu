@@ -178,7 +178,8 @@ struct pg_ctx {
   bool have_scan = false;
   pg::DBuf<float> rbar;
   pg::DBuf<double> rbar_in;
-  pg::DBuf<unsigned int> max_abs_r;
+  pg::DBuf<unsigned long long> max_abs_r;  // fp64 bits; tracked only when track_max_abs_r
+  bool track_max_abs_r = false;
 
   // batch buffers
   pg::DBuf<uint8_t> packed;
@@ -213,8 +214,12 @@ struct pg_ctx {
   pg::DBuf<int8_t> v, v127;
   pg::DBuf<unsigned long long> cand_key, cand_key_sorted;
   pg::DBuf<double> cand_r, cand_r_sorted, cand_t, cand_p;
+  // effect sizes (pg_ctx_set_beta_scale): sd of each kept residualized phenotype, and the
+  // candidates' beta / se
+  bool beta_on = false;
+  pg::DBuf<double> pheno_sd, cand_beta, cand_se;
   pg::DBuf<int64_t> cand_rows, cand_cols;
-  pg::DBuf<int> cand_count;
+  pg::DBuf<unsigned long long> cand_count;
   pg::DBuf<unsigned long long> counters;  // [0] clamp, [1..2] skip counts, [3] n_ok
   pg::DBuf<uint8_t> sort_tmp;
   pg::DBuf<double> full_r;
@@ -227,6 +232,7 @@ struct pg_ctx {
   int64_t last_m = 0, last_ncand = 0;
   int last_R = 1;
   int64_t cand_capacity = 0;
+  unsigned long long cand_base = 0;  // test hook: initial candidate-counter value (pg_ctx_debug_candidate_base)
   bool fused_decode = true;
   bool wide_digits = true;
 
@@ -312,6 +318,7 @@ int upload_panel_common(pg_ctx* c, const double* d_y, int64_t n_kept, int64_t n_
   c->have_panel = true;
   c->have_scan = false;
   c->have_basis = false;
+  c->beta_on = false;  // phenotype scales belong to the previous panel's columns
   return PG_OK;
 }
 
@@ -324,6 +331,10 @@ int64_t expected_row_bytes(int kind, int64_t n_src) {
     default: return -1;
   }
 }
+
+// Largest candidate count of one batch: the cub sort takes int item counts, and 2^30 pairs
+// already hold ~70 GB of device candidate buffers.
+constexpr int64_t kMaxCandidates = int64_t(1) << 30;
 
 int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t pitch, pg_batch_info* info,
                 int64_t probs_off = 0, int64_t ploidy_off = -1) {
@@ -454,7 +465,7 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
   ep.scale_d = c->scale_d.p;
   ep.cq_f = c->cq_f.p;
   ep.cq = c->cq.p;
-  ep.max_abs_r = c->max_abs_r.p;
+  ep.max_abs_r = c->track_max_abs_r ? c->max_abs_r.p : nullptr;
   PG_CHECK_STATUS(c->cand_count.ensure(1));
   ep.cand_count = c->cand_count.p;
   if (c->k_pad > kSliceK) {  // K-sliced contraction: exact int64 partials per (marker, phenotype)
@@ -469,7 +480,7 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
     ep.full_ld = c->p_pad;
     ep.rbar = nullptr;
     ep.cand_cap = 0;
-    PG_CUDA_CHECK(cudaMemsetAsync(c->cand_count.p, 0, sizeof(int), s));
+    PG_CUDA_CHECK(cudaMemsetAsync(c->cand_count.p, 0, sizeof(unsigned long long), s));
     PG_CUDA_CHECK(cudaEventRecord(c->ev[1], s));
     PG_CHECK_STATUS(run_gemm(ep));
     PG_CUDA_CHECK(cudaEventRecord(c->ev[2], s));
@@ -485,17 +496,28 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
       ep.cand_key = c->cand_key.p;
       ep.cand_r = c->cand_r.p;
       ep.cand_cap = c->cand_capacity;
-      PG_CUDA_CHECK(cudaMemsetAsync(c->cand_count.p, 0, sizeof(int), s));
+      ep.cand_base = c->cand_base;
+      // the 64-bit counter starts at cand_base (0 except under the test hook); slots are
+      // counter - cand_base, so a count that crosses 2^31 inside a launch stays exact
+      PG_CUDA_CHECK(cudaMemcpyAsync(c->cand_count.p, &c->cand_base, sizeof(unsigned long long),
+                                    cudaMemcpyHostToDevice, s));
       PG_CUDA_CHECK(cudaEventRecord(c->ev[1], s));
       PG_CHECK_STATUS(run_gemm(ep));
       PG_CUDA_CHECK(cudaEventRecord(c->ev[2], s));
       ++launches;
-      int hcount = 0;
-      PG_CUDA_CHECK(cudaMemcpyAsync(&hcount, c->cand_count.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+      unsigned long long hcount = 0;
+      PG_CUDA_CHECK(cudaMemcpyAsync(&hcount, c->cand_count.p, sizeof(hcount), cudaMemcpyDeviceToHost, s));
       PG_CUDA_CHECK(cudaStreamSynchronize(s));
-      ncand = hcount;
+      ncand = static_cast<int64_t>(hcount - c->cand_base);
       if (ncand <= c->cand_capacity) break;
-      // overflow: grow to fit and recompute (results are order-independent after the sort)
+      // overflow: grow to fit and recompute (results are order-independent after the sort).
+      // Growth is bounded: the sort takes int item counts and every candidate costs ~64 B of
+      // device buffers, so a batch whose premask admits more than kMaxCandidates pairs is an
+      // error the caller fixes with smaller batches (engine.device_batch_size bounds it).
+      PG_REQUIRE(ncand <= kMaxCandidates, PG_ERR_CONFIG,
+                 "pg_scan: %lld candidate pairs in one batch of %lld markers exceed the limit of %lld; "
+                 "scan smaller batches (expected candidates ~ p_threshold x markers x phenotypes)",
+                 (long long)ncand, (long long)m, (long long)kMaxCandidates);
       const int64_t newcap = ncand + ncand / 8 + 1024;
       PG_CHECK_STATUS(c->cand_key.ensure(newcap));
       PG_CHECK_STATUS(c->cand_r.ensure(newcap));
@@ -518,9 +540,18 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
     PG_CHECK_STATUS(c->sort_tmp.ensure(tmp_bytes));
     PG_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(c->sort_tmp.p, tmp_bytes, c->cand_key.p, c->cand_key_sorted.p,
                                                   c->cand_r.p, c->cand_r_sorted.p, ncand, 0, end_bit, s));
+    BetaArgs beta;
+    if (c->beta_on) {
+      PG_CHECK_STATUS(c->cand_beta.ensure(ncand));
+      PG_CHECK_STATUS(c->cand_se.ensure(ncand));
+      beta.var_m = c->var.p;
+      beta.sd_p = c->pheno_sd.p;
+      beta.beta = c->cand_beta.p;
+      beta.se = c->cand_se.p;
+    }
     PG_CHECK_STATUS(finalize_candidates(c->cand_key_sorted.p, c->cand_r_sorted.p, ncand, c->df, c->cand_rows.p,
                                         c->cand_cols.p, c->cand_r_sorted.p, c->cand_t.p, c->cand_p.p, c->counters.p,
-                                        s));
+                                        beta, s));
     ++launches;
   }
   PG_CUDA_CHECK(cudaEventRecord(c->ev[3], s));
@@ -586,7 +617,7 @@ int pg_ctx_destroy(pg_ctx* c) {
   for (auto* b : {&c->qh, &c->q1, &c->q0, &c->v, &c->v127, &c->skip}) b->release();
   for (auto* b : {&c->scale_d, &c->maxabs, &c->ystage, &c->rbar_in, &c->sum_d, &c->af, &c->var, &c->mu_d,
                   &c->invd_d, &c->cand_r, &c->cand_r_sorted, &c->cand_t, &c->cand_p, &c->full_r, &c->scratch_a,
-                  &c->scratch_b, &c->scratch_c, &c->scratch_d})
+                  &c->scratch_b, &c->scratch_c, &c->scratch_d, &c->pheno_sd, &c->cand_beta, &c->cand_se})
     b->release();
   for (auto* b : {&c->scale_f, &c->cq_f, &c->rbar, &c->mu_f, &c->invd_f}) b->release();
   for (auto* b : {&c->cq, &c->n_miss, &c->s_u, &c->ss_u}) b->release();
@@ -847,6 +878,7 @@ int pg_ctx_import_panel(pg_ctx* c, const void* d_src, int64_t n_kept, int64_t n_
   c->have_panel = true;
   c->have_scan = false;
   c->have_basis = false;
+  c->beta_on = false;  // phenotype scales belong to the previous panel's columns
   return PG_OK;
 }
 
@@ -859,10 +891,11 @@ int pg_ctx_set_scan(pg_ctx* c, double df, int mode, const double* r_bar) {
   PG_REQUIRE(mode == PG_MODE_FULL || r_bar != nullptr, PG_ERR_INVALID, "r_bar required for THRESHOLD/TOPK");
   c->df = df;
   c->mode = mode;
+  c->track_max_abs_r = false;
   PG_CHECK_STATUS(c->rbar.ensure(c->p_pad));
   PG_CHECK_STATUS(c->rbar_in.ensure(c->n_pheno));
   PG_CHECK_STATUS(c->max_abs_r.ensure(c->p_pad));
-  PG_CUDA_CHECK(cudaMemsetAsync(c->max_abs_r.p, 0, sizeof(unsigned) * c->p_pad, c->stream));
+  PG_CUDA_CHECK(cudaMemsetAsync(c->max_abs_r.p, 0, sizeof(unsigned long long) * c->p_pad, c->stream));
   if (r_bar != nullptr) {
     PG_CUDA_CHECK(
         cudaMemcpyAsync(c->rbar_in.p, r_bar, sizeof(double) * c->n_pheno, cudaMemcpyHostToDevice, c->stream));
@@ -914,6 +947,33 @@ int pg_ctx_set_basis(pg_ctx* c, const double* q, int64_t n_kept, int64_t rank) {
   c->bstage.release();
   c->basis_cols = rank - 1;
   c->have_basis = true;
+  return PG_OK;
+}
+
+int pg_ctx_set_beta_scale(pg_ctx* c, const double* pheno_sd, int64_t n_pheno) {
+  PG_CHECK_STATUS(ctx_check(c));
+  if (pheno_sd == nullptr) {
+    c->beta_on = false;
+    return PG_OK;
+  }
+  PG_REQUIRE(c->have_panel, PG_ERR_STATE, "pg_ctx_set_beta_scale: no panel");
+  PG_REQUIRE(n_pheno == c->n_pheno, PG_ERR_INVALID, "pg_ctx_set_beta_scale: %lld scales for %lld phenotypes",
+             (long long)n_pheno, (long long)c->n_pheno);
+  for (int64_t j = 0; j < n_pheno; ++j)
+    PG_REQUIRE(std::isfinite(pheno_sd[j]) && pheno_sd[j] > 0.0, PG_ERR_INVALID,
+               "pg_ctx_set_beta_scale: phenotype %lld has sd %g", (long long)j, pheno_sd[j]);
+  PG_CHECK_STATUS(c->pheno_sd.ensure(c->p_pad));
+  PG_CUDA_CHECK(cudaMemsetAsync(c->pheno_sd.p, 0, sizeof(double) * c->p_pad, c->stream));
+  PG_CUDA_CHECK(
+      cudaMemcpyAsync(c->pheno_sd.p, pheno_sd, sizeof(double) * n_pheno, cudaMemcpyHostToDevice, c->stream));
+  PG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  c->beta_on = true;
+  return PG_OK;
+}
+
+int pg_ctx_debug_candidate_base(pg_ctx* c, uint64_t base) {
+  PG_CHECK_STATUS(ctx_check(c));
+  c->cand_base = base;
   return PG_OK;
 }
 
@@ -1188,9 +1248,10 @@ int pg_fetch_candidates(pg_ctx* c, int64_t* rows, int64_t* cols, double* r, doub
   return PG_OK;
 }
 
-int pg_fetch_full(pg_ctx* c, void* out, int elem_bytes, int64_t* n_rows) {
-  PG_CHECK_STATUS(ctx_check(c));
-  PG_REQUIRE(c->mode == PG_MODE_FULL, PG_ERR_STATE, "pg_fetch_full: ctx not in FULL mode");
+namespace {
+// FULL rows of the last batch: new_row[m] = output row of non-skipped marker m (-1 skipped)
+int full_row_map(pg_ctx* c, const char* who, int elem_bytes, unsigned long long* n_ok) {
+  PG_REQUIRE(c->mode == PG_MODE_FULL, PG_ERR_STATE, "%s: ctx not in FULL mode", who);
   PG_REQUIRE(elem_bytes == 4 || elem_bytes == 8, PG_ERR_INVALID, "elem_bytes must be 4 or 8");
   const int64_t m = c->last_m;
   PG_REQUIRE(m > 0, PG_ERR_STATE, "no scanned batch");
@@ -1199,9 +1260,18 @@ int pg_fetch_full(pg_ctx* c, void* out, int elem_bytes, int64_t* n_rows) {
   PG_CUDA_CHECK(cudaMemsetAsync(c->counters.p + 3, 0, sizeof(unsigned long long), s));
   row_map_kernel<<<1, 1024, 0, s>>>(c->skip.p, m, c->new_row.p, c->counters.p + 3);
   PG_CUDA_CHECK(cudaGetLastError());
-  unsigned long long n_ok = 0;
-  PG_CUDA_CHECK(cudaMemcpyAsync(&n_ok, c->counters.p + 3, 8, cudaMemcpyDeviceToHost, s));
+  PG_CUDA_CHECK(cudaMemcpyAsync(n_ok, c->counters.p + 3, 8, cudaMemcpyDeviceToHost, s));
   PG_CUDA_CHECK(cudaStreamSynchronize(s));
+  return PG_OK;
+}
+}  // namespace
+
+int pg_fetch_full(pg_ctx* c, void* out, int elem_bytes, int64_t* n_rows) {
+  PG_CHECK_STATUS(ctx_check(c));
+  unsigned long long n_ok = 0;
+  PG_CHECK_STATUS(full_row_map(c, "pg_fetch_full", elem_bytes, &n_ok));
+  const int64_t m = c->last_m;
+  cudaStream_t s = c->stream;
   if (n_rows) *n_rows = static_cast<int64_t>(n_ok);
   if (out == nullptr || n_ok == 0) return PG_OK;
   const size_t bytes = static_cast<size_t>(n_ok) * c->n_pheno * elem_bytes;
@@ -1213,18 +1283,50 @@ int pg_fetch_full(pg_ctx* c, void* out, int elem_bytes, int64_t* n_rows) {
   return PG_OK;
 }
 
+int pg_fetch_full_beta(pg_ctx* c, void* out, int elem_bytes, int64_t* n_rows) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(c->beta_on, PG_ERR_STATE, "pg_fetch_full_beta: effect sizes not enabled (pg_ctx_set_beta_scale)");
+  unsigned long long n_ok = 0;
+  PG_CHECK_STATUS(full_row_map(c, "pg_fetch_full_beta", elem_bytes, &n_ok));
+  if (n_rows) *n_rows = static_cast<int64_t>(n_ok);
+  if (out == nullptr || n_ok == 0) return PG_OK;
+  cudaStream_t s = c->stream;
+  const size_t bytes = static_cast<size_t>(n_ok) * c->n_pheno * elem_bytes;
+  PG_CHECK_STATUS(c->full_out.ensure(bytes));
+  PG_CHECK_STATUS(full_rows_to_beta(c->full_r.p, c->last_m, c->p_pad, c->n_pheno, c->new_row.p, c->df, elem_bytes,
+                                    c->full_out.p, c->var.p, c->pheno_sd.p, s));
+  PG_CUDA_CHECK(cudaMemcpyAsync(out, c->full_out.p, bytes, cudaMemcpyDeviceToHost, s));
+  PG_CUDA_CHECK(cudaStreamSynchronize(s));
+  return PG_OK;
+}
+
+int pg_fetch_candidate_beta(pg_ctx* c, double* beta, double* se) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(c->beta_on, PG_ERR_STATE,
+             "pg_fetch_candidate_beta: effect sizes not enabled (pg_ctx_set_beta_scale)");
+  const int64_t n = c->last_ncand;
+  if (n == 0) return PG_OK;
+  if (beta) PG_CUDA_CHECK(cudaMemcpyAsync(beta, c->cand_beta.p, 8 * n, cudaMemcpyDeviceToHost, c->stream));
+  if (se) PG_CUDA_CHECK(cudaMemcpyAsync(se, c->cand_se.p, 8 * n, cudaMemcpyDeviceToHost, c->stream));
+  PG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  return PG_OK;
+}
+
 int pg_fetch_max_abs_r(pg_ctx* c, double* out) {
   PG_CHECK_STATUS(ctx_check(c));
   PG_REQUIRE(c->have_scan, PG_ERR_STATE, "no scan");
-  std::vector<unsigned> bits(c->n_pheno);
-  PG_CUDA_CHECK(
-      cudaMemcpyAsync(bits.data(), c->max_abs_r.p, sizeof(unsigned) * c->n_pheno, cudaMemcpyDeviceToHost, c->stream));
+  PG_REQUIRE(c->track_max_abs_r, PG_ERR_STATE, "pg_fetch_max_abs_r: tracking not enabled (pg_ctx_track_max_abs_r)");
+  static_assert(sizeof(double) == sizeof(unsigned long long), "fp64 bits");
+  PG_CUDA_CHECK(cudaMemcpyAsync(out, c->max_abs_r.p, sizeof(double) * c->n_pheno, cudaMemcpyDeviceToHost, c->stream));
   PG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
-  for (int64_t i = 0; i < c->n_pheno; ++i) {
-    float f;
-    std::memcpy(&f, &bits[i], 4);
-    out[i] = f;
-  }
+  return PG_OK;
+}
+
+int pg_ctx_track_max_abs_r(pg_ctx* c, int enable) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(c->have_scan, PG_ERR_STATE, "pg_ctx_track_max_abs_r: call after pg_ctx_set_scan");
+  c->track_max_abs_r = enable != 0;
+  PG_CUDA_CHECK(cudaMemsetAsync(c->max_abs_r.p, 0, sizeof(unsigned long long) * c->p_pad, c->stream));
   return PG_OK;
 }
 

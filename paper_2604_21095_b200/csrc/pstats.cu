@@ -102,9 +102,23 @@ __device__ __forceinline__ double t_from_r_dev(double r, double df) {
   return sg * a * sqrt(df / (1.0 - a * a));
 }
 
+// Effect size on the phenotype's scale (north star: beta / t / -log10 p). With r the
+// correlation of the (imputed, centred[, projected]) dosage g with the residualized
+// phenotype y_res, the slope of y_res on g is beta = r * sd(y_res) / sd(g) and its standard
+// error se = sd(y_res) / sd(g) * sqrt((1 - r^2) / df), so beta / se == t exactly as
+// t_from_r defines it. Extension mode + adjusted df: the Frisch-Waugh-Lovell identity makes
+// these the full OLS estimates of y ~ 1 + C + g (oracle.ols_single, oracle.py:35-90).
+__device__ __forceinline__ void beta_se(double r, double t, double var_m, double sd_p, double df, double& b,
+                                        double& se) {
+  const double ratio = sd_p / sqrt(var_m);
+  b = r * ratio;
+  const double a = fmin(fabs(r), kRCap);
+  se = isinf(t) ? 0.0 : ratio * sqrt((1.0 - a * a) / df);
+}
+
 __global__ void finalize_kernel(const unsigned long long* __restrict__ key, const double* __restrict__ r_in,
                                 int64_t n, double df, int64_t* rows, int64_t* cols, double* r_out, double* t_out,
-                                double* p_out, unsigned long long* clamp) {
+                                double* p_out, unsigned long long* clamp, BetaArgs beta) {
   unsigned long long nclamp = 0;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -119,6 +133,12 @@ __global__ void finalize_kernel(const unsigned long long* __restrict__ key, cons
     r_out[i] = r;
     t_out[i] = t;
     p_out[i] = p_from_t_arr(t, df, nullptr);
+    if (beta.beta) {
+      double b, se;
+      beta_se(r, t, beta.var_m[rows[i]], beta.sd_p[cols[i]], df, b, se);
+      beta.beta[i] = b;
+      beta.se[i] = se;
+    }
   }
   if (nclamp) atomicAdd(clamp, nclamp);
 }
@@ -143,6 +163,26 @@ __global__ void full_t_kernel(const double* __restrict__ r, int64_t m, int64_t l
       reinterpret_cast<double*>(out)[dst * n_pheno + p] = t;
   }
   if (nclamp) atomicAdd(clamp, nclamp);
+}
+
+// FULL mode beta rows: out[new_row(m), p] = beta(r[m, p]) for non-skipped markers
+__global__ void full_beta_kernel(const double* __restrict__ r, int64_t m, int64_t ld, int64_t n_pheno,
+                                 const int64_t* __restrict__ new_row, double df, int elem_bytes, void* out,
+                                 const double* __restrict__ var_m, const double* __restrict__ sd_p) {
+  const int64_t row = blockIdx.x;
+  const int64_t dst = new_row[row];
+  if (dst < 0) return;
+  const double vm = var_m[row];
+  for (int64_t p = threadIdx.x; p < n_pheno; p += blockDim.x) {
+    double v = r[row * ld + p];
+    if (fabs(v) > 1.0) v = v > 0.0 ? 1.0 : -1.0;
+    double b, se;
+    beta_se(v, t_from_r_dev(v, df), vm, sd_p[p], df, b, se);
+    if (elem_bytes == 4)
+      reinterpret_cast<float*>(out)[dst * n_pheno + p] = static_cast<float>(b);
+    else
+      reinterpret_cast<double*>(out)[dst * n_pheno + p] = b;
+  }
 }
 
 __global__ void t_from_r_kernel(const double* r, int64_t n, double df, double* t) {
@@ -208,9 +248,10 @@ unsigned grid_for(int64_t n, int threads) {
 
 int finalize_candidates(const unsigned long long* key, const double* r_in, int64_t n, double df, int64_t* rows,
                         int64_t* cols, double* r_out, double* t_out, double* p_out, unsigned long long* clamp,
-                        cudaStream_t s) {
+                        const BetaArgs& beta, cudaStream_t s) {
   if (n <= 0) return PG_OK;
-  finalize_kernel<<<grid_for(n, 256), 256, 0, s>>>(key, r_in, n, df, rows, cols, r_out, t_out, p_out, clamp);
+  finalize_kernel<<<grid_for(n, 256), 256, 0, s>>>(key, r_in, n, df, rows, cols, r_out, t_out, p_out, clamp,
+                                                   beta);
   PG_CUDA_CHECK(cudaGetLastError());
   return PG_OK;
 }
@@ -219,6 +260,15 @@ int full_rows_to_t(const double* r, int64_t m, int64_t ld, int64_t n_pheno, cons
                    int elem_bytes, void* out, unsigned long long* clamp, cudaStream_t s) {
   if (m <= 0) return PG_OK;
   full_t_kernel<<<static_cast<unsigned>(m), 256, 0, s>>>(r, m, ld, n_pheno, new_row, df, elem_bytes, out, clamp);
+  PG_CUDA_CHECK(cudaGetLastError());
+  return PG_OK;
+}
+
+int full_rows_to_beta(const double* r, int64_t m, int64_t ld, int64_t n_pheno, const int64_t* new_row, double df,
+                      int elem_bytes, void* out, const double* var_m, const double* sd_p, cudaStream_t s) {
+  if (m <= 0) return PG_OK;
+  full_beta_kernel<<<static_cast<unsigned>(m), 256, 0, s>>>(r, m, ld, n_pheno, new_row, df, elem_bytes, out, var_m,
+                                                            sd_p);
   PG_CUDA_CHECK(cudaGetLastError());
   return PG_OK;
 }

@@ -114,6 +114,30 @@ int pg_format_float_repr(const double* x, int64_t n, char* out, int64_t out_cap,
   return PG_OK;
 }
 
+// n lines of ncols tab-separated floats (Python repr), line i = cols[0][i] \t ... cols[ncols-1][i] \n
+// (the effect-size sidecar of the record writers: BETA \t SE per record line).
+int pg_format_float_columns(int64_t n, int ncols, const double* const* cols, char* out, int64_t out_cap,
+                            int64_t* out_len) {
+  int64_t o = 0;
+  if (ncols < 1) {
+    pg::set_error("pg_format_float_columns: ncols must be >= 1");
+    return PG_ERR_INVALID;
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    if (o + 40 * static_cast<int64_t>(ncols) > out_cap) {
+      *out_len = o;
+      pg::set_error("pg_format_float_columns: output buffer too small at line %lld", (long long)i);
+      return PG_ERR_INVALID;
+    }
+    for (int j = 0; j < ncols; ++j) {
+      o += pg::py_repr(cols[j][i], out + o);
+      out[o++] = j + 1 < ncols ? '\t' : '\n';
+    }
+  }
+  *out_len = o;
+  return PG_OK;
+}
+
 // One TSV line per record: <marker prefix>AF\tN_MISS<mid>R\tT\tP\t<pheno>\n
 //   marker prefix of row k = prefix_blob[prefix_off[k] : prefix_off[k+1]]  ("CHR\tID\tPOS\tA1\tA2\t")
 //   pheno name of col j    = pheno_blob[pheno_off[j] : pheno_off[j+1]]

@@ -77,16 +77,18 @@ def shard_path(out_path: Path, rank: int) -> Path:
     return Path(f"{out_path}.rank{rank}")
 
 
-def merge_tsv(shards: list[Path], out_path: Path) -> int:
-    """Concatenate THRESHOLD shard TSVs (header once) in rank order; returns records."""
+def merge_tsv(shards: list[Path], out_path: Path, header: str | None = None) -> int:
+    """Concatenate line-oriented shard files (header once) in rank order; returns data lines.
+
+    Used for THRESHOLD record TSVs and their line-aligned .beta.tsv sidecars."""
+    want = header if header is not None else "\t".join(output.TSV_COLUMNS)
     n = 0
     with open(out_path, "w") as out:
-        out.write("\t".join(output.TSV_COLUMNS) + "\n")
+        out.write(want + "\n")
         for p in shards:
             with open(p) as fh:
-                header = fh.readline()
-                if header.rstrip("\n").split("\t") != list(output.TSV_COLUMNS):
-                    raise PanelGwasError(f"{p}: not a panelgwas TSV shard")
+                if fh.readline().rstrip("\n") != want:
+                    raise PanelGwasError(f"{p}: not a panelgwas shard of this kind")
                 for line in fh:
                     out.write(line)
                     n += 1
@@ -94,35 +96,68 @@ def merge_tsv(shards: list[Path], out_path: Path) -> int:
 
 
 def merge_topk(shards: list[Path], out_path: Path, top_k: int, phenotype_names: list[str],
-               source_index_of: dict[str, int]) -> int:
-    """Per phenotype keep the k best of all shard records by (p, marker source index)."""
-    recs = []
-    for p in shards:
-        recs.extend(output.load_association_records(p))
-    lines_of = {}
-    for p in shards:
-        with open(p) as fh:
-            fh.readline()
-            for line in fh:
-                f = line.rstrip("\n").split("\t")
-                lines_of[(f[1], f[12])] = line
+               effect_sizes: bool = False) -> int:
+    """Per phenotype keep the k best shard records by (p, marker source index).
+
+    Shard r holds the contiguous marker block [start_r, stop_r) and writes its records in
+    (phenotype, p, source index) order, so (phenotype, p, rank, line) orders the union exactly
+    as (phenotype, p, source index) would: no lookup by marker ID (IDs may repeat, e.g. '.').
+    The optional .beta.tsv sidecars follow the same permutation."""
     col = {name: j for j, name in enumerate(phenotype_names)}
-    recs.sort(key=lambda r: (col[r.phenotype], r.p, source_index_of[r.id]))
-    n = 0
-    taken: dict[str, int] = {}
+    keys, lines, betas = [], [], []
+    for rank, p in enumerate(shards):
+        with open(p) as fh:
+            if fh.readline().rstrip("\n").split("\t") != list(output.TSV_COLUMNS):
+                raise PanelGwasError(f"{p}: not a panelgwas TSV shard")
+            shard_lines = fh.readlines()
+        if effect_sizes:
+            with open(output.beta_sidecar(p)) as fh:
+                fh.readline()
+                shard_betas = fh.readlines()
+            if len(shard_betas) != len(shard_lines):
+                raise PanelGwasError(f"{p}: effect-size sidecar is not aligned with the records")
+            betas.extend(shard_betas)
+        for i, line in enumerate(shard_lines):
+            f = line.rstrip("\n").split("\t")
+            keys.append((col[f[12]], float(f[11]), rank, i))
+        lines.extend(shard_lines)
+    order = sorted(range(len(keys)), key=keys.__getitem__)
+    taken: dict[int, int] = {}
+    chosen = []
+    for i in order:
+        c = keys[i][0]
+        if taken.get(c, 0) < top_k:
+            taken[c] = taken.get(c, 0) + 1
+            chosen.append(i)
     with open(out_path, "w") as out:
         out.write("\t".join(output.TSV_COLUMNS) + "\n")
-        for r in recs:
-            if taken.get(r.phenotype, 0) >= top_k:
-                continue
-            taken[r.phenotype] = taken.get(r.phenotype, 0) + 1
-            out.write(lines_of[(r.id, r.phenotype)])
-            n += 1
-    return n
+        out.writelines(lines[i] for i in chosen)
+    if effect_sizes:
+        with open(output.beta_sidecar(out_path), "w") as out:
+            out.write("\t".join(output.BETA_COLUMNS) + "\n")
+            out.writelines(betas[i] for i in chosen)
+    return len(chosen)
 
 
-def merge_full(shards: list[Path], out_path: Path) -> int:
-    """Concatenate FULL shard matrices (rank order) and their marker sidecars; patch the row count."""
+def merge_qc(shards: list[Path], out_path: Path) -> int:
+    """QC sidecars: every shard's skipped-marker rows in rank order, then the phenotype rows
+    (identical in every shard: the panel is shared) once, as a single-GPU scan writes them."""
+    markers, phenos = [], None
+    for p in shards:
+        with open(p) as fh:
+            header = fh.readline()
+            rows = fh.readlines()
+        markers.extend(r for r in rows if r.startswith("marker\t"))
+        if phenos is None:
+            phenos = [r for r in rows if r.startswith("phenotype\t")]
+    with open(out_path, "w") as out:
+        out.write(header)
+        out.writelines(markers)
+        out.writelines(phenos or [])
+    return len(markers)
+
+
+def _concat_full_matrices(shards: list[Path], out_path: Path) -> int:
     header = struct.Struct("<16sIQQI")
     rows = 0
     with open(out_path, "wb") as out:
@@ -137,6 +172,15 @@ def merge_full(shards: list[Path], out_path: Path) -> int:
             rows += m
         out.seek(len(output.FULL_MAGIC) + 4)
         out.write(struct.pack("<Q", rows))
+    return rows
+
+
+def merge_full(shards: list[Path], out_path: Path, effect_sizes: bool = False) -> int:
+    """Concatenate FULL shard matrices (rank order) and their marker sidecars; patch the row count."""
+    rows = _concat_full_matrices(shards, out_path)
+    if effect_sizes:
+        _concat_full_matrices([output.beta_sidecar(p, full=True) for p in shards],
+                              output.beta_sidecar(out_path, full=True))
     side = Path(str(out_path) + ".markers.tsv")
     with open(side, "w") as out:
         out.write("SOURCE_INDEX\tCHR\tID\tPOS\tA1\tA2\tAF\tN_MISS\n")
@@ -171,6 +215,17 @@ def merge_min_p(shards: list[Path], out_path: Path) -> int:
 
 
 # ----------------------------------------------------------------------------- the distributed scan
+def object_group(dist):
+    """Process group for the pickled host collectives (panel metadata, flags, summaries).
+
+    Under NCCL those would be staged through device memory and serialised with the data
+    path; a gloo group keeps them on the host so the NCCL communicator carries only the
+    one panel broadcast. Returns None (the default group) when the default is already gloo."""
+    if dist.get_backend() == "gloo":
+        return None
+    return dist.new_group(backend="gloo")
+
+
 def run_scan_distributed(config):
     """torchrun entry: every rank scans its marker shard; rank 0 merges and writes the summary."""
     import torch
@@ -196,9 +251,11 @@ def run_scan_distributed(config):
         else:
             dist.init_process_group(backend)
     torch.cuda.set_device(local)
+    objs = object_group(dist)
     src = open_genotype_source(config.source)
     try:
         n_markers = src.n_markers
+        n_src = src.n_samples
     finally:
         src.close()
     start, stop = shard_span(n_markers, world, rank)
@@ -207,8 +264,9 @@ def run_scan_distributed(config):
     dev = torch.device("cuda", local)
 
     def panel_hook(ctx, prep):
-        # rank 0 prepares + quantizes the panel on its GPU; the zero-variance flags and
-        # the quantized limbs reach the other GPUs in two broadcasts (NCCL)
+        # rank 0 prepares + quantizes the panel on its GPU; the zero-variance flags and the
+        # phenotype scales go to the other ranks over the host group, the quantized limbs in
+        # the one NCCL broadcast
         from .engine import stage_panel
 
         err = None
@@ -217,20 +275,19 @@ def run_scan_distributed(config):
                 stage_panel(ctx, prep, n_src)
             except Exception as exc:  # tell the other ranks before re-raising
                 err = exc
-        flags = [(prep.zero_variance, None if err is None else f"{type(err).__name__}: {err}") if rank == 0 else None]
-        dist.broadcast_object_list(flags, 0)
+        box = [(prep.zero_variance, prep.pheno_sd, None if err is None else f"{type(err).__name__}: {err}")
+               if rank == 0 else None]
+        dist.broadcast_object_list(box, 0, group=objs)
         if err is not None:
             raise err
-        if flags[0][1] is not None:
-            raise PanelGwasError(f"rank 0 panel preparation failed: {flags[0][1]}")
+        if box[0][2] is not None:
+            raise PanelGwasError(f"rank 0 panel preparation failed: {box[0][2]}")
         if rank != 0:
-            prep.set_flags(flags[0][0])
+            prep.set_flags(box[0][0])
+            prep.pheno_sd = box[0][1]
         broadcast_panel(ctx, torch, dist, rank, prep.align.n_kept, len(prep.pheno_names),
                         prep.align.genotype_row_index, n_src, dev)
 
-    src = open_genotype_source(config.source)
-    n_src = src.n_samples
-    src.close()
     def prep_hook(source):
         # rank 0 parses the phenotype / covariate tables and sends the small metadata; the
         # other ranks never read the (multi-GB) tables
@@ -242,7 +299,7 @@ def run_scan_distributed(config):
             except Exception as exc:
                 err = exc
         box = [(meta, None if err is None else f"{type(err).__name__}: {err}") if rank == 0 else None]
-        dist.broadcast_object_list(box, 0)
+        dist.broadcast_object_list(box, 0, group=objs)
         if err is not None:
             raise err
         if box[0][1] is not None:
@@ -256,26 +313,24 @@ def run_scan_distributed(config):
     if stop <= start:
         summary = None
     gathered = [None] * world
-    dist.all_gather_object(gathered, (summary.to_dict(), summary.phenotype_names) if summary else None)
+    dist.all_gather_object(gathered, (summary.to_dict(), summary.phenotype_names) if summary else None, group=objs)
     names_of = next((g[1] for g in gathered if g is not None), [])
     gathered = [g[0] if g is not None else None for g in gathered]
     result = None
     if rank == 0:
-        shards = [shard_path(Path(config.out_path), r) for r in range(world) if gathered[r] is not None]
+        out = Path(config.out_path)
+        shards = [shard_path(out, r) for r in range(world) if gathered[r] is not None]
         first = next(g for g in gathered if g is not None)
+        beta = config.effect_sizes
         if config.output_mode is engine.OutputMode.FULL:
-            records = merge_full(shards, Path(config.out_path)) * first["phenotypes_scanned"]
+            records = merge_full(shards, out, effect_sizes=beta) * first["phenotypes_scanned"]
         elif config.output_mode is engine.OutputMode.TOPK:
-            with open(shards[0]) as fh:
-                fh.readline()
-            src = open_genotype_source(config.source)
-            try:
-                index = {m.id: m.source_index for m in src.marker_catalog}
-            finally:
-                src.close()
-            records = merge_topk(shards, Path(config.out_path), config.top_k, names_of, index)
+            records = merge_topk(shards, out, config.top_k, names_of, effect_sizes=beta)
         else:
-            records = merge_tsv(shards, Path(config.out_path))
+            records = merge_tsv(shards, out)
+            if beta:
+                merge_tsv([output.beta_sidecar(p) for p in shards], output.beta_sidecar(out),
+                          header="\t".join(output.BETA_COLUMNS))
         total = dict(first)
         for key in ("markers_scanned", "markers_skipped_monomorphic", "markers_skipped_all_missing", "clamp_count",
                     "p_underflow_count"):
@@ -283,21 +338,24 @@ def run_scan_distributed(config):
         total["n_markers"] = n_markers
         total["records_emitted"] = records
         if config.min_p_sidecar:
-            merge_min_p([Path(str(p) + ".minp.tsv") for p in shards], Path(str(config.out_path) + ".minp.tsv"))
+            merge_min_p([Path(str(p) + ".minp.tsv") for p in shards], Path(str(out) + ".minp.tsv"))
+        if config.qc_sidecar:
+            merge_qc([Path(str(p) + ".qc.tsv") for p in shards], Path(str(out) + ".qc.tsv"))
         for key in ("time_decode_s", "time_prepare_s", "time_correlate_s", "time_emit_s", "wall_s"):
             total[key] = max(g[key] for g in gathered if g is not None)
         import json
 
-        with open(Path(str(config.out_path) + ".summary.json"), "w") as fh:
+        with open(Path(str(out) + ".summary.json"), "w") as fh:
             json.dump(total, fh, indent=2, sort_keys=True)
             fh.write("\n")
-        for p in [shard_path(Path(config.out_path), r) for r in range(world)]:
-            for suffix in ("", ".summary.json", ".markers.tsv", ".phenotypes.txt", ".qc.tsv", ".minp.tsv"):
+        for p in [shard_path(out, r) for r in range(world)]:
+            for suffix in ("", ".summary.json", ".markers.tsv", ".phenotypes.txt", ".qc.tsv", ".minp.tsv",
+                           ".beta.tsv", ".beta.bin"):
                 q = Path(str(p) + suffix)
                 if q.exists():
                     q.unlink()
         result = total
-    dist.barrier()
+    dist.barrier(group=objs)
     return result
 
 

@@ -69,6 +69,10 @@ _PLINK_DEVICE_BATCH = 65536
 _SLICE_SAMPLES = 131072  # csrc/assoc.cuh kSliceK
 _MAX_GEMM_ROWS = 1 << 17
 _MAX_FULL_BYTES = 2 << 30
+# candidate pairs one device batch may produce (each costs ~64 B of device buffers + 40 B of
+# host arrays): THRESHOLD / TOPK batches are sized so the expected count stays below this
+# (the native hard limit, ctx.cu kMaxCandidates, is 8x higher)
+_CAND_BUDGET = 1 << 27
 
 _MODE_CODE = {
     OutputMode.THRESHOLD: _native.PG_MODE_THRESHOLD,
@@ -103,6 +107,8 @@ class ScanConfig:
     allow_large_full: bool = False
     qc_sidecar: bool = False
     min_p_sidecar: bool = False  # engine extension: <out>.minp.tsv, per-phenotype max |t| / min p
+    # engine extension: per-record effect size and standard error (<out>.beta.tsv / .beta.bin)
+    effect_sizes: bool = False
     summary_to_stderr: bool = True
     device: int | None = None
     # markers per device launch; None = sized automatically (results do not depend on it)
@@ -201,13 +207,16 @@ def topk_batch_bars(writer, top_k: int, batch_markers: int, t_floor: float, df: 
     reference's rule, engine.py:205-211). A phenotype still short of k records would admit
     every marker (the reference's per-4,096-marker batches can afford that; a 65,536-marker
     device batch x 20,480 phenotypes cannot), so its bar is the null quantile at
-    p = max(4, 32 / k) * missing / batch: all markers beating the batch's k-th best are then
-    above the bar whenever at least `missing` candidates pass, which the caller checks (and
-    rescans the batch without a bar for any phenotype that falls short)."""
+    p = max(4, 32 / k) * k / batch: all markers beating the batch's k-th best are then above
+    the bar whenever at least k candidates pass, which the caller checks (and rescans the
+    batch without a bar for any phenotype that falls short)."""
     bars = topk_premask(writer.worst_abs_t, t_floor, df)
     kept = writer.kept_counts()
     short = kept < top_k
-    need = np.where(short, top_k - kept, 0)
+    # a short phenotype needs the batch's own k best above its bar, not just k - kept: a
+    # marker under the bar could still beat a weak held record otherwise. With >= k batch
+    # candidates above the bar, every marker below it has k better records and cannot enter.
+    need = np.where(short, top_k, 0)
     # expected null candidates per phenotype: factor x missing slots (>= 32), so falling short
     # needs a Poisson(>= 32) draw below `missing` (rescans stay rare) while the first batch
     # of a C3-sized scan admits ~k x max(4, ...) candidates per phenotype, not 65,536
@@ -227,6 +236,21 @@ def _free_pinned(bufs) -> None:
         b.close()
 
 
+def expected_candidates_per_marker(config: ScanConfig, batch: int, n_pheno: int) -> int:
+    """Upper estimate of the premask's candidate pairs per marker of a `batch`-marker launch.
+
+    THRESHOLD: the null admits ~p_threshold of the pairs (the bar is p_threshold's |r|,
+    engine.py:321-330 of the reference); x4 headroom for real signal, and every pair at p = 1.
+    TOPK: the first batch's null-quantile bars admit ~max(4k, 32) markers per phenotype
+    (topk_batch_bars), or the whole batch when that is larger."""
+    n_pheno = max(1, n_pheno)
+    if config.output_mode is OutputMode.TOPK:
+        per_pheno = min(batch, 2 * max(4 * config.top_k, 32))
+        return -(-per_pheno * n_pheno // max(batch, 1))
+    frac = min(1.0, 4.0 * config.p_threshold + 1e-6)
+    return max(1, int(np.ceil(frac * n_pheno)))
+
+
 def device_batch_size(config: ScanConfig, n_markers: int, n_pheno: int, n_samples: int = 0) -> int:
     """Markers per device launch: at least the configured batch, sized for the GEMM, memory-bounded."""
     if config.device_batch is not None:
@@ -241,6 +265,8 @@ def device_batch_size(config: ScanConfig, n_markers: int, n_pheno: int, n_sample
     b = min(b, _MAX_GEMM_ROWS if plink else _MAX_GEMM_ROWS // (4 if wide else 16))
     if config.output_mode is OutputMode.FULL:
         b = min(b, max(256, _MAX_FULL_BYTES // (8 * max(n_pheno, 1))))
+    else:
+        b = min(b, max(256, _CAND_BUDGET // max(1, expected_candidates_per_marker(config, b, n_pheno))))
     if n_samples > _SLICE_SAMPLES:  # K-sliced device runs hold 16 B of partials per test
         b = min(b, max(256, _MAX_FULL_BYTES * 2 // (16 * max(n_pheno, 1))))
     return max(1, min(b, n_markers))
@@ -255,6 +281,7 @@ class _PreparedPanel:
     pheno_names: list[str] = field(default_factory=list)
     zero_variance: np.ndarray | None = None
     kept_cols: np.ndarray | None = None
+    pheno_sd: np.ndarray | None = None  # sd (1/N) of each scanned residualized phenotype (effect sizes)
 
     def set_flags(self, zero_variance: np.ndarray) -> None:
         self.zero_variance = np.asarray(zero_variance, dtype=bool)
@@ -309,9 +336,10 @@ def panel_from_metadata(meta: dict) -> _PreparedPanel:
 
 def stage_panel(ctx, prep: _PreparedPanel, n_samples_src: int, commit: bool = True) -> None:
     """Device panel preparation (pg_ctx_prepare_panel) + quantization of the kept columns."""
-    flat, _sd = ctx.prepare_panel(prep.panel.y, prep.basis.q)
+    flat, sd = ctx.prepare_panel(prep.panel.y, prep.basis.q)
     prep.panel.state = PanelState.STANDARDIZED
     prep.set_flags(flat)
+    prep.pheno_sd = np.ascontiguousarray(sd[prep.kept_cols])
     if commit:
         ctx.commit_panel(prep.kept_cols, prep.align.genotype_row_index, n_samples_src)
 
@@ -409,12 +437,16 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, init, ctx_fut, mark
                     f"FULL output would be ~{projected} bytes, over the {config.full_byte_budget}-byte budget; "
                     "pass the large-output override to proceed"
                 )
-            writer = output.FullMatrixWriter(config.out_path, dtype, df, n, source.counts_allele1, names)
+            writer = output.FullMatrixWriter(config.out_path, dtype, df, n, source.counts_allele1, names,
+                                             effect_sizes=config.effect_sizes)
         elif config.output_mode is OutputMode.TOPK:
-            writer = output.TopKWriter(config.out_path, config.top_k, df, n, source.counts_allele1, names)
+            writer = output.TopKWriter(config.out_path, config.top_k, df, n, source.counts_allele1, names,
+                                       effect_sizes=config.effect_sizes)
         else:
             writer = output.ThresholdWriter(config.out_path, config.p_threshold, df, n, source.counts_allele1,
-                                            names)
+                                            names, effect_sizes=config.effect_sizes)
+        if config.effect_sizes:
+            ctx.set_beta_scale(prep.pheno_sd)
     except BaseException:
         try:
             _free_pinned(ring_fut.result())
@@ -438,6 +470,8 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, init, ctx_fut, mark
         else:
             rbar = None
         ctx.set_scan(df, _MODE_CODE[config.output_mode], rbar)
+        if config.min_p_sidecar:
+            ctx.track_max_abs_r(True)
 
         skip_mono = skip_missing = clamp_total = 0
         t_decode = t_prepare = t_corr = t_emit = 0.0
@@ -506,7 +540,8 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, init, ctx_fut, mark
             rows_ = np.concatenate([res.cand_rows[keep_old], extra.cand_rows])
             cols_ = np.concatenate([res.cand_cols[keep_old], extra.cand_cols])
             order = np.lexsort((cols_, rows_))  # (marker, phenotype) order
-            for name in ("cand_r", "cand_t", "cand_p"):
+            names_ = ("cand_r", "cand_t", "cand_p") + (("cand_beta", "cand_se") if config.effect_sizes else ())
+            for name in names_:
                 setattr(res, name, np.concatenate([getattr(res, name)[keep_old], getattr(extra, name)])[order])
             res.cand_rows, res.cand_cols = rows_[order], cols_[order]
             return res
@@ -521,7 +556,7 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, init, ctx_fut, mark
                 markers=markers, allele_frequency=res.af, missing_count=res.missing_count,
                 skip_reason=res.skip, clamp_count=res.clamp_count, cand_rows=res.cand_rows,
                 cand_cols=res.cand_cols, cand_r=res.cand_r, cand_t=res.cand_t, t_rows=res.t_rows,
-                cand_p=res.cand_p,
+                cand_p=res.cand_p, cand_beta=res.cand_beta, cand_se=res.cand_se, beta_rows=res.beta_rows,
             )
             clamp_total += res.clamp_count
             skip_mono += int(np.count_nonzero(res.skip == SkipReason.MONOMORPHIC))

@@ -178,15 +178,68 @@ def make_bgen() -> None:
     np.savez_compressed(OUT / "bgen.npz", **out)
 
 
+def make_ols() -> None:
+    """Effect sizes from the reference's own per-pair OLS (oracle.ols_single, oracle.py:35-90)
+    on the s1 and c1 cohorts: y ~ 1 + C + g (the extension-mode / adjusted-df target) and the
+    marginal slope of the covariate-residualized phenotype y_res ~ 1 + g (the paper-mode
+    target), g mean-imputed as prepare_genotype_batch does (kernel.py:392-408)."""
+    rng = np.random.default_rng(2024)
+    out = {}
+    with tempfile.TemporaryDirectory() as tmp:
+        tmp = Path(tmp)
+        for name, kw, n_pairs in (("s1", S1_SPEC, 1200), ("c1", C1_SPEC, 400)):
+            spec = ref.SimSpec(**kw)
+            cohort = ref.simulate_cohort(spec, tmp / name)
+            n, m = spec.n_samples, spec.n_markers
+            ids = [f"S{i + 1}" for i in range(n)]
+            src = ref.PlinkSource(cohort.bed_path, cohort.bim_path, cohort.fam_path)
+            dos = src.read_marker_batch(0, m).dosages
+            src.close()
+            ptab = ref.load_table(cohort.pheno_path)
+            ctab = ref.load_table(cohort.covar_path)
+            align = ref.align_samples(ids, ptab, ctab)
+            y = ref.build_panel(ptab, align).y
+            c = ref.covariate_matrix(ctab, align)
+            basis = rk.build_covariate_basis(c, True)
+            y_res = rk.residualize(y, basis)
+            rows = rng.integers(0, m, n_pairs)
+            cols = rng.integers(0, spec.n_phenotypes, n_pairs)
+            res = {"beta_adj": [], "se_adj": [], "t_adj": [], "beta_paper": [], "se_paper": [], "t_paper": []}
+            for i, j in zip(rows.tolist(), cols.tolist()):
+                g = dos[i].copy()
+                miss = np.isnan(g)
+                g[miss] = g[~miss].mean()
+                a = ref.ols_single(y[:, j], g, c)
+                b = ref.ols_single(y_res[:, j], g)
+                for key, o in (("adj", a), ("paper", b)):
+                    res[f"beta_{key}"].append(o.beta)
+                    res[f"se_{key}"].append(o.se)
+                    res[f"t_{key}"].append(o.t)
+            out[f"{name}_rows"] = rows
+            out[f"{name}_cols"] = cols
+            for k, v in res.items():
+                out[f"{name}_{k}"] = np.array(v)
+    np.savez_compressed(OUT / "ols.npz", **out)
+
+
+S1_SPEC = dict(seed=11, n_samples=300, n_markers=600, n_phenotypes=12, n_covariates=3, causal_fraction=0.03,
+               effect_sd=0.3, genotype_missing_rate=0.02, phenotype_missing_rate=0.01)
+C1_SPEC = dict(seed=1, n_samples=2000, n_markers=10000, n_phenotypes=64, n_covariates=10, causal_fraction=0.01,
+               effect_sd=0.15)
+
+
 def main() -> None:
+    if sys.argv[1:] == ["ols"]:
+        make_ols()
+        print("ols fixture written to", OUT)
+        return
     make_decode()
     make_pvalues()
     make_prepare()
     F64 = ref.Precision.F64
     scan_fixture(
         "s1",
-        dict(seed=11, n_samples=300, n_markers=600, n_phenotypes=12, n_covariates=3, causal_fraction=0.03,
-             effect_sd=0.3, genotype_missing_rate=0.02, phenotype_missing_rate=0.01),
+        S1_SPEC,
         {
             "all_f64": {"config": dict(p_threshold=1.0, precision=F64)},
             "thr_f64": {"config": dict(p_threshold=1e-3, precision=F64), "keep_bytes": True},
@@ -199,8 +252,7 @@ def main() -> None:
     )
     scan_fixture(
         "c1",
-        dict(seed=1, n_samples=2000, n_markers=10000, n_phenotypes=64, n_covariates=10, causal_fraction=0.01,
-             effect_sd=0.15),
+        C1_SPEC,
         {
             "thr_f64": {"config": dict(p_threshold=1e-4, precision=F64)},
             "thr_f32": {"config": dict(p_threshold=1e-4)},
@@ -208,6 +260,7 @@ def main() -> None:
         },
     )
     make_bgen()
+    make_ols()
     print("golden fixtures written to", OUT)
 
 

@@ -48,5 +48,26 @@ def oracle_inputs(name: str, out_dir: Path):
     return dos, ytil, float(n - 2), paths
 
 
+def panel_inputs(name: str, out_dir: Path):
+    """(dosages [M, N], imputed panel y [N, P], covariates C [N, c], basis Q, paths) of a golden
+    cohort, regenerated locally, with the package's host table logic (reference behaviour)."""
+    from oracle import scan_oracle as orc
+    from paper_2604_21095_b200 import phenotypes
+
+    paths = regenerate(name, out_dir)
+    spec = spec_of(name)
+    n, m = spec["n_samples"], spec["n_markers"]
+    bpm = (n + 3) // 4
+    blob = np.frombuffer(Path(paths["bed_path"]).read_bytes()[3:], dtype=np.uint8).reshape(m, bpm)
+    dos = orc.decode_bed(blob, n)
+    ids = [f"S{i + 1}" for i in range(n)]
+    ptab = phenotypes.load_table(paths["pheno_path"])
+    ctab = phenotypes.load_table(paths["covar_path"])
+    align = phenotypes.align_samples(ids, ptab, ctab)
+    y = phenotypes.build_panel(ptab, align).y
+    c = phenotypes.covariate_matrix(ctab, align)
+    return dos, y, c, orc.covariate_basis(c), paths
+
+
 def load_cohort(name: str):
     return np.load(GOLD / f"{name}.npz")

@@ -56,71 +56,102 @@ def test_panel_bytes_broadcast_gloo(tmp_path):
         assert np.array_equal(np.load(tmp_path / f"r{r}.npy"), payload)
 
 
-def _markers(n):
-    return [pg.MarkerRecord("1", f"snp{i + 1}", i + 1, "A", "B", i) for i in range(n)]
+def _markers(n, dup_ids=False):
+    # dup_ids: '.' IDs (common in .bim files) on every other marker
+    return [pg.MarkerRecord("1", "." if dup_ids and i % 2 else f"snp{i + 1}", i + 1, "A", "B", i) for i in range(n)]
 
 
 def _stats(markers, rows, cols, t, p):
     m = len(markers)
+    t = np.asarray(t, float)
     return output.BatchStats(markers=tuple(markers), allele_frequency=np.full(m, 0.3),
                              missing_count=np.zeros(m, np.int64), skip_reason=np.zeros(m, np.int8), clamp_count=0,
                              cand_rows=np.asarray(rows, np.int64), cand_cols=np.asarray(cols, np.int64),
-                             cand_r=np.asarray(t, float) / 10, cand_t=np.asarray(t, float),
-                             cand_p=np.asarray(p, float))
+                             cand_r=t / 10, cand_t=t, cand_p=np.asarray(p, float), cand_beta=t * 0.37,
+                             cand_se=np.full(t.size, 0.37))
 
 
-def test_merge_threshold_and_topk_equal_single_process(tmp_path):
+@pytest.mark.parametrize("dup_ids", [False, True])
+@pytest.mark.parametrize("top_k", [2, 5])
+def test_merge_threshold_and_topk_equal_single_process(tmp_path, dup_ids, top_k):
+    """Shard merges == one process, for THRESHOLD / TOPK records and their effect-size
+    sidecars, with tied p across shards and duplicated ('.') marker IDs."""
     rng = np.random.default_rng(3)
-    mk = _markers(10)
+    mk = _markers(10, dup_ids)
     names = ["ph1", "ph2", "ph3"]
     rows = np.repeat(np.arange(10), 3)
     cols = np.tile(np.arange(3), 10)
     t = rng.standard_normal(30) * 3
-    p = np.round(rng.random(30), 2)  # coarse p -> ties exercise the source-index tie-break
+    p = np.round(rng.random(30), 1)  # coarse p -> ties exercise the source-index tie-break
     # single process
-    w = output.ThresholdWriter(tmp_path / "single.tsv", 0.5, 8.0, 10, True, names)
+    w = output.ThresholdWriter(tmp_path / "single.tsv", 0.5, 8.0, 10, True, names, effect_sizes=True)
     w.emit(_stats(mk, rows, cols, t, p))
     w.finalize()
-    k = output.TopKWriter(tmp_path / "single_top.tsv", 2, 8.0, 10, True, names)
+    k = output.TopKWriter(tmp_path / "single_top.tsv", top_k, 8.0, 10, True, names, effect_sizes=True)
     k.emit(_stats(mk, rows, cols, t, p))
     k.finalize()
     # two shards: markers [0, 6) and [6, 10)
     shards, tshards = [], []
     for r, (lo, hi) in enumerate(((0, 6), (6, 10))):
         sel = (rows >= lo) & (rows < hi)
-        ws = output.ThresholdWriter(tmp_path / f"o.rank{r}", 0.5, 8.0, 10, True, names)
+        ws = output.ThresholdWriter(tmp_path / f"o.rank{r}", 0.5, 8.0, 10, True, names, effect_sizes=True)
         ws.emit(_stats(mk[lo:hi], rows[sel] - lo, cols[sel], t[sel], p[sel]))
         ws.finalize()
         shards.append(tmp_path / f"o.rank{r}")
-        ks = output.TopKWriter(tmp_path / f"k.rank{r}", 2, 8.0, 10, True, names)
+        ks = output.TopKWriter(tmp_path / f"k.rank{r}", top_k, 8.0, 10, True, names, effect_sizes=True)
         ks.emit(_stats(mk[lo:hi], rows[sel] - lo, cols[sel], t[sel], p[sel]))
         ks.finalize()
         tshards.append(tmp_path / f"k.rank{r}")
     distributed.merge_tsv(shards, tmp_path / "merged.tsv")
     assert (tmp_path / "merged.tsv").read_bytes() == (tmp_path / "single.tsv").read_bytes()
-    distributed.merge_topk(tshards, tmp_path / "merged_top.tsv", 2, names, {m.id: m.source_index for m in mk})
+    distributed.merge_tsv([output.beta_sidecar(x) for x in shards], output.beta_sidecar(tmp_path / "merged.tsv"),
+                          header="\t".join(output.BETA_COLUMNS))
+    assert (output.beta_sidecar(tmp_path / "merged.tsv").read_bytes()
+            == output.beta_sidecar(tmp_path / "single.tsv").read_bytes())
+    distributed.merge_topk(tshards, tmp_path / "merged_top.tsv", top_k, names, effect_sizes=True)
     assert (tmp_path / "merged_top.tsv").read_bytes() == (tmp_path / "single_top.tsv").read_bytes()
+    assert (output.beta_sidecar(tmp_path / "merged_top.tsv").read_bytes()
+            == output.beta_sidecar(tmp_path / "single_top.tsv").read_bytes())
+    beta, se = output.load_effect_sizes(tmp_path / "single_top.tsv")
+    recs = output.load_association_records(tmp_path / "single_top.tsv")
+    assert np.allclose(beta, [r.t * 0.37 for r in recs]) and np.all(se == 0.37)
+
+
+def test_merge_qc(tmp_path):
+    """QC shards -> marker rows in rank order, then the phenotype rows once."""
+    head = "KIND\tNAME\tREASON\n"
+    (tmp_path / "a").write_text(head + "marker\tm1\tMONOMORPHIC\nphenotype\tz\tZERO_VARIANCE\n")
+    (tmp_path / "b").write_text(head + "marker\tm9\tALL_MISSING\nphenotype\tz\tZERO_VARIANCE\n")
+    assert distributed.merge_qc([tmp_path / "a", tmp_path / "b"], tmp_path / "m") == 2
+    assert (tmp_path / "m").read_text() == (head + "marker\tm1\tMONOMORPHIC\nmarker\tm9\tALL_MISSING\n"
+                                            "phenotype\tz\tZERO_VARIANCE\n")
 
 
 def test_merge_full(tmp_path):
     mk = _markers(5)
     names = ["p1", "p2"]
     t = np.arange(10, dtype=np.float64).reshape(5, 2)
-    single = output.FullMatrixWriter(tmp_path / "s.bin", np.float64, 3.0, 5, True, names)
+    single = output.FullMatrixWriter(tmp_path / "s.bin", np.float64, 3.0, 5, True, names, effect_sizes=True)
     b = _stats(mk, [], [], [], [])
     b.t_rows = t
+    b.beta_rows = t * 0.5
     single.emit(b)
     single.finalize()
     shards = []
     for r, (lo, hi) in enumerate(((0, 3), (3, 5))):
-        w = output.FullMatrixWriter(tmp_path / f"f.bin.rank{r}", np.float64, 3.0, 5, True, names)
+        w = output.FullMatrixWriter(tmp_path / f"f.bin.rank{r}", np.float64, 3.0, 5, True, names,
+                                    effect_sizes=True)
         bs = _stats(mk[lo:hi], [], [], [], [])
         bs.t_rows = t[lo:hi]
+        bs.beta_rows = t[lo:hi] * 0.5
         w.emit(bs)
         w.finalize()
         shards.append(tmp_path / f"f.bin.rank{r}")
-    distributed.merge_full(shards, tmp_path / "f.bin")
+    distributed.merge_full(shards, tmp_path / "f.bin", effect_sizes=True)
     assert (tmp_path / "f.bin").read_bytes() == (tmp_path / "s.bin").read_bytes()
+    assert np.array_equal(output.read_full_beta(tmp_path / "f.bin"), t * 0.5)
+    assert (output.beta_sidecar(tmp_path / "f.bin", full=True).read_bytes()
+            == output.beta_sidecar(tmp_path / "s.bin", full=True).read_bytes())
     assert (tmp_path / "f.bin.markers.tsv").read_text() == (tmp_path / "s.bin.markers.tsv").read_text()
 
 

@@ -221,7 +221,7 @@ class TestCli:
 
 def test_min_p_sidecar_equals_full_scan_minimum(tmp_path):
     """<out>.minp.tsv (per-phenotype max |t| / min p, fused into the GEMM epilogue) ==
-    the minimum over the FULL t matrix of the same scan (tolerance of the fp32 max)."""
+    the minimum over the FULL t matrix of the same scan, bit for bit (fp64 r of the maximum)."""
     rng = np.random.default_rng(41)
     d, y = random_dataset(rng, 300, 120, 9)
     y[:, 3] += 0.7 * d[11]
@@ -235,10 +235,16 @@ def test_min_p_sidecar_equals_full_scan_minimum(tmp_path):
     got_t = np.array([float(r[2]) for r in rows[1:]])
     got_p = np.array([float(r[3]) for r in rows[1:]])
     want_t = np.abs(t).max(axis=0)
-    np.testing.assert_allclose(got_t, want_t, rtol=1e-6)
+    assert np.array_equal(got_t, want_t)
     want_p = pg.p_from_t(want_t, 118.0)
-    np.testing.assert_allclose(-np.log10(got_p), -np.log10(want_p), rtol=1e-4)
+    np.testing.assert_allclose(got_p, want_p, rtol=1e-13)
     assert np.argmin(got_p) == 3
+    # the records the threshold scan emitted agree with the sidecar's minimum
+    recs = pg.load_association_records(root / "thr.tsv")
+    for j, name in enumerate(names):
+        ps = [r.p for r in recs if r.phenotype == name]
+        if ps:
+            assert min(ps) == got_p[j]
 
 
 def test_topk_large_batches_null_bar_and_rescan(tmp_path):
@@ -313,3 +319,52 @@ def test_null_calibration(tmp_path):
         assert abs(np.mean(p <= a) - a) < tol
     ks = np.max(np.abs(p - (np.arange(1, m + 1) / m)))
     assert ks < 0.01
+
+
+def test_candidate_counter_crosses_int32_range(tmp_path):
+    """The epilogue's candidate counter is 64-bit: a launch whose counter starts just below
+    2^31 (test hook) and crosses it yields exactly the candidates of a normal launch (the
+    32-bit counter of round 1 wrapped to negative slots here)."""
+    from paper_2604_21095_b200 import _native
+    from paper_2604_21095_b200._device import DeviceContext
+    from oracle import scan_oracle as orc
+
+    rng = np.random.default_rng(77)
+    n, m, p = 256, 700, 300
+    d, y = random_dataset(rng, m, n, p)
+    ytil, _ = orc.standardized_panel(y, orc.covariate_basis(np.zeros((n, 0))))
+    codes = np.select([d == 2, d == 1, d == 0], [0, 2, 3]).astype(np.uint8)
+    q = codes.reshape(m, n // 4, 4)
+    packed = (q[:, :, 0] | (q[:, :, 1] << 2) | (q[:, :, 2] << 4) | (q[:, :, 3] << 6)).astype(np.uint8)
+    with DeviceContext(0) as ctx:
+        ctx.set_panel(ytil, np.arange(n, dtype=np.int64), n)
+        ctx.set_scan(float(n - 2), _native.PG_MODE_THRESHOLD, np.zeros(p))  # every pair is a candidate
+        a = ctx.scan(_native.PG_GENO_BED, packed, n // 4)
+        ctx.debug_candidate_base(2**31 - 1000)
+        b = ctx.scan(_native.PG_GENO_BED, packed, n // 4)
+        ctx.debug_candidate_base(2**32 - 5)
+        c = ctx.scan(_native.PG_GENO_BED, packed, n // 4)
+    assert a.cand_t.size == m * p
+    for x in (b, c):
+        assert np.array_equal(x.cand_rows, a.cand_rows) and np.array_equal(x.cand_cols, a.cand_cols)
+        assert np.array_equal(x.cand_t, a.cand_t)
+
+
+def test_topk_larger_than_device_batch(tmp_path):
+    """top_k above the device batch, ~3 batches: phenotypes holding some but fewer than k
+    records must not lose true top-k markers to the null-quantile bar (advisor finding)."""
+    rng = np.random.default_rng(12)
+    n, m, k = 80, 1500, 700
+    d, y = random_dataset(rng, m, n, 5)
+    spec, pheno, _, root = dataset(tmp_path, d, y)
+    scan(spec, pheno, root / "all.tsv", p_threshold=1.0, precision=pg.Precision.F64)
+    scan(spec, pheno, root / "top.tsv", output_mode=pg.OutputMode.TOPK, top_k=k, precision=pg.Precision.F64,
+         device_batch=512)
+    by = {}
+    for r in pg.load_association_records(root / "all.tsv"):
+        by.setdefault(r.phenotype, []).append(r)
+    expected = []
+    for name in sorted(by):
+        expected += [(name, r.id) for r in sorted(by[name], key=lambda r: (r.p, r.pos))[:k]]
+    got = [(r.phenotype, r.id) for r in pg.load_association_records(root / "top.tsv")]
+    assert got == expected

@@ -458,3 +458,20 @@ def test_device_batch_sizes(monkeypatch):
     assert 256 <= full < 65536
     sliced = device_batch_size(cfg(plink), 10**6, 20480, 500_000)
     assert 256 <= sliced < 65536
+
+
+def test_device_batch_bounds_candidates(tmp_path):
+    """THRESHOLD / TOPK device batches keep the expected candidate pairs under the budget:
+    at p = 1 (every pair a candidate) a C3-sized scan shrinks its 65,536-marker launches so
+    markers x phenotypes stays far below 2^31 (the round-1 int32 counter overflowed here)."""
+    from paper_2604_21095_b200 import engine
+
+    spec = pg.SourceSpec(pg.GenotypeFormat.PLINK_BED, bed_path=tmp_path / "g.bed")
+    P = 20480
+    for kw in ({"p_threshold": 1.0}, {"p_threshold": 0.3}, {"output_mode": pg.OutputMode.TOPK, "top_k": 16384}):
+        cfg = pg.ScanConfig(source=spec, pheno_path=tmp_path / "p", out_path=tmp_path / "o", batch_size=131072,
+                            **kw)
+        b = engine.device_batch_size(cfg, 1_000_000, P, 23000)
+        assert b * P <= engine._CAND_BUDGET * 1.01 and b * P < 2**31, (kw, b)
+    cfg = pg.ScanConfig(source=spec, pheno_path=tmp_path / "p", out_path=tmp_path / "o", p_threshold=1e-4)
+    assert engine.device_batch_size(cfg, 1_000_000, P, 23000) == 65536  # the C3 default is unchanged

@@ -91,3 +91,26 @@ def test_oracle_scan_matches_reference_c1(tmp_path):
     np.testing.assert_allclose(res["t"][order], g["thr_f64_t"], rtol=1e-9)
     sub = g["full_f64_rows"]
     np.testing.assert_allclose(orc.t_from_r(res["full_r"][sub], df), g["full_f64_t"], rtol=1e-9, atol=1e-12)
+
+
+@pytest.mark.parametrize("name", ["s1", "c1"])
+def test_oracle_effect_sizes_match_reference_ols(tmp_path, name):
+    """The oracle's beta / se (slope of y_res on g) == the reference's own per-pair OLS
+    (oracle.ols_single) on the golden cohorts: y ~ 1 + C + g in extension mode with the
+    adjusted df, y_res ~ 1 + g in paper mode."""
+    from scan_fixtures import panel_inputs
+
+    dos, y, c, q, _ = panel_inputs(name, tmp_path)
+    g = np.load(GOLD / "ols.npz")
+    rows, cols = g[f"{name}_rows"], g[f"{name}_cols"]
+    n = y.shape[0]
+    ytil, _ = orc.standardized_panel(y, q)
+    sd = orc.panel_sd(y, q)
+    for mode, gq, df in (("paper", None, float(n - 2)), ("adj", q, float(n - q.shape[1] - 1))):
+        mat, _, _, var, _ = orc.prepare(dos[np.unique(rows)], gq)
+        idx = np.searchsorted(np.unique(rows), rows)
+        r = np.einsum("kn,nk->k", mat[idx], ytil[:, cols]) / n
+        beta, se = orc.effect_sizes(r, var[idx], sd[cols], df)
+        np.testing.assert_allclose(beta, g[f"{name}_beta_{mode}"], rtol=1e-9, atol=1e-14)
+        np.testing.assert_allclose(se, g[f"{name}_se_{mode}"], rtol=1e-9)
+        np.testing.assert_allclose(beta / se, g[f"{name}_t_{mode}"], rtol=1e-9, atol=1e-12)
