@@ -4,11 +4,16 @@ samples, P=20,480 phenotypes (config 3: synthetic PLINK .bed, M=1,000,000
 markers per GPU, THRESHOLD hit compaction at p <= 1e-4).
 
   python bench.py [--gpus N --steps K --warmup W]             # this repo (B200 kernels)
-  python bench.py --impl reference [--steps K --warmup W]     # reference CPU path (oracle port)
-  torchrun --nproc-per-node N bench.py --gpus N ...            # one rank per GPU (weak scaling)
+  python bench.py --impl reference [--steps K --warmup W]     # the reference's own scan loop on the host cores
+  torchrun --nproc-per-node N bench.py --gpus N ...            # one rank per GPU
+  python bench.py --workload c4 ...                            # 8.9M markers in total (the paper headline)
+  python bench.py --markers-per-gpu 1000000 ...                # weak scaling instead
 
-A step scans the rank's whole marker shard (M markers) against the resident
-panel and returns the hits: value = (markers x phenotypes over all ranks) /
+Scaling: by default the C3 job (M = 1,000,000 markers in total) is split into contiguous
+256-aligned marker shards over the N ranks (strong scaling, BASELINE config 3 at 1/2/4/8
+GPUs); `--workload c4` scans C4's 8.9M markers in total; `--markers-per-gpu M` fixes the
+per-rank shard instead (weak scaling). A step scans the rank's whole marker shard against
+the resident panel and returns the hits: value = (markers x phenotypes over all ranks) /
 (max over ranks of the device time of K steps). `e2e` times the same through
 the host-buffer C-ABI path (raw panel upload + device prep + NCCL broadcast + pinned .bed rows
 H2D inside the step; the panel enters raw (phenotypes + 10 covariates) and is
@@ -46,15 +51,35 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--samples", type=int, default=23_000)
-    ap.add_argument("--markers", type=int, default=1_000_000, help="markers per GPU")
+    ap.add_argument("--workload", choices=["c3", "c4"], default="c3",
+                    help="c3: 1,000,000 markers in total; c4: 8,900,000 markers in total (paper headline)")
+    ap.add_argument("--total-markers", type=int, default=None, help="markers in the whole job (strong scaling)")
+    ap.add_argument("--markers-per-gpu", type=int, default=None, help="fixed shard per GPU (weak scaling)")
     ap.add_argument("--phenotypes", type=int, default=20_480)
     ap.add_argument("--p-threshold", type=float, default=1e-4)
     ap.add_argument("--device-batch", type=int, default=65_536)
     ap.add_argument("--cpu-sample", type=int, default=4096, help="markers in the timed CPU-baseline sample")
+    ap.add_argument("--ref-workers", type=int, default=2, help="reference arm: engine worker threads")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=3)
-    return ap.parse_args()
+    a = ap.parse_args()
+    a.total = a.total_markers or (8_900_000 if a.workload == "c4" else 1_000_000)
+    a.scaling = "weak" if a.markers_per_gpu else "strong"
+    return a
+
+
+def job_markers(a, world: int) -> int:
+    return a.markers_per_gpu * world if a.markers_per_gpu else a.total
+
+
+def rank_span(a, world: int, rank: int) -> tuple[int, int]:
+    """[start, stop) of this rank's markers: contiguous 256-aligned shards of the job."""
+    if a.markers_per_gpu:
+        return rank * a.markers_per_gpu, (rank + 1) * a.markers_per_gpu
+    from paper_2604_21095_b200.distributed import shard_span
+
+    return shard_span(a.total, world, rank)
 
 
 # --------------------------------------------------------------------------- helpers
@@ -66,11 +91,16 @@ def dist_env():
 
 
 def workload_config(a, world: int) -> dict:
+    total = job_markers(a, world)
+    name = "C4" if total == 8_900_000 else "C3" if total == 1_000_000 * (world if a.markers_per_gpu else 1) else "custom"
+    split = (f"{a.markers_per_gpu:,} markers per GPU" if a.markers_per_gpu
+             else f"M={total:,} markers split over {world} GPU(s)")
     return {
-        "workload": (f"C3: synthetic PLINK .bed N={a.samples:,} x M={a.markers:,} markers per GPU x "
+        "workload": (f"{name}: synthetic PLINK .bed N={a.samples:,} x {split} x "
                      f"P={a.phenotypes:,} phenotypes, THRESHOLD p<={a.p_threshold:g} hit compaction"),
         "n_samples": a.samples,
-        "n_markers_per_gpu": a.markers,
+        "n_markers_total": total,
+        "n_markers_per_gpu": -(-total // world),
         "n_phenotypes": a.phenotypes,
         "p_threshold": a.p_threshold,
         "device_batch_markers": a.device_batch,
@@ -170,7 +200,7 @@ def cpu_threads() -> int:
 
 
 def run_cpu_sample(packed_rows: np.ndarray, ytil: np.ndarray, n: int, p_thr: float) -> tuple[float, int]:
-    """Oracle (numpy restatement of the reference path) on a bounded marker sample -> (seconds, hits)."""
+    """Fallback when oracle/_ref is absent: the oracle port on a bounded marker sample -> (seconds, hits)."""
     from oracle import scan_oracle as orc
 
     t0 = time.perf_counter()
@@ -179,36 +209,63 @@ def run_cpu_sample(packed_rows: np.ndarray, ytil: np.ndarray, n: int, p_thr: flo
     return time.perf_counter() - t0, int(res["rows"].size)
 
 
+def ref_loop_sample(a, n_markers: int, batch: int, workers: int):
+    """The reference's own THRESHOLD scan loop (oracle/ref_scan_loop.py, panelgwas 0.1.0 from
+    oracle/_ref) at N, P and p_threshold of the workload, over an n_markers .bed sample."""
+    from oracle.ref_scan_loop import ReferenceScanLoop
+
+    return ReferenceScanLoop(a.samples, a.phenotypes, n_markers, a.p_threshold, seed=a.seed, n_cov=N_COVARIATES,
+                             batch_size=batch, workers=workers)
+
+
 def reference_arm(a) -> None:
+    """Reference CPU path on the host cores (rank 0 only; other ranks exit without work)."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    rng = np.random.default_rng(a.seed)
+    from oracle import ref_scan_loop
+
     n, p = a.samples, a.phenotypes
-    sample = max(16, min(a.cpu_sample, a.markers))
-    per_step = max(16, sample // 4)
-    y = rng.standard_normal((n, p))
-    y -= y.mean(axis=0)
-    y /= np.sqrt((y * y).mean(axis=0))
-    bpm = (n + 3) // 4
-    af = rng.uniform(0.05, 0.95, per_step)
-    g = rng.binomial(2, af[:, None], size=(per_step, n))
-    codes = np.array([3, 2, 0], dtype=np.uint8)[g]
-    codes = np.pad(codes, ((0, 0), (0, bpm * 4 - n))).reshape(per_step, bpm, 4)
-    packed = (codes[:, :, 0] | (codes[:, :, 1] << 2) | (codes[:, :, 2] << 4) | (codes[:, :, 3] << 6)).astype(np.uint8)
-    for _ in range(a.warmup):
-        run_cpu_sample(packed, y, n, a.p_threshold)
-    times = [run_cpu_sample(packed, y, n, a.p_threshold)[0] for _ in range(a.steps)]
-    total = sum(times)
+    # a bounded sample per step so that W + K steps end within a few minutes: 2 engine batches
+    per_step = int(2 ** np.floor(np.log2(40_000 / max(1, a.steps + a.warmup))))
+    per_step = max(1024, min(8192, per_step))
+    if ref_scan_loop.available():
+        loop = ref_loop_sample(a, per_step, per_step // 2, a.ref_workers)
+        for _ in range(a.warmup):
+            loop.step()
+        steps = [loop.step() for _ in range(a.steps)]
+        loop.close()
+        total = sum(x["seconds"] for x in steps)
+        kind, cores = "reference", ref_scan_loop.host_threads()
+        sample = (f"{per_step} markers x {n} samples x {p} phenotypes per step through the reference's own "
+                  f"scan loop (panelgwas 0.1.0 from oracle/_ref: PlinkSource.read_marker_batch -> "
+                  f"engine._process_batch on {a.ref_workers} workers, batch {per_step // 2} -> ThresholdWriter); "
+                  f"panel prep (build_covariate_basis/residualize/standardize_columns, 10 covariates) "
+                  f"{loop.setup_s:.1f} s once, outside the steps; phenotype TSV parse not included")
+        extra = {"setup_s": loop.setup_s, "records_per_step": steps[-1]["records"]}
+    else:  # oracle/_ref not built (no /root/reference where build() ran): the numpy port
+        rng = np.random.default_rng(a.seed)
+        y = rng.standard_normal((n, p))
+        y -= y.mean(axis=0)
+        y /= np.sqrt((y * y).mean(axis=0))
+        bpm = (n + 3) // 4
+        g = rng.binomial(2, rng.uniform(0.05, 0.95, per_step)[:, None], size=(per_step, n))
+        codes = np.array([3, 2, 0], dtype=np.uint8)[g]
+        codes = np.pad(codes, ((0, 0), (0, bpm * 4 - n))).reshape(per_step, bpm, 4)
+        packed = (codes[:, :, 0] | (codes[:, :, 1] << 2) | (codes[:, :, 2] << 4) | (codes[:, :, 3] << 6)).astype(np.uint8)
+        for _ in range(a.warmup):
+            run_cpu_sample(packed, y, n, a.p_threshold)
+        total = sum(run_cpu_sample(packed, y, n, a.p_threshold)[0] for _ in range(a.steps))
+        kind, cores = "port", cpu_threads()
+        sample = f"{per_step} markers x {n} samples x {p} phenotypes per step (oracle/scan_oracle.py port)"
+        extra = {}
     value = a.steps * per_step * p / total
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tests/s", "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * total / a.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(a, world),
-        "cpu_baseline": {"value": value, "unit": "tests/s", "cores": cpu_threads(), "kind": "port",
-                         "sample": f"{per_step} markers x {n} samples x {p} phenotypes per step "
-                                   "(oracle/scan_oracle.py: decode + prepare + f64 tiled GEMM + premask + Lentz p)"},
+        "scaling": a.scaling, "vs_baseline": None, "dtype": "f64 (f32 genotype store, reference default)",
+        "data": "synthetic", "config": workload_config(a, world),
+        "cpu_baseline": {"value": value, "unit": "tests/s", "cores": cores, "kind": kind, "sample": sample, **extra},
         "e2e": {"value": value, "unit": "tests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -238,7 +295,10 @@ def our_arm(a) -> None:
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     _build.build()  # no-op when the in-tree .so is current
-    n, p, m = a.samples, a.phenotypes, a.markers
+    n, p = a.samples, a.phenotypes
+    span = rank_span(a, world, rank)
+    m = span[1] - span[0]
+    job = job_markers(a, world)
     bpm = (n + 3) // 4
     pitch = (bpm + 15) // 16 * 16
     df = float(n - 2)
@@ -318,8 +378,8 @@ def our_arm(a) -> None:
         scan_step_device()
     with ClockSampler(local) as clk:
         ms, outs = timed(scan_step_device, a.steps)
-    tests_per_step = m * p
-    value = world * tests_per_step * a.steps / (ms / 1e3)
+    tests_per_step = job * p  # the whole job (all ranks); ms is the max over ranks
+    value = tests_per_step * a.steps / (ms / 1e3)
     gemm_ms = sum(o["gemm_ms"] for o in outs)
     launches = sum(o["launches"] for o in outs)
     hits = outs[-1]["hits"]
@@ -406,24 +466,36 @@ def our_arm(a) -> None:
 
         e2e_step()
         ms_e2e, outs_e2e = timed(e2e_step, a.steps)
-        e2e = {"value": world * tests_per_step * a.steps / (ms_e2e / 1e3), "unit": "tests/s",
+        e2e = {"value": tests_per_step * a.steps / (ms_e2e / 1e3), "unit": "tests/s",
                "h2d_bytes_per_step": int(outs_e2e[-1][0]), "d2h_bytes_per_step": int(outs_e2e[-1][1]),
                "ms_per_step": ms_e2e / a.steps}
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        sample = max(16, min(a.cpu_sample, m))
-        rows_np = synth_packed(torch, sample, n, pitch, a.seed * 7919 + 17, dev)[:, :bpm].cpu().numpy()
-        y_np = ytil.cpu().numpy()
-        sec, _ = run_cpu_sample(rows_np, y_np, n, a.p_threshold)
-        cpu = {"value": sample * p / sec, "unit": "tests/s", "cores": cpu_threads(), "kind": "port",
-               "sample": f"{sample} markers x {n} samples x {p} phenotypes, one pass of oracle/scan_oracle.py "
-                         f"(numpy restatement of the reference path) in {sec:.1f} s"}
+        from oracle import ref_scan_loop
+
+        sample = max(256, min(a.cpu_sample, m))
+        if ref_scan_loop.available():
+            loop = ref_loop_sample(a, sample, sample // 2, a.ref_workers)
+            sec = loop.step()["seconds"]
+            cpu = {"value": sample * p / sec, "unit": "tests/s", "cores": ref_scan_loop.host_threads(),
+                   "kind": "reference",
+                   "sample": f"{sample} markers x {n} samples x {p} phenotypes through the reference's own scan loop "
+                             f"(panelgwas 0.1.0 from oracle/_ref, {a.ref_workers} engine workers, batch "
+                             f"{sample // 2}) in {sec:.1f} s; its panel prep ({loop.setup_s:.1f} s) not counted"}
+            loop.close()
+        else:
+            rows_np = synth_packed(torch, sample, n, pitch, a.seed * 7919 + 17, dev)[:, :bpm].cpu().numpy()
+            y_np = ytil.cpu().numpy()
+            sec, _ = run_cpu_sample(rows_np, y_np, n, a.p_threshold)
+            cpu = {"value": sample * p / sec, "unit": "tests/s", "cores": cpu_threads(), "kind": "port",
+                   "sample": f"{sample} markers x {n} samples x {p} phenotypes, one pass of oracle/scan_oracle.py "
+                             f"(numpy restatement of the reference path) in {sec:.1f} s"}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "tests/s", "n_gpus": world, "steps": a.steps,
-            "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": a.scaling,
             "vs_baseline": None, "dtype": "int8 (exact int32 accumulate; fp64 epilogue)", "data": "synthetic",
             "config": workload_config(a, world),
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",

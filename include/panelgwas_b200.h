@@ -245,6 +245,11 @@ PG_API int pg_t_from_r(pg_ctx* ctx, const double* r, int64_t n, double df, doubl
 PG_API int pg_p_from_t(pg_ctx* ctx, const double* t, int64_t n, double df, double* p, int64_t* underflow);
 /* kernel.reg_inc_beta (kernel.py:147-189), broadcast already applied by caller */
 PG_API int pg_reg_inc_beta(pg_ctx* ctx, const double* a, const double* b, const double* x, int64_t n, double* out);
+/* kernel.p_from_t for a scalar t: the reference's scalar path (kernel.py:201-204 ->
+ * _reg_inc_beta_scalar, kernel.py:136-144), the form t_threshold_for_p bisects on */
+PG_API int pg_p_from_t_scalar(pg_ctx* ctx, double t, double df, double* p);
+/* kernel.reg_inc_beta with scalar a, b, x (kernel.py:156-163 -> _reg_inc_beta_scalar) */
+PG_API int pg_reg_inc_beta_scalar(pg_ctx* ctx, double a, double b, double x, double* out);
 /* kernel.t_threshold_for_p (kernel.py:212-235) */
 PG_API int pg_t_threshold_for_p(pg_ctx* ctx, double p_threshold, double df, double* t_crit);
 

@@ -354,6 +354,18 @@ class DeviceContext:
             call("pg_p_from_t", self._h, ptr(a), a.size, float(df), ptr(out), byref(under))
         return out, under.value
 
+    def p_from_t_scalar(self, t: float, df: float) -> float:
+        out = c_double(0.0)
+        with self.lock:
+            call("pg_p_from_t_scalar", self._h, float(t), float(df), byref(out))
+        return out.value
+
+    def reg_inc_beta_scalar(self, a: float, b: float, x: float) -> float:
+        out = c_double(0.0)
+        with self.lock:
+            call("pg_reg_inc_beta_scalar", self._h, float(a), float(b), float(x), byref(out))
+        return out.value
+
     def reg_inc_beta(self, a: np.ndarray, b: np.ndarray, x: np.ndarray) -> np.ndarray:
         a = np.ascontiguousarray(a, dtype=np.float64)
         b = np.ascontiguousarray(b, dtype=np.float64)

@@ -95,6 +95,8 @@ SIGNATURES: dict[str, list] = {
     "pg_ctx_debug_candidate_base": [_P, ctypes.c_uint64],
     "pg_t_from_r": [_P, _P, c_int64, c_double, _P],
     "pg_p_from_t": [_P, _P, c_int64, c_double, _P, _P],
+    "pg_p_from_t_scalar": [_P, c_double, c_double, _P],
+    "pg_reg_inc_beta_scalar": [_P, c_double, c_double, c_double, _P],
     "pg_reg_inc_beta": [_P, _P, _P, _P, c_int64, _P],
     "pg_t_threshold_for_p": [_P, c_double, c_double, _P],
     "pg_decode_bed": [_P, _P, c_int64, c_int64, c_int64, c_int, _P, _P],

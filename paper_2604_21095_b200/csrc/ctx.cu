@@ -1385,6 +1385,32 @@ int pg_reg_inc_beta(pg_ctx* c, const double* a, const double* b, const double* x
   return PG_OK;
 }
 
+static int scalar_stat_call(pg_ctx* c, int which, double a, double b, double x, double* out) {
+  PG_CHECK_STATUS(c->scratch_a.ensure(1));
+  PG_CHECK_STATUS(c->flags.ensure(2));
+  PG_CUDA_CHECK(cudaMemsetAsync(c->flags.p, 0, 8, c->stream));
+  PG_CHECK_STATUS(scalar_stat(which, a, b, x, c->scratch_a.p, c->flags.p, c->stream));
+  int err = 0;
+  PG_CUDA_CHECK(cudaMemcpyAsync(out, c->scratch_a.p, 8, cudaMemcpyDeviceToHost, c->stream));
+  PG_CUDA_CHECK(cudaMemcpyAsync(&err, c->flags.p, 4, cudaMemcpyDeviceToHost, c->stream));
+  PG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  PG_REQUIRE(err == 0, PG_ERR_STATE, "incomplete beta continued fraction did not converge; this is a bug");
+  return PG_OK;
+}
+
+int pg_p_from_t_scalar(pg_ctx* c, double t, double df, double* p) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(df >= 1.0, PG_ERR_INVALID, "p_from_t requires df >= 1");
+  return scalar_stat_call(c, 1, t, df, 0.0, p);
+}
+
+int pg_reg_inc_beta_scalar(pg_ctx* c, double a, double b, double x, double* out) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(a > 0.0 && b > 0.0, PG_ERR_INVALID, "reg_inc_beta requires a > 0 and b > 0");
+  PG_REQUIRE(x >= 0.0 && x <= 1.0, PG_ERR_INVALID, "reg_inc_beta requires x in [0, 1]");
+  return scalar_stat_call(c, 0, a, b, x, out);
+}
+
 int pg_t_threshold_for_p(pg_ctx* c, double p_threshold, double df, double* t_crit) {
   PG_CHECK_STATUS(ctx_check(c));
   PG_REQUIRE(p_threshold > 0.0 && p_threshold <= 1.0, PG_ERR_INVALID, "p_threshold must be in (0, 1]");

@@ -209,6 +209,13 @@ __global__ void reg_inc_beta_kernel(const double* a, const double* b, const doub
     out[i] = reg_inc_beta_arr(a[i], b[i], x[i], err);
 }
 
+// Scalar inputs take the reference's scalar path (kernel.py:136-144, :201-204):
+// which 0 -> I_x(a, b) (a, b, x); which 1 -> p_from_t (t = a, df = b).
+__global__ void scalar_stat_kernel(int which, double a, double b, double x, double* out, int* err) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  *out = which == 0 ? reg_inc_beta_scalar(a, b, x, err) : p_from_t_scalar(a, b, err);
+}
+
 __global__ void t_threshold_kernel(double p_thr, double df, double* out) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
@@ -292,6 +299,12 @@ int elementwise_reg_inc_beta(const double* a, const double* b, const double* x, 
                              int* err_flag, cudaStream_t s) {
   if (n <= 0) return PG_OK;
   reg_inc_beta_kernel<<<grid_for(n, 128), 128, 0, s>>>(a, b, x, n, out, err_flag);
+  PG_CUDA_CHECK(cudaGetLastError());
+  return PG_OK;
+}
+
+int scalar_stat(int which, double a, double b, double x, double* d_out, int* err_flag, cudaStream_t s) {
+  scalar_stat_kernel<<<1, 32, 0, s>>>(which, a, b, x, d_out, err_flag);
   PG_CUDA_CHECK(cudaGetLastError());
   return PG_OK;
 }

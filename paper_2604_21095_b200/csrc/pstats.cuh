@@ -35,5 +35,7 @@ int elementwise_p_from_t(const double* t, int64_t n, double df, double* p, unsig
 int elementwise_reg_inc_beta(const double* a, const double* b, const double* x, int64_t n, double* out,
                              int* err_flag, cudaStream_t s);
 int t_threshold(double p_threshold, double df, double* d_out, cudaStream_t s);
+// One scalar through the reference's scalar forms: which 0 -> I_x(a, b), 1 -> p_from_t(t = a, df = b).
+int scalar_stat(int which, double a, double b, double x, double* d_out, int* err_flag, cudaStream_t s);
 
 }  // namespace pg

@@ -70,6 +70,8 @@ def t_from_r(r, df: float):
 def p_from_t(t, df: float):
     """Two-sided Student-t p = I_{df/(df+t^2)}(df/2, 1/2), floored at P_FLOOR (p(0) = 1)."""
     _require(df >= 1.0, "p_from_t requires df >= 1")
+    if np.ndim(t) == 0:  # the reference's scalar path (kernel.py:201-204), as t_threshold_for_p uses
+        return _dev().p_from_t_scalar(float(t), float(df))
     v, shape, scalar = _flat64(t)
     p, _ = _dev().p_from_t(v, df)
     return _reshape(p, shape, scalar)
@@ -81,6 +83,8 @@ def reg_inc_beta(a, b, x):
     arrs = [np.asarray(v, dtype=np.float64) for v in (a, b, x)]
     _require(not (np.any(arrs[0] <= 0.0) or np.any(arrs[1] <= 0.0)), "reg_inc_beta requires a > 0 and b > 0")
     _require(not (np.any(arrs[2] < 0.0) or np.any(arrs[2] > 1.0)), "reg_inc_beta requires x in [0, 1]")
+    if all(w.ndim == 0 for w in arrs):  # scalar path (kernel.py:156-163)
+        return _dev().reg_inc_beta_scalar(float(arrs[0]), float(arrs[1]), float(arrs[2]))
     wide = np.broadcast_arrays(*arrs)
     vals = _dev().reg_inc_beta(*(w.ravel() for w in wide))
     return _reshape(vals, wide[2].shape, all(w.ndim == 0 for w in arrs))

@@ -5,6 +5,8 @@ oracle/_ref/reference_tests.zip) run unmodified against the drop-in: `import pan
 `from panelgwas.cli import main`, `python -m panelgwas.cli` all resolve to this package's
 modules (registered once in sys.modules, so exception classes and module state are shared).
 The reference's `panelgwas.oracle` (per-pair OLS) maps to the drop-in's `validation`.
+`panelgwas.cli` is a real file (cli.py) so that `python -m panelgwas.cli` runs; on import it
+replaces itself with the drop-in's cli module.
 """
 import importlib
 import sys
@@ -16,7 +18,7 @@ __version__ = _impl.__version__
 __all__ = list(getattr(_impl, "__all__", []))
 
 _ALIASES = {
-    "cli": "cli", "engine": "engine", "errors": "errors", "kernel": "kernel", "output": "output",
+    "engine": "engine", "errors": "errors", "kernel": "kernel", "output": "output",
     "phenotypes": "phenotypes", "simulate": "simulate", "oracle": "validation", "genotypes": "genotypes",
     "genotypes.types": "genotypes.types", "genotypes.plink": "genotypes.plink", "genotypes.bgen": "genotypes.bgen",
     "genotypes.dense": "genotypes.dense",

@@ -64,15 +64,17 @@ def test_two_rank_driver_equals_single_process(tmp_path, mode):
     assert not list(tmp_path.glob("multi.out.rank*"))  # shard files cleaned up
 
 
-def test_bench_two_ranks_functional():
+@pytest.mark.parametrize("shape", [["--total-markers", "12800"], ["--markers-per-gpu", "8192"]])
+def test_bench_two_ranks_functional(shape):
     """bench.py under torchrun with 2 ranks (functional check of the multi-GPU bench path on
-    one GPU over gloo: panel broadcast, max-over-ranks timing, one JSON line from rank 0)."""
+    one GPU over gloo: panel broadcast, max-over-ranks timing, one JSON line from rank 0),
+    strong (a fixed job split into 256-aligned shards) and weak (a fixed shard per rank)."""
     import json
 
     env = {**os.environ, "PANELGWAS_DIST_BACKEND": "gloo", "PANELGWAS_DIST_DEVICE": "0"}
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "2",
-           "--markers", "8192", "--phenotypes", "512", "--samples", "2000", "--steps", "3", "--warmup", "3",
+           *shape, "--phenotypes", "512", "--samples", "2000", "--steps", "3", "--warmup", "3",
            "--device-batch", "4096"]
     res = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert res.returncode == 0, res.stderr[-4000:]
@@ -80,3 +82,8 @@ def test_bench_two_ranks_functional():
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0 and d["cpu_baseline"] is None
+    strong = shape[0] == "--total-markers"
+    assert d["scaling"] == ("strong" if strong else "weak")
+    assert d["config"]["n_markers_total"] == (12800 if strong else 16384)
+    # value counts every rank's tests once: (job markers x P x K) / max-over-ranks time
+    assert abs(d["value"] * d["ms_per_step"] / 1e3 - d["config"]["n_markers_total"] * 512) < 1e-3 * d["value"]

@@ -130,6 +130,34 @@ def test_correlate_handworked_and_row_stable():
         pg.correlate(np.zeros((2, 3)), np.zeros((4, 1)))
 
 
+def test_compute_stats_block():
+    """compute_stats (reference kernel.py:493-504; tests/test_kernel.py:297, :305-320):
+    r/t/p of a whole block on the device == oracle correlate -> t_from_r -> p_from_t, with
+    the StatBlock invariants, the clamp count and the hand-worked pair r 0.5 -> t(df 2) = sqrt(2/3), p 0.5."""
+    g, _, _ = pg.standardize_columns(np.array([0.0, 1.0, 2.0, 1.0])[:, None])
+    y, _, _ = pg.standardize_columns(np.array([0.0, 1.0, 1.0, 2.0])[:, None])
+    s = pg.compute_stats(np.ascontiguousarray(g.T), y, df=2.0)
+    assert s.r[0, 0] == pytest.approx(0.5, abs=1e-15) and s.t[0, 0] == pytest.approx(np.sqrt(2 / 3), rel=1e-14)
+    assert s.p[0, 0] == pytest.approx(0.5, rel=1e-13) and s.clamp_count == 0 and s.df == 2.0
+    rng = np.random.default_rng(30)
+    gt, _, _ = pg.standardize_columns(rng.standard_normal((60, 40)))
+    yt, _, _ = pg.standardize_columns(rng.standard_normal((60, 7)))
+    gt = np.ascontiguousarray(gt.T)
+    s = pg.compute_stats(gt, yt, df=58.0)
+    r, _ = orc.correlate(gt, yt)
+    np.testing.assert_allclose(s.r, r, atol=1e-14)
+    np.testing.assert_allclose(s.t, orc.t_from_r(r, 58.0), rtol=1e-12, atol=1e-13)
+    np.testing.assert_allclose(s.p, orc.p_from_t(orc.t_from_r(r, 58.0), 58.0), rtol=1e-11)
+    assert s.r.shape == s.t.shape == s.p.shape == (40, 7)
+    assert np.all(np.abs(s.r) <= 1.0) and np.all(np.sign(s.t) == np.sign(s.r))
+    assert np.all((s.p > 0.0) & (s.p <= 1.0)) and s.p_underflow_count == 0
+    s2 = pg.compute_stats(gt, yt, df=58.0, with_p=False)
+    assert s2.p is None and np.array_equal(s2.t, s.t)
+    # a clamped pair and an underflowing p
+    s3 = pg.compute_stats(np.array([[2.0, -2.0]]), np.array([[1.0], [-1.0]]), df=1e6)
+    assert s3.clamp_count == 1 and s3.t[0, 0] == np.inf and s3.p_underflow_count == 1
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("n,p,n_cov", [(300, 12, 3), (2000, 64, 10), (5000, 700, 20), (1100, 33, 0),
                                        (12000, 1601, 5)])  # 154 MB: chunked pinned upload

@@ -2,7 +2,7 @@
 # DRAM bytes per assoc_i8 launch for raster / L2 configs (ncu metrics pass; one gpurun call).
 #   DRAM_CFGS="group:codes ..." as tools/sweep_l2.sh
 cd "${GRAFT_REPO_ROOT:-.}"
-CMD="python bench.py --markers 131072 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline"
+CMD="python bench.py --total-markers 131072 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline"
 for cfg in ${DRAM_CFGS:-74:5 -2:9}; do
   g=${cfg%%:*}
   c=${cfg##*:}

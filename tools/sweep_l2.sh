@@ -13,7 +13,7 @@ for cfg in ${SWEEP_CFGS:-0:-1 0:4 0:0 0:1 32:1 74:4 18:4 0:5 0:8}; do
     timeout 300 python tools/bench_workloads.py --workload c5 --markers ${SWEEP_MARKERS:-262144} --steps 3 2>&1 \
       | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'])"
   else
-    timeout 300 python bench.py --markers ${SWEEP_MARKERS:-524288} --steps ${SWEEP_STEPS:-4} --warmup 3 --no-e2e \
+    timeout 300 python bench.py --total-markers ${SWEEP_MARKERS:-524288} --steps ${SWEEP_STEPS:-4} --warmup 3 --no-e2e \
       --no-cpu-baseline 2>&1 | tail -1 | python -c "
 import json,sys
 d=json.loads(sys.stdin.read()); r=d['roofline']
