@@ -63,6 +63,11 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=3)
+    ap.add_argument("--missing-share", type=float, default=0.0,
+                    help="share of markers with missing calls (C3 variants; default none)")
+    ap.add_argument("--missing-rate", type=float, default=0.0, help="missing-call rate within those markers")
+    ap.add_argument("--no-missing-side", action="store_true",
+                    help="A/B: batches with missing calls take the two-row planes path")
     a = ap.parse_args()
     a.total = a.total_markers or (8_900_000 if a.workload == "c4" else 1_000_000)
     a.scaling = "weak" if a.markers_per_gpu else "strong"
@@ -106,6 +111,8 @@ def workload_config(a, world: int) -> dict:
         "device_batch_markers": a.device_batch,
         "parallelism": f"marker shards x{world} (panel broadcast once over NCCL)",
         "l2_policy": "inputs larger than L2 (5.75 GB packed genotypes + 1.4 GB panel limbs per GPU per step)",
+        "missing_calls": ({"marker_share": a.missing_share, "rate": a.missing_rate} if a.missing_share > 0
+                          and a.missing_rate > 0 else None),
     }
 
 
@@ -159,8 +166,10 @@ def measured_peaks() -> dict:
 
 
 # --------------------------------------------------------------------------- synthetic data (device, torch plumbing)
-def synth_packed(torch, n_markers: int, n_samples: int, pitch: int, seed: int, device):
-    """Packed .bed rows [M, pitch] uint8 on the device: G ~ Binomial(2, AF), AF ~ U(0.05, 0.95)."""
+def synth_packed(torch, n_markers: int, n_samples: int, pitch: int, seed: int, device, miss_share: float = 0.0,
+                 miss_rate: float = 0.0):
+    """Packed .bed rows [M, pitch] uint8 on the device: G ~ Binomial(2, AF), AF ~ U(0.05, 0.95);
+    a share `miss_share` of the markers has each call missing with probability `miss_rate`."""
     out = torch.zeros((n_markers, pitch), dtype=torch.uint8, device=device)
     gen = torch.Generator(device=device).manual_seed(seed)
     bpm = (n_samples + 3) // 4
@@ -172,6 +181,10 @@ def synth_packed(torch, n_markers: int, n_samples: int, pitch: int, seed: int, d
         g = (torch.rand(e - s, n_samples, generator=gen, device=device) < af).to(torch.uint8)
         g += (torch.rand(e - s, n_samples, generator=gen, device=device) < af).to(torch.uint8)
         codes = lut[g.long()]
+        if miss_share > 0 and miss_rate > 0:
+            rows = torch.rand(e - s, 1, generator=gen, device=device) < miss_share
+            miss = (torch.rand(e - s, n_samples, generator=gen, device=device) < miss_rate) & rows
+            codes = torch.where(miss, torch.ones_like(codes), codes)  # code 01 = missing
         pad = bpm * 4 - n_samples
         if pad:
             codes = torch.nn.functional.pad(codes, (0, pad))
@@ -304,6 +317,8 @@ def our_arm(a) -> None:
     df = float(n - 2)
 
     ctx = DeviceContext(local)
+    if a.no_missing_side:
+        ctx.set_missing_side_gemm(False)
     gidx = np.arange(n, dtype=np.int64)
     ytil = synth_panel(torch, n, p, a.seed, dev) if rank == 0 else None
 
@@ -340,7 +355,7 @@ def our_arm(a) -> None:
     distribute_panel(None)
     rbar = np.full(p, threshold_premask(a.p_threshold, df))
     ctx.set_scan(df, _native.PG_MODE_THRESHOLD, rbar)
-    packed = synth_packed(torch, m, n, pitch, a.seed * 7919 + rank, dev)
+    packed = synth_packed(torch, m, n, pitch, a.seed * 7919 + rank, dev, a.missing_share, a.missing_rate)
     torch.cuda.synchronize()
     stream = torch.cuda.ExternalStream(ctx.stream_handle(), device=dev)
     batches = [(s, min(a.device_batch, m - s)) for s in range(0, m, a.device_batch)]

@@ -143,6 +143,11 @@ PG_API int pg_ctx_set_wide_digits(pg_ctx* ctx, int enable);
 /* Tuning switch: decode PLINK rows inside the GEMM producer (default 1) or through
  * materialized int8 planes (0). Results are identical; exposed for A/B measurement. */
 PG_API int pg_ctx_set_fused_decode(pg_ctx* ctx, int enable);
+/* PLINK batches with missing calls (reference imputes them per marker, kernel.py:399-408):
+ * 1 (default) keeps the fused one-row-per-marker GEMM and runs the missing-call mask rows of
+ * only the markers that have any through a side GEMM; 0 sends the whole batch to the two-row
+ * (dosage, mask) planes. Exact either way: results are bitwise identical (A/B switch). */
+PG_API int pg_ctx_set_missing_side_gemm(pg_ctx* ctx, int enable);
 
 /* Result summary of the last scan call. */
 typedef struct pg_batch_info {

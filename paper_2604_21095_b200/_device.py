@@ -200,6 +200,9 @@ class DeviceContext:
     def set_fused_decode(self, enable: bool) -> None:
         call("pg_ctx_set_fused_decode", self._h, 1 if enable else 0)
 
+    def set_missing_side_gemm(self, enable: bool) -> None:
+        call("pg_ctx_set_missing_side_gemm", self._h, 1 if enable else 0)
+
     def set_rbar(self, r_bar: np.ndarray) -> None:
         rb = np.ascontiguousarray(r_bar, dtype=np.float64)
         with self.lock:

@@ -55,6 +55,14 @@ struct AssocEpilogue {
   int64_t full_ld;
   long long* x_accum;           // K-sliced runs (k_pad > kSliceK): int64 (xu, xm) partials
   int64_t x_ld;                 //   [marker slot][x_ld = p_pad][2]; null otherwise
+  // Missing-call side path (PLINK, fused decode, rows_per_marker 1): a planes GEMM over the
+  // mask rows of the markers that have missing calls writes Mq = sum_missing q per
+  // (row j, phenotype) to side_out[j * side_ld + p] (nothing else); the fused GEMM then reads
+  // xm = side_x[side_slot[m] * side_ld + p] for markers with side_slot[m] >= 0 (else 0).
+  long long* side_out;
+  const long long* side_x;
+  const int* side_slot;
+  int64_t side_ld;
 };
 
 // Launch K2/K3 on `stream`. Panel limbs q*[p_pad, k_pad], genotype planes

@@ -298,8 +298,17 @@ __device__ __forceinline__ void epilogue_tile(const AssocEpilogue& ep, uint32_t 
     for (int j = 0; j < 16; j += R) {
       // exact per-row products, then recombine the rows of this marker
       long long xu = 0, xm = 0;
+      const int m = ct * kMarkersPerTile + (c + j) / R;
       if constexpr (R == 1) {
         xu = kWH * static_cast<long long>(static_cast<int>(h[j])) + static_cast<int>(l[j]);
+        if (ep.side_out) {  // side GEMM over mask rows: keep Mq of row m
+          ep.side_out[static_cast<int64_t>(m) * ep.side_ld + pheno] = xu;
+          continue;
+        }
+        if (ep.side_slot) {  // fused GEMM: Mq of the markers with missing calls
+          const int sl = __ldg(ep.side_slot + m);
+          if (sl >= 0) xm = __ldg(ep.side_x + static_cast<int64_t>(sl) * ep.side_ld + pheno);
+        }
       } else {
         long long w = 1;
 #pragma unroll
@@ -309,7 +318,6 @@ __device__ __forceinline__ void epilogue_tile(const AssocEpilogue& ep, uint32_t 
         }
         xm = kWH * static_cast<long long>(static_cast<int>(h[j + R - 1])) + static_cast<int>(l[j + R - 1]);
       }
-      const int m = ct * kMarkersPerTile + (c + j) / R;
       if (ep.x_accum) {  // K-sliced run: exact int64 partials, statistics after the last slice
         long long* x = ep.x_accum + (static_cast<int64_t>(m) * ep.x_ld + pheno) * 2;
         x[0] += xu;

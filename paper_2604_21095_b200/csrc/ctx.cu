@@ -227,6 +227,12 @@ struct pg_ctx {
   pg::DBuf<uint8_t> full_out;
   pg::DBuf<double> scratch_a, scratch_b, scratch_c, scratch_d;
   pg::DBuf<long long> xacc, xacc_b;  // K-sliced runs (cohorts above kSliceK samples)
+  // missing-call side path of the fused PLINK GEMM (pg_ctx_set_missing_side_gemm)
+  bool side_missing = true;
+  pg::DBuf<int> miss_flag, miss_prefix, miss_slot, miss_list, miss_count;
+  pg::DBuf<int8_t> side_v, side_v127;
+  pg::DBuf<long long> side_x;
+  pg::DBuf<uint8_t> scan_tmp;
 
   // last batch
   int64_t last_m = 0, last_ncand = 0;
@@ -335,6 +341,9 @@ int64_t expected_row_bytes(int kind, int64_t n_src) {
 // Largest candidate count of one batch: the cub sort takes int item counts, and 2^30 pairs
 // already hold ~70 GB of device candidate buffers.
 constexpr int64_t kMaxCandidates = int64_t(1) << 30;
+// Largest side-GEMM output (8 B per marker-with-missing-calls x phenotype) before a batch
+// falls back to the two-row planes path.
+constexpr int64_t kSideBytesMax = int64_t(12) << 30;
 
 int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t pitch, pg_batch_info* info,
                 int64_t probs_off = 0, int64_t ploidy_off = -1) {
@@ -388,11 +397,36 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
   st.invd_f = c->invd_f.p;
   st.flags = c->flags.p;
   PG_CHECK_STATUS(geno_stats(b, st, m_cap, s));
+  // PLINK batches with missing calls: only the markers that have them carry a mask row, in
+  // a side GEMM; the batch keeps the fused one-row-per-marker GEMM (K-sliced and extension
+  // runs use the two-row planes instead)
+  const bool side_ok = c->side_missing && c->fused_decode && kind == PG_GENO_BED && c->k_pad <= kSliceK &&
+                       !c->have_basis;
+  int n_side = 0;
+  if (side_ok) {
+    for (auto* buf : {&c->miss_flag, &c->miss_prefix, &c->miss_list}) PG_CHECK_STATUS(buf->ensure(m));
+    PG_CHECK_STATUS(c->miss_slot.ensure(m_cap));
+    PG_CHECK_STATUS(c->miss_count.ensure(1));
+    PG_CUDA_CHECK(cudaMemsetAsync(c->miss_slot.p, 0xFF, sizeof(int) * m_cap, s));  // -1: no missing calls
+    PG_CHECK_STATUS(missing_flags(c->n_miss.p, c->skip.p, m, c->miss_flag.p, s));
+    size_t tmp_bytes = 0;
+    PG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, c->miss_flag.p, c->miss_prefix.p,
+                                                static_cast<int>(m), s));
+    PG_CHECK_STATUS(c->scan_tmp.ensure(tmp_bytes));
+    PG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(c->scan_tmp.p, tmp_bytes, c->miss_flag.p, c->miss_prefix.p,
+                                                static_cast<int>(m), s));
+    PG_CHECK_STATUS(missing_slot_map(c->miss_flag.p, c->miss_prefix.p, m, c->miss_slot.p, c->miss_list.p,
+                                     c->miss_count.p, s));
+    PG_CUDA_CHECK(cudaMemcpyAsync(&n_side, c->miss_count.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  }
   PG_CUDA_CHECK(cudaMemcpyAsync(hflags, c->flags.p, sizeof(int) * 2, cudaMemcpyDeviceToHost, s));
   PG_CUDA_CHECK(cudaStreamSynchronize(s));
   // dosage sources use the wide-digit GEMM (3 rows per BGEN-8 marker, 4 otherwise) unless
   // disabled for A/B tests
-  const int R = geno_rows_per_marker(b, hflags[0] != 0, c->wide_digits);
+  int R = geno_rows_per_marker(b, hflags[0] != 0, c->wide_digits);
+  const int64_t side_rows = round_up(n_side, kTileC);
+  const bool use_side = side_ok && R == 2 && side_rows * c->p_pad * 8 <= kSideBytesMax;
+  if (use_side) R = 1;
   const bool wide = R == kWideRows || R == kWideRows3;
   const int64_t c_pad = round_up(m * R, wide ? (R == kWideRows3 ? kTileCWide3 : kTileCWide) : kTileC);
   // PLINK rows without missing calls: the GEMM decodes the packed codes itself
@@ -410,7 +444,39 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
     if (wide) return launch_assoc_wide(a, b1, b0, pp, c->v.p, c_pad, c->k_pad, e, s);
     return launch_assoc(a, b1, b0, pp, c->v.p, c->v127.p, c_pad, c->k_pad, e, s);
   };
-  auto run_gemm = [&](const AssocEpilogue& e) -> int { return run_gemm_on(e, c->qh.p, c->q1.p, c->q0.p, c->p_pad); };
+  // side GEMM over the mask rows of the markers with missing calls -> Mq per (marker, phenotype)
+  bool side_pending = use_side && n_side > 0;
+  if (side_pending) {
+    PG_CHECK_STATUS(c->side_v.ensure(static_cast<size_t>(side_rows) * c->k_pad));
+    PG_CHECK_STATUS(c->side_v127.ensure(static_cast<size_t>(side_rows) * c->k_pad));
+    PG_CHECK_STATUS(c->side_x.ensure(static_cast<size_t>(side_rows) * c->p_pad));
+    PG_CHECK_STATUS(missing_mask_planes(b, c->miss_list.p, n_side, c->side_v.p, c->side_v127.p, side_rows, c->k_pad, s));
+    ++launches;
+  }
+  auto run_side = [&]() -> int {
+    if (!side_pending) return PG_OK;
+    side_pending = false;
+    AssocEpilogue es{};
+    es.rows_per_marker = 1;
+    es.m_valid = n_side;
+    es.p_valid = c->n_pheno;
+    es.mu_f = c->mu_f.p;
+    es.mu_d = c->mu_d.p;
+    es.invd_f = c->invd_f.p;
+    es.invd_d = c->invd_d.p;
+    es.scale_f = c->scale_f.p;
+    es.scale_d = c->scale_d.p;
+    es.cq_f = c->cq_f.p;
+    es.cq = c->cq.p;
+    es.side_out = c->side_x.p;
+    es.side_ld = c->p_pad;
+    ++launches;
+    return launch_assoc(c->qh.p, c->q1.p, c->q0.p, c->p_pad, c->side_v.p, c->side_v127.p, side_rows, c->k_pad, es, s);
+  };
+  auto run_gemm = [&](const AssocEpilogue& e) -> int {
+    PG_CHECK_STATUS(run_side());
+    return run_gemm_on(e, c->qh.p, c->q1.p, c->q0.p, c->p_pad);
+  };
   if (c->have_basis) {
     // K5: w = Q^T u_imp for every marker (exact side GEMM against the quantized basis)
     PG_CHECK_STATUS(c->wbuf.ensure(static_cast<size_t>(c_pad / R) * kTileP));
@@ -466,6 +532,11 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
   ep.cq_f = c->cq_f.p;
   ep.cq = c->cq.p;
   ep.max_abs_r = c->track_max_abs_r ? c->max_abs_r.p : nullptr;
+  if (use_side && n_side > 0) {
+    ep.side_x = c->side_x.p;
+    ep.side_slot = c->miss_slot.p;
+    ep.side_ld = c->p_pad;
+  }
   PG_CHECK_STATUS(c->cand_count.ensure(1));
   ep.cand_count = c->cand_count.p;
   if (c->k_pad > kSliceK) {  // K-sliced contraction: exact int64 partials per (marker, phenotype)
@@ -980,6 +1051,12 @@ int pg_ctx_debug_candidate_base(pg_ctx* c, uint64_t base) {
 int pg_ctx_set_wide_digits(pg_ctx* c, int enable) {
   PG_CHECK_STATUS(ctx_check(c));
   c->wide_digits = enable != 0;
+  return PG_OK;
+}
+
+int pg_ctx_set_missing_side_gemm(pg_ctx* c, int enable) {
+  PG_CHECK_STATUS(ctx_check(c));
+  c->side_missing = enable != 0;
   return PG_OK;
 }
 

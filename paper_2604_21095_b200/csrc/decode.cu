@@ -15,6 +15,7 @@
 // with the reference. The GEMM operand is the balanced-ternary expansion of u,
 // one int8 row per digit (plus a 0/1 row of missing calls when present), and
 // its x127 copy (assoc.cuh).
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 
@@ -499,6 +500,48 @@ int stats_dispatch(const GenoBlock& b, MarkerStats& st, int64_t m_pad, cudaStrea
   return PG_OK;
 }
 
+// Missing-call side path of the fused PLINK GEMM: the mask row (kept missing calls) and
+// its x127 copy of marker list[j] go to row j of v / v127; rows past n_list are zero.
+__global__ void mask_planes_kernel(GenoBlock b, const int* __restrict__ list, int64_t n_list, int8_t* __restrict__ v,
+                                   int8_t* __restrict__ v127, int64_t k_pad) {
+  const int64_t j = blockIdx.x;
+  const int64_t ci = static_cast<int64_t>(blockIdx.y) * blockDim.x + threadIdx.x;
+  if (ci * kChunk >= k_pad) return;
+  int mk[kChunk];
+  uint32_t miss = 0;
+  if (j < n_list && ci * kChunk < b.n_src) {
+    int u[kChunk];
+    uint32_t obs = 0;
+    double ds = 0;
+    bool ni = false;
+    load16<PG_GENO_BED>(b, list[j], ci, u, miss, obs, ds, ni);
+  }
+#pragma unroll
+  for (int i = 0; i < kChunk; ++i) mk[i] = (miss >> i) & 1u;
+  *reinterpret_cast<uint4*>(v + j * k_pad + ci * kChunk) = pack16(mk, 1);
+  *reinterpret_cast<uint4*>(v127 + j * k_pad + ci * kChunk) = pack16(mk, 127);
+}
+
+// flag[m] = marker m is scanned (not skipped) and has a kept missing call
+__global__ void miss_flag_kernel(const long long* __restrict__ n_miss, const int8_t* __restrict__ skip, int64_t m,
+                                 int* __restrict__ flag) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    flag[i] = (n_miss[i] > 0 && skip[i] == 0) ? 1 : 0;
+}
+
+// exclusive prefix of the flags -> slot[m] (-1 when unflagged), list[slot] = m, *count
+__global__ void miss_slot_kernel(const int* __restrict__ flag, const int* __restrict__ prefix, int64_t m,
+                                 int* __restrict__ slot, int* __restrict__ list, int* __restrict__ count) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int f = flag[i];
+    slot[i] = f ? prefix[i] : -1;
+    if (f) list[prefix[i]] = static_cast<int>(i);
+    if (i == m - 1) *count = prefix[i] + f;
+  }
+}
+
 template <int KIND, int R>
 int planes_launch(const GenoBlock& b, int8_t* v, int8_t* v127, int64_t c_pad, int64_t k_pad, cudaStream_t s) {
   const int64_t m_slots = c_pad / R;
@@ -525,6 +568,32 @@ int planes_dispatch(const GenoBlock& b, int R, int8_t* v, int8_t* v127, int64_t 
 }
 
 }  // namespace
+
+int missing_flags(const long long* n_miss, const int8_t* skip, int64_t m, int* flag, cudaStream_t s) {
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>((m + 255) / 256, 4096));
+  miss_flag_kernel<<<grid, 256, 0, s>>>(n_miss, skip, m, flag);
+  PG_CUDA_CHECK(cudaGetLastError());
+  return PG_OK;
+}
+
+int missing_slot_map(const int* flag, const int* prefix, int64_t m, int* slot, int* list, int* d_count,
+                     cudaStream_t s) {
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>((m + 255) / 256, 4096));
+  miss_slot_kernel<<<grid, 256, 0, s>>>(flag, prefix, m, slot, list, d_count);
+  PG_CUDA_CHECK(cudaGetLastError());
+  return PG_OK;
+}
+
+int missing_mask_planes(const GenoBlock& b, const int* list, int64_t n_list, int8_t* v, int8_t* v127, int64_t c_pad,
+                        int64_t k_pad, cudaStream_t s) {
+  PG_REQUIRE(b.kind == PG_GENO_BED && k_pad % 64 == 0 && c_pad >= n_list, PG_ERR_INVALID,
+             "missing_mask_planes: bad arguments");
+  const int64_t chunks = k_pad / kChunk;
+  dim3 grid(static_cast<unsigned>(c_pad), static_cast<unsigned>((chunks + 127) / 128));
+  mask_planes_kernel<<<grid, 128, 0, s>>>(b, list, n_list, v, v127, k_pad);
+  PG_CUDA_CHECK(cudaGetLastError());
+  return PG_OK;
+}
 
 int geno_check_integral(const GenoBlock& b, MarkerStats& st, cudaStream_t s) {
   if (b.kind != PG_GENO_DENSE_F64 || b.n_markers == 0) return PG_OK;

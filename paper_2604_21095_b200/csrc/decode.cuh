@@ -58,6 +58,17 @@ int geno_stats(const GenoBlock& b, MarkerStats& st, int64_t m_pad, cudaStream_t 
 // (R = 1, 2, 8, 16), or for R = 4 (wide mode, geno_wide) base-255 digits in v only.
 int geno_planes(const GenoBlock& b, int rows_per_marker, int8_t* v, int8_t* v127, int64_t c_pad, int64_t k_pad,
                 cudaStream_t s);
+// Missing-call side path of the fused PLINK GEMM (markers with missing calls carry a mask
+// row in a separate GEMM; the rest of the batch keeps one row per marker):
+// flag[m] = scanned marker m has a kept missing call; after an exclusive prefix sum of the
+// flags: slot[m] = its index among those markers (-1 if none), list[slot] = m, *d_count.
+int missing_flags(const long long* n_miss, const int8_t* skip, int64_t m, int* flag, cudaStream_t s);
+int missing_slot_map(const int* flag, const int* prefix, int64_t m, int* slot, int* list, int* d_count,
+                     cudaStream_t s);
+// Mask rows (kept missing calls; v = mask, v127 = 127 mask) of markers list[0..n_list) as
+// rows 0..n_list of [c_pad, k_pad] planes (rows past n_list zero).
+int missing_mask_planes(const GenoBlock& b, const int* list, int64_t n_list, int8_t* v, int8_t* v127, int64_t c_pad,
+                        int64_t k_pad, cudaStream_t s);
 // Dosage decode for the reader API: out[m, n_src] f32/f64 with NaN missing, missing counts.
 int geno_dosages(const GenoBlock& b, int elem_bytes, void* out, int64_t* missing, cudaStream_t s);
 

@@ -456,6 +456,8 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, init, ctx_fut, mark
 
     if os.environ.get("PANELGWAS_FUSED_DECODE", "1") == "0":
         ctx.set_fused_decode(False)  # A/B switch; results are identical either way
+    if os.environ.get("PANELGWAS_MISSING_SIDE_GEMM", "1") == "0":
+        ctx.set_missing_side_gemm(False)  # A/B switch: two-row planes for batches with missing calls
     if os.environ.get("PANELGWAS_WIDE_DIGITS", "1") == "0":
         ctx.set_wide_digits(False)  # A/B switch; results are identical either way
     try:

@@ -53,7 +53,7 @@ def run(json_out: Path | None, extra: list[str]) -> dict:
         cmd = [sys.executable, "-m", "pytest", str(tests), "-q", "-p", "no:cacheprovider", "-rfE",
                f"--junitxml={junit}", "--rootdir", str(tmp)]
         for node in EXCLUDED:
-            cmd += ["--deselect", f"{tests}/{node}"]
+            cmd += ["--deselect", f"tests/{node}"]
         proc = subprocess.run(cmd + extra, cwd=tmp, env=env, capture_output=True, text=True)
         out = proc.stdout + proc.stderr
         summary = {"returncode": proc.returncode, "excluded": EXCLUDED}
