@@ -195,6 +195,8 @@ struct pg_ctx {
   pg::DBuf<uint8_t> bgen_blob[2], bgen_raw[2];
   pg::DBuf<int64_t> bgen_off[2], bgen_size[2], bgen_len[2];
   pg::DBuf<int> bgen_zstatus[2], bgen_bits[2];
+  pg::DBuf<uint32_t> bgen_tok[2];  // two-phase GPU inflate: LZ77 tokens per stream
+  pg::DBuf<int32_t> bgen_ntok[2];
   pg::DBuf<long long> bgen_diag[2];
   pg::DBuf<unsigned long long> bgen_summary[2];
   void* bgen_host[2] = {nullptr, nullptr};  // pinned copies of the validation summaries
@@ -1140,13 +1142,17 @@ int pg_stage_bgen_begin(pg_ctx* c, int slot, const void* blob, int64_t blob_byte
   // the slot's buffers may still be read by the scan that last used it
   PG_CUDA_CHECK(cudaStreamWaitEvent(cs, c->slot_free_ev[slot], 0));
   if (c->bgen_blob[slot].cap < static_cast<size_t>(blob_bytes + 16) ||
-      c->bgen_raw[slot].cap < static_cast<size_t>(raw_stride) * count || c->bgen_off[slot].cap < static_cast<size_t>(count))
+      c->bgen_raw[slot].cap < static_cast<size_t>(raw_stride) * count || c->bgen_off[slot].cap < static_cast<size_t>(count) ||
+      c->bgen_tok[slot].cap < static_cast<size_t>(pg::inflate_token_stride(raw_stride)) * count ||
+      c->bgen_ntok[slot].cap < static_cast<size_t>(2 * count))
     PG_CUDA_CHECK(cudaStreamSynchronize(cs));  // reallocation below must not free memory in use
   PG_CHECK_STATUS(c->bgen_blob[slot].ensure(blob_bytes + 16));  // the decoder reads ahead <= 8 B past a stream
   PG_CHECK_STATUS(c->bgen_raw[slot].ensure(static_cast<size_t>(raw_stride) * count));
   for (auto* b : {&c->bgen_off[slot], &c->bgen_size[slot], &c->bgen_len[slot]}) PG_CHECK_STATUS(b->ensure(count));
   PG_CHECK_STATUS(c->bgen_zstatus[slot].ensure(count));
   PG_CHECK_STATUS(c->bgen_bits[slot].ensure(count));
+  PG_CHECK_STATUS(c->bgen_tok[slot].ensure(static_cast<size_t>(pg::inflate_token_stride(raw_stride)) * count));
+  PG_CHECK_STATUS(c->bgen_ntok[slot].ensure(2 * count));
   PG_CHECK_STATUS(c->bgen_diag[slot].ensure(3 * count));
   PG_CHECK_STATUS(c->bgen_summary[slot].ensure(2));
   if (c->bgen_host[slot] == nullptr) PG_CUDA_CHECK(cudaHostAlloc(&c->bgen_host[slot], 64, cudaHostAllocDefault));
@@ -1157,7 +1163,7 @@ int pg_stage_bgen_begin(pg_ctx* c, int slot, const void* blob, int64_t blob_byte
   // genotype block = u32 uncompressed length + zlib stream
   PG_CHECK_STATUS(pg::inflate_streams(c->bgen_blob[slot].p, c->bgen_off[slot].p, c->bgen_size[slot].p, count, 4,
                                       c->bgen_raw[slot].p, raw_stride, c->bgen_len[slot].p, c->bgen_zstatus[slot].p,
-                                      cs));
+                                      cs, c->bgen_tok[slot].p, c->bgen_ntok[slot].p));
   PG_CUDA_CHECK(cudaMemsetAsync(c->bgen_summary[slot].p, 0xFF, sizeof(unsigned long long), cs));
   PG_CUDA_CHECK(cudaMemsetAsync(c->bgen_summary[slot].p + 1, 0, sizeof(unsigned long long), cs));
   PG_CHECK_STATUS(pg::bgen_validate(c->bgen_blob[slot].p, c->bgen_off[slot].p, c->bgen_size[slot].p,

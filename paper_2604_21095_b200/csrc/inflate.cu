@@ -503,17 +503,492 @@ __global__ void __launch_bounds__(4 * L) inflate_kernel(const uint8_t* __restric
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// Two-phase decoder (default). The warp-per-stream kernel above runs the serial Huffman decode
+// on all 32 lanes in lock-step: ~100 warp instructions per DEFLATE symbol, 32x redundant. Here
+//   phase 1 (thread per stream): each thread decodes its own stream's Huffman codes into LZ77
+//            tokens (literal runs of 1-3 bytes | (length, distance) matches) and validates the
+//            stream completely (header, block types, code tables, distances vs output so far,
+//            output capacity) — 32 streams per warp, no redundant lanes;
+//   phase 2 (warp per stream): the warp expands 32 tokens at a time — a prefix sum of their
+//            lengths places every literal run, which lanes write in parallel, then the
+//            matches are copied cooperatively in order — and checks the Adler-32 trailer.
+// Tables of phase 1 live in shared memory per thread (first level: 2^10 literal/length,
+// 2^8 distance entries, same pre-decoded entry formats as above); the canonical arrays for
+// longer codes are thread-local.
+//
+// Token (u32): literal run: n << 30 | b0 | b1 << 8 | b2 << 16 (n = 1..3);
+//              match:       length << 16 | distance (length 3..258, distance 1..32768).
+constexpr int kTokLitBits = 10;
+constexpr int kTokDistBits = 8;
+constexpr int kTokThreads = 32;  // streams per block (one warp)
+
+struct ThreadTables {
+  uint16_t lit[1 << kTokLitBits];
+  uint16_t dist[1 << kTokDistBits];
+};
+
+struct Canon {  // canonical (count, symbol) arrays for codes longer than the first level
+  uint16_t count[16];
+  uint16_t sym[288];
+};
+
+// Per-thread canonical table build (zlib completeness rules, as `build` above).
+template <class Enc, int BITS>
+__device__ bool build1(uint16_t* lut, Canon& cn, const uint8_t* lens, int n, bool code_lengths) {
+  uint16_t count[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) count[i] = 0;
+  for (int s = 0; s < n; ++s) ++count[lens[s]];
+  int left = 1, max_len = 0;
+#pragma unroll
+  for (int l = 1; l < 16; ++l) {
+    left = (left << 1) - count[l];
+    if (left < 0) return false;
+    if (count[l]) max_len = l;
+  }
+  if (left > 0 && (code_lengths || max_len != 1) && !(!code_lengths && max_len == 0)) return false;
+  uint16_t next[16], offs[16];
+  int code = 0, off = 0;
+  count[0] = 0;
+  for (int l = 1; l < 16; ++l) {
+    code = (code + count[l - 1]) << 1;
+    next[l] = static_cast<uint16_t>(code);
+    offs[l] = static_cast<uint16_t>(off);
+    off += count[l];
+    cn.count[l] = count[l];
+  }
+  for (int i = 0; i < (1 << BITS); ++i) lut[i] = 0;
+  for (int s = 0; s < n; ++s) {
+    const int l = lens[s];
+    if (!l) continue;
+    const uint32_t c = next[l]++;
+    cn.sym[offs[l]++] = static_cast<uint16_t>(s);
+    if (l > BITS) continue;
+    const uint32_t rev = __brev(c) >> (32 - l);
+    const uint16_t e = static_cast<uint16_t>(Enc::enc(s, l));
+    for (uint32_t i = rev; i < (1u << BITS); i += 1u << l) lut[i] = e;
+  }
+  return true;
+}
+
+__device__ __forceinline__ int decode_canon(Bits& br, const Canon& cn) {
+  const uint32_t bits = static_cast<uint32_t>(br.buf);
+  int code = 0, first = 0, index = 0;
+  for (int l = 1; l < 16; ++l) {
+    code |= static_cast<int>((bits >> (l - 1)) & 1u);
+    const int c = cn.count[l];
+    if (code - c < first) {
+      br.get(l);
+      return cn.sym[index + (code - first)];
+    }
+    index += c;
+    first = (first + c) << 1;
+    code <<= 1;
+  }
+  return -1;
+}
+
+template <class Enc, int BITS>
+__device__ __forceinline__ uint32_t decode1(Bits& br, const uint16_t* lut, const Canon& cn) {
+  const uint32_t e = lut[static_cast<uint32_t>(br.buf) & ((1u << BITS) - 1u)];
+  if (e & 15u) {
+    br.get(e & 15u);
+    return e;
+  }
+  const int sym = decode_canon(br, cn);
+  return sym < 0 ? Enc::kInvalid : Enc::enc(sym, 1);
+}
+
+struct TokenSink {  // 4 tokens per 16-byte store
+  uint32_t* dst;
+  int32_t n = 0, cap;
+  uint32_t q[4];
+  uint32_t lit = 0;
+  int nlit = 0;
+  __device__ __forceinline__ bool put(uint32_t t) {
+    if (n >= cap) return false;
+    q[n & 3] = t;
+    ++n;
+    if ((n & 3) == 0) *reinterpret_cast<uint4*>(dst + n - 4) = make_uint4(q[0], q[1], q[2], q[3]);
+    return true;
+  }
+  __device__ __forceinline__ bool literal(uint32_t b) {
+    lit |= b << (8 * nlit);
+    if (++nlit < 3) return true;
+    return flush_lit();
+  }
+  __device__ __forceinline__ bool flush_lit() {
+    if (!nlit) return true;
+    const bool ok = put((static_cast<uint32_t>(nlit) << 30) | lit);
+    lit = 0;
+    nlit = 0;
+    return ok;
+  }
+  __device__ __forceinline__ void finish() {
+    for (int i = n & ~3; i < n; ++i) dst[i] = q[i & 3];
+  }
+};
+
+__global__ void __launch_bounds__(kTokThreads) inflate_tokens_kernel(
+    const uint8_t* __restrict__ blob, const int64_t* __restrict__ off, const int64_t* __restrict__ len, int64_t count,
+    int64_t skip, int64_t out_stride, uint32_t* __restrict__ tokens, int64_t tok_stride, int32_t* __restrict__ ntok,
+    int64_t* __restrict__ out_len, int* __restrict__ status) {
+  extern __shared__ ThreadTables tabs[];  // kTokThreads entries (dynamic: 80 KB)
+  const int64_t stream = static_cast<int64_t>(blockIdx.x) * kTokThreads + threadIdx.x;
+  if (stream >= count) return;
+  ThreadTables& tb = tabs[threadIdx.x];
+  Canon clit, cdist;
+  uint8_t lens[288 + 32];
+
+  const uint8_t* start = blob + off[stream] + skip;
+  const int64_t n_in = len[stream] - skip;
+  const uintptr_t base = reinterpret_cast<uintptr_t>(start) & ~uintptr_t(3);
+  const uint8_t* b8 = reinterpret_cast<const uint8_t*>(base);
+  const uint32_t lead = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(start) - base) * 8u;
+  Bits br;
+  br.w = reinterpret_cast<const uint32_t*>(base);
+  br.wi = 0;
+  br.nextw = __ldg(br.w);
+  br.buf = 0;
+  br.cnt = 0;
+  br.end = n_in < 0 ? 0 : lead + static_cast<uint32_t>(n_in) * 8u;
+  br.last_word = (br.end + 31) / 32 + 1;
+  br.refill();
+  br.refill();
+  br.get(lead);
+  TokenSink sink;
+  sink.dst = tokens + stream * tok_stride;
+  sink.cap = static_cast<int32_t>(tok_stride);
+  const int32_t cap = static_cast<int32_t>(out_stride);
+  int32_t pos = 0;
+  int err = n_in < 2 ? 1 : 0;
+  if (!err) {
+    const uint32_t cmf = br.get(8), flg = br.get(8);
+    if ((cmf & 15) != 8 || (cmf >> 4) > 7 || ((cmf << 8) | flg) % 31 != 0 || (flg & 0x20)) err = 1;
+  }
+  bool last = false;
+  while (!err && !last) {
+    br.refill();
+    last = br.get(1);
+    const uint32_t type = br.get(2);
+    if (!br.ok() || type == 3) {
+      err = 1;
+      break;
+    }
+    if (type == 0) {
+      const uint32_t byte_pos = (br.consumed() + 7) >> 3;
+      if (byte_pos * 8 + 32 > br.end) {
+        err = 1;
+        break;
+      }
+      const uint32_t n = b8[byte_pos] | (b8[byte_pos + 1] << 8);
+      const uint32_t nn = b8[byte_pos + 2] | (b8[byte_pos + 3] << 8);
+      if ((n ^ 0xFFFFu) != nn || (byte_pos + 4 + n) * 8 > br.end) {
+        err = 1;
+        break;
+      }
+      if (pos + static_cast<int32_t>(n) > cap) {
+        err = 2;
+        break;
+      }
+      for (uint32_t j = 0; j < n; ++j)
+        if (!sink.literal(b8[byte_pos + 4 + j])) err = 2;
+      pos += n;
+      const uint32_t next_bit = (byte_pos + 4 + n) * 8;
+      br.wi = next_bit >> 5;
+      br.nextw = br.wi <= br.last_word ? __ldg(br.w + br.wi) : 0u;
+      br.buf = 0;
+      br.cnt = 0;
+      br.refill();
+      br.refill();
+      br.get(next_bit & 31);
+      continue;
+    }
+    if (type == 1) {
+      for (int s = 0; s < 320; ++s) lens[s] = s < 144 ? 8 : s < 256 ? 9 : s < 280 ? 7 : s < 288 ? 8 : 5;
+      build1<EncLit, kTokLitBits>(tb.lit, clit, lens, 288, false);
+      build1<EncDist, kTokDistBits>(tb.dist, cdist, lens + 288, 32, false);
+    } else {
+      const int hlit = br.get(5) + 257, hdist = br.get(5) + 1, hclen = br.get(4) + 4;
+      if (hlit > 286 || hdist > 30) {
+        err = 1;
+        break;
+      }
+      br.refill();
+      uint8_t cl[19];
+#pragma unroll
+      for (int i = 0; i < 19; ++i) cl[i] = 0;
+      for (int i = 0; i < hclen; ++i) {
+        if (i == 10) br.refill();
+        cl[c_clen_order[i]] = static_cast<uint8_t>(br.get(3));
+      }
+      // code-length code: first level in the distance table's storage (2^7 <= 2^8 entries)
+      Canon ccl;
+      if (!build1<EncClen, kClenBits>(tb.dist, ccl, cl, 19, true)) {
+        err = 1;
+        break;
+      }
+      int idx = 0;
+      const int total = hlit + hdist;
+      uint8_t prev = 0;
+      while (idx < total) {
+        br.refill();
+        const uint32_t ce = decode1<EncClen, kClenBits>(br, tb.dist, ccl);
+        if (!ce) {
+          err = 1;
+          break;
+        }
+        const int sym = static_cast<int>(ce >> 4);
+        if (sym < 16) {
+          lens[idx++] = static_cast<uint8_t>(sym);
+          prev = static_cast<uint8_t>(sym);
+          continue;
+        }
+        int rep;
+        uint8_t val = 0;
+        if (sym == 16) {
+          if (idx == 0) {
+            err = 1;
+            break;
+          }
+          val = prev;
+          rep = 3 + br.get(2);
+        } else if (sym == 17) {
+          rep = 3 + br.get(3);
+        } else {
+          rep = 11 + br.get(7);
+        }
+        if (idx + rep > total) {
+          err = 1;
+          break;
+        }
+        for (int j = 0; j < rep; ++j) lens[idx + j] = val;
+        idx += rep;
+        prev = val;
+      }
+      if (err || !br.ok()) {
+        err = 1;
+        break;
+      }
+      if (lens[256] == 0 || !build1<EncLit, kTokLitBits>(tb.lit, clit, lens, hlit, false)) {
+        err = 1;
+        break;
+      }
+      uint8_t dl[32];
+      for (int q = 0; q < 32; ++q) dl[q] = q < hdist ? lens[hlit + q] : 0;
+      if (!build1<EncDist, kTokDistBits>(tb.dist, cdist, dl, hdist, false)) {
+        err = 1;
+        break;
+      }
+    }
+    for (;;) {
+      br.refill();
+      const uint32_t e = decode1<EncLit, kTokLitBits>(br, tb.lit, clit);
+      if (!(e & EncLit::kLength)) {
+        if (!e) {
+          err = 1;
+          break;
+        }
+        if (pos >= cap) {
+          err = 2;
+          break;
+        }
+        if (!sink.literal((e >> 7) & 255u)) {
+          err = 2;
+          break;
+        }
+        ++pos;
+        continue;
+      }
+      const uint32_t extra = (e >> 4) & 7u;
+      if (extra >= 6) {
+        if (extra == 6 || !br.ok()) err = 1;
+        break;
+      }
+      const int length = 3 + static_cast<int>((e >> 7) & 255u) + static_cast<int>(br.get(extra));
+      br.refill();
+      const uint32_t de = decode1<EncDist, kTokDistBits>(br, tb.dist, cdist);
+      const int distance = c_dist_base[de >> 8] + static_cast<int>(br.get((de >> 4) & 15u));
+      if (distance > pos || pos + length > cap) {
+        err = distance > pos ? 1 : 2;
+        break;
+      }
+      if (!sink.flush_lit() || !sink.put((static_cast<uint32_t>(length) << 16) | static_cast<uint32_t>(distance))) {
+        err = 2;
+        break;
+      }
+      pos += length;
+    }
+  }
+  uint32_t trailer = 0;
+  if (!err) {
+    const uint32_t byte_pos = (br.consumed() + 7) >> 3;
+    if (byte_pos * 8 + 32 > br.end) {
+      err = 1;
+    } else {
+      trailer = (static_cast<uint32_t>(b8[byte_pos]) << 24) | (b8[byte_pos + 1] << 16) | (b8[byte_pos + 2] << 8) |
+                b8[byte_pos + 3];
+    }
+  }
+  if (!err && !sink.flush_lit()) err = 2;
+  sink.finish();
+  ntok[stream] = err ? 0 : sink.n;
+  out_len[stream] = pos;
+  status[stream] = err;
+  // phase 2 checks the Adler-32 against the trailer: keep it after the tokens' count
+  reinterpret_cast<uint32_t*>(ntok + count)[stream] = trailer;
+}
+
+// Phase 2: warp per stream; expands the tokens, then checks the Adler-32 trailer.
+__global__ void __launch_bounds__(128) inflate_expand_kernel(const uint32_t* __restrict__ tokens, int64_t tok_stride,
+                                                             const int32_t* __restrict__ ntok, int64_t count,
+                                                             uint8_t* __restrict__ out, int64_t out_stride,
+                                                             const int64_t* __restrict__ out_len,
+                                                             int* __restrict__ status) {
+  constexpr int kWarps = 4;
+  __shared__ uint8_t ring_all[kWarps][kRing];
+  const int lane = threadIdx.x & 31;
+  const int64_t stream = static_cast<int64_t>(blockIdx.x) * kWarps + (threadIdx.x >> 5);
+  if (stream >= count) return;
+  if (status[stream] != 0) return;
+  uint8_t* ring = ring_all[threadIdx.x >> 5];
+  const uint32_t* tk = tokens + stream * tok_stride;
+  const int32_t nt = ntok[stream];
+  uint8_t* const dst = out + stream * out_stride;
+  int32_t pos = 0;
+  for (int32_t b = 0; b < nt; b += 32) {
+    const bool have = b + lane < nt;
+    const uint32_t t = have ? __ldg(tk + b + lane) : 0u;
+    const uint32_t nl = t >> 30;
+    const bool is_match = have && nl == 0;
+    const int32_t tlen = !have ? 0 : (is_match ? static_cast<int32_t>((t >> 16) & 0x3FFu) : static_cast<int32_t>(nl));
+    int32_t incl = tlen;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int32_t my_pos = pos + incl - tlen;
+    const int32_t chunk_end = pos + __shfl_sync(0xffffffffu, incl, 31);
+    if (have && !is_match) {
+      for (uint32_t i = 0; i < nl; ++i) {
+        const uint8_t v = static_cast<uint8_t>(t >> (8 * i));
+        dst[my_pos + i] = v;
+        ring[(my_pos + i) & (kRing - 1)] = v;
+      }
+    }
+    uint32_t mm = __ballot_sync(0xffffffffu, is_match);
+    while (mm) {
+      const int j = __ffs(mm) - 1;
+      mm &= mm - 1;
+      const uint32_t tj = __shfl_sync(0xffffffffu, t, j);
+      const int32_t p0 = __shfl_sync(0xffffffffu, my_pos, j);
+      const int length = static_cast<int>((tj >> 16) & 0x3FFu);
+      const int distance = static_cast<int>(tj & 0xFFFFu);
+      __syncwarp();  // literals and earlier matches are visible
+      // the ring holds position x until x + kRing is written; the chunk's literals are written
+      // up to chunk_end - 1 already, so a source is in the ring iff it is >= chunk_end - kRing
+      const bool from_ring = p0 - distance >= chunk_end - kRing;
+      if (length <= 32 && distance >= length) {
+        if (lane < length) {
+          const int src = p0 - distance + lane;
+          const uint8_t v = from_ring ? ring[src & (kRing - 1)] : dst[src];
+          dst[p0 + lane] = v;
+          ring[(p0 + lane) & (kRing - 1)] = v;
+        }
+      } else {
+        int jj = lane, step = 32;
+        if (distance < length) {
+          const float inv_d = __frcp_rn(static_cast<float>(distance));
+          jj = lane - distance * __float2int_rz(static_cast<float>(lane) * inv_d);
+          jj += jj < 0 ? distance : 0;
+          jj -= jj >= distance ? distance : 0;
+          step = 32 - distance * __float2int_rz(32.f * inv_d);
+          step += step < 0 ? distance : 0;
+          step -= step >= distance ? distance : 0;
+        }
+        for (int q = lane; q < length; q += 32) {
+          const int src = p0 - distance + jj;
+          const uint8_t v = from_ring ? ring[src & (kRing - 1)] : dst[src];
+          dst[p0 + q] = v;
+          ring[(p0 + q) & (kRing - 1)] = v;
+          if (distance < length) {
+            jj += step;
+            jj -= jj >= distance ? distance : 0;
+          } else {
+            jj += 32;
+          }
+        }
+      }
+    }
+    pos = chunk_end;
+    __syncwarp();
+  }
+  // Adler-32 (as the warp kernel above)
+  const uint32_t want = reinterpret_cast<const uint32_t*>(ntok + count)[stream];
+  unsigned long long s1 = 0, tt = 0;
+  int32_t head = static_cast<int32_t>((4u - (reinterpret_cast<uintptr_t>(dst) & 3u)) & 3u);
+  head = min(head, pos);
+  const int32_t n_words = (pos - head) >> 2;
+  const int32_t tail = head + 4 * n_words;
+  for (int32_t k = lane; k < head; k += 32) {
+    const uint32_t d = dst[k];
+    s1 += d;
+    tt += static_cast<unsigned long long>(k) * d;
+  }
+  for (int32_t k = tail + lane; k < pos; k += 32) {
+    const uint32_t d = dst[k];
+    s1 += d;
+    tt += static_cast<unsigned long long>(k) * d;
+  }
+  const uint32_t* words = reinterpret_cast<const uint32_t*>(dst + head);
+  uint32_t s1w = 0;
+  for (int32_t w = lane; w < n_words; w += 32) {
+    const uint32_t x = words[w];
+    const uint32_t sb = __dp4a(x, 0x01010101u, 0u);
+    s1w += sb;
+    tt += static_cast<unsigned long long>(head + 4 * w) * sb + __dp4a(x, 0x03020100u, 0u);
+  }
+  s1 += s1w;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    tt += __shfl_xor_sync(0xffffffffu, tt, o);
+  }
+  const unsigned long long s2 = static_cast<unsigned long long>(pos) * s1 - tt;
+  const uint32_t A = static_cast<uint32_t>((1 + s1) % 65521ull);
+  const uint32_t B = static_cast<uint32_t>((static_cast<unsigned long long>(pos) + s2) % 65521ull);
+  if (lane == 0 && (pos != out_len[stream] || ((B << 16) | A) != want)) status[stream] = 1;
+}
+
 }  // namespace
 
+int64_t inflate_token_stride(int64_t out_stride) { return (out_stride / 2 + 16 + 3) / 4 * 4; }
+
 int inflate_streams(const uint8_t* d_blob, const int64_t* d_off, const int64_t* d_len, int64_t count, int64_t skip,
-                    uint8_t* d_out, int64_t out_stride, int64_t* d_out_len, int* d_status, cudaStream_t s) {
+                    uint8_t* d_out, int64_t out_stride, int64_t* d_out_len, int* d_status, cudaStream_t s,
+                    uint32_t* d_tokens, int32_t* d_ntok) {
   if (count <= 0) return PG_OK;
-  // PG_INFLATE_LANES=16: two streams per warp (A/B switch; measured 10 % slower on C5: the
-  // half-warps diverge on literal / match often enough to lose the shared issue slots)
+  // PG_INFLATE_LANES=32 / 16: the warp-per-stream decoder (A/B switch); 16 = two streams per
+  // warp (measured 10 % slower than 32 on C5: the half-warps diverge on literal / match)
   static const int lanes = [] {
     const char* e = std::getenv("PG_INFLATE_LANES");
-    return e && std::atoi(e) == 16 ? 16 : 32;
+    return e ? std::atoi(e) : 0;
   }();
+  if (d_tokens != nullptr && d_ntok != nullptr && lanes == 0) {
+    const int64_t tok_stride = inflate_token_stride(out_stride);
+    constexpr int kSmem = static_cast<int>(sizeof(ThreadTables)) * kTokThreads;
+    PG_CUDA_CHECK(cudaFuncSetAttribute(inflate_tokens_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    inflate_tokens_kernel<<<static_cast<unsigned>((count + kTokThreads - 1) / kTokThreads), kTokThreads, kSmem, s>>>(
+        d_blob, d_off, d_len, count, skip, out_stride, d_tokens, tok_stride, d_ntok, d_out_len, d_status);
+    PG_CUDA_CHECK(cudaGetLastError());
+    inflate_expand_kernel<<<static_cast<unsigned>((count + 3) / 4), 128, 0, s>>>(d_tokens, tok_stride, d_ntok, count,
+                                                                                  d_out, out_stride, d_out_len,
+                                                                                  d_status);
+    PG_CUDA_CHECK(cudaGetLastError());
+    return PG_OK;
+  }
   const unsigned blocks = static_cast<unsigned>((count + 3) / 4);  // 4 streams per block
   if (lanes == 16) {
     inflate_kernel<16><<<blocks, 64, 0, s>>>(d_blob, d_off, d_len, count, skip, d_out, out_stride, d_out_len,
@@ -537,6 +1012,8 @@ extern "C" int pg_debug_inflate(const void* blob, int64_t blob_bytes, const int6
   uint8_t *d_blob = nullptr, *d_out = nullptr;
   int64_t *d_off = nullptr, *d_size = nullptr, *d_len = nullptr;
   int* d_status = nullptr;
+  uint32_t* d_tok = nullptr;
+  int32_t* d_ntok = nullptr;
   int rc = PG_OK;
   cudaError_t e;
   if ((e = cudaMalloc(&d_blob, blob_bytes + 16)) != cudaSuccess ||  // the decoder reads ahead <= 8 bytes
@@ -544,14 +1021,17 @@ extern "C" int pg_debug_inflate(const void* blob, int64_t blob_bytes, const int6
       (e = cudaMalloc(&d_off, sizeof(int64_t) * count)) != cudaSuccess ||
       (e = cudaMalloc(&d_size, sizeof(int64_t) * count)) != cudaSuccess ||
       (e = cudaMalloc(&d_len, sizeof(int64_t) * count)) != cudaSuccess ||
-      (e = cudaMalloc(&d_status, sizeof(int) * count)) != cudaSuccess) {
+      (e = cudaMalloc(&d_status, sizeof(int) * count)) != cudaSuccess ||
+      (e = cudaMalloc(&d_tok, sizeof(uint32_t) * inflate_token_stride(out_stride) * count)) != cudaSuccess ||
+      (e = cudaMalloc(&d_ntok, sizeof(int32_t) * 2 * count)) != cudaSuccess) {
     set_error("pg_debug_inflate: %s", cudaGetErrorString(e));
     rc = PG_ERR_CUDA;
   } else {
     cudaMemcpy(d_blob, blob, blob_bytes, cudaMemcpyHostToDevice);
     cudaMemcpy(d_off, off, sizeof(int64_t) * count, cudaMemcpyHostToDevice);
     cudaMemcpy(d_size, size, sizeof(int64_t) * count, cudaMemcpyHostToDevice);
-    rc = inflate_streams(d_blob, d_off, d_size, count, skip, d_out, out_stride, d_len, d_status, nullptr);
+    rc = inflate_streams(d_blob, d_off, d_size, count, skip, d_out, out_stride, d_len, d_status, nullptr, d_tok,
+                         d_ntok);
     if (rc == PG_OK) {
       if ((e = cudaDeviceSynchronize()) != cudaSuccess) {
         set_error("pg_debug_inflate: %s", cudaGetErrorString(e));
@@ -568,5 +1048,7 @@ extern "C" int pg_debug_inflate(const void* blob, int64_t blob_bytes, const int6
   cudaFree(d_size);
   cudaFree(d_len);
   cudaFree(d_status);
+  cudaFree(d_tok);
+  cudaFree(d_ntok);
   return rc;
 }
