@@ -87,5 +87,9 @@ constexpr int kTileCWide3 = 144;
 constexpr int kWideRows3 = 3;
 int launch_assoc_wide(const int8_t* qh, const int8_t* q1, const int8_t* q0, int64_t p_pad, const int8_t* v,
                       int64_t c_pad, int64_t k_pad, const AssocEpilogue& ep, cudaStream_t stream);
+// BGEN-8 transposed variant: v in the quartered layout (geno_planes(quartered)), c_pad a
+// multiple of 256 rows (80 markers per 256 rows); no K slicing, no max |r| tracking.
+int launch_assoc_wide3t(const int8_t* qh, const int8_t* q1, const int8_t* q0, int64_t p_pad, const int8_t* v,
+                        int64_t c_pad, int64_t k_pad, const AssocEpilogue& ep, cudaStream_t stream);
 
 }  // namespace pg

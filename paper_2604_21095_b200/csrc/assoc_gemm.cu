@@ -60,7 +60,15 @@ constexpr int kTileCW = kTileCWide;
 constexpr int kHalfCW = kTileCW / 2;
 constexpr int kVBytesW = kHalfCW * kTileK;  // 5 KB
 constexpr int kRowsW = 4;                   // digits 255^0, 255^1, 255^2 + missing row
-constexpr int kPlanes = 0, kFused = 1, kWide = 2, kWide3 = 3;
+constexpr int kPlanes = 0, kFused = 1, kWide = 2, kWide3 = 3, kWide3T = 4;
+// kWide3T (BGEN-8, transposed): genotype digit rows are the A operand (M = 256 rows per pair
+// tile = 80 markers in 32-row groups of 10 x 3 rows, see geno_planes(quartered)), the three
+// panel limbs three B tiles of N = 144 phenotypes: operand bytes per MAC are 24 % lower than
+// kWide3's (three 128-row limb tiles streamed past a 72-row genotype tile).
+constexpr int kTPheno = 144;                 // phenotypes per transposed pair tile (UMMA N)
+constexpr int kTHalfPheno = kTPheno / 2;     // 72 per CTA
+constexpr int kTLimbBytes = kTHalfPheno * kTileK;  // 4.5 KB per limb half-tile
+constexpr int kTMarkers = 80;                // markers per transposed pair tile
 constexpr int kEpiWarps = 16;
 constexpr int kFirstEpiWarp = 8;
 constexpr int kThreads = 32 * (kFirstEpiWarp + kEpiWarps);
@@ -75,18 +83,24 @@ constexpr int kTmemCols = 512;
 template <int MODE>
 struct Cfg {
   static constexpr bool FUSED = MODE == kFused;
-  static constexpr bool WIDE = MODE == kWide || MODE == kWide3;
-  static constexpr int kStages = WIDE ? 7 : 5;
+  static constexpr bool TRANS = MODE == kWide3T;
+  static constexpr bool WIDE = MODE == kWide || MODE == kWide3 || TRANS;
+  static constexpr int kStages = TRANS ? 9 : (WIDE ? 7 : 5);
   // genotype rows per pair tile; wide modes: rows per marker
-  static constexpr int kTileRows = MODE == kWide3 ? kTileCWide3 : (WIDE ? kTileCW : kTileC);
+  static constexpr int kTileRows = TRANS ? kTileC : (MODE == kWide3 ? kTileCWide3 : (WIDE ? kTileCW : kTileC));
   static constexpr int kHalfRows = kTileRows / 2;
-  static constexpr int kWideR = MODE == kWide3 ? kWideRows3 : kRowsW;
+  static constexpr int kWideR = (MODE == kWide3 || TRANS) ? kWideRows3 : kRowsW;
   static constexpr int kVBytesWide = kHalfRows * kTileK;
-  // 1 KB-aligned stages
+  // accumulator width (UMMA N): genotype rows, or phenotypes in the transposed mode
+  static constexpr int kAccCols = TRANS ? kTPheno : kTileRows;
+  // 1 KB-aligned stages (transposed: genotype A half-tile, then the three limb B half-tiles)
   static constexpr int kStageBytes =
-      WIDE ? kOffV + (kVBytesWide + 1023) / 1024 * 1024 : (FUSED ? kOffPacked + 2048 : kOffPacked);
+      TRANS ? (kVBytesWide + 3 * kTLimbBytes + 1023) / 1024 * 1024
+            : (WIDE ? kOffV + (kVBytesWide + 1023) / 1024 * 1024 : (FUSED ? kOffPacked + 2048 : kOffPacked));
   static constexpr int kPanelBytes = 3 * kQBytes;
-  static constexpr int kTmaBytes = FUSED ? kPanelBytes : (WIDE ? kOffV + kVBytesWide : kOffPacked);  // per CTA
+  static constexpr int kTmaBytes =
+      TRANS ? kVBytesWide + 3 * kTLimbBytes
+            : (FUSED ? kPanelBytes : (WIDE ? kOffV + kVBytesWide : kOffPacked));  // per CTA
   static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 512 /*barriers*/;
   static_assert(kStageBytes % 1024 == 0 && kOffV % 512 == 0, "stage / operand alignment (SW64 atoms)");
   static_assert(kTileRows % 16 == 0 && kHalfRows % 8 == 0, "UMMA N and swizzle-atom granularity");
@@ -156,19 +170,21 @@ struct MaxAbsR {
 };
 
 // shared tail of the epilogues: fp32 premask, fp64 r for candidates / FULL, compaction
+// valid = false (transposed tiles: padding rows / phenotypes past the panel): no result, but
+// the lane still takes part in the warp's compaction ballot.
 __device__ __forceinline__ void epilogue_value(const AssocEpilogue& ep, long long xu, long long xm, int m, int pheno,
                                                float sc_f, double sc_d, float cq_f, long long cq, float rb, int lane,
-                                               uint32_t lanemask_lt, MaxAbsR& mx) {
+                                               uint32_t lanemask_lt, MaxAbsR& mx, bool valid = true) {
   const float mu = __ldg(ep.mu_f + m);
   const float iv = ep.raw ? 1.f : __ldg(ep.invd_f + m);  // NaN for skipped / padding markers
   const float xf = static_cast<float>(xu) - mu * (cq_f - static_cast<float>(xm));
   const float r = xf * sc_f * iv;
   const float ar = fabsf(r);
-  const bool hit = ar >= rb;
+  const bool hit = valid && ar >= rb;
   // same widening as the premask bar (ctx.cu rbar_kernel), doubled
-  const bool near_max = ep.max_abs_r != nullptr && ar >= mx.f * (1.f - 2e-5f) - 2e-7f;
+  const bool near_max = valid && ep.max_abs_r != nullptr && ar >= mx.f * (1.f - 2e-5f) - 2e-7f;
   double r64 = 0.0;
-  if (hit || ep.full_r || near_max) {
+  if (hit || (valid && ep.full_r) || near_max) {
     r64 = sc_d * (static_cast<double>(xu) - __ldg(ep.mu_d + m) * static_cast<double>(cq - xm)) *
           (ep.raw ? 1.0 : __ldg(ep.invd_d + m));
   }
@@ -176,7 +192,7 @@ __device__ __forceinline__ void epilogue_value(const AssocEpilogue& ep, long lon
     mx.f = fmaxf(mx.f, ar);
     mx.d = fmax(mx.d, fabs(r64));  // NaN (skipped / padding markers) is ignored by fmax
   }
-  if (ep.full_r) ep.full_r[static_cast<int64_t>(m) * ep.full_ld + pheno] = r64;
+  if (valid && ep.full_r) ep.full_r[static_cast<int64_t>(m) * ep.full_ld + pheno] = r64;
   const uint32_t mask = __ballot_sync(0xffffffffu, hit);
   if (mask) {
     unsigned long long base = 0;
@@ -275,6 +291,63 @@ __device__ __forceinline__ void epilogue_tile_wide3(const AssocEpilogue& ep, uin
   }
   if (ep.max_abs_r && !ep.x_accum && pheno < ep.p_valid)
     atomicMax(ep.max_abs_r + pheno, static_cast<unsigned long long>(__double_as_longlong(mx.d)));
+}
+
+__device__ __forceinline__ long long shfl64(long long v, int src) {
+  const int lo = __shfl_sync(0xffffffffu, static_cast<int>(v & 0xffffffffll), src);
+  const int hi = __shfl_sync(0xffffffffu, static_cast<int>(v >> 32), src);
+  return (static_cast<long long>(hi) << 32) | static_cast<unsigned int>(lo);
+}
+
+// Transposed BGEN-8 tile: TMEM lanes are genotype rows (lane 3j + d = digit d of marker j of
+// this quarter; d = 2 the missing row; lanes 30-31 padding), columns phenotypes. Per
+// 3-column step, three rotating shuffles hand lane 3j + t the three rows of marker j at
+// column c + t, so all 30 lanes evaluate a different (marker, phenotype) pair.
+__device__ __forceinline__ void epilogue_tile_wide3t(const AssocEpilogue& ep, uint32_t tA, int ct, int cr, int pt,
+                                                     int quarter, int lane, int c_begin, int c_end) {
+  const uint32_t lanemask_lt = (1u << lane) - 1u;
+  const int s = lane % 3;
+  const int grp = lane - s;
+  const int m = ct * kTMarkers + cr * (kTMarkers / 2) + quarter * 10 + lane / 3;
+  const bool row_ok = lane < 30 && m < ep.m_valid;
+  const int m_safe = row_ok ? m : 0;
+  MaxAbsR mx;
+#pragma unroll 1
+  for (int c = c_begin; c < c_end; c += 12) {
+    uint32_t a[12], b[12], d[12];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      tmem_ld_32x32b_x4(tA + c + 4 * q, a + 4 * q);
+      tmem_ld_32x32b_x4(tA + kTPheno + c + 4 * q, b + 4 * q);
+      tmem_ld_32x32b_x4(tA + 2 * kTPheno + c + 4 * q, d + 4 * q);
+    }
+    tmem_ld_wait();
+#pragma unroll
+    for (int c3 = 0; c3 < 12; c3 += 3) {
+      long long x[3], row[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+        x[i] = kWH * static_cast<long long>(static_cast<int>(a[c3 + i])) + 127ll * static_cast<int>(b[c3 + i]) +
+               static_cast<int>(d[c3 + i]);
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        const int idx = (s + 3 - r) % 3;  // the column the lane that needs my row receives
+        const long long send = idx == 0 ? x[0] : (idx == 1 ? x[1] : x[2]);
+        const int from = (s + r) % 3;
+        const long long got = shfl64(send, grp + from);
+        if (from == 0) row[0] = got;
+        else if (from == 1) row[1] = got;
+        else row[2] = got;
+      }
+      const int pheno = pt * kTPheno + c + c3 + s;
+      const bool valid = row_ok && pheno < ep.p_valid;
+      const int p_safe = valid ? pheno : 0;
+      const long long xu = row[0] + 255ll * row[1];
+      epilogue_value(ep, xu, row[2], m_safe, p_safe, __ldg(ep.scale_f + p_safe), __ldg(ep.scale_d + p_safe),
+                     __ldg(ep.cq_f + p_safe), __ldg(ep.cq + p_safe), ep.rbar ? __ldg(ep.rbar + p_safe) : INFINITY,
+                     lane, lanemask_lt, mx, valid);
+    }
+  }
 }
 
 template <int R>
@@ -393,7 +466,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int t = cid; t < n_tiles; t += n_clusters) {
         int ct, pt;
         tile_coords(t, n_ctile, n_ptile, group_c, ct, pt);
-        const int prow = pt * kTileP + cr * kHalfP;
+        const int prow = C::TRANS ? pt * kTPheno + cr * kTHalfPheno : pt * kTileP + cr * kHalfP;
         const int grow = ct * C::kTileRows + cr * C::kHalfRows;
         for (int kb = 0; kb < n_kb; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
@@ -401,6 +474,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const int kx = (kb_begin + kb) * kTileK;
           const uint32_t full0 = map_to_cta(&full[s], 0);
           mbar_arrive_expect_tx_cluster(full0, C::kTmaBytes);
+          if constexpr (C::TRANS) {
+            tma_load_2d_pair(st, &tm_v, full0, kx, grow, pol_geno);
+            tma_load_2d_pair(st + C::kVBytesWide, &tm_qh, full0, kx, prow, pol_panel);
+            tma_load_2d_pair(st + C::kVBytesWide + kTLimbBytes, &tm_q1, full0, kx, prow, pol_panel);
+            tma_load_2d_pair(st + C::kVBytesWide + 2 * kTLimbBytes, &tm_q0, full0, kx, prow, pol_panel);
+            if (++s == S) {
+              s = 0;
+              ph ^= 1;
+            }
+            continue;
+          }
           tma_load_2d_pair(st, &tm_qh, full0, kx, prow, pol_panel);
           tma_load_2d_pair(st + kQBytes, &tm_q1, full0, kx, prow, pol_panel);
           tma_load_2d_pair(st + 2 * kQBytes, &tm_q0, full0, kx, prow, pol_panel);
@@ -423,10 +507,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     if (leader && lane == 0) {
       // ------------------------------------------------------------ MMA issuer (leader CTA)
-      constexpr uint32_t idesc = idesc_s8_s32(kTileP, C::kTileRows);  // M = 256 across the pair
+      constexpr uint32_t idesc = idesc_s8_s32(kTileP, C::kAccCols);  // M = 256 across the pair
       const uint32_t dH = tmem_base;
-      const uint32_t dL = tmem_base + C::kTileRows;
-      const uint32_t dC = tmem_base + 2 * C::kTileRows;  // wide mode only
+      const uint32_t dL = tmem_base + C::kAccCols;
+      const uint32_t dC = tmem_base + 2 * C::kAccCols;  // wide modes only
       uint32_t s = 0, ph = 0, aph = 0;
       for (int t = cid; t < n_tiles; t += n_clusters) {
         mbar_wait_cluster(tempty, aph ^ 1);
@@ -437,6 +521,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if constexpr (FUSED) mbar_wait_cluster(&dec[s], ph);
           tc_fence_after();
           const uint32_t st = smem_u32(smem + s * C::kStageBytes);
+          if constexpr (C::TRANS) {
+            // A = genotype digit rows, B = limb j -> accumulator j
+            const uint64_t d_g = umma_desc_sw64(st);
+            const uint64_t d_h = umma_desc_sw64(st + C::kVBytesWide);
+            const uint64_t d_1 = umma_desc_sw64(st + C::kVBytesWide + kTLimbBytes);
+            const uint64_t d_0 = umma_desc_sw64(st + C::kVBytesWide + 2 * kTLimbBytes);
+#pragma unroll
+            for (int k = 0; k < kTileK / 32; ++k) {
+              mma_i8_ss_pair(dH, d_g + 2 * k, d_h + 2 * k, idesc, acc);
+              mma_i8_ss_pair(dL, d_g + 2 * k, d_1 + 2 * k, idesc, acc);
+              mma_i8_ss_pair(dC, d_g + 2 * k, d_0 + 2 * k, idesc, acc);
+              acc = 1;
+            }
+            mma_commit_pair_multicast(&empty[s], 0x3);
+            if (++s == S) {
+              s = 0;
+              ph ^= 1;
+            }
+            continue;
+          }
           const uint64_t d_qh = umma_desc_sw64(st);
           const uint64_t d_q1 = umma_desc_sw64(st + kQBytes);
           const uint64_t d_q0 = umma_desc_sw64(st + 2 * kQBytes);
@@ -515,13 +619,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_wait_cluster(tfull, aph);
       tc_fence_after();
       const uint32_t tH = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16);
-      const uint32_t tL = tH + C::kTileRows;
+      const uint32_t tL = tH + C::kAccCols;
       // split the tile's 16-column chunks over the 4 column groups (12-column = 4-marker
-      // units in the 3-row mode)
-      constexpr int kUnit = MODE == kWide3 ? 12 : 16;
-      constexpr int kChunks = C::kTileRows / kUnit;
+      // units in the 3-row mode, 12-column = 4 phenotype triples in the transposed mode)
+      constexpr int kUnit = (MODE == kWide3 || C::TRANS) ? 12 : 16;
+      constexpr int kChunks = C::kAccCols / kUnit;
       const int c0 = kUnit * ((cg * kChunks) / 4), c1 = kUnit * (((cg + 1) * kChunks) / 4);
-      if constexpr (MODE == kWide3) {
+      if constexpr (C::TRANS) {
+        epilogue_tile_wide3t(ep, tH, ct, static_cast<int>(cr), pt, quarter, lane, c0, c1);
+      } else if constexpr (MODE == kWide3) {
         epilogue_tile_wide3(ep, tH, ct, pheno, lane, c0, c1);
       } else if constexpr (WIDE) {
         epilogue_tile_wide(ep, tH, ct, pheno, lane, c0, c1);
@@ -587,7 +693,7 @@ int launch_common(const CUtensorMap& tm_qh, const CUtensorMap& tm_q1, const CUte
   PG_CUDA_CHECK(cudaGetDevice(&dev));
   PG_CUDA_CHECK(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
   const int n_ctile = static_cast<int>(c_pad / Cfg<MODE>::kTileRows);
-  const int n_ptile = static_cast<int>(p_pad / kTileP);
+  const int n_ptile = static_cast<int>(Cfg<MODE>::TRANS ? (p_pad + kTPheno - 1) / kTPheno : p_pad / kTileP);
   const int n_tiles = n_ctile * n_ptile;
   const int max_pairs = n_sm / 2;
   const int pairs = n_tiles < max_pairs ? n_tiles : max_pairs;
@@ -611,6 +717,7 @@ int launch_common(const CUtensorMap& tm_qh, const CUtensorMap& tm_q1, const CUte
     assoc_i8_kernel<MODE><<<grid, kThreads, Cfg<MODE>::kSmemBytes, stream>>>(
         tm_qh, tm_q1, tm_q0, tm_v, tm_v127, n_ctile, n_ptile, 0, n_kb, group_c, l2_codes, ep);
   } else {
+    PG_REQUIRE(!Cfg<MODE>::TRANS, PG_ERR_INVALID, "assoc(wide3t): K-sliced runs use the untransposed kernel");
     // more samples than one int32-exact slice: accumulate int64 partials slice by slice,
     // then derive the statistics (same epilogue arithmetic) from the exact sums
     PG_REQUIRE(ep.x_accum != nullptr && ep.x_ld == p_pad, PG_ERR_INVALID, "assoc: K-sliced run needs x_accum");
@@ -670,6 +777,22 @@ int launch_assoc_packed(const int8_t* qh, const int8_t* q1, const int8_t* q0, in
   PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_pk, packed, k_pad / 4, n_markers, pitch, kTileK / 4, kHalfC, false));
   const int64_t c_pad = round_up(n_markers, kTileC);
   return launch_common<kFused>(tm_qh, tm_q1, tm_q0, tm_pk, tm_pk, p_pad, c_pad, k_pad, ep, stream);
+}
+
+int launch_assoc_wide3t(const int8_t* qh, const int8_t* q1, const int8_t* q0, int64_t p_pad, const int8_t* v,
+                        int64_t c_pad, int64_t k_pad, const AssocEpilogue& ep, cudaStream_t stream) {
+  PG_REQUIRE(ep.rows_per_marker == kWideRows3 && ep.max_abs_r == nullptr && ep.x_accum == nullptr &&
+                 p_pad % kTileP == 0 && c_pad % kTileC == 0 && k_pad % kTileK == 0 && p_pad > 0 && c_pad > 0 &&
+                 k_pad > 0 && k_pad <= kSliceK,
+             PG_ERR_INVALID, "assoc(wide3t): bad arguments p=%lld c=%lld k=%lld", (long long)p_pad, (long long)c_pad,
+             (long long)k_pad);
+  CUtensorMap tm_qh, tm_q1, tm_q0, tm_v;
+  const uint64_t pitch = static_cast<uint64_t>(k_pad);
+  PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_qh, qh, k_pad, p_pad, pitch, kTileK, kTHalfPheno));
+  PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_q1, q1, k_pad, p_pad, pitch, kTileK, kTHalfPheno));
+  PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_q0, q0, k_pad, p_pad, pitch, kTileK, kTHalfPheno));
+  PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_v, v, k_pad, c_pad, k_pad, kTileK, kTileC / 2));
+  return launch_common<kWide3T>(tm_qh, tm_q1, tm_q0, tm_v, tm_v, p_pad, c_pad, k_pad, ep, stream);
 }
 
 int launch_assoc_wide(const int8_t* qh, const int8_t* q1, const int8_t* q0, int64_t p_pad, const int8_t* v,

@@ -243,6 +243,7 @@ struct pg_ctx {
   unsigned long long cand_base = 0;  // test hook: initial candidate-counter value (pg_ctx_debug_candidate_base)
   bool fused_decode = true;
   bool wide_digits = true;
+  bool wide3t = true;  // BGEN-8: transposed wide GEMM (PG_WIDE3T=0: the kWide3 kernel, A/B)
 
   // extension mode: quantized covariate basis (columns 1..rank-1) + side-GEMM output
   bool have_basis = false;
@@ -421,8 +422,12 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
                                      c->miss_count.p, s));
     PG_CUDA_CHECK(cudaMemcpyAsync(&n_side, c->miss_count.p, sizeof(int), cudaMemcpyDeviceToHost, s));
   }
-  PG_CUDA_CHECK(cudaMemcpyAsync(hflags, c->flags.p, sizeof(int) * 2, cudaMemcpyDeviceToHost, s));
-  PG_CUDA_CHECK(cudaStreamSynchronize(s));
+  // the row layout depends on the batch's missing calls only for PLINK / integral dense rows;
+  // wide-digit batches (BGEN, real dense) go on to the GEMM without a host round trip
+  if (!(c->wide_digits && geno_wide(b)) || side_ok) {
+    PG_CUDA_CHECK(cudaMemcpyAsync(hflags, c->flags.p, sizeof(int) * 2, cudaMemcpyDeviceToHost, s));
+    PG_CUDA_CHECK(cudaStreamSynchronize(s));
+  }
   // dosage sources use the wide-digit GEMM (3 rows per BGEN-8 marker, 4 otherwise) unless
   // disabled for A/B tests
   int R = geno_rows_per_marker(b, hflags[0] != 0, c->wide_digits);
@@ -430,19 +435,24 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
   const bool use_side = side_ok && R == 2 && side_rows * c->p_pad * 8 <= kSideBytesMax;
   if (use_side) R = 1;
   const bool wide = R == kWideRows || R == kWideRows3;
-  const int64_t c_pad = round_up(m * R, wide ? (R == kWideRows3 ? kTileCWide3 : kTileCWide) : kTileC);
+  // BGEN-8: the transposed wide GEMM (genotype rows as A) unless the run needs K slices,
+  // the extension-mode side GEMM or the per-phenotype max |r| (kept on the kWide3 kernel)
+  const bool wide3t = R == kWideRows3 && c->wide3t && c->k_pad <= kSliceK && !c->have_basis && !c->track_max_abs_r;
+  const int64_t c_pad = wide3t ? round_up((m + 9) / 10 * 32, kTileC)
+                               : round_up(m * R, wide ? (R == kWideRows3 ? kTileCWide3 : kTileCWide) : kTileC);
   // PLINK rows without missing calls: the GEMM decodes the packed codes itself
   const bool fused = c->fused_decode && kind == PG_GENO_BED && R == 1;
   int64_t launches = (kind == PG_GENO_DENSE_F64 ? 2 : 1);
   if (!fused) {
     PG_CHECK_STATUS(c->v.ensure(static_cast<size_t>(c_pad) * c->k_pad));
     if (!wide) PG_CHECK_STATUS(c->v127.ensure(static_cast<size_t>(c_pad) * c->k_pad));
-    PG_CHECK_STATUS(geno_planes(b, R, c->v.p, wide ? nullptr : c->v127.p, c_pad, c->k_pad, s));
+    PG_CHECK_STATUS(geno_planes(b, R, c->v.p, wide ? nullptr : c->v127.p, c_pad, c->k_pad, s, wide3t));
     ++launches;
   }
   auto run_gemm_on = [&](const AssocEpilogue& e, const int8_t* a, const int8_t* b1, const int8_t* b0,
                          int64_t pp) -> int {
     if (fused) return launch_assoc_packed(a, b1, b0, pp, d_data, pitch, m, c->k_pad, e, s);
+    if (wide3t) return launch_assoc_wide3t(a, b1, b0, pp, c->v.p, c_pad, c->k_pad, e, s);
     if (wide) return launch_assoc_wide(a, b1, b0, pp, c->v.p, c_pad, c->k_pad, e, s);
     return launch_assoc(a, b1, b0, pp, c->v.p, c->v127.p, c_pad, c->k_pad, e, s);
   };
@@ -672,6 +682,7 @@ int pg_ctx_create(int device, pg_ctx** out) {
   PG_CUDA_CHECK(cudaSetDevice(device));
   pg_ctx* c = new pg_ctx();
   c->device = device;
+  if (const char* e = std::getenv("PG_WIDE3T")) c->wide3t = std::atoi(e) != 0;
   PG_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   PG_CUDA_CHECK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
   for (auto& e : c->ev) PG_CUDA_CHECK(cudaEventCreate(&e));

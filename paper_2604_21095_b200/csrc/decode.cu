@@ -349,7 +349,9 @@ __device__ __forceinline__ uint4 pack16(const int (&x)[kChunk], int mul) {
 }
 
 // grid.x = marker slot (incl. padding), grid.y * blockDim = 16-sample chunks of k_pad.
-template <int KIND, int R>
+// QUART (R = 3 only): the transposed wide GEMM's layout, 10 markers per 32-row group
+// (rows 3j..3j+2 of marker j, rows 30-31 zero) so a marker's rows share one TMEM lane quarter.
+template <int KIND, int R, bool QUART = false>
 __global__ void planes_kernel(GenoBlock b, int8_t* __restrict__ v, int8_t* __restrict__ v127, int64_t k_pad) {
   const int64_t m = blockIdx.x;
   const int64_t ci = static_cast<int64_t>(blockIdx.y) * blockDim.x + threadIdx.x;
@@ -364,7 +366,7 @@ __global__ void planes_kernel(GenoBlock b, int8_t* __restrict__ v, int8_t* __res
 #pragma unroll
     for (int i = 0; i < kChunk; ++i) u[i] = 0;
   }
-  const int64_t base = m * R;
+  const int64_t base = QUART ? (m / 10) * 32 + 3 * (m % 10) : m * R;
   auto put = [&](int64_t row, const int (&x)[kChunk]) {
     uint4* pv = reinterpret_cast<uint4*>(v + row * k_pad + ci * kChunk);
     *pv = pack16(x, 1);
@@ -393,6 +395,12 @@ __global__ void planes_kernel(GenoBlock b, int8_t* __restrict__ v, int8_t* __res
 #pragma unroll
     for (int i = 0; i < kChunk; ++i) t[i] = (miss >> i) & 1u;
     put(base + R - 1, t);
+    if (QUART && m % 10 == 9) {  // the group's two padding rows
+#pragma unroll
+      for (int i = 0; i < kChunk; ++i) t[i] = 0;
+      put(base + 3, t);
+      put(base + 4, t);
+    }
   } else if constexpr (R == 1) {
     put(base, u);
   } else if constexpr (R == 2) {
@@ -554,6 +562,17 @@ int planes_launch(const GenoBlock& b, int8_t* v, int8_t* v127, int64_t c_pad, in
 }
 
 template <int KIND>
+int planes_quart_launch(const GenoBlock& b, int8_t* v, int64_t c_pad, int64_t k_pad, cudaStream_t s) {
+  const int64_t m_slots = c_pad / 32 * 10;
+  const int64_t chunks = k_pad / kChunk;
+  const int threads = 128;
+  dim3 grid(static_cast<unsigned>(m_slots), static_cast<unsigned>((chunks + threads - 1) / threads));
+  planes_kernel<KIND, 3, true><<<grid, threads, 0, s>>>(b, v, nullptr, k_pad);
+  PG_CUDA_CHECK(cudaGetLastError());
+  return PG_OK;
+}
+
+template <int KIND>
 int planes_dispatch(const GenoBlock& b, int R, int8_t* v, int8_t* v127, int64_t c_pad, int64_t k_pad,
                     cudaStream_t s) {
   switch (R) {
@@ -614,7 +633,17 @@ int geno_stats(const GenoBlock& b, MarkerStats& st, int64_t m_pad, cudaStream_t 
   }
 }
 
-int geno_planes(const GenoBlock& b, int R, int8_t* v, int8_t* v127, int64_t c_pad, int64_t k_pad, cudaStream_t s) {
+int geno_planes(const GenoBlock& b, int R, int8_t* v, int8_t* v127, int64_t c_pad, int64_t k_pad, cudaStream_t s,
+                bool quartered) {
+  if (quartered) {
+    PG_REQUIRE(R == 3 && k_pad % 64 == 0 && c_pad % 32 == 0, PG_ERR_INVALID, "geno_planes: bad quartered layout");
+    switch (b.kind) {
+      case PG_GENO_BGEN8: return planes_quart_launch<PG_GENO_BGEN8>(b, v, c_pad, k_pad, s);
+      case PG_GENO_BGEN16: return planes_quart_launch<PG_GENO_BGEN16>(b, v, c_pad, k_pad, s);
+      case PG_GENO_DENSE_F64: return planes_quart_launch<PG_GENO_DENSE_F64>(b, v, c_pad, k_pad, s);
+      default: set_error("quartered planes: unsupported kind %d", b.kind); return PG_ERR_INVALID;
+    }
+  }
   PG_REQUIRE(k_pad % 64 == 0 && c_pad % R == 0, PG_ERR_INVALID, "geno_planes: bad padding");
   switch (b.kind) {
     case PG_GENO_BED: return planes_dispatch<PG_GENO_BED>(b, R, v, v127, c_pad, k_pad, s);

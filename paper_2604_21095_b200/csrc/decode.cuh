@@ -56,8 +56,10 @@ int geno_check_integral(const GenoBlock& b, MarkerStats& st, cudaStream_t s);
 int geno_stats(const GenoBlock& b, MarkerStats& st, int64_t m_pad, cudaStream_t s);
 // Pass 3: GEMM operand planes [c_pad, k_pad] with R rows per marker: ternary digits v / 127v
 // (R = 1, 2, 8, 16), or for R = 4 (wide mode, geno_wide) base-255 digits in v only.
+// quartered (R = 3): rows of marker m at (m / 10) * 32 + 3 (m % 10) + d, rows 30-31 of every
+// 32-row group zero (the transposed wide GEMM, launch_assoc_wide3t).
 int geno_planes(const GenoBlock& b, int rows_per_marker, int8_t* v, int8_t* v127, int64_t c_pad, int64_t k_pad,
-                cudaStream_t s);
+                cudaStream_t s, bool quartered = false);
 // Missing-call side path of the fused PLINK GEMM (markers with missing calls carry a mask
 // row in a separate GEMM; the rest of the batch keeps one row per marker):
 // flag[m] = scanned marker m has a kept missing call; after an exclusive prefix sum of the

@@ -160,3 +160,31 @@ def test_bgen8_in_place_blocks_equal_host_inflate_with_sample_subset(tmp_path, m
     assert (tmp_path / "gpu.bin").read_bytes() == (tmp_path / "host.bin").read_bytes()
     t, markers, names = pg.read_full_matrix(tmp_path / "gpu.bin")
     assert t.shape == (m, 4) and np.isfinite(t).all()
+
+
+@pytest.mark.parametrize("m,k,mode", [(7, 5, "full"), (95, 150, "full"), (161, 290, "thr"), (401, 33, "thr")])
+def test_wide3t_equals_wide3_bitwise(m, k, mode, tmp_path, monkeypatch):
+    """BGEN-8 through the transposed wide GEMM (genotype rows as A, 80 markers and 144
+    phenotypes per pair tile, shuffled 3-row recombination) == the kWide3 kernel bit for bit,
+    for marker / phenotype counts that leave partial tiles and groups of 10."""
+    from bgen_fixture import write_bgen
+
+    rng = np.random.default_rng(m + k)
+    n = 211
+    ids = [f"S{i + 1}" for i in range(n)]
+    d = rng.uniform(0, 2, (m, n))
+    hard = rng.random(d.shape) < 0.6
+    d[hard] = np.round(d[hard])
+    d[rng.random(d.shape) < 0.05] = np.nan
+    y = rng.standard_normal((n, k))
+    pheno = write_tsv(tmp_path / "p.tsv", ids, [f"ph{j}" for j in range(k)], y)
+    spec = pg.SourceSpec(pg.GenotypeFormat.BGEN, bgen_path=write_bgen(tmp_path / "g.bgen", d, ids, bits=8))
+    kw = dict(source=spec, pheno_path=pheno, precision=pg.Precision.F64, summary_to_stderr=False, device_batch=256)
+    kw.update(output_mode=pg.OutputMode.FULL) if mode == "full" else kw.update(p_threshold=0.05)
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("PG_WIDE3T", flag)
+        path = tmp_path / f"o{flag}.{'bin' if mode == 'full' else 'tsv'}"
+        pg.run_scan(pg.ScanConfig(out_path=path, **kw))
+        out[flag] = path.read_bytes()
+    assert out["1"] == out["0"]
