@@ -528,8 +528,14 @@ struct ThreadTables {
   uint16_t dist[1 << kTokDistBits];
 };
 
-struct Canon {  // canonical (count, symbol) arrays for codes longer than the first level
-  uint16_t count[16];
+// Codes longer than the first level: canonical decode by left-justified limits. With
+// rev = the next 15 input bits in code order (first bit read = MSB), the code length is the
+// smallest L with rev < lim[L] (lim[L] = (first[L] + count[L]) << (15 - L), non-decreasing),
+// found by independent compares instead of a bit-serial loop (32 streams share a warp here,
+// so a slow path taken by one lane is paid by all).
+struct Canon {
+  uint16_t lim[16];
+  int16_t base[16];  // index of the first length-L code in sym[] minus first[L]
   uint16_t sym[288];
 };
 
@@ -555,8 +561,9 @@ __device__ bool build1(uint16_t* lut, Canon& cn, const uint8_t* lens, int n, boo
     code = (code + count[l - 1]) << 1;
     next[l] = static_cast<uint16_t>(code);
     offs[l] = static_cast<uint16_t>(off);
+    cn.lim[l] = static_cast<uint16_t>((code + count[l]) << (15 - l));
+    cn.base[l] = static_cast<int16_t>(off - code);
     off += count[l];
-    cn.count[l] = count[l];
   }
   for (int i = 0; i < (1 << BITS); ++i) lut[i] = 0;
   for (int s = 0; s < n; ++s) {
@@ -572,21 +579,15 @@ __device__ bool build1(uint16_t* lut, Canon& cn, const uint8_t* lens, int n, boo
   return true;
 }
 
+template <int BITS>
 __device__ __forceinline__ int decode_canon(Bits& br, const Canon& cn) {
-  const uint32_t bits = static_cast<uint32_t>(br.buf);
-  int code = 0, first = 0, index = 0;
-  for (int l = 1; l < 16; ++l) {
-    code |= static_cast<int>((bits >> (l - 1)) & 1u);
-    const int c = cn.count[l];
-    if (code - c < first) {
-      br.get(l);
-      return cn.sym[index + (code - first)];
-    }
-    index += c;
-    first = (first + c) << 1;
-    code <<= 1;
-  }
-  return -1;
+  const uint32_t rev = __brev(static_cast<uint32_t>(br.buf)) >> 17;  // 15 bits, first read = MSB
+  int l = BITS + 1;
+#pragma unroll
+  for (int k = BITS + 1; k < 15; ++k) l += rev >= cn.lim[k] ? 1 : 0;
+  if (rev >= cn.lim[l]) return -1;  // past every code (incomplete single-code tables)
+  br.get(l);
+  return cn.sym[cn.base[l] + static_cast<int>(rev >> (15 - l))];
 }
 
 template <class Enc, int BITS>
@@ -596,21 +597,25 @@ __device__ __forceinline__ uint32_t decode1(Bits& br, const uint16_t* lut, const
     br.get(e & 15u);
     return e;
   }
-  const int sym = decode_canon(br, cn);
+  const int sym = decode_canon<BITS>(br, cn);
   return sym < 0 ? Enc::kInvalid : Enc::enc(sym, 1);
 }
 
-struct TokenSink {  // 4 tokens per 16-byte store
+struct TokenSink {  // 4 tokens per 16-byte store, queued in registers
   uint32_t* dst;
   int32_t n = 0, cap;
-  uint32_t q[4];
+  uint32_t q0 = 0, q1 = 0, q2 = 0;
   uint32_t lit = 0;
   int nlit = 0;
   __device__ __forceinline__ bool put(uint32_t t) {
     if (n >= cap) return false;
-    q[n & 3] = t;
+    switch (n & 3) {
+      case 0: q0 = t; break;
+      case 1: q1 = t; break;
+      case 2: q2 = t; break;
+      default: *reinterpret_cast<uint4*>(dst + n - 3) = make_uint4(q0, q1, q2, t);
+    }
     ++n;
-    if ((n & 3) == 0) *reinterpret_cast<uint4*>(dst + n - 4) = make_uint4(q[0], q[1], q[2], q[3]);
     return true;
   }
   __device__ __forceinline__ bool literal(uint32_t b) {
@@ -626,7 +631,10 @@ struct TokenSink {  // 4 tokens per 16-byte store
     return ok;
   }
   __device__ __forceinline__ void finish() {
-    for (int i = n & ~3; i < n; ++i) dst[i] = q[i & 3];
+    const int r = n & 3, b0 = n - r;
+    if (r > 0) dst[b0] = q0;
+    if (r > 1) dst[b0 + 1] = q1;
+    if (r > 2) dst[b0 + 2] = q2;
   }
 };
 
@@ -863,6 +871,7 @@ __global__ void __launch_bounds__(128) inflate_expand_kernel(const uint32_t* __r
     const uint32_t nl = t >> 30;
     const bool is_match = have && nl == 0;
     const int32_t tlen = !have ? 0 : (is_match ? static_cast<int32_t>((t >> 16) & 0x3FFu) : static_cast<int32_t>(nl));
+    const int32_t distance = is_match ? static_cast<int32_t>(t & 0xFFFFu) : 0;
     int32_t incl = tlen;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -871,55 +880,75 @@ __global__ void __launch_bounds__(128) inflate_expand_kernel(const uint32_t* __r
     }
     const int32_t my_pos = pos + incl - tlen;
     const int32_t chunk_end = pos + __shfl_sync(0xffffffffu, incl, 31);
+    const int32_t ring_lo = chunk_end - kRing;  // the ring holds positions >= ring_lo (and older ones < pos)
+    // round 0: literal runs, in parallel
     if (have && !is_match) {
       for (uint32_t i = 0; i < nl; ++i) {
         const uint8_t v = static_cast<uint8_t>(t >> (8 * i));
         dst[my_pos + i] = v;
-        ring[(my_pos + i) & (kRing - 1)] = v;
+        if (my_pos + static_cast<int32_t>(i) >= ring_lo) ring[(my_pos + i) & (kRing - 1)] = v;
       }
     }
-    uint32_t mm = __ballot_sync(0xffffffffu, is_match);
+    // A match whose source bytes (before its own output) are covered by no match of this chunk
+    // depends only on earlier chunks and this chunk's literals: those copy in parallel.
+    // Covering tokens are the lanes whose output [start, end) meets [src0, ext_end).
+    const uint32_t match_lanes = __ballot_sync(0xffffffffu, is_match);
+    const int32_t src0 = my_pos - distance;
+    const int32_t ext_end = is_match ? min(src0 + tlen, my_pos) : 0;
+    int lo = 0, hi = 0;  // lo = #lanes ending <= src0, hi = #lanes starting < ext_end
+#pragma unroll
+    for (int st = 16; st; st >>= 1) {
+      if (__shfl_sync(0xffffffffu, incl, lo + st - 1) + pos <= src0) lo += st;
+      if (__shfl_sync(0xffffffffu, incl - tlen, hi + st - 1) + pos < ext_end) hi += st;
+    }
+    const uint32_t cover = hi > lo ? ((hi - lo >= 32 ? 0xffffffffu : ((1u << (hi - lo)) - 1u)) << lo) : 0u;
+    const bool par = is_match && (cover & match_lanes) == 0;
+    // round 1: independent matches, their bytes dealt out over the lanes
+    const int32_t plen = par ? tlen : 0;
+    int32_t pincl = plen;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t v = __shfl_up_sync(0xffffffffu, pincl, o);
+      if (lane >= o) pincl += v;
+    }
+    const int32_t ptotal = __shfl_sync(0xffffffffu, pincl, 31);
+    __syncwarp();  // literal bytes visible
+    for (int32_t g0 = 0; g0 < ptotal; g0 += 32) {
+      const int32_t g = g0 + lane;
+      int j = 0;  // the lane whose match holds byte g: #lanes with pincl <= g
+#pragma unroll
+      for (int st = 16; st; st >>= 1)
+        if (__shfl_sync(0xffffffffu, pincl, j + st - 1) <= g) j += st;
+      j = min(j, 31);
+      const int32_t jstart = __shfl_sync(0xffffffffu, pincl - plen, j);
+      const int32_t jp0 = __shfl_sync(0xffffffffu, my_pos, j);
+      const int32_t jd = __shfl_sync(0xffffffffu, distance, j);
+      if (g < ptotal) {
+        int32_t o = g - jstart;
+        const int32_t q = jp0 + o;
+        if (o >= jd) o -= jd * (o / jd);  // overlapping copy: repeats the jd bytes before jp0
+        const int32_t src = jp0 - jd + o;
+        const uint8_t v = jp0 - jd >= ring_lo ? ring[src & (kRing - 1)] : dst[src];
+        dst[q] = v;
+        if (q >= ring_lo) ring[q & (kRing - 1)] = v;
+      }
+    }
+    // round 2: the remaining matches in order, each copied by the whole warp
+    uint32_t mm = __ballot_sync(0xffffffffu, is_match && !par);
     while (mm) {
       const int j = __ffs(mm) - 1;
       mm &= mm - 1;
-      const uint32_t tj = __shfl_sync(0xffffffffu, t, j);
       const int32_t p0 = __shfl_sync(0xffffffffu, my_pos, j);
-      const int length = static_cast<int>((tj >> 16) & 0x3FFu);
-      const int distance = static_cast<int>(tj & 0xFFFFu);
-      __syncwarp();  // literals and earlier matches are visible
-      // the ring holds position x until x + kRing is written; the chunk's literals are written
-      // up to chunk_end - 1 already, so a source is in the ring iff it is >= chunk_end - kRing
-      const bool from_ring = p0 - distance >= chunk_end - kRing;
-      if (length <= 32 && distance >= length) {
-        if (lane < length) {
-          const int src = p0 - distance + lane;
-          const uint8_t v = from_ring ? ring[src & (kRing - 1)] : dst[src];
-          dst[p0 + lane] = v;
-          ring[(p0 + lane) & (kRing - 1)] = v;
-        }
-      } else {
-        int jj = lane, step = 32;
-        if (distance < length) {
-          const float inv_d = __frcp_rn(static_cast<float>(distance));
-          jj = lane - distance * __float2int_rz(static_cast<float>(lane) * inv_d);
-          jj += jj < 0 ? distance : 0;
-          jj -= jj >= distance ? distance : 0;
-          step = 32 - distance * __float2int_rz(32.f * inv_d);
-          step += step < 0 ? distance : 0;
-          step -= step >= distance ? distance : 0;
-        }
-        for (int q = lane; q < length; q += 32) {
-          const int src = p0 - distance + jj;
-          const uint8_t v = from_ring ? ring[src & (kRing - 1)] : dst[src];
-          dst[p0 + q] = v;
-          ring[(p0 + q) & (kRing - 1)] = v;
-          if (distance < length) {
-            jj += step;
-            jj -= jj >= distance ? distance : 0;
-          } else {
-            jj += 32;
-          }
-        }
+      const int length = __shfl_sync(0xffffffffu, tlen, j);
+      const int dj = __shfl_sync(0xffffffffu, distance, j);
+      __syncwarp();  // earlier bytes of the chunk are visible
+      const bool from_ring = p0 - dj >= ring_lo;
+      for (int qo = lane; qo < length; qo += 32) {
+        const int o = qo < dj ? qo : qo - dj * (qo / dj);
+        const int src = p0 - dj + o;
+        const uint8_t v = from_ring ? ring[src & (kRing - 1)] : dst[src];
+        dst[p0 + qo] = v;
+        if (p0 + qo >= ring_lo) ring[(p0 + qo) & (kRing - 1)] = v;
       }
     }
     pos = chunk_end;
