@@ -243,7 +243,9 @@ struct pg_ctx {
   unsigned long long cand_base = 0;  // test hook: initial candidate-counter value (pg_ctx_debug_candidate_base)
   bool fused_decode = true;
   bool wide_digits = true;
-  bool wide3t = true;  // BGEN-8: transposed wide GEMM (PG_WIDE3T=0: the kWide3 kernel, A/B)
+  // BGEN-8: transposed wide GEMM (A/B, PG_WIDE3T=1). Measured 9 % slower than kWide3 on C5
+  // (4.56e9 vs 4.96-5.08e9 tests/s; no raster recovered it), so off by default.
+  bool wide3t = false;
 
   // extension mode: quantized covariate basis (columns 1..rank-1) + side-GEMM output
   bool have_basis = false;

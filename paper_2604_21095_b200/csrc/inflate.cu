@@ -20,6 +20,7 @@
 // with host zlib to raise zlib's own message.
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 
 #include "inflate.cuh"
 
@@ -504,7 +505,7 @@ __global__ void __launch_bounds__(4 * L) inflate_kernel(const uint8_t* __restric
 }
 
 // ------------------------------------------------------------------------------------------
-// Two-phase decoder (default). The warp-per-stream kernel above runs the serial Huffman decode
+// Two-phase decoder (A/B: PG_INFLATE_MODE=tokens). The warp-per-stream kernel above runs the serial Huffman decode
 // on all 32 lanes in lock-step: ~100 warp instructions per DEFLATE symbol, 32x redundant. Here
 //   phase 1 (thread per stream): each thread decodes its own stream's Huffman codes into LZ77
 //            tokens (literal runs of 1-3 bytes | (length, distance) matches) and validates the
@@ -999,13 +1000,15 @@ int inflate_streams(const uint8_t* d_blob, const int64_t* d_off, const int64_t* 
                     uint8_t* d_out, int64_t out_stride, int64_t* d_out_len, int* d_status, cudaStream_t s,
                     uint32_t* d_tokens, int32_t* d_ntok) {
   if (count <= 0) return PG_OK;
-  // PG_INFLATE_LANES=32 / 16: the warp-per-stream decoder (A/B switch); 16 = two streams per
-  // warp (measured 10 % slower than 32 on C5: the half-warps diverge on literal / match)
-  static const int lanes = [] {
-    const char* e = std::getenv("PG_INFLATE_LANES");
-    return e ? std::atoi(e) : 0;
-  }();
-  if (d_tokens != nullptr && d_ntok != nullptr && lanes == 0) {
+  // Default: the warp-per-stream decoder. PG_INFLATE_MODE=tokens selects the two-phase
+  // decoder (measured slower on C5: 15.0 + 4.6 ms vs 8.5 ms per 8,192 BGEN-8 variants; a
+  // batch gives phase 1 only ~55 streams = 1.7 warps per SM, so its serial per-thread decode
+  // is latency-bound). PG_INFLATE_LANES=16: two streams per warp (10 % slower than 32).
+  // Read per call (A/B tests switch it inside one process).
+  const char* mode = std::getenv("PG_INFLATE_MODE");
+  const char* lanes_env = std::getenv("PG_INFLATE_LANES");
+  const int lanes = lanes_env && std::atoi(lanes_env) == 16 ? 16 : 32;
+  if (d_tokens != nullptr && d_ntok != nullptr && mode != nullptr && std::strcmp(mode, "tokens") == 0) {
     const int64_t tok_stride = inflate_token_stride(out_stride);
     constexpr int kSmem = static_cast<int>(sizeof(ThreadTables)) * kTokThreads;
     PG_CUDA_CHECK(cudaFuncSetAttribute(inflate_tokens_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));

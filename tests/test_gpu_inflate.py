@@ -41,7 +41,11 @@ def _payloads(rng):
                                             (6, zlib.Z_DEFAULT_STRATEGY), (9, zlib.Z_DEFAULT_STRATEGY),
                                             (6, zlib.Z_FIXED), (6, zlib.Z_RLE), (6, zlib.Z_HUFFMAN_ONLY),
                                             (6, zlib.Z_FILTERED)])
-def test_matches_zlib(level, strategy):
+@pytest.mark.parametrize("decoder", ["warp", "tokens"])
+def test_matches_zlib(level, strategy, decoder, monkeypatch):
+    """Both GPU decoders (warp per stream; two-phase tokens, PG_INFLATE_MODE=tokens) == zlib."""
+    if decoder == "tokens":
+        monkeypatch.setenv("PG_INFLATE_MODE", "tokens")
     rng = np.random.default_rng(level * 10 + strategy)
     data = _payloads(rng)
     streams = []
@@ -53,7 +57,10 @@ def test_matches_zlib(level, strategy):
         assert st == 0 and out == d
 
 
-def test_many_streams_and_multiple_blocks():
+@pytest.mark.parametrize("decoder", ["warp", "tokens"])
+def test_many_streams_and_multiple_blocks(decoder, monkeypatch):
+    if decoder == "tokens":
+        monkeypatch.setenv("PG_INFLATE_MODE", "tokens")
     rng = np.random.default_rng(7)
     data = [rng.integers(0, 3, rng.integers(1, 200000), dtype=np.uint8).tobytes() for _ in range(200)]
     streams = []
@@ -67,7 +74,10 @@ def test_many_streams_and_multiple_blocks():
         assert st == 0 and out == d
 
 
-def test_corrupt_streams_rejected():
+@pytest.mark.parametrize("decoder", ["warp", "tokens"])
+def test_corrupt_streams_rejected(decoder, monkeypatch):
+    if decoder == "tokens":
+        monkeypatch.setenv("PG_INFLATE_MODE", "tokens")
     good = zlib.compress(b"hello world " * 500)
     bad_header = b"\x78\x9d" + good[2:]                            # FCHECK wrong
     bad_sum = good[:-1] + bytes([good[-1] ^ 1])                     # Adler-32 mismatch
