@@ -348,6 +348,7 @@ def our_arm(a) -> None:
             if rank != 0:
                 if wbuf is not buf:
                     buf.copy_(wbuf)
+                torch.cuda.current_stream(dev).synchronize()  # broadcast / copy done before the ctx's stream reads buf
                 ctx.import_panel(buf.data_ptr(), n, p, gidx, n)
             return int(nb.item())
         return 0

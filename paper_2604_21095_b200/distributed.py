@@ -68,6 +68,9 @@ def broadcast_panel(ctx, torch, dist, rank: int, n_kept: int, n_pheno: int, gidx
     if rank != 0:
         if wire == "cpu":
             buf = buf.to(device)
+        # the NCCL broadcast (and the copy) complete on torch's stream; the ctx reads the
+        # buffer on its own stream, so wait for torch's before handing the pointer over
+        torch.cuda.current_stream(device).synchronize()
         ctx.import_panel(buf.data_ptr(), n_kept, n_pheno, gidx, n_src)
     return int(buf.numel())
 
