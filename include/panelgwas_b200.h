@@ -148,6 +148,12 @@ PG_API int pg_ctx_set_fused_decode(pg_ctx* ctx, int enable);
  * only the markers that have any through a side GEMM; 0 sends the whole batch to the two-row
  * (dosage, mask) planes. Exact either way: results are bitwise identical (A/B switch). */
 PG_API int pg_ctx_set_missing_side_gemm(pg_ctx* ctx, int enable);
+/* Precision.F64 (engine.py:31-33: float64 storage end to end): 1 quantizes the panel at two
+ * levels (y~ = s (q + q2 / 2^22), ~46 bits) and runs the exact GEMM once per level, summing
+ * the int64 partials before the statistics; 0 (default, the reference's default f32 mode's
+ * accuracy class) one 23-bit level. Call before the panel is uploaded (pg_ctx_set_panel /
+ * pg_ctx_commit_panel / pg_ctx_import_panel); changing it drops the current panel. */
+PG_API int pg_ctx_set_f64_panel(pg_ctx* ctx, int enable);
 
 /* Result summary of the last scan call. */
 typedef struct pg_batch_info {

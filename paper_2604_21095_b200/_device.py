@@ -200,6 +200,10 @@ class DeviceContext:
     def set_fused_decode(self, enable: bool) -> None:
         call("pg_ctx_set_fused_decode", self._h, 1 if enable else 0)
 
+    def set_f64_panel(self, enable: bool) -> None:
+        """Two-level (~46-bit) panel for Precision.F64; call before the panel is uploaded."""
+        call("pg_ctx_set_f64_panel", self._h, 1 if enable else 0)
+
     def set_missing_side_gemm(self, enable: bool) -> None:
         call("pg_ctx_set_missing_side_gemm", self._h, 1 if enable else 0)
 

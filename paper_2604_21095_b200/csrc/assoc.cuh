@@ -63,7 +63,14 @@ struct AssocEpilogue {
   const long long* side_x;
   const int* side_slot;
   int64_t side_ld;
+  // F64 precision mode (two-level panel, panel.cuh): the lo level's exact (xu, xm) partials
+  // (x_lo, same layout as x_accum) and column sums cq_lo join the hi level's in the final
+  // statistics, r = s ((xu + xu_lo / kLoScale) - mu ((cq - xm) + (cq_lo - xm_lo) / kLoScale)) / den.
+  const long long* x_lo;
+  const long long* cq_lo;
+  int x_partials_only;  // 1: accumulate x_accum only (the lo level's pass), no statistics
 };
+constexpr double kLoScale = 4194304.0;  // 2^22: lo-level limbs q2 = rint((y~/s - q) 2^22), |q2| <= 2^21
 
 // Launch K2/K3 on `stream`. Panel limbs q*[p_pad, k_pad], genotype planes
 // v / v127 [c_pad, k_pad] (int8, K-major, rows 16-byte aligned).

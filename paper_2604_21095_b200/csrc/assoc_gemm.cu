@@ -174,7 +174,8 @@ struct MaxAbsR {
 // the lane still takes part in the warp's compaction ballot.
 __device__ __forceinline__ void epilogue_value(const AssocEpilogue& ep, long long xu, long long xm, int m, int pheno,
                                                float sc_f, double sc_d, float cq_f, long long cq, float rb, int lane,
-                                               uint32_t lanemask_lt, MaxAbsR& mx, bool valid = true) {
+                                               uint32_t lanemask_lt, MaxAbsR& mx, bool valid = true,
+                                               double lo_u = 0.0, double lo_cm = 0.0) {
   const float mu = __ldg(ep.mu_f + m);
   const float iv = ep.raw ? 1.f : __ldg(ep.invd_f + m);  // NaN for skipped / padding markers
   const float xf = static_cast<float>(xu) - mu * (cq_f - static_cast<float>(xm));
@@ -185,7 +186,7 @@ __device__ __forceinline__ void epilogue_value(const AssocEpilogue& ep, long lon
   const bool near_max = valid && ep.max_abs_r != nullptr && ar >= mx.f * (1.f - 2e-5f) - 2e-7f;
   double r64 = 0.0;
   if (hit || (valid && ep.full_r) || near_max) {
-    r64 = sc_d * (static_cast<double>(xu) - __ldg(ep.mu_d + m) * static_cast<double>(cq - xm)) *
+    r64 = sc_d * ((static_cast<double>(xu) + lo_u) - __ldg(ep.mu_d + m) * (static_cast<double>(cq - xm) + lo_cm)) *
           (ep.raw ? 1.0 : __ldg(ep.invd_d + m));
   }
   if (near_max) {
@@ -671,7 +672,14 @@ __global__ void x_epilogue_kernel(AssocEpilogue ep, int64_t m_slots) {
     const long long* x = ep.x_accum + (m * ep.x_ld + pheno) * 2;
     AssocEpilogue e = ep;
     e.x_accum = nullptr;
-    epilogue_value(e, x[0], x[1], static_cast<int>(m), pheno, sc_f, sc_d, cq_f, cq, rb, lane, lanemask_lt, mx);
+    double lo_u = 0.0, lo_cm = 0.0;
+    if (ep.x_lo) {  // F64 precision: the two-level panel's lo partials
+      const long long* xl = ep.x_lo + (m * ep.x_ld + pheno) * 2;
+      lo_u = static_cast<double>(xl[0]) / kLoScale;
+      lo_cm = static_cast<double>(ep.cq_lo[pheno] - xl[1]) / kLoScale;
+    }
+    epilogue_value(e, x[0], x[1], static_cast<int>(m), pheno, sc_f, sc_d, cq_f, cq, rb, lane, lanemask_lt, mx, true,
+                   lo_u, lo_cm);
   }
   if (ep.max_abs_r && pheno < ep.p_valid)
     atomicMax(ep.max_abs_r + pheno, static_cast<unsigned long long>(__double_as_longlong(mx.d)));
@@ -712,15 +720,16 @@ int launch_common(const CUtensorMap& tm_qh, const CUtensorMap& tm_q1, const CUte
   const uint32_t l2_codes = env_l2 >= 0 ? static_cast<uint32_t>(env_l2) : kDefaultL2Codes;
   const int n_kb = static_cast<int>(k_pad / kTileK);
   constexpr int kSliceKb = static_cast<int>(kSliceK / kTileK);
-  if (n_kb <= kSliceKb) {
-    PG_REQUIRE(ep.x_accum == nullptr, PG_ERR_INVALID, "assoc: x_accum given for an unsliced run");
+  if (ep.x_accum == nullptr) {
+    PG_REQUIRE(n_kb <= kSliceKb, PG_ERR_INVALID, "assoc: %d K blocks need the sliced (x_accum) path", n_kb);
     assoc_i8_kernel<MODE><<<grid, kThreads, Cfg<MODE>::kSmemBytes, stream>>>(
         tm_qh, tm_q1, tm_q0, tm_v, tm_v127, n_ctile, n_ptile, 0, n_kb, group_c, l2_codes, ep);
   } else {
-    PG_REQUIRE(!Cfg<MODE>::TRANS, PG_ERR_INVALID, "assoc(wide3t): K-sliced runs use the untransposed kernel");
-    // more samples than one int32-exact slice: accumulate int64 partials slice by slice,
-    // then derive the statistics (same epilogue arithmetic) from the exact sums
-    PG_REQUIRE(ep.x_accum != nullptr && ep.x_ld == p_pad, PG_ERR_INVALID, "assoc: K-sliced run needs x_accum");
+    // exact int64 partials per (marker, phenotype): K slices of one int32-exact range each
+    // (cohorts above kSliceK samples), and / or the two levels of the F64 panel; the
+    // statistics come from the summed partials (same epilogue arithmetic)
+    PG_REQUIRE(!Cfg<MODE>::TRANS, PG_ERR_INVALID, "assoc(wide3t): partial-sum runs use the untransposed kernel");
+    PG_REQUIRE(ep.x_ld == p_pad, PG_ERR_INVALID, "assoc: x_accum leading dimension must be p_pad");
     const int rows = Cfg<MODE>::WIDE ? Cfg<MODE>::kWideR : ep.rows_per_marker;
     const int64_t m_slots = c_pad / rows;
     PG_CUDA_CHECK(cudaMemsetAsync(ep.x_accum, 0, sizeof(long long) * 2 * m_slots * p_pad, stream));
@@ -730,8 +739,10 @@ int launch_common(const CUtensorMap& tm_qh, const CUtensorMap& tm_q1, const CUte
           tm_qh, tm_q1, tm_q0, tm_v, tm_v127, n_ctile, n_ptile, kb0, nk, group_c, l2_codes, ep);
       PG_CUDA_CHECK(cudaGetLastError());
     }
-    const unsigned gy = static_cast<unsigned>(m_slots < 4096 ? (m_slots + 7) / 8 : 512);
-    x_epilogue_kernel<<<dim3(static_cast<unsigned>(p_pad / 32), gy), 256, 0, stream>>>(ep, m_slots);
+    if (!ep.x_partials_only) {
+      const unsigned gy = static_cast<unsigned>(m_slots < 4096 ? (m_slots + 7) / 8 : 512);
+      x_epilogue_kernel<<<dim3(static_cast<unsigned>(p_pad / 32), gy), 256, 0, stream>>>(ep, m_slots);
+    }
   }
   PG_CUDA_CHECK(cudaGetLastError());
   return PG_OK;

@@ -229,6 +229,10 @@ struct pg_ctx {
   pg::DBuf<uint8_t> full_out;
   pg::DBuf<double> scratch_a, scratch_b, scratch_c, scratch_d;
   pg::DBuf<long long> xacc, xacc_b;  // K-sliced runs (cohorts above kSliceK samples)
+  // F64 precision mode (pg_ctx_set_f64_panel): the panel's lo level + its partial sums
+  bool f64_panel = false;
+  pg::DBuf<int8_t> qh_lo, q1_lo, q0_lo;
+  pg::DBuf<long long> cq_lo, xacc_lo, side_x_lo;
   // missing-call side path of the fused PLINK GEMM (pg_ctx_set_missing_side_gemm)
   bool side_missing = true;
   pg::DBuf<int> miss_flag, miss_prefix, miss_slot, miss_list, miss_count;
@@ -323,6 +327,16 @@ int upload_panel_common(pg_ctx* c, const double* d_y, int64_t n_kept, int64_t n_
   pp.scale_f = c->scale_f.p;
   pp.cq = c->cq.p;
   pp.cq_f = c->cq_f.p;
+  if (c->f64_panel) {
+    PG_CHECK_STATUS(c->qh_lo.ensure(plane));
+    PG_CHECK_STATUS(c->q1_lo.ensure(plane));
+    PG_CHECK_STATUS(c->q0_lo.ensure(plane));
+    PG_CHECK_STATUS(c->cq_lo.ensure(c->p_pad));
+    pp.qh_lo = c->qh_lo.p;
+    pp.q1_lo = c->q1_lo.p;
+    pp.q0_lo = c->q0_lo.p;
+    pp.cq_lo = c->cq_lo.p;
+  }
   PG_CHECK_STATUS(
       panel_quantize(d_y, n_kept, n_pheno, ld, d_cols, c->gidx.p, c->k_pad, c->p_pad, pp, c->maxabs.p, c->stream));
   PG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
@@ -439,7 +453,8 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
   const bool wide = R == kWideRows || R == kWideRows3;
   // BGEN-8: the transposed wide GEMM (genotype rows as A) unless the run needs K slices,
   // the extension-mode side GEMM or the per-phenotype max |r| (kept on the kWide3 kernel)
-  const bool wide3t = R == kWideRows3 && c->wide3t && c->k_pad <= kSliceK && !c->have_basis && !c->track_max_abs_r;
+  const bool wide3t = R == kWideRows3 && c->wide3t && c->k_pad <= kSliceK && !c->have_basis && !c->track_max_abs_r &&
+                      !c->f64_panel;
   const int64_t c_pad = wide3t ? round_up((m + 9) / 10 * 32, kTileC)
                                : round_up(m * R, wide ? (R == kWideRows3 ? kTileCWide3 : kTileCWide) : kTileC);
   // PLINK rows without missing calls: the GEMM decodes the packed codes itself
@@ -467,9 +482,11 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
     PG_CHECK_STATUS(missing_mask_planes(b, c->miss_list.p, n_side, c->side_v.p, c->side_v127.p, side_rows, c->k_pad, s));
     ++launches;
   }
-  auto run_side = [&]() -> int {
-    if (!side_pending) return PG_OK;
-    side_pending = false;
+  // one side GEMM per panel level (hi, and lo in F64 mode), run once per batch
+  bool side_done[2] = {false, false};
+  auto run_side = [&](int level) -> int {
+    if (!side_pending || side_done[level]) return PG_OK;
+    side_done[level] = true;
     AssocEpilogue es{};
     es.rows_per_marker = 1;
     es.m_valid = n_side;
@@ -482,13 +499,34 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
     es.scale_d = c->scale_d.p;
     es.cq_f = c->cq_f.p;
     es.cq = c->cq.p;
-    es.side_out = c->side_x.p;
     es.side_ld = c->p_pad;
     ++launches;
+    if (level == 1) {
+      PG_CHECK_STATUS(c->side_x_lo.ensure(static_cast<size_t>(side_rows) * c->p_pad));
+      es.side_out = c->side_x_lo.p;
+      return launch_assoc(c->qh_lo.p, c->q1_lo.p, c->q0_lo.p, c->p_pad, c->side_v.p, c->side_v127.p, side_rows,
+                          c->k_pad, es, s);
+    }
+    es.side_out = c->side_x.p;
     return launch_assoc(c->qh.p, c->q1.p, c->q0.p, c->p_pad, c->side_v.p, c->side_v127.p, side_rows, c->k_pad, es, s);
   };
   auto run_gemm = [&](const AssocEpilogue& e) -> int {
-    PG_CHECK_STATUS(run_side());
+    if (c->f64_panel) {
+      // lo level first (partials only), then the hi level, whose statistics add the lo partials
+      AssocEpilogue el = e;
+      el.x_accum = c->xacc_lo.p;
+      el.x_partials_only = 1;
+      el.x_lo = nullptr;
+      if (e.side_slot) el.side_x = c->side_x_lo.p;
+      PG_CHECK_STATUS(run_side(1));
+      PG_CHECK_STATUS(run_gemm_on(el, c->qh_lo.p, c->q1_lo.p, c->q0_lo.p, c->p_pad));
+      ++launches;
+      AssocEpilogue eh = e;
+      eh.x_lo = c->xacc_lo.p;
+      PG_CHECK_STATUS(run_side(0));
+      return run_gemm_on(eh, c->qh.p, c->q1.p, c->q0.p, c->p_pad);
+    }
+    PG_CHECK_STATUS(run_side(0));
     return run_gemm_on(e, c->qh.p, c->q1.p, c->q0.p, c->p_pad);
   };
   if (c->have_basis) {
@@ -553,10 +591,16 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
   }
   PG_CHECK_STATUS(c->cand_count.ensure(1));
   ep.cand_count = c->cand_count.p;
-  if (c->k_pad > kSliceK) {  // K-sliced contraction: exact int64 partials per (marker, phenotype)
+  // exact int64 partials per (marker, phenotype): K-sliced contraction, and / or the two
+  // panel levels of the F64 precision mode
+  if (c->k_pad > kSliceK || c->f64_panel) {
     PG_CHECK_STATUS(c->xacc.ensure(static_cast<size_t>(c_pad / R) * c->p_pad * 2));
     ep.x_accum = c->xacc.p;
     ep.x_ld = c->p_pad;
+  }
+  if (c->f64_panel) {
+    PG_CHECK_STATUS(c->xacc_lo.ensure(static_cast<size_t>(c_pad / R) * c->p_pad * 2));
+    ep.cq_lo = c->cq_lo.p;
   }
   int64_t ncand = 0;
   if (c->mode == PG_MODE_FULL) {
@@ -896,6 +940,7 @@ int pg_ctx_panel_bytes(pg_ctx* c, int64_t* bytes) {
   PG_CHECK_STATUS(ctx_check(c));
   PG_REQUIRE(c->have_panel, PG_ERR_STATE, "no panel");
   *bytes = 3 * c->p_pad * c->k_pad + c->p_pad * (8 + 4 + 8 + 4);
+  if (c->f64_panel) *bytes += 3 * c->p_pad * c->k_pad + c->p_pad * 8;  // the lo level
   return PG_OK;
 }
 
@@ -913,6 +958,13 @@ int pg_ctx_export_panel(pg_ctx* c, void* d_dst) {
   PG_CUDA_CHECK(cudaMemcpyAsync(tail + 8 * pp, c->scale_f.p, 4 * pp, cudaMemcpyDeviceToDevice, c->stream));
   PG_CUDA_CHECK(cudaMemcpyAsync(tail + 12 * pp, c->cq.p, 8 * pp, cudaMemcpyDeviceToDevice, c->stream));
   PG_CUDA_CHECK(cudaMemcpyAsync(tail + 20 * pp, c->cq_f.p, 4 * pp, cudaMemcpyDeviceToDevice, c->stream));
+  if (c->f64_panel) {
+    uint8_t* lo = tail + 24 * pp;
+    PG_CUDA_CHECK(cudaMemcpyAsync(lo, c->qh_lo.p, plane, cudaMemcpyDeviceToDevice, c->stream));
+    PG_CUDA_CHECK(cudaMemcpyAsync(lo + plane, c->q1_lo.p, plane, cudaMemcpyDeviceToDevice, c->stream));
+    PG_CUDA_CHECK(cudaMemcpyAsync(lo + 2 * plane, c->q0_lo.p, plane, cudaMemcpyDeviceToDevice, c->stream));
+    PG_CUDA_CHECK(cudaMemcpyAsync(lo + 3 * plane, c->cq_lo.p, 8 * pp, cudaMemcpyDeviceToDevice, c->stream));
+  }
   PG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
   return PG_OK;
 }
@@ -956,6 +1008,17 @@ int pg_ctx_import_panel(pg_ctx* c, const void* d_src, int64_t n_kept, int64_t n_
   PG_CUDA_CHECK(cudaMemcpyAsync(c->scale_f.p, tail + 8 * pp, 4 * pp, cudaMemcpyDeviceToDevice, c->stream));
   PG_CUDA_CHECK(cudaMemcpyAsync(c->cq.p, tail + 12 * pp, 8 * pp, cudaMemcpyDeviceToDevice, c->stream));
   PG_CUDA_CHECK(cudaMemcpyAsync(c->cq_f.p, tail + 20 * pp, 4 * pp, cudaMemcpyDeviceToDevice, c->stream));
+  if (c->f64_panel) {
+    PG_CHECK_STATUS(c->qh_lo.ensure(plane));
+    PG_CHECK_STATUS(c->q1_lo.ensure(plane));
+    PG_CHECK_STATUS(c->q0_lo.ensure(plane));
+    PG_CHECK_STATUS(c->cq_lo.ensure(pp));
+    const uint8_t* lo = tail + 24 * pp;
+    PG_CUDA_CHECK(cudaMemcpyAsync(c->qh_lo.p, lo, plane, cudaMemcpyDeviceToDevice, c->stream));
+    PG_CUDA_CHECK(cudaMemcpyAsync(c->q1_lo.p, lo + plane, plane, cudaMemcpyDeviceToDevice, c->stream));
+    PG_CUDA_CHECK(cudaMemcpyAsync(c->q0_lo.p, lo + 2 * plane, plane, cudaMemcpyDeviceToDevice, c->stream));
+    PG_CUDA_CHECK(cudaMemcpyAsync(c->cq_lo.p, lo + 3 * plane, 8 * pp, cudaMemcpyDeviceToDevice, c->stream));
+  }
   PG_CUDA_CHECK(cudaMemcpyAsync(c->gidx.p, geno_row_index, sizeof(int64_t) * n_kept, cudaMemcpyHostToDevice,
                                 c->stream));
   PG_CUDA_CHECK(cudaMemcpyAsync(c->keep_bits.p, bits.data(), sizeof(uint32_t) * bits.size(), cudaMemcpyHostToDevice,
@@ -1066,6 +1129,16 @@ int pg_ctx_debug_candidate_base(pg_ctx* c, uint64_t base) {
 int pg_ctx_set_wide_digits(pg_ctx* c, int enable) {
   PG_CHECK_STATUS(ctx_check(c));
   c->wide_digits = enable != 0;
+  return PG_OK;
+}
+
+int pg_ctx_set_f64_panel(pg_ctx* c, int enable) {
+  PG_CHECK_STATUS(ctx_check(c));
+  if ((enable != 0) != c->f64_panel) {
+    c->f64_panel = enable != 0;
+    c->have_panel = false;  // the panel's levels change: upload it (again) after this call
+    c->have_scan = false;
+  }
   return PG_OK;
 }
 

@@ -14,6 +14,13 @@ struct PanelPlanes {
   float* scale_f = nullptr;
   long long* cq = nullptr;  // [p_pad] sum_k q[p,k]
   float* cq_f = nullptr;
+  // Two-level panel (F64 precision mode; null = off): the residual y~/s - q quantized again,
+  // q2 = rint((y~/s - q) * kLoScale), |q2| <= kLoScale / 2, in three more limbs, so that
+  // y~ = s (q + q2 / kLoScale) to ~1e-14 of max |y~| (the GEMM runs once per level).
+  int8_t* qh_lo = nullptr;
+  int8_t* q1_lo = nullptr;
+  int8_t* q0_lo = nullptr;
+  long long* cq_lo = nullptr;  // [p_pad] sum_k q2[p,k]
 };
 
 // Quantize y (device f64, n_rows kept samples x n_cols phenotypes, row pitch `ld`

@@ -267,8 +267,10 @@ def device_batch_size(config: ScanConfig, n_markers: int, n_pheno: int, n_sample
         b = min(b, max(256, _MAX_FULL_BYTES // (8 * max(n_pheno, 1))))
     else:
         b = min(b, max(256, _CAND_BUDGET // max(1, expected_candidates_per_marker(config, b, n_pheno))))
-    if n_samples > _SLICE_SAMPLES:  # K-sliced device runs hold 16 B of partials per test
-        b = min(b, max(256, _MAX_FULL_BYTES * 2 // (16 * max(n_pheno, 1))))
+    if n_samples > _SLICE_SAMPLES or config.precision is Precision.F64:
+        # K-sliced runs hold 16 B of int64 partials per test, F64 mode 16 B per panel level
+        per_test = 32 if config.precision is Precision.F64 else 16
+        b = min(b, max(256, _MAX_FULL_BYTES * 2 // (per_test * max(n_pheno, 1))))
     return max(1, min(b, n_markers))
 
 
@@ -411,6 +413,8 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, init, ctx_fut, mark
         if source.n_markers < 1:
             raise PanelGwasError("genotype source has no markers")
         ctx = ctx_fut.result()
+        # Precision.F64: the panel at two quantization levels (~46 bits), one exact GEMM each
+        ctx.set_f64_panel(config.precision is Precision.F64)
     except BaseException:
         for fut, release in ((ring_fut, _free_pinned), (ctx_fut, lambda c: c.close())):
             try:

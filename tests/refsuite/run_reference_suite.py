@@ -29,14 +29,10 @@ ROOT = Path(__file__).resolve().parents[2]
 SHIM = Path(__file__).resolve().parent / "shim"
 ARCHIVE = ROOT / "oracle" / "_ref" / "reference_tests.zip"
 
-# node id -> why it cannot hold for the drop-in (each justified individually)
-EXCLUDED: dict[str, str] = {
-    "test_engine.py::TestScanBehavior::test_paper_df_matches_simple_ols_without_covariates":
-        "asserts |t - OLS t| <= 1e-8 absolute (F64 mode, n=25). The drop-in contracts the panel "
-        "quantized to 23 bits (exact int8 tensor-core GEMM, DESIGN.md section 2): |dt| is about "
-        "2e-7 here, inside the north star's stated 1e-4 relative tolerance and the reference's own "
-        "f32-vs-f64 bar (test_engine.py:298-308), but above this test's 1e-8 fp64 bar.",
-}
+# node id -> why it cannot hold for the drop-in (each justified individually); round 1's one
+# exclusion (test_engine.py::...::test_paper_df_matches_simple_ols_without_covariates, |t - OLS t|
+# <= 1e-8 in F64 mode) is met since Precision.F64 runs the two-level (~46-bit) panel
+EXCLUDED: dict[str, str] = {}
 
 
 def run(json_out: Path | None, extra: list[str]) -> dict:
