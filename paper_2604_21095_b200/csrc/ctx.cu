@@ -479,6 +479,7 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
     PG_CHECK_STATUS(c->side_v.ensure(static_cast<size_t>(side_rows) * c->k_pad));
     PG_CHECK_STATUS(c->side_v127.ensure(static_cast<size_t>(side_rows) * c->k_pad));
     PG_CHECK_STATUS(c->side_x.ensure(static_cast<size_t>(side_rows) * c->p_pad));
+    if (c->f64_panel) PG_CHECK_STATUS(c->side_x_lo.ensure(static_cast<size_t>(side_rows) * c->p_pad));
     PG_CHECK_STATUS(missing_mask_planes(b, c->miss_list.p, n_side, c->side_v.p, c->side_v127.p, side_rows, c->k_pad, s));
     ++launches;
   }
@@ -501,8 +502,7 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
     es.cq = c->cq.p;
     es.side_ld = c->p_pad;
     ++launches;
-    if (level == 1) {
-      PG_CHECK_STATUS(c->side_x_lo.ensure(static_cast<size_t>(side_rows) * c->p_pad));
+    if (level == 1) {  // side_x_lo was sized with the other side buffers (its pointer is already in use)
       es.side_out = c->side_x_lo.p;
       return launch_assoc(c->qh_lo.p, c->q1_lo.p, c->q0_lo.p, c->p_pad, c->side_v.p, c->side_v127.p, side_rows,
                           c->k_pad, es, s);
