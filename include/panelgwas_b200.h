@@ -154,6 +154,11 @@ PG_API int pg_ctx_set_missing_side_gemm(pg_ctx* ctx, int enable);
  * accuracy class) one 23-bit level. Call before the panel is uploaded (pg_ctx_set_panel /
  * pg_ctx_commit_panel / pg_ctx_import_panel); changing it drops the current panel. */
 PG_API int pg_ctx_set_f64_panel(pg_ctx* ctx, int enable);
+/* PLINK THRESHOLD / TOPK scans (default 1): the GEMM runs two of the three panel limbs (two
+ * MMAs per 32 samples); the premask is widened by the rigorous bound |sum_k q0 u| <=
+ * ||q0_p||_2 ||u_m||_2 on the deferred limb, and every candidate gets sum_k q0 u added
+ * exactly before its fp64 r, t and p (results bitwise identical to 0 = all three limbs). */
+PG_API int pg_ctx_set_two_limb_premask(pg_ctx* ctx, int enable);
 
 /* Result summary of the last scan call. */
 typedef struct pg_batch_info {

@@ -204,6 +204,9 @@ class DeviceContext:
         """Two-level (~46-bit) panel for Precision.F64; call before the panel is uploaded."""
         call("pg_ctx_set_f64_panel", self._h, 1 if enable else 0)
 
+    def set_two_limb_premask(self, enable: bool) -> None:
+        call("pg_ctx_set_two_limb_premask", self._h, 1 if enable else 0)
+
     def set_missing_side_gemm(self, enable: bool) -> None:
         call("pg_ctx_set_missing_side_gemm", self._h, 1 if enable else 0)
 

@@ -76,6 +76,7 @@ SIGNATURES: dict[str, list] = {
     "pg_ctx_set_fused_decode": [_P, c_int],
     "pg_ctx_set_missing_side_gemm": [_P, c_int],
     "pg_ctx_set_f64_panel": [_P, c_int],
+    "pg_ctx_set_two_limb_premask": [_P, c_int],
     "pg_ctx_set_wide_digits": [_P, c_int],
     "pg_ctx_set_basis": [_P, _P, c_int64, c_int64],
     "pg_scan": [_P, c_int, _P, c_int64, c_int64, _P],

@@ -69,6 +69,12 @@ struct AssocEpilogue {
   const long long* x_lo;
   const long long* cq_lo;
   int x_partials_only;  // 1: accumulate x_accum only (the lo level's pass), no statistics
+  // Two-limb premask (PLINK fused, THRESHOLD / TOPK): the GEMM skips the q0 limb, so it sees
+  // X' = X - sum_k q0 u. The premask widens by the rigorous bound |sum q0 u| <= ||q0_p||_2 ||u_m||_2
+  // (q0n[p] = ||q0_p||_2, ss_u[m] = sum u^2) and a candidate stores X' (int64 bits in cand_r);
+  // refine_two_limb adds sum q0 u exactly afterwards and writes the fp64 r.
+  const float* q0n;
+  const long long* ss_u;
 };
 constexpr double kLoScale = 4194304.0;  // 2^22: lo-level limbs q2 = rint((y~/s - q) 2^22), |q2| <= 2^21
 
@@ -82,6 +88,12 @@ int launch_assoc(const int8_t* qh, const int8_t* q1, const int8_t* q0, int64_t p
 int launch_assoc_packed(const int8_t* qh, const int8_t* q1, const int8_t* q0, int64_t p_pad, const uint8_t* packed,
                         int64_t pitch, int64_t n_markers, int64_t k_pad, const AssocEpilogue& ep,
                         cudaStream_t stream);
+// Candidates of a two-limb launch (ep.q0n set): cand_r holds X' (int64 bits) on entry and the
+// exact fp64 r on exit, r = s_p (X' + sum_k q0[p,k] u[m,k] - mu_m (Cq_p - Mq)) / sqrt(N V_m).
+int refine_two_limb(const unsigned long long* cand_key, double* cand_r, int64_t n, const uint8_t* packed,
+                    int64_t pitch, const int8_t* q0, int64_t k_pad, const AssocEpilogue& ep, cudaStream_t stream);
+// ||q0_p||_2 per phenotype (rounded up) for the two-limb premask bound.
+int panel_q0_norms(const int8_t* q0, int64_t p_pad, int64_t k_pad, float* out, cudaStream_t stream);
 
 // Wide-digit variant for dosage sources: one int8 plane v [c_pad, k_pad] of balanced
 // base-255 digits (rows per marker: digit0, digit1, digit2, missing mask; rows_per_marker

@@ -34,6 +34,7 @@
 //   warps 8..23   : epilogue, 4 lane quarters x 4 column groups
 #include <cuda.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 
@@ -60,7 +61,10 @@ constexpr int kTileCW = kTileCWide;
 constexpr int kHalfCW = kTileCW / 2;
 constexpr int kVBytesW = kHalfCW * kTileK;  // 5 KB
 constexpr int kRowsW = 4;                   // digits 255^0, 255^1, 255^2 + missing row
-constexpr int kPlanes = 0, kFused = 1, kWide = 2, kWide3 = 3, kWide3T = 4;
+constexpr int kPlanes = 0, kFused = 1, kWide = 2, kWide3 = 3, kWide3T = 4, kFused2 = 5;
+// kFused2: kFused without the q0 limb (two MMAs per 32 samples instead of three) for
+// THRESHOLD / TOPK scans; the premask is widened by a rigorous bound on the skipped limb and
+// the candidates are completed exactly by refine_two_limb (AssocEpilogue::q0n).
 // kWide3T (BGEN-8, transposed): genotype digit rows are the A operand (M = 256 rows per pair
 // tile = 80 markers in 32-row groups of 10 x 3 rows, see geno_planes(quartered)), the three
 // panel limbs three B tiles of N = 144 phenotypes: operand bytes per MAC are 24 % lower than
@@ -82,7 +86,8 @@ constexpr int kTmemCols = 512;
 
 template <int MODE>
 struct Cfg {
-  static constexpr bool FUSED = MODE == kFused;
+  static constexpr bool FUSED = MODE == kFused || MODE == kFused2;
+  static constexpr bool TWO = MODE == kFused2;
   static constexpr bool TRANS = MODE == kWide3T;
   static constexpr bool WIDE = MODE == kWide || MODE == kWide3 || TRANS;
   static constexpr int kStages = TRANS ? 9 : (WIDE ? 7 : 5);
@@ -97,7 +102,7 @@ struct Cfg {
   static constexpr int kStageBytes =
       TRANS ? (kVBytesWide + 3 * kTLimbBytes + 1023) / 1024 * 1024
             : (WIDE ? kOffV + (kVBytesWide + 1023) / 1024 * 1024 : (FUSED ? kOffPacked + 2048 : kOffPacked));
-  static constexpr int kPanelBytes = 3 * kQBytes;
+  static constexpr int kPanelBytes = (TWO ? 2 : 3) * kQBytes;
   static constexpr int kTmaBytes =
       TRANS ? kVBytesWide + 3 * kTLimbBytes
             : (FUSED ? kPanelBytes : (WIDE ? kOffV + kVBytesWide : kOffPacked));  // per CTA
@@ -181,6 +186,26 @@ __device__ __forceinline__ void epilogue_value(const AssocEpilogue& ep, long lon
   const float xf = static_cast<float>(xu) - mu * (cq_f - static_cast<float>(xm));
   const float r = xf * sc_f * iv;
   const float ar = fabsf(r);
+  if (ep.q0n) {
+    // two-limb premask: |r - r'| <= s ||q0_p||_2 ||u_m||_2 / sqrt(N V) (Cauchy-Schwarz), widened
+    // by 1e-4 relative against fp32 rounding; the candidate keeps X' for the exact refinement
+    const float delta = sc_f * __ldg(ep.q0n + pheno) * sqrtf(static_cast<float>(__ldg(ep.ss_u + m))) * iv * 1.0001f;
+    const bool hit2 = valid && ar + delta >= rb;
+    const uint32_t mask2 = __ballot_sync(0xffffffffu, hit2);
+    if (mask2) {
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(ep.cand_count, static_cast<unsigned long long>(__popc(mask2)));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (hit2) {
+        const unsigned long long idx = base - ep.cand_base + __popc(mask2 & lanemask_lt);
+        if (idx < static_cast<unsigned long long>(ep.cand_cap)) {
+          ep.cand_key[idx] = (static_cast<unsigned long long>(m) << 32) | static_cast<unsigned>(pheno);
+          ep.cand_r[idx] = __longlong_as_double(xu);
+        }
+      }
+    }
+    return;
+  }
   const bool hit = valid && ar >= rb;
   // same widening as the premask bar (ctx.cu rbar_kernel), doubled
   const bool near_max = valid && ep.max_abs_r != nullptr && ar >= mx.f * (1.f - 2e-5f) - 2e-7f;
@@ -488,7 +513,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
           tma_load_2d_pair(st, &tm_qh, full0, kx, prow, pol_panel);
           tma_load_2d_pair(st + kQBytes, &tm_q1, full0, kx, prow, pol_panel);
-          tma_load_2d_pair(st + 2 * kQBytes, &tm_q0, full0, kx, prow, pol_panel);
+          if constexpr (!C::TWO) tma_load_2d_pair(st + 2 * kQBytes, &tm_q0, full0, kx, prow, pol_panel);
           if constexpr (FUSED) {
             mbar_arrive_expect_tx(&pk[s], kPackedBytes);
             tma_load_2d_hint(st + kOffPacked, &tm_v, &pk[s], (kb_begin + kb) * (kTileK / 4), grow, pol_geno);
@@ -557,7 +582,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             } else {
               mma_i8_ss_pair(dH, d_qh + 2 * k, d_v + 2 * k, idesc, acc);
               mma_i8_ss_pair(dL, d_q1 + 2 * k, d_v127 + 2 * k, idesc, acc);
-              mma_i8_ss_pair(dL, d_q0 + 2 * k, d_v + 2 * k, idesc, 1);
+              if constexpr (!C::TWO) mma_i8_ss_pair(dL, d_q0 + 2 * k, d_v + 2 * k, idesc, 1);
             }
             acc = 1;
           }
@@ -787,7 +812,95 @@ int launch_assoc_packed(const int8_t* qh, const int8_t* q1, const int8_t* q0, in
   // packed rows: k_pad/4 bytes of codes per marker (rows past n_markers read as zeros by TMA)
   PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_pk, packed, k_pad / 4, n_markers, pitch, kTileK / 4, kHalfC, false));
   const int64_t c_pad = round_up(n_markers, kTileC);
+  if (ep.q0n) {
+    PG_REQUIRE(ep.full_r == nullptr && ep.max_abs_r == nullptr && ep.x_accum == nullptr && ep.ss_u != nullptr,
+               PG_ERR_INVALID, "assoc(two-limb): THRESHOLD / TOPK candidates of unsliced runs only");
+    return launch_common<kFused2>(tm_qh, tm_q1, tm_q0, tm_pk, tm_pk, p_pad, c_pad, k_pad, ep, stream);
+  }
   return launch_common<kFused>(tm_qh, tm_q1, tm_q0, tm_pk, tm_pk, p_pad, c_pad, k_pad, ep, stream);
+}
+
+namespace {
+
+// Warp per candidate: c0 = sum_k q0[p,k] u[m,k] over the packed 2-bit row (u as the GEMM
+// decodes it: 00 -> +1, 10 -> 0, 11 -> -1, 01 missing -> 0; q0 is 0 on excluded / padding
+// samples), 16 samples per lane step by DP4A; then the exact fp64 r of the candidate.
+__global__ void refine_two_limb_kernel(const unsigned long long* __restrict__ key, double* __restrict__ cand_r,
+                                       int64_t n, const uint8_t* __restrict__ packed, int64_t pitch,
+                                       const int8_t* __restrict__ q0, int64_t k_pad, AssocEpilogue ep) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  const int64_t chunks = k_pad / 16;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += warps) {
+    const unsigned long long kk = key[i];
+    const int m = static_cast<int>(kk >> 32);
+    const int p = static_cast<int>(kk & 0xffffffffull);
+    const uint32_t* row = reinterpret_cast<const uint32_t*>(packed + static_cast<int64_t>(m) * pitch);
+    const uint4* qrow = reinterpret_cast<const uint4*>(q0 + static_cast<int64_t>(p) * k_pad);
+    int acc = 0;
+    for (int64_t c = lane; c < chunks; c += 32) {
+      uint32_t u[4], u7[4];
+      decode_word(__ldg(row + c), u, u7);
+      const uint4 w = __ldg(qrow + c);
+      acc = __dp4a(static_cast<int>(w.x), static_cast<int>(u[0]), acc);
+      acc = __dp4a(static_cast<int>(w.y), static_cast<int>(u[1]), acc);
+      acc = __dp4a(static_cast<int>(w.z), static_cast<int>(u[2]), acc);
+      acc = __dp4a(static_cast<int>(w.w), static_cast<int>(u[3]), acc);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      const long long xu = __double_as_longlong(cand_r[i]) + acc;
+      long long xm = 0;
+      if (ep.side_slot) {
+        const int sl = ep.side_slot[m];
+        if (sl >= 0) xm = ep.side_x[static_cast<int64_t>(sl) * ep.side_ld + p];
+      }
+      cand_r[i] = ep.scale_d[p] * (static_cast<double>(xu) - ep.mu_d[m] * static_cast<double>(ep.cq[p] - xm)) *
+                  ep.invd_d[m];
+    }
+  }
+}
+
+__global__ void q0_norm_kernel(const int8_t* __restrict__ q0, int64_t k_pad, float* __restrict__ out) {
+  const int64_t p = blockIdx.x;
+  const uint4* row = reinterpret_cast<const uint4*>(q0 + p * k_pad);
+  unsigned long long s = 0;
+  for (int64_t c = threadIdx.x; c < k_pad / 16; c += blockDim.x) {
+    const uint4 w = row[c];
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) s += static_cast<unsigned long long>(__dp4a(static_cast<int>(ws[j]), static_cast<int>(ws[j]), 0));
+  }
+  __shared__ unsigned long long red[32];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += red[w];
+    out[p] = __double2float_ru(sqrt(static_cast<double>(t)) * (1.0 + 1e-12));
+  }
+}
+
+}  // namespace
+
+int refine_two_limb(const unsigned long long* cand_key, double* cand_r, int64_t n, const uint8_t* packed,
+                    int64_t pitch, const int8_t* q0, int64_t k_pad, const AssocEpilogue& ep, cudaStream_t stream) {
+  if (n <= 0) return PG_OK;
+  PG_REQUIRE(k_pad % 64 == 0 && pitch % 16 == 0 && pitch * 4 >= k_pad, PG_ERR_INVALID, "refine_two_limb: bad shape");
+  const int64_t warps = (n + 0);
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>((warps + 7) / 8, 148 * 16));
+  refine_two_limb_kernel<<<grid, 256, 0, stream>>>(cand_key, cand_r, n, packed, pitch, q0, k_pad, ep);
+  PG_CUDA_CHECK(cudaGetLastError());
+  return PG_OK;
+}
+
+int panel_q0_norms(const int8_t* q0, int64_t p_pad, int64_t k_pad, float* out, cudaStream_t stream) {
+  q0_norm_kernel<<<static_cast<unsigned>(p_pad), 256, 0, stream>>>(q0, k_pad, out);
+  PG_CUDA_CHECK(cudaGetLastError());
+  return PG_OK;
 }
 
 int launch_assoc_wide3t(const int8_t* qh, const int8_t* q1, const int8_t* q0, int64_t p_pad, const int8_t* v,

@@ -229,6 +229,10 @@ struct pg_ctx {
   pg::DBuf<uint8_t> full_out;
   pg::DBuf<double> scratch_a, scratch_b, scratch_c, scratch_d;
   pg::DBuf<long long> xacc, xacc_b;  // K-sliced runs (cohorts above kSliceK samples)
+  // two-limb premask of PLINK THRESHOLD / TOPK scans (pg_ctx_set_two_limb_premask): ||q0_p||_2
+  bool two_limb = true;
+  bool q0n_valid = false;
+  pg::DBuf<float> q0n;
   // F64 precision mode (pg_ctx_set_f64_panel): the panel's lo level + its partial sums
   bool f64_panel = false;
   pg::DBuf<int8_t> qh_lo, q1_lo, q0_lo;
@@ -337,6 +341,7 @@ int upload_panel_common(pg_ctx* c, const double* d_y, int64_t n_kept, int64_t n_
     pp.q0_lo = c->q0_lo.p;
     pp.cq_lo = c->cq_lo.p;
   }
+  c->q0n_valid = false;
   PG_CHECK_STATUS(
       panel_quantize(d_y, n_kept, n_pheno, ld, d_cols, c->gidx.p, c->k_pad, c->p_pad, pp, c->maxabs.p, c->stream));
   PG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
@@ -459,6 +464,14 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
                                : round_up(m * R, wide ? (R == kWideRows3 ? kTileCWide3 : kTileCWide) : kTileC);
   // PLINK rows without missing calls: the GEMM decodes the packed codes itself
   const bool fused = c->fused_decode && kind == PG_GENO_BED && R == 1;
+  // THRESHOLD / TOPK: two MMAs per 32 samples (the q0 limb deferred to the candidates)
+  const bool two_limb = fused && c->two_limb && c->mode != PG_MODE_FULL && !c->track_max_abs_r &&
+                        c->k_pad <= kSliceK && !c->f64_panel;
+  if (two_limb && !c->q0n_valid) {
+    PG_CHECK_STATUS(c->q0n.ensure(c->p_pad));
+    PG_CHECK_STATUS(panel_q0_norms(c->q0.p, c->p_pad, c->k_pad, c->q0n.p, s));
+    c->q0n_valid = true;
+  }
   int64_t launches = (kind == PG_GENO_DENSE_F64 ? 2 : 1);
   if (!fused) {
     PG_CHECK_STATUS(c->v.ensure(static_cast<size_t>(c_pad) * c->k_pad));
@@ -589,6 +602,10 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
     ep.side_slot = c->miss_slot.p;
     ep.side_ld = c->p_pad;
   }
+  if (two_limb) {
+    ep.q0n = c->q0n.p;
+    ep.ss_u = c->ss_u.p;
+  }
   PG_CHECK_STATUS(c->cand_count.ensure(1));
   ep.cand_count = c->cand_count.p;
   // exact int64 partials per (marker, phenotype): K-sliced contraction, and / or the two
@@ -654,6 +671,11 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
     }
   }
 
+  if (ncand > 0 && two_limb) {
+    // candidates hold X' = X - sum q0 u: add the deferred limb exactly, then r in fp64
+    PG_CHECK_STATUS(refine_two_limb(c->cand_key.p, c->cand_r.p, ncand, d_data, pitch, c->q0.p, c->k_pad, ep, s));
+    ++launches;
+  }
   if (ncand > 0) {
     PG_CHECK_STATUS(c->cand_key_sorted.ensure(ncand));
     PG_CHECK_STATUS(c->cand_r_sorted.ensure(ncand));
@@ -729,6 +751,7 @@ int pg_ctx_create(int device, pg_ctx** out) {
   pg_ctx* c = new pg_ctx();
   c->device = device;
   if (const char* e = std::getenv("PG_WIDE3T")) c->wide3t = std::atoi(e) != 0;
+  if (const char* e = std::getenv("PG_TWO_LIMB")) c->two_limb = std::atoi(e) != 0;
   PG_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   PG_CUDA_CHECK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
   for (auto& e : c->ev) PG_CUDA_CHECK(cudaEventCreate(&e));
@@ -1000,6 +1023,7 @@ int pg_ctx_import_panel(pg_ctx* c, const void* d_src, int64_t n_kept, int64_t n_
   PG_CHECK_STATUS(c->gidx.ensure(n_kept));
   PG_CHECK_STATUS(c->keep_bits.ensure(bits.size()));
   const uint8_t* s = static_cast<const uint8_t*>(d_src);
+  c->q0n_valid = false;
   PG_CUDA_CHECK(cudaMemcpyAsync(c->qh.p, s, plane, cudaMemcpyDeviceToDevice, c->stream));
   PG_CUDA_CHECK(cudaMemcpyAsync(c->q1.p, s + plane, plane, cudaMemcpyDeviceToDevice, c->stream));
   PG_CUDA_CHECK(cudaMemcpyAsync(c->q0.p, s + 2 * plane, plane, cudaMemcpyDeviceToDevice, c->stream));
@@ -1129,6 +1153,12 @@ int pg_ctx_debug_candidate_base(pg_ctx* c, uint64_t base) {
 int pg_ctx_set_wide_digits(pg_ctx* c, int enable) {
   PG_CHECK_STATUS(ctx_check(c));
   c->wide_digits = enable != 0;
+  return PG_OK;
+}
+
+int pg_ctx_set_two_limb_premask(pg_ctx* c, int enable) {
+  PG_CHECK_STATUS(ctx_check(c));
+  c->two_limb = enable != 0;
   return PG_OK;
 }
 
