@@ -415,7 +415,10 @@ def our_arm(a) -> None:
             traffic = None
     # hardware view: the kernel issues 3 int8 MMAs (limbs) per padded sample, exact int32 accumulation
     k_pad = (n + 63) // 64 * 64
-    int8_ops = 2.0 * 3 * k_pad * m * ((p + 127) // 128 * 128) * a.steps
+    # THRESHOLD scans of PLINK rows run two of the three panel limbs (the third is added to the
+    # candidates exactly, csrc/assoc_gemm.cu refine_two_limb); PG_TWO_LIMB=0 runs all three
+    limbs = 3 if os.environ.get("PG_TWO_LIMB", "1") == "0" else 2
+    int8_ops = 2.0 * limbs * k_pad * m * ((p + 127) // 128 * 128) * a.steps
     int8_achieved = int8_ops / (gemm_ms / 1e3) / 1e12
     int8_peak = None
     try:
@@ -521,7 +524,7 @@ def our_arm(a) -> None:
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)"},
             "hw_int8": {"achieved_tops": int8_achieved, "cublas_int8_tops_measured": int8_peak,
                         "frac": (int8_achieved / int8_peak) if int8_peak else None,
-                        "ops_def": "2 * 3 limbs * K_pad * M * P_pad per launch"},
+                        "ops_def": f"2 * {limbs} limbs * K_pad * M * P_pad per launch"},
             "decode_hbm": decode_hbm,
             "e2e": e2e,
             "cpu_baseline": cpu,
