@@ -226,7 +226,8 @@ def test_min_p_sidecar_equals_full_scan_minimum(tmp_path):
     d, y = random_dataset(rng, 300, 120, 9)
     y[:, 3] += 0.7 * d[11]
     spec, pheno, _, root = dataset(tmp_path, d, y)
-    scan(spec, pheno, root / "thr.tsv", p_threshold=1e-3, min_p_sidecar=True, device_batch=64)
+    scan(spec, pheno, root / "thr.tsv", p_threshold=1e-3, min_p_sidecar=True, device_batch=64,
+         precision=pg.Precision.F64)
     scan(spec, pheno, root / "full.bin", output_mode=pg.OutputMode.FULL, precision=pg.Precision.F64)
     t, _, names = pg.read_full_matrix(root / "full.bin")
     rows = [ln.split("\t") for ln in (root / "thr.tsv.minp.tsv").read_text().splitlines()]
