@@ -90,7 +90,11 @@ struct Cfg {
   static constexpr bool TWO = MODE == kFused2;
   static constexpr bool TRANS = MODE == kWide3T;
   static constexpr bool WIDE = MODE == kWide || MODE == kWide3 || TRANS;
-  static constexpr int kStages = TRANS ? 9 : (WIDE ? 7 : 5);
+  static constexpr int kStages = TRANS ? 9 : (WIDE ? 7 : (TWO ? 6 : 5));
+  // fused / planes stage layout: panel limbs (2 in the two-limb mode), v, 127 v, packed codes
+  static constexpr int kOffV = (TWO ? 2 : 3) * kQBytes;
+  static constexpr int kOffV127 = kOffV + kVBytes;
+  static constexpr int kOffPacked = kOffV127 + kVBytes;
   // genotype rows per pair tile; wide modes: rows per marker
   static constexpr int kTileRows = TRANS ? kTileC : (MODE == kWide3 ? kTileCWide3 : (WIDE ? kTileCW : kTileC));
   static constexpr int kHalfRows = kTileRows / 2;
@@ -101,11 +105,11 @@ struct Cfg {
   // 1 KB-aligned stages (transposed: genotype A half-tile, then the three limb B half-tiles)
   static constexpr int kStageBytes =
       TRANS ? (kVBytesWide + 3 * kTLimbBytes + 1023) / 1024 * 1024
-            : (WIDE ? kOffV + (kVBytesWide + 1023) / 1024 * 1024 : (FUSED ? kOffPacked + 2048 : kOffPacked));
+            : (WIDE ? ::pg::kOffV + (kVBytesWide + 1023) / 1024 * 1024 : (FUSED ? kOffPacked + 2048 : kOffPacked));
   static constexpr int kPanelBytes = (TWO ? 2 : 3) * kQBytes;
   static constexpr int kTmaBytes =
       TRANS ? kVBytesWide + 3 * kTLimbBytes
-            : (FUSED ? kPanelBytes : (WIDE ? kOffV + kVBytesWide : kOffPacked));  // per CTA
+            : (FUSED ? kPanelBytes : (WIDE ? ::pg::kOffV + kVBytesWide : kOffPacked));  // per CTA
   static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 512 /*barriers*/;
   static_assert(kStageBytes % 1024 == 0 && kOffV % 512 == 0, "stage / operand alignment (SW64 atoms)");
   static_assert(kTileRows % 16 == 0 && kHalfRows % 8 == 0, "UMMA N and swizzle-atom granularity");
@@ -516,12 +520,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if constexpr (!C::TWO) tma_load_2d_pair(st + 2 * kQBytes, &tm_q0, full0, kx, prow, pol_panel);
           if constexpr (FUSED) {
             mbar_arrive_expect_tx(&pk[s], kPackedBytes);
-            tma_load_2d_hint(st + kOffPacked, &tm_v, &pk[s], (kb_begin + kb) * (kTileK / 4), grow, pol_geno);
+            tma_load_2d_hint(st + C::kOffPacked, &tm_v, &pk[s], (kb_begin + kb) * (kTileK / 4), grow, pol_geno);
           } else if constexpr (WIDE) {
-            tma_load_2d_pair(st + kOffV, &tm_v, full0, kx, grow, pol_geno);
+            tma_load_2d_pair(st + ::pg::kOffV, &tm_v, full0, kx, grow, pol_geno);
           } else {
-            tma_load_2d_pair(st + kOffV, &tm_v, full0, kx, grow, pol_geno);
-            tma_load_2d_pair(st + kOffV127, &tm_v127, full0, kx, grow, pol_geno);
+            tma_load_2d_pair(st + C::kOffV, &tm_v, full0, kx, grow, pol_geno);
+            tma_load_2d_pair(st + C::kOffV127, &tm_v127, full0, kx, grow, pol_geno);
           }
           if (++s == S) {
             s = 0;
@@ -570,8 +574,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const uint64_t d_qh = umma_desc_sw64(st);
           const uint64_t d_q1 = umma_desc_sw64(st + kQBytes);
           const uint64_t d_q0 = umma_desc_sw64(st + 2 * kQBytes);
-          const uint64_t d_v = umma_desc_sw64(st + kOffV);
-          const uint64_t d_v127 = umma_desc_sw64(st + kOffV127);
+          const uint64_t d_v = umma_desc_sw64(st + (WIDE ? ::pg::kOffV : C::kOffV));
+          const uint64_t d_v127 = umma_desc_sw64(st + C::kOffV127);
 #pragma unroll
           for (int k = 0; k < kTileK / 32; ++k) {
             // +32 bytes along K inside the 64-byte swizzle row == +2 in the >>4 address field
@@ -609,15 +613,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < n_kb; ++kb) {
           mbar_wait(&pk[s], ph);
           uint8_t* st = smem + s * C::kStageBytes;
-          const uint4 w = reinterpret_cast<const uint4*>(st + kOffPacked)[r];
+          const uint4 w = reinterpret_cast<const uint4*>(st + C::kOffPacked)[r];
           const uint32_t words[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             uint32_t u[4], u7[4];
             decode_word(words[c], u, u7);
             const uint32_t off = r * 64 + ((c ^ sw) << 4);
-            *reinterpret_cast<uint4*>(st + kOffV + off) = make_uint4(u[0], u[1], u[2], u[3]);
-            *reinterpret_cast<uint4*>(st + kOffV127 + off) = make_uint4(u7[0], u7[1], u7[2], u7[3]);
+            *reinterpret_cast<uint4*>(st + C::kOffV + off) = make_uint4(u[0], u[1], u[2], u[3]);
+            *reinterpret_cast<uint4*>(st + C::kOffV127 + off) = make_uint4(u7[0], u7[1], u7[2], u7[3]);
           }
           fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the tensor core
           __syncwarp();

@@ -53,8 +53,11 @@ def test_side_gemm_equals_planes_and_oracle(share):
     any_missing = np.isnan(d[want["skip"] == 0]).any()
     assert fs.rows_per_marker == 1 and fp.rows_per_marker == (2 if np.isnan(d).any() else 1)
     assert np.array_equal(fs.t_rows, fp.t_rows)  # bitwise: both exact integer contractions
+    # THRESHOLD: the records (candidates with p <= threshold) agree bit for bit; the side path's
+    # two-limb premask may admit a few more candidates above the threshold
+    ks, kp = ts.cand_p <= 1e-2, tp.cand_p <= 1e-2
     for a in ("cand_rows", "cand_cols", "cand_r", "cand_t", "cand_p"):
-        assert np.array_equal(getattr(ts, a), getattr(tp, a))
+        assert np.array_equal(getattr(ts, a)[ks], getattr(tp, a)[kp])
     assert np.array_equal(fs.missing_count, want["missing"]) and np.array_equal(fs.skip, want["skip"])
     t_ref = orc.t_from_r(want["full_r"][want["skip"] == 0], df)
     rel = np.abs(fs.t_rows - t_ref) / np.maximum(1.0, np.abs(t_ref))
