@@ -73,9 +73,7 @@ constexpr int kTPheno = 144;                 // phenotypes per transposed pair t
 constexpr int kTHalfPheno = kTPheno / 2;     // 72 per CTA
 constexpr int kTLimbBytes = kTHalfPheno * kTileK;  // 4.5 KB per limb half-tile
 constexpr int kTMarkers = 80;                // markers per transposed pair tile
-constexpr int kEpiWarps = 16;
-constexpr int kFirstEpiWarp = 8;
-constexpr int kThreads = 32 * (kFirstEpiWarp + kEpiWarps);
+constexpr int kThreads = 768;  // 24 warps: TMA, MMA, TMEM alloc, idle, decoders, epilogue
 constexpr int kTmemCols = 512;
 // Raster (tile_coords): groups of tiles visited by the persistent grid so that one wave
 // (74 pair tiles) shares operands in L2. Measured on the C3 slice (tools/sweep_l2.sh,
@@ -91,6 +89,12 @@ struct Cfg {
   static constexpr bool TRANS = MODE == kWide3T;
   static constexpr bool WIDE = MODE == kWide || MODE == kWide3 || TRANS;
   static constexpr int kStages = TRANS ? 9 : (WIDE ? 7 : (TWO ? 6 : 5));
+  // decoder / epilogue warp split: the two-limb mainloop (512 tensor cycles per 64-sample
+  // stage instead of 768) gets 8 decoder warps, two threads per packed row
+  static constexpr int kDecWarps = TWO ? 8 : 4;
+  static constexpr int kFirstEpiWarp = 4 + kDecWarps;
+  static constexpr int kEpiWarps = kThreads / 32 - kFirstEpiWarp;
+  static constexpr int kColGroups = kEpiWarps / 4;
   // fused / planes stage layout: panel limbs (2 in the two-limb mode), v, 127 v, packed codes
   static constexpr int kOffV = (TWO ? 2 : 3) * kQBytes;
   static constexpr int kOffV127 = kOffV + kVBytes;
@@ -473,11 +477,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 2);
       mbar_init(&empty[s], 1);
-      mbar_init(&dec[s], 8);
+      mbar_init(&dec[s], 2 * C::kDecWarps);
       mbar_init(&pk[s], 1);
     }
     mbar_init(tfull, 1);
-    mbar_init(tempty, 2 * kEpiWarps);
+    mbar_init(tempty, 2 * C::kEpiWarps);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc_pair(tmem_slot, kTmemCols);
@@ -600,25 +604,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         aph ^= 1;
       }
     }
-  } else if (warp >= 4 && warp < kFirstEpiWarp) {
+  } else if (warp >= 4 && warp < C::kFirstEpiWarp) {
     if constexpr (FUSED) {
       // ------------------------------------------------------------ decoders (both CTAs)
-      // thread r expands row r of this CTA's packed half-tile: 16 bytes = 64 samples
-      // -> 64 B of v and 64 B of 127v, as 4 swizzled 16-byte chunks each
-      // (SW64: chunk c of row r lives at r*64 + ((c ^ ((r >> 1) & 3)) << 4)).
-      const int r = threadIdx.x - 128;
+      // row r of this CTA's packed half-tile (16 bytes = 64 samples) -> 64 B of v and 64 B of
+      // 127v, as 4 swizzled 16-byte chunks each (SW64: chunk c of row r lives at
+      // r*64 + ((c ^ ((r >> 1) & 3)) << 4)); kWords chunks per thread (4, or 2 with 8 warps)
+      constexpr int kWords = 4 * 4 / C::kDecWarps;
+      const int t_dec = threadIdx.x - 128;
+      const int r = t_dec / (4 / kWords);
+      const int c_first = (t_dec % (4 / kWords)) * kWords;
       const uint32_t sw = (static_cast<uint32_t>(r) >> 1) & 3u;
       uint32_t s = 0, ph = 0;
       for (int t = cid; t < n_tiles; t += n_clusters) {
         for (int kb = 0; kb < n_kb; ++kb) {
           mbar_wait(&pk[s], ph);
           uint8_t* st = smem + s * C::kStageBytes;
-          const uint4 w = reinterpret_cast<const uint4*>(st + C::kOffPacked)[r];
-          const uint32_t words[4] = {w.x, w.y, w.z, w.w};
+          uint32_t words[kWords];
+          if constexpr (kWords == 4) {
+            const uint4 w = reinterpret_cast<const uint4*>(st + C::kOffPacked)[r];
+            words[0] = w.x;
+            words[1] = w.y;
+            words[2] = w.z;
+            words[3] = w.w;
+          } else {
+            const uint2 w = reinterpret_cast<const uint2*>(st + C::kOffPacked + r * 16)[c_first >> 1];
+            words[0] = w.x;
+            words[1] = w.y;
+          }
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
+          for (int i = 0; i < kWords; ++i) {
+            const int c = c_first + i;
             uint32_t u[4], u7[4];
-            decode_word(words[c], u, u7);
+            decode_word(words[i], u, u7);
             const uint32_t off = r * 64 + ((c ^ sw) << 4);
             *reinterpret_cast<uint4*>(st + C::kOffV + off) = make_uint4(u[0], u[1], u[2], u[3]);
             *reinterpret_cast<uint4*>(st + C::kOffV127 + off) = make_uint4(u7[0], u7[1], u7[2], u7[3]);
@@ -633,13 +651,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp >= kFirstEpiWarp) {
+  } else if (warp >= C::kFirstEpiWarp) {
     // -------------------------------------------------------------- epilogue (both CTAs)
     // this CTA's TMEM holds its 128 phenotypes (lanes) x all 256 genotype rows of the
-    // pair tile (columns). Warp w reads lanes [32*(w%4), +32) (lane-quarter rule) and
-    // columns [64*cg, +64): 16 warps drain the 2 x 256 columns 4x faster.
+    // pair tile (columns). Warp w reads lanes [32*(w%4), +32) (lane-quarter rule) and one
+    // of kColGroups column ranges (16 warps: 4 groups of 64 columns; 12 warps: 3 groups).
     const int quarter = warp & 3;
-    const int cg = (warp - kFirstEpiWarp) >> 2;
+    const int cg = (warp - C::kFirstEpiWarp) >> 2;
     const uint32_t tempty0 = map_to_cta(tempty, 0);
     uint32_t aph = 0;
     for (int t = cid; t < n_tiles; t += n_clusters) {
@@ -654,7 +672,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // units in the 3-row mode, 12-column = 4 phenotype triples in the transposed mode)
       constexpr int kUnit = (MODE == kWide3 || C::TRANS) ? 12 : 16;
       constexpr int kChunks = C::kAccCols / kUnit;
-      const int c0 = kUnit * ((cg * kChunks) / 4), c1 = kUnit * (((cg + 1) * kChunks) / 4);
+      constexpr int G = C::kColGroups;
+      const int c0 = kUnit * ((cg * kChunks) / G), c1 = kUnit * (((cg + 1) * kChunks) / G);
       if constexpr (C::TRANS) {
         epilogue_tile_wide3t(ep, tH, ct, static_cast<int>(cr), pt, quarter, lane, c0, c1);
       } else if constexpr (MODE == kWide3) {
