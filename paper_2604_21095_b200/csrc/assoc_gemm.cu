@@ -89,11 +89,9 @@ struct Cfg {
   static constexpr bool TRANS = MODE == kWide3T;
   static constexpr bool WIDE = MODE == kWide || MODE == kWide3 || TRANS;
   static constexpr int kStages = TRANS ? 9 : (WIDE ? 7 : (TWO ? 6 : 5));
-  // fused decode: the packed .bed tiles (2 KB per stage) run in their own, deeper ring that a
-  // second producer (warp 3) fills ahead of the stage ring, so their TMA latency is off the
-  // decode -> MMA critical path (the decoders wait only for the stage's operand slots)
-  static constexpr int kPkDepth = FUSED ? (TWO ? 12 : 12) : 0;
-  static constexpr int kDecWarps = 4;
+  // decoder / epilogue warp split: the two-limb mainloop (512 tensor cycles per 64-sample
+  // stage instead of 768) gets 8 decoder warps, two threads per packed row
+  static constexpr int kDecWarps = TWO ? 8 : 4;
   static constexpr int kFirstEpiWarp = 4 + kDecWarps;
   static constexpr int kEpiWarps = kThreads / 32 - kFirstEpiWarp;
   static constexpr int kColGroups = kEpiWarps / 4;
@@ -111,13 +109,12 @@ struct Cfg {
   // 1 KB-aligned stages (transposed: genotype A half-tile, then the three limb B half-tiles)
   static constexpr int kStageBytes =
       TRANS ? (kVBytesWide + 3 * kTLimbBytes + 1023) / 1024 * 1024
-            : (WIDE ? ::pg::kOffV + (kVBytesWide + 1023) / 1024 * 1024 : kOffPacked);
-  static constexpr int kPkBytes = kPackedBytes;  // one packed half-tile per ring slot
+            : (WIDE ? ::pg::kOffV + (kVBytesWide + 1023) / 1024 * 1024 : (FUSED ? kOffPacked + 2048 : kOffPacked));
   static constexpr int kPanelBytes = (TWO ? 2 : 3) * kQBytes;
   static constexpr int kTmaBytes =
       TRANS ? kVBytesWide + 3 * kTLimbBytes
             : (FUSED ? kPanelBytes : (WIDE ? ::pg::kOffV + kVBytesWide : kOffPacked));  // per CTA
-  static constexpr int kSmemBytes = kStages * kStageBytes + kPkDepth * kPkBytes + 1024 /*align*/ + 1024 /*barriers*/;
+  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 512 /*barriers*/;
   static_assert(kStageBytes % 1024 == 0 && kOffV % 512 == 0, "stage / operand alignment (SW64 atoms)");
   static_assert(kTileRows % 16 == 0 && kHalfRows % 8 == 0, "UMMA N and swizzle-atom granularity");
   static_assert(kSmemBytes <= 227 * 1024, "shared memory per CTA");
@@ -453,14 +450,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   constexpr int S = C::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr int Q = C::kPkDepth;
-  uint8_t* pkring = smem + S * C::kStageBytes;                                // packed tiles (fused modes)
-  uint64_t* full = reinterpret_cast<uint64_t*>(pkring + Q * C::kPkBytes);    // leader: TMA of both CTAs
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * C::kStageBytes);  // leader: TMA of both CTAs
   uint64_t* empty = full + S;                                                // each CTA: MMA done with stage
   uint64_t* dec = empty + S;                                                 // leader: decoders of both CTAs
-  uint64_t* pkfull = dec + S;                                                // each CTA: packed slot landed
-  uint64_t* pkempty = pkfull + (Q ? Q : 1);                                  // each CTA: decoders done with slot
-  uint64_t* tfull = pkempty + (Q ? Q : 1);                                   // each CTA: accumulators ready
+  uint64_t* pk = dec + S;                                                    // each CTA: its packed tile landed
+  uint64_t* tfull = pk + S;                                                  // each CTA: accumulators ready
   uint64_t* tempty = tfull + 1;                                              // leader: both CTAs drained TMEM
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
 
@@ -484,10 +478,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&full[s], 2);
       mbar_init(&empty[s], 1);
       mbar_init(&dec[s], 2 * C::kDecWarps);
-    }
-    for (int q = 0; q < Q; ++q) {
-      mbar_init(&pkfull[q], 1);
-      mbar_init(&pkempty[q], C::kDecWarps);
+      mbar_init(&pk[s], 1);
     }
     mbar_init(tfull, 1);
     mbar_init(tempty, 2 * C::kEpiWarps);
@@ -532,7 +523,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           tma_load_2d_pair(st + kQBytes, &tm_q1, full0, kx, prow, pol_panel);
           if constexpr (!C::TWO) tma_load_2d_pair(st + 2 * kQBytes, &tm_q0, full0, kx, prow, pol_panel);
           if constexpr (FUSED) {
-            // packed codes: warp 3's ring
+            mbar_arrive_expect_tx(&pk[s], kPackedBytes);
+            tma_load_2d_hint(st + C::kOffPacked, &tm_v, &pk[s], (kb_begin + kb) * (kTileK / 4), grow, pol_geno);
           } else if constexpr (WIDE) {
             tma_load_2d_pair(st + ::pg::kOffV, &tm_v, full0, kx, grow, pol_geno);
           } else {
@@ -542,29 +534,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (++s == S) {
             s = 0;
             ph ^= 1;
-          }
-        }
-      }
-    }
-  } else if (warp == 3) {
-    if constexpr (FUSED) {
-      if (lane == 0) {
-        // ---------------------------------------------------------- packed-tile producer (both CTAs)
-        const uint64_t pol_geno = l2_policy_code((l2_codes >> 2) & 3u);
-        uint32_t q = 0, qph = 0;
-        for (int t = cid; t < n_tiles; t += n_clusters) {
-          int ct, pt;
-          tile_coords(t, n_ctile, n_ptile, group_c, ct, pt);
-          const int grow = ct * C::kTileRows + cr * C::kHalfRows;
-          for (int kb = 0; kb < n_kb; ++kb) {
-            mbar_wait(&pkempty[q], qph ^ 1);
-            mbar_arrive_expect_tx(&pkfull[q], kPackedBytes);
-            tma_load_2d_hint(pkring + q * C::kPkBytes, &tm_v, &pkfull[q], (kb_begin + kb) * (kTileK / 4), grow,
-                             pol_geno);
-            if (++q == Q) {
-              q = 0;
-              qph ^= 1;
-            }
           }
         }
       }
@@ -646,31 +615,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int r = t_dec / (4 / kWords);
       const int c_first = (t_dec % (4 / kWords)) * kWords;
       const uint32_t sw = (static_cast<uint32_t>(r) >> 1) & 3u;
-      uint32_t s = 0, ph = 0, q = 0, qph = 0;
+      uint32_t s = 0, ph = 0;
       for (int t = cid; t < n_tiles; t += n_clusters) {
         for (int kb = 0; kb < n_kb; ++kb) {
-          mbar_wait(&pkfull[q], qph);
-          const uint8_t* pkt = pkring + q * C::kPkBytes;
+          mbar_wait(&pk[s], ph);
+          uint8_t* st = smem + s * C::kStageBytes;
           uint32_t words[kWords];
           if constexpr (kWords == 4) {
-            const uint4 w = reinterpret_cast<const uint4*>(pkt)[r];
+            const uint4 w = reinterpret_cast<const uint4*>(st + C::kOffPacked)[r];
             words[0] = w.x;
             words[1] = w.y;
             words[2] = w.z;
             words[3] = w.w;
           } else {
-            const uint2 w = reinterpret_cast<const uint2*>(pkt + r * 16)[c_first >> 1];
+            const uint2 w = reinterpret_cast<const uint2*>(st + C::kOffPacked + r * 16)[c_first >> 1];
             words[0] = w.x;
             words[1] = w.y;
           }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&pkempty[q]);  // the packed slot is in registers
-          if (++q == Q) {
-            q = 0;
-            qph ^= 1;
-          }
-          mbar_wait(&empty[s], ph ^ 1);  // the MMA is done with this stage's operand slots
-          uint8_t* st = smem + s * C::kStageBytes;
 #pragma unroll
           for (int i = 0; i < kWords; ++i) {
             const int c = c_first + i;
