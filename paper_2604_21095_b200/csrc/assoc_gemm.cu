@@ -73,7 +73,8 @@ constexpr int kTPheno = 144;                 // phenotypes per transposed pair t
 constexpr int kTHalfPheno = kTPheno / 2;     // 72 per CTA
 constexpr int kTLimbBytes = kTHalfPheno * kTileK;  // 4.5 KB per limb half-tile
 constexpr int kTMarkers = 80;                // markers per transposed pair tile
-constexpr int kThreads = 768;  // 24 warps: TMA, MMA, TMEM alloc, idle, decoders, epilogue
+// warps: TMA, MMA, TMEM alloc, idle, decoders, 16 epilogue (24 warps; 28 in the two-limb mode)
+constexpr int kThreads = 768;
 constexpr int kTmemCols = 512;
 // Raster (tile_coords): groups of tiles visited by the persistent grid so that one wave
 // (74 pair tiles) shares operands in L2. Measured on the C3 slice (tools/sweep_l2.sh,
@@ -93,8 +94,9 @@ struct Cfg {
   // stage instead of 768) gets 8 decoder warps, two threads per packed row
   static constexpr int kDecWarps = TWO ? 8 : 4;
   static constexpr int kFirstEpiWarp = 4 + kDecWarps;
-  static constexpr int kEpiWarps = kThreads / 32 - kFirstEpiWarp;
+  static constexpr int kEpiWarps = 16;
   static constexpr int kColGroups = kEpiWarps / 4;
+  static constexpr int kThreadsM = 32 * (kFirstEpiWarp + kEpiWarps);  // 768, or 896 (two-limb)
   // fused / planes stage layout: panel limbs (2 in the two-limb mode), v, 127 v, packed codes
   static constexpr int kOffV = (TWO ? 2 : 3) * kQBytes;
   static constexpr int kOffV127 = kOffV + kVBytes;
@@ -439,7 +441,7 @@ __device__ __forceinline__ void epilogue_tile(const AssocEpilogue& ep, uint32_t 
 }
 
 template <int MODE>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<MODE>::kThreadsM, 1)
     assoc_i8_kernel(const __grid_constant__ CUtensorMap tm_qh, const __grid_constant__ CUtensorMap tm_q1,
                     const __grid_constant__ CUtensorMap tm_q0, const __grid_constant__ CUtensorMap tm_v,
                     const __grid_constant__ CUtensorMap tm_v127, int n_ctile, int n_ptile, int kb_begin, int n_kb,
@@ -770,7 +772,7 @@ int launch_common(const CUtensorMap& tm_qh, const CUtensorMap& tm_q1, const CUte
   constexpr int kSliceKb = static_cast<int>(kSliceK / kTileK);
   if (ep.x_accum == nullptr) {
     PG_REQUIRE(n_kb <= kSliceKb, PG_ERR_INVALID, "assoc: %d K blocks need the sliced (x_accum) path", n_kb);
-    assoc_i8_kernel<MODE><<<grid, kThreads, Cfg<MODE>::kSmemBytes, stream>>>(
+    assoc_i8_kernel<MODE><<<grid, Cfg<MODE>::kThreadsM, Cfg<MODE>::kSmemBytes, stream>>>(
         tm_qh, tm_q1, tm_q0, tm_v, tm_v127, n_ctile, n_ptile, 0, n_kb, group_c, l2_codes, ep);
   } else {
     // exact int64 partials per (marker, phenotype): K slices of one int32-exact range each
@@ -783,7 +785,7 @@ int launch_common(const CUtensorMap& tm_qh, const CUtensorMap& tm_q1, const CUte
     PG_CUDA_CHECK(cudaMemsetAsync(ep.x_accum, 0, sizeof(long long) * 2 * m_slots * p_pad, stream));
     for (int kb0 = 0; kb0 < n_kb; kb0 += kSliceKb) {
       const int nk = n_kb - kb0 < kSliceKb ? n_kb - kb0 : kSliceKb;
-      assoc_i8_kernel<MODE><<<grid, kThreads, Cfg<MODE>::kSmemBytes, stream>>>(
+      assoc_i8_kernel<MODE><<<grid, Cfg<MODE>::kThreadsM, Cfg<MODE>::kSmemBytes, stream>>>(
           tm_qh, tm_q1, tm_q0, tm_v, tm_v127, n_ctile, n_ptile, kb0, nk, group_c, l2_codes, ep);
       PG_CUDA_CHECK(cudaGetLastError());
     }
