@@ -73,7 +73,7 @@ constexpr int kTPheno = 144;                 // phenotypes per transposed pair t
 constexpr int kTHalfPheno = kTPheno / 2;     // 72 per CTA
 constexpr int kTLimbBytes = kTHalfPheno * kTileK;  // 4.5 KB per limb half-tile
 constexpr int kTMarkers = 80;                // markers per transposed pair tile
-// warps: TMA, MMA, TMEM alloc, idle, decoders, 16 epilogue (24 warps; 28 in the two-limb mode)
+// warps: TMA, MMA, TMEM alloc, idle, 4 decoders, 16 epilogue
 constexpr int kThreads = 768;
 constexpr int kTmemCols = 512;
 // Raster (tile_coords): groups of tiles visited by the persistent grid so that one wave
@@ -92,11 +92,14 @@ struct Cfg {
   static constexpr int kStages = TRANS ? 9 : (WIDE ? 7 : (TWO ? 6 : 5));
   // decoder / epilogue warp split: the two-limb mainloop (512 tensor cycles per 64-sample
   // stage instead of 768) gets 8 decoder warps, two threads per packed row
-  static constexpr int kDecWarps = TWO ? 8 : 4;
+  // decoder warps: 4 (one thread per packed row). Measured on the two-limb C3 scan: 8 decoder
+  // warps with 12 epilogue warps 2.45e10 tests/s, with 16 epilogue warps (896 threads) 2.54e10,
+  // 4 + 16 (768 threads) 2.60e10; a separate 12-deep packed-tile ring 2.50e10
+  static constexpr int kDecWarps = 4;
   static constexpr int kFirstEpiWarp = 4 + kDecWarps;
   static constexpr int kEpiWarps = 16;
   static constexpr int kColGroups = kEpiWarps / 4;
-  static constexpr int kThreadsM = 32 * (kFirstEpiWarp + kEpiWarps);  // 768, or 896 (two-limb)
+  static constexpr int kThreadsM = 32 * (kFirstEpiWarp + kEpiWarps);  // 768
   // fused / planes stage layout: panel limbs (2 in the two-limb mode), v, 127 v, packed codes
   static constexpr int kOffV = (TWO ? 2 : 3) * kQBytes;
   static constexpr int kOffV127 = kOffV + kVBytes;
