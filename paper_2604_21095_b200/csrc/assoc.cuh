@@ -75,7 +75,13 @@ struct AssocEpilogue {
   // refine_two_limb adds sum q0 u exactly afterwards and writes the fp64 r.
   const float* q0n;
   const long long* ss_u;
+  // per-marker (mu_f, invd_f, ||u_m||_2 * invd_f, 0) packed for the two-limb epilogue (one
+  // 16-byte broadcast load per marker column instead of three loads and a conversion)
+  const float4* mpack;
 };
+// (mu_f, invd_f, sqrt(ss_u) * invd_f) per marker slot [0, m_cap) for the two-limb epilogue.
+int pack_marker_terms(const float* mu_f, const float* invd_f, const long long* ss_u, int64_t m_cap, float4* out,
+                      cudaStream_t stream);
 constexpr double kLoScale = 4194304.0;  // 2^22: lo-level limbs q2 = rint((y~/s - q) 2^22), |q2| <= 2^21
 
 // Launch K2/K3 on `stream`. Panel limbs q*[p_pad, k_pad], genotype planes

@@ -389,6 +389,58 @@ __device__ __forceinline__ void epilogue_tile_wide3t(const AssocEpilogue& ep, ui
   }
 }
 
+// Two-limb tile (kFused2, THRESHOLD / TOPK): per pair only the premask test
+//   |r'| + delta >= bar,  r' = s (X' - mu (Cq - Mq)) / sqrt(N V),  delta = s ||q0_p|| ||u_m|| / sqrt(N V)
+// in fp32 (X' = kWH h + l rounded to fp32: ~3 ulp, inside the bar's 1e-5 widening), and the
+// warp-aggregated compaction of (key, exact int64 X') for the hits.
+__device__ __forceinline__ void epilogue_tile_two(const AssocEpilogue& ep, uint32_t tH, uint32_t tL, int ct, int pheno,
+                                                  int lane, int c_begin, int c_end) {
+  const uint32_t lanemask_lt = (1u << lane) - 1u;
+  const float sc_f = ep.scale_f[pheno];
+  const float cq_f = ep.cq_f[pheno];
+  const float rb = ep.rbar ? ep.rbar[pheno] : INFINITY;
+  const float dp = sc_f * __ldg(ep.q0n + pheno) * 1.0001f;  // delta = dp * (||u_m|| / sqrt(N V))
+  const int* slot = ep.side_slot;
+#pragma unroll 1
+  for (int c = c_begin; c < c_end; c += 16) {
+    uint32_t h[16], l[16];
+    tmem_ld_32x32b_x16(tH + c, h);
+    tmem_ld_32x32b_x16(tL + c, l);
+    tmem_ld_wait();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int m = ct * kTileC + c + j;
+      const float4 mk = __ldg(ep.mpack + m);  // mu, 1/sqrt(N V) (NaN: skipped / padding), ||u|| / sqrt(N V)
+      float xm_f = 0.f;
+      long long xm = 0;
+      if (slot) {
+        const int sl = __ldg(slot + m);
+        if (sl >= 0) {
+          xm = __ldg(ep.side_x + static_cast<int64_t>(sl) * ep.side_ld + pheno);
+          xm_f = static_cast<float>(xm);
+        }
+      }
+      const float xf = fmaf(static_cast<float>(static_cast<int>(h[j])), static_cast<float>(kWH),
+                            static_cast<float>(static_cast<int>(l[j]))) - mk.x * (cq_f - xm_f);
+      const bool hit = fabsf(xf * sc_f * mk.y) + dp * mk.z >= rb;
+      const uint32_t mask = __ballot_sync(0xffffffffu, hit);
+      if (mask) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(ep.cand_count, static_cast<unsigned long long>(__popc(mask)));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (hit) {
+          const unsigned long long idx = base - ep.cand_base + __popc(mask & lanemask_lt);
+          if (idx < static_cast<unsigned long long>(ep.cand_cap)) {
+            const long long xu = kWH * static_cast<long long>(static_cast<int>(h[j])) + static_cast<int>(l[j]);
+            ep.cand_key[idx] = (static_cast<unsigned long long>(m) << 32) | static_cast<unsigned>(pheno);
+            ep.cand_r[idx] = __longlong_as_double(xu);
+          }
+        }
+      }
+    }
+  }
+}
+
 template <int R>
 __device__ __forceinline__ void epilogue_tile(const AssocEpilogue& ep, uint32_t tH, uint32_t tL, int ct, int pheno,
                                               int lane, int c_begin, int c_end) {
@@ -686,7 +738,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<MODE>::kThreadsM
       } else if constexpr (WIDE) {
         epilogue_tile_wide(ep, tH, ct, pheno, lane, c0, c1);
       } else {
-        switch (ep.rows_per_marker) {
+        if constexpr (C::TWO) {
+          epilogue_tile_two(ep, tH, tL, ct, pheno, lane, c0, c1);
+        } else switch (ep.rows_per_marker) {
           case 1: epilogue_tile<1>(ep, tH, tL, ct, pheno, lane, c0, c1); break;
           case 2: epilogue_tile<2>(ep, tH, tL, ct, pheno, lane, c0, c1); break;
           case 8: epilogue_tile<8>(ep, tH, tL, ct, pheno, lane, c0, c1); break;
@@ -841,7 +895,7 @@ int launch_assoc_packed(const int8_t* qh, const int8_t* q1, const int8_t* q0, in
   PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_pk, packed, k_pad / 4, n_markers, pitch, kTileK / 4, kHalfC, false));
   const int64_t c_pad = round_up(n_markers, kTileC);
   if (ep.q0n) {
-    PG_REQUIRE(ep.full_r == nullptr && ep.max_abs_r == nullptr && ep.x_accum == nullptr && ep.ss_u != nullptr,
+    PG_REQUIRE(ep.full_r == nullptr && ep.max_abs_r == nullptr && ep.x_accum == nullptr && ep.mpack != nullptr,
                PG_ERR_INVALID, "assoc(two-limb): THRESHOLD / TOPK candidates of unsliced runs only");
     return launch_common<kFused2>(tm_qh, tm_q1, tm_q0, tm_pk, tm_pk, p_pad, c_pad, k_pad, ep, stream);
   }
@@ -921,6 +975,26 @@ int refine_two_limb(const unsigned long long* cand_key, double* cand_r, int64_t 
   const int64_t warps = (n + 0);
   const unsigned grid = static_cast<unsigned>(std::min<int64_t>((warps + 7) / 8, 148 * 16));
   refine_two_limb_kernel<<<grid, 256, 0, stream>>>(cand_key, cand_r, n, packed, pitch, q0, k_pad, ep);
+  PG_CUDA_CHECK(cudaGetLastError());
+  return PG_OK;
+}
+
+namespace {
+__global__ void pack_marker_kernel(const float* __restrict__ mu_f, const float* __restrict__ invd_f,
+                                   const long long* __restrict__ ss_u, int64_t m_cap, float4* __restrict__ out) {
+  for (int64_t m = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; m < m_cap;
+       m += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float iv = invd_f[m];
+    const float un = __fsqrt_ru(static_cast<float>(static_cast<double>(ss_u[m]) * (1.0 + 1e-7)));
+    out[m] = make_float4(mu_f[m], iv, __fmul_ru(un, iv), 0.f);
+  }
+}
+}  // namespace
+
+int pack_marker_terms(const float* mu_f, const float* invd_f, const long long* ss_u, int64_t m_cap, float4* out,
+                      cudaStream_t stream) {
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>((m_cap + 255) / 256, 2048));
+  pack_marker_kernel<<<grid, 256, 0, stream>>>(mu_f, invd_f, ss_u, m_cap, out);
   PG_CUDA_CHECK(cudaGetLastError());
   return PG_OK;
 }

@@ -233,6 +233,7 @@ struct pg_ctx {
   bool two_limb = true;
   bool q0n_valid = false;
   pg::DBuf<float> q0n;
+  pg::DBuf<float4> mpack;
   // F64 precision mode (pg_ctx_set_f64_panel): the panel's lo level + its partial sums
   bool f64_panel = false;
   pg::DBuf<int8_t> qh_lo, q1_lo, q0_lo;
@@ -605,6 +606,10 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
   if (two_limb) {
     ep.q0n = c->q0n.p;
     ep.ss_u = c->ss_u.p;
+    PG_CHECK_STATUS(c->mpack.ensure(m_cap));
+    PG_CHECK_STATUS(pack_marker_terms(c->mu_f.p, c->invd_f.p, c->ss_u.p, m_cap, c->mpack.p, s));
+    ep.mpack = c->mpack.p;
+    ++launches;
   }
   PG_CHECK_STATUS(c->cand_count.ensure(1));
   ep.cand_count = c->cand_count.p;
