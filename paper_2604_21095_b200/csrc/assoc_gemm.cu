@@ -97,7 +97,7 @@ struct Cfg {
   // 4 + 16 (768 threads) 2.60e10; a separate 12-deep packed-tile ring 2.50e10
   static constexpr int kDecWarps = 4;
   static constexpr int kFirstEpiWarp = 4 + kDecWarps;
-  static constexpr int kEpiWarps = 16;
+  static constexpr int kEpiWarps = 16;  // 20 for the two-limb tile measured no faster (2.71 vs 2.73e10)
   static constexpr int kColGroups = kEpiWarps / 4;
   static constexpr int kThreadsM = 32 * (kFirstEpiWarp + kEpiWarps);  // 768
   // fused / planes stage layout: panel limbs (2 in the two-limb mode), v, 127 v, packed codes
