@@ -78,10 +78,16 @@ struct AssocEpilogue {
   // per-marker (mu_f, invd_f, ||u_m||_2 * invd_f, 0) packed for the two-limb epilogue (one
   // 16-byte broadcast load per marker column instead of three loads and a conversion)
   const float4* mpack;
+  long long* cand_xm;  // wide two-limb candidates: X'_m (the missing row's deferred-limb sum comes later)
 };
-// (mu_f, invd_f, sqrt(ss_u) * invd_f) per marker slot [0, m_cap) for the two-limb epilogue.
-int pack_marker_terms(const float* mu_f, const float* invd_f, const long long* ss_u, int64_t m_cap, float4* out,
-                      cudaStream_t stream);
+// (mu_f, invd_f, sqrt(ss_u + mu^2 n_miss) * invd_f) per marker slot [0, m_cap) for the
+// two-limb epilogues.
+int pack_marker_terms(const float* mu_f, const double* mu_d, const float* invd_f, const long long* ss_u,
+                      const long long* n_miss, int64_t m_cap, float4* out, cudaStream_t stream);
+// Candidates of a wide two-limb launch (BGEN-8 digit planes v, 3 rows per marker): cand_r holds
+// X'_u bits and cand_xm X'_m on entry; cand_r the exact fp64 r on exit.
+int refine_wide_two(const unsigned long long* cand_key, double* cand_r, const long long* cand_xm, int64_t n,
+                    const int8_t* v, const int8_t* q0, int64_t k_pad, const AssocEpilogue& ep, cudaStream_t stream);
 constexpr double kLoScale = 4194304.0;  // 2^22: lo-level limbs q2 = rint((y~/s - q) 2^22), |q2| <= 2^21
 
 // Launch K2/K3 on `stream`. Panel limbs q*[p_pad, k_pad], genotype planes
@@ -110,6 +116,8 @@ constexpr int kWideRows = 4;
 // 144-row pair tiles (48 markers; 3 x 144 = 432 TMEM columns)
 constexpr int kTileCWide3 = 144;
 constexpr int kWideRows3 = 3;
+// two-limb BGEN-8 tiles (THRESHOLD / TOPK, q0 limb deferred): two accumulators, 240 rows
+constexpr int kTileCWide3Two = 240;
 int launch_assoc_wide(const int8_t* qh, const int8_t* q1, const int8_t* q0, int64_t p_pad, const int8_t* v,
                       int64_t c_pad, int64_t k_pad, const AssocEpilogue& ep, cudaStream_t stream);
 // BGEN-8 transposed variant: v in the quartered layout (geno_planes(quartered)), c_pad a

@@ -61,7 +61,10 @@ constexpr int kTileCW = kTileCWide;
 constexpr int kHalfCW = kTileCW / 2;
 constexpr int kVBytesW = kHalfCW * kTileK;  // 5 KB
 constexpr int kRowsW = 4;                   // digits 255^0, 255^1, 255^2 + missing row
-constexpr int kPlanes = 0, kFused = 1, kWide = 2, kWide3 = 3, kWide3T = 4, kFused2 = 5;
+constexpr int kPlanes = 0, kFused = 1, kWide = 2, kWide3 = 3, kWide3T = 4, kFused2 = 5, kWide3Two = 6;
+// kWide3Two: kWide3 (BGEN-8 digit rows) without the q0 limb: two accumulators, so the tile
+// widens to 240 rows (80 markers; kTileCWide3Two); the q0 part is added to the candidates by
+// refine_wide_two.
 // kFused2: kFused without the q0 limb (two MMAs per 32 samples instead of three) for
 // THRESHOLD / TOPK scans; the premask is widened by a rigorous bound on the skipped limb and
 // the candidates are completed exactly by refine_two_limb (AssocEpilogue::q0n).
@@ -86,10 +89,10 @@ constexpr int kTmemCols = 512;
 template <int MODE>
 struct Cfg {
   static constexpr bool FUSED = MODE == kFused || MODE == kFused2;
-  static constexpr bool TWO = MODE == kFused2;
+  static constexpr bool TWO = MODE == kFused2 || MODE == kWide3Two;  // the q0 limb is deferred
   static constexpr bool TRANS = MODE == kWide3T;
-  static constexpr bool WIDE = MODE == kWide || MODE == kWide3 || TRANS;
-  static constexpr int kStages = TRANS ? 9 : (WIDE ? 7 : (TWO ? 6 : 5));
+  static constexpr bool WIDE = MODE == kWide || MODE == kWide3 || MODE == kWide3Two || TRANS;
+  static constexpr int kStages = (TRANS || MODE == kWide3Two) ? 9 : (WIDE ? 7 : (TWO ? 6 : 5));
   // decoder / epilogue warp split: the two-limb mainloop (512 tensor cycles per 64-sample
   // stage instead of 768) gets 8 decoder warps, two threads per packed row
   // decoder warps: 4 (one thread per packed row). Measured on the two-limb C3 scan: 8 decoder
@@ -105,20 +108,22 @@ struct Cfg {
   static constexpr int kOffV127 = kOffV + kVBytes;
   static constexpr int kOffPacked = kOffV127 + kVBytes;
   // genotype rows per pair tile; wide modes: rows per marker
-  static constexpr int kTileRows = TRANS ? kTileC : (MODE == kWide3 ? kTileCWide3 : (WIDE ? kTileCW : kTileC));
+  static constexpr int kTileRows =
+      TRANS ? kTileC
+            : (MODE == kWide3 ? kTileCWide3 : (MODE == kWide3Two ? kTileCWide3Two : (WIDE ? kTileCW : kTileC)));
   static constexpr int kHalfRows = kTileRows / 2;
-  static constexpr int kWideR = (MODE == kWide3 || TRANS) ? kWideRows3 : kRowsW;
+  static constexpr int kWideR = (MODE == kWide3 || MODE == kWide3Two || TRANS) ? kWideRows3 : kRowsW;
   static constexpr int kVBytesWide = kHalfRows * kTileK;
   // accumulator width (UMMA N): genotype rows, or phenotypes in the transposed mode
   static constexpr int kAccCols = TRANS ? kTPheno : kTileRows;
   // 1 KB-aligned stages (transposed: genotype A half-tile, then the three limb B half-tiles)
   static constexpr int kStageBytes =
       TRANS ? (kVBytesWide + 3 * kTLimbBytes + 1023) / 1024 * 1024
-            : (WIDE ? ::pg::kOffV + (kVBytesWide + 1023) / 1024 * 1024 : (FUSED ? kOffPacked + 2048 : kOffPacked));
+            : (WIDE ? kOffV + (kVBytesWide + 1023) / 1024 * 1024 : (FUSED ? kOffPacked + 2048 : kOffPacked));
   static constexpr int kPanelBytes = (TWO ? 2 : 3) * kQBytes;
   static constexpr int kTmaBytes =
       TRANS ? kVBytesWide + 3 * kTLimbBytes
-            : (FUSED ? kPanelBytes : (WIDE ? ::pg::kOffV + kVBytesWide : kOffPacked));  // per CTA
+            : (FUSED ? kPanelBytes : (WIDE ? kOffV + kVBytesWide : kOffPacked));  // per CTA
   static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 512 /*barriers*/;
   static_assert(kStageBytes % 1024 == 0 && kOffV % 512 == 0, "stage / operand alignment (SW64 atoms)");
   static_assert(kTileRows % 16 == 0 && kHalfRows % 8 == 0, "UMMA N and swizzle-atom granularity");
@@ -441,6 +446,56 @@ __device__ __forceinline__ void epilogue_tile_two(const AssocEpilogue& ep, uint3
   }
 }
 
+// Two-limb BGEN-8 tile (kWide3Two): per marker rows (digit0, digit1, missing) of
+// X'_row = kWH A + 127 B; the premask as epilogue_tile_two with the bound over u and the
+// missing row (AssocEpilogue::mpack); a hit stores X'_u (cand_r bits) and X'_m (cand_xm).
+__device__ __forceinline__ void epilogue_tile_wide3two(const AssocEpilogue& ep, uint32_t tA, int ct, int pheno,
+                                                       int lane, int c_begin, int c_end) {
+  constexpr int kR = kWideRows3;
+  constexpr int kMarkersPerTile = kTileCWide3Two / kR;
+  const uint32_t lanemask_lt = (1u << lane) - 1u;
+  const float sc_f = ep.scale_f[pheno];
+  const float cq_f = ep.cq_f[pheno];
+  const float rb = ep.rbar ? ep.rbar[pheno] : INFINITY;
+  const float dp = sc_f * __ldg(ep.q0n + pheno) * 1.0001f;
+#pragma unroll 1
+  for (int c = c_begin; c < c_end; c += 12) {
+    uint32_t a[12], b[12];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      tmem_ld_32x32b_x4(tA + c + 4 * q, a + 4 * q);
+      tmem_ld_32x32b_x4(tA + kTileCWide3Two + c + 4 * q, b + 4 * q);
+    }
+    tmem_ld_wait();
+#pragma unroll
+    for (int j = 0; j < 12; j += kR) {
+      long long x[kR];
+#pragma unroll
+      for (int t = 0; t < kR; ++t)
+        x[t] = kWH * static_cast<long long>(static_cast<int>(a[j + t])) + 127ll * static_cast<int>(b[j + t]);
+      const long long xu = x[0] + 255ll * x[1];
+      const int m = ct * kMarkersPerTile + (c + j) / kR;
+      const float4 mk = __ldg(ep.mpack + m);
+      const float xf = static_cast<float>(xu) - mk.x * (cq_f - static_cast<float>(x[2]));
+      const bool hit = fabsf(xf * sc_f * mk.y) + dp * mk.z >= rb;
+      const uint32_t mask = __ballot_sync(0xffffffffu, hit);
+      if (mask) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(ep.cand_count, static_cast<unsigned long long>(__popc(mask)));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (hit) {
+          const unsigned long long idx = base - ep.cand_base + __popc(mask & lanemask_lt);
+          if (idx < static_cast<unsigned long long>(ep.cand_cap)) {
+            ep.cand_key[idx] = (static_cast<unsigned long long>(m) << 32) | static_cast<unsigned>(pheno);
+            ep.cand_r[idx] = __longlong_as_double(xu);
+            ep.cand_xm[idx] = x[2];
+          }
+        }
+      }
+    }
+  }
+}
+
 template <int R>
 __device__ __forceinline__ void epilogue_tile(const AssocEpilogue& ep, uint32_t tH, uint32_t tL, int ct, int pheno,
                                               int lane, int c_begin, int c_end) {
@@ -583,7 +638,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<MODE>::kThreadsM
             mbar_arrive_expect_tx(&pk[s], kPackedBytes);
             tma_load_2d_hint(st + C::kOffPacked, &tm_v, &pk[s], (kb_begin + kb) * (kTileK / 4), grow, pol_geno);
           } else if constexpr (WIDE) {
-            tma_load_2d_pair(st + ::pg::kOffV, &tm_v, full0, kx, grow, pol_geno);
+            tma_load_2d_pair(st + C::kOffV, &tm_v, full0, kx, grow, pol_geno);
           } else {
             tma_load_2d_pair(st + C::kOffV, &tm_v, full0, kx, grow, pol_geno);
             tma_load_2d_pair(st + C::kOffV127, &tm_v127, full0, kx, grow, pol_geno);
@@ -635,7 +690,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<MODE>::kThreadsM
           const uint64_t d_qh = umma_desc_sw64(st);
           const uint64_t d_q1 = umma_desc_sw64(st + kQBytes);
           const uint64_t d_q0 = umma_desc_sw64(st + 2 * kQBytes);
-          const uint64_t d_v = umma_desc_sw64(st + (WIDE ? ::pg::kOffV : C::kOffV));
+          const uint64_t d_v = umma_desc_sw64(st + C::kOffV);
           const uint64_t d_v127 = umma_desc_sw64(st + C::kOffV127);
 #pragma unroll
           for (int k = 0; k < kTileK / 32; ++k) {
@@ -643,7 +698,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<MODE>::kThreadsM
             if constexpr (WIDE) {
               mma_i8_ss_pair(dH, d_qh + 2 * k, d_v + 2 * k, idesc, acc);
               mma_i8_ss_pair(dL, d_q1 + 2 * k, d_v + 2 * k, idesc, acc);
-              mma_i8_ss_pair(dC, d_q0 + 2 * k, d_v + 2 * k, idesc, acc);
+              if constexpr (!C::TWO) mma_i8_ss_pair(dC, d_q0 + 2 * k, d_v + 2 * k, idesc, acc);
             } else {
               mma_i8_ss_pair(dH, d_qh + 2 * k, d_v + 2 * k, idesc, acc);
               mma_i8_ss_pair(dL, d_q1 + 2 * k, d_v127 + 2 * k, idesc, acc);
@@ -727,12 +782,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<MODE>::kThreadsM
       const uint32_t tL = tH + C::kAccCols;
       // split the tile's 16-column chunks over the 4 column groups (12-column = 4-marker
       // units in the 3-row mode, 12-column = 4 phenotype triples in the transposed mode)
-      constexpr int kUnit = (MODE == kWide3 || C::TRANS) ? 12 : 16;
+      constexpr int kUnit = (MODE == kWide3 || MODE == kWide3Two || C::TRANS) ? 12 : 16;
       constexpr int kChunks = C::kAccCols / kUnit;
       constexpr int G = C::kColGroups;
       const int c0 = kUnit * ((cg * kChunks) / G), c1 = kUnit * (((cg + 1) * kChunks) / G);
       if constexpr (C::TRANS) {
         epilogue_tile_wide3t(ep, tH, ct, static_cast<int>(cr), pt, quarter, lane, c0, c1);
+      } else if constexpr (MODE == kWide3Two) {
+        epilogue_tile_wide3two(ep, tH, ct, pheno, lane, c0, c1);
       } else if constexpr (MODE == kWide3) {
         epilogue_tile_wide3(ep, tH, ct, pheno, lane, c0, c1);
       } else if constexpr (WIDE) {
@@ -980,21 +1037,85 @@ int refine_two_limb(const unsigned long long* cand_key, double* cand_r, int64_t 
 }
 
 namespace {
-__global__ void pack_marker_kernel(const float* __restrict__ mu_f, const float* __restrict__ invd_f,
-                                   const long long* __restrict__ ss_u, int64_t m_cap, float4* __restrict__ out) {
+// ||u_m + mu_m mask_m||_2 = sqrt(sum u^2 + mu^2 n_miss) (u = 0 on missing calls) bounds what the
+// deferred limb can add to X - mu (Cq - Mq) when Mq is deferred too (wide two-limb tiles), and
+// bounds it from above when Mq is exact (the PLINK side GEMM)
+__global__ void pack_marker_kernel(const float* __restrict__ mu_f, const double* __restrict__ mu_d,
+                                   const float* __restrict__ invd_f, const long long* __restrict__ ss_u,
+                                   const long long* __restrict__ n_miss, int64_t m_cap, float4* __restrict__ out) {
   for (int64_t m = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; m < m_cap;
        m += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const float iv = invd_f[m];
-    const float un = __fsqrt_ru(static_cast<float>(static_cast<double>(ss_u[m]) * (1.0 + 1e-7)));
+    const double mu = mu_d[m];
+    const double sq = static_cast<double>(ss_u[m]) + mu * mu * static_cast<double>(n_miss[m]);
+    const float un = __fsqrt_ru(static_cast<float>(sq * (1.0 + 1e-7)));
     out[m] = make_float4(mu_f[m], iv, __fmul_ru(un, iv), 0.f);
+  }
+}
+
+// Warp per wide two-limb candidate: the q0 limb against the marker's digit rows (u = d0 + 255 d1)
+// and missing row, by DP4A over the int8 planes; then the exact fp64 r.
+__global__ void refine_wide_two_kernel(const unsigned long long* __restrict__ key, double* __restrict__ cand_r,
+                                       const long long* __restrict__ cand_xm, int64_t n, const int8_t* __restrict__ v,
+                                       const int8_t* __restrict__ q0, int64_t k_pad, AssocEpilogue ep) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  const int64_t chunks = k_pad / 16;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += warps) {
+    const unsigned long long kk = key[i];
+    const int64_t m = static_cast<int64_t>(kk >> 32);
+    const int p = static_cast<int>(kk & 0xffffffffull);
+    const uint4* r0 = reinterpret_cast<const uint4*>(v + (3 * m) * k_pad);
+    const uint4* r1 = reinterpret_cast<const uint4*>(v + (3 * m + 1) * k_pad);
+    const uint4* r2 = reinterpret_cast<const uint4*>(v + (3 * m + 2) * k_pad);
+    const uint4* qrow = reinterpret_cast<const uint4*>(q0 + static_cast<int64_t>(p) * k_pad);
+    int d0 = 0, d1 = 0, dm = 0;
+    for (int64_t c = lane; c < chunks; c += 32) {
+      const uint4 w = __ldg(qrow + c);
+      const uint4 a = __ldg(r0 + c), b = __ldg(r1 + c), z = __ldg(r2 + c);
+      d0 = __dp4a(static_cast<int>(w.x), static_cast<int>(a.x), d0);
+      d0 = __dp4a(static_cast<int>(w.y), static_cast<int>(a.y), d0);
+      d0 = __dp4a(static_cast<int>(w.z), static_cast<int>(a.z), d0);
+      d0 = __dp4a(static_cast<int>(w.w), static_cast<int>(a.w), d0);
+      d1 = __dp4a(static_cast<int>(w.x), static_cast<int>(b.x), d1);
+      d1 = __dp4a(static_cast<int>(w.y), static_cast<int>(b.y), d1);
+      d1 = __dp4a(static_cast<int>(w.z), static_cast<int>(b.z), d1);
+      d1 = __dp4a(static_cast<int>(w.w), static_cast<int>(b.w), d1);
+      dm = __dp4a(static_cast<int>(w.x), static_cast<int>(z.x), dm);
+      dm = __dp4a(static_cast<int>(w.y), static_cast<int>(z.y), dm);
+      dm = __dp4a(static_cast<int>(w.z), static_cast<int>(z.z), dm);
+      dm = __dp4a(static_cast<int>(w.w), static_cast<int>(z.w), dm);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      d0 += __shfl_xor_sync(0xffffffffu, d0, o);
+      d1 += __shfl_xor_sync(0xffffffffu, d1, o);
+      dm += __shfl_xor_sync(0xffffffffu, dm, o);
+    }
+    if (lane == 0) {
+      const long long xu = __double_as_longlong(cand_r[i]) + d0 + 255ll * d1;
+      const long long xm = cand_xm[i] + dm;
+      cand_r[i] = ep.scale_d[p] * (static_cast<double>(xu) - ep.mu_d[m] * static_cast<double>(ep.cq[p] - xm)) *
+                  ep.invd_d[m];
+    }
   }
 }
 }  // namespace
 
-int pack_marker_terms(const float* mu_f, const float* invd_f, const long long* ss_u, int64_t m_cap, float4* out,
-                      cudaStream_t stream) {
+int refine_wide_two(const unsigned long long* cand_key, double* cand_r, const long long* cand_xm, int64_t n,
+                    const int8_t* v, const int8_t* q0, int64_t k_pad, const AssocEpilogue& ep, cudaStream_t stream) {
+  if (n <= 0) return PG_OK;
+  PG_REQUIRE(k_pad % 64 == 0, PG_ERR_INVALID, "refine_wide_two: bad shape");
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>((n + 7) / 8, 148 * 16));
+  refine_wide_two_kernel<<<grid, 256, 0, stream>>>(cand_key, cand_r, cand_xm, n, v, q0, k_pad, ep);
+  PG_CUDA_CHECK(cudaGetLastError());
+  return PG_OK;
+}
+
+int pack_marker_terms(const float* mu_f, const double* mu_d, const float* invd_f, const long long* ss_u,
+                      const long long* n_miss, int64_t m_cap, float4* out, cudaStream_t stream) {
   const unsigned grid = static_cast<unsigned>(std::min<int64_t>((m_cap + 255) / 256, 2048));
-  pack_marker_kernel<<<grid, 256, 0, stream>>>(mu_f, invd_f, ss_u, m_cap, out);
+  pack_marker_kernel<<<grid, 256, 0, stream>>>(mu_f, mu_d, invd_f, ss_u, n_miss, m_cap, out);
   PG_CUDA_CHECK(cudaGetLastError());
   return PG_OK;
 }
@@ -1026,13 +1147,20 @@ int launch_assoc_wide(const int8_t* qh, const int8_t* q1, const int8_t* q0, int6
   const int R = ep.rows_per_marker;
   PG_REQUIRE(R == kRowsW || R == kWideRows3, PG_ERR_INVALID, "assoc(wide): rows_per_marker must be 3 or 4, got %d",
              R);
-  const int tile = R == kWideRows3 ? kTileCWide3 : kTileCW;
+  const int tile = R == kWideRows3 ? (ep.q0n ? kTileCWide3Two : kTileCWide3) : kTileCW;
   PG_REQUIRE(p_pad % kTileP == 0 && c_pad % tile == 0 && k_pad % kTileK == 0 && p_pad > 0 && c_pad > 0 &&
                  k_pad > 0,
              PG_ERR_INVALID, "assoc(wide): bad padded shape p=%lld c=%lld k=%lld", (long long)p_pad,
              (long long)c_pad, (long long)k_pad);
   CUtensorMap tm_qh, tm_q1, tm_q0, tm_v;
   PG_CHECK_STATUS(encode_panel(qh, q1, q0, p_pad, k_pad, tm_qh, tm_q1, tm_q0));
+  if (R == kWideRows3 && ep.q0n) {  // two-limb premask: 240-row tiles
+    PG_REQUIRE(c_pad % kTileCWide3Two == 0 && ep.full_r == nullptr && ep.max_abs_r == nullptr && ep.x_accum == nullptr &&
+                   ep.mpack != nullptr && ep.cand_xm != nullptr,
+               PG_ERR_INVALID, "assoc(wide, two-limb): bad arguments");
+    PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_v, v, k_pad, c_pad, k_pad, kTileK, kTileCWide3Two / 2));
+    return launch_common<kWide3Two>(tm_qh, tm_q1, tm_q0, tm_v, tm_v, p_pad, c_pad, k_pad, ep, stream);
+  }
   PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_v, v, k_pad, c_pad, k_pad, kTileK, tile / 2));
   if (R == kWideRows3) return launch_common<kWide3>(tm_qh, tm_q1, tm_q0, tm_v, tm_v, p_pad, c_pad, k_pad, ep, stream);
   return launch_common<kWide>(tm_qh, tm_q1, tm_q0, tm_v, tm_v, p_pad, c_pad, k_pad, ep, stream);

@@ -234,6 +234,7 @@ struct pg_ctx {
   bool q0n_valid = false;
   pg::DBuf<float> q0n;
   pg::DBuf<float4> mpack;
+  pg::DBuf<long long> cand_xm;
   // F64 precision mode (pg_ctx_set_f64_panel): the panel's lo level + its partial sums
   bool f64_panel = false;
   pg::DBuf<int8_t> qh_lo, q1_lo, q0_lo;
@@ -391,7 +392,7 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
   b.ploidy_off = ploidy_off;
 
   // marker slots for any tiling: ternary tiles hold 256 / R markers, wide tiles 40
-  const int64_t m_cap = round_up(m, 256) + 64;
+  const int64_t m_cap = round_up(m, 256) + 256;
   PG_CHECK_STATUS(c->flags.ensure(2));
   PG_CUDA_CHECK(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * 2, s));
   int hflags[2] = {0, 0};
@@ -461,13 +462,17 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
   // the extension-mode side GEMM or the per-phenotype max |r| (kept on the kWide3 kernel)
   const bool wide3t = R == kWideRows3 && c->wide3t && c->k_pad <= kSliceK && !c->have_basis && !c->track_max_abs_r &&
                       !c->f64_panel;
-  const int64_t c_pad = wide3t ? round_up((m + 9) / 10 * 32, kTileC)
-                               : round_up(m * R, wide ? (R == kWideRows3 ? kTileCWide3 : kTileCWide) : kTileC);
   // PLINK rows without missing calls: the GEMM decodes the packed codes itself
   const bool fused = c->fused_decode && kind == PG_GENO_BED && R == 1;
-  // THRESHOLD / TOPK: two MMAs per 32 samples (the q0 limb deferred to the candidates)
-  const bool two_limb = fused && c->two_limb && c->mode != PG_MODE_FULL && !c->track_max_abs_r &&
-                        c->k_pad <= kSliceK && !c->f64_panel;
+  // THRESHOLD / TOPK: two MMAs per 32 samples (the q0 limb deferred to the candidates), for the
+  // fused PLINK GEMM and the BGEN-8 wide GEMM (whose tile then widens to 240 rows)
+  const bool two_limb_ok =
+      c->two_limb && c->mode != PG_MODE_FULL && !c->track_max_abs_r && c->k_pad <= kSliceK && !c->f64_panel;
+  const bool wide_two = two_limb_ok && R == kWideRows3 && !wide3t && !c->have_basis;
+  const bool two_limb = two_limb_ok && (fused || wide_two);
+  const int64_t c_pad =
+      wide3t ? round_up((m + 9) / 10 * 32, kTileC)
+             : round_up(m * R, wide ? (R == kWideRows3 ? (wide_two ? kTileCWide3Two : kTileCWide3) : kTileCWide) : kTileC);
   if (two_limb && !c->q0n_valid) {
     PG_CHECK_STATUS(c->q0n.ensure(c->p_pad));
     PG_CHECK_STATUS(panel_q0_norms(c->q0.p, c->p_pad, c->k_pad, c->q0n.p, s));
@@ -606,8 +611,8 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
   if (two_limb) {
     ep.q0n = c->q0n.p;
     ep.ss_u = c->ss_u.p;
-    PG_CHECK_STATUS(c->mpack.ensure(m_cap));
-    PG_CHECK_STATUS(pack_marker_terms(c->mu_f.p, c->invd_f.p, c->ss_u.p, m_cap, c->mpack.p, s));
+    PG_CHECK_STATUS(c->mpack.ensure(m_cap));  // m_cap covers every marker slot of the tiles
+    PG_CHECK_STATUS(pack_marker_terms(c->mu_f.p, c->mu_d.p, c->invd_f.p, c->ss_u.p, c->n_miss.p, m_cap, c->mpack.p, s));
     ep.mpack = c->mpack.p;
     ++launches;
   }
@@ -644,8 +649,10 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
         PG_CHECK_STATUS(c->cand_r.ensure(1 << 20));
         c->cand_capacity = 1 << 20;
       }
+      if (wide_two) PG_CHECK_STATUS(c->cand_xm.ensure(c->cand_capacity));
       ep.cand_key = c->cand_key.p;
       ep.cand_r = c->cand_r.p;
+      ep.cand_xm = wide_two ? c->cand_xm.p : nullptr;
       ep.cand_cap = c->cand_capacity;
       ep.cand_base = c->cand_base;
       // the 64-bit counter starts at cand_base (0 except under the test hook); slots are
@@ -678,7 +685,10 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
 
   if (ncand > 0 && two_limb) {
     // candidates hold X' = X - sum q0 u: add the deferred limb exactly, then r in fp64
-    PG_CHECK_STATUS(refine_two_limb(c->cand_key.p, c->cand_r.p, ncand, d_data, pitch, c->q0.p, c->k_pad, ep, s));
+    if (wide_two)
+      PG_CHECK_STATUS(refine_wide_two(c->cand_key.p, c->cand_r.p, c->cand_xm.p, ncand, c->v.p, c->q0.p, c->k_pad, ep, s));
+    else
+      PG_CHECK_STATUS(refine_two_limb(c->cand_key.p, c->cand_r.p, ncand, d_data, pitch, c->q0.p, c->k_pad, ep, s));
     ++launches;
   }
   if (ncand > 0) {

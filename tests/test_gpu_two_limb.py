@@ -79,3 +79,33 @@ def test_two_limb_candidates_match_oracle():
     assert a.n_candidates >= b.n_candidates  # the widened premask admits a few more pairs
     assert np.array_equal(a.cand_rows[ka], want["rows"]) and np.array_equal(a.cand_cols[ka], want["cols"])
     np.testing.assert_allclose(a.cand_t[ka], want["t"], rtol=1e-4)
+
+
+@pytest.mark.parametrize("mode", ["thr", "topk"])
+def test_wide_two_limb_bgen8_equals_three_limb_bitwise(mode, tmp_path, monkeypatch):
+    """BGEN-8 through the 240-row two-limb wide GEMM (kWide3Two, deferred q0 limb for the digit
+    rows and the missing row) == the three-limb kWide3 GEMM, record for record."""
+    from bgen_fixture import write_bgen
+    from conftest_helpers import write_tsv
+
+    rng = np.random.default_rng(29)
+    n, m, k = 333, 500, 12
+    ids = [f"S{i + 1}" for i in range(n)]
+    af = rng.uniform(0.02, 0.9, m)
+    d = rng.binomial(2, af[:, None], size=(m, n)).astype(np.float64)
+    frac = rng.random((m, n)) < 0.3
+    d[frac] = np.clip(d[frac] + rng.normal(0, 0.3, frac.sum()), 0, 2)
+    d[rng.random((m, n)) < 0.05] = np.nan
+    y = rng.standard_normal((n, k))
+    y[:, 3] += 0.4 * np.nan_to_num(d[7], nan=1.0)
+    pheno = write_tsv(tmp_path / "p.tsv", ids, [f"ph{j + 1}" for j in range(k)], y)
+    spec = pg.SourceSpec(pg.GenotypeFormat.BGEN, bgen_path=write_bgen(tmp_path / "g.bgen", d, ids, bits=8))
+    kw = dict(p_threshold=0.02) if mode == "thr" else dict(output_mode=pg.OutputMode.TOPK, top_k=9)
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("PG_TWO_LIMB", flag)
+        path = tmp_path / f"o{flag}.tsv"
+        pg.run_scan(pg.ScanConfig(source=spec, pheno_path=pheno, out_path=path, summary_to_stderr=False,
+                                  device_batch=300, **kw))
+        out[flag] = path.read_bytes()
+    assert out["1"] == out["0"] and out["1"].count(b"\n") > 1
