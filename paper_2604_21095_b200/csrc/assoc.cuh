@@ -79,6 +79,7 @@ struct AssocEpilogue {
   // 16-byte broadcast load per marker column instead of three loads and a conversion)
   const float4* mpack;
   long long* cand_xm;  // wide two-limb candidates: X'_m (the missing row's deferred-limb sum comes later)
+  int side_two;        // the side GEMM ran two limbs: side_x holds Mq' (refine_two_limb adds sum_missing q0)
 };
 // (mu_f, invd_f, sqrt(ss_u + mu^2 n_miss) * invd_f) per marker slot [0, m_cap) for the
 // two-limb epilogues.

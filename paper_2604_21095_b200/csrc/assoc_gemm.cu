@@ -61,7 +61,9 @@ constexpr int kTileCW = kTileCWide;
 constexpr int kHalfCW = kTileCW / 2;
 constexpr int kVBytesW = kHalfCW * kTileK;  // 5 KB
 constexpr int kRowsW = 4;                   // digits 255^0, 255^1, 255^2 + missing row
-constexpr int kPlanes = 0, kFused = 1, kWide = 2, kWide3 = 3, kWide3T = 4, kFused2 = 5, kWide3Two = 6;
+constexpr int kPlanes = 0, kFused = 1, kWide = 2, kWide3 = 3, kWide3T = 4, kFused2 = 5, kWide3Two = 6, kPlanes2 = 7;
+// kPlanes2: kPlanes without the q0 limb (the missing-call side GEMM of a two-limb scan: its
+// Mq' is completed per candidate by refine_two_limb).
 // kWide3Two: kWide3 (BGEN-8 digit rows) without the q0 limb: two accumulators, so the tile
 // widens to 240 rows (80 markers; kTileCWide3Two); the q0 part is added to the candidates by
 // refine_wide_two.
@@ -89,7 +91,7 @@ constexpr int kTmemCols = 512;
 template <int MODE>
 struct Cfg {
   static constexpr bool FUSED = MODE == kFused || MODE == kFused2;
-  static constexpr bool TWO = MODE == kFused2 || MODE == kWide3Two;  // the q0 limb is deferred
+  static constexpr bool TWO = MODE == kFused2 || MODE == kWide3Two || MODE == kPlanes2;  // q0 limb deferred
   static constexpr bool TRANS = MODE == kWide3T;
   static constexpr bool WIDE = MODE == kWide || MODE == kWide3 || MODE == kWide3Two || TRANS;
   static constexpr int kStages = (TRANS || MODE == kWide3Two) ? 9 : (WIDE ? 7 : (TWO ? 6 : 5));
@@ -181,6 +183,16 @@ __device__ __forceinline__ void decode_word(uint32_t w, uint32_t (&u)[4], uint32
     u[i] = __byte_perm(kLutU, 0u, sel[i]);
     u127[i] = __byte_perm(kLutU127, 0u, sel[i]);
   }
+}
+
+// 16 packed codes -> 16 int8 missing flags (code 01 -> 1, else 0), as decode_word's layout.
+__device__ __forceinline__ void decode_word_missing(uint32_t w, uint32_t (&mk)[4]) {
+  constexpr uint32_t kLutMiss = 0x00000100u;  // bytes for codes 0,1,2,3: 0, 1, 0, 0
+  const uint32_t n_lo = codes_to_nibbles(w);
+  const uint32_t n_hi = codes_to_nibbles(w >> 16);
+  const uint32_t sel[4] = {n_lo & 0xFFFFu, n_lo >> 16, n_hi & 0xFFFFu, n_hi >> 16};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) mk[i] = __byte_perm(kLutMiss, 0u, sel[i]);
 }
 
 // Running per-phenotype max |r| (min-p sidecar, only when ep.max_abs_r is set): the fp32
@@ -795,7 +807,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<MODE>::kThreadsM
       } else if constexpr (WIDE) {
         epilogue_tile_wide(ep, tH, ct, pheno, lane, c0, c1);
       } else {
-        if constexpr (C::TWO) {
+        if constexpr (MODE == kFused2) {
           epilogue_tile_two(ep, tH, tL, ct, pheno, lane, c0, c1);
         } else switch (ep.rows_per_marker) {
           case 1: epilogue_tile<1>(ep, tH, tL, ct, pheno, lane, c0, c1); break;
@@ -936,6 +948,11 @@ int launch_assoc(const int8_t* qh, const int8_t* q1, const int8_t* q0, int64_t p
   PG_CHECK_STATUS(encode_panel(qh, q1, q0, p_pad, k_pad, tm_qh, tm_q1, tm_q0));
   PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_v, v, k_pad, c_pad, k_pad, kTileK, kHalfC));
   PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_v127, v127, k_pad, c_pad, k_pad, kTileK, kHalfC));
+  if (ep.q0n) {  // two-limb side GEMM (Mq' only): the candidates get sum_missing q0 later
+    PG_REQUIRE(ep.side_out != nullptr && ep.rows_per_marker == 1 && ep.x_accum == nullptr, PG_ERR_INVALID,
+               "assoc(planes, two-limb): side GEMMs only");
+    return launch_common<kPlanes2>(tm_qh, tm_q1, tm_q0, tm_v, tm_v127, p_pad, c_pad, k_pad, ep, stream);
+  }
   return launch_common<kPlanes>(tm_qh, tm_q1, tm_q0, tm_v, tm_v127, p_pad, c_pad, k_pad, ep, stream);
 }
 
@@ -976,24 +993,38 @@ __global__ void refine_two_limb_kernel(const unsigned long long* __restrict__ ke
     const int p = static_cast<int>(kk & 0xffffffffull);
     const uint32_t* row = reinterpret_cast<const uint32_t*>(packed + static_cast<int64_t>(m) * pitch);
     const uint4* qrow = reinterpret_cast<const uint4*>(q0 + static_cast<int64_t>(p) * k_pad);
-    int acc = 0;
+    // with a two-limb side GEMM (side_two) the missing calls' q0 sum is deferred too
+    const bool side_two = ep.side_slot != nullptr && ep.side_two && ep.side_slot[m] >= 0;
+    int acc = 0, acc_m = 0;
     for (int64_t c = lane; c < chunks; c += 32) {
       uint32_t u[4], u7[4];
-      decode_word(__ldg(row + c), u, u7);
+      const uint32_t word = __ldg(row + c);
+      decode_word(word, u, u7);
       const uint4 w = __ldg(qrow + c);
       acc = __dp4a(static_cast<int>(w.x), static_cast<int>(u[0]), acc);
       acc = __dp4a(static_cast<int>(w.y), static_cast<int>(u[1]), acc);
       acc = __dp4a(static_cast<int>(w.z), static_cast<int>(u[2]), acc);
       acc = __dp4a(static_cast<int>(w.w), static_cast<int>(u[3]), acc);
+      if (side_two) {
+        uint32_t mk[4];
+        decode_word_missing(word, mk);
+        acc_m = __dp4a(static_cast<int>(w.x), static_cast<int>(mk[0]), acc_m);
+        acc_m = __dp4a(static_cast<int>(w.y), static_cast<int>(mk[1]), acc_m);
+        acc_m = __dp4a(static_cast<int>(w.z), static_cast<int>(mk[2]), acc_m);
+        acc_m = __dp4a(static_cast<int>(w.w), static_cast<int>(mk[3]), acc_m);
+      }
     }
 #pragma unroll
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    for (int o = 16; o; o >>= 1) {
+      acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      acc_m += __shfl_xor_sync(0xffffffffu, acc_m, o);
+    }
     if (lane == 0) {
       const long long xu = __double_as_longlong(cand_r[i]) + acc;
       long long xm = 0;
       if (ep.side_slot) {
         const int sl = ep.side_slot[m];
-        if (sl >= 0) xm = ep.side_x[static_cast<int64_t>(sl) * ep.side_ld + p];
+        if (sl >= 0) xm = ep.side_x[static_cast<int64_t>(sl) * ep.side_ld + p] + acc_m;
       }
       cand_r[i] = ep.scale_d[p] * (static_cast<double>(xu) - ep.mu_d[m] * static_cast<double>(ep.cq[p] - xm)) *
                   ep.invd_d[m];

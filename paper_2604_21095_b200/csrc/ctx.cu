@@ -520,6 +520,7 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
     es.cq_f = c->cq_f.p;
     es.cq = c->cq.p;
     es.side_ld = c->p_pad;
+    if (two_limb) es.q0n = c->q0n.p;  // two-limb scans: the side GEMM defers q0 as well
     ++launches;
     if (level == 1) {  // side_x_lo was sized with the other side buffers (its pointer is already in use)
       es.side_out = c->side_x_lo.p;
@@ -607,6 +608,7 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
     ep.side_x = c->side_x.p;
     ep.side_slot = c->miss_slot.p;
     ep.side_ld = c->p_pad;
+    ep.side_two = two_limb ? 1 : 0;
   }
   if (two_limb) {
     ep.q0n = c->q0n.p;
