@@ -69,14 +69,14 @@ struct AssocEpilogue {
   const long long* x_lo;
   const long long* cq_lo;
   int x_partials_only;  // 1: accumulate x_accum only (the lo level's pass), no statistics
-  // Two-limb premask (PLINK fused, THRESHOLD / TOPK): the GEMM skips the q0 limb, so it sees
-  // X' = X - sum_k q0 u. The premask widens by the rigorous bound |sum q0 u| <= ||q0_p||_2 ||u_m||_2
-  // (q0n[p] = ||q0_p||_2, ss_u[m] = sum u^2) and a candidate stores X' (int64 bits in cand_r);
-  // refine_two_limb adds sum q0 u exactly afterwards and writes the fp64 r.
+  // Two-limb premask (THRESHOLD / TOPK; kFused2, kWide3Two, kPlanes2 side GEMMs): the GEMM
+  // skips the q0 limb, so it sees X' = X - sum_k q0 (u + mu mask) terms. The premask widens by
+  // the rigorous bound |sum q0 (u + mu mask)| <= ||q0_p||_2 ||u_m + mu_m mask_m||_2
+  // (q0n[p] = ||q0_p||_2; mpack[m] = (mu_f, invd_f, ||u_m + mu_m mask_m||_2 invd_f, 0), one
+  // 16-byte broadcast load per marker column) and a candidate stores X' (int64 bits in cand_r);
+  // refine_two_limb / refine_wide_two add the q0 sums exactly afterwards and write the fp64 r.
+  // A non-null q0n selects the two-limb kernels.
   const float* q0n;
-  const long long* ss_u;
-  // per-marker (mu_f, invd_f, ||u_m||_2 * invd_f, 0) packed for the two-limb epilogue (one
-  // 16-byte broadcast load per marker column instead of three loads and a conversion)
   const float4* mpack;
   long long* cand_xm;  // wide two-limb candidates: X'_m (the missing row's deferred-limb sum comes later)
   int side_two;        // the side GEMM ran two limbs: side_x holds Mq' (refine_two_limb adds sum_missing q0)

@@ -216,26 +216,6 @@ __device__ __forceinline__ void epilogue_value(const AssocEpilogue& ep, long lon
   const float xf = static_cast<float>(xu) - mu * (cq_f - static_cast<float>(xm));
   const float r = xf * sc_f * iv;
   const float ar = fabsf(r);
-  if (ep.q0n) {
-    // two-limb premask: |r - r'| <= s ||q0_p||_2 ||u_m||_2 / sqrt(N V) (Cauchy-Schwarz), widened
-    // by 1e-4 relative against fp32 rounding; the candidate keeps X' for the exact refinement
-    const float delta = sc_f * __ldg(ep.q0n + pheno) * sqrtf(static_cast<float>(__ldg(ep.ss_u + m))) * iv * 1.0001f;
-    const bool hit2 = valid && ar + delta >= rb;
-    const uint32_t mask2 = __ballot_sync(0xffffffffu, hit2);
-    if (mask2) {
-      unsigned long long base = 0;
-      if (lane == 0) base = atomicAdd(ep.cand_count, static_cast<unsigned long long>(__popc(mask2)));
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (hit2) {
-        const unsigned long long idx = base - ep.cand_base + __popc(mask2 & lanemask_lt);
-        if (idx < static_cast<unsigned long long>(ep.cand_cap)) {
-          ep.cand_key[idx] = (static_cast<unsigned long long>(m) << 32) | static_cast<unsigned>(pheno);
-          ep.cand_r[idx] = __longlong_as_double(xu);
-        }
-      }
-    }
-    return;
-  }
   const bool hit = valid && ar >= rb;
   // same widening as the premask bar (ctx.cu rbar_kernel), doubled
   const bool near_max = valid && ep.max_abs_r != nullptr && ar >= mx.f * (1.f - 2e-5f) - 2e-7f;

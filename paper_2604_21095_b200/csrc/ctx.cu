@@ -612,7 +612,6 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
   }
   if (two_limb) {
     ep.q0n = c->q0n.p;
-    ep.ss_u = c->ss_u.p;
     PG_CHECK_STATUS(c->mpack.ensure(m_cap));  // m_cap covers every marker slot of the tiles
     PG_CHECK_STATUS(pack_marker_terms(c->mu_f.p, c->mu_d.p, c->invd_f.p, c->ss_u.p, c->n_miss.p, m_cap, c->mpack.p, s));
     ep.mpack = c->mpack.p;

@@ -109,3 +109,26 @@ def test_wide_two_limb_bgen8_equals_three_limb_bitwise(mode, tmp_path, monkeypat
                                   device_batch=300, **kw))
         out[flag] = path.read_bytes()
     assert out["1"] == out["0"] and out["1"].count(b"\n") > 1
+
+
+def test_two_limb_extension_mode_and_covariates_bitwise(tmp_path, monkeypatch):
+    """Extension mode (residualize_genotypes, adjusted df: the K5 basis GEMM stays three-limb and
+    rewrites V_m) with covariates and missing calls: two-limb records == three-limb records."""
+    from conftest_helpers import write_tsv
+
+    rng = np.random.default_rng(71)
+    n, m, p = 401, 900, 16
+    d, y = _cohort(rng, m, n, p)
+    rows = rng.random(m) < 0.2
+    d[rows] = np.where(rng.random((rows.sum(), n)) < 0.04, np.nan, d[rows])
+    spec, pheno, _, root = dataset(tmp_path, d, y)
+    ids = [f"S{i + 1}" for i in range(n)]
+    covar = write_tsv(root / "c.tsv", ids, ["c1", "c2", "c3"], rng.standard_normal((n, 3)))
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("PG_TWO_LIMB", flag)
+        path = root / f"e{flag}.tsv"
+        scan(spec, pheno, path, covar=covar, p_threshold=0.01, residualize_genotypes=True,
+             df_mode=pg.DfMode.ADJUSTED, device_batch=400)
+        out[flag] = path.read_bytes()
+    assert out["1"] == out["0"] and out["1"].count(b"\n") > 1
