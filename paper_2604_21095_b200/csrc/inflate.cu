@@ -21,6 +21,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "inflate.cuh"
 
@@ -83,13 +84,14 @@ struct EncDist {
   }
 };
 
+template <int RING = kRing>
 struct WarpSmem {
   Table<kLitBits, 288> lit;
   Table<kDistBits, 32> dist;
   Table<kClenBits, 19> clen;
   uint16_t codes[288];
   uint8_t lens[288 + 32];
-  uint8_t ring[kRing];
+  uint8_t ring[RING];
 };
 
 // Register bit buffer over 4-byte aligned input words. After refill(): cnt >= 33.
@@ -203,18 +205,31 @@ __device__ __forceinline__ uint32_t decode(Bits& br, const Table<BITS, NSYM, T>&
 // L lanes decode one stream: L = 32 (a warp per stream, the default) or 16 (two streams per
 // warp; the two half-warps share an instruction only while their streams take the same branch).
 // Blocks hold 4 streams either way (27 KB of static shared memory).
+// L lanes per stream: 32 (a warp per stream), 16, 8 or 4 (32 / L streams share a warp; the
+// serial Huffman decode is then replicated on L lanes instead of 32, at the price of
+// divergence between the warp's streams). Sub-warp groups keep a 1 KB output ring so a
+// warp's 8 streams fit the 48 KB of static shared memory.
 template <int L>
-__global__ void __launch_bounds__(4 * L) inflate_kernel(const uint8_t* __restrict__ blob,
+struct InflateGeom {
+  static constexpr int kStreams = L >= 8 ? 4 : 32 / L;  // streams per block
+  static constexpr int kRingL = L >= 16 ? kRing : 1024;
+  static constexpr int kRingSafeL = kRingL - 258;
+};
+
+template <int L>
+__global__ void __launch_bounds__(InflateGeom<L>::kStreams * L) inflate_kernel(const uint8_t* __restrict__ blob,
                                                                      const int64_t* __restrict__ off,
                                                                      const int64_t* __restrict__ len, int64_t count,
                                                                      int64_t skip, uint8_t* __restrict__ out,
                                                                      int64_t out_stride, int64_t* __restrict__ out_len,
                                                                      int* __restrict__ status) {
-  constexpr int kStreams = 4;
-  __shared__ WarpSmem sm_all[kStreams];
+  constexpr int kStreams = InflateGeom<L>::kStreams;
+  constexpr int kRing = InflateGeom<L>::kRingL;  // shadows the file-level 2 KB ring size
+  constexpr int kRingSafe = InflateGeom<L>::kRingSafeL;
+  __shared__ WarpSmem<kRing> sm_all[kStreams];
   const int lane = threadIdx.x & (L - 1);
-  const unsigned mask = L == 32 ? 0xffffffffu : (0xffffu << (threadIdx.x & 16));
-  WarpSmem& sm = sm_all[threadIdx.x / L];
+  const unsigned mask = L == 32 ? 0xffffffffu : (((1u << L) - 1u) << (threadIdx.x & 31u & ~static_cast<unsigned>(L - 1)));
+  WarpSmem<kRing>& sm = sm_all[threadIdx.x / L];
   const int64_t stream = static_cast<int64_t>(blockIdx.x) * kStreams + threadIdx.x / L;
   if (stream >= count) return;
 
@@ -1007,7 +1022,8 @@ int inflate_streams(const uint8_t* d_blob, const int64_t* d_off, const int64_t* 
   // Read per call (A/B tests switch it inside one process).
   const char* mode = std::getenv("PG_INFLATE_MODE");
   const char* lanes_env = std::getenv("PG_INFLATE_LANES");
-  const int lanes = lanes_env && std::atoi(lanes_env) == 16 ? 16 : 32;
+  const int lanes_req = lanes_env ? std::atoi(lanes_env) : 32;
+  const int lanes = (lanes_req == 16 || lanes_req == 8 || lanes_req == 4) ? lanes_req : 32;
   if (d_tokens != nullptr && d_ntok != nullptr && mode != nullptr && std::strcmp(mode, "tokens") == 0) {
     const int64_t tok_stride = inflate_token_stride(out_stride);
     constexpr int kSmem = static_cast<int>(sizeof(ThreadTables)) * kTokThreads;
@@ -1021,13 +1037,18 @@ int inflate_streams(const uint8_t* d_blob, const int64_t* d_off, const int64_t* 
     PG_CUDA_CHECK(cudaGetLastError());
     return PG_OK;
   }
-  const unsigned blocks = static_cast<unsigned>((count + 3) / 4);  // 4 streams per block
-  if (lanes == 16) {
-    inflate_kernel<16><<<blocks, 64, 0, s>>>(d_blob, d_off, d_len, count, skip, d_out, out_stride, d_out_len,
-                                            d_status);
-  } else {
-    inflate_kernel<32><<<blocks, 128, 0, s>>>(d_blob, d_off, d_len, count, skip, d_out, out_stride, d_out_len,
-                                             d_status);
+  auto launch = [&](auto lanes_c) {
+    constexpr int Lc = decltype(lanes_c)::value;
+    constexpr int kS = InflateGeom<Lc>::kStreams;
+    const unsigned blocks = static_cast<unsigned>((count + kS - 1) / kS);
+    inflate_kernel<Lc><<<blocks, kS * Lc, 0, s>>>(d_blob, d_off, d_len, count, skip, d_out, out_stride, d_out_len,
+                                                  d_status);
+  };
+  switch (lanes) {
+    case 4: launch(std::integral_constant<int, 4>{}); break;
+    case 8: launch(std::integral_constant<int, 8>{}); break;
+    case 16: launch(std::integral_constant<int, 16>{}); break;
+    default: launch(std::integral_constant<int, 32>{}); break;
   }
   PG_CUDA_CHECK(cudaGetLastError());
   return PG_OK;

@@ -28,6 +28,15 @@ def _gpu_inflate(streams, out_stride=None, skip=0):
     return [(int(st), out[i * stride:i * stride + int(n)].tobytes()) for i, (st, n) in enumerate(zip(status, out_len))]
 
 
+def _decoder_env(decoder, monkeypatch):
+    """warp: a warp per stream (default); lanesN: N lanes per stream (32 / N streams per warp);
+    tokens: the two-phase decoder."""
+    if decoder == "tokens":
+        monkeypatch.setenv("PG_INFLATE_MODE", "tokens")
+    elif decoder.startswith("lanes"):
+        monkeypatch.setenv("PG_INFLATE_LANES", decoder[5:])
+
+
 def _payloads(rng):
     n = 23000
     g = rng.binomial(2, 0.3, n)
@@ -41,11 +50,10 @@ def _payloads(rng):
                                             (6, zlib.Z_DEFAULT_STRATEGY), (9, zlib.Z_DEFAULT_STRATEGY),
                                             (6, zlib.Z_FIXED), (6, zlib.Z_RLE), (6, zlib.Z_HUFFMAN_ONLY),
                                             (6, zlib.Z_FILTERED)])
-@pytest.mark.parametrize("decoder", ["warp", "tokens"])
+@pytest.mark.parametrize("decoder", ["warp", "lanes8", "lanes4", "tokens"])
 def test_matches_zlib(level, strategy, decoder, monkeypatch):
     """Both GPU decoders (warp per stream; two-phase tokens, PG_INFLATE_MODE=tokens) == zlib."""
-    if decoder == "tokens":
-        monkeypatch.setenv("PG_INFLATE_MODE", "tokens")
+    _decoder_env(decoder, monkeypatch)
     rng = np.random.default_rng(level * 10 + strategy)
     data = _payloads(rng)
     streams = []
@@ -57,10 +65,9 @@ def test_matches_zlib(level, strategy, decoder, monkeypatch):
         assert st == 0 and out == d
 
 
-@pytest.mark.parametrize("decoder", ["warp", "tokens"])
+@pytest.mark.parametrize("decoder", ["warp", "lanes8", "lanes4", "tokens"])
 def test_many_streams_and_multiple_blocks(decoder, monkeypatch):
-    if decoder == "tokens":
-        monkeypatch.setenv("PG_INFLATE_MODE", "tokens")
+    _decoder_env(decoder, monkeypatch)
     rng = np.random.default_rng(7)
     data = [rng.integers(0, 3, rng.integers(1, 200000), dtype=np.uint8).tobytes() for _ in range(200)]
     streams = []
@@ -74,10 +81,9 @@ def test_many_streams_and_multiple_blocks(decoder, monkeypatch):
         assert st == 0 and out == d
 
 
-@pytest.mark.parametrize("decoder", ["warp", "tokens"])
+@pytest.mark.parametrize("decoder", ["warp", "lanes8", "lanes4", "tokens"])
 def test_corrupt_streams_rejected(decoder, monkeypatch):
-    if decoder == "tokens":
-        monkeypatch.setenv("PG_INFLATE_MODE", "tokens")
+    _decoder_env(decoder, monkeypatch)
     good = zlib.compress(b"hello world " * 500)
     bad_header = b"\x78\x9d" + good[2:]                            # FCHECK wrong
     bad_sum = good[:-1] + bytes([good[-1] ^ 1])                     # Adler-32 mismatch
