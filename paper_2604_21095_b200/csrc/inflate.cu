@@ -1018,7 +1018,9 @@ int inflate_streams(const uint8_t* d_blob, const int64_t* d_off, const int64_t* 
   // Default: the warp-per-stream decoder. PG_INFLATE_MODE=tokens selects the two-phase
   // decoder (measured slower on C5: 15.0 + 4.6 ms vs 8.5 ms per 8,192 BGEN-8 variants; a
   // batch gives phase 1 only ~55 streams = 1.7 warps per SM, so its serial per-thread decode
-  // is latency-bound). PG_INFLATE_LANES=16: two streams per warp (10 % slower than 32).
+  // is latency-bound). PG_INFLATE_LANES=16 / 8 / 4: 2 / 4 / 8 streams per warp (C5 end to end
+// 10 % slower at 16; 1.80e9 at 8 and 1.36e9 at 4 vs 2.69e9 at 32 lanes: divergence between
+// the warp's streams and fewer resident warps outweigh the lower decode replication).
   // Read per call (A/B tests switch it inside one process).
   const char* mode = std::getenv("PG_INFLATE_MODE");
   const char* lanes_env = std::getenv("PG_INFLATE_LANES");
