@@ -94,9 +94,7 @@ struct Cfg {
   static constexpr bool TWO = MODE == kFused2 || MODE == kWide3Two || MODE == kPlanes2;  // q0 limb deferred
   static constexpr bool TRANS = MODE == kWide3T;
   static constexpr bool WIDE = MODE == kWide || MODE == kWide3 || MODE == kWide3Two || TRANS;
-  static constexpr int kStages = (TRANS || MODE == kWide3Two) ? 9 : (WIDE ? 7 : (TWO ? 6 : 5));
-  // decoder / epilogue warp split: the two-limb mainloop (512 tensor cycles per 64-sample
-  // stage instead of 768) gets 8 decoder warps, two threads per packed row
+  static constexpr int kStages = (TRANS || MODE == kWide3Two) ? 9 : (WIDE ? 7 : (MODE == kFused2 ? 8 : (TWO ? 6 : 5)));
   // decoder warps: 4 (one thread per packed row). Measured on the two-limb C3 scan: 8 decoder
   // warps with 12 epilogue warps 2.45e10 tests/s, with 16 epilogue warps (896 threads) 2.54e10,
   // 4 + 16 (768 threads) 2.60e10; a separate 12-deep packed-tile ring 2.50e10
@@ -105,9 +103,13 @@ struct Cfg {
   static constexpr int kEpiWarps = 16;  // 20 for the two-limb tile measured no faster (2.71 vs 2.73e10)
   static constexpr int kColGroups = kEpiWarps / 4;
   static constexpr int kThreadsM = 32 * (kFirstEpiWarp + kEpiWarps);  // 768
-  // fused / planes stage layout: panel limbs (2 in the two-limb mode), v, 127 v, packed codes
+  // fused / planes stage layout: panel limbs (2 in the two-limb mode), v, 127 v, packed codes.
+  // The fused two-limb GEMM needs no 127 v plane: without q0, the q1 accumulator holds
+  // sum q1 * v alone and the epilogue scales it by 127 (halves the decoders' stores and frees
+  // 8 KB per stage for a deeper ring).
+  static constexpr bool NO127 = FUSED && TWO;
   static constexpr int kOffV = (TWO ? 2 : 3) * kQBytes;
-  static constexpr int kOffV127 = kOffV + kVBytes;
+  static constexpr int kOffV127 = kOffV + (NO127 ? 0 : kVBytes);
   static constexpr int kOffPacked = kOffV127 + kVBytes;
   // genotype rows per pair tile; wide modes: rows per marker
   static constexpr int kTileRows =
@@ -417,8 +419,9 @@ __device__ __forceinline__ void epilogue_tile_two(const AssocEpilogue& ep, uint3
           xm_f = static_cast<float>(xm);
         }
       }
+      // X' = kWH h + 127 l (the q1 accumulator holds sum q1 v: no 127 v plane in this mode)
       const float xf = fmaf(static_cast<float>(static_cast<int>(h[j])), static_cast<float>(kWH),
-                            static_cast<float>(static_cast<int>(l[j]))) - mk.x * (cq_f - xm_f);
+                            127.f * static_cast<float>(static_cast<int>(l[j]))) - mk.x * (cq_f - xm_f);
       const bool hit = fabsf(xf * sc_f * mk.y) + dp * mk.z >= rb;
       const uint32_t mask = __ballot_sync(0xffffffffu, hit);
       if (mask) {
@@ -428,7 +431,8 @@ __device__ __forceinline__ void epilogue_tile_two(const AssocEpilogue& ep, uint3
         if (hit) {
           const unsigned long long idx = base - ep.cand_base + __popc(mask & lanemask_lt);
           if (idx < static_cast<unsigned long long>(ep.cand_cap)) {
-            const long long xu = kWH * static_cast<long long>(static_cast<int>(h[j])) + static_cast<int>(l[j]);
+            const long long xu =
+                kWH * static_cast<long long>(static_cast<int>(h[j])) + 127ll * static_cast<int>(l[j]);
             ep.cand_key[idx] = (static_cast<unsigned long long>(m) << 32) | static_cast<unsigned>(pheno);
             ep.cand_r[idx] = __longlong_as_double(xu);
           }
@@ -693,7 +697,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<MODE>::kThreadsM
               if constexpr (!C::TWO) mma_i8_ss_pair(dC, d_q0 + 2 * k, d_v + 2 * k, idesc, acc);
             } else {
               mma_i8_ss_pair(dH, d_qh + 2 * k, d_v + 2 * k, idesc, acc);
-              mma_i8_ss_pair(dL, d_q1 + 2 * k, d_v127 + 2 * k, idesc, acc);
+              mma_i8_ss_pair(dL, d_q1 + 2 * k, (C::NO127 ? d_v : d_v127) + 2 * k, idesc, acc);
               if constexpr (!C::TWO) mma_i8_ss_pair(dL, d_q0 + 2 * k, d_v + 2 * k, idesc, 1);
             }
             acc = 1;
@@ -743,7 +747,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<MODE>::kThreadsM
             decode_word(words[i], u, u7);
             const uint32_t off = r * 64 + ((c ^ sw) << 4);
             *reinterpret_cast<uint4*>(st + C::kOffV + off) = make_uint4(u[0], u[1], u[2], u[3]);
-            *reinterpret_cast<uint4*>(st + C::kOffV127 + off) = make_uint4(u7[0], u7[1], u7[2], u7[3]);
+            if constexpr (!C::NO127)
+              *reinterpret_cast<uint4*>(st + C::kOffV127 + off) = make_uint4(u7[0], u7[1], u7[2], u7[3]);
           }
           fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the tensor core
           __syncwarp();
