@@ -61,7 +61,10 @@ constexpr int kTileCW = kTileCWide;
 constexpr int kHalfCW = kTileCW / 2;
 constexpr int kVBytesW = kHalfCW * kTileK;  // 5 KB
 constexpr int kRowsW = 4;                   // digits 255^0, 255^1, 255^2 + missing row
-constexpr int kPlanes = 0, kFused = 1, kWide = 2, kWide3 = 3, kWide3T = 4, kFused2 = 5, kWide3Two = 6, kPlanes2 = 7;
+constexpr int kPlanes = 0, kFused = 1, kWide = 2, kWide3 = 3, kWide3T = 4, kFused2 = 5, kWide3Two = 6, kPlanes2 = 7,
+              kWide4Two = 8;
+// kWide4Two: the 4-row wide digits (BGEN-16, real-valued dense) without the q0 limb: 256-row
+// tiles (64 markers) with two accumulators, refine_wide_two<4> completes the candidates.
 // kPlanes2: kPlanes without the q0 limb (the missing-call side GEMM of a two-limb scan: its
 // Mq' is completed per candidate by refine_two_limb).
 // kWide3Two: kWide3 (BGEN-8 digit rows) without the q0 limb: two accumulators, so the tile
@@ -91,10 +94,12 @@ constexpr int kTmemCols = 512;
 template <int MODE>
 struct Cfg {
   static constexpr bool FUSED = MODE == kFused || MODE == kFused2;
-  static constexpr bool TWO = MODE == kFused2 || MODE == kWide3Two || MODE == kPlanes2;  // q0 limb deferred
+  static constexpr bool TWO =
+      MODE == kFused2 || MODE == kWide3Two || MODE == kWide4Two || MODE == kPlanes2;  // q0 limb deferred
   static constexpr bool TRANS = MODE == kWide3T;
-  static constexpr bool WIDE = MODE == kWide || MODE == kWide3 || MODE == kWide3Two || TRANS;
-  static constexpr int kStages = (TRANS || MODE == kWide3Two) ? 9 : (WIDE ? 7 : (MODE == kFused2 ? 8 : (TWO ? 6 : 5)));
+  static constexpr bool WIDE = MODE == kWide || MODE == kWide3 || MODE == kWide3Two || MODE == kWide4Two || TRANS;
+  static constexpr int kStages =
+      (TRANS || MODE == kWide3Two || MODE == kWide4Two) ? 9 : (WIDE ? 7 : (MODE == kFused2 ? 8 : (TWO ? 6 : 5)));
   // decoder warps: 4 (one thread per packed row). Measured on the two-limb C3 scan: 8 decoder
   // warps with 12 epilogue warps 2.45e10 tests/s, with 16 epilogue warps (896 threads) 2.54e10,
   // 4 + 16 (768 threads) 2.60e10; a separate 12-deep packed-tile ring 2.50e10
@@ -114,9 +119,10 @@ struct Cfg {
   // genotype rows per pair tile; wide modes: rows per marker
   static constexpr int kTileRows =
       TRANS ? kTileC
-            : (MODE == kWide3 ? kTileCWide3 : (MODE == kWide3Two ? kTileCWide3Two : (WIDE ? kTileCW : kTileC)));
+            : (MODE == kWide3 ? kTileCWide3
+                              : (MODE == kWide3Two ? kTileCWide3Two : (MODE == kWide4Two ? kTileC : (WIDE ? kTileCW : kTileC))));
   static constexpr int kHalfRows = kTileRows / 2;
-  static constexpr int kWideR = (MODE == kWide3 || MODE == kWide3Two || TRANS) ? kWideRows3 : kRowsW;
+  static constexpr int kWideR = (MODE == kWide3 || MODE == kWide3Two || TRANS) ? kWideRows3 : kRowsW;  // kWide4Two: 4
   static constexpr int kVBytesWide = kHalfRows * kTileK;
   // accumulator width (UMMA N): genotype rows, or phenotypes in the transposed mode
   static constexpr int kAccCols = TRANS ? kTPheno : kTileRows;
@@ -442,37 +448,40 @@ __device__ __forceinline__ void epilogue_tile_two(const AssocEpilogue& ep, uint3
   }
 }
 
-// Two-limb BGEN-8 tile (kWide3Two): per marker rows (digit0, digit1, missing) of
-// X'_row = kWH A + 127 B; the premask as epilogue_tile_two with the bound over u and the
+// Two-limb wide tile (kWide3Two: rows digit0, digit1, missing; kWide4Two: digit0..2, missing)
+// of X'_row = kWH A + 127 B; the premask as epilogue_tile_two with the bound over u and the
 // missing row (AssocEpilogue::mpack); a hit stores X'_u (cand_r bits) and X'_m (cand_xm).
-__device__ __forceinline__ void epilogue_tile_wide3two(const AssocEpilogue& ep, uint32_t tA, int ct, int pheno,
+template <int kR>
+__device__ __forceinline__ void epilogue_tile_wide_two(const AssocEpilogue& ep, uint32_t tA, int ct, int pheno,
                                                        int lane, int c_begin, int c_end) {
-  constexpr int kR = kWideRows3;
-  constexpr int kMarkersPerTile = kTileCWide3Two / kR;
+  constexpr int kTileRowsW = kR == 3 ? kTileCWide3Two : kTileC;
+  constexpr int kUnitW = kR == 3 ? 12 : 16;
+  constexpr int kMarkersPerTile = kTileRowsW / kR;
   const uint32_t lanemask_lt = (1u << lane) - 1u;
   const float sc_f = ep.scale_f[pheno];
   const float cq_f = ep.cq_f[pheno];
   const float rb = ep.rbar ? ep.rbar[pheno] : INFINITY;
   const float dp = sc_f * __ldg(ep.q0n + pheno) * 1.0001f;
 #pragma unroll 1
-  for (int c = c_begin; c < c_end; c += 12) {
-    uint32_t a[12], b[12];
+  for (int c = c_begin; c < c_end; c += kUnitW) {
+    uint32_t a[kUnitW], b[kUnitW];
 #pragma unroll
-    for (int q = 0; q < 3; ++q) {
+    for (int q = 0; q < kUnitW / 4; ++q) {
       tmem_ld_32x32b_x4(tA + c + 4 * q, a + 4 * q);
-      tmem_ld_32x32b_x4(tA + kTileCWide3Two + c + 4 * q, b + 4 * q);
+      tmem_ld_32x32b_x4(tA + kTileRowsW + c + 4 * q, b + 4 * q);
     }
     tmem_ld_wait();
 #pragma unroll
-    for (int j = 0; j < 12; j += kR) {
+    for (int j = 0; j < kUnitW; j += kR) {
       long long x[kR];
 #pragma unroll
       for (int t = 0; t < kR; ++t)
         x[t] = kWH * static_cast<long long>(static_cast<int>(a[j + t])) + 127ll * static_cast<int>(b[j + t]);
-      const long long xu = x[0] + 255ll * x[1];
+      long long xu = x[0] + 255ll * x[1];
+      if constexpr (kR == 4) xu += 65025ll * x[2];
       const int m = ct * kMarkersPerTile + (c + j) / kR;
       const float4 mk = __ldg(ep.mpack + m);
-      const float xf = static_cast<float>(xu) - mk.x * (cq_f - static_cast<float>(x[2]));
+      const float xf = static_cast<float>(xu) - mk.x * (cq_f - static_cast<float>(x[kR - 1]));
       const bool hit = fabsf(xf * sc_f * mk.y) + dp * mk.z >= rb;
       const uint32_t mask = __ballot_sync(0xffffffffu, hit);
       if (mask) {
@@ -484,7 +493,7 @@ __device__ __forceinline__ void epilogue_tile_wide3two(const AssocEpilogue& ep, 
           if (idx < static_cast<unsigned long long>(ep.cand_cap)) {
             ep.cand_key[idx] = (static_cast<unsigned long long>(m) << 32) | static_cast<unsigned>(pheno);
             ep.cand_r[idx] = __longlong_as_double(xu);
-            ep.cand_xm[idx] = x[2];
+            ep.cand_xm[idx] = x[kR - 1];
           }
         }
       }
@@ -779,14 +788,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<MODE>::kThreadsM
       const uint32_t tL = tH + C::kAccCols;
       // split the tile's 16-column chunks over the 4 column groups (12-column = 4-marker
       // units in the 3-row mode, 12-column = 4 phenotype triples in the transposed mode)
-      constexpr int kUnit = (MODE == kWide3 || MODE == kWide3Two || C::TRANS) ? 12 : 16;
+      constexpr int kUnit = (MODE == kWide3 || MODE == kWide3Two || C::TRANS) ? 12 : 16;  // kWide4Two: 16
       constexpr int kChunks = C::kAccCols / kUnit;
       constexpr int G = C::kColGroups;
       const int c0 = kUnit * ((cg * kChunks) / G), c1 = kUnit * (((cg + 1) * kChunks) / G);
       if constexpr (C::TRANS) {
         epilogue_tile_wide3t(ep, tH, ct, static_cast<int>(cr), pt, quarter, lane, c0, c1);
       } else if constexpr (MODE == kWide3Two) {
-        epilogue_tile_wide3two(ep, tH, ct, pheno, lane, c0, c1);
+        epilogue_tile_wide_two<3>(ep, tH, ct, pheno, lane, c0, c1);
+      } else if constexpr (MODE == kWide4Two) {
+        epilogue_tile_wide_two<4>(ep, tH, ct, pheno, lane, c0, c1);
       } else if constexpr (MODE == kWide3) {
         epilogue_tile_wide3(ep, tH, ct, pheno, lane, c0, c1);
       } else if constexpr (WIDE) {
@@ -1071,6 +1082,7 @@ __global__ void pack_marker_kernel(const float* __restrict__ mu_f, const double*
 
 // Warp per wide two-limb candidate: the q0 limb against the marker's digit rows (u = d0 + 255 d1)
 // and missing row, by DP4A over the int8 planes; then the exact fp64 r.
+template <int R>
 __global__ void refine_wide_two_kernel(const unsigned long long* __restrict__ key, double* __restrict__ cand_r,
                                        const long long* __restrict__ cand_xm, int64_t n, const int8_t* __restrict__ v,
                                        const int8_t* __restrict__ q0, int64_t k_pad, AssocEpilogue ep) {
@@ -1081,36 +1093,34 @@ __global__ void refine_wide_two_kernel(const unsigned long long* __restrict__ ke
     const unsigned long long kk = key[i];
     const int64_t m = static_cast<int64_t>(kk >> 32);
     const int p = static_cast<int>(kk & 0xffffffffull);
-    const uint4* r0 = reinterpret_cast<const uint4*>(v + (3 * m) * k_pad);
-    const uint4* r1 = reinterpret_cast<const uint4*>(v + (3 * m + 1) * k_pad);
-    const uint4* r2 = reinterpret_cast<const uint4*>(v + (3 * m + 2) * k_pad);
     const uint4* qrow = reinterpret_cast<const uint4*>(q0 + static_cast<int64_t>(p) * k_pad);
-    int d0 = 0, d1 = 0, dm = 0;
+    int d[R];  // per row: sum q0 * row (digits 0..R-2, then the missing row)
+#pragma unroll
+    for (int t = 0; t < R; ++t) d[t] = 0;
     for (int64_t c = lane; c < chunks; c += 32) {
       const uint4 w = __ldg(qrow + c);
-      const uint4 a = __ldg(r0 + c), b = __ldg(r1 + c), z = __ldg(r2 + c);
-      d0 = __dp4a(static_cast<int>(w.x), static_cast<int>(a.x), d0);
-      d0 = __dp4a(static_cast<int>(w.y), static_cast<int>(a.y), d0);
-      d0 = __dp4a(static_cast<int>(w.z), static_cast<int>(a.z), d0);
-      d0 = __dp4a(static_cast<int>(w.w), static_cast<int>(a.w), d0);
-      d1 = __dp4a(static_cast<int>(w.x), static_cast<int>(b.x), d1);
-      d1 = __dp4a(static_cast<int>(w.y), static_cast<int>(b.y), d1);
-      d1 = __dp4a(static_cast<int>(w.z), static_cast<int>(b.z), d1);
-      d1 = __dp4a(static_cast<int>(w.w), static_cast<int>(b.w), d1);
-      dm = __dp4a(static_cast<int>(w.x), static_cast<int>(z.x), dm);
-      dm = __dp4a(static_cast<int>(w.y), static_cast<int>(z.y), dm);
-      dm = __dp4a(static_cast<int>(w.z), static_cast<int>(z.z), dm);
-      dm = __dp4a(static_cast<int>(w.w), static_cast<int>(z.w), dm);
+#pragma unroll
+      for (int t = 0; t < R; ++t) {
+        const uint4 a = __ldg(reinterpret_cast<const uint4*>(v + (R * m + t) * k_pad) + c);
+        d[t] = __dp4a(static_cast<int>(w.x), static_cast<int>(a.x), d[t]);
+        d[t] = __dp4a(static_cast<int>(w.y), static_cast<int>(a.y), d[t]);
+        d[t] = __dp4a(static_cast<int>(w.z), static_cast<int>(a.z), d[t]);
+        d[t] = __dp4a(static_cast<int>(w.w), static_cast<int>(a.w), d[t]);
+      }
     }
 #pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      d0 += __shfl_xor_sync(0xffffffffu, d0, o);
-      d1 += __shfl_xor_sync(0xffffffffu, d1, o);
-      dm += __shfl_xor_sync(0xffffffffu, dm, o);
-    }
+    for (int o = 16; o; o >>= 1)
+#pragma unroll
+      for (int t = 0; t < R; ++t) d[t] += __shfl_xor_sync(0xffffffffu, d[t], o);
     if (lane == 0) {
-      const long long xu = __double_as_longlong(cand_r[i]) + d0 + 255ll * d1;
-      const long long xm = cand_xm[i] + dm;
+      long long du = 0, w = 1;
+#pragma unroll
+      for (int t = 0; t < R - 1; ++t) {
+        du += w * d[t];
+        w *= 255;
+      }
+      const long long xu = __double_as_longlong(cand_r[i]) + du;
+      const long long xm = cand_xm[i] + d[R - 1];
       cand_r[i] = ep.scale_d[p] * (static_cast<double>(xu) - ep.mu_d[m] * static_cast<double>(ep.cq[p] - xm)) *
                   ep.invd_d[m];
     }
@@ -1121,9 +1131,13 @@ __global__ void refine_wide_two_kernel(const unsigned long long* __restrict__ ke
 int refine_wide_two(const unsigned long long* cand_key, double* cand_r, const long long* cand_xm, int64_t n,
                     const int8_t* v, const int8_t* q0, int64_t k_pad, const AssocEpilogue& ep, cudaStream_t stream) {
   if (n <= 0) return PG_OK;
-  PG_REQUIRE(k_pad % 64 == 0, PG_ERR_INVALID, "refine_wide_two: bad shape");
+  PG_REQUIRE(k_pad % 64 == 0 && (ep.rows_per_marker == 3 || ep.rows_per_marker == 4), PG_ERR_INVALID,
+             "refine_wide_two: bad shape");
   const unsigned grid = static_cast<unsigned>(std::min<int64_t>((n + 7) / 8, 148 * 16));
-  refine_wide_two_kernel<<<grid, 256, 0, stream>>>(cand_key, cand_r, cand_xm, n, v, q0, k_pad, ep);
+  if (ep.rows_per_marker == 4)
+    refine_wide_two_kernel<4><<<grid, 256, 0, stream>>>(cand_key, cand_r, cand_xm, n, v, q0, k_pad, ep);
+  else
+    refine_wide_two_kernel<3><<<grid, 256, 0, stream>>>(cand_key, cand_r, cand_xm, n, v, q0, k_pad, ep);
   PG_CUDA_CHECK(cudaGetLastError());
   return PG_OK;
 }
@@ -1163,7 +1177,7 @@ int launch_assoc_wide(const int8_t* qh, const int8_t* q1, const int8_t* q0, int6
   const int R = ep.rows_per_marker;
   PG_REQUIRE(R == kRowsW || R == kWideRows3, PG_ERR_INVALID, "assoc(wide): rows_per_marker must be 3 or 4, got %d",
              R);
-  const int tile = R == kWideRows3 ? (ep.q0n ? kTileCWide3Two : kTileCWide3) : kTileCW;
+  const int tile = R == kWideRows3 ? (ep.q0n ? kTileCWide3Two : kTileCWide3) : (ep.q0n ? kTileC : kTileCW);
   PG_REQUIRE(p_pad % kTileP == 0 && c_pad % tile == 0 && k_pad % kTileK == 0 && p_pad > 0 && c_pad > 0 &&
                  k_pad > 0,
              PG_ERR_INVALID, "assoc(wide): bad padded shape p=%lld c=%lld k=%lld", (long long)p_pad,
@@ -1176,6 +1190,13 @@ int launch_assoc_wide(const int8_t* qh, const int8_t* q1, const int8_t* q0, int6
                PG_ERR_INVALID, "assoc(wide, two-limb): bad arguments");
     PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_v, v, k_pad, c_pad, k_pad, kTileK, kTileCWide3Two / 2));
     return launch_common<kWide3Two>(tm_qh, tm_q1, tm_q0, tm_v, tm_v, p_pad, c_pad, k_pad, ep, stream);
+  }
+  if (R == kRowsW && ep.q0n) {  // two-limb premask: 256-row tiles (64 markers)
+    PG_REQUIRE(c_pad % kTileC == 0 && ep.full_r == nullptr && ep.max_abs_r == nullptr && ep.x_accum == nullptr &&
+                   ep.mpack != nullptr && ep.cand_xm != nullptr,
+               PG_ERR_INVALID, "assoc(wide4, two-limb): bad arguments");
+    PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_v, v, k_pad, c_pad, k_pad, kTileK, kTileC / 2));
+    return launch_common<kWide4Two>(tm_qh, tm_q1, tm_q0, tm_v, tm_v, p_pad, c_pad, k_pad, ep, stream);
   }
   PG_CHECK_STATUS(encode_tmap_2d_i8(&tm_v, v, k_pad, c_pad, k_pad, kTileK, tile / 2));
   if (R == kWideRows3) return launch_common<kWide3>(tm_qh, tm_q1, tm_q0, tm_v, tm_v, p_pad, c_pad, k_pad, ep, stream);

@@ -468,11 +468,13 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
   // fused PLINK GEMM and the BGEN-8 wide GEMM (whose tile then widens to 240 rows)
   const bool two_limb_ok =
       c->two_limb && c->mode != PG_MODE_FULL && !c->track_max_abs_r && c->k_pad <= kSliceK && !c->f64_panel;
-  const bool wide_two = two_limb_ok && R == kWideRows3 && !wide3t && !c->have_basis;
+  const bool wide_two = two_limb_ok && (R == kWideRows3 || R == kWideRows) && !wide3t && !c->have_basis;
   const bool two_limb = two_limb_ok && (fused || wide_two);
   const int64_t c_pad =
       wide3t ? round_up((m + 9) / 10 * 32, kTileC)
-             : round_up(m * R, wide ? (R == kWideRows3 ? (wide_two ? kTileCWide3Two : kTileCWide3) : kTileCWide) : kTileC);
+             : round_up(m * R, wide ? (R == kWideRows3 ? (wide_two ? kTileCWide3Two : kTileCWide3)
+                                                        : (wide_two ? kTileC : kTileCWide))
+                                    : kTileC);
   if (two_limb && !c->q0n_valid) {
     PG_CHECK_STATUS(c->q0n.ensure(c->p_pad));
     PG_CHECK_STATUS(panel_q0_norms(c->q0.p, c->p_pad, c->k_pad, c->q0n.p, s));

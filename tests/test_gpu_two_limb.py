@@ -132,3 +132,37 @@ def test_two_limb_extension_mode_and_covariates_bitwise(tmp_path, monkeypatch):
              df_mode=pg.DfMode.ADJUSTED, device_batch=400)
         out[flag] = path.read_bytes()
     assert out["1"] == out["0"] and out["1"].count(b"\n") > 1
+
+
+@pytest.mark.parametrize("source", ["bgen16", "dense_real"])
+def test_wide4_two_limb_equals_three_limb_bitwise(source, tmp_path, monkeypatch):
+    """4-row wide digits (BGEN-16, real-valued dense) through the 256-row two-limb GEMM
+    (kWide4Two) == the three-limb kWide GEMM, record for record (THRESHOLD and TOPK)."""
+    from conftest_helpers import write_tsv
+
+    rng = np.random.default_rng(91)
+    n, m, k = 271, 300, 10
+    ids = [f"S{i + 1}" for i in range(n)]
+    d = np.clip(rng.binomial(2, rng.uniform(0.05, 0.9, m)[:, None], size=(m, n)) +
+                rng.normal(0, 0.2, (m, n)), 0, 2)
+    d[rng.random((m, n)) < 0.05] = np.nan
+    y = rng.standard_normal((n, k))
+    y[:, 1] += 0.5 * np.nan_to_num(d[9], nan=1.0)
+    pheno = write_tsv(tmp_path / "p.tsv", ids, [f"ph{j + 1}" for j in range(k)], y)
+    if source == "bgen16":
+        from bgen_fixture import write_bgen
+
+        spec = pg.SourceSpec(pg.GenotypeFormat.BGEN, bgen_path=write_bgen(tmp_path / "g.bgen", d, ids, bits=16))
+    else:
+        np.save(tmp_path / "g.npy", d)
+        (tmp_path / "s.txt").write_text("\n".join(ids) + "\n")
+        spec = pg.SourceSpec(pg.GenotypeFormat.DENSE, dense_path=tmp_path / "g.npy", sample_id_path=tmp_path / "s.txt")
+    for kw in (dict(p_threshold=0.02), dict(output_mode=pg.OutputMode.TOPK, top_k=6)):
+        out = {}
+        for flag in ("1", "0"):
+            monkeypatch.setenv("PG_TWO_LIMB", flag)
+            path = tmp_path / f"o{flag}.tsv"
+            pg.run_scan(pg.ScanConfig(source=spec, pheno_path=pheno, out_path=path, summary_to_stderr=False,
+                                      device_batch=128, **kw))
+            out[flag] = path.read_bytes()
+        assert out["1"] == out["0"] and out["1"].count(b"\n") > 1
