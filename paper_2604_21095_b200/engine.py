@@ -26,6 +26,7 @@ import enum
 import json
 import os
 import sys
+import threading
 import time
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
@@ -357,6 +358,42 @@ def write_min_p(path: Path, names, max_abs_r, max_abs_t, min_p) -> None:
             fh.write(f"{name}\t{float(max_abs_r[j])!r}\t{float(max_abs_t[j])!r}\t{float(min_p[j])!r}\n")
 
 
+# One idle device context per device, kept for the next scan of this process: a context owns
+# its CUDA streams and device buffers (grown, never shrunk), so a process that runs many scans
+# (tests, notebooks, the acceptance suite's hundreds of tiny scans) creates them once. A scan
+# takes the idle context only if it was created under the same PG_* / PANELGWAS_* switches
+# (some are read when a context is created); a failed scan closes its context instead.
+_CTX_POOL: dict = {}
+_CTX_POOL_LOCK = threading.Lock()
+
+
+def _switches() -> tuple:
+    return tuple(sorted((k, v) for k, v in os.environ.items() if k.startswith(("PG_", "PANELGWAS_"))))
+
+
+def _acquire_context(device):
+    from ._device import DeviceContext
+
+    key = _switches()
+    with _CTX_POOL_LOCK:
+        held = _CTX_POOL.pop(device, None)
+    if held is not None:
+        if held[0] == key:
+            return held[1]
+        held[1].close()
+    ctx = DeviceContext(device)
+    ctx.pool_key = key
+    return ctx
+
+
+def _release_context(device, ctx) -> None:
+    with _CTX_POOL_LOCK:
+        old = _CTX_POOL.pop(device, None)
+        _CTX_POOL[device] = (getattr(ctx, "pool_key", None), ctx)
+    if old is not None and old[1] is not ctx:
+        old[1].close()
+
+
 def run_scan(config: ScanConfig, marker_range: tuple[int, int] | None = None, panel_hook=None,
              prep_hook=None) -> ScanSummary:
     """Execute a full scan on the GPU and write results plus the summary files.
@@ -366,15 +403,13 @@ def run_scan(config: ScanConfig, marker_range: tuple[int, int] | None = None, pa
     `panel_hook(ctx, prep)` (NCCL broadcast from rank 0) instead of uploading it, and the host
     panel metadata through `prep_hook(source)` (rank 0 parses the tables for everyone).
     """
-    from ._device import DeviceContext
-
     wall0 = time.perf_counter()
     config.validate()
     # CUDA context creation (0.5-2 s) overlaps opening the source (the BGEN index) and parsing
     # the tables; every C-ABI entry selects the ctx's device itself, so the handle may be
     # created on another thread
     init = ThreadPoolExecutor(max_workers=1)
-    ctx_fut = init.submit(DeviceContext, config.device)
+    ctx_fut = init.submit(_acquire_context, config.device)
     try:
         source = open_genotype_source(config.source)
     except BaseException:
@@ -458,12 +493,12 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, init, ctx_fut, mark
             ctx.close()
         raise
 
-    if os.environ.get("PANELGWAS_FUSED_DECODE", "1") == "0":
-        ctx.set_fused_decode(False)  # A/B switch; results are identical either way
-    if os.environ.get("PANELGWAS_MISSING_SIDE_GEMM", "1") == "0":
-        ctx.set_missing_side_gemm(False)  # A/B switch: two-row planes for batches with missing calls
-    if os.environ.get("PANELGWAS_WIDE_DIGITS", "1") == "0":
-        ctx.set_wide_digits(False)  # A/B switch; results are identical either way
+    scan_ok = False
+    # A/B switches (results are identical either way); set on every scan since the context may
+    # be a reused one
+    ctx.set_fused_decode(os.environ.get("PANELGWAS_FUSED_DECODE", "1") != "0")
+    ctx.set_missing_side_gemm(os.environ.get("PANELGWAS_MISSING_SIDE_GEMM", "1") != "0")
+    ctx.set_wide_digits(os.environ.get("PANELGWAS_WIDE_DIGITS", "1") != "0")
     try:
         if config.residualize_genotypes and prep.basis.rank:
             ctx.set_basis(prep.basis.q)  # extension mode: side GEMM K5 for |Q^T g|^2
@@ -661,8 +696,12 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, init, ctx_fut, mark
                 ctx.sync()
                 for b in (pinned or []) + pinned_out:
                     b.close()
+        scan_ok = True
     finally:
-        ctx.close()
+        if scan_ok:
+            _release_context(config.device, ctx)  # kept for the next scan of this process
+        else:
+            ctx.close()
 
     phases["scan_loop_done"] = time.perf_counter() - wall0
     phases["loop_main_thread_waits"] = waits
