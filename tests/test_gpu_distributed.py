@@ -87,3 +87,53 @@ def test_bench_two_ranks_functional(shape):
     assert d["config"]["n_markers_total"] == (12800 if strong else 16384)
     # value counts every rank's tests once: (job markers x P x K) / max-over-ranks time
     assert abs(d["value"] * d["ms_per_step"] / 1e3 - d["config"]["n_markers_total"] * 512) < 1e-3 * d["value"]
+
+
+@pytest.mark.parametrize("f64", [False, True])
+def test_nccl_panel_broadcast_round_trip(f64):
+    """The NCCL data plane of the multi-GPU scan on this box's one GPU: a one-rank NCCL group
+    broadcasts the exported device panel (incl. the F64 panel's lo level), a second context
+    imports it after syncing torch's stream (distributed.broadcast_panel), and its scans equal
+    the exporting context's bit for bit (THRESHOLD two-limb and FULL)."""
+    import torch
+    import torch.distributed as dist
+
+    from oracle import scan_oracle as orc
+    from paper_2604_21095_b200 import _native
+    from paper_2604_21095_b200._device import DeviceContext
+    from paper_2604_21095_b200.distributed import broadcast_bytes
+
+    rng = np.random.default_rng(4)
+    n, m, p = 300, 500, 40
+    d = rng.binomial(2, rng.uniform(0.1, 0.9, m)[:, None], size=(m, n)).astype(np.float64)
+    d[rng.random((m, n)) < 0.02] = np.nan
+    codes = np.where(np.isnan(d), 1, np.select([d == 2, d == 1, d == 0], [0, 2, 3])).astype(np.uint8)
+    bpm = (n + 3) // 4
+    q = codes.reshape(m, bpm, 4)
+    packed = (q[:, :, 0] | (q[:, :, 1] << 2) | (q[:, :, 2] << 4) | (q[:, :, 3] << 6)).astype(np.uint8)
+    ytil, _ = orc.standardized_panel(rng.standard_normal((n, p)), orc.covariate_basis(np.zeros((n, 0))))
+    gidx = np.arange(n, dtype=np.int64)
+    df = float(n - 2)
+    dev = torch.device("cuda", 0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_port()}", rank=0, world_size=1, device_id=dev)
+    try:
+        with DeviceContext(0) as a, DeviceContext(0) as b:
+            for c in (a, b):
+                c.set_f64_panel(f64)
+            a.set_panel(ytil, gidx, n)
+            buf = torch.empty(a.panel_bytes(), dtype=torch.uint8, device=dev)
+            a.export_panel(buf.data_ptr())
+            buf = broadcast_bytes(torch, dist, buf, buf.numel(), 0, dev)
+            torch.cuda.current_stream(dev).synchronize()
+            b.import_panel(buf.data_ptr(), n, p, gidx, n)
+            out = []
+            for c in (a, b):
+                c.set_scan(df, _native.PG_MODE_THRESHOLD, np.full(p, orc.premask_abs_r(0.05, df)))
+                t = c.scan(_native.PG_GENO_BED, packed, bpm)
+                c.set_scan(df, _native.PG_MODE_FULL, None)
+                f = c.scan(_native.PG_GENO_BED, packed, bpm)
+                out.append((t.cand_rows, t.cand_cols, t.cand_t, t.cand_p, f.t_rows))
+        for x, y in zip(*out):
+            assert np.array_equal(x, y)
+    finally:
+        dist.destroy_process_group()
