@@ -171,36 +171,61 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 // 16 packed 2-bit codes (one 32-bit .bed word, low pair first) -> 16 int8 u values
 // (u[0..3]) and their x127 copies (u127[0..3]).  Code 00 -> +1 (two copies of
 // allele1), 10 -> 0, 11 -> -1, 01 (missing) -> 0.  Each code is moved to its own
-// nibble (3 shift/mask steps) and used as a PRMT byte selector into a 4-entry
-// table held in one register: ~1.4 instructions per sample.
-__device__ __forceinline__ uint32_t codes_to_nibbles(uint32_t x16) {
-  uint32_t x = x16 & 0xFFFFu;
-  x = (x | (x << 8)) & 0x00FF00FFu;
-  x = (x | (x << 4)) & 0x0F0F0F0Fu;
-  x = (x | (x << 2)) & 0x33333333u;
-  return x;
+// nibble (one PRMT byte spread + 2 shift/mask steps per 8 codes) and used as a PRMT byte
+// selector into a 4-entry table held in one register: 16 instructions per 16 samples.
+// (x | (x << sh)) & mask as one shift + one LOP3 (left to itself, ptxas splits the mask)
+template <int kShift, uint32_t kMask>
+__device__ __forceinline__ uint32_t spread_step(uint32_t x) {
+  uint32_t r;
+  asm("{\n\t.reg .b32 t;\n\tshl.b32 t, %1, %2;\n\tlop3.b32 %0, t, %1, %3, 0xA8;\n\t}"
+      : "=r"(r) : "r"(x), "n"(kShift), "n"(kMask));
+  return r;
 }
-__device__ __forceinline__ void decode_word(uint32_t w, uint32_t (&u)[4], uint32_t (&u127)[4]) {
-  constexpr uint32_t kLutU = 0xFF000001u;     // bytes for codes 0,1,2,3: +1, 0, 0, -1
-  constexpr uint32_t kLutU127 = 0x8100007Fu;  // +127, 0, 0, -127
-  const uint32_t n_lo = codes_to_nibbles(w);
-  const uint32_t n_hi = codes_to_nibbles(w >> 16);
-  const uint32_t sel[4] = {n_lo & 0xFFFFu, n_lo >> 16, n_hi & 0xFFFFu, n_hi >> 16};
+__device__ __forceinline__ void codes_to_nibbles(uint32_t w, uint32_t& lo, uint32_t& hi) {
+  const uint32_t a = __byte_perm(w, 0u, 0x4140);  // byte 0 -> bits 0-7, byte 1 -> bits 16-23
+  const uint32_t b = __byte_perm(w, 0u, 0x4342);  // bytes 2, 3
+  lo = spread_step<2, 0x33333333u>(spread_step<4, 0x0F0F0F0Fu>(a));
+  hi = spread_step<2, 0x33333333u>(spread_step<4, 0x0F0F0F0Fu>(b));
+}
+// the table as a register operand (PRMT reads its data from registers; without this the
+// compiler re-materialises the immediate before every PRMT)
+__device__ __forceinline__ uint32_t reg_const(uint32_t v) {
+  uint32_t r;
+  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+  return r;
+}
+// PRMT without the intrinsic's `& 0x7777` on the selector (the nibbles' bit 3 is already 0)
+__device__ __forceinline__ uint32_t prmt_lut(uint32_t lut, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, 0, %2;" : "=r"(r) : "r"(lut), "r"(sel));
+  return r;
+}
+template <bool kWith127 = true>
+__device__ __forceinline__ void decode_word(uint32_t w, uint32_t (&u)[4], uint32_t (&u127)[4],
+                                            uint32_t lut_u = 0xFF000001u,      // codes 0..3: +1, 0, 0, -1
+                                            uint32_t lut_u127 = 0x8100007Fu) {  // +127, 0, 0, -127
+  uint32_t n_lo, n_hi;
+  codes_to_nibbles(w, n_lo, n_hi);
+  const uint32_t sel[4] = {n_lo, n_lo >> 16, n_hi, n_hi >> 16};  // PRMT reads selector bits 0-15
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    u[i] = __byte_perm(kLutU, 0u, sel[i]);
-    u127[i] = __byte_perm(kLutU127, 0u, sel[i]);
+    u[i] = prmt_lut(lut_u, sel[i]);
+    if constexpr (kWith127) u127[i] = prmt_lut(lut_u127, sel[i]);
   }
 }
 
 // 16 packed codes -> 16 int8 missing flags (code 01 -> 1, else 0), as decode_word's layout.
 __device__ __forceinline__ void decode_word_missing(uint32_t w, uint32_t (&mk)[4]) {
   constexpr uint32_t kLutMiss = 0x00000100u;  // bytes for codes 0,1,2,3: 0, 1, 0, 0
-  const uint32_t n_lo = codes_to_nibbles(w);
-  const uint32_t n_hi = codes_to_nibbles(w >> 16);
-  const uint32_t sel[4] = {n_lo & 0xFFFFu, n_lo >> 16, n_hi & 0xFFFFu, n_hi >> 16};
+  uint32_t n_lo, n_hi;
+  codes_to_nibbles(w, n_lo, n_hi);
+  const uint32_t sel[4] = {n_lo, n_lo >> 16, n_hi, n_hi >> 16};
 #pragma unroll
-  for (int i = 0; i < 4; ++i) mk[i] = __byte_perm(kLutMiss, 0u, sel[i]);
+  for (int i = 0; i < 4; ++i) mk[i] = prmt_lut(kLutMiss, sel[i]);
+}
+
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
 
 // Running per-phenotype max |r| (min-p sidecar, only when ep.max_abs_r is set): the fp32
@@ -732,6 +757,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<MODE>::kThreadsM
       const int r = t_dec / (4 / kWords);
       const int c_first = (t_dec % (4 / kWords)) * kWords;
       const uint32_t sw = (static_cast<uint32_t>(r) >> 1) & 3u;
+      const uint32_t lut_u = reg_const(0xFF000001u), lut_u127 = reg_const(0x8100007Fu);
       uint32_t s = 0, ph = 0;
       for (int t = cid; t < n_tiles; t += n_clusters) {
         for (int kb = 0; kb < n_kb; ++kb) {
@@ -749,15 +775,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<MODE>::kThreadsM
             words[0] = w.x;
             words[1] = w.y;
           }
+          const uint32_t st_a = smem_u32(st);
 #pragma unroll
           for (int i = 0; i < kWords; ++i) {
             const int c = c_first + i;
             uint32_t u[4], u7[4];
-            decode_word(words[i], u, u7);
+            decode_word<!C::NO127>(words[i], u, u7, lut_u, lut_u127);
             const uint32_t off = r * 64 + ((c ^ sw) << 4);
-            *reinterpret_cast<uint4*>(st + C::kOffV + off) = make_uint4(u[0], u[1], u[2], u[3]);
-            if constexpr (!C::NO127)
-              *reinterpret_cast<uint4*>(st + C::kOffV127 + off) = make_uint4(u7[0], u7[1], u7[2], u7[3]);
+            st_shared_v4(st_a + C::kOffV + off, u[0], u[1], u[2], u[3]);
+            if constexpr (!C::NO127) st_shared_v4(st_a + C::kOffV127 + off, u7[0], u7[1], u7[2], u7[3]);
           }
           fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the tensor core
           __syncwarp();
