@@ -39,6 +39,10 @@
 #include <cstdlib>
 
 #include "assoc.cuh"
+
+#ifndef PG_DEC_TEAMS
+#define PG_DEC_TEAMS 2
+#endif
 #include "pg_ptx.cuh"
 
 namespace pg {
@@ -100,11 +104,14 @@ struct Cfg {
   static constexpr bool WIDE = MODE == kWide || MODE == kWide3 || MODE == kWide3Two || MODE == kWide4Two || TRANS;
   static constexpr int kStages =
       (TRANS || MODE == kWide3Two || MODE == kWide4Two) ? 9 : (WIDE ? 7 : (MODE == kFused2 ? 8 : (TWO ? 6 : 5)));
-  // decoder warps: 4 (one thread per packed row). Measured on the two-limb C3 scan: 8 decoder
-  // warps with 12 epilogue warps 2.45e10 tests/s, with 16 epilogue warps (896 threads) 2.54e10,
-  // 4 + 16 (768 threads) 2.60e10; a separate 12-deep packed-tile ring 2.50e10
-  static constexpr int kDecWarps = 4;
-  static constexpr int kFirstEpiWarp = 4 + kDecWarps;
+  // decoder warps: 4 per team (one thread per packed row). Measured on the two-limb C3 scan
+  // (old decoder): 8 warps splitting each stage's rows with 12 epilogue warps 2.45e10 tests/s,
+  // with 16 epilogue warps 2.54e10, 4 + 16 2.60e10; a separate 12-deep packed-tile ring 2.50e10.
+  // Two teams of 4 taking alternate stages (896 threads, 66 registers): equal or slightly better
+  static constexpr int kDecWarps = 4;  // per team
+  // decoder teams taking alternate stages (each team's fence + arrive overlaps the other's decode)
+  static constexpr int kDecTeams = (MODE == kFused2) ? PG_DEC_TEAMS : 1;
+  static constexpr int kFirstEpiWarp = 4 + kDecWarps * kDecTeams;
   static constexpr int kEpiWarps = 16;  // 20 for the two-limb tile measured no faster (2.71 vs 2.73e10)
   static constexpr int kColGroups = kEpiWarps / 4;
   static constexpr int kThreadsM = 32 * (kFirstEpiWarp + kEpiWarps);  // 768
@@ -753,7 +760,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<MODE>::kThreadsM
       // 127v, as 4 swizzled 16-byte chunks each (SW64: chunk c of row r lives at
       // r*64 + ((c ^ ((r >> 1) & 3)) << 4)); kWords chunks per thread (4, or 2 with 8 warps)
       constexpr int kWords = 4 * 4 / C::kDecWarps;
-      const int t_dec = threadIdx.x - 128;
+      const int t_dec = (threadIdx.x - 128) % (32 * C::kDecWarps);
+      const int team = (threadIdx.x - 128) / (32 * C::kDecWarps);
+      uint32_t it = 0;
       const int r = t_dec / (4 / kWords);
       const int c_first = (t_dec % (4 / kWords)) * kWords;
       const uint32_t sw = (static_cast<uint32_t>(r) >> 1) & 3u;
@@ -761,6 +770,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<MODE>::kThreadsM
       uint32_t s = 0, ph = 0;
       for (int t = cid; t < n_tiles; t += n_clusters) {
         for (int kb = 0; kb < n_kb; ++kb) {
+          if (C::kDecTeams > 1 && static_cast<int>(it++ % C::kDecTeams) != team) {
+            if (++s == S) {
+              s = 0;
+              ph ^= 1;
+            }
+            continue;
+          }
           mbar_wait(&pk[s], ph);
           uint8_t* st = smem + s * C::kStageBytes;
           uint32_t words[kWords];
@@ -888,6 +904,11 @@ constexpr uint32_t kDefaultL2Codes = 1u | (1u << 2);  // panel and genotypes evi
 // genotype tiles stream past): DRAM per C3 launch 22 GB vs 49 GB for 74-tile
 // genotype-stationary groups (tools/dram_sweep.sh, ncu), with equal or better throughput.
 constexpr int kDefaultGroup = -2;
+// Two-limb GEMMs: a phenotype tile's limbs are 2/3 the bytes, so 4-tile slices (47 MB at
+// N 23k) still stay in L2, with the streamed genotype tiles evict_first: DRAM per C3 launch
+// 17.7 -> 12.0 GB, equal or better throughput (profiles/r2_c3_raster_sweep.txt, round 2b)
+constexpr uint32_t kDefaultL2CodesTwo = 1u | (2u << 2);
+constexpr int kDefaultGroupTwo = -4;
 
 template <int MODE>
 int launch_common(const CUtensorMap& tm_qh, const CUtensorMap& tm_q1, const CUtensorMap& tm_q0,
@@ -914,8 +935,9 @@ int launch_common(const CUtensorMap& tm_qh, const CUtensorMap& tm_q1, const CUte
     const char* e = std::getenv("PG_L2_CODES");
     return e ? std::atoi(e) : -1;
   }();
-  const int group_c = env_group != 0 ? env_group : kDefaultGroup;
-  const uint32_t l2_codes = env_l2 >= 0 ? static_cast<uint32_t>(env_l2) : kDefaultL2Codes;
+  const int group_c = env_group != 0 ? env_group : (Cfg<MODE>::TWO ? kDefaultGroupTwo : kDefaultGroup);
+  const uint32_t l2_codes =
+      env_l2 >= 0 ? static_cast<uint32_t>(env_l2) : (Cfg<MODE>::TWO ? kDefaultL2CodesTwo : kDefaultL2Codes);
   const int n_kb = static_cast<int>(k_pad / kTileK);
   constexpr int kSliceKb = static_cast<int>(kSliceK / kTileK);
   if (ep.x_accum == nullptr) {
