@@ -57,9 +57,23 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -> Path:
-    """Compile csrc/*.cu into the shared library (object files cached in build/)."""
+    """Compile csrc/*.cu into the shared library (object files cached in build/).
+
+    Processes that find the library stale at the same time (the ranks of a torchrun job)
+    serialise on a lock file; the later ones see the fresh library and return."""
     if not force and not _stale():
         return LIB_PATH
+    import fcntl
+
+    (REPO / "build").mkdir(parents=True, exist_ok=True)
+    with open(REPO / "build" / ".lock", "w") as lock:
+        fcntl.flock(lock, fcntl.LOCK_EX)
+        if not force and not _stale():
+            return LIB_PATH
+        return _build_locked(force, verbose)
+
+
+def _build_locked(force: bool, verbose: bool) -> Path:
     nvcc = _nvcc()
     obj_dir = REPO / "build" / "obj"
     obj_dir.mkdir(parents=True, exist_ok=True)
