@@ -61,6 +61,9 @@ def parse_args():
     ap.add_argument("--cpu-sample", type=int, default=4096, help="markers in the timed CPU-baseline sample")
     ap.add_argument("--ref-workers", type=int, default=2, help="reference arm: engine worker threads")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sync-panel", action="store_true",
+                    help="A/B: e2e uploads + prepares the whole panel before the first scan")
+    ap.add_argument("--panel-chunk", type=int, default=1280, help="phenotypes per pipelined panel chunk")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=3)
     ap.add_argument("--missing-share", type=float, default=0.0,
@@ -326,13 +329,19 @@ def our_arm(a) -> None:
         """rank 0 builds the resident panel; its limbs are broadcast once over NCCL; others import.
 
         raw_host = (Y [N, P], C [N, c]) host arrays: the public path (covariate basis on the
-        host, residualize + standardize + quantize on the device: engine.stage_panel)."""
+        host, residualize + standardize + quantize on the device). Y is page-locked, so the
+        pipelined upload (pg_ctx_set_panel_async) is used: phenotype chunks are prepared as
+        they land and the first batch's GEMM follows them chunk by chunk; the zero-variance
+        flags are checked once the step's scans are done (panel_checked)."""
         if rank == 0:
             if raw_host is not None:
                 y_raw, c_raw = raw_host
                 basis = build_covariate_basis(c_raw, True)
-                flat, _sd = ctx.prepare_panel(y_raw, basis.q)
-                ctx.commit_panel(np.nonzero(~flat)[0], gidx, n)
+                if a.sync_panel:
+                    flat, _sd = ctx.prepare_panel(y_raw, basis.q)
+                    ctx.commit_panel(np.nonzero(~flat)[0], gidx, n)
+                else:
+                    ctx.set_panel_async(y_raw, basis.q, gidx, n, chunk_cols=a.panel_chunk)
             else:
                 ctx.set_panel_device(ytil.data_ptr(), n, p, p, gidx, n)
         if world > 1:
@@ -481,6 +490,10 @@ def our_arm(a) -> None:
                     d2h += r.cand_rows.size * 40 + r.n_markers * 25
             r = ctx.scan_staged((len(batches) - 1) % 2)
             d2h += r.cand_rows.size * 40 + r.n_markers * 25
+            if rank == 0 and not a.sync_panel:
+                flat, _sd = ctx.panel_async_wait()  # (complete long ago: no wait)
+                if flat.any():
+                    raise RuntimeError("synthetic panel has zero-variance phenotypes")
             return h2d, d2h
 
         e2e_step()

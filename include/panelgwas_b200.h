@@ -96,6 +96,20 @@ PG_API int pg_ctx_commit_panel(pg_ctx* ctx, const int64_t* kept_cols, int64_t n_
                                const int64_t* geno_row_index, int64_t n_samples_src);
 /* Copy the prepared (standardized, uncompacted) panel back: out f64 [n_kept, n_pheno]. */
 PG_API int pg_ctx_fetch_prepared_panel(pg_ctx* ctx, double* out);
+/* Pipelined prepare + commit of ALL columns (the same reference steps as
+ * pg_ctx_prepare_panel + pg_ctx_commit_panel with kept_cols = every column): `y` (page-locked
+ * host memory) is uploaded in chunks of `chunk_cols` phenotypes (rounded up to 256), each
+ * prepared and quantized as it lands, and the call returns at once. The next scan's GEMM
+ * runs chunk by chunk as the chunks become ready, so the upload overlaps the first batch.
+ * Without zero-variance columns the panel is bit-identical to the synchronous path; a
+ * zero-variance column stays in the panel with r = 0 (the caller drops it, or uses the
+ * synchronous path). pg_ctx_panel_async_wait returns the zero-variance flags and sd
+ * (as pg_ctx_prepare_panel) once the preparation is complete; non-finite input ->
+ * PG_ERR_INVALID there. */
+PG_API int pg_ctx_set_panel_async(pg_ctx* ctx, const double* y, int64_t n_kept, int64_t n_pheno, int64_t ld,
+                                  const double* basis_q, int64_t rank, const int64_t* geno_row_index,
+                                  int64_t n_samples_src, int64_t chunk_cols);
+PG_API int pg_ctx_panel_async_wait(pg_ctx* ctx, uint8_t* zero_variance, double* sd);
 
 /* Upload the standardized phenotype panel once; it stays resident in HBM as
  * three int8 limb planes [P_pad, K_pad] (q = 32385 qH + 127 q1 + q0, 23-bit

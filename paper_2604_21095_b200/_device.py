@@ -131,6 +131,37 @@ class DeviceContext:
             self._prep_shape = (n, p)
         return flat.astype(bool), sd
 
+    def set_panel_async(self, y: np.ndarray, basis_q: np.ndarray | None, geno_row_index: np.ndarray,
+                        n_samples_src: int, chunk_cols: int = 1280) -> None:
+        """Pipelined prepare + commit of every column (pg_ctx_set_panel_async): `y` must be a
+        C-contiguous f64 view of page-locked memory (e.g. a pinned torch tensor's .numpy())
+        and stay alive until panel_async_wait(); returns at once, the next scan's GEMM
+        overlaps the upload."""
+        if y.dtype != np.float64 or y.ndim != 2 or not y.flags["C_CONTIGUOUS"]:
+            raise ValueError("expected a C-contiguous float64 (samples x phenotypes) matrix")
+        n, p = y.shape
+        q = None
+        rank = 0
+        if basis_q is not None and basis_q.shape[1]:
+            q = np.ascontiguousarray(basis_q, dtype=np.float64)
+            rank = q.shape[1]
+        gidx = np.ascontiguousarray(geno_row_index, dtype=np.int64)
+        with self.lock:
+            call("pg_ctx_set_panel_async", self._h, ptr(y), n, p, p, ptr(q), rank, ptr(gidx), int(n_samples_src),
+                 int(chunk_cols))
+            self.n_pheno = p
+            self.beta_on = False
+            self._async_shape = (n, p)
+
+    def panel_async_wait(self) -> tuple[np.ndarray, np.ndarray]:
+        """(zero-variance flags, sd) of the pipelined panel once its preparation is complete."""
+        p = self._async_shape[1]
+        flat = np.zeros(p, dtype=np.uint8)
+        sd = np.zeros(p, dtype=np.float64)
+        with self.lock:
+            call("pg_ctx_panel_async_wait", self._h, ptr(flat), ptr(sd))
+        return flat.astype(bool), sd
+
     def fetch_prepared_panel(self) -> np.ndarray:
         out = np.empty(self._prep_shape, dtype=np.float64)
         with self.lock:

@@ -80,6 +80,11 @@ struct AssocEpilogue {
   const float4* mpack;
   long long* cand_xm;  // wide two-limb candidates: X'_m (the missing row's deferred-limb sum comes later)
   int side_two;        // the side GEMM ran two limbs: side_x holds Mq' (refine_two_limb adds sum_missing q0)
+  // Phenotype-tile range of this launch (pipelined panel, pg_ctx_set_panel_async: the first
+  // batch's GEMM runs one phenotype chunk at a time as the chunks land): tiles
+  // [pt_base, pt_base + pt_count) of kTileP phenotypes; pt_count 0 = every tile.
+  int pt_base;
+  int pt_count;
 };
 // (mu_f, invd_f, sqrt(ss_u + mu^2 n_miss) * invd_f) per marker slot [0, m_cap) for the
 // two-limb epilogues.

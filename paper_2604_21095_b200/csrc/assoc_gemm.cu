@@ -649,6 +649,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<MODE>::kThreadsM
       for (int t = cid; t < n_tiles; t += n_clusters) {
         int ct, pt;
         tile_coords(t, n_ctile, n_ptile, group_c, ct, pt);
+        pt += ep.pt_base;
         const int prow = C::TRANS ? pt * kTPheno + cr * kTHalfPheno : pt * kTileP + cr * kHalfP;
         const int grow = ct * C::kTileRows + cr * C::kHalfRows;
         for (int kb = 0; kb < n_kb; ++kb) {
@@ -823,6 +824,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<MODE>::kThreadsM
     for (int t = cid; t < n_tiles; t += n_clusters) {
       int ct, pt;
       tile_coords(t, n_ctile, n_ptile, group_c, ct, pt);
+      pt += ep.pt_base;
       const int pheno = pt * kTileP + cr * kHalfP + quarter * 32 + lane;
       mbar_wait_cluster(tfull, aph);
       tc_fence_after();
@@ -920,7 +922,10 @@ int launch_common(const CUtensorMap& tm_qh, const CUtensorMap& tm_q1, const CUte
   PG_CUDA_CHECK(cudaGetDevice(&dev));
   PG_CUDA_CHECK(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
   const int n_ctile = static_cast<int>(c_pad / Cfg<MODE>::kTileRows);
-  const int n_ptile = static_cast<int>(Cfg<MODE>::TRANS ? (p_pad + kTPheno - 1) / kTPheno : p_pad / kTileP);
+  const int n_ptile = ep.pt_count > 0 ? ep.pt_count
+                                      : static_cast<int>(Cfg<MODE>::TRANS ? (p_pad + kTPheno - 1) / kTPheno : p_pad / kTileP);
+  PG_REQUIRE(!Cfg<MODE>::TRANS || (ep.pt_base == 0 && ep.pt_count == 0), PG_ERR_INVALID,
+             "assoc: phenotype-tile ranges are not supported by the transposed GEMM");
   const int n_tiles = n_ctile * n_ptile;
   const int max_pairs = n_sm / 2;
   const int pairs = n_tiles < max_pairs ? n_tiles : max_pairs;

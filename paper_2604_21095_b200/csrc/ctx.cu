@@ -171,6 +171,22 @@ struct pg_ctx {
   pg::DBuf<uint8_t> prep_flat;
   pg::DBuf<int> prep_bad;
   pg::DBuf<int64_t> colmap;
+  // pipelined panel (pg_ctx_set_panel_async): phenotype column chunks are uploaded on
+  // panel_copy and prepared + quantized on panel_prep; the first scan's GEMM waits for each
+  // chunk in turn (chunk_ready) instead of for the whole panel
+  cudaStream_t panel_copy = nullptr, panel_prep = nullptr;
+  std::vector<cudaEvent_t> chunk_h2d, chunk_ready;
+  std::vector<int64_t> chunk_pt;  // phenotype-tile boundaries, n_chunks + 1
+  int64_t n_chunks = 0;
+  // Chunk copies are issued lazily, at most two in flight: host-to-device copies run in
+  // submission order across streams, so a batch staged after the panel call would otherwise
+  // wait for the whole panel upload.
+  int64_t chunk_issued = 0;
+  int64_t async_chunk = 0, async_ld = 0, async_rank = 0;
+  const double* async_y = nullptr;
+  bool panel_pending = false;  // the compute stream has not yet waited for every chunk
+  bool async_flags = false;    // zero-variance flags / sd / finiteness of the async panel on the device
+  cudaEvent_t panel_ev = nullptr;
 
   // scan parameters
   double df = 1.0;
@@ -290,9 +306,104 @@ int ctx_check(pg_ctx* c) {
   return PG_OK;
 }
 
-int upload_panel_common(pg_ctx* c, const double* d_y, int64_t n_kept, int64_t n_pheno, int64_t ld,
-                        const int64_t* h_gidx, int64_t n_src, const int64_t* d_cols = nullptr) {
-  PG_REQUIRE(n_kept >= 1 && n_pheno >= 1 && n_src >= n_kept && ld >= n_pheno, PG_ERR_INVALID,
+// Pipelined panel (pg_ctx_set_panel_async): enqueue chunk j — its H2D on panel_copy, then
+// prepare + quantize + q0 norms on panel_prep, ending in chunk_ready[j].
+int panel_issue(pg_ctx* c, int64_t j) {
+  cudaStream_t ps = c->panel_prep, cs = c->panel_copy;
+  const int64_t n_kept = c->prep_rows, n_pheno = c->prep_cols, chunk = c->async_chunk;
+  const int64_t c0 = j * chunk;
+  const int64_t w = std::min(chunk, n_pheno - c0);
+  const int64_t rows = j == c->n_chunks - 1 ? c->p_pad - c0 : w;  // panel rows (padding in the last chunk)
+  double* yj = c->ystage.p + static_cast<size_t>(n_kept) * c0;    // the chunk as its own [n_kept, w] matrix
+  PG_CUDA_CHECK(cudaMemcpy2DAsync(yj, sizeof(double) * w, c->async_y + c0, sizeof(double) * c->async_ld,
+                                  sizeof(double) * w, n_kept, cudaMemcpyHostToDevice, cs));
+  PG_CUDA_CHECK(cudaEventRecord(c->chunk_h2d[j], cs));
+  PG_CUDA_CHECK(cudaStreamWaitEvent(ps, c->chunk_h2d[j], 0));
+  pg::PanelPrepOut po;
+  po.mean = c->prep_mean.p + c0;
+  po.centre = c->prep_centre.p + c0;
+  po.sd = c->prep_sd.p + c0;
+  po.flat = c->prep_flat.p + c0;
+  po.bad = c->prep_bad.p + j;
+  PG_CHECK_STATUS(
+      pg::panel_prepare(yj, n_kept, w, c->async_rank ? c->prep_q.p : nullptr, c->async_rank, c->prep_scratch.p, po, ps));
+  // every column is kept (zero-variance ones quantize to 0): per column this is the
+  // synchronous prepare + commit of all columns, bit for bit
+  PanelPlanes pj;
+  pj.qh = c->qh.p;
+  pj.q1 = c->q1.p;
+  pj.q0 = c->q0.p;
+  const size_t off = static_cast<size_t>(c0) * c->k_pad;
+  pj.qh += off;
+  pj.q1 += off;
+  pj.q0 += off;
+  pj.scale_d = c->scale_d.p + c0;
+  pj.scale_f = c->scale_f.p + c0;
+  pj.cq = c->cq.p + c0;
+  pj.cq_f = c->cq_f.p + c0;
+  if (c->f64_panel) {
+    pj.qh_lo = c->qh_lo.p + off;
+    pj.q1_lo = c->q1_lo.p + off;
+    pj.q0_lo = c->q0_lo.p + off;
+    pj.cq_lo = c->cq_lo.p + c0;
+  }
+  PG_CHECK_STATUS(panel_quantize(yj, n_kept, w, w, nullptr, c->gidx.p, c->k_pad, rows, pj, c->maxabs.p + c0, ps));
+  PG_CHECK_STATUS(panel_q0_norms(c->q0.p + off, rows, c->k_pad, c->q0n.p + c0, ps));
+  PG_CUDA_CHECK(cudaEventRecord(c->chunk_ready[j], ps));
+  return PG_OK;
+}
+
+// Issue chunks up to `upto` (inclusive), keeping at most two chunk copies in flight
+// (blocks the host on an earlier chunk's copy when needed); upto < 0: only as many as can
+// be issued without blocking.
+int panel_pump(pg_ctx* c, int64_t upto) {
+  while (c->chunk_issued < c->n_chunks) {
+    const int64_t j = c->chunk_issued;
+    if (j >= 2) {
+      if (j > upto) {
+        const cudaError_t q = cudaEventQuery(c->chunk_h2d[j - 2]);
+        if (q == cudaErrorNotReady) break;
+        PG_CUDA_CHECK(q);
+      } else {
+        PG_CUDA_CHECK(cudaEventSynchronize(c->chunk_h2d[j - 2]));
+      }
+    } else if (j > upto && upto >= 0) {
+      break;
+    }
+    PG_CHECK_STATUS(panel_issue(c, j));
+    ++c->chunk_issued;
+  }
+  return PG_OK;
+}
+
+// A pipelined panel still being prepared: `s` waits for every chunk (work that reads the
+// whole panel), after which the panel is an ordinary resident panel for that stream.
+int panel_wait_all(pg_ctx* c, cudaStream_t s) {
+  if (c->panel_pending) {
+    PG_CHECK_STATUS(panel_pump(c, c->n_chunks - 1));
+    PG_CUDA_CHECK(cudaStreamWaitEvent(s, c->chunk_ready[c->n_chunks - 1], 0));
+    c->panel_pending = false;
+  }
+  return PG_OK;
+}
+
+// Before a new panel replaces the current one: no pipelined preparation may still write it.
+int panel_drain(pg_ctx* c) {
+  if (c->panel_prep) {
+    PG_CHECK_STATUS(panel_pump(c, c->n_chunks - 1));
+    PG_CUDA_CHECK(cudaStreamSynchronize(c->panel_prep));
+  }
+  c->panel_pending = false;
+  c->async_flags = false;
+  c->async_y = nullptr;
+  return PG_OK;
+}
+
+// Panel geometry, keep bits and limb buffers (shared by the synchronous and pipelined
+// uploads); the small index uploads go on `s`.
+int panel_geometry(pg_ctx* c, int64_t n_kept, int64_t n_pheno, int64_t n_src, const int64_t* h_gidx, cudaStream_t s,
+                   PanelPlanes& pp) {
+  PG_REQUIRE(n_kept >= 1 && n_pheno >= 1 && n_src >= n_kept, PG_ERR_INVALID,
              "invalid panel geometry n_kept=%lld n_pheno=%lld n_src=%lld", (long long)n_kept, (long long)n_pheno,
              (long long)n_src);
   std::vector<uint32_t> bits;
@@ -322,10 +433,10 @@ int upload_panel_common(pg_ctx* c, const double* d_y, int64_t n_kept, int64_t n_
   PG_CHECK_STATUS(c->maxabs.ensure(c->p_pad));
   PG_CHECK_STATUS(c->gidx.ensure(n_kept));
   PG_CHECK_STATUS(c->keep_bits.ensure(bits.size()));
-  PG_CUDA_CHECK(cudaMemcpyAsync(c->gidx.p, h_gidx, sizeof(int64_t) * n_kept, cudaMemcpyHostToDevice, c->stream));
-  PG_CUDA_CHECK(
-      cudaMemcpyAsync(c->keep_bits.p, bits.data(), sizeof(uint32_t) * bits.size(), cudaMemcpyHostToDevice, c->stream));
-  PanelPlanes pp;
+  // pageable sources: both copies are complete (staged) when the calls return
+  PG_CUDA_CHECK(cudaMemcpyAsync(c->gidx.p, h_gidx, sizeof(int64_t) * n_kept, cudaMemcpyHostToDevice, s));
+  PG_CUDA_CHECK(cudaMemcpyAsync(c->keep_bits.p, bits.data(), sizeof(uint32_t) * bits.size(), cudaMemcpyHostToDevice, s));
+  pp = PanelPlanes{};
   pp.qh = c->qh.p;
   pp.q1 = c->q1.p;
   pp.q0 = c->q0.p;
@@ -344,6 +455,16 @@ int upload_panel_common(pg_ctx* c, const double* d_y, int64_t n_kept, int64_t n_
     pp.cq_lo = c->cq_lo.p;
   }
   c->q0n_valid = false;
+  return PG_OK;
+}
+
+int upload_panel_common(pg_ctx* c, const double* d_y, int64_t n_kept, int64_t n_pheno, int64_t ld,
+                        const int64_t* h_gidx, int64_t n_src, const int64_t* d_cols = nullptr) {
+  PG_REQUIRE(ld >= n_pheno, PG_ERR_INVALID, "invalid panel leading dimension %lld < %lld", (long long)ld,
+             (long long)n_pheno);
+  PG_CHECK_STATUS(panel_drain(c));
+  PanelPlanes pp;
+  PG_CHECK_STATUS(panel_geometry(c, n_kept, n_pheno, n_src, h_gidx, c->stream, pp));
   PG_CHECK_STATUS(
       panel_quantize(d_y, n_kept, n_pheno, ld, d_cols, c->gidx.p, c->k_pad, c->p_pad, pp, c->maxabs.p, c->stream));
   PG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
@@ -509,6 +630,7 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
   auto run_side = [&](int level) -> int {
     if (!side_pending || side_done[level]) return PG_OK;
     side_done[level] = true;
+    PG_CHECK_STATUS(panel_wait_all(c, s));
     AssocEpilogue es{};
     es.rows_per_marker = 1;
     es.m_valid = n_side;
@@ -534,6 +656,7 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
   };
   auto run_gemm = [&](const AssocEpilogue& e) -> int {
     if (c->f64_panel) {
+      PG_CHECK_STATUS(panel_wait_all(c, s));
       // lo level first (partials only), then the hi level, whose statistics add the lo partials
       AssocEpilogue el = e;
       el.x_accum = c->xacc_lo.p;
@@ -549,9 +672,26 @@ int scan_common(pg_ctx* c, int kind, const uint8_t* d_data, int64_t m, int64_t p
       return run_gemm_on(eh, c->qh.p, c->q1.p, c->q0.p, c->p_pad);
     }
     PG_CHECK_STATUS(run_side(0));
+    if (c->panel_pending && !wide3t && e.x_accum == nullptr) {
+      // pipelined panel: one launch per phenotype chunk, each as soon as its chunk is ready,
+      // so the first batch's GEMM overlaps the upload of the later chunks
+      for (int64_t j = 0; j < c->n_chunks; ++j) {
+        PG_CHECK_STATUS(panel_pump(c, j));
+        PG_CUDA_CHECK(cudaStreamWaitEvent(s, c->chunk_ready[j], 0));
+        AssocEpilogue ej = e;
+        ej.pt_base = static_cast<int>(c->chunk_pt[j]);
+        ej.pt_count = static_cast<int>(c->chunk_pt[j + 1] - c->chunk_pt[j]);
+        PG_CHECK_STATUS(run_gemm_on(ej, c->qh.p, c->q1.p, c->q0.p, c->p_pad));
+        if (j) ++launches;
+      }
+      c->panel_pending = false;
+      return PG_OK;
+    }
+    PG_CHECK_STATUS(panel_wait_all(c, s));
     return run_gemm_on(e, c->qh.p, c->q1.p, c->q0.p, c->p_pad);
   };
   if (c->have_basis) {
+    PG_CHECK_STATUS(panel_wait_all(c, s));
     // K5: w = Q^T u_imp for every marker (exact side GEMM against the quantized basis)
     PG_CHECK_STATUS(c->wbuf.ensure(static_cast<size_t>(c_pad / R) * kTileP));
     PG_CHECK_STATUS(c->cand_count.ensure(1));
@@ -785,6 +925,15 @@ int pg_ctx_destroy(pg_ctx* c) {
   if (c == nullptr) return PG_OK;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
+  if (c->panel_prep) {
+    cudaStreamSynchronize(c->panel_prep);
+    cudaStreamSynchronize(c->panel_copy);
+    for (auto e : c->chunk_h2d) cudaEventDestroy(e);
+    for (auto e : c->chunk_ready) cudaEventDestroy(e);
+    cudaEventDestroy(c->panel_ev);
+    cudaStreamDestroy(c->panel_prep);
+    cudaStreamDestroy(c->panel_copy);
+  }
   for (auto* b : {&c->qh, &c->q1, &c->q0, &c->v, &c->v127, &c->skip}) b->release();
   for (auto* b : {&c->scale_d, &c->maxabs, &c->ystage, &c->rbar_in, &c->sum_d, &c->af, &c->var, &c->mu_d,
                   &c->invd_d, &c->cand_r, &c->cand_r_sorted, &c->cand_t, &c->cand_p, &c->full_r, &c->scratch_a,
@@ -844,6 +993,7 @@ int pg_ctx_set_panel(pg_ctx* c, const double* ytil, int64_t n_kept, int64_t n_ph
   PG_CHECK_STATUS(ctx_check(c));
   PG_REQUIRE(ytil != nullptr && geno_row_index != nullptr, PG_ERR_INVALID, "pg_ctx_set_panel: null input");
   PG_REQUIRE(ld >= n_pheno && n_pheno >= 1 && n_kept >= 1, PG_ERR_INVALID, "pg_ctx_set_panel: bad shape");
+  PG_CHECK_STATUS(panel_drain(c));
   PG_CHECK_STATUS(c->ystage.ensure(static_cast<size_t>(n_kept) * n_pheno));
   if (ld == n_pheno) {
     PG_CUDA_CHECK(cudaMemcpyAsync(c->ystage.p, ytil, sizeof(double) * n_pheno * n_kept, cudaMemcpyHostToDevice,
@@ -907,6 +1057,7 @@ int pg_ctx_prepare_panel(pg_ctx* c, const double* y, int64_t n_kept, int64_t n_p
              "pg_ctx_prepare_panel: null input");
   PG_REQUIRE(n_kept >= 1 && n_pheno >= 1 && ld >= n_pheno && rank >= 0, PG_ERR_INVALID,
              "pg_ctx_prepare_panel: bad shape");
+  PG_CHECK_STATUS(panel_drain(c));
   cudaStream_t s = c->stream;
   PG_CHECK_STATUS(c->ystage.ensure(static_cast<size_t>(n_kept) * n_pheno));
   if (ld == n_pheno) {
@@ -941,6 +1092,92 @@ int pg_ctx_prepare_panel(pg_ctx* c, const double* y, int64_t n_kept, int64_t n_p
   c->have_prepared = true;
   c->prep_rows = n_kept;
   c->prep_cols = n_pheno;
+  return PG_OK;
+}
+
+int pg_ctx_set_panel_async(pg_ctx* c, const double* y, int64_t n_kept, int64_t n_pheno, int64_t ld,
+                           const double* basis_q, int64_t rank, const int64_t* geno_row_index, int64_t n_samples_src,
+                           int64_t chunk_cols) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(y != nullptr && geno_row_index != nullptr && (rank == 0 || basis_q != nullptr), PG_ERR_INVALID,
+             "pg_ctx_set_panel_async: null input");
+  PG_REQUIRE(n_kept >= 1 && n_pheno >= 1 && ld >= n_pheno && rank >= 0 && chunk_cols >= 1, PG_ERR_INVALID,
+             "pg_ctx_set_panel_async: bad shape");
+  cudaPointerAttributes attr{};
+  const bool pinned = cudaPointerGetAttributes(&attr, y) == cudaSuccess && attr.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+  PG_REQUIRE(pinned, PG_ERR_INVALID,
+             "pg_ctx_set_panel_async: the raw panel must be in page-locked host memory (else pg_ctx_prepare_panel)");
+  PG_CHECK_STATUS(panel_drain(c));
+  if (c->panel_prep == nullptr) {
+    PG_CUDA_CHECK(cudaStreamCreateWithFlags(&c->panel_copy, cudaStreamNonBlocking));
+    PG_CUDA_CHECK(cudaStreamCreateWithFlags(&c->panel_prep, cudaStreamNonBlocking));
+    PG_CUDA_CHECK(cudaEventCreateWithFlags(&c->panel_ev, cudaEventDisableTiming));
+  }
+  cudaStream_t ps = c->panel_prep, cs = c->panel_copy;
+  // earlier scans on the compute stream may still read the current panel
+  PG_CUDA_CHECK(cudaEventRecord(c->panel_ev, c->stream));
+  PG_CUDA_CHECK(cudaStreamWaitEvent(ps, c->panel_ev, 0));
+  PG_CUDA_CHECK(cudaStreamWaitEvent(cs, c->panel_ev, 0));
+  PanelPlanes pp;
+  PG_CHECK_STATUS(panel_geometry(c, n_kept, n_pheno, n_samples_src, geno_row_index, ps, pp));
+  const int64_t chunk = round_up(std::max<int64_t>(chunk_cols, kTileP), kTileP);
+  const int64_t n_ch = (n_pheno + chunk - 1) / chunk;
+  while (static_cast<int64_t>(c->chunk_ready.size()) < n_ch) {
+    cudaEvent_t a, b;
+    PG_CUDA_CHECK(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+    PG_CUDA_CHECK(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+    c->chunk_h2d.push_back(a);
+    c->chunk_ready.push_back(b);
+  }
+  c->chunk_pt.assign(n_ch + 1, 0);
+  for (int64_t j = 0; j < n_ch; ++j) {
+    c->chunk_pt[j] = j * chunk / kTileP;
+    c->chunk_pt[j + 1] = j == n_ch - 1 ? c->p_pad / kTileP : (j + 1) * chunk / kTileP;
+  }
+  PG_CHECK_STATUS(c->ystage.ensure(static_cast<size_t>(n_kept) * n_pheno));
+  if (rank > 0) {
+    PG_CHECK_STATUS(c->prep_q.ensure(static_cast<size_t>(n_kept) * rank));
+    PG_CUDA_CHECK(cudaMemcpyAsync(c->prep_q.p, basis_q, sizeof(double) * n_kept * rank, cudaMemcpyHostToDevice, ps));
+  }
+  PG_CHECK_STATUS(c->prep_scratch.ensure(pg::panel_prep_scratch_doubles(n_kept, std::min(chunk, n_pheno), rank)));
+  for (auto* b : {&c->prep_mean, &c->prep_centre, &c->prep_sd}) PG_CHECK_STATUS(b->ensure(n_pheno));
+  PG_CHECK_STATUS(c->prep_flat.ensure(n_pheno));
+  PG_CHECK_STATUS(c->prep_bad.ensure(n_ch));
+  PG_CHECK_STATUS(c->q0n.ensure(c->p_pad));
+  c->prep_rows = n_kept;
+  c->prep_cols = n_pheno;
+  c->async_chunk = chunk;
+  c->async_ld = ld;
+  c->async_rank = rank;
+  c->async_y = y;
+  c->chunk_issued = 0;
+  c->n_chunks = n_ch;
+  PG_CHECK_STATUS(panel_pump(c, 1));  // the first two chunks; the rest as they are needed
+  c->panel_pending = true;
+  c->async_flags = true;
+  c->q0n_valid = true;
+  c->have_prepared = false;
+  c->have_panel = true;
+  c->have_scan = false;
+  c->have_basis = false;
+  c->beta_on = false;
+  return PG_OK;
+}
+
+int pg_ctx_panel_async_wait(pg_ctx* c, uint8_t* zero_variance, double* sd) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(c->async_flags, PG_ERR_STATE, "pg_ctx_panel_async_wait: no pipelined panel (pg_ctx_set_panel_async)");
+  PG_CHECK_STATUS(panel_pump(c, c->n_chunks - 1));
+  cudaStream_t ps = c->panel_prep;
+  std::vector<int> bad(static_cast<size_t>(c->n_chunks), 0);
+  PG_CUDA_CHECK(cudaMemcpyAsync(bad.data(), c->prep_bad.p, sizeof(int) * c->n_chunks, cudaMemcpyDeviceToHost, ps));
+  if (zero_variance)
+    PG_CUDA_CHECK(cudaMemcpyAsync(zero_variance, c->prep_flat.p, c->prep_cols, cudaMemcpyDeviceToHost, ps));
+  if (sd) PG_CUDA_CHECK(cudaMemcpyAsync(sd, c->prep_sd.p, sizeof(double) * c->prep_cols, cudaMemcpyDeviceToHost, ps));
+  PG_CUDA_CHECK(cudaStreamSynchronize(ps));
+  c->panel_pending = false;  // every chunk is complete: no stream needs to wait any more
+  for (int v : bad) PG_REQUIRE(!v, PG_ERR_INVALID, "standardize_columns requires finite input");
   return PG_OK;
 }
 
@@ -988,6 +1225,7 @@ int pg_ctx_panel_bytes(pg_ctx* c, int64_t* bytes) {
 int pg_ctx_export_panel(pg_ctx* c, void* d_dst) {
   PG_CHECK_STATUS(ctx_check(c));
   PG_REQUIRE(c->have_panel, PG_ERR_STATE, "no panel");
+  PG_CHECK_STATUS(panel_wait_all(c, c->stream));
   uint8_t* d = static_cast<uint8_t*>(d_dst);
   const size_t plane = static_cast<size_t>(c->p_pad) * c->k_pad;
   const size_t pp = static_cast<size_t>(c->p_pad);
@@ -1014,6 +1252,7 @@ int pg_ctx_import_panel(pg_ctx* c, const void* d_src, int64_t n_kept, int64_t n_
                         const int64_t* geno_row_index, int64_t n_samples_src) {
   PG_CHECK_STATUS(ctx_check(c));
   PG_REQUIRE(d_src != nullptr && geno_row_index != nullptr, PG_ERR_INVALID, "pg_ctx_import_panel: null input");
+  PG_CHECK_STATUS(panel_drain(c));
   // geometry + keep mask exactly as set_panel would build them
   std::vector<uint32_t> bits;
   c->n_src = n_samples_src;
@@ -1102,6 +1341,7 @@ int pg_ctx_set_scan(pg_ctx* c, double df, int mode, const double* r_bar) {
 int pg_ctx_set_basis(pg_ctx* c, const double* q, int64_t n_kept, int64_t rank) {
   PG_CHECK_STATUS(ctx_check(c));
   PG_REQUIRE(c->have_panel, PG_ERR_STATE, "pg_ctx_set_basis: set the panel first");
+  PG_CHECK_STATUS(panel_wait_all(c, c->stream));
   if (q == nullptr || rank <= 1) {
     c->have_basis = false;
     return PG_OK;

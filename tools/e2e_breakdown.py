@@ -56,6 +56,15 @@ def main():
 
         t_prep, _ = wall(prep)
         t_commit, _ = wall(lambda: ctx.commit_panel(np.nonzero(~state["flat"])[0], gidx, n))
+        t_async = {}
+        for chunk in (1280, 2560, 5120, 20480):
+            def run_async(chunk=chunk):
+                ctx.set_panel_async(y_np, basis.q, gidx, n, chunk_cols=chunk)
+                ctx.panel_async_wait()
+
+            t_async[chunk], _ = wall(run_async)
+        ctx.prepare_panel(y_np, basis.q)
+        ctx.commit_panel(np.nonzero(~state["flat"])[0], gidx, n)
         ctx.set_scan(df, _native.PG_MODE_THRESHOLD, np.full(p, threshold_premask(5e-8, df)))
         batches = [(s, min(db, m - s)) for s in range(0, m, db)]
 
@@ -79,6 +88,8 @@ def main():
     print(f"prepare_panel (Y H2D+prep)  {t_prep:8.1f} ms   (Y = {y_gb:.2f} GB; bare pinned H2D {h2d_ms:.1f} ms"
           f" = {y_gb / h2d_ms * 1e3:.1f} GB/s)")
     print(f"commit_panel (quantize)     {t_commit:8.1f} ms")
+    for chunk, t in t_async.items():
+        print(f"set_panel_async + wait, {chunk:5d}-phenotype chunks {t:8.1f} ms")
     print(f"staged scan of {m} markers {t_staged:8.1f} ms")
 
 
