@@ -76,6 +76,28 @@ def main():
             ctx.scan_staged((len(batches) - 1) % 2)
 
         t_staged, _ = wall(staged, 2)
+
+        def e2e_like(trace):
+            t0 = time.perf_counter()
+            b = build_covariate_basis(c_np, True)
+            ctx.set_panel_async(y_np, b.q, gidx, n)
+            trace.append(("panel call", time.perf_counter() - t0))
+            ctx.set_scan(df, _native.PG_MODE_THRESHOLD, np.full(p, threshold_premask(5e-8, df)))
+            for i, (s, c) in enumerate(batches):
+                ctx.stage(i % 2, _native.PG_GENO_BED, host_np[s:s + c], bpm)
+                if i:
+                    r = ctx.scan_staged((i - 1) % 2)
+                    trace.append((f"scan {i - 1} (gemm {r.gemm_ms:.1f} ms)", time.perf_counter() - t0))
+            r = ctx.scan_staged((len(batches) - 1) % 2)
+            trace.append((f"scan {len(batches) - 1} (gemm {r.gemm_ms:.1f} ms)", time.perf_counter() - t0))
+            ctx.panel_async_wait()
+            trace.append(("panel wait", time.perf_counter() - t0))
+
+        for _ in range(2):
+            trace = []
+            torch.cuda.synchronize()
+            e2e_like(trace)
+        e2e_trace = trace
         y_gb = y_np.nbytes / 1e9
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         d = torch.empty(yh.shape, dtype=torch.float64, device=dev)
@@ -91,6 +113,9 @@ def main():
     for chunk, t in t_async.items():
         print(f"set_panel_async + wait, {chunk:5d}-phenotype chunks {t:8.1f} ms")
     print(f"staged scan of {m} markers {t_staged:8.1f} ms")
+    print("e2e-like step with the pipelined panel (cumulative wall ms):")
+    for name, t in e2e_trace:
+        print(f"  {1e3 * t:8.1f}  {name}")
 
 
 if __name__ == "__main__":
