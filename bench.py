@@ -32,6 +32,7 @@ import statistics
 import subprocess
 import sys
 import threading
+from concurrent.futures import ThreadPoolExecutor
 import time
 from pathlib import Path
 
@@ -61,6 +62,8 @@ def parse_args():
     ap.add_argument("--cpu-sample", type=int, default=4096, help="markers in the timed CPU-baseline sample")
     ap.add_argument("--ref-workers", type=int, default=2, help="reference arm: engine worker threads")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--contexts", type=int, choices=[1, 2], default=2,
+                    help="device contexts the batches alternate between (2: host work overlaps kernels)")
     ap.add_argument("--sync-panel", action="store_true",
                     help="A/B: e2e uploads + prepares the whole panel before the first scan")
     ap.add_argument("--panel-chunk", type=int, default=1280, help="phenotypes per pipelined panel chunk")
@@ -116,6 +119,8 @@ def workload_config(a, world: int) -> dict:
         "l2_policy": "inputs larger than L2 (5.75 GB packed genotypes + 1.4 GB panel limbs per GPU per step)",
         "missing_calls": ({"marker_share": a.missing_share, "rate": a.missing_rate} if a.missing_share > 0
                           and a.missing_rate > 0 else None),
+        "device_contexts": a.contexts,  # batches alternate between contexts driven by host threads
+        "panel_upload": "synchronous" if a.sync_panel else f"pipelined ({a.panel_chunk}-phenotype chunks)",
     }
 
 
@@ -370,14 +375,52 @@ def our_arm(a) -> None:
     stream = torch.cuda.ExternalStream(ctx.stream_handle(), device=dev)
     batches = [(s, min(a.device_batch, m - s)) for s in range(0, m, a.device_batch)]
 
+    # Two contexts (default): batches alternate between two DeviceContexts driven by two host
+    # threads (the C ABI releases the GIL), so one context's host work between batches (result
+    # fetch, candidate-count round trips) overlaps the other's kernels; the second context
+    # imports the first one's panel (device to device).
+    ctx2 = stream2 = None
+    pool = None
+    if a.contexts == 2:
+        ctx2 = DeviceContext(local)
+        if a.no_missing_side:
+            ctx2.set_missing_side_gemm(False)
+        pbuf = torch.empty(ctx.panel_bytes(), dtype=torch.uint8, device=dev)
+        ctx.export_panel(pbuf.data_ptr())
+        torch.cuda.synchronize()
+        ctx2.import_panel(pbuf.data_ptr(), n, p, gidx, n)
+        ctx2.set_scan(df, _native.PG_MODE_THRESHOLD, rbar)
+        del pbuf
+        stream2 = torch.cuda.ExternalStream(ctx2.stream_handle(), device=dev)
+        pool = ThreadPoolExecutor(max_workers=2)
+
+    def alternate(work, items):
+        """work(ctx, k, item) for every item: item i on context i % 2 (or all on ctx)."""
+        if ctx2 is None:
+            return [work(ctx, 0, it) for it in items]
+        out = [None] * len(items)
+
+        def lane(k):
+            for i in range(k, len(items), 2):
+                out[i] = work((ctx, ctx2)[k], k, items[i])
+
+        for f in [pool.submit(lane, 0), pool.submit(lane, 1)]:
+            f.result()
+        return out
+
     def scan_step_device():
         stats = {"gemm_ms": 0.0, "hits": 0, "launches": 0, "d2h": 0}
-        for s, c in batches:
-            r = ctx.scan_device(_native.PG_GENO_BED, packed.data_ptr() + s * pitch, c, bpm, pitch)
-            stats["gemm_ms"] += r.gemm_ms
-            stats["hits"] += int(np.count_nonzero(r.cand_p <= a.p_threshold))
-            stats["launches"] += r.launches
-            stats["d2h"] += r.cand_rows.size * 40 + c * 25
+
+        def one(cx, _k, sc):
+            s, c = sc
+            r = cx.scan_device(_native.PG_GENO_BED, packed.data_ptr() + s * pitch, c, bpm, pitch)
+            return r.gemm_ms, int(np.count_nonzero(r.cand_p <= a.p_threshold)), r.launches, r.cand_rows.size * 40 + c * 25
+
+        for g, h, ln, d in alternate(one, batches):
+            stats["gemm_ms"] += g
+            stats["hits"] += h
+            stats["launches"] += ln
+            stats["d2h"] += d
         return stats
 
     def timed(fn, steps):
@@ -388,6 +431,8 @@ def our_arm(a) -> None:
         torch.cuda.synchronize()
         ev0.record(stream)
         out = [fn() for _ in range(steps)]
+        if stream2 is not None:
+            stream.wait_stream(stream2)  # the end event follows both contexts' work
         ev1.record(stream)
         ev1.synchronize()
         torch.cuda.synchronize()
@@ -408,6 +453,15 @@ def our_arm(a) -> None:
     gemm_ms = sum(o["gemm_ms"] for o in outs)
     launches = sum(o["launches"] for o in outs)
     hits = outs[-1]["hits"]
+    if ctx2 is not None:
+        # with two contexts a GEMM's event span can include waiting for the other context's
+        # GEMM to leave the SMs: the kernel's own duration (roofline) comes from the same
+        # steps run on one context
+        gemm_ms = 0.0
+        for _ in range(a.steps):
+            for s0, c0 in batches:
+                gemm_ms += ctx.scan_device(_native.PG_GENO_BED, packed.data_ptr() + s0 * pitch, c0, bpm, pitch,
+                                           fetch=False).gemm_ms
 
     # roofline of the dominant kernel (assoc_i8_kernel): BASELINE accounting 2*N*M*P x2 (hi/lo) = 4*N*M*P
     flops = 4.0 * n * m * p * a.steps
@@ -477,19 +531,52 @@ def our_arm(a) -> None:
         del packed
         torch.cuda.empty_cache()
 
+        pbuf2 = torch.empty(ctx.panel_bytes(), dtype=torch.uint8, device=dev) if ctx2 is not None else None
+
+        panel_ready = threading.Event()
+
+        def e2e_lane(cx, k, items):
+            """One context's share of the step: the host-buffer C-ABI path, pipelined (the H2D
+            of its next batch overlaps the scan of its current one). With two contexts the
+            first exports the step's panel right after its first batch (the pipelined panel
+            is complete by then) and the second imports it (device to device)."""
+            h2d = d2h = 0
+
+            def hand_over():
+                if k == 0 and ctx2 is not None and not panel_ready.is_set():
+                    ctx.export_panel(pbuf2.data_ptr())
+                    panel_ready.set()
+
+            for j, (s, c) in enumerate(items):
+                cx.stage(j % 2, _native.PG_GENO_BED, host_np[s:s + c], bpm)
+                h2d += c * bpm
+                if j == 0 and k == 1:
+                    panel_ready.wait()
+                    cx.import_panel(pbuf2.data_ptr(), n, p, gidx, n)
+                    cx.set_scan(df, _native.PG_MODE_THRESHOLD, rbar)
+                if j:
+                    r = cx.scan_staged((j - 1) % 2)
+                    d2h += r.cand_rows.size * 40 + r.n_markers * 25
+                    hand_over()
+            if items:
+                r = cx.scan_staged((len(items) - 1) % 2)
+                d2h += r.cand_rows.size * 40 + r.n_markers * 25
+            hand_over()
+            return h2d, d2h
+
         def e2e_step():
             h2d = distribute_panel(raw) + (n * (p + N_COVARIATES + 1) * 8 if rank == 0 else 0)
             ctx.set_scan(df, _native.PG_MODE_THRESHOLD, rbar)
             d2h = 0
-            # public host-buffer C-ABI path, pipelined: H2D of batch i+1 overlaps the scan of batch i
-            for i, (s, c) in enumerate(batches):
-                ctx.stage(i % 2, _native.PG_GENO_BED, host_np[s:s + c], bpm)
-                h2d += c * bpm
-                if i:
-                    r = ctx.scan_staged((i - 1) % 2)
-                    d2h += r.cand_rows.size * 40 + r.n_markers * 25
-            r = ctx.scan_staged((len(batches) - 1) % 2)
-            d2h += r.cand_rows.size * 40 + r.n_markers * 25
+            if ctx2 is None:
+                h, d = e2e_lane(ctx, 0, batches)
+                h2d, d2h = h2d + h, d2h + d
+            else:
+                panel_ready.clear()
+                futs = [pool.submit(e2e_lane, (ctx, ctx2)[k], k, batches[k::2]) for k in range(2)]
+                for f in futs:
+                    h, d = f.result()
+                    h2d, d2h = h2d + h, d2h + d
             if rank == 0 and not a.sync_panel:
                 flat, _sd = ctx.panel_async_wait()  # (complete long ago: no wait)
                 if flat.any():
