@@ -61,6 +61,8 @@ def main():
     ap.add_argument("--distinct", type=int, default=0,
                     help="distinct markers in the resident batch = markers per launch (default: the engine's device "
                          "batch, 65,536 for PLINK and 8,192 for BGEN)")
+    ap.add_argument("--contexts", type=int, choices=[1, 2], default=2,
+                    help="C5 e2e: batches alternate between two device contexts on two host threads")
     a = ap.parse_args()
 
     import torch
@@ -132,15 +134,39 @@ def main():
         pinned.numpy()[:] = np.frombuffer(blob, np.uint8)
         host_blob = pinned.numpy()
 
-        def e2e_step():
+        ctxs = [ctx]
+        if a.contexts == 2:
+            from concurrent.futures import ThreadPoolExecutor
+
+            c2 = DeviceContext(0)
+            buf = torch.empty(ctx.panel_bytes(), dtype=torch.uint8, device=dev)
+            ctx.export_panel(buf.data_ptr())
+            torch.cuda.synchronize()
+            c2.import_panel(buf.data_ptr(), n, p, gidx, n)
+            c2.set_scan(df, _native.PG_MODE_THRESHOLD, np.full(p, threshold_premask(1e-4, df)))
+            del buf
+            ctxs.append(c2)
+            pool = ThreadPoolExecutor(max_workers=2)
+
+        def lane(cx, count):
             # staging of batch i+1 (H2D + GPU inflate) overlaps the scan of batch i
-            ctx.stage_bgen_begin(0, host_blob, offs, sizes)
-            for i in range(reps):
-                bad = ctx.stage_bgen_end(i % 2)
+            if count == 0:
+                return
+            cx.stage_bgen_begin(0, host_blob, offs, sizes)
+            for i in range(count):
+                bad = cx.stage_bgen_end(i % 2)
                 assert bad is None, bad
-                if i + 1 < reps:
-                    ctx.stage_bgen_begin((i + 1) % 2, host_blob, offs, sizes)
-                ctx.scan_staged(i % 2)
+                if i + 1 < count:
+                    cx.stage_bgen_begin((i + 1) % 2, host_blob, offs, sizes)
+                cx.scan_staged(i % 2)
+
+        def e2e_step():
+            if len(ctxs) == 1:
+                lane(ctx, reps)
+            else:
+                futs = [pool.submit(lane, ctxs[k], len(range(k, reps, 2))) for k in range(2)]
+                for f in futs:
+                    f.result()
 
         e2e_step()
         torch.cuda.synchronize()
@@ -152,10 +178,12 @@ def main():
         line["e2e"] = {"value": tests / sec, "unit": "tests/s", "s_per_step": sec,
                        "h2d_compressed_bytes_per_step": int(sizes.sum()) * reps,
                        "inflated_bytes_per_step": int((10 + 3 * n) * reps * batch),
-                       "path": "pinned compressed blocks -> pg_stage_bgen_begin/_end (GPU inflate, overlapped) -> pg_scan_staged"}
+                       "path": "pinned compressed blocks -> pg_stage_bgen_begin/_end (GPU inflate, overlapped) -> pg_scan_staged",
+                       "device_contexts": len(ctxs)}
         line["compressed_bytes_per_variant"] = float(sizes.mean())
     print(json.dumps(line), flush=True)
-    ctx.close()
+    for cx in ctxs if blocks is not None else [ctx]:
+        cx.close()
 
 
 if __name__ == "__main__":
