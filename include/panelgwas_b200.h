@@ -110,6 +110,10 @@ PG_API int pg_ctx_set_panel_async(pg_ctx* ctx, const double* y, int64_t n_kept, 
                                   const double* basis_q, int64_t rank, const int64_t* geno_row_index,
                                   int64_t n_samples_src, int64_t chunk_cols);
 PG_API int pg_ctx_panel_async_wait(pg_ctx* ctx, uint8_t* zero_variance, double* sd);
+/* Copy `src`'s resident panel (limbs, scales, sample map) into `dst` on the same device, device
+ * to device (export + import), so that two contexts can scan batches of one job in turn
+ * ("two contexts per GPU"). Both must have the same precision mode. */
+PG_API int pg_ctx_clone_panel(pg_ctx* dst, pg_ctx* src);
 
 /* Upload the standardized phenotype panel once; it stays resident in HBM as
  * three int8 limb planes [P_pad, K_pad] (q = 32385 qH + 127 q1 + q0, 23-bit

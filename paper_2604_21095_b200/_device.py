@@ -153,6 +153,13 @@ class DeviceContext:
             self.beta_on = False
             self._async_shape = (n, p)
 
+    def clone_panel_from(self, src: "DeviceContext") -> None:
+        """This context takes `src`'s resident panel, device to device (pg_ctx_clone_panel)."""
+        with src.lock, self.lock:
+            call("pg_ctx_clone_panel", self._h, src._h)
+            self.n_pheno = src.n_pheno
+            self.beta_on = False
+
     def panel_async_wait(self) -> tuple[np.ndarray, np.ndarray]:
         """(zero-variance flags, sd) of the pipelined panel once its preparation is complete."""
         p = self._async_shape[1]

@@ -1248,6 +1248,31 @@ int pg_ctx_export_panel(pg_ctx* c, void* d_dst) {
   return PG_OK;
 }
 
+int pg_ctx_clone_panel(pg_ctx* dst, pg_ctx* src) {
+  PG_CHECK_STATUS(ctx_check(src));
+  PG_REQUIRE(dst != nullptr && dst != src, PG_ERR_INVALID, "pg_ctx_clone_panel: need two distinct contexts");
+  PG_REQUIRE(src->have_panel, PG_ERR_STATE, "pg_ctx_clone_panel: the source context has no panel");
+  PG_REQUIRE(dst->device == src->device, PG_ERR_INVALID, "pg_ctx_clone_panel: contexts on different devices");
+  PG_REQUIRE(dst->f64_panel == src->f64_panel, PG_ERR_STATE,
+             "pg_ctx_clone_panel: set the same precision (pg_ctx_set_f64_panel) on both contexts");
+  int64_t bytes = 0;
+  PG_CHECK_STATUS(pg_ctx_panel_bytes(src, &bytes));
+  std::vector<int64_t> gidx(static_cast<size_t>(src->n_kept));
+  void* tmp = nullptr;
+  PG_CUDA_CHECK(cudaMalloc(&tmp, static_cast<size_t>(bytes)));
+  int rc = pg_ctx_export_panel(src, tmp);  // waits for a pipelined preparation; synchronous
+  if (rc == PG_OK) {
+    const cudaError_t e = cudaMemcpy(gidx.data(), src->gidx.p, sizeof(int64_t) * gidx.size(), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) {
+      pg::set_error("pg_ctx_clone_panel: %s", cudaGetErrorString(e));
+      rc = PG_ERR_CUDA;
+    }
+  }
+  if (rc == PG_OK) rc = pg_ctx_import_panel(dst, tmp, src->n_kept, src->n_pheno, gidx.data(), src->n_src);
+  cudaFree(tmp);
+  return rc;
+}
+
 int pg_ctx_import_panel(pg_ctx* c, const void* d_src, int64_t n_kept, int64_t n_pheno,
                         const int64_t* geno_row_index, int64_t n_samples_src) {
   PG_CHECK_STATUS(ctx_check(c));

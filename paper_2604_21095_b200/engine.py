@@ -371,27 +371,124 @@ def _switches() -> tuple:
     return tuple(sorted((k, v) for k, v in os.environ.items() if k.startswith(("PG_", "PANELGWAS_"))))
 
 
+_POOL_PER_DEVICE = 2  # a scan drives up to two contexts (_two_lane_loop)
+
+
 def _acquire_context(device):
     from ._device import DeviceContext
 
     key = _switches()
+    stale = []
+    ctx = None
     with _CTX_POOL_LOCK:
-        held = _CTX_POOL.pop(device, None)
-    if held is not None:
-        if held[0] == key:
-            return held[1]
-        held[1].close()
-    ctx = DeviceContext(device)
-    ctx.pool_key = key
+        held = _CTX_POOL.setdefault(device, [])
+        while held and ctx is None:
+            k, c = held.pop()
+            if k == key:
+                ctx = c
+            else:
+                stale.append(c)
+    for c in stale:
+        c.close()
+    if ctx is None:
+        ctx = DeviceContext(device)
+        ctx.pool_key = key
     return ctx
 
 
 def _release_context(device, ctx) -> None:
+    extra = None
     with _CTX_POOL_LOCK:
-        old = _CTX_POOL.pop(device, None)
-        _CTX_POOL[device] = (getattr(ctx, "pool_key", None), ctx)
-    if old is not None and old[1] is not ctx:
-        old[1].close()
+        held = _CTX_POOL.setdefault(device, [])
+        if any(c is ctx for _, c in held):
+            return
+        held.append((getattr(ctx, "pool_key", None), ctx))
+        if len(held) > _POOL_PER_DEVICE:
+            extra = held.pop(0)[1]
+    if extra is not None:
+        extra.close()
+
+
+def _two_contexts_wanted(config: ScanConfig) -> bool:
+    """THRESHOLD / FULL scans alternate batches between two device contexts (_two_lane_loop);
+    TOPK (per-batch bars from the writer's state) and PANELGWAS_CONTEXTS=1 use one."""
+    return config.output_mode is not OutputMode.TOPK and os.environ.get("PANELGWAS_CONTEXTS", "2") != "1"
+
+
+def _two_lane_loop(ctx, ctx2, plan, read_lane, stage_on, ready_on, dispatch, full_bufs, dtype, waits) -> float:
+    """Batches alternate between two device contexts, one host thread each: batch i runs on
+    context i % 2 (its reads, staging and scans pipelined as in the one-context loop), and
+    results are handed to `dispatch` strictly in batch order. While one context's thread
+    fetches results or waits for its turn, the other context's kernels keep the GPU busy.
+    Returns the host read time."""
+    seq = threading.Condition()
+    state = {"next": 0, "error": None, "t_read": 0.0}
+
+    def ordered_dispatch(i, res):
+        with seq:
+            while state["next"] != i and state["error"] is None:
+                seq.wait()
+            if state["error"] is not None:
+                return
+            try:
+                dispatch(i, res)
+            except BaseException as exc:
+                state["error"] = exc
+                raise
+            finally:
+                state["next"] = i + 1
+                seq.notify_all()
+
+    def scan_on(cx, slot, i):
+        t0 = time.perf_counter()
+        out = full_bufs[i % len(full_bufs)].array if full_bufs else None
+        res = cx.scan_staged(slot, full_elem_bytes=dtype.itemsize, full_out=out)
+        with seq:
+            waits["scan"] += time.perf_counter() - t0
+        return res
+
+    def lane(k):
+        cx = (ctx, ctx2)[k]
+        mine = list(range(k, len(plan), 2))
+        if not mine:
+            return
+        try:
+            with ThreadPoolExecutor(max_workers=1) as reader:
+                fut = reader.submit(read_lane, mine[0], 2 * k)
+                prev = None
+                for j, i in enumerate(mine):
+                    t0 = time.perf_counter()
+                    block, dt_read = fut.result()
+                    with seq:
+                        waits["read"] += time.perf_counter() - t0
+                        state["t_read"] += dt_read
+                    stage_on(cx, j % 2, block)
+                    if prev is not None:
+                        ordered_dispatch(prev[0], scan_on(cx, prev[1], prev[0]))
+                    if state["error"] is not None:
+                        return
+                    if j + 1 < len(mine):  # into the buffer of the batch just scanned
+                        fut = reader.submit(read_lane, mine[j + 1], 2 * k + (j + 1) % 2)
+                    ready_on(cx, j % 2, i)
+                    prev = (i, j % 2)
+                ordered_dispatch(prev[0], scan_on(cx, prev[1], prev[0]))
+        except BaseException as exc:
+            with seq:
+                if state["error"] is None:
+                    state["error"] = exc
+                seq.notify_all()
+            raise
+
+    with ThreadPoolExecutor(max_workers=2) as lanes:
+        futs = [lanes.submit(lane, k) for k in range(2)]
+        for f in futs:
+            try:
+                f.result()
+            except BaseException:
+                pass
+    if state["error"] is not None:
+        raise state["error"]
+    return state["t_read"]
 
 
 def run_scan(config: ScanConfig, marker_range: tuple[int, int] | None = None, panel_hook=None,
@@ -410,14 +507,17 @@ def run_scan(config: ScanConfig, marker_range: tuple[int, int] | None = None, pa
     # created on another thread
     init = ThreadPoolExecutor(max_workers=1)
     ctx_fut = init.submit(_acquire_context, config.device)
+    ctx2_fut = init.submit(_acquire_context, config.device) if _two_contexts_wanted(config) else None
     try:
         source = open_genotype_source(config.source)
     except BaseException:
         init.shutdown(wait=False)
         _close_when_done(ctx_fut)
+        if ctx2_fut is not None:
+            _close_when_done(ctx2_fut)
         raise
     try:
-        return _run_scan_open(config, source, wall0, init, ctx_fut, marker_range, panel_hook, prep_hook)
+        return _run_scan_open(config, source, wall0, init, ctx_fut, marker_range, panel_hook, prep_hook, ctx2_fut)
     finally:
         source.close()
 
@@ -430,7 +530,7 @@ def _close_when_done(ctx_fut) -> None:
 
 
 def _run_scan_open(config: ScanConfig, source, wall0: float, init, ctx_fut, marker_range=None, panel_hook=None,
-                   prep_hook=None) -> ScanSummary:
+                   prep_hook=None, ctx2_fut=None) -> ScanSummary:
     # the pinned read ring (~0.4 s per GB) is allocated on the init thread after the context,
     # also while the tables parse
     lo, hi = marker_range if marker_range is not None else (0, source.n_markers)
@@ -439,7 +539,8 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, init, ctx_fut, mark
                  else getattr(source, "bytes_per_marker", 0))
     # the batch only shrinks as phenotypes are added, so one phenotype bounds every ring slot
     ring_bytes = device_batch_size(config, max(hi - lo, 1), 1, source.n_samples) * row_bytes
-    ring_fut = init.submit(_pinned_buffers, [ring_bytes] * 3 if ring_bytes else [])
+    # 3 buffers for one context's pipeline; 4 (two per context) when two contexts alternate
+    ring_fut = init.submit(_pinned_buffers, [ring_bytes] * (4 if ctx2_fut is not None else 3) if ring_bytes else [])
     init.shutdown(wait=False)
     try:
         phases = {"start": time.perf_counter() - wall0}
@@ -451,9 +552,11 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, init, ctx_fut, mark
         # Precision.F64: the panel at two quantization levels (~46 bits), one exact GEMM each
         ctx.set_f64_panel(config.precision is Precision.F64)
     except BaseException:
-        for fut, release in ((ring_fut, _free_pinned), (ctx_fut, lambda c: c.close())):
+        for fut, release in ((ring_fut, _free_pinned), (ctx_fut, lambda c: c.close()),
+                             (ctx2_fut, lambda c: c.close())):
             try:
-                release(fut.result())
+                if fut is not None:
+                    release(fut.result())
             except Exception:
                 pass
         raise
@@ -494,6 +597,7 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, init, ctx_fut, mark
         raise
 
     scan_ok = False
+    ctx2 = None
     # A/B switches (results are identical either way); set on every scan since the context may
     # be a reused one
     ctx.set_fused_decode(os.environ.get("PANELGWAS_FUSED_DECODE", "1") != "0")
@@ -520,6 +624,26 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, init, ctx_fut, mark
         step = device_batch_size(config, hi - lo, n_pheno, source.n_samples)
         plan = [(lo + s0, c0) for s0, c0 in plan_batches(hi - lo, step)]
         read_kw = {"dtype": dtype} if config.source.format.value == "dense" else {}
+        if ctx2_fut is not None:
+            # a second context (created while the tables parsed) takes the panel device to
+            # device and scans every other batch (_two_lane loop below)
+            ctx2 = ctx2_fut.result()
+            if len(plan) >= 2:
+                ctx2.set_f64_panel(config.precision is Precision.F64)
+                ctx2.clone_panel_from(ctx)
+                if config.effect_sizes:
+                    ctx2.set_beta_scale(prep.pheno_sd)
+                ctx2.set_fused_decode(os.environ.get("PANELGWAS_FUSED_DECODE", "1") != "0")
+                ctx2.set_missing_side_gemm(os.environ.get("PANELGWAS_MISSING_SIDE_GEMM", "1") != "0")
+                ctx2.set_wide_digits(os.environ.get("PANELGWAS_WIDE_DIGITS", "1") != "0")
+                if config.residualize_genotypes and prep.basis.rank:
+                    ctx2.set_basis(prep.basis.q)
+                ctx2.set_scan(df, _MODE_CODE[config.output_mode], rbar)
+                if config.min_p_sidecar:
+                    ctx2.track_max_abs_r(True)
+            else:
+                _release_context(config.device, ctx2)
+                ctx2 = None
 
         # pinned ring of 3 host buffers + 2 device staging slots: the read of batch i+1 and
         # its H2D overlap the device scan of batch i. BGEN batches travel compressed and are
@@ -548,6 +672,31 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, init, ctx_fut, mark
         def staged_ready(i):
             if compressed:
                 bad = ctx.stage_bgen_end(i % 2)
+                if bad is not None:
+                    source.raise_block_error(plan[i][0] + bad[0], bad[1], bad[2], bad[3])
+
+        # two contexts (_two_lane_loop): context k reads into pinned buffers 2k, 2k+1 and stages
+        # into its own two slots
+        def read_lane(i, buf):
+            t0 = time.perf_counter()
+            s0, c0 = plan[i]
+            if compressed:
+                block = source.read_compressed_block(s0, c0, out=pinned[buf].array)
+            elif pinned is not None:
+                block = source.read_raw_block(s0, c0, out=pinned[buf].array)
+            else:
+                block = source.read_raw_block(s0, c0, **read_kw)
+            return block, time.perf_counter() - t0
+
+        def stage_on(cx, slot, block):
+            if compressed:
+                return cx.stage_bgen_begin(slot, *block)
+            kind, rows, row_bytes = block
+            return cx.stage(slot, kind, rows, row_bytes)
+
+        def ready_on(cx, slot, i):
+            if compressed:
+                bad = cx.stage_bgen_end(slot)
                 if bad is not None:
                     source.raise_block_error(plan[i][0] + bad[0], bad[1], bad[2], bad[3])
 
@@ -642,9 +791,12 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, init, ctx_fut, mark
             # FULL: t rows land in two pinned buffers used alternately. The writer holds at most
             # one batch (dispatch waits for it before handing over the next), so batch i's
             # buffer is free again by the time batch i+2 is fetched into it.
+            # (two contexts: batch i uses buffer i % 4 — the writer holds batch i-2 at most while
+            # the contexts fetch batches i-1 and i)
             full_bufs = []
             if config.output_mode is OutputMode.FULL and os.environ.get("PANELGWAS_FULL_PINNED") != "0":
-                full_bufs = [_native.PinnedBuffer(step * n_pheno * dtype.itemsize) for _ in range(2)]
+                full_bufs = [_native.PinnedBuffer(step * n_pheno * dtype.itemsize)
+                             for _ in range(4 if ctx2 is not None else 2)]
                 pinned_out.extend(full_bufs)
             n_scanned = [0]
 
@@ -662,24 +814,28 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, init, ctx_fut, mark
             switch_interval = sys.getswitchinterval()
             sys.setswitchinterval(2e-4)
             try:
-                with ThreadPoolExecutor(max_workers=1) as reader:
-                    fut = reader.submit(read, 0)
-                    pending = None
-                    for i in range(len(plan)):
-                        t0 = time.perf_counter()
-                        block, dt_read = fut.result()
-                        waits["read"] += time.perf_counter() - t0
-                        t_decode += dt_read
-                        t0 = time.perf_counter()
-                        staged[i % 2] = stage(i, block)
-                        waits["stage"] += time.perf_counter() - t0
-                        if i + 1 < len(plan):
-                            fut = reader.submit(read, i + 1)
-                        if pending is not None:
-                            dispatch(pending, scan(pending % 2))
-                        staged_ready(i)
-                        pending = i
-                    dispatch(pending, scan(pending % 2))
+                if ctx2 is not None:
+                    t_decode += _two_lane_loop(ctx, ctx2, plan, read_lane, stage_on, ready_on, dispatch, full_bufs,
+                                               dtype, waits)
+                else:
+                    with ThreadPoolExecutor(max_workers=1) as reader:
+                        fut = reader.submit(read, 0)
+                        pending = None
+                        for i in range(len(plan)):
+                            t0 = time.perf_counter()
+                            block, dt_read = fut.result()
+                            waits["read"] += time.perf_counter() - t0
+                            t_decode += dt_read
+                            t0 = time.perf_counter()
+                            staged[i % 2] = stage(i, block)
+                            waits["stage"] += time.perf_counter() - t0
+                            if i + 1 < len(plan):
+                                fut = reader.submit(read, i + 1)
+                            if pending is not None:
+                                dispatch(pending, scan(pending % 2))
+                            staged_ready(i)
+                            pending = i
+                        dispatch(pending, scan(pending % 2))
                 if emit_fut is not None:
                     emit_fut.result()
             finally:
@@ -689,19 +845,26 @@ def _run_scan_open(config: ScanConfig, source, wall0: float, init, ctx_fut, mark
             if config.min_p_sidecar:
                 # per-phenotype max |r| over every scanned marker (fused into the GEMM epilogue)
                 max_abs_r = ctx.max_abs_r()
+                if ctx2 is not None:
+                    max_abs_r = np.maximum(max_abs_r, ctx2.max_abs_r())
                 max_abs_t = ctx.t_from_r(max_abs_r, df)
                 min_p, _ = ctx.p_from_t(max_abs_t, df)
         finally:
             if pinned is not None or pinned_out:
                 ctx.sync()
+                if ctx2 is not None:
+                    ctx2.sync()
                 for b in (pinned or []) + pinned_out:
                     b.close()
         scan_ok = True
     finally:
-        if scan_ok:
-            _release_context(config.device, ctx)  # kept for the next scan of this process
-        else:
-            ctx.close()
+        for cx in (ctx, ctx2):
+            if cx is None:
+                continue
+            if scan_ok:
+                _release_context(config.device, cx)  # kept for the next scan of this process
+            else:
+                cx.close()
 
     phases["scan_loop_done"] = time.perf_counter() - wall0
     phases["loop_main_thread_waits"] = waits
