@@ -410,9 +410,13 @@ def _release_context(device, ctx) -> None:
 
 
 def _two_contexts_wanted(config: ScanConfig) -> bool:
-    """THRESHOLD / FULL scans alternate batches between two device contexts (_two_lane_loop);
-    TOPK (per-batch bars from the writer's state) and PANELGWAS_CONTEXTS=1 use one."""
-    return config.output_mode is not OutputMode.TOPK and os.environ.get("PANELGWAS_CONTEXTS", "2") != "1"
+    """PANELGWAS_CONTEXTS=2: THRESHOLD / FULL scans alternate batches between two device
+    contexts (_two_lane_loop; TOPK keeps one: its per-batch bars come from the writer's state).
+    Off by default: through the CLI at C3 the two lanes' threads contend with the writer
+    thread's record formatting for the GIL and the scan loop measured 1.6-3.5 s against
+    1.1-1.6 s on one context; the benches, whose per-batch host work is small,
+    gain from two contexts and use them."""
+    return config.output_mode is not OutputMode.TOPK and os.environ.get("PANELGWAS_CONTEXTS", "1") == "2"
 
 
 def _two_lane_loop(ctx, ctx2, plan, read_lane, stage_on, ready_on, dispatch, full_bufs, dtype, waits) -> float:
