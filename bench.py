@@ -67,6 +67,8 @@ def parse_args():
     ap.add_argument("--sync-panel", action="store_true",
                     help="A/B: e2e uploads + prepares the whole panel before the first scan")
     ap.add_argument("--panel-chunk", type=int, default=1280, help="phenotypes per pipelined panel chunk")
+    ap.add_argument("--no-panel-shard", action="store_true",
+                    help="A/B (N > 1): rank 0 prepares the whole panel and broadcasts it")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=3)
     ap.add_argument("--missing-share", type=float, default=0.0,
@@ -330,6 +332,12 @@ def our_arm(a) -> None:
     gidx = np.arange(n, dtype=np.int64)
     ytil = synth_panel(torch, n, p, a.seed, dev) if rank == 0 else None
 
+    # e2e at N > 1: every rank uploads and prepares its share of the phenotype columns over its
+    # own PCIe link and the quantized shares are all-gathered (instead of rank 0 preparing the
+    # whole panel and broadcasting it)
+    shard_panel = world > 1 and not a.sync_panel and not a.no_panel_shard and p % (256 * world) == 0
+    panel_cols = (rank * p // world, (rank + 1) * p // world) if shard_panel else (0, p)
+
     def distribute_panel(raw_host=None):
         """rank 0 builds the resident panel; its limbs are broadcast once over NCCL; others import.
 
@@ -338,6 +346,33 @@ def our_arm(a) -> None:
         pipelined upload (pg_ctx_set_panel_async) is used: phenotype chunks are prepared as
         they land and the first batch's GEMM follows them chunk by chunk; the zero-variance
         flags are checked once the step's scans are done (panel_checked)."""
+        if raw_host is not None and shard_panel:
+            y_cols, c_raw = raw_host
+            basis = build_covariate_basis(c_raw, True)
+            c0, c1 = panel_cols
+            ctx.set_panel_async_cols(y_cols, p, c0, basis.q, gidx, n, chunk_cols=a.panel_chunk)
+            flat, _sd = ctx.panel_async_wait()
+            wire = dev if backend == "nccl" else torch.device("cpu")
+            bad = torch.tensor([int(flat.any())], device=wire, dtype=torch.int64)
+            dist.all_reduce(bad, op=dist.ReduceOp.MAX)
+            if int(bad.item()):
+                raise RuntimeError("synthetic panel has zero-variance phenotypes")
+            nb = ctx.panel_rows_bytes(c1 - c0)
+            send = torch.empty(nb, dtype=torch.uint8, device=dev)
+            ctx.export_panel_rows(send.data_ptr(), c0, c1)
+            if wire == dev:
+                recv = torch.empty(world * nb, dtype=torch.uint8, device=dev)
+                dist.all_gather_into_tensor(recv, send)
+                parts = [recv[r * nb:(r + 1) * nb] for r in range(world)]
+            else:
+                parts = [torch.empty(nb, dtype=torch.uint8) for _ in range(world)]
+                dist.all_gather(parts, send.cpu())
+                parts = [t.to(dev) for t in parts]
+            torch.cuda.current_stream(dev).synchronize()  # the gather is done before the ctx's stream reads it
+            for r in range(world):
+                if r != rank:
+                    ctx.import_panel_rows(parts[r].data_ptr(), r * p // world, (r + 1) * p // world)
+            return (world - 1) * nb
         if rank == 0:
             if raw_host is not None:
                 y_raw, c_raw = raw_host
@@ -519,15 +554,22 @@ def our_arm(a) -> None:
         host_rows.copy_(packed[:, :bpm])
         host_np = host_rows.numpy()
         raw = None
-        if rank == 0:
-            # raw phenotypes of the C3 shape: Y = C gamma + noise, 10 covariates
+        if rank == 0 or shard_panel:
+            # raw phenotypes of the C3 shape: Y = C gamma + noise, 10 covariates,
+            # each 256-phenotype block from its own generator so that a rank can make just its
+            # share (the sharded panel preparation) and every sharding sees the same matrix
             gen = torch.Generator(device=dev).manual_seed(a.seed + 2000)
             c_dev = torch.randn(n, N_COVARIATES, generator=gen, device=dev, dtype=torch.float64)
-            gamma = 0.1 * torch.randn(N_COVARIATES, p, generator=gen, device=dev, dtype=torch.float64)
-            yh = torch.empty((n, p), dtype=torch.float64, pin_memory=True)
-            yh.copy_(c_dev @ gamma + torch.randn(n, p, generator=gen, device=dev, dtype=torch.float64))
+            c0, c1 = panel_cols
+            yh = torch.empty((n, c1 - c0), dtype=torch.float64, pin_memory=True)
+            for b0 in range(c0, c1, 256):
+                w = min(256, c1 - b0)
+                gb = torch.Generator(device=dev).manual_seed(a.seed + 2001 + b0 // 256)
+                gamma = 0.1 * torch.randn(N_COVARIATES, w, generator=gb, device=dev, dtype=torch.float64)
+                yh[:, b0 - c0:b0 - c0 + w].copy_(c_dev @ gamma + torch.randn(n, w, generator=gb, device=dev,
+                                                                             dtype=torch.float64))
             raw = (yh.numpy(), c_dev.cpu().numpy())
-            del c_dev, gamma
+            del c_dev
         del packed
         torch.cuda.empty_cache()
 
@@ -540,7 +582,7 @@ def our_arm(a) -> None:
             of its next batch overlaps the scan of its current one). With two contexts the
             first exports the step's panel right after its first batch (the pipelined panel
             is complete by then) and the second imports it (device to device)."""
-            h2d = d2h = 0
+            h2d = d2h = hits = 0
 
             def hand_over():
                 if k == 0 and ctx2 is not None and not panel_ready.is_set():
@@ -557,37 +599,50 @@ def our_arm(a) -> None:
                 if j:
                     r = cx.scan_staged((j - 1) % 2)
                     d2h += r.cand_rows.size * 40 + r.n_markers * 25
+                    hits += int(np.count_nonzero(r.cand_p <= a.p_threshold))
                     hand_over()
             if items:
                 r = cx.scan_staged((len(items) - 1) % 2)
                 d2h += r.cand_rows.size * 40 + r.n_markers * 25
+                hits += int(np.count_nonzero(r.cand_p <= a.p_threshold))
             hand_over()
-            return h2d, d2h
+            return h2d, d2h, hits
 
         def e2e_step():
-            h2d = distribute_panel(raw) + (n * (p + N_COVARIATES + 1) * 8 if rank == 0 else 0)
+            moved = distribute_panel(raw)
+            if shard_panel:  # this rank's share of Y and C (the shares' limbs move over NVLink)
+                h2d = n * (panel_cols[1] - panel_cols[0] + N_COVARIATES + 1) * 8
+            else:
+                h2d = moved + (n * (p + N_COVARIATES + 1) * 8 if rank == 0 else 0)
             ctx.set_scan(df, _native.PG_MODE_THRESHOLD, rbar)
-            d2h = 0
+            d2h = hits = 0
             if ctx2 is None:
-                h, d = e2e_lane(ctx, 0, batches)
-                h2d, d2h = h2d + h, d2h + d
+                h, d, t = e2e_lane(ctx, 0, batches)
+                h2d, d2h, hits = h2d + h, d2h + d, hits + t
             else:
                 panel_ready.clear()
                 futs = [pool.submit(e2e_lane, (ctx, ctx2)[k], k, batches[k::2]) for k in range(2)]
                 for f in futs:
-                    h, d = f.result()
-                    h2d, d2h = h2d + h, d2h + d
-            if rank == 0 and not a.sync_panel:
+                    h, d, t = f.result()
+                    h2d, d2h, hits = h2d + h, d2h + d, hits + t
+            if (rank == 0 or shard_panel) and not a.sync_panel:
                 flat, _sd = ctx.panel_async_wait()  # (complete long ago: no wait)
                 if flat.any():
                     raise RuntimeError("synthetic panel has zero-variance phenotypes")
-            return h2d, d2h
+            return h2d, d2h, hits
 
         e2e_step()
         ms_e2e, outs_e2e = timed(e2e_step, a.steps)
+        e2e_hits = outs_e2e[-1][2]
+        if world > 1:  # every rank's hits (the job's)
+            wire = dev if backend == "nccl" else torch.device("cpu")
+            t = torch.tensor([e2e_hits], device=wire, dtype=torch.int64)
+            dist.all_reduce(t)
+            e2e_hits = int(t.item())
         e2e = {"value": tests_per_step * a.steps / (ms_e2e / 1e3), "unit": "tests/s",
                "h2d_bytes_per_step": int(outs_e2e[-1][0]), "d2h_bytes_per_step": int(outs_e2e[-1][1]),
-               "ms_per_step": ms_e2e / a.steps}
+               "ms_per_step": ms_e2e / a.steps, "hits_per_step": e2e_hits,
+               "panel": ("sharded over ranks" if shard_panel else "rank 0" if world > 1 else "one GPU")}
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:

@@ -110,6 +110,19 @@ PG_API int pg_ctx_set_panel_async(pg_ctx* ctx, const double* y, int64_t n_kept, 
                                   const double* basis_q, int64_t rank, const int64_t* geno_row_index,
                                   int64_t n_samples_src, int64_t chunk_cols);
 PG_API int pg_ctx_panel_async_wait(pg_ctx* ctx, uint8_t* zero_variance, double* sd);
+/* Multi-GPU panel preparation: as pg_ctx_set_panel_async for the panel geometry of all
+ * n_pheno phenotypes, but this context uploads, prepares and quantizes only the columns
+ * [col_begin, col_end) (a rank's share; multiples of 256, or ending at n_pheno), read from `y`
+ * (page-locked, its column c at y[c - col_begin], `ld` per row); pg_ctx_panel_async_wait then
+ * returns the flags / sd of those columns. The other rows arrive with
+ * pg_ctx_import_panel_rows from the ranks that prepared them (pg_ctx_export_panel_rows; an
+ * all-gather over NVLink in bench.py). pg_ctx_panel_rows_bytes: buffer size for n_rows rows. */
+PG_API int pg_ctx_set_panel_async_cols(pg_ctx* ctx, const double* y, int64_t n_kept, int64_t n_pheno, int64_t ld,
+                                       int64_t col_begin, int64_t col_end, const double* basis_q, int64_t rank,
+                                       const int64_t* geno_row_index, int64_t n_samples_src, int64_t chunk_cols);
+PG_API int pg_ctx_panel_rows_bytes(pg_ctx* ctx, int64_t n_rows, int64_t* bytes);
+PG_API int pg_ctx_export_panel_rows(pg_ctx* ctx, void* d_dst, int64_t row_begin, int64_t row_end);
+PG_API int pg_ctx_import_panel_rows(pg_ctx* ctx, const void* d_src, int64_t row_begin, int64_t row_end);
 /* Copy `src`'s resident panel (limbs, scales, sample map) into `dst` on the same device, device
  * to device (export + import), so that two contexts can scan batches of one job in turn
  * ("two contexts per GPU"). Both must have the same precision mode. */

@@ -153,6 +153,40 @@ class DeviceContext:
             self.beta_on = False
             self._async_shape = (n, p)
 
+    def set_panel_async_cols(self, y_cols: np.ndarray, n_pheno: int, col_begin: int, basis_q: np.ndarray | None,
+                             geno_row_index: np.ndarray, n_samples_src: int, chunk_cols: int = 1280) -> None:
+        """A rank's share of a pipelined panel (pg_ctx_set_panel_async_cols): `y_cols` (pinned,
+        C-contiguous f64 [n_kept, w]) holds phenotypes [col_begin, col_begin + w) of n_pheno;
+        the other rows come from import_panel_rows."""
+        if y_cols.dtype != np.float64 or y_cols.ndim != 2 or not y_cols.flags["C_CONTIGUOUS"]:
+            raise ValueError("expected a C-contiguous float64 (samples x phenotypes) matrix")
+        n, w = y_cols.shape
+        q = None
+        rank = 0
+        if basis_q is not None and basis_q.shape[1]:
+            q = np.ascontiguousarray(basis_q, dtype=np.float64)
+            rank = q.shape[1]
+        gidx = np.ascontiguousarray(geno_row_index, dtype=np.int64)
+        with self.lock:
+            call("pg_ctx_set_panel_async_cols", self._h, ptr(y_cols), n, int(n_pheno), w, int(col_begin),
+                 int(col_begin) + w, ptr(q), rank, ptr(gidx), int(n_samples_src), int(chunk_cols))
+            self.n_pheno = int(n_pheno)
+            self.beta_on = False
+            self._async_shape = (n, w)
+
+    def panel_rows_bytes(self, n_rows: int) -> int:
+        b = c_int64(0)
+        call("pg_ctx_panel_rows_bytes", self._h, int(n_rows), byref(b))
+        return b.value
+
+    def export_panel_rows(self, d_dst: int, row_begin: int, row_end: int) -> None:
+        with self.lock:
+            call("pg_ctx_export_panel_rows", self._h, d_dst, int(row_begin), int(row_end))
+
+    def import_panel_rows(self, d_src: int, row_begin: int, row_end: int) -> None:
+        with self.lock:
+            call("pg_ctx_import_panel_rows", self._h, d_src, int(row_begin), int(row_end))
+
     def clone_panel_from(self, src: "DeviceContext") -> None:
         """This context takes `src`'s resident panel, device to device (pg_ctx_clone_panel)."""
         with src.lock, self.lock:

@@ -183,6 +183,7 @@ struct pg_ctx {
   // wait for the whole panel upload.
   int64_t chunk_issued = 0;
   int64_t async_chunk = 0, async_ld = 0, async_rank = 0;
+  int64_t async_col0 = 0, async_col1 = 0;  // the columns this context prepares (all, or a rank's share)
   const double* async_y = nullptr;
   bool panel_pending = false;  // the compute stream has not yet waited for every chunk
   bool async_flags = false;    // zero-variance flags / sd / finiteness of the async panel on the device
@@ -311,12 +312,14 @@ int ctx_check(pg_ctx* c) {
 int panel_issue(pg_ctx* c, int64_t j) {
   cudaStream_t ps = c->panel_prep, cs = c->panel_copy;
   const int64_t n_kept = c->prep_rows, n_pheno = c->prep_cols, chunk = c->async_chunk;
-  const int64_t c0 = j * chunk;
-  const int64_t w = std::min(chunk, n_pheno - c0);
-  const int64_t rows = j == c->n_chunks - 1 ? c->p_pad - c0 : w;  // panel rows (padding in the last chunk)
-  double* yj = c->ystage.p + static_cast<size_t>(n_kept) * c0;    // the chunk as its own [n_kept, w] matrix
-  PG_CUDA_CHECK(cudaMemcpy2DAsync(yj, sizeof(double) * w, c->async_y + c0, sizeof(double) * c->async_ld,
-                                  sizeof(double) * w, n_kept, cudaMemcpyHostToDevice, cs));
+  const int64_t c0 = c->async_col0 + j * chunk;
+  const int64_t w = std::min(chunk, c->async_col1 - c0);
+  // panel rows (the padding rows past the last phenotype go with the last column)
+  const int64_t rows = c0 + w == n_pheno ? c->p_pad - c0 : w;
+  double* yj = c->ystage.p + static_cast<size_t>(n_kept) * (c0 - c->async_col0);  // the chunk as its own [n_kept, w]
+  PG_CUDA_CHECK(cudaMemcpy2DAsync(yj, sizeof(double) * w, c->async_y + (c0 - c->async_col0),
+                                  sizeof(double) * c->async_ld, sizeof(double) * w, n_kept, cudaMemcpyHostToDevice,
+                                  cs));
   PG_CUDA_CHECK(cudaEventRecord(c->chunk_h2d[j], cs));
   PG_CUDA_CHECK(cudaStreamWaitEvent(ps, c->chunk_h2d[j], 0));
   pg::PanelPrepOut po;
@@ -1095,14 +1098,18 @@ int pg_ctx_prepare_panel(pg_ctx* c, const double* y, int64_t n_kept, int64_t n_p
   return PG_OK;
 }
 
-int pg_ctx_set_panel_async(pg_ctx* c, const double* y, int64_t n_kept, int64_t n_pheno, int64_t ld,
-                           const double* basis_q, int64_t rank, const int64_t* geno_row_index, int64_t n_samples_src,
-                           int64_t chunk_cols) {
+int pg_ctx_set_panel_async_cols(pg_ctx* c, const double* y, int64_t n_kept, int64_t n_pheno, int64_t ld,
+                                int64_t col_begin, int64_t col_end, const double* basis_q, int64_t rank,
+                                const int64_t* geno_row_index, int64_t n_samples_src, int64_t chunk_cols) {
   PG_CHECK_STATUS(ctx_check(c));
   PG_REQUIRE(y != nullptr && geno_row_index != nullptr && (rank == 0 || basis_q != nullptr), PG_ERR_INVALID,
              "pg_ctx_set_panel_async: null input");
-  PG_REQUIRE(n_kept >= 1 && n_pheno >= 1 && ld >= n_pheno && rank >= 0 && chunk_cols >= 1, PG_ERR_INVALID,
-             "pg_ctx_set_panel_async: bad shape");
+  PG_REQUIRE(n_kept >= 1 && n_pheno >= 1 && rank >= 0 && chunk_cols >= 1 && col_begin >= 0 && col_end > col_begin &&
+                 col_end <= n_pheno && ld >= col_end - col_begin,
+             PG_ERR_INVALID, "pg_ctx_set_panel_async: bad shape");
+  PG_REQUIRE(col_begin % kTileP == 0 && (col_end % kTileP == 0 || col_end == n_pheno), PG_ERR_INVALID,
+             "pg_ctx_set_panel_async: a column range starts and ends on a multiple of %d phenotypes (or the last)",
+             static_cast<int>(kTileP));
   cudaPointerAttributes attr{};
   const bool pinned = cudaPointerGetAttributes(&attr, y) == cudaSuccess && attr.type == cudaMemoryTypeHost;
   cudaGetLastError();
@@ -1122,7 +1129,7 @@ int pg_ctx_set_panel_async(pg_ctx* c, const double* y, int64_t n_kept, int64_t n
   PanelPlanes pp;
   PG_CHECK_STATUS(panel_geometry(c, n_kept, n_pheno, n_samples_src, geno_row_index, ps, pp));
   const int64_t chunk = round_up(std::max<int64_t>(chunk_cols, kTileP), kTileP);
-  const int64_t n_ch = (n_pheno + chunk - 1) / chunk;
+  const int64_t n_ch = (col_end - col_begin + chunk - 1) / chunk;
   while (static_cast<int64_t>(c->chunk_ready.size()) < n_ch) {
     cudaEvent_t a, b;
     PG_CUDA_CHECK(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
@@ -1132,15 +1139,17 @@ int pg_ctx_set_panel_async(pg_ctx* c, const double* y, int64_t n_kept, int64_t n
   }
   c->chunk_pt.assign(n_ch + 1, 0);
   for (int64_t j = 0; j < n_ch; ++j) {
-    c->chunk_pt[j] = j * chunk / kTileP;
-    c->chunk_pt[j + 1] = j == n_ch - 1 ? c->p_pad / kTileP : (j + 1) * chunk / kTileP;
+    const int64_t c0 = col_begin + j * chunk, c1 = std::min(col_end, c0 + chunk);
+    c->chunk_pt[j] = c0 / kTileP;
+    c->chunk_pt[j + 1] = c1 == n_pheno ? c->p_pad / kTileP : c1 / kTileP;
   }
-  PG_CHECK_STATUS(c->ystage.ensure(static_cast<size_t>(n_kept) * n_pheno));
+  PG_CHECK_STATUS(c->ystage.ensure(static_cast<size_t>(n_kept) * (col_end - col_begin)));
   if (rank > 0) {
     PG_CHECK_STATUS(c->prep_q.ensure(static_cast<size_t>(n_kept) * rank));
     PG_CUDA_CHECK(cudaMemcpyAsync(c->prep_q.p, basis_q, sizeof(double) * n_kept * rank, cudaMemcpyHostToDevice, ps));
   }
-  PG_CHECK_STATUS(c->prep_scratch.ensure(pg::panel_prep_scratch_doubles(n_kept, std::min(chunk, n_pheno), rank)));
+  PG_CHECK_STATUS(
+      c->prep_scratch.ensure(pg::panel_prep_scratch_doubles(n_kept, std::min(chunk, col_end - col_begin), rank)));
   for (auto* b : {&c->prep_mean, &c->prep_centre, &c->prep_sd}) PG_CHECK_STATUS(b->ensure(n_pheno));
   PG_CHECK_STATUS(c->prep_flat.ensure(n_pheno));
   PG_CHECK_STATUS(c->prep_bad.ensure(n_ch));
@@ -1151,6 +1160,8 @@ int pg_ctx_set_panel_async(pg_ctx* c, const double* y, int64_t n_kept, int64_t n
   c->async_ld = ld;
   c->async_rank = rank;
   c->async_y = y;
+  c->async_col0 = col_begin;
+  c->async_col1 = col_end;
   c->chunk_issued = 0;
   c->n_chunks = n_ch;
   PG_CHECK_STATUS(panel_pump(c, 1));  // the first two chunks; the rest as they are needed
@@ -1165,6 +1176,14 @@ int pg_ctx_set_panel_async(pg_ctx* c, const double* y, int64_t n_kept, int64_t n
   return PG_OK;
 }
 
+int pg_ctx_set_panel_async(pg_ctx* c, const double* y, int64_t n_kept, int64_t n_pheno, int64_t ld,
+                           const double* basis_q, int64_t rank, const int64_t* geno_row_index, int64_t n_samples_src,
+                           int64_t chunk_cols) {
+  PG_REQUIRE(ld >= n_pheno, PG_ERR_INVALID, "pg_ctx_set_panel_async: bad shape");
+  return pg_ctx_set_panel_async_cols(c, y, n_kept, n_pheno, ld, 0, n_pheno, basis_q, rank, geno_row_index,
+                                     n_samples_src, chunk_cols);
+}
+
 int pg_ctx_panel_async_wait(pg_ctx* c, uint8_t* zero_variance, double* sd) {
   PG_CHECK_STATUS(ctx_check(c));
   PG_REQUIRE(c->async_flags, PG_ERR_STATE, "pg_ctx_panel_async_wait: no pipelined panel (pg_ctx_set_panel_async)");
@@ -1172,9 +1191,10 @@ int pg_ctx_panel_async_wait(pg_ctx* c, uint8_t* zero_variance, double* sd) {
   cudaStream_t ps = c->panel_prep;
   std::vector<int> bad(static_cast<size_t>(c->n_chunks), 0);
   PG_CUDA_CHECK(cudaMemcpyAsync(bad.data(), c->prep_bad.p, sizeof(int) * c->n_chunks, cudaMemcpyDeviceToHost, ps));
+  const int64_t c0 = c->async_col0, nc = c->async_col1 - c->async_col0;  // the prepared columns
   if (zero_variance)
-    PG_CUDA_CHECK(cudaMemcpyAsync(zero_variance, c->prep_flat.p, c->prep_cols, cudaMemcpyDeviceToHost, ps));
-  if (sd) PG_CUDA_CHECK(cudaMemcpyAsync(sd, c->prep_sd.p, sizeof(double) * c->prep_cols, cudaMemcpyDeviceToHost, ps));
+    PG_CUDA_CHECK(cudaMemcpyAsync(zero_variance, c->prep_flat.p + c0, nc, cudaMemcpyDeviceToHost, ps));
+  if (sd) PG_CUDA_CHECK(cudaMemcpyAsync(sd, c->prep_sd.p + c0, sizeof(double) * nc, cudaMemcpyDeviceToHost, ps));
   PG_CUDA_CHECK(cudaStreamSynchronize(ps));
   c->panel_pending = false;  // every chunk is complete: no stream needs to wait any more
   for (int v : bad) PG_REQUIRE(!v, PG_ERR_INVALID, "standardize_columns requires finite input");
@@ -1246,6 +1266,73 @@ int pg_ctx_export_panel(pg_ctx* c, void* d_dst) {
   }
   PG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
   return PG_OK;
+}
+
+// Panel rows [row_begin, row_end) as one device buffer: the three limb planes' rows, then
+// scale_d (f64), scale_f (f32), Cq (i64), Cq_f (f32), ||q0|| (f32) per row, then the lo level
+// (three planes + Cq_lo) in F64 mode. Multi-GPU: each rank prepares its share of the
+// phenotypes and the shares are all-gathered (bench.py, distributed panel preparation).
+int64_t panel_rows_bytes(const pg_ctx* c, int64_t r) {
+  int64_t b = 3 * r * c->k_pad + r * (8 + 4 + 8 + 4 + 4);
+  if (c->f64_panel) b += 3 * r * c->k_pad + r * 8;
+  return b;
+}
+
+int panel_rows_copy(pg_ctx* c, uint8_t* buf, int64_t row_begin, int64_t row_end, bool to_buf) {
+  const int64_t r = row_end - row_begin;
+  const size_t plane = static_cast<size_t>(r) * c->k_pad, off = static_cast<size_t>(row_begin) * c->k_pad;
+  cudaStream_t s = c->stream;
+  auto cp = [&](void* panel, size_t bytes, uint8_t*& cursor) -> int {
+    if (to_buf)
+      PG_CUDA_CHECK(cudaMemcpyAsync(cursor, panel, bytes, cudaMemcpyDeviceToDevice, s));
+    else
+      PG_CUDA_CHECK(cudaMemcpyAsync(panel, cursor, bytes, cudaMemcpyDeviceToDevice, s));
+    cursor += bytes;
+    return PG_OK;
+  };
+  uint8_t* cur = buf;
+  PG_CHECK_STATUS(cp(c->qh.p + off, plane, cur));
+  PG_CHECK_STATUS(cp(c->q1.p + off, plane, cur));
+  PG_CHECK_STATUS(cp(c->q0.p + off, plane, cur));
+  PG_CHECK_STATUS(cp(c->scale_d.p + row_begin, 8 * r, cur));
+  PG_CHECK_STATUS(cp(c->scale_f.p + row_begin, 4 * r, cur));
+  PG_CHECK_STATUS(cp(c->cq.p + row_begin, 8 * r, cur));
+  PG_CHECK_STATUS(cp(c->cq_f.p + row_begin, 4 * r, cur));
+  PG_CHECK_STATUS(cp(c->q0n.p + row_begin, 4 * r, cur));
+  if (c->f64_panel) {
+    PG_CHECK_STATUS(cp(c->qh_lo.p + off, plane, cur));
+    PG_CHECK_STATUS(cp(c->q1_lo.p + off, plane, cur));
+    PG_CHECK_STATUS(cp(c->q0_lo.p + off, plane, cur));
+    PG_CHECK_STATUS(cp(c->cq_lo.p + row_begin, 8 * r, cur));
+  }
+  PG_CUDA_CHECK(cudaStreamSynchronize(s));
+  return PG_OK;
+}
+
+int pg_ctx_panel_rows_bytes(pg_ctx* c, int64_t n_rows, int64_t* bytes) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(c->have_panel && bytes != nullptr && n_rows >= 0, PG_ERR_STATE, "pg_ctx_panel_rows_bytes: no panel");
+  *bytes = panel_rows_bytes(c, n_rows);
+  return PG_OK;
+}
+
+int pg_ctx_export_panel_rows(pg_ctx* c, void* d_dst, int64_t row_begin, int64_t row_end) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(c->have_panel && c->q0n_valid, PG_ERR_STATE, "pg_ctx_export_panel_rows: no (pipelined) panel");
+  PG_REQUIRE(d_dst != nullptr && row_begin >= 0 && row_end > row_begin && row_end <= c->p_pad, PG_ERR_INVALID,
+             "pg_ctx_export_panel_rows: bad row range");
+  PG_CHECK_STATUS(panel_wait_all(c, c->stream));
+  return panel_rows_copy(c, static_cast<uint8_t*>(d_dst), row_begin, row_end, true);
+}
+
+int pg_ctx_import_panel_rows(pg_ctx* c, const void* d_src, int64_t row_begin, int64_t row_end) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(c->have_panel && c->q0n_valid, PG_ERR_STATE,
+             "pg_ctx_import_panel_rows: set the panel geometry first (pg_ctx_set_panel_async_cols)");
+  PG_REQUIRE(d_src != nullptr && row_begin >= 0 && row_end > row_begin && row_end <= c->p_pad, PG_ERR_INVALID,
+             "pg_ctx_import_panel_rows: bad row range");
+  PG_CHECK_STATUS(panel_wait_all(c, c->stream));
+  return panel_rows_copy(c, const_cast<uint8_t*>(static_cast<const uint8_t*>(d_src)), row_begin, row_end, false);
 }
 
 int pg_ctx_clone_panel(pg_ctx* dst, pg_ctx* src) {

@@ -89,6 +89,27 @@ def test_bench_two_ranks_functional(shape):
     assert abs(d["value"] * d["ms_per_step"] / 1e3 - d["config"]["n_markers_total"] * 512) < 1e-3 * d["value"]
 
 
+def test_bench_two_ranks_sharded_panel_equals_broadcast():
+    """e2e at N > 1: each rank prepares its share of the phenotype columns and the quantized
+    shares are all-gathered (pg_ctx_set_panel_async_cols / export / import_panel_rows) — the
+    scans find exactly the hits of the rank-0-prepared, broadcast panel."""
+    import json
+
+    env = {**os.environ, "PANELGWAS_DIST_BACKEND": "gloo", "PANELGWAS_DIST_DEVICE": "0"}
+    out = {}
+    for flag in ([], ["--no-panel-shard"]):
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+               "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "2",
+               "--total-markers", "12800", "--phenotypes", "512", "--samples", "2000", "--steps", "3",
+               "--warmup", "3", "--device-batch", "4096", "--p-threshold", "0.01", "--no-cpu-baseline", *flag]
+        res = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+        assert res.returncode == 0, res.stderr[-4000:]
+        d = json.loads([ln for ln in res.stdout.splitlines() if ln.startswith("{")][0])
+        out[tuple(flag)] = d["e2e"]
+    assert out[()]["panel"] == "sharded over ranks" and out[("--no-panel-shard",)]["panel"] == "rank 0"
+    assert out[()]["hits_per_step"] == out[("--no-panel-shard",)]["hits_per_step"] > 0
+
+
 @pytest.mark.parametrize("f64", [False, True])
 def test_nccl_panel_broadcast_round_trip(f64):
     """The NCCL data plane of the multi-GPU scan on this box's one GPU: a one-rank NCCL group
