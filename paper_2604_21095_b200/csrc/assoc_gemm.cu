@@ -40,6 +40,9 @@
 
 #include "assoc.cuh"
 
+#ifndef PG_FUSED2_STAGES
+#define PG_FUSED2_STAGES 8
+#endif
 #ifndef PG_DEC_TEAMS
 #define PG_DEC_TEAMS 2
 #endif
@@ -103,7 +106,7 @@ struct Cfg {
   static constexpr bool TRANS = MODE == kWide3T;
   static constexpr bool WIDE = MODE == kWide || MODE == kWide3 || MODE == kWide3Two || MODE == kWide4Two || TRANS;
   static constexpr int kStages =
-      (TRANS || MODE == kWide3Two || MODE == kWide4Two) ? 9 : (WIDE ? 7 : (MODE == kFused2 ? 8 : (TWO ? 6 : 5)));
+      (TRANS || MODE == kWide3Two || MODE == kWide4Two) ? 9 : (WIDE ? 7 : (MODE == kFused2 ? PG_FUSED2_STAGES : (TWO ? 6 : 5)));
   // decoder warps: 4 per team (one thread per packed row). Measured on the two-limb C3 scan
   // (old decoder): 8 warps splitting each stage's rows with 12 epilogue warps 2.45e10 tests/s,
   // with 16 epilogue warps 2.54e10, 4 + 16 2.60e10; a separate 12-deep packed-tile ring 2.50e10.
