@@ -126,3 +126,37 @@ def test_async_panel_zero_variance_and_errors():
             ctx.panel_async_wait()
         with pytest.raises(ValueError, match="page-locked"):
             ctx.set_panel_async(np.ascontiguousarray(y), q, gidx, n_src)
+
+
+@pytest.mark.parametrize("f64", [False, True])
+def test_panel_shares_assemble_the_sync_panel(f64):
+    """Multi-GPU panel preparation on one GPU: two contexts each prepare their share of the
+    phenotype columns (pg_ctx_set_panel_async_cols), exchange rows (export / import_panel_rows)
+    and both end up with the synchronous path's panel, bit for bit (incl. the last share's
+    padding rows and the F64 lo level)."""
+    y, q, gidx, n_src = _case(13, p=700)  # shares [0, 512) and [512, 700) (+ padding to 768)
+    cut = 512
+    with DeviceContext(0) as ref, DeviceContext(0) as a, DeviceContext(0) as b:
+        for cx in (ref, a, b):
+            cx.set_f64_panel(f64)
+        ref.prepare_panel(y, q)
+        ref.commit_panel(np.arange(y.shape[1]), gidx, n_src)
+        shares = [(a, 0, cut), (b, cut, y.shape[1])]
+        for cx, c0, c1 in shares:
+            cx.set_panel_async_cols(_pinned(np.ascontiguousarray(y[:, c0:c1])), y.shape[1], c0, q, gidx, n_src,
+                                    chunk_cols=256)
+        for cx, c0, c1 in shares:
+            flat, _ = cx.panel_async_wait()
+            assert flat.shape == (c1 - c0,) and not flat.any()
+        p_pad = (y.shape[1] + 255) // 256 * 256
+        rows = {}
+        for cx, c0, c1 in shares:
+            r1 = p_pad if c1 == y.shape[1] else c1
+            buf = torch.empty(cx.panel_rows_bytes(r1 - c0), dtype=torch.uint8, device="cuda")
+            cx.export_panel_rows(buf.data_ptr(), c0, r1)
+            rows[cx] = (buf, c0, r1)
+        torch.cuda.synchronize()
+        a.import_panel_rows(rows[b][0].data_ptr(), rows[b][1], rows[b][2])
+        b.import_panel_rows(rows[a][0].data_ptr(), rows[a][1], rows[a][2])
+        want = _panel_bytes(ref)
+        assert np.array_equal(_panel_bytes(a), want) and np.array_equal(_panel_bytes(b), want)
