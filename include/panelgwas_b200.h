@@ -353,6 +353,18 @@ PG_API int pg_format_tsv(int64_t n, const int64_t* rows, const int64_t* cols, co
 PG_API int pg_format_float_columns(int64_t n, int ncols, const double* const* cols, char* out, int64_t out_cap,
                                    int64_t* out_len);
 
+/* TOPK writer merge (host; output.TopKWriter.emit, output.py:153-211): the held records
+ * (sorted by phenotype, p, marker source index) and a batch's new candidates (any order, every
+ * source index above the held ones) merged per phenotype, the first k of each kept. out_idx
+ * (capacity n_pheno * k) receives indices into [held ++ fresh] in (phenotype, p, source index)
+ * order, *n_out their count. Phenotypes are merged in parallel on host threads. */
+PG_API int pg_topk_merge(int64_t n_pheno, int64_t k, const int64_t* held_col, const double* held_p,
+                         const int64_t* held_src, int64_t n_held, const int64_t* fresh_col, const double* fresh_p,
+                         const int64_t* fresh_src, int64_t n_fresh, int64_t* out_idx, int64_t* n_out);
+
+/* out = src[starts[i] .. starts[i] + lens[i]) for i < n, concatenated (TOPK line prefixes). */
+PG_API int pg_gather_spans(const char* src, const int64_t* starts, const int64_t* lens, int64_t n, char* out);
+
 /* FULL-mode marker sidecar lines "SOURCE_INDEX CHR ID POS A1 A2 AF N_MISS" (tab-separated, LF) of
  * markers rows[0..n): replaces the per-marker f-string of FullMatrixWriter.emit
  * (/root/reference/pkg/src/panelgwas/output.py:245-252). prefix blob/offsets as in pg_format_tsv;

@@ -282,6 +282,34 @@ class TestWriters:
         assert [r.id for r in recs] == ["snp2", "snp3"]  # equal p: earlier source index first
         assert recs[0].counted_allele == "B"  # counts_allele1=False swaps labels
 
+    def test_topk_writer_matches_brute_force(self, tmp_path):
+        """The native per-phenotype merge (pg_topk_merge) over many batches — candidates in
+        (marker, phenotype) order, p ties within and across batches, phenotypes that never
+        fill k — keeps exactly the k smallest (p, source index) records of each phenotype."""
+        rng = np.random.default_rng(12)
+        n_pheno, k, n_batches, per = 7, 5, 9, 40
+        names = [f"ph{j + 1}" for j in range(n_pheno)]
+        w = output.TopKWriter(tmp_path / "t.tsv", k, 30.0, 40, True, names)
+        allrec = []
+        for b in range(n_batches):
+            mk = [pg.MarkerRecord("1", f"snp{b * per + i + 1}", b * per + i + 1, "A", "B", b * per + i)
+                  for i in range(per)]
+            cand = []
+            for i in range(per):
+                for j in range(n_pheno - 1):  # the last phenotype never gets a record
+                    if rng.random() < 0.4:
+                        p = float(rng.choice([0.5, 0.25, 0.125, 1e-3])) if rng.random() < 0.5 else float(rng.random())
+                        cand.append((i, j, 0.1, 2.0 - p, p))
+                        allrec.append((j, p, b * per + i))
+            w.emit(_batch(mk, cand))
+        assert w.finalize() > 0
+        recs = pg.load_association_records(tmp_path / "t.tsv")
+        got = [(int(r.phenotype[2:]) - 1, r.p, int(r.id[3:]) - 1) for r in recs]
+        want = []
+        for j in range(n_pheno):
+            want += sorted((x for x in allrec if x[0] == j), key=lambda x: (x[1], x[2]))[:k]
+        assert got == want
+
     def test_full_matrix_round_trip(self, tmp_path):
         mk = [pg.MarkerRecord("1", f"snp{i + 1}", i + 1, "A", "B", i) for i in range(3)]
         w = output.FullMatrixWriter(tmp_path / "f.bin", np.float32, 5.0, 7, True, ["p1", "p2"])
