@@ -362,6 +362,10 @@ PG_API int pg_topk_merge(int64_t n_pheno, int64_t k, const int64_t* held_col, co
                          const int64_t* held_src, int64_t n_held, const int64_t* fresh_col, const double* fresh_p,
                          const int64_t* fresh_src, int64_t n_fresh, int64_t* out_idx, int64_t* n_out);
 
+/* The merge's column gather: out_cols[c][i] = held_cols[c][idx[i]] (idx[i] < n_held) or
+ * fresh_cols[c][idx[i] - n_held], for n_cols columns of 8-byte elements, on host threads. */
+PG_API int pg_topk_gather(int64_t n_out, const int64_t* idx, int64_t n_held, int n_cols, const void* const* held_cols,
+                          const void* const* fresh_cols, void* const* out_cols);
 /* out = src[starts[i] .. starts[i] + lens[i]) for i < n, concatenated (TOPK line prefixes). */
 PG_API int pg_gather_spans(const char* src, const int64_t* starts, const int64_t* lens, int64_t n, char* out);
 

@@ -87,6 +87,34 @@ int pg_topk_merge(int64_t n_pheno, int64_t k, const int64_t* held_col, const dou
   return PG_OK;
 }
 
+// out_cols[c][i] = (idx[i] < n_held ? held_cols[c][idx[i]] : fresh_cols[c][idx[i] - n_held]) for the
+// n_cols 8-byte columns of the TOPK writer (the merge's gather, on host threads).
+int pg_topk_gather(int64_t n_out, const int64_t* idx, int64_t n_held, int n_cols, const void* const* held_cols,
+                   const void* const* fresh_cols, void* const* out_cols) {
+  PG_REQUIRE(n_out >= 0 && n_cols >= 0 && (n_out == 0 || (idx && held_cols && fresh_cols && out_cols)), PG_ERR_INVALID,
+             "pg_topk_gather: bad arguments");
+  auto work = [&](int64_t lo, int64_t hi) {
+    for (int c = 0; c < n_cols; ++c) {
+      const uint64_t* h = static_cast<const uint64_t*>(held_cols[c]);
+      const uint64_t* f = static_cast<const uint64_t*>(fresh_cols[c]);
+      uint64_t* o = static_cast<uint64_t*>(out_cols[c]);
+      for (int64_t i = lo; i < hi; ++i) {
+        const int64_t j = idx[i];
+        o[i] = j < n_held ? h[j] : f[j - n_held];
+      }
+    }
+  };
+  const int nt = n_out < (1 << 16) ? 1 : static_cast<int>(std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
+  if (nt == 1) {
+    work(0, n_out);
+  } else {
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t) th.emplace_back(work, n_out * t / nt, n_out * (t + 1) / nt);
+    for (auto& x : th) x.join();
+  }
+  return PG_OK;
+}
+
 // out = concatenation of src[starts[i], starts[i] + lens[i]) for i < n (the held TOPK records'
 // line prefixes, gathered from the per-batch prefix blobs at finalize).
 int pg_gather_spans(const char* src, const int64_t* starts, const int64_t* lens, int64_t n, char* out) {
