@@ -7,9 +7,12 @@
 // (std::to_chars) laid out with CPython's 'r' rules — exponent form when the
 // decimal point position is <= -4 or > 16, otherwise fixed with a trailing
 // ".0" for integral values; "inf", "-inf", "nan".
+#include <algorithm>
 #include <charconv>
 #include <cmath>
 #include <cstring>
+#include <thread>
+#include <vector>
 
 #include "pg_common.cuh"
 
@@ -146,32 +149,79 @@ int pg_format_tsv(int64_t n, const int64_t* rows, const int64_t* cols, const dou
                   const double* p, const double* af, const int64_t* n_miss, const char* prefix_blob,
                   const int64_t* prefix_off, const char* pheno_blob, const int64_t* pheno_off, const char* mid,
                   int64_t mid_len, char* out, int64_t out_cap, int64_t* out_len) {
-  int64_t o = 0;
-  for (int64_t i = 0; i < n; ++i) {
-    const int64_t k = rows[i], j = cols[i];
-    const int64_t plen = prefix_off[k + 1] - prefix_off[k];
-    const int64_t nlen = pheno_off[j + 1] - pheno_off[j];
-    if (o + plen + nlen + mid_len + 4 * 40 + 8 > out_cap) {
+  // records [i0, i1) into dst (room for their worst case); returns the bytes written
+  auto format_range = [&](int64_t i0, int64_t i1, char* dst) -> int64_t {
+    int64_t o = 0;
+    for (int64_t i = i0; i < i1; ++i) {
+      const int64_t k = rows[i], j = cols[i];
+      const int64_t plen = prefix_off[k + 1] - prefix_off[k];
+      const int64_t nlen = pheno_off[j + 1] - pheno_off[j];
+      std::memcpy(dst + o, prefix_blob + prefix_off[k], plen);
+      o += plen;
+      o += pg::py_repr(af[k], dst + o);
+      dst[o++] = '\t';
+      o += pg::put_int(n_miss[k], dst + o);
+      std::memcpy(dst + o, mid, mid_len);
+      o += mid_len;
+      o += pg::py_repr(r[i], dst + o);
+      dst[o++] = '\t';
+      o += pg::py_repr(t[i], dst + o);
+      dst[o++] = '\t';
+      o += pg::py_repr(p[i], dst + o);
+      dst[o++] = '\t';
+      std::memcpy(dst + o, pheno_blob + pheno_off[j], nlen);
+      o += nlen;
+      dst[o++] = '\n';
+    }
+    return o;
+  };
+  auto worst = [&](int64_t i0, int64_t i1) {
+    int64_t w = 0;
+    for (int64_t i = i0; i < i1; ++i)
+      w += (prefix_off[rows[i] + 1] - prefix_off[rows[i]]) + (pheno_off[cols[i] + 1] - pheno_off[cols[i]]) + mid_len +
+           4 * 40 + 8;
+    return w;
+  };
+  const int nt = n < (1 << 15) ? 1 : static_cast<int>(std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
+  if (nt == 1) {
+    if (worst(0, n) > out_cap) {  // the serial path checks per record, as before
+      int64_t o = 0;
+      for (int64_t i = 0; i < n; ++i) {
+        const int64_t need = worst(i, i + 1);
+        if (o + need > out_cap) {
+          *out_len = o;
+          pg::set_error("pg_format_tsv: output buffer too small at record %lld", (long long)i);
+          return PG_ERR_INVALID;
+        }
+        o += format_range(i, i + 1, out + o);
+      }
       *out_len = o;
-      pg::set_error("pg_format_tsv: output buffer too small at record %lld", (long long)i);
+      return PG_OK;
+    }
+    *out_len = format_range(0, n, out);
+    return PG_OK;
+  }
+  // records split over host threads, each into its own buffer, then concatenated in order
+  std::vector<std::vector<char>> parts(nt);
+  std::vector<int64_t> used(nt, 0);
+  std::vector<std::thread> th;
+  for (int tix = 0; tix < nt; ++tix) {
+    th.emplace_back([&, tix] {
+      const int64_t i0 = n * tix / nt, i1 = n * (tix + 1) / nt;
+      parts[tix].resize(static_cast<size_t>(worst(i0, i1)));
+      used[tix] = format_range(i0, i1, parts[tix].data());
+    });
+  }
+  for (auto& x : th) x.join();
+  int64_t o = 0;
+  for (int tix = 0; tix < nt; ++tix) {
+    if (o + used[tix] > out_cap) {
+      *out_len = o;
+      pg::set_error("pg_format_tsv: output buffer too small at record %lld", (long long)(n * tix / nt));
       return PG_ERR_INVALID;
     }
-    std::memcpy(out + o, prefix_blob + prefix_off[k], plen);
-    o += plen;
-    o += pg::py_repr(af[k], out + o);
-    out[o++] = '\t';
-    o += pg::put_int(n_miss[k], out + o);
-    std::memcpy(out + o, mid, mid_len);
-    o += mid_len;
-    o += pg::py_repr(r[i], out + o);
-    out[o++] = '\t';
-    o += pg::py_repr(t[i], out + o);
-    out[o++] = '\t';
-    o += pg::py_repr(p[i], out + o);
-    out[o++] = '\t';
-    std::memcpy(out + o, pheno_blob + pheno_off[j], nlen);
-    o += nlen;
-    out[o++] = '\n';
+    std::memcpy(out + o, parts[tix].data(), static_cast<size_t>(used[tix]));
+    o += used[tix];
   }
   *out_len = o;
   return PG_OK;

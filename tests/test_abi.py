@@ -108,6 +108,31 @@ def test_native_tsv_lines_match_python_formatting():
     assert text == want
 
 
+def test_native_tsv_lines_threaded_equal_serial():
+    """Above 32,768 records pg_format_tsv formats chunks on host threads and concatenates them:
+    the text equals the serial formatting of the same records (small calls), byte for byte."""
+    import numpy as np
+
+    import paper_2604_21095_b200 as pg
+    from paper_2604_21095_b200 import output
+
+    rng = np.random.default_rng(8)
+    markers = [pg.MarkerRecord(str(1 + i % 22), f"rs{i}", 1000 * i + 1, "A", "GT", i) for i in range(500)]
+    names = [f"ph{j}" for j in range(40)]
+    fmt = output._RecordText(812.0, 815, True, names)
+    n = 70_001
+    rows, cols = rng.integers(0, 500, n), rng.integers(0, 40, n)
+    r, t, p = rng.standard_normal(n) / 10, rng.standard_normal(n) * 5, rng.random(n) ** 8
+    af, miss = rng.random(500), rng.integers(0, 9, 500)
+    whole = output.format_records_bytes(markers, af, miss, rows, cols, r, t, p, fmt.pheno_blob, fmt.pheno_off,
+                                        fmt.mid, True)
+    step = 20_000
+    parts = b"".join(output.format_records_bytes(markers, af, miss, rows[a:a + step], cols[a:a + step], r[a:a + step],
+                                                 t[a:a + step], p[a:a + step], fmt.pheno_blob, fmt.pheno_off, fmt.mid,
+                                                 True) for a in range(0, n, step))
+    assert whole == parts and whole.count(b"\n") == n
+
+
 def test_full_writer_marker_sidecar_matches_python_formatting(tmp_path, monkeypatch):
     """FullMatrixWriter renders <out>.markers.tsv natively (pg_format_marker_lines); the lines
     equal the reference's per-marker f-string with repr() floats, skipped markers omitted."""
