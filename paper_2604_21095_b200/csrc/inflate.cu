@@ -31,7 +31,13 @@ namespace {
 constexpr int kLitBits = 10;
 constexpr int kDistBits = 8;
 constexpr int kClenBits = 7;
-constexpr int kRing = 2048;             // bytes of recent output mirrored in smem
+#ifndef PG_INFLATE_RING
+#define PG_INFLATE_RING 2048
+#endif
+#ifndef PG_INFLATE_MINB
+#define PG_INFLATE_MINB 1
+#endif
+constexpr int kRing = PG_INFLATE_RING;  // bytes of recent output mirrored in smem
 constexpr int kRingSafe = kRing - 258;  // a copy never overwrites its own sources
 
 __constant__ uint16_t c_len_base[29] = {3,  4,  5,  6,  7,  8,  9,  10, 11,  13,  15,  17,  19,  23, 27,
@@ -217,7 +223,7 @@ struct InflateGeom {
 };
 
 template <int L>
-__global__ void __launch_bounds__(InflateGeom<L>::kStreams * L) inflate_kernel(const uint8_t* __restrict__ blob,
+__global__ void __launch_bounds__(InflateGeom<L>::kStreams * L, PG_INFLATE_MINB) inflate_kernel(const uint8_t* __restrict__ blob,
                                                                      const int64_t* __restrict__ off,
                                                                      const int64_t* __restrict__ len, int64_t count,
                                                                      int64_t skip, uint8_t* __restrict__ out,
