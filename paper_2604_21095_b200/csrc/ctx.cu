@@ -149,6 +149,10 @@ __global__ void rbar_kernel(const double* rbar_in, int64_t n, int64_t p_pad, flo
 }  // namespace
 }  // namespace pg
 
+namespace pg {
+constexpr size_t kH2DBounce = size_t{64} << 20;  // pinned bounce buffers of upload_pageable (two)
+}  // namespace pg
+
 struct pg_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -919,6 +923,10 @@ int pg_ctx_create(int device, pg_ctx** out) {
   for (int i = 0; i < 2; ++i) {
     PG_CUDA_CHECK(cudaEventCreateWithFlags(&c->stage_ev[i], cudaEventDisableTiming));
     PG_CUDA_CHECK(cudaEventCreateWithFlags(&c->slot_free_ev[i], cudaEventDisableTiming));
+    // the pageable-upload bounce buffers are page-locked now (contexts are created while the
+    // host parses tables), not on the first panel upload
+    PG_CUDA_CHECK(cudaHostAlloc(&c->h2d_stage[i], pg::kH2DBounce, cudaHostAllocDefault));
+    PG_CUDA_CHECK(cudaEventCreateWithFlags(&c->h2d_ev[i], cudaEventDisableTiming));
   }
   *out = c;
   return PG_OK;
@@ -1017,7 +1025,7 @@ namespace {
 // bounce buffers by several host threads (one memcpy thread cannot feed the link) while
 // the previous chunk's H2D runs on `s`. Already page-locked sources go straight through.
 int upload_pageable(pg_ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t s) {
-  constexpr size_t kChunk = size_t{64} << 20;
+  constexpr size_t kChunk = kH2DBounce;
   cudaPointerAttributes attr{};
   const bool pinned = cudaPointerGetAttributes(&attr, src) == cudaSuccess && attr.type == cudaMemoryTypeHost;
   cudaGetLastError();  // a pageable pointer may leave an error behind on older drivers
@@ -1029,7 +1037,7 @@ int upload_pageable(pg_ctx* c, void* dst, const void* src, size_t bytes, cudaStr
     if (c->h2d_stage[i] == nullptr) PG_CUDA_CHECK(cudaHostAlloc(&c->h2d_stage[i], kChunk, cudaHostAllocDefault));
     if (c->h2d_ev[i] == nullptr) PG_CUDA_CHECK(cudaEventCreateWithFlags(&c->h2d_ev[i], cudaEventDisableTiming));
   }
-  const int nt = static_cast<int>(std::max(1u, std::min(8u, std::thread::hardware_concurrency() / 2)));
+  const int nt = static_cast<int>(std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
   const char* from = static_cast<const char*>(src);
   char* to = static_cast<char*>(dst);
   int k = 0;
