@@ -40,6 +40,9 @@
 
 #include "assoc.cuh"
 
+#ifndef PG_PACKED_PREFETCH
+#define PG_PACKED_PREFETCH 0  // stages ahead of the ring for the packed-row L2 prefetch (0: off)
+#endif
 #ifndef PG_FUSED2_STAGES
 #define PG_FUSED2_STAGES 8
 #endif
@@ -678,6 +681,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<MODE>::kThreadsM
           if constexpr (FUSED) {
             mbar_arrive_expect_tx(&pk[s], kPackedBytes);
             tma_load_2d_hint(st + C::kOffPacked, &tm_v, &pk[s], (kb_begin + kb) * (kTileK / 4), grow, pol_geno);
+            // the packed rows often come from DRAM (streamed, evict_first) while the panel hits
+            // in L2: start them into L2 further ahead than the ring reaches
+            if (PG_PACKED_PREFETCH > 0 && kb + PG_PACKED_PREFETCH < n_kb)
+              tma_prefetch_2d(&tm_v, (kb_begin + kb + PG_PACKED_PREFETCH) * (kTileK / 4), grow, pol_geno);
           } else if constexpr (WIDE) {
             tma_load_2d_pair(st + C::kOffV, &tm_v, full0, kx, grow, pol_geno);
           } else {

@@ -100,6 +100,13 @@ __device__ __forceinline__ void tma_load_2d_hint(void* smem_dst, const void* tma
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(x), "r"(y), "l"(policy)
       : "memory");
 }
+// L2 prefetch of a 2-D tile (no shared-memory destination, no completion)
+__device__ __forceinline__ void tma_prefetch_2d(const void* tmap, int32_t x, int32_t y, uint64_t policy) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile.L2::cache_hint [%0, {%1, %2}], %3;" ::"l"(
+                   reinterpret_cast<uint64_t>(tmap)),
+               "r"(x), "r"(y), "l"(policy)
+               : "memory");
+}
 // 2-SM form: the destination is this CTA's shared memory, the completion is
 // signalled on an mbarrier of either CTA of the pair (here: the leader's).
 __device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const void* tmap, uint32_t bar_cluster_addr, int32_t x,
