@@ -46,9 +46,9 @@ def _case(seed, n_src=613, n_kept=590, p=700, cov=3):
     return y, build_covariate_basis(c, True).q, gidx, n_src
 
 
-@pytest.mark.parametrize("f64", [False, True])
-def test_async_panel_bitwise_equals_sync(f64):
-    y, q, gidx, n_src = _case(1)
+@pytest.mark.parametrize("f64,p", [(False, 700), (True, 700), (False, 100), (True, 1)])
+def test_async_panel_bitwise_equals_sync(f64, p):
+    y, q, gidx, n_src = _case(1, p=p)
     with DeviceContext(0) as a, DeviceContext(0) as b:
         a.set_f64_panel(f64)
         b.set_f64_panel(f64)
