@@ -1280,13 +1280,13 @@ int pg_ctx_export_panel(pg_ctx* c, void* d_dst) {
 // scale_d (f64), scale_f (f32), Cq (i64), Cq_f (f32), ||q0|| (f32) per row, then the lo level
 // (three planes + Cq_lo) in F64 mode. Multi-GPU: each rank prepares its share of the
 // phenotypes and the shares are all-gathered (bench.py, distributed panel preparation).
-int64_t panel_rows_bytes(const pg_ctx* c, int64_t r) {
+static int64_t panel_rows_bytes(const pg_ctx* c, int64_t r) {
   int64_t b = 3 * r * c->k_pad + r * (8 + 4 + 8 + 4 + 4);
   if (c->f64_panel) b += 3 * r * c->k_pad + r * 8;
   return b;
 }
 
-int panel_rows_copy(pg_ctx* c, uint8_t* buf, int64_t row_begin, int64_t row_end, bool to_buf) {
+static int panel_rows_copy(pg_ctx* c, uint8_t* buf, int64_t row_begin, int64_t row_end, bool to_buf) {
   const int64_t r = row_end - row_begin;
   const size_t plane = static_cast<size_t>(r) * c->k_pad, off = static_cast<size_t>(row_begin) * c->k_pad;
   cudaStream_t s = c->stream;
