@@ -576,6 +576,10 @@ def our_arm(a) -> None:
         pbuf2 = torch.empty(ctx.panel_bytes(), dtype=torch.uint8, device=dev) if ctx2 is not None else None
 
         panel_ready = threading.Event()
+        # one GPU, pipelined panel: the second context follows the first one's panel chunk by
+        # chunk (pg_ctx_follow_panel), so both contexts' first batches run behind the upload;
+        # otherwise it takes the finished panel from the first context after its first batch
+        follow = ctx2 is not None and world == 1 and not a.sync_panel
 
         def e2e_lane(cx, k, items):
             """One context's share of the step: the host-buffer C-ABI path, pipelined (the H2D
@@ -585,14 +589,14 @@ def our_arm(a) -> None:
             h2d = d2h = hits = 0
 
             def hand_over():
-                if k == 0 and ctx2 is not None and not panel_ready.is_set():
+                if k == 0 and ctx2 is not None and not follow and not panel_ready.is_set():
                     ctx.export_panel(pbuf2.data_ptr())
                     panel_ready.set()
 
             for j, (s, c) in enumerate(items):
                 cx.stage(j % 2, _native.PG_GENO_BED, host_np[s:s + c], bpm)
                 h2d += c * bpm
-                if j == 0 and k == 1:
+                if j == 0 and k == 1 and not follow:
                     panel_ready.wait()
                     cx.import_panel(pbuf2.data_ptr(), n, p, gidx, n)
                     cx.set_scan(df, _native.PG_MODE_THRESHOLD, rbar)
@@ -615,6 +619,9 @@ def our_arm(a) -> None:
             else:
                 h2d = moved + (n * (p + N_COVARIATES + 1) * 8 if rank == 0 else 0)
             ctx.set_scan(df, _native.PG_MODE_THRESHOLD, rbar)
+            if follow:
+                ctx2.follow_panel(ctx)
+                ctx2.set_scan(df, _native.PG_MODE_THRESHOLD, rbar)
             d2h = hits = 0
             if ctx2 is None:
                 h, d, t = e2e_lane(ctx, 0, batches)

@@ -123,6 +123,12 @@ PG_API int pg_ctx_set_panel_async_cols(pg_ctx* ctx, const double* y, int64_t n_k
 PG_API int pg_ctx_panel_rows_bytes(pg_ctx* ctx, int64_t n_rows, int64_t* bytes);
 PG_API int pg_ctx_export_panel_rows(pg_ctx* ctx, void* d_dst, int64_t row_begin, int64_t row_end);
 PG_API int pg_ctx_import_panel_rows(pg_ctx* ctx, const void* d_src, int64_t row_begin, int64_t row_end);
+/* `follower` takes `leader`'s pipelined panel (pg_ctx_set_panel_async) chunk by chunk: each
+ * chunk, once prepared on the leader, is copied device to device to the follower and marked
+ * ready there, so both contexts' first scans run their GEMMs behind the one upload (two
+ * contexts per GPU). Chunks are issued by whichever context needs the next
+ * one. The leader must outlive the follower's use of the panel. */
+PG_API int pg_ctx_follow_panel(pg_ctx* follower, pg_ctx* leader);
 /* Copy `src`'s resident panel (limbs, scales, sample map) into `dst` on the same device, device
  * to device (export + import), so that two contexts can scan batches of one job in turn
  * ("two contexts per GPU"). Both must have the same precision mode. */

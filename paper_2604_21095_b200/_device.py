@@ -187,6 +187,13 @@ class DeviceContext:
         with self.lock:
             call("pg_ctx_import_panel_rows", self._h, d_src, int(row_begin), int(row_end))
 
+    def follow_panel(self, leader: "DeviceContext") -> None:
+        """Take `leader`'s pipelined panel chunk by chunk as it is prepared (pg_ctx_follow_panel)."""
+        with leader.lock, self.lock:
+            call("pg_ctx_follow_panel", self._h, leader._h)
+            self.n_pheno = leader.n_pheno
+            self.beta_on = False
+
     def clone_panel_from(self, src: "DeviceContext") -> None:
         """This context takes `src`'s resident panel, device to device (pg_ctx_clone_panel)."""
         with src.lock, self.lock:

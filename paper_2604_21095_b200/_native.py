@@ -69,6 +69,7 @@ SIGNATURES: dict[str, list] = {
     "pg_ctx_set_panel_async": [_P, _P, c_int64, c_int64, c_int64, _P, c_int64, _P, c_int64, c_int64],
     "pg_ctx_panel_async_wait": [_P, _P, _P],
     "pg_ctx_clone_panel": [_P, _P],
+    "pg_ctx_follow_panel": [_P, _P],
     "pg_topk_merge": [c_int64, c_int64, _P, _P, _P, c_int64, _P, _P, _P, c_int64, _P, _P],
     "pg_gather_spans": [_P, _P, _P, c_int64, _P],
     "pg_topk_gather": [c_int64, _P, c_int64, c_int, _P, _P, _P],

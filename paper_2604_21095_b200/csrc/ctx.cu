@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <mutex>
 #include <thread>
 #include <cstdlib>
 #include <cstring>
@@ -192,6 +193,14 @@ struct pg_ctx {
   bool panel_pending = false;  // the compute stream has not yet waited for every chunk
   bool async_flags = false;    // zero-variance flags / sd / finiteness of the async panel on the device
   cudaEvent_t panel_ev = nullptr;
+  cudaEvent_t geom_ev = nullptr;  // panel geometry (sample map) uploaded on panel_prep
+  // A second context of the same job following this pipelined panel
+  // (pg_ctx_follow_panel): each chunk, once prepared here, is copied to the follower's
+  // buffers on its prep stream and marked ready there; the chunks are issued under pump_mu
+  // by whichever of the two contexts needs the next one.
+  pg_ctx* follower = nullptr;
+  pg_ctx* leader = nullptr;
+  std::mutex pump_mu;
 
   // scan parameters
   double df = 1.0;
@@ -311,6 +320,38 @@ int ctx_check(pg_ctx* c) {
   return PG_OK;
 }
 
+// Chunk j of leader c's pipelined panel -> follower f (pg_ctx_follow_panel): on f's prep
+// stream, after the chunk is ready on c; then the chunk is ready on f as well.
+int panel_copy_chunk(pg_ctx* c, pg_ctx* f, int64_t j) {
+  const int64_t n_pheno = c->prep_cols, chunk = c->async_chunk;
+  const int64_t c0 = c->async_col0 + j * chunk;
+  const int64_t w = std::min(chunk, c->async_col1 - c0);
+  const int64_t rows = c0 + w == n_pheno ? c->p_pad - c0 : w;
+  const size_t off = static_cast<size_t>(c0) * c->k_pad, bytes = static_cast<size_t>(rows) * c->k_pad;
+  cudaStream_t fs = f->panel_prep;
+  PG_CUDA_CHECK(cudaStreamWaitEvent(fs, c->chunk_ready[j], 0));
+  auto cp = [&](void* dst, const void* src, size_t n) -> int {
+    PG_CUDA_CHECK(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToDevice, fs));
+    return PG_OK;
+  };
+  PG_CHECK_STATUS(cp(f->qh.p + off, c->qh.p + off, bytes));
+  PG_CHECK_STATUS(cp(f->q1.p + off, c->q1.p + off, bytes));
+  PG_CHECK_STATUS(cp(f->q0.p + off, c->q0.p + off, bytes));
+  PG_CHECK_STATUS(cp(f->scale_d.p + c0, c->scale_d.p + c0, 8 * rows));
+  PG_CHECK_STATUS(cp(f->scale_f.p + c0, c->scale_f.p + c0, 4 * rows));
+  PG_CHECK_STATUS(cp(f->cq.p + c0, c->cq.p + c0, 8 * rows));
+  PG_CHECK_STATUS(cp(f->cq_f.p + c0, c->cq_f.p + c0, 4 * rows));
+  PG_CHECK_STATUS(cp(f->q0n.p + c0, c->q0n.p + c0, 4 * rows));
+  if (c->f64_panel) {
+    PG_CHECK_STATUS(cp(f->qh_lo.p + off, c->qh_lo.p + off, bytes));
+    PG_CHECK_STATUS(cp(f->q1_lo.p + off, c->q1_lo.p + off, bytes));
+    PG_CHECK_STATUS(cp(f->q0_lo.p + off, c->q0_lo.p + off, bytes));
+    PG_CHECK_STATUS(cp(f->cq_lo.p + c0, c->cq_lo.p + c0, 8 * rows));
+  }
+  PG_CUDA_CHECK(cudaEventRecord(f->chunk_ready[j], fs));
+  return PG_OK;
+}
+
 // Pipelined panel (pg_ctx_set_panel_async): enqueue chunk j — its H2D on panel_copy, then
 // prepare + quantize + q0 norms on panel_prep, ending in chunk_ready[j].
 int panel_issue(pg_ctx* c, int64_t j) {
@@ -357,6 +398,7 @@ int panel_issue(pg_ctx* c, int64_t j) {
   PG_CHECK_STATUS(panel_quantize(yj, n_kept, w, w, nullptr, c->gidx.p, c->k_pad, rows, pj, c->maxabs.p + c0, ps));
   PG_CHECK_STATUS(panel_q0_norms(c->q0.p + off, rows, c->k_pad, c->q0n.p + c0, ps));
   PG_CUDA_CHECK(cudaEventRecord(c->chunk_ready[j], ps));
+  if (c->follower != nullptr) PG_CHECK_STATUS(panel_copy_chunk(c, c->follower, j));
   return PG_OK;
 }
 
@@ -364,6 +406,8 @@ int panel_issue(pg_ctx* c, int64_t j) {
 // (blocks the host on an earlier chunk's copy when needed); upto < 0: only as many as can
 // be issued without blocking.
 int panel_pump(pg_ctx* c, int64_t upto) {
+  if (c->leader != nullptr) return panel_pump(c->leader, upto);  // the leader issues for both
+  std::lock_guard<std::mutex> lock(c->pump_mu);
   while (c->chunk_issued < c->n_chunks) {
     const int64_t j = c->chunk_issued;
     if (j >= 2) {
@@ -397,8 +441,19 @@ int panel_wait_all(pg_ctx* c, cudaStream_t s) {
 // Before a new panel replaces the current one: no pipelined preparation may still write it.
 int panel_drain(pg_ctx* c) {
   if (c->panel_prep) {
-    PG_CHECK_STATUS(panel_pump(c, c->n_chunks - 1));
+    if (c->leader == nullptr || c->panel_pending) PG_CHECK_STATUS(panel_pump(c, c->n_chunks - 1));
     PG_CUDA_CHECK(cudaStreamSynchronize(c->panel_prep));
+  }
+  if (c->follower != nullptr) {  // every chunk was issued (and copied): release the follower
+    PG_CUDA_CHECK(cudaStreamSynchronize(c->follower->panel_prep));
+    c->follower->chunk_issued = c->follower->n_chunks;
+    c->follower->leader = nullptr;
+    c->follower = nullptr;
+  }
+  if (c->leader != nullptr) {
+    c->leader->follower = nullptr;
+    c->leader = nullptr;
+    c->chunk_issued = c->n_chunks;
   }
   c->panel_pending = false;
   c->async_flags = false;
@@ -936,12 +991,19 @@ int pg_ctx_destroy(pg_ctx* c) {
   if (c == nullptr) return PG_OK;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
+  if (c->follower) {  // chunks not issued yet will never reach the follower
+    if (c->chunk_issued < c->n_chunks) c->follower->have_panel = false;
+    c->follower->chunk_issued = c->follower->n_chunks;
+    c->follower->leader = nullptr;
+  }
+  if (c->leader) c->leader->follower = nullptr;
   if (c->panel_prep) {
     cudaStreamSynchronize(c->panel_prep);
     cudaStreamSynchronize(c->panel_copy);
     for (auto e : c->chunk_h2d) cudaEventDestroy(e);
     for (auto e : c->chunk_ready) cudaEventDestroy(e);
     cudaEventDestroy(c->panel_ev);
+    if (c->geom_ev) cudaEventDestroy(c->geom_ev);
     cudaStreamDestroy(c->panel_prep);
     cudaStreamDestroy(c->panel_copy);
   }
@@ -1136,6 +1198,8 @@ int pg_ctx_set_panel_async_cols(pg_ctx* c, const double* y, int64_t n_kept, int6
   PG_CUDA_CHECK(cudaStreamWaitEvent(cs, c->panel_ev, 0));
   PanelPlanes pp;
   PG_CHECK_STATUS(panel_geometry(c, n_kept, n_pheno, n_samples_src, geno_row_index, ps, pp));
+  if (c->geom_ev == nullptr) PG_CUDA_CHECK(cudaEventCreateWithFlags(&c->geom_ev, cudaEventDisableTiming));
+  PG_CUDA_CHECK(cudaEventRecord(c->geom_ev, ps));
   const int64_t chunk = round_up(std::max<int64_t>(chunk_cols, kTileP), kTileP);
   const int64_t n_ch = (col_end - col_begin + chunk - 1) / chunk;
   while (static_cast<int64_t>(c->chunk_ready.size()) < n_ch) {
@@ -1190,6 +1254,73 @@ int pg_ctx_set_panel_async(pg_ctx* c, const double* y, int64_t n_kept, int64_t n
   PG_REQUIRE(ld >= n_pheno, PG_ERR_INVALID, "pg_ctx_set_panel_async: bad shape");
   return pg_ctx_set_panel_async_cols(c, y, n_kept, n_pheno, ld, 0, n_pheno, basis_q, rank, geno_row_index,
                                      n_samples_src, chunk_cols);
+}
+
+int pg_ctx_follow_panel(pg_ctx* f, pg_ctx* c) {
+  PG_CHECK_STATUS(ctx_check(c));
+  PG_REQUIRE(f != nullptr && f != c && f->device == c->device, PG_ERR_INVALID,
+             "pg_ctx_follow_panel: need a second context on the same device");
+  PG_REQUIRE(c->async_flags && c->leader == nullptr && c->follower == nullptr, PG_ERR_STATE,
+             "pg_ctx_follow_panel: the source context has no pipelined panel of its own, or already a follower");
+  PG_REQUIRE(f->f64_panel == c->f64_panel, PG_ERR_STATE,
+             "pg_ctx_follow_panel: set the same precision (pg_ctx_set_f64_panel) on both contexts");
+  PG_CHECK_STATUS(panel_drain(f));
+  if (f->panel_prep == nullptr) {
+    PG_CUDA_CHECK(cudaStreamCreateWithFlags(&f->panel_copy, cudaStreamNonBlocking));
+    PG_CUDA_CHECK(cudaStreamCreateWithFlags(&f->panel_prep, cudaStreamNonBlocking));
+    PG_CUDA_CHECK(cudaEventCreateWithFlags(&f->panel_ev, cudaEventDisableTiming));
+  }
+  cudaStream_t fs = f->panel_prep;
+  // the follower's earlier scans may still read its current panel
+  PG_CUDA_CHECK(cudaEventRecord(f->panel_ev, f->stream));
+  PG_CUDA_CHECK(cudaStreamWaitEvent(fs, f->panel_ev, 0));
+  f->n_src = c->n_src;
+  f->n_kept = c->n_kept;
+  f->n_pheno = c->n_pheno;
+  f->p_pad = c->p_pad;
+  f->k_pad = c->k_pad;
+  const size_t plane = static_cast<size_t>(c->p_pad) * c->k_pad;
+  for (auto* b : {&f->qh, &f->q1, &f->q0}) PG_CHECK_STATUS(b->ensure(plane));
+  PG_CHECK_STATUS(f->scale_d.ensure(c->p_pad));
+  PG_CHECK_STATUS(f->scale_f.ensure(c->p_pad));
+  PG_CHECK_STATUS(f->cq.ensure(c->p_pad));
+  PG_CHECK_STATUS(f->cq_f.ensure(c->p_pad));
+  PG_CHECK_STATUS(f->q0n.ensure(c->p_pad));
+  if (c->f64_panel) {
+    for (auto* b : {&f->qh_lo, &f->q1_lo, &f->q0_lo}) PG_CHECK_STATUS(b->ensure(plane));
+    PG_CHECK_STATUS(f->cq_lo.ensure(c->p_pad));
+  }
+  const size_t kb_words = static_cast<size_t>(c->k_pad / 32 + 1);
+  PG_CHECK_STATUS(f->gidx.ensure(c->n_kept));
+  PG_CHECK_STATUS(f->keep_bits.ensure(kb_words));
+  PG_CUDA_CHECK(cudaStreamWaitEvent(fs, c->geom_ev, 0));
+  PG_CUDA_CHECK(cudaMemcpyAsync(f->gidx.p, c->gidx.p, sizeof(int64_t) * c->n_kept, cudaMemcpyDeviceToDevice, fs));
+  PG_CUDA_CHECK(cudaMemcpyAsync(f->keep_bits.p, c->keep_bits.p, sizeof(uint32_t) * kb_words, cudaMemcpyDeviceToDevice, fs));
+  while (f->chunk_ready.size() < c->chunk_ready.size()) {
+    cudaEvent_t a, b;
+    PG_CUDA_CHECK(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+    PG_CUDA_CHECK(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+    f->chunk_h2d.push_back(a);
+    f->chunk_ready.push_back(b);
+  }
+  f->n_chunks = c->n_chunks;
+  f->chunk_pt = c->chunk_pt;
+  {
+    std::lock_guard<std::mutex> lock(c->pump_mu);
+    for (int64_t j = 0; j < c->chunk_issued; ++j) PG_CHECK_STATUS(panel_copy_chunk(c, f, j));  // already issued
+    c->follower = f;
+    f->leader = c;
+  }
+  f->chunk_issued = 0;
+  f->panel_pending = true;
+  f->async_flags = false;
+  f->q0n_valid = true;
+  f->have_prepared = false;
+  f->have_panel = true;
+  f->have_scan = false;
+  f->have_basis = false;
+  f->beta_on = false;
+  return PG_OK;
 }
 
 int pg_ctx_panel_async_wait(pg_ctx* c, uint8_t* zero_variance, double* sd) {

@@ -160,3 +160,36 @@ def test_panel_shares_assemble_the_sync_panel(f64):
         b.import_panel_rows(rows[a][0].data_ptr(), rows[a][1], rows[a][2])
         want = _panel_bytes(ref)
         assert np.array_equal(_panel_bytes(a), want) and np.array_equal(_panel_bytes(b), want)
+
+
+@pytest.mark.parametrize("f64", [False, True])
+def test_follower_context_scans_equal_leader(f64):
+    """pg_ctx_follow_panel: a second context takes the pipelined panel chunk by chunk. Its
+    first scan (run before the leader has scanned, so it drives the chunk issuing itself)
+    equals the leader's and the synchronous context's, bit for bit; a second pipelined panel
+    on the leader releases the follower, which can follow again."""
+    y, q, gidx, n_src = _case(21, p=900)
+    rng = np.random.default_rng(6)
+    m = 600
+    d = rng.binomial(2, rng.uniform(0.05, 0.95, m)[:, None], size=(m, n_src)).astype(np.float64)
+    packed, bpm = _packed(d)
+    df = float(len(gidx) - 1 - q.shape[1])
+    rbar = np.full(y.shape[1], orc.premask_abs_r(1e-2, df))
+    with DeviceContext(0) as ref, DeviceContext(0) as lead, DeviceContext(0) as fol:
+        for cx in (ref, lead, fol):
+            cx.set_f64_panel(f64)
+        ref.prepare_panel(y, q)
+        ref.commit_panel(np.arange(y.shape[1]), gidx, n_src)
+        ref.set_scan(df, _native.PG_MODE_THRESHOLD, rbar)
+        want = ref.scan(_native.PG_GENO_BED, packed, bpm)
+        for rep in range(2):
+            yp = _pinned(y)
+            lead.set_panel_async(yp, q, gidx, n_src, chunk_cols=256)
+            fol.follow_panel(lead)
+            for cx in (fol, lead):  # the follower first
+                cx.set_scan(df, _native.PG_MODE_THRESHOLD, rbar)
+                got = cx.scan(_native.PG_GENO_BED, packed, bpm)
+                for f in ("cand_rows", "cand_cols", "cand_r", "cand_t", "cand_p"):
+                    assert np.array_equal(getattr(got, f), getattr(want, f)), (rep, f)
+            lead.panel_async_wait()
+        assert np.array_equal(_panel_bytes(fol), _panel_bytes(ref))
