@@ -359,7 +359,7 @@ PG_API int pg_format_tsv(int64_t n, const int64_t* rows, const int64_t* cols, co
 PG_API int pg_format_float_columns(int64_t n, int ncols, const double* const* cols, char* out, int64_t out_cap,
                                    int64_t* out_len);
 
-/* TOPK writer merge (host; output.TopKWriter.emit, output.py:153-211): the held records
+/* TOPK writer merge (host; output.TopKWriter.emit, output.py:155-213): the held records
  * (sorted by phenotype, p, marker source index) and a batch's new candidates (any order, every
  * source index above the held ones) merged per phenotype, the first k of each kept. out_idx
  * (capacity n_pheno * k) receives indices into [held ++ fresh] in (phenotype, p, source index)

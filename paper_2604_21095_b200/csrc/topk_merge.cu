@@ -1,4 +1,4 @@
-// Host-side merge step of the TOPK writer (reference output.TopKWriter.emit, output.py:153-211):
+// Host-side merge step of the TOPK writer (reference output.TopKWriter.emit, output.py:155-213):
 // the records held so far (sorted by phenotype, then p, then marker source index) and a batch's
 // new candidates are merged per phenotype and the first k of each phenotype kept, in that order.
 // A batch's candidates all come from markers later in the source than every held record, so
