@@ -160,3 +160,40 @@ def test_full_writer_marker_sidecar_matches_python_formatting(tmp_path, monkeypa
     assert lines == want
     assert names == ["a", "b", "c"]
     assert np.array_equal(t, t_rows)
+
+
+def test_topk_merge_matches_lexsort():
+    """pg_topk_merge (threaded above 65,536 records) against a lexsort of held ++ fresh by
+    (phenotype, p, source index) cut to k per phenotype — with p ties, k = 1, empty sides and
+    phenotypes that have no records."""
+    import ctypes
+
+    import numpy as np
+
+    from paper_2604_21095_b200 import _native
+
+    rng = np.random.default_rng(3)
+    for n_pheno, k, n_held_raw, n_fresh in ((5, 1, 0, 40), (300, 7, 1500, 90_000), (64, 3, 400, 0), (1, 4, 9, 9)):
+        def draw(n, src0):
+            col = rng.integers(0, max(1, n_pheno - 1), n)  # the last phenotype stays empty
+            p = np.where(rng.random(n) < 0.3, 0.5, rng.random(n))  # ties
+            return col.astype(np.int64), p, (src0 + rng.permutation(n)).astype(np.int64)
+
+        hc, hp, hs = draw(n_held_raw, 0)
+        order = np.lexsort((hs, hp, hc))
+        hc, hp, hs = hc[order], hp[order], hs[order]
+        rank = np.arange(hc.size) - np.searchsorted(hc, hc, side="left")
+        keep = rank < k  # a valid held state: at most k per phenotype
+        hc, hp, hs = hc[keep], hp[keep], hs[keep]
+        fc, fp, fs = draw(n_fresh, 10**9)  # every candidate after every held record
+        allc, allp, alls = np.concatenate([hc, fc]), np.concatenate([hp, fp]), np.concatenate([hs, fs])
+        order = np.lexsort((alls, allp, allc))
+        r = np.arange(order.size) - np.searchsorted(allc[order], allc[order], side="left")
+        want = order[r < k]
+        out = np.empty(n_pheno * k, dtype=np.int64)
+        n_out = ctypes.c_int64(0)
+        arrs = [np.ascontiguousarray(a) for a in (hc, hp, hs, fc, fp, fs)]
+        _native.call("pg_topk_merge", n_pheno, k, arrs[0].ctypes.data, arrs[1].ctypes.data, arrs[2].ctypes.data,
+                     hc.size, arrs[3].ctypes.data, arrs[4].ctypes.data, arrs[5].ctypes.data, fc.size,
+                     out.ctypes.data, ctypes.byref(n_out))
+        assert np.array_equal(out[:n_out.value], want), (n_pheno, k)
